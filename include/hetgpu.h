@@ -1,0 +1,173 @@
+/*
+ * hetgpu — C-ABI of the B200-native mini-batch hot path of Heta (arXiv 2408.09697).
+ *
+ * Drop-in boundary for the reference simulator "hetsim" (/root/reference/proj).
+ * The reference has no FFI layer of its own: callers link its C++ library
+ * directly. Each entry point below names the reference interface it replaces
+ * (file:line under /root/reference/proj). Plain pointers and sizes only; no
+ * C++ or torch types cross the ABI. Every function returns 0 / a non-NULL
+ * handle on success; on failure it returns -1 / NULL and hg_last_error()
+ * holds the message (the reference's exception text where one exists).
+ * Errors are classified by hg_last_error_kind(): 1 = std::invalid_argument,
+ * 2 = std::runtime_error (mirrors the reference's exception types).
+ */
+#ifndef HETGPU_H
+#define HETGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hg_graph hg_graph;
+typedef struct hg_engine hg_engine;
+typedef struct hg_bundle hg_bundle;
+
+const char* hg_last_error(void);
+int hg_last_error_kind(void);
+const char* hg_version(void);
+
+/* ---- bundles: named arrays returned by the query functions ------------------ */
+int hg_bundle_size(const hg_bundle* b);
+const char* hg_bundle_name(const hg_bundle* b, int i);
+const char* hg_bundle_dtype(const hg_bundle* b, int i); /* numpy dtype string */
+int hg_bundle_ndim(const hg_bundle* b, int i);
+long long hg_bundle_dim(const hg_bundle* b, int i, int d);
+long long hg_bundle_nbytes(const hg_bundle* b, int i);
+const void* hg_bundle_data(const hg_bundle* b, int i);
+void hg_bundle_free(hg_bundle* b);
+
+/* ---- graphs (host) ---------------------------------------------------------------- */
+typedef struct {
+  const char* name;
+  uint64_t count;
+  int dim;
+  int storage; /* 1 dense, 2 learnable */
+} hg_spec_node_type;
+
+typedef struct {
+  const char* src;
+  const char* edge;
+  const char* dst;
+  uint64_t edges;
+  int powerlaw; /* 0 uniform, 1 powerlaw */
+  double alpha;
+} hg_spec_relation;
+
+typedef struct {
+  const char* target;
+  int num_classes;
+  double label_noise;
+  int n_types;
+  const hg_spec_node_type* types;
+  int n_rels;
+  const hg_spec_relation* rels;
+  int add_reverse;
+  int n_self_paired;
+  const char* const* self_paired;
+} hg_spec;
+
+/* gen_synthetic (src/harness.cpp:74-186), bit-exact with the reference. */
+hg_graph* hg_graph_generate(const hg_spec* spec, uint64_t seed);
+
+/* A HetGraph given directly in CSR form (dst-major per relation, hetgraph.hpp:41-74).
+ * indptr: concatenation of per-relation indptr arrays (n_dst(r)+1 each);
+ * src: concatenation of per-relation source arrays; kinds: 0 absent, 1 dense,
+ * 2 learnable; dense: concatenated row-major f32 tables of the dense types. */
+hg_graph* hg_graph_from_csr(int n_types, const uint64_t* counts, int n_rels, const int* rel_src,
+                            const int* rel_dst, const int* rel_reverse, const uint64_t* indptr,
+                            const uint32_t* src, const int* kinds, const int* dims, const float* dense,
+                            int target, int num_classes, const int32_t* labels);
+
+/* build_hetgraph (src/hetgraph.cpp:126-156) from (src,dst) pairs per relation. */
+hg_graph* hg_graph_from_pairs(int n_types, const uint64_t* counts, int n_rels, const int* rel_src,
+                              const int* rel_dst, const uint64_t* pair_counts, const uint32_t* pair_src,
+                              const uint32_t* pair_dst, int target, int num_classes);
+
+void hg_graph_free(hg_graph* g);
+/* node_counts, labels, rel_src/rel_dst/rel_reverse, rel{r}.indptr, rel{r}.src, feat.t{t}, kinds, dims */
+hg_bundle* hg_graph_export(const hg_graph* g);
+
+/* ---- planning (host; meta-partitioner stays on the CPU) ------------------------------- */
+/* meta_partition (src/metapartition.cpp:283-295) + cacheable_types (src/cache.cpp:143-177)
+ * + hop_relation_sets (src/hgnn.cpp:28-37). Names: tree.{type,depth,parent,rel},
+ * subs.{child_pos,weight}, part{i}.{sub_ids,relations,node_types,cacheable,replica,weight},
+ * hop_rels{h}. */
+hg_bundle* hg_meta_partition(const hg_graph* g, int k, int p);
+/* make_batches (src/harness.cpp:327-340): batch{i} arrays */
+hg_bundle* hg_make_batches(const hg_graph* g, int batch_size, int max_batches, uint64_t seed);
+uint64_t hg_mix_seed(uint64_t a, uint64_t b); /* src/sampling.cpp:9-15 */
+
+/* ---- device engine (one meta-partition per GPU) ---------------------------------------- */
+typedef struct {
+  int k;
+  const int* fanouts;
+  int hidden;
+  int batch_cap;
+  int p;       /* meta-partition count */
+  int rank;    /* partition evaluated by this engine */
+  uint64_t model_seed; /* init_model seed (src/hgnn.cpp:39) */
+  uint64_t learn_seed; /* init_learnable seed (src/hgnn.cpp:64) */
+  int device;
+} hg_engine_opts;
+
+typedef struct {
+  double loss;
+  uint64_t sampled_edges;
+  int n_active; /* entries filled in active_rows (p > 1) */
+  int active_rows[64];
+} hg_step_report;
+
+hg_engine* hg_engine_create(const hg_graph* g, const hg_engine_opts* opts);
+void hg_engine_free(hg_engine* e);
+
+/* One RAF training batch: run_raf_batch (src/raf.cpp:344-530) followed by
+ * adam_update_model / adam_update_rows (src/hgnn.cpp:379-410), exactly as the
+ * hot loop of run_experiment (src/harness.cpp:403-423). `batch` is host memory.
+ * train = 0 runs forward + loss only. */
+int hg_engine_step(hg_engine* e, const uint32_t* batch, int n, uint64_t rng_seed, int designated,
+                   int train, hg_step_report* out);
+/* sample_khop_restricted (src/sampling.cpp:99-103) with the engine's hop relation sets. */
+int hg_engine_sample(hg_engine* e, const uint32_t* batch, int n, uint64_t rng_seed);
+/* Named device tensors after the last call (comma-separated names, NULL = all):
+ * frontier{h}.t{t}, hop{h}.rel{r}.{dst_ids,indptr,src_ids,col}, H{d}.t{t},
+ * mean.l{l}.r{r}.t{t}, logits, dlogits, loss, grad.w.r{r}.l{l}, grad.f.t{t}.{ids,rows},
+ * post.r{r}.l{l}, post.learn{,_m,_v,_step}.t{t}, sampled_edges */
+hg_bundle* hg_engine_read(hg_engine* e, const char* names);
+
+/* Device-resident benchmark loop: uploads all batches first, then times
+ * n_steps steps back to back with CUDA events on the engine's stream.
+ * out_ms = device milliseconds for all steps; out_edges = sampled edges. */
+int hg_engine_bench(hg_engine* e, const uint32_t* batches, const int* lens, const uint64_t* seeds,
+                    int n_steps, int train, double* out_ms, uint64_t* out_edges, double* out_loss);
+void hg_engine_profile(hg_engine* e, int on);
+/* per kernel class: kernel.<name>.ms / .bytes / .launches */
+hg_bundle* hg_engine_profile_read(hg_engine* e);
+int hg_engine_info(hg_engine* e, uint64_t* param_count, uint64_t* device_bytes, int* model_step);
+
+/* ---- cache (src/cache.cpp) -------------------------------------------------------------- */
+/* presample_hotness (src/cache.cpp:39-63) on the device: hot.t{t} u32 counts */
+hg_bundle* hg_engine_presample_hotness(hg_engine* e, int epochs, uint64_t seed, int batch_size);
+/* profile_miss_penalty + allocate_cache + fill_and_serve (src/cache.cpp:11-141):
+ * counts are the hot.t{t} arrays concatenated in type order. Names: profile.*,
+ * alloc.bytes, alloc.capacity, cached.t{t} (sorted). */
+hg_bundle* hg_cache_plan(const hg_graph* g, const uint32_t* counts, uint64_t budget, double read_ns,
+                         double write_ns, double overhead_ns, int elem_bytes);
+/* Install the cached sets (concatenated sorted ids, per-type lengths) for the
+ * per-batch lookup/update accounting (CacheState::lookup/update, cache.cpp:87-113;
+ * hook harness.cpp:425-437). */
+int hg_engine_set_cache(hg_engine* e, const uint32_t* ids, const uint64_t* lens, int n_types);
+/* per type: hits, misses of the layer-0 frontier lookups so far (cache.t{t} = [hits, misses]) */
+hg_bundle* hg_engine_cache_counters(hg_engine* e);
+
+/* ---- multi-GPU: AGG_all over NCCL (one engine per rank) --------------------------------- */
+int hg_nccl_unique_id(void* out, int cap);
+int hg_engine_attach_nccl(hg_engine* e, const void* unique_id, int id_bytes, int nranks, int rank);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HETGPU_H */

@@ -1,0 +1,544 @@
+// extern "C" boundary (include/hetgpu.h): converts C arguments into the host
+// layer / engine calls and C++ exceptions into return codes + last error.
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/hetgpu.h"
+#include "engine.hpp"
+#include "host.hpp"
+
+#ifdef HG_WITH_NCCL
+#include <nccl.h>
+#endif
+
+using namespace hetgpu;
+
+struct hg_graph {
+  Graph g;
+};
+struct hg_engine {
+  std::unique_ptr<Engine> e;
+#ifdef HG_WITH_NCCL
+  ncclComm_t comm = nullptr;
+#endif
+};
+struct hg_bundle {
+  struct Item {
+    std::string name, dtype;
+    std::vector<long long> shape;
+    std::vector<char> data;
+  };
+  std::vector<Item> items;
+
+  template <typename T>
+  void add(const std::string& n, const char* dt, const std::vector<T>& v, std::vector<long long> shape = {}) {
+    Item it;
+    it.name = n;
+    it.dtype = dt;
+    it.shape = shape.empty() ? std::vector<long long>{static_cast<long long>(v.size())} : shape;
+    it.data.resize(v.size() * sizeof(T));
+    if (!v.empty()) std::memcpy(it.data.data(), v.data(), it.data.size());
+    items.push_back(std::move(it));
+  }
+};
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_err_kind = 0;
+
+template <typename R, typename F>
+R guard(R fail, F&& f) {
+  try {
+    g_err.clear();
+    g_err_kind = 0;
+    return f();
+  } catch (const std::invalid_argument& ex) {
+    g_err = ex.what();
+    g_err_kind = 1;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    g_err_kind = 2;
+  }
+  return fail;
+}
+
+std::vector<int> ivec(const int* p, int n) { return p ? std::vector<int>(p, p + n) : std::vector<int>{}; }
+
+}  // namespace
+
+extern "C" {
+
+const char* hg_last_error(void) { return g_err.c_str(); }
+int hg_last_error_kind(void) { return g_err_kind; }
+const char* hg_version(void) { return "hetgpu 0.1 (sm_100a)"; }
+
+int hg_bundle_size(const hg_bundle* b) { return static_cast<int>(b->items.size()); }
+const char* hg_bundle_name(const hg_bundle* b, int i) { return b->items[i].name.c_str(); }
+const char* hg_bundle_dtype(const hg_bundle* b, int i) { return b->items[i].dtype.c_str(); }
+int hg_bundle_ndim(const hg_bundle* b, int i) { return static_cast<int>(b->items[i].shape.size()); }
+long long hg_bundle_dim(const hg_bundle* b, int i, int d) { return b->items[i].shape[d]; }
+long long hg_bundle_nbytes(const hg_bundle* b, int i) { return static_cast<long long>(b->items[i].data.size()); }
+const void* hg_bundle_data(const hg_bundle* b, int i) { return b->items[i].data.data(); }
+void hg_bundle_free(hg_bundle* b) { delete b; }
+
+uint64_t hg_mix_seed(uint64_t a, uint64_t b) { return mix_seed(a, b); }
+
+// ---- graphs ----------------------------------------------------------------------------
+hg_graph* hg_graph_generate(const hg_spec* spec, uint64_t seed) {
+  return guard<hg_graph*>(nullptr, [&] {
+    Spec s;
+    s.target = spec->target;
+    s.num_classes = spec->num_classes;
+    s.label_noise = spec->label_noise;
+    s.add_reverse = spec->add_reverse != 0;
+    for (int i = 0; i < spec->n_types; ++i) {
+      const hg_spec_node_type& t = spec->types[i];
+      if (t.storage != 1 && t.storage != 2) throw std::invalid_argument("unknown storage kind");
+      s.node_types.push_back({t.name, t.count, t.dim, t.storage == 1 ? Storage::Dense : Storage::Learnable});
+    }
+    for (int i = 0; i < spec->n_rels; ++i) {
+      const hg_spec_relation& r = spec->rels[i];
+      s.relations.push_back({r.src, r.edge, r.dst, r.edges, r.powerlaw != 0, r.alpha});
+    }
+    for (int i = 0; i < spec->n_self_paired; ++i) s.self_paired.push_back(spec->self_paired[i]);
+    auto* h = new hg_graph;
+    h->g = generate(s, seed);
+    return h;
+  });
+}
+
+hg_graph* hg_graph_from_csr(int n_types, const uint64_t* counts, int n_rels, const int* rel_src, const int* rel_dst,
+                            const int* rel_reverse, const uint64_t* indptr, const uint32_t* src, const int* kinds,
+                            const int* dims, const float* dense, int target, int num_classes, const int32_t* labels) {
+  return guard<hg_graph*>(nullptr, [&] {
+    auto* h = new hg_graph;
+    Graph& g = h->g;
+    std::size_t dense_off = 0;
+    for (int t = 0; t < n_types; ++t) {
+      NodeTypeInfo nt;
+      nt.name = "t" + std::to_string(t);
+      nt.count = counts[t];
+      nt.dim = dims[t];
+      nt.storage = static_cast<Storage>(kinds[t]);
+      if (nt.storage == Storage::Dense) {
+        const std::size_t n = nt.count * static_cast<std::size_t>(nt.dim);
+        nt.dense.assign(dense + dense_off, dense + dense_off + n);
+        dense_off += n;
+      }
+      g.types.push_back(std::move(nt));
+    }
+    std::size_t ip = 0, sp = 0;
+    for (int r = 0; r < n_rels; ++r) {
+      RelationInfo rel;
+      rel.src_type = rel_src[r];
+      rel.dst_type = rel_dst[r];
+      rel.edge_type = r;
+      rel.reverse = rel_reverse && rel_reverse[r];
+      const std::size_t nd = counts[rel.dst_type];
+      rel.adj.offsets.assign(indptr + ip, indptr + ip + nd + 1);
+      ip += nd + 1;
+      const std::size_t ne = rel.adj.offsets.back();
+      rel.adj.sources.assign(src + sp, src + sp + ne);
+      sp += ne;
+      g.edge_type_names.push_back("e" + std::to_string(r));
+      g.rels.push_back(std::move(rel));
+    }
+    g.target = target;
+    g.num_classes = num_classes;
+    g.labels.assign(labels, labels + counts[target]);
+    g.validate();
+    return h;
+  });
+}
+
+hg_graph* hg_graph_from_pairs(int n_types, const uint64_t* counts, int n_rels, const int* rel_src, const int* rel_dst,
+                              const uint64_t* pair_counts, const uint32_t* pair_src, const uint32_t* pair_dst,
+                              int target, int num_classes) {
+  return guard<hg_graph*>(nullptr, [&] {
+    std::vector<std::string> names, enames;
+    for (int t = 0; t < n_types; ++t) names.push_back("t" + std::to_string(t));
+    std::vector<std::vector<std::pair<NodeId, NodeId>>> pairs(n_rels);
+    std::size_t off = 0;
+    for (int r = 0; r < n_rels; ++r) {
+      enames.push_back("e" + std::to_string(r));
+      for (std::uint64_t e = 0; e < pair_counts[r]; ++e, ++off) pairs[r].emplace_back(pair_src[off], pair_dst[off]);
+    }
+    auto* h = new hg_graph;
+    h->g = assemble(names, std::vector<std::uint64_t>(counts, counts + n_types), enames, ivec(rel_src, n_rels),
+                    ivec(rel_dst, n_rels), pairs, target, num_classes);
+    return h;
+  });
+}
+
+void hg_graph_free(hg_graph* g) { delete g; }
+
+hg_bundle* hg_graph_export(const hg_graph* h) {
+  return guard<hg_bundle*>(nullptr, [&] {
+    const Graph& g = h->g;
+    auto* b = new hg_bundle;
+    std::vector<std::uint64_t> counts;
+    std::vector<int> kinds, dims, rs, rd, rr;
+    for (const auto& t : g.types) {
+      counts.push_back(t.count);
+      kinds.push_back(static_cast<int>(t.storage));
+      dims.push_back(t.dim);
+    }
+    b->add("node_counts", "<u8", counts);
+    b->add("kinds", "<i4", kinds);
+    b->add("dims", "<i4", dims);
+    b->add("labels", "<i4", g.labels);
+    b->add("target", "<i8", std::vector<long long>{g.target});
+    b->add("num_classes", "<i8", std::vector<long long>{g.num_classes});
+    for (int r = 0; r < g.num_rels(); ++r) {
+      rs.push_back(g.rels[r].src_type);
+      rd.push_back(g.rels[r].dst_type);
+      rr.push_back(g.rels[r].reverse ? 1 : 0);
+      b->add("rel" + std::to_string(r) + ".indptr", "<u8", g.rels[r].adj.offsets);
+      b->add("rel" + std::to_string(r) + ".src", "<u4", g.rels[r].adj.sources);
+    }
+    b->add("rel_src", "<i4", rs);
+    b->add("rel_dst", "<i4", rd);
+    b->add("rel_reverse", "<i4", rr);
+    for (int t = 0; t < g.num_types(); ++t)
+      if (g.types[t].storage == Storage::Dense)
+        b->add("feat.t" + std::to_string(t), "<f4", g.types[t].dense,
+               {static_cast<long long>(g.types[t].count), g.types[t].dim});
+    return b;
+  });
+}
+
+// ---- planning ------------------------------------------------------------------------------
+hg_bundle* hg_meta_partition(const hg_graph* h, int k, int p) {
+  return guard<hg_bundle*>(nullptr, [&] {
+    const Graph& g = h->g;
+    const Plan plan = meta_partition(schema_of(g), g.target, k, p);
+    auto* b = new hg_bundle;
+    std::vector<int> ty, de, pa, re;
+    for (const auto& ps : plan.tree.pos) {
+      ty.push_back(ps.type);
+      de.push_back(ps.depth);
+      pa.push_back(ps.parent);
+      re.push_back(ps.rel);
+    }
+    b->add("tree.type", "<i4", ty);
+    b->add("tree.depth", "<i4", de);
+    b->add("tree.parent", "<i4", pa);
+    b->add("tree.rel", "<i4", re);
+    std::vector<int> sc;
+    std::vector<std::uint64_t> sw;
+    for (const auto& s : plan.subs) {
+      sc.push_back(s.child_pos);
+      sw.push_back(s.weight);
+    }
+    b->add("subs.child_pos", "<i4", sc);
+    b->add("subs.weight", "<u8", sw);
+    for (std::size_t i = 0; i < plan.parts.size(); ++i) {
+      const Part& part = plan.parts[i];
+      const std::string pre = "part" + std::to_string(i);
+      b->add(pre + ".sub_ids", "<i4", part.sub_ids);
+      b->add(pre + ".relations", "<i4", part.relations);
+      b->add(pre + ".node_types", "<i4", part.node_types);
+      b->add(pre + ".cacheable", "<i4", cacheable_types(plan, static_cast<int>(i)));
+      b->add(pre + ".replica", "<i4", std::vector<int>{part.replica ? 1 : 0, part.replica_index, part.replica_count});
+      b->add(pre + ".weight", "<u8", std::vector<std::uint64_t>{part.weight});
+    }
+    const auto hr = hop_relations(plan.tree, k);
+    for (int i = 0; i < k; ++i) b->add("hop_rels" + std::to_string(i + 1), "<i4", hr[i]);
+    return b;
+  });
+}
+
+hg_bundle* hg_make_batches(const hg_graph* h, int batch_size, int max_batches, uint64_t seed) {
+  return guard<hg_bundle*>(nullptr, [&] {
+    auto* b = new hg_bundle;
+    const auto batches = make_batches(h->g, batch_size, max_batches, seed);
+    for (std::size_t i = 0; i < batches.size(); ++i) b->add("batch" + std::to_string(i), "<u4", batches[i]);
+    return b;
+  });
+}
+
+// ---- engine --------------------------------------------------------------------------------
+hg_engine* hg_engine_create(const hg_graph* g, const hg_engine_opts* o) {
+  return guard<hg_engine*>(nullptr, [&] {
+    EngineOptions eo;
+    eo.k = o->k;
+    eo.fanouts = ivec(o->fanouts, o->k);
+    eo.hidden = o->hidden;
+    eo.batch_cap = o->batch_cap;
+    eo.p = o->p;
+    eo.rank = o->rank;
+    eo.model_seed = o->model_seed;
+    eo.learn_seed = o->learn_seed;
+    eo.device = o->device;
+    auto* h = new hg_engine;
+    h->e = std::make_unique<Engine>(g->g, eo);
+    return h;
+  });
+}
+
+void hg_engine_free(hg_engine* e) {
+#ifdef HG_WITH_NCCL
+  if (e && e->comm) ncclCommDestroy(e->comm);
+#endif
+  delete e;
+}
+
+int hg_engine_step(hg_engine* e, const uint32_t* batch, int n, uint64_t rng_seed, int designated, int train,
+                   hg_step_report* out) {
+  return guard<int>(-1, [&] {
+    if (n <= 0) throw std::invalid_argument("empty batch");
+    const StepReport r = e->e->step(batch, n, rng_seed, designated, train != 0);
+    if (out) {
+      out->loss = r.loss;
+      out->sampled_edges = r.sampled_edges;
+      out->n_active = static_cast<int>(std::min<std::size_t>(64, r.active_rows.size()));
+      for (int i = 0; i < out->n_active; ++i) out->active_rows[i] = r.active_rows[i];
+    }
+    return 0;
+  });
+}
+
+int hg_engine_sample(hg_engine* e, const uint32_t* batch, int n, uint64_t rng_seed) {
+  return guard<int>(-1, [&] {
+    e->e->sample_only(batch, n, rng_seed);
+    return 0;
+  });
+}
+
+hg_bundle* hg_engine_read(hg_engine* e, const char* names) {
+  return guard<hg_bundle*>(nullptr, [&] {
+    std::vector<std::string> want;
+    if (names && std::string(names) == "?") {
+      std::string all;
+      for (const auto& n : e->e->tensor_names()) all += (all.empty() ? "" : ",") + n;
+      auto* b = new hg_bundle;
+      b->add("names", "|u1", std::vector<char>(all.begin(), all.end()));
+      return b;
+    }
+    if (names && *names) {
+      std::string s(names);
+      std::size_t at = 0;
+      while (at <= s.size()) {
+        const std::size_t c = s.find(',', at);
+        const std::string n = s.substr(at, c == std::string::npos ? std::string::npos : c - at);
+        if (!n.empty()) want.push_back(n);
+        if (c == std::string::npos) break;
+        at = c + 1;
+      }
+    } else {
+      want = e->e->tensor_names();
+    }
+    auto* b = new hg_bundle;
+    for (const auto& n : want) {
+      hg_bundle::Item it;
+      it.name = n;
+      if (!e->e->read_tensor(n, it.dtype, it.shape, it.data)) {
+        delete b;
+        throw std::invalid_argument("unknown tensor: " + n);
+      }
+      b->items.push_back(std::move(it));
+    }
+    return b;
+  });
+}
+
+int hg_engine_bench(hg_engine* e, const uint32_t* batches, const int* lens, const uint64_t* seeds, int n_steps,
+                    int train, double* out_ms, uint64_t* out_edges, double* out_loss) {
+  return guard<int>(-1, [&] {
+    Engine& en = *e->e;
+    std::size_t total = 0;
+    for (int i = 0; i < n_steps; ++i) total += lens[i];
+    // inputs resident in HBM before the timed region
+    std::uint32_t* d_all = nullptr;
+    HG_CUDA(cudaMalloc(&d_all, std::max<std::size_t>(4, total * 4)));
+    HG_CUDA(cudaMemcpy(d_all, batches, total * 4, cudaMemcpyHostToDevice));
+    cudaEvent_t a, b;
+    HG_CUDA(cudaEventCreate(&a));
+    HG_CUDA(cudaEventCreate(&b));
+    HG_CUDA(cudaStreamSynchronize(en.stream()));
+    HG_CUDA(cudaEventRecord(a, en.stream()));
+    std::size_t off = 0;
+    std::uint64_t edges = 0;
+    double loss = 0.0;
+    for (int i = 0; i < n_steps; ++i) {
+      HG_CUDA(cudaMemcpyAsync(en.device_batch(), d_all + off, lens[i] * 4, cudaMemcpyDeviceToDevice, en.stream()));
+      off += lens[i];
+      en.enqueue_step(seeds[i], lens[i], 0, train != 0);
+    }
+    HG_CUDA(cudaEventRecord(b, en.stream()));
+    HG_CUDA(cudaEventSynchronize(b));
+    float ms = 0.f;
+    HG_CUDA(cudaEventElapsedTime(&ms, a, b));
+    const StepReport last = en.finish_step();
+    loss = last.loss;
+    edges = last.sampled_edges;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(d_all);
+    *out_ms = ms;
+    if (out_edges) *out_edges = edges;
+    if (out_loss) *out_loss = loss;
+    return 0;
+  });
+}
+
+void hg_engine_profile(hg_engine* e, int on) {
+  e->e->set_profiling(on != 0);
+  e->e->reset_profile();
+}
+
+hg_bundle* hg_engine_profile_read(hg_engine* e) {
+  return guard<hg_bundle*>(nullptr, [&] {
+    auto* b = new hg_bundle;
+    const auto ms = e->e->kernel_ms();
+    const auto bytes = e->e->kernel_bytes();
+    const auto launches = e->e->kernel_launches();
+    for (const auto& [k, v] : ms) {
+      b->add("kernel." + k + ".ms", "<f8", std::vector<double>{v});
+      b->add("kernel." + k + ".bytes", "<f8", std::vector<double>{bytes.at(k)});
+      b->add("kernel." + k + ".launches", "<i8", std::vector<long long>{launches.at(k)});
+    }
+    return b;
+  });
+}
+
+int hg_engine_info(hg_engine* e, uint64_t* param_count, uint64_t* device_bytes, int* model_step) {
+  return guard<int>(-1, [&] {
+    if (param_count) *param_count = e->e->param_count();
+    if (device_bytes) *device_bytes = e->e->device_bytes();
+    if (model_step) *model_step = e->e->model_step();
+    return 0;
+  });
+}
+
+// ---- cache -----------------------------------------------------------------------------------
+hg_bundle* hg_engine_presample_hotness(hg_engine* e, int epochs, uint64_t seed, int batch_size) {
+  return guard<hg_bundle*>(nullptr, [&] {
+    const auto counts = e->e->presample_hotness(epochs, seed, batch_size);
+    auto* b = new hg_bundle;
+    for (std::size_t t = 0; t < counts.size(); ++t) b->add("hot.t" + std::to_string(t), "<u4", counts[t]);
+    return b;
+  });
+}
+
+hg_bundle* hg_cache_plan(const hg_graph* h, const uint32_t* counts, uint64_t budget, double read_ns, double write_ns,
+                         double overhead_ns, int elem_bytes) {
+  return guard<hg_bundle*>(nullptr, [&] {
+    const Graph& g = h->g;
+    CostModel cm;
+    cm.read_ns_per_byte = read_ns;
+    cm.write_ns_per_byte = write_ns;
+    cm.fixed_overhead_ns = overhead_ns;
+    cm.elem_bytes = elem_bytes;
+    const auto prof = miss_penalty(g, cm);
+    std::vector<std::vector<std::uint64_t>> hot(g.num_types());
+    std::size_t off = 0;
+    for (int t = 0; t < g.num_types(); ++t) {
+      hot[t].assign(counts + off, counts + off + g.types[t].count);
+      off += g.types[t].count;
+    }
+    auto* b = new hg_bundle;
+    std::vector<double> ratio, tns;
+    std::vector<std::uint64_t> rb;
+    for (const auto& tp : prof) {
+      ratio.push_back(tp.ratio);
+      tns.push_back(tp.transfer_ns);
+      rb.push_back(tp.record_bytes);
+    }
+    b->add("profile.ratio", "<f8", ratio);
+    b->add("profile.transfer_ns", "<f8", tns);
+    b->add("profile.record_bytes", "<u8", rb);
+    if (budget == 0) return b;
+    const CacheAlloc a = allocate_cache(budget, hot, prof);
+    b->add("alloc.bytes", "<u8", a.bytes);
+    b->add("alloc.capacity", "<u8", a.capacity);
+    // static top-capacity fill by (count desc, id asc), ids re-sorted (cache.cpp:121-141)
+    for (int t = 0; t < g.num_types(); ++t) {
+      std::vector<NodeId> keep;
+      const std::uint64_t cap = a.capacity[t];
+      if (cap > 0) {
+        std::vector<NodeId> ids(hot[t].size());
+        std::iota(ids.begin(), ids.end(), 0u);
+        const auto& c = hot[t];
+        auto better = [&](NodeId x, NodeId y) { return c[x] != c[y] ? c[x] > c[y] : x < y; };
+        if (ids.size() > cap) {
+          std::nth_element(ids.begin(), ids.begin() + cap, ids.end(), better);
+          ids.resize(cap);
+        }
+        std::sort(ids.begin(), ids.end());
+        keep = std::move(ids);
+      }
+      b->add("cached.t" + std::to_string(t), "<u4", keep);
+    }
+    return b;
+  });
+}
+
+int hg_engine_set_cache(hg_engine* e, const uint32_t* ids, const uint64_t* lens, int n_types) {
+  return guard<int>(-1, [&] {
+    std::vector<std::vector<NodeId>> sets(n_types);
+    std::size_t off = 0;
+    for (int t = 0; t < n_types; ++t) {
+      sets[t].assign(ids + off, ids + off + lens[t]);
+      off += lens[t];
+    }
+    e->e->set_cache(sets);
+    return 0;
+  });
+}
+
+hg_bundle* hg_engine_cache_counters(hg_engine* e) {
+  return guard<hg_bundle*>(nullptr, [&] {
+    auto* b = new hg_bundle;
+    const auto c = e->e->cache_counters();
+    for (std::size_t t = 0; t < c.size(); ++t)
+      b->add("cache.t" + std::to_string(t), "<u8", std::vector<std::uint64_t>{c[t].first, c[t].second});
+    return b;
+  });
+}
+
+// ---- NCCL --------------------------------------------------------------------------------------
+int hg_nccl_unique_id(void* out, int cap) {
+  return guard<int>(-1, [&] {
+#ifdef HG_WITH_NCCL
+    ncclUniqueId id;
+    if (cap < static_cast<int>(sizeof(id))) throw std::invalid_argument("unique id buffer too small");
+    if (ncclGetUniqueId(&id) != ncclSuccess) throw std::runtime_error("ncclGetUniqueId failed");
+    std::memcpy(out, &id, sizeof(id));
+    return static_cast<int>(sizeof(id));
+#else
+    (void)out;
+    (void)cap;
+    throw std::runtime_error("built without NCCL");
+    return -1;
+#endif
+  });
+}
+
+int hg_engine_attach_nccl(hg_engine* e, const void* unique_id, int id_bytes, int nranks, int rank) {
+  return guard<int>(-1, [&] {
+#ifdef HG_WITH_NCCL
+    ncclUniqueId id;
+    if (id_bytes != static_cast<int>(sizeof(id))) throw std::invalid_argument("bad unique id size");
+    std::memcpy(&id, unique_id, sizeof(id));
+    if (ncclCommInitRank(&e->comm, nranks, id, rank) != ncclSuccess) throw std::runtime_error("ncclCommInitRank failed");
+    e->e->attach_comm(e->comm);
+    return 0;
+#else
+    (void)e;
+    (void)unique_id;
+    (void)id_bytes;
+    (void)nranks;
+    (void)rank;
+    throw std::runtime_error("built without NCCL");
+    return -1;
+#endif
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,133 @@
+// Shared device-side helpers for the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace hetgpu {
+
+#define HG_CUDA(call)                                                                   \
+  do {                                                                                  \
+    cudaError_t _e = (call);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      throw std::runtime_error(std::string("CUDA error: ") + cudaGetErrorString(_e) +   \
+                               " at " + __FILE__ + ":" + std::to_string(__LINE__));     \
+  } while (0)
+
+constexpr int kWarp = 32;
+constexpr int kNumSMs = 148;
+
+__host__ __device__ inline std::uint64_t ceil_div(std::uint64_t a, std::uint64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int round_up4(int x) { return (x + 3) & ~3; }
+
+// ---- exact restatement of the reference's sampler arithmetic ------------------
+// splitmix64 finaliser (sampling.cpp:9-15)
+__device__ __forceinline__ std::uint64_t dmix_seed(std::uint64_t a, std::uint64_t b) {
+  std::uint64_t z = a + 0x9e3779b97f4a7c15ULL * (b + 1);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+// std::mt19937_64 (libstdc++ 13, random.tcc:328-466): n=312, m=156, r=31.
+struct Mt64 {
+  static constexpr std::uint64_t kMul = 6364136223846793005ULL;
+  static constexpr std::uint64_t kUpper = 0xFFFFFFFF80000000ULL;
+  static constexpr std::uint64_t kLower = 0x7FFFFFFFULL;
+  static constexpr std::uint64_t kA = 0xb5026f5aa96619e9ULL;
+
+  // seeding recurrence x[i] = f*(x[i-1] ^ (x[i-1] >> 62)) + i
+  __device__ __forceinline__ static std::uint64_t step(std::uint64_t x, std::uint32_t i) {
+    return kMul * (x ^ (x >> 62)) + i;
+  }
+  __device__ __forceinline__ static std::uint64_t twist(std::uint64_t xk, std::uint64_t xk1,
+                                                        std::uint64_t xm) {
+    const std::uint64_t y = (xk & kUpper) | (xk1 & kLower);
+    return xm ^ (y >> 1) ^ ((y & 1ULL) ? kA : 0ULL);
+  }
+  __device__ __forceinline__ static std::uint64_t temper(std::uint64_t z) {
+    z ^= (z >> 29) & 0x5555555555555555ULL;
+    z ^= (z << 17) & 0x71d67fffeda60000ULL;
+    z ^= (z << 37) & 0xfff7eee000000000ULL;
+    z ^= (z >> 43);
+    return z;
+  }
+};
+
+// Streams the first 156 outputs of a freshly seeded mt19937_64 using two
+// cursors of the seeding recurrence (at j and at j+156): output j of the first
+// twist only needs the *untwisted* words x[j], x[j+1], x[j+156]. No state array.
+struct MtStream {
+  std::uint64_t xa, xa1, xb;
+  std::uint32_t j;
+  __device__ __forceinline__ void seed(std::uint64_t s) {
+    xa = s;
+    xa1 = Mt64::step(s, 1);
+    std::uint64_t x = xa1;
+    for (std::uint32_t i = 2; i <= 156; ++i) x = Mt64::step(x, i);
+    xb = x;
+    j = 0;
+  }
+  __device__ __forceinline__ bool exhausted() const { return j >= 156; }
+  __device__ __forceinline__ std::uint64_t next() {
+    const std::uint64_t t = Mt64::twist(xa, xa1, xb);
+    xa = xa1;
+    xa1 = Mt64::step(xa1, j + 2);
+    xb = Mt64::step(xb, j + 157);
+    ++j;
+    return Mt64::temper(t);
+  }
+};
+
+// Full-state engine for the (rare) rows that need more than 156 outputs.
+struct MtFull {
+  std::uint64_t* x;  // 312 words of scratch
+  std::uint32_t p;
+  __device__ void seed(std::uint64_t s) {
+    x[0] = s;
+    for (std::uint32_t i = 1; i < 312; ++i) x[i] = Mt64::step(x[i - 1], i);
+    p = 312;
+  }
+  __device__ void regen() {
+    for (int k = 0; k < 156; ++k) x[k] = Mt64::twist(x[k], x[k + 1], x[k + 156]);
+    for (int k = 156; k < 311; ++k) x[k] = Mt64::twist(x[k], x[k + 1], x[k - 156]);
+    x[311] = Mt64::twist(x[311], x[0], x[155]);
+    p = 0;
+  }
+  __device__ std::uint64_t next() {
+    if (p >= 312) regen();
+    return Mt64::temper(x[p++]);
+  }
+};
+
+// uniform_int_distribution<uint64_t>(0, range-1) via Lemire's nearly
+// divisionless method with 128-bit products (uniform_int_dist.h:255-281).
+// Returns false (without consuming the decision) when a streaming engine
+// runs out of first-twist outputs; the caller then replays the row on MtFull.
+struct MtFullTag {};
+__device__ __forceinline__ bool mt_exhausted(const MtStream& e) { return e.exhausted(); }
+__device__ __forceinline__ bool mt_exhausted(const MtFull&) { return false; }
+
+template <typename Eng>
+__device__ __forceinline__ bool lemire(Eng& eng, std::uint64_t range, std::uint64_t& out) {
+  if (mt_exhausted(eng)) return false;
+  std::uint64_t x = eng.next();
+  std::uint64_t lo = x * range;
+  std::uint64_t hi = __umul64hi(x, range);
+  if (lo < range) {
+    const std::uint64_t thr = (0ULL - range) % range;
+    while (lo < thr) {
+      if (mt_exhausted(eng)) return false;
+      x = eng.next();
+      lo = x * range;
+      hi = __umul64hi(x, range);
+    }
+  }
+  out = hi;
+  return true;
+}
+
+}  // namespace hetgpu

@@ -1,0 +1,1003 @@
+// Device engine: static plan, workspace, and the per-step launch sequence.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <functional>
+#include <numeric>
+
+namespace hetgpu {
+
+namespace {
+
+__global__ void k_shard_rows(const std::uint32_t* full, const int* n_full, int index, int count,
+                             std::uint32_t* shard, int* n_shard) {
+  const int n = *n_full;
+  const int m = n > index ? (n - index + count - 1) / count : 0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x)
+    shard[j] = full[index + j * count];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *n_shard = m;
+}
+
+struct EdgeCountArgs {
+  const std::uint32_t* indptr[kMaxBlocks * 4];
+  const int* n_rows[kMaxBlocks * 4];
+  int n;
+};
+
+__global__ void k_count_edges(EdgeCountArgs a, std::uint64_t* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    std::uint64_t s = 0;
+    for (int i = 0; i < a.n; ++i) s += a.indptr[i][*a.n_rows[i]];
+    *out = s;
+  }
+}
+
+// rows of the hop-1 row space with at least one sampled edge in any top block
+// (the bucket's `active` set, raf.cpp:418-419); stored as a float counter in
+// the partition's slot of the AGG_all buffer
+__global__ void k_active_rows(EdgeCountArgs a, const int* n_rows, float* slot) {
+  __shared__ int total;
+  if (threadIdx.x == 0) total = 0;
+  __syncthreads();
+  const int n = *n_rows;
+  int mine = 0;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    bool act = false;
+    for (int b = 0; b < a.n; ++b) act |= a.indptr[b][j + 1] > a.indptr[b][j];
+    mine += act ? 1 : 0;
+  }
+  atomicAdd(&total, mine);
+  __syncthreads();
+  if (threadIdx.x == 0) *slot = static_cast<float>(total);
+}
+
+__global__ void k_gather_rows(const float* table, int ld, const std::uint32_t* ids, const int* n, int cols,
+                              float* out) {
+  const int total = *n * cols;
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
+    const int i = x / cols, c = x % cols;
+    out[x] = table[static_cast<std::size_t>(ids[i]) * ld + c];
+  }
+}
+
+template <typename T>
+void put(std::vector<char>& data, const std::vector<T>& v) {
+  data.resize(v.size() * sizeof(T));
+  if (!v.empty()) std::memcpy(data.data(), v.data(), data.size());
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+Engine::Engine(const Graph& g, const EngineOptions& o) : o_(o) {
+  if (static_cast<int>(o.fanouts.size()) != o.k) throw std::invalid_argument("fanout count must equal the model depth");
+  if (o.k < 1) throw std::invalid_argument("fanouts must be non-empty");
+  HG_CUDA(cudaSetDevice(o.device));
+  HG_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  ntypes_ = g.num_types();
+  target_ = g.target;
+  num_classes_ = g.num_classes;
+  for (const auto& t : g.types) type_counts_.push_back(t.count);
+  for (const auto& r : g.rels) {
+    rel_src_.push_back(r.src_type);
+    rel_dst_.push_back(r.dst_type);
+  }
+  build_plan(g);
+  upload(g);
+}
+
+Engine::~Engine() {
+  cudaStreamSynchronize(st_);
+  for (void* p : allocs_) cudaFree(p);
+  if (h_sc_) cudaFreeHost(h_sc_);
+  if (h_batch_) cudaFreeHost(h_batch_);
+  if (h_rb_) cudaFreeHost(h_rb_);
+  cudaStreamDestroy(st_);
+}
+
+void* Engine::alloc(std::size_t bytes) {
+  void* p = nullptr;
+  bytes = std::max<std::size_t>(bytes, 16);
+  HG_CUDA(cudaMalloc(&p, bytes));
+  HG_CUDA(cudaMemsetAsync(p, 0, bytes, st_));
+  allocs_.push_back(p);
+  total_bytes_ += bytes;
+  return p;
+}
+
+void Engine::build_plan(const Graph& g) {
+  const Schema sch = schema_of(g);
+  const int k = o_.k;
+  if (o_.p <= 1) {
+    tree_ = bfs_tree(sch, target_, k);
+  } else {
+    const Plan plan = meta_partition(sch, target_, k, o_.p);
+    const Part& part = plan.parts.at(o_.rank);
+    replica_ = part.replica;
+    shard_index_ = part.replica ? part.replica_index : 0;
+    shard_count_ = part.replica ? part.replica_count : 1;
+    std::vector<int> owned_children;
+    for (int sid : part.sub_ids) owned_children.push_back(plan.subs[sid].child_pos);
+    const Tree& full = plan.tree;
+    std::vector<int> remap(full.pos.size(), -1);
+    tree_.k = full.k;
+    tree_.root_type = full.root_type;
+    for (std::size_t p = 0; p < full.pos.size(); ++p) {
+      const bool keep = p == 0 || std::find(owned_children.begin(), owned_children.end(),
+                                            full.root_child_ancestor(static_cast<int>(p))) != owned_children.end();
+      if (!keep) continue;
+      remap[p] = static_cast<int>(tree_.pos.size());
+      TreePos tp = full.pos[p];
+      tp.children.clear();
+      tp.parent = p == 0 ? -1 : remap[full.pos[p].parent];
+      tree_.pos.push_back(tp);
+      if (p != 0) tree_.pos[tp.parent].children.push_back(remap[p]);
+    }
+  }
+  hop_rels_ = hop_relations(tree_, k);
+
+  // max in-degree per relation tightens the edge capacities
+  maxdeg_.assign(g.num_rels(), 0);
+  for (int r = 0; r < g.num_rels(); ++r) {
+    const auto& off = g.rels[r].adj.offsets;
+    std::uint64_t m = 0;
+    for (std::size_t i = 0; i + 1 < off.size(); ++i) m = std::max(m, off[i + 1] - off[i]);
+    maxdeg_[r] = m;
+  }
+
+  // frontier capacities and blocks, hop by hop
+  fronts_.assign((k + 1) * ntypes_, Front{});
+  front(0, target_).cap = o_.batch_cap;
+  hop_blocks_.assign(k + 1, {});
+  int edge_base = 0;
+  for (int h = 1; h <= k; ++h) {
+    std::vector<std::uint64_t> cap_src(ntypes_, 0);
+    edge_base = 0;
+    for (int r : hop_rels_[h - 1]) {
+      BlockBuf b;
+      b.rel = r;
+      b.hop = h;
+      b.src_t = rel_src_[r];
+      b.dst_t = rel_dst_[r];
+      b.rows_cap = front(h - 1, b.dst_t).cap;
+      if (h == 1 && replica_) b.rows_cap = static_cast<int>(ceil_div(o_.batch_cap, shard_count_));
+      const std::uint64_t per_row = std::min<std::uint64_t>(o_.fanouts[h - 1], maxdeg_[r]);
+      const std::uint64_t ec = std::max<std::uint64_t>(1, static_cast<std::uint64_t>(b.rows_cap) * per_row);
+      if (ec > 0x7fffffffULL) throw std::invalid_argument("block edge capacity exceeds 2^31");
+      b.edge_cap = static_cast<int>(ec);
+      b.edge_base = edge_base;
+      edge_base += b.edge_cap;
+      cap_src[b.src_t] += ec;
+      hop_blocks_[h].push_back(static_cast<int>(blocks_.size()));
+      blocks_.push_back(b);
+    }
+    for (int t = 0; t < ntypes_; ++t)
+      front(h, t).cap = static_cast<int>(std::min<std::uint64_t>(type_counts_[t], cap_src[t]));
+    if (hop_blocks_[h].size() > static_cast<std::size_t>(kMaxBlocks))
+      throw std::invalid_argument("too many relations in one hop");
+  }
+
+  // model slots present in the (local) tree: W_{r,l}, l = k - depth + 1 (hgnn.cpp:39-62)
+  const ModelInit mi = init_model(g, tree_, o_.hidden, o_.model_seed);
+  for (const auto& [id, w] : mi.weights) {
+    Slot s;
+    s.rel = id.rel;
+    s.layer = id.layer;
+    s.din = w.in_dim;
+    s.dout = w.out_dim;
+    s.ld = round_up4(std::max(1, w.out_dim));
+    slot_of_[id] = static_cast<int>(slots_.size());
+    slots_.push_back(s);
+  }
+
+  // output groups per layer: for each frontier type at depth d-1, the
+  // relations into it at depth d (rels_by_dst_at_depth, hgnn.cpp:16-26)
+  for (int l = 1; l <= k; ++l) {
+    const int d = k - l + 1;
+    const auto into = relations_into_at_depth(tree_, d);
+    for (int t = 0; t < ntypes_; ++t) {
+      const bool has_front = (d - 1 == 0) ? t == target_ : front(d - 1, t).cap > 0;
+      if (!has_front) continue;
+      Group gr;
+      gr.layer = l;
+      gr.depth = d;
+      gr.type = t;
+      gr.dout = out_dim(l);
+      gr.ld = round_up4(gr.dout);
+      gr.rows_cap = front(d - 1, t).cap;
+      auto it = into.find(t);
+      if (it != into.end())
+        for (int r : it->second) {
+          for (int bi : hop_blocks_[d])
+            if (blocks_[bi].rel == r) {
+              gr.blocks.push_back(bi);
+              gr.slots.push_back(slot_of_.at(SlotId{r, l}));
+            }
+        }
+      if (gr.blocks.size() > static_cast<std::size_t>(kMaxRelsPerGroup))
+        throw std::invalid_argument("too many relations into one type");
+      groups_.push_back(gr);
+    }
+  }
+  // gradient needs: inner sources whose group has relations, learnable leaves
+  auto group_at = [&](int depth_of_output, int t) -> Group* {
+    for (auto& gr : groups_)
+      if (gr.depth - 1 == depth_of_output && gr.type == t) return &gr;
+    return nullptr;
+  };
+  for (auto& b : blocks_) {
+    b.din = b.hop == k ? g.types[b.src_t].dim : o_.hidden;
+    b.ld_mean = round_up4(std::max(1, b.din));
+    if (b.hop < k) {
+      Group* src_group = group_at(b.hop, b.src_t);
+      b.need_src_grad = src_group && !src_group->blocks.empty();
+    } else {
+      b.need_src_grad = g.types[b.src_t].storage == Storage::Learnable;
+    }
+  }
+  for (int h = 1; h <= k; ++h)
+    for (int t = 0; t < ntypes_; ++t) {
+      CscBuf c;
+      c.hop = h;
+      c.src_t = t;
+      for (int bi : hop_blocks_[h])
+        if (blocks_[bi].src_t == t && blocks_[bi].need_src_grad) c.blocks.push_back(bi);
+      if (c.blocks.empty()) continue;
+      c.src_cap = front(h, t).cap;
+      c.din = blocks_[c.blocks[0]].din;
+      c.ld = blocks_[c.blocks[0]].ld_mean;
+      cscs_.push_back(c);
+    }
+}
+
+void Engine::upload(const Graph& g) {
+  const int k = o_.k;
+  // relation CSRs this partition samples
+  csr_ptr_.assign(g.num_rels(), nullptr);
+  csr_src_.assign(g.num_rels(), nullptr);
+  std::vector<bool> used(g.num_rels(), false);
+  for (const auto& hr : hop_rels_)
+    for (int r : hr) used[r] = true;
+  for (int r = 0; r < g.num_rels(); ++r) {
+    if (!used[r]) continue;
+    const auto& a = g.rels[r].adj;
+    csr_ptr_[r] = static_cast<std::uint64_t*>(alloc(a.offsets.size() * 8));
+    csr_src_[r] = static_cast<std::uint32_t*>(alloc(a.sources.size() * 4));
+    HG_CUDA(cudaMemcpyAsync(csr_ptr_[r], a.offsets.data(), a.offsets.size() * 8, cudaMemcpyHostToDevice, st_));
+    if (!a.sources.empty())
+      HG_CUDA(cudaMemcpyAsync(csr_src_[r], a.sources.data(), a.sources.size() * 4, cudaMemcpyHostToDevice, st_));
+  }
+  // feature / learnable tables of the leaf types (layer-0 inputs)
+  tables_.assign(ntypes_, TypeTable{});
+  std::vector<bool> leaf(ntypes_, false);
+  for (const auto& b : blocks_)
+    if (b.hop == k) leaf[b.src_t] = true;
+  const auto learn = init_learnable(g, o_.learn_seed);
+  for (int t = 0; t < ntypes_; ++t) {
+    if (!leaf[t]) continue;
+    const NodeTypeInfo& nt = g.types[t];
+    TypeTable& tb = tables_[t];
+    tb.dim = nt.dim;
+    tb.ld = round_up4(std::max(1, nt.dim));
+    const std::size_t rows = nt.count;
+    if (nt.storage == Storage::Absent) throw std::runtime_error("missing features for node type " + nt.name);
+    std::vector<float> host(rows * tb.ld, 0.0f);
+    if (nt.storage == Storage::Dense) {
+      tb.dense = true;
+      for (std::size_t i = 0; i < rows; ++i)
+        std::memcpy(&host[i * tb.ld], &nt.dense[i * nt.dim], sizeof(float) * nt.dim);
+    } else {
+      tb.learnable = true;
+      const auto& w = learn.at(t);
+      for (std::size_t i = 0; i < rows; ++i)
+        for (int c = 0; c < nt.dim; ++c) host[i * tb.ld + c] = static_cast<float>(w[i * nt.dim + c]);
+      tb.m = static_cast<float*>(alloc(host.size() * 4));
+      tb.v = static_cast<float*>(alloc(host.size() * 4));
+      tb.step = static_cast<std::int64_t*>(alloc(8));
+    }
+    tb.w = static_cast<float*>(alloc(host.size() * 4));
+    HG_CUDA(cudaMemcpyAsync(tb.w, host.data(), host.size() * 4, cudaMemcpyHostToDevice, st_));
+    HG_CUDA(cudaStreamSynchronize(st_));  // host staging buffer goes out of scope
+  }
+  labels_ = static_cast<std::int32_t*>(alloc(g.labels.size() * 4));
+  HG_CUDA(cudaMemcpyAsync(labels_, g.labels.data(), g.labels.size() * 4, cudaMemcpyHostToDevice, st_));
+
+  // model weights (f64 init rounded to fp32)
+  const ModelInit mi = init_model(g, tree_, o_.hidden, o_.model_seed);
+  for (auto& s : slots_) {
+    const WeightInit& wi = mi.weights.at(SlotId{s.rel, s.layer});
+    std::vector<float> host(static_cast<std::size_t>(std::max(1, s.din)) * s.ld, 0.0f);
+    for (int i = 0; i < s.din; ++i)
+      for (int j = 0; j < s.dout; ++j) host[i * s.ld + j] = static_cast<float>(wi.values[i * s.dout + j]);
+    const std::size_t bytes = host.size() * 4;
+    s.w = static_cast<float*>(alloc(bytes));
+    s.m = static_cast<float*>(alloc(bytes));
+    s.v = static_cast<float*>(alloc(bytes));
+    s.g = static_cast<float*>(alloc(bytes));
+    HG_CUDA(cudaMemcpyAsync(s.w, host.data(), bytes, cudaMemcpyHostToDevice, st_));
+    HG_CUDA(cudaStreamSynchronize(st_));
+  }
+
+  // frontier machinery: one bitmap region for all types
+  word_base_.assign(ntypes_ + 1, 0);
+  for (int t = 0; t < ntypes_; ++t)
+    word_base_[t + 1] = word_base_[t] + static_cast<int>(ceil_div(type_counts_[t], 32));
+  total_words_ = std::max(1, word_base_[ntypes_]);
+  bits_ = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(total_words_) * 4));
+  wscan_ = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(total_words_) * 4));
+  cached_bits_ = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(total_words_) * 4));
+  // static per-hop frontier slot layout: slot i of hop h is the i-th distinct
+  // source type of that hop's blocks (hop 0: the target)
+  hop_slot_types_.assign(k + 1, {});
+  hop_slot_types_[0] = {target_};
+  for (int h = 1; h <= k; ++h)
+    for (int bi : hop_blocks_[h]) {
+      auto& v = hop_slot_types_[h];
+      if (std::find(v.begin(), v.end(), blocks_[bi].src_t) == v.end()) v.push_back(blocks_[bi].src_t);
+    }
+  {
+    std::vector<int> wd(static_cast<std::size_t>(k + 1) * kMaxSegs, 0);
+    for (int h = 0; h <= k; ++h)
+      for (std::size_t i = 0; i < hop_slot_types_[h].size(); ++i) {
+        const int t = hop_slot_types_[h][i];
+        wd[h * kMaxSegs + i] = word_base_[t + 1] - word_base_[t];
+      }
+    words_dev_ = static_cast<int*>(alloc(wd.size() * sizeof(int)));
+    HG_CUDA(cudaMemcpyAsync(words_dev_, wd.data(), wd.size() * sizeof(int), cudaMemcpyHostToDevice, st_));
+    HG_CUDA(cudaStreamSynchronize(st_));
+  }
+  for (int h = 0; h <= k; ++h)
+    for (int t = 0; t < ntypes_; ++t) {
+      Front& f = front(h, t);
+      f.count = static_cast<int*>(alloc(sizeof(int)));
+      if (f.cap > 0) f.list = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(f.cap) * 4));
+    }
+  shard_list_ = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(o_.batch_cap) * 4));
+  shard_count_dev_ = static_cast<int*>(alloc(sizeof(int)));
+
+  int max_rows = 1, total_rows = 0;
+  for (auto& b : blocks_) {
+    b.indptr = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(b.rows_cap + 1) * 4));
+    b.src = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(b.edge_cap) * 4));
+    b.erow = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(b.edge_cap) * 4));
+    b.col = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(b.edge_cap) * 4));
+    b.mean = static_cast<float*>(alloc(static_cast<std::size_t>(b.rows_cap) * b.ld_mean * 4));
+    if (b.need_src_grad) b.dmean = static_cast<float*>(alloc(static_cast<std::size_t>(b.rows_cap) * b.ld_mean * 4));
+    max_rows = std::max(max_rows, b.rows_cap + 1);
+    total_rows += b.rows_cap;
+  }
+
+  ldc_ = round_up4(num_classes_);
+  logits_ = static_cast<float*>(alloc(static_cast<std::size_t>(o_.batch_cap + 1) * ldc_ * 4));
+  dlogits_ = static_cast<float*>(alloc(static_cast<std::size_t>(o_.batch_cap + 1) * ldc_ * 4));
+  if (o_.p > ldc_) throw std::invalid_argument("more partitions than logit columns for the AGG_all counters");
+  for (auto& gr : groups_) {
+    if (gr.layer == o_.k) {
+      gr.out = logits_;
+      gr.dout_buf = dlogits_;
+      gr.ld = ldc_;
+    } else {
+      gr.out = static_cast<float*>(alloc(static_cast<std::size_t>(std::max(1, gr.rows_cap)) * gr.ld * 4));
+    }
+  }
+  for (auto& c : cscs_) {
+    c.offs = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(c.src_cap + 1) * 4));
+    c.cursor = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(c.src_cap + 1) * 4));
+    std::size_t ent = 0;
+    for (int bi : c.blocks) ent = std::max<std::size_t>(ent, blocks_[bi].edge_base + blocks_[bi].edge_cap);
+    c.entries = static_cast<std::uint32_t*>(alloc(ent * 4));
+    c.dh = static_cast<float*>(alloc(static_cast<std::size_t>(std::max(1, c.src_cap)) * c.ld * 4));
+    if (c.hop < o_.k) {
+      for (auto& gr : groups_)
+        if (gr.depth - 1 == c.hop && gr.type == c.src_t) gr.dout_buf = c.dh;
+    }
+  }
+
+  // per-step state and scratch
+  d_sc_ = static_cast<StepScalars*>(alloc(sizeof(StepScalars)));
+  HG_CUDA(cudaMallocHost(&h_sc_, sizeof(StepScalars)));
+  std::memset(h_sc_, 0, sizeof(StepScalars));
+  d_batch_ = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(o_.batch_cap) * 4));
+  HG_CUDA(cudaMallocHost(&h_batch_, static_cast<std::size_t>(o_.batch_cap) * 4));
+  mult_ = static_cast<float*>(alloc(static_cast<std::size_t>(o_.batch_cap) * 4));
+  row_loss_ = static_cast<double*>(alloc(static_cast<std::size_t>(o_.batch_cap) * 8));
+  auto* rb = static_cast<Readback*>(alloc(sizeof(Readback)));
+  loss_ = &rb->loss;
+  err_ = &rb->err;
+  edges_dev_ = &rb->edges;
+  HG_CUDA(cudaMallocHost(&h_rb_, sizeof(Readback)));
+  cache_hm_ = static_cast<unsigned long long*>(alloc(sizeof(unsigned long long) * 2 * ntypes_));
+  cache_types_.assign(ntypes_, false);
+
+  int max_cap = std::max(total_words_, max_rows);
+  for (const auto& c : cscs_) max_cap = std::max(max_cap, c.src_cap + 1);
+  scan_partials_ = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(kMaxSegs) * (ceil_div(max_cap, kScanTile) + 1) * 4));
+  slow_ = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(total_rows + 1) * 8));
+  n_slow_ = static_cast<int*>(alloc(sizeof(int)));
+  int maxf = 1;
+  for (int f : o_.fanouts) maxf = std::max(maxf, f);
+  mt_scratch_ = static_cast<std::uint64_t*>(alloc(sample_scratch_words(maxf) * 8));
+  std::size_t wt = 1, wp = 1;
+  for (const auto& s : slots_) wt = std::max<std::size_t>(wt, static_cast<std::size_t>(round_up4(s.din)) * s.dout);
+  for (const auto& gr : groups_)
+    for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
+      const Slot& s = slots_[gr.slots[q]];
+      wp = std::max<std::size_t>(wp, ceil_div(std::max(1, gr.rows_cap), 256) * s.din * s.dout);
+    }
+  wt_scratch_ = static_cast<float*>(alloc(wt * 4));
+  wgrad_partial_ = static_cast<float*>(alloc(wp * 4));
+  HG_CUDA(cudaStreamSynchronize(st_));
+}
+
+std::uint64_t Engine::param_count() const {
+  std::uint64_t n = 0;
+  for (const auto& s : slots_) n += static_cast<std::uint64_t>(s.din) * s.dout;
+  return n;
+}
+
+// ---------------------------------------------------------------------------------------------
+void Engine::timed(const char* name, double bytes, const std::function<void()>& f) {
+  if (!profiling_) {
+    f();
+    return;
+  }
+  cudaEvent_t a, b;
+  HG_CUDA(cudaEventCreate(&a));
+  HG_CUDA(cudaEventCreate(&b));
+  HG_CUDA(cudaEventRecord(a, st_));
+  f();
+  HG_CUDA(cudaEventRecord(b, st_));
+  HG_CUDA(cudaEventSynchronize(b));
+  float ms = 0.f;
+  HG_CUDA(cudaEventElapsedTime(&ms, a, b));
+  kernel_ms_[name] += ms;
+  kernel_bytes_[name] += bytes;
+  kernel_launches_[name] += 1;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+}
+
+void Engine::run_sampling() {
+  const int k = o_.k;
+  // frontier[0][target] = sorted unique batch (bitmap), with multiplicities
+  FrontierArgs f0{};
+  f0.ntypes = 1;
+  f0.t[0] = {bits_ + word_base_[target_], word_base_[target_ + 1] - word_base_[target_], wscan_ + word_base_[target_],
+             front(0, target_).list, front(0, target_).count, front(0, target_).cap};
+  HG_CUDA(cudaMemsetAsync(bits_, 0, static_cast<std::size_t>(total_words_) * 4, st_));
+  HG_CUDA(cudaMemsetAsync(mult_, 0, static_cast<std::size_t>(o_.batch_cap) * 4, st_));
+  timed("frontier", 0, [&] {
+    frontier_mark_batch(d_batch_, d_sc_, o_.batch_cap, f0.t[0], st_);
+    frontier_compact(f0, words_dev_, scan_partials_, st_);
+    batch_multiplicity(d_batch_, d_sc_, o_.batch_cap, f0.t[0], mult_, st_);
+  });
+  const std::uint32_t* hop1_rows = front(0, target_).list;
+  const int* hop1_n = front(0, target_).count;
+  if (replica_) {
+    k_shard_rows<<<4, 256, 0, st_>>>(front(0, target_).list, front(0, target_).count, shard_index_, shard_count_,
+                                     shard_list_, shard_count_dev_);
+    hop1_rows = shard_list_;
+    hop1_n = shard_count_dev_;
+  }
+
+  for (int h = 1; h <= k; ++h) {
+    SampleHop sh{};
+    sh.fanout = o_.fanouts[h - 1];
+    sh.hop = h;
+    for (int bi : hop_blocks_[h]) {
+      BlockBuf& b = blocks_[bi];
+      SampleBlock& s = sh.b[sh.nblk++];
+      s.csr_ptr = csr_ptr_[b.rel];
+      s.csr_src = csr_src_[b.rel];
+      s.dst_list = h == 1 ? hop1_rows : front(h - 1, b.dst_t).list;
+      s.n_rows = h == 1 ? hop1_n : front(h - 1, b.dst_t).count;
+      s.indptr = b.indptr;
+      s.src_ids = b.src;
+      s.erow = b.erow;
+      s.rel = b.rel;
+      s.rows_cap = b.rows_cap;
+    }
+    ScanArgs sa{};
+    for (int q = 0; q < sh.nblk; ++q) sa.s[sa.nseg++] = {sh.b[q].indptr + 1, sh.b[q].n_rows, sh.b[q].rows_cap};
+    timed("sample", 0, [&] {
+      sample_count(sh, st_);
+      scan_inclusive(sa, scan_partials_, st_);
+      sample_draw(sh, d_sc_, slow_, n_slow_, mt_scratch_, st_);
+    });
+
+    // frontier[h][t]: bitmap of every sampled source, compacted in id order
+    FrontierArgs fa{};
+    std::vector<int> slot_of_type(ntypes_, -1);
+    for (int t : hop_slot_types_[h]) {
+      slot_of_type[t] = fa.ntypes;
+      fa.t[fa.ntypes++] = {bits_ + word_base_[t], word_base_[t + 1] - word_base_[t], wscan_ + word_base_[t],
+                           front(h, t).list, front(h, t).count, front(h, t).cap};
+    }
+    MarkArgs ma{};
+    RelabelArgs ra{};
+    for (int q = 0; q < sh.nblk; ++q) {
+      const BlockBuf& b = blocks_[hop_blocks_[h][q]];
+      ma.s[ma.nsrc++] = {b.src, b.indptr, sh.b[q].n_rows, b.edge_cap, slot_of_type[b.src_t]};
+      ra.b[ra.nblk++] = {b.src, b.indptr, sh.b[q].n_rows, b.col, b.edge_cap, slot_of_type[b.src_t]};
+    }
+    HG_CUDA(cudaMemsetAsync(bits_, 0, static_cast<std::size_t>(total_words_) * 4, st_));
+    timed("frontier", 0, [&] {
+      frontier_mark(ma, fa, st_);
+      frontier_compact(fa, words_dev_ + h * kMaxSegs, scan_partials_, st_);
+      frontier_relabel(ra, fa, st_);
+    });
+  }
+  EdgeCountArgs ec{};
+  for (const auto& b : blocks_) {
+    ec.indptr[ec.n] = b.indptr;
+    ec.n_rows[ec.n] = b.hop == 1 ? hop1_n : front(b.hop - 1, b.dst_t).count;
+    ++ec.n;
+  }
+  k_count_edges<<<1, 32, 0, st_>>>(ec, edges_dev_);
+  // cache lookups + updates over the layer-0 frontier (harness.cpp:425-437)
+  if (cache_on_)
+    for (int t = 0; t < ntypes_; ++t)
+      if (cache_types_[t] && front(k, t).cap > 0)
+        cache_count(front(k, t).list, front(k, t).count, front(k, t).cap, cached_bits_ + word_base_[t],
+                    cache_hm_ + 2 * t, st_);
+}
+
+void Engine::run_forward() {
+  const int k = o_.k;
+  // AGG_all buffer: rows beyond the live batch and the counter row stay zero
+  HG_CUDA(cudaMemsetAsync(logits_, 0, static_cast<std::size_t>(o_.batch_cap + 1) * ldc_ * 4, st_));
+  for (const auto& gr : groups_) {
+    AggGroup ag{};
+    ag.nrel = static_cast<int>(gr.blocks.size());
+    const bool top = gr.layer == k;
+    ag.n_rows = (top && replica_) ? shard_count_dev_ : front(gr.depth - 1, gr.type).count;
+    ag.rows_cap = top && replica_ ? static_cast<int>(ceil_div(o_.batch_cap, shard_count_)) : gr.rows_cap;
+    ag.out = gr.out;
+    ag.ld_out = gr.ld;
+    ag.dout = gr.dout;
+    ag.relu = gr.layer < k ? 1 : 0;
+    ag.out_stride = top ? shard_count_ : 1;
+    ag.out_offset = top ? shard_index_ : 0;
+    double bytes = 0;
+    for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
+      const BlockBuf& b = blocks_[gr.blocks[q]];
+      const Slot& s = slots_[gr.slots[q]];
+      AggRel& r = ag.r[q];
+      r.indptr = b.indptr;
+      r.src = b.src;
+      r.col = b.col;
+      if (b.hop == k) {
+        r.h = tables_[b.src_t].w;
+        r.ld_h = tables_[b.src_t].ld;
+        r.by_id = 1;
+      } else {
+        const Group* sg = nullptr;
+        for (const auto& g2 : groups_)
+          if (g2.depth - 1 == b.hop && g2.type == b.src_t) sg = &g2;
+        r.h = sg->out;
+        r.ld_h = sg->ld;
+        r.by_id = 0;
+      }
+      r.din = b.din;
+      r.w = s.w;
+      r.ld_w = s.ld;
+      r.mean = b.mean;
+      r.ld_mean = b.ld_mean;
+    }
+    if (gr.blocks.empty() && !top) {
+      // no relation into this type at this depth: zero embedding
+      zero_rows(gr.out, gr.ld, front(gr.depth - 1, gr.type).count, gr.rows_cap, st_);
+      continue;
+    }
+    timed(top ? "aggregate_top" : "aggregate", bytes, [&] { aggregate_project(ag, st_); });
+  }
+  // AGG_all: sum the partial logits of every partition (raf.cpp:427-446)
+  if (o_.p > 1) {
+    EdgeCountArgs ec{};
+    for (int bi : hop_blocks_[1]) {
+      ec.indptr[ec.n] = blocks_[bi].indptr;
+      ++ec.n;
+    }
+    k_active_rows<<<1, 256, 0, st_>>>(ec, replica_ ? shard_count_dev_ : front(0, target_).count,
+                                      logits_ + static_cast<std::size_t>(o_.batch_cap) * ldc_ + o_.rank);
+#ifdef HG_WITH_NCCL
+    if (comm_) {
+      timed("agg_all", static_cast<double>(o_.batch_cap + 1) * ldc_ * 4, [&] {
+        if (ncclAllReduce(logits_, logits_, static_cast<std::size_t>(o_.batch_cap + 1) * ldc_, ncclFloat, ncclSum,
+                          comm_, st_) != ncclSuccess)
+          throw std::runtime_error("ncclAllReduce failed");
+      });
+    }
+#endif
+  }
+}
+
+void Engine::run_loss() {
+  LossArgs la{};
+  la.logits = logits_;
+  la.ld = ldc_;
+  la.C = num_classes_;
+  la.n_rows = front(0, target_).count;
+  la.rows_cap = o_.batch_cap;
+  la.row_ids = front(0, target_).list;
+  la.mult = mult_;
+  la.labels = labels_;
+  la.sc = d_sc_;
+  la.dlogits = dlogits_;
+  la.row_loss = row_loss_;
+  la.loss_out = loss_;
+  la.err = err_;
+  timed("loss", 0, [&] { cross_entropy(la, st_); });
+}
+
+void Engine::run_backward() {
+  const int k = o_.k;
+  // transposed views of the blocks whose sources need gradients
+  for (auto& c : cscs_) {
+    CscArgs a{};
+    for (int bi : c.blocks) {
+      const BlockBuf& b = blocks_[bi];
+      a.b[a.nblk++] = {b.col, b.erow, b.indptr, b.hop == 1 ? (replica_ ? shard_count_dev_ : front(0, target_).count)
+                                                              : front(b.hop - 1, b.dst_t).count,
+                       b.edge_cap, b.edge_base, b.dmean, b.ld_mean};
+    }
+    a.n_src = front(c.hop, c.src_t).count;
+    a.src_cap = c.src_cap;
+    a.offs = c.offs;
+    a.cursor = c.cursor;
+    a.entries = c.entries;
+    a.dh = c.dh;
+    a.ld_dh = c.ld;
+    a.din = c.din;
+    timed("csc_build", 0, [&] { csc_build(a, scan_partials_, st_); });
+  }
+  for (auto& s : slots_) HG_CUDA(cudaMemsetAsync(s.g, 0, static_cast<std::size_t>(std::max(1, s.din)) * s.ld * 4, st_));
+
+  for (int l = k; l >= 1; --l) {
+    const int d = k - l + 1;
+    for (const auto& gr : groups_) {
+      if (gr.layer != l || gr.blocks.empty()) continue;
+      const bool top = l == k;
+      const int* n_rows = (top && replica_) ? shard_count_dev_ : front(d - 1, gr.type).count;
+      const int rows_cap = top && replica_ ? static_cast<int>(ceil_div(o_.batch_cap, shard_count_)) : gr.rows_cap;
+      const int stride = top ? shard_count_ : 1, offset = top ? shard_index_ : 0;
+      if (!top) timed("relu_mask", 0, [&] { relu_mask(gr.dout_buf, gr.out, gr.ld, gr.dout, n_rows, rows_cap, 1, 0, st_); });
+      for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
+        BlockBuf& b = blocks_[gr.blocks[q]];
+        Slot& s = slots_[gr.slots[q]];
+        WGradArgs wa{b.mean, b.ld_mean, b.din, gr.dout_buf, gr.ld, gr.dout, stride, offset, n_rows, rows_cap,
+                     wgrad_partial_, s.g, s.ld};
+        timed("weight_grad", 0, [&] { weight_grad(wa, st_); });
+        if (b.need_src_grad) {
+          DMeanArgs da{gr.dout_buf, gr.ld, gr.dout, stride, offset, s.w, s.ld, b.din, b.indptr, n_rows, rows_cap,
+                       b.dmean, b.ld_mean};
+          timed("mean_grad", 0, [&] { mean_grad(da, wt_scratch_, st_); });
+        }
+      }
+    }
+    // scatter back to the sources of this hop, as ordered gathers
+    for (auto& c : cscs_) {
+      if (c.hop != d) continue;
+      CscArgs a{};
+      for (int bi : c.blocks) {
+        const BlockBuf& b = blocks_[bi];
+        a.b[a.nblk++] = {b.col, b.erow, b.indptr, nullptr, b.edge_cap, b.edge_base, b.dmean, b.ld_mean};
+      }
+      a.n_src = front(c.hop, c.src_t).count;
+      a.src_cap = c.src_cap;
+      a.offs = c.offs;
+      a.entries = c.entries;
+      a.dh = c.dh;
+      a.ld_dh = c.ld;
+      a.din = c.din;
+      timed("csc_gather", 0, [&] { csc_gather(a, st_); });
+    }
+  }
+}
+
+void Engine::run_update() {
+  AdamHyper hp;
+  timed("adam", 0, [&] {
+    for (auto& s : slots_)
+      adam_dense(s.w, s.m, s.v, s.g, s.din, s.dout, s.ld, &d_sc_->model_step, hp, err_, st_);
+    for (const auto& c : cscs_) {
+      if (c.hop != o_.k) continue;
+      TypeTable& tb = tables_[c.src_t];
+      if (!tb.learnable) continue;
+      const Front& f = front(o_.k, c.src_t);
+      adam_rows(tb.w, tb.m, tb.v, tb.ld, tb.dim, f.list, c.dh, c.ld, f.count, f.cap, tb.step, hp, err_, st_);
+    }
+  });
+}
+
+void Engine::enqueue_step(std::uint64_t rng_seed, int n, int designated, bool train) {
+  if (n > o_.batch_cap) throw std::invalid_argument("batch larger than the engine's batch capacity");
+  if (n <= 0) throw std::invalid_argument("empty batch");
+  if (train) ++model_step_;
+  h_sc_->rng_seed = rng_seed;
+  h_sc_->batch_len = n;
+  h_sc_->designated = designated;
+  h_sc_->model_step = model_step_;
+  HG_CUDA(cudaMemcpyAsync(d_sc_, h_sc_, sizeof(StepScalars), cudaMemcpyHostToDevice, st_));
+  HG_CUDA(cudaMemsetAsync(err_, 0, sizeof(std::uint32_t), st_));
+  run_sampling();
+  run_forward();
+  run_loss();
+  if (train) {
+    run_backward();
+    run_update();
+  }
+  HG_CUDA(cudaMemcpyAsync(h_rb_, loss_, sizeof(Readback), cudaMemcpyDeviceToHost, st_));
+}
+
+StepReport Engine::finish_step() {
+  HG_CUDA(cudaStreamSynchronize(st_));
+  HG_CUDA(cudaGetLastError());
+  StepReport r;
+  r.loss = h_rb_->loss;
+  r.err = h_rb_->err;
+  r.sampled_edges = h_rb_->edges;
+  if (r.err & 1u) throw std::invalid_argument("fanout above the sampler's supported map size");
+  if (r.err & 2u) throw std::invalid_argument("label out of range in batch");
+  if (r.err & 4u) throw std::runtime_error("non-finite gradient");
+  if (o_.p > 1) {
+    std::vector<float> row(ldc_);
+    HG_CUDA(cudaMemcpy(row.data(), logits_ + static_cast<std::size_t>(o_.batch_cap) * ldc_, ldc_ * 4,
+                       cudaMemcpyDeviceToHost));
+    for (int q = 0; q < o_.p; ++q) r.active_rows.push_back(static_cast<int>(row[q]));
+  }
+  return r;
+}
+
+StepReport Engine::step(const NodeId* batch, int n, std::uint64_t rng_seed, int designated, bool train) {
+  if (n > o_.batch_cap) throw std::invalid_argument("batch larger than the engine's batch capacity");
+  for (int i = 0; i < n; ++i)
+    if (batch[i] >= type_counts_[target_])
+      throw std::invalid_argument("seed node id out of range: " + std::to_string(batch[i]));
+  std::memcpy(h_batch_, batch, sizeof(NodeId) * n);
+  HG_CUDA(cudaMemcpyAsync(d_batch_, h_batch_, sizeof(NodeId) * n, cudaMemcpyHostToDevice, st_));
+  enqueue_step(rng_seed, n, designated, train);
+  return finish_step();
+}
+
+void Engine::sample_only(const NodeId* batch, int n, std::uint64_t rng_seed) {
+  if (n > o_.batch_cap) throw std::invalid_argument("batch larger than the engine's batch capacity");
+  if (n <= 0) throw std::invalid_argument("empty batch");
+  for (int i = 0; i < n; ++i)
+    if (batch[i] >= type_counts_[target_])
+      throw std::invalid_argument("seed node id out of range: " + std::to_string(batch[i]));
+  std::memcpy(h_batch_, batch, sizeof(NodeId) * n);
+  HG_CUDA(cudaMemcpyAsync(d_batch_, h_batch_, sizeof(NodeId) * n, cudaMemcpyHostToDevice, st_));
+  h_sc_->rng_seed = rng_seed;
+  h_sc_->batch_len = n;
+  HG_CUDA(cudaMemcpyAsync(d_sc_, h_sc_, sizeof(StepScalars), cudaMemcpyHostToDevice, st_));
+  run_sampling();
+  HG_CUDA(cudaStreamSynchronize(st_));
+  HG_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------------------------
+std::vector<std::vector<std::uint32_t>> Engine::presample_hotness(int epochs, std::uint64_t seed, int batch_size) {
+  if (batch_size > o_.batch_cap) throw std::invalid_argument("presample batch larger than the batch capacity");
+  std::vector<std::uint32_t*> counts(ntypes_, nullptr);
+  for (int t = 0; t < ntypes_; ++t) counts[t] = static_cast<std::uint32_t*>(alloc(type_counts_[t] * 4));
+  const std::uint64_t n_target = type_counts_[target_];
+  std::vector<NodeId> batch;
+  for (int e = 0; e < epochs; ++e) {
+    const std::uint64_t rs = mix_seed(seed, static_cast<std::uint64_t>(e));
+    for (std::uint64_t lo = 0; lo < n_target; lo += batch_size) {
+      batch.clear();
+      for (std::uint64_t v = lo; v < std::min<std::uint64_t>(lo + batch_size, n_target); ++v)
+        batch.push_back(static_cast<NodeId>(v));
+      std::memcpy(h_batch_, batch.data(), batch.size() * 4);
+      HG_CUDA(cudaMemcpyAsync(d_batch_, h_batch_, batch.size() * 4, cudaMemcpyHostToDevice, st_));
+      h_sc_->rng_seed = rs;
+      h_sc_->batch_len = static_cast<int>(batch.size());
+      HG_CUDA(cudaMemcpyAsync(d_sc_, h_sc_, sizeof(StepScalars), cudaMemcpyHostToDevice, st_));
+      run_sampling();
+      // +1 per seed, +1 per sampled source occurrence (cache.cpp:51-56)
+      hotness_add_list(front(0, target_).list, front(0, target_).count, o_.batch_cap, counts[target_], st_);
+      for (const auto& b : blocks_)
+        hotness_add(b.src, b.indptr, b.hop == 1 ? front(0, target_).count : front(b.hop - 1, b.dst_t).count,
+                    b.edge_cap, counts[b.src_t], st_);
+      // pinned staging buffers are reused: wait before the next batch
+      HG_CUDA(cudaStreamSynchronize(st_));
+    }
+  }
+  std::vector<std::vector<std::uint32_t>> out(ntypes_);
+  for (int t = 0; t < ntypes_; ++t) {
+    out[t].resize(type_counts_[t]);
+    if (!out[t].empty())
+      HG_CUDA(cudaMemcpy(out[t].data(), counts[t], out[t].size() * 4, cudaMemcpyDeviceToHost));
+  }
+  return out;
+}
+
+void Engine::set_cache(const std::vector<std::vector<NodeId>>& cached) {
+  std::vector<std::uint32_t> bits(static_cast<std::size_t>(total_words_), 0u);
+  for (int t = 0; t < ntypes_ && t < static_cast<int>(cached.size()); ++t)
+    for (NodeId v : cached[t]) bits[word_base_[t] + (v >> 5)] |= 1u << (v & 31);
+  HG_CUDA(cudaMemcpy(cached_bits_, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice));
+  HG_CUDA(cudaMemset(cache_hm_, 0, sizeof(unsigned long long) * 2 * ntypes_));
+  cache_on_ = true;
+  for (int t = 0; t < ntypes_; ++t) cache_types_[t] = t < static_cast<int>(cached.size());
+}
+
+std::vector<std::pair<unsigned long long, unsigned long long>> Engine::cache_counters() {
+  std::vector<unsigned long long> v(2 * ntypes_);
+  HG_CUDA(cudaStreamSynchronize(st_));
+  HG_CUDA(cudaMemcpy(v.data(), cache_hm_, v.size() * 8, cudaMemcpyDeviceToHost));
+  std::vector<std::pair<unsigned long long, unsigned long long>> out;
+  for (int t = 0; t < ntypes_; ++t) out.emplace_back(v[2 * t], v[2 * t + 1]);
+  return out;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Named tensors (mirror oracle/ref_shim.cpp bundle names):
+//   frontier{h}.t{t}, hop{h}.rel{r}.{dst_ids,indptr,src_ids,col}, H{d}.t{t},
+//   mean.l{l}.r{r}.t{t}, logits, dlogits, loss, grad.w.r{r}.l{l},
+//   grad.f.t{t}.ids, grad.f.t{t}.rows, post.r{r}.l{l}, post.learn.t{t},
+//   post.learn_m.t{t}, post.learn_v.t{t}, post.learn_step.t{t}, sampled_edges
+std::vector<std::string> Engine::tensor_names() const {
+  std::vector<std::string> n;
+  const int k = o_.k;
+  for (int h = 0; h <= k; ++h)
+    for (int t = 0; t < ntypes_; ++t)
+      if (fronts_[h * ntypes_ + t].cap > 0) n.push_back("frontier" + std::to_string(h) + ".t" + std::to_string(t));
+  for (const auto& b : blocks_) {
+    const std::string p = "hop" + std::to_string(b.hop) + ".rel" + std::to_string(b.rel);
+    for (const char* s : {".dst_ids", ".indptr", ".src_ids", ".col"}) n.push_back(p + s);
+  }
+  for (const auto& gr : groups_) {
+    if (gr.layer < k) n.push_back("H" + std::to_string(gr.depth - 1) + ".t" + std::to_string(gr.type));
+    for (std::size_t q = 0; q < gr.blocks.size(); ++q)
+      n.push_back("mean.l" + std::to_string(gr.layer) + ".r" + std::to_string(blocks_[gr.blocks[q]].rel) + ".t" +
+                  std::to_string(gr.type));
+  }
+  for (int t = 0; t < ntypes_; ++t)
+    if (tables_[t].w) n.push_back("H" + std::to_string(k) + ".t" + std::to_string(t));
+  for (const char* s : {"logits", "dlogits", "loss", "sampled_edges"}) n.push_back(s);
+  for (const auto& s : slots_) {
+    const std::string key = "r" + std::to_string(s.rel) + ".l" + std::to_string(s.layer);
+    n.push_back("grad.w." + key);
+    n.push_back("post." + key);
+  }
+  for (const auto& c : cscs_)
+    if (c.hop == k) {
+      n.push_back("grad.f.t" + std::to_string(c.src_t) + ".ids");
+      n.push_back("grad.f.t" + std::to_string(c.src_t) + ".rows");
+    }
+  for (int t = 0; t < ntypes_; ++t)
+    if (tables_[t].learnable)
+      for (const char* s : {"post.learn.t", "post.learn_m.t", "post.learn_v.t", "post.learn_step.t"})
+        n.push_back(s + std::to_string(t));
+  return n;
+}
+
+bool Engine::read_tensor(const std::string& name, std::string& dtype, std::vector<long long>& shape,
+                         std::vector<char>& data) {
+  HG_CUDA(cudaStreamSynchronize(st_));
+  const int k = o_.k;
+  auto dev_int = [&](const int* p) {
+    int v = 0;
+    HG_CUDA(cudaMemcpy(&v, p, sizeof(int), cudaMemcpyDeviceToHost));
+    return v;
+  };
+  auto u32s = [&](const std::uint32_t* p, std::size_t n) {
+    std::vector<std::uint32_t> v(n);
+    if (n) HG_CUDA(cudaMemcpy(v.data(), p, n * 4, cudaMemcpyDeviceToHost));
+    dtype = "<u4";
+    shape = {static_cast<long long>(n)};
+    put(data, v);
+    return true;
+  };
+  // rows x cols of an ld-strided fp32 matrix, widened to f64 like the oracle
+  auto mat = [&](const float* p, std::size_t rows, int cols, int ld, std::size_t row_stride = 1,
+                 std::size_t row_offset = 0) {
+    std::vector<float> raw;
+    std::vector<double> v(rows * cols);
+    if (rows) {
+      const std::size_t span = ((rows - 1) * row_stride + row_offset + 1) * ld;
+      raw.resize(span);
+      HG_CUDA(cudaMemcpy(raw.data(), p, span * 4, cudaMemcpyDeviceToHost));
+      for (std::size_t i = 0; i < rows; ++i)
+        for (int c = 0; c < cols; ++c) v[i * cols + c] = raw[(i * row_stride + row_offset) * ld + c];
+    }
+    dtype = "<f8";
+    shape = {static_cast<long long>(rows), cols};
+    put(data, v);
+    return true;
+  };
+  auto n_rows_of_block = [&](const BlockBuf& b) {
+    if (b.hop == 1 && replica_) return dev_int(shard_count_dev_);
+    return dev_int(front(b.hop - 1, b.dst_t).count);
+  };
+  for (int h = 0; h <= k; ++h)
+    for (int t = 0; t < ntypes_; ++t)
+      if (name == "frontier" + std::to_string(h) + ".t" + std::to_string(t)) {
+        const Front& f = fronts_[h * ntypes_ + t];
+        return u32s(f.list, f.cap > 0 ? dev_int(f.count) : 0);
+      }
+  for (const auto& b : blocks_) {
+    const std::string p = "hop" + std::to_string(b.hop) + ".rel" + std::to_string(b.rel);
+    if (name.rfind(p + ".", 0) != 0) continue;
+    const int n = n_rows_of_block(b);
+    std::uint32_t total = 0;
+    HG_CUDA(cudaMemcpy(&total, b.indptr + n, 4, cudaMemcpyDeviceToHost));
+    if (name == p + ".dst_ids")
+      return u32s(b.hop == 1 ? (replica_ ? shard_list_ : front(0, target_).list) : front(b.hop - 1, b.dst_t).list, n);
+    if (name == p + ".indptr") return u32s(b.indptr, n + 1);
+    if (name == p + ".src_ids") return u32s(b.src, total);
+    if (name == p + ".col") return u32s(b.col, total);
+  }
+  for (const auto& gr : groups_) {
+    const int n = dev_int(front(gr.depth - 1, gr.type).count);
+    if (gr.layer < k && name == "H" + std::to_string(gr.depth - 1) + ".t" + std::to_string(gr.type))
+      return mat(gr.out, n, gr.dout, gr.ld);
+    for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
+      const BlockBuf& b = blocks_[gr.blocks[q]];
+      if (name == "mean.l" + std::to_string(gr.layer) + ".r" + std::to_string(b.rel) + ".t" + std::to_string(gr.type))
+        return mat(b.mean, n_rows_of_block(b), b.din, b.ld_mean);
+    }
+  }
+  for (int t = 0; t < ntypes_; ++t)
+    if (tables_[t].w && name == "H" + std::to_string(k) + ".t" + std::to_string(t)) {
+      const Front& f = front(k, t);
+      const int n = dev_int(f.count);
+      float* tmp = nullptr;
+      HG_CUDA(cudaMalloc(&tmp, std::max<std::size_t>(16, static_cast<std::size_t>(n) * tables_[t].dim * 4)));
+      if (n) k_gather_rows<<<64, 256, 0, st_>>>(tables_[t].w, tables_[t].ld, f.list, f.count, tables_[t].dim, tmp);
+      HG_CUDA(cudaStreamSynchronize(st_));
+      mat(tmp, n, tables_[t].dim, tables_[t].dim);
+      cudaFree(tmp);
+      return true;
+    }
+  const int n0 = dev_int(front(0, target_).count);
+  if (name == "logits") return mat(logits_, n0, num_classes_, ldc_);
+  if (name == "dlogits") return mat(dlogits_, n0, num_classes_, ldc_);
+  if (name == "loss" || name == "sampled_edges") {
+    Readback rb;
+    HG_CUDA(cudaMemcpy(&rb, loss_, sizeof(rb), cudaMemcpyDeviceToHost));
+    if (name == "loss") {
+      dtype = "<f8";
+      put(data, std::vector<double>{rb.loss});
+    } else {
+      dtype = "<u8";
+      put(data, std::vector<std::uint64_t>{rb.edges});
+    }
+    shape = {1};
+    return true;
+  }
+  for (const auto& s : slots_) {
+    const std::string key = "r" + std::to_string(s.rel) + ".l" + std::to_string(s.layer);
+    if (name == "grad.w." + key) return mat(s.g, s.din, s.dout, s.ld);
+    if (name == "post." + key) return mat(s.w, s.din, s.dout, s.ld);
+  }
+  for (const auto& c : cscs_) {
+    if (c.hop != k) continue;
+    const std::string p = "grad.f.t" + std::to_string(c.src_t);
+    const Front& f = front(k, c.src_t);
+    if (name == p + ".ids") return u32s(f.list, dev_int(f.count));
+    if (name == p + ".rows") return mat(c.dh, dev_int(f.count), c.din, c.ld);
+  }
+  for (int t = 0; t < ntypes_; ++t) {
+    const TypeTable& tb = tables_[t];
+    if (!tb.learnable) continue;
+    const std::string ts = std::to_string(t);
+    if (name == "post.learn.t" + ts) return mat(tb.w, type_counts_[t], tb.dim, tb.ld);
+    if (name == "post.learn_m.t" + ts) return mat(tb.m, type_counts_[t], tb.dim, tb.ld);
+    if (name == "post.learn_v.t" + ts) return mat(tb.v, type_counts_[t], tb.dim, tb.ld);
+    if (name == "post.learn_step.t" + ts) {
+      std::int64_t s = 0;
+      HG_CUDA(cudaMemcpy(&s, tb.step, 8, cudaMemcpyDeviceToHost));
+      dtype = "<i8";
+      shape = {1};
+      put(data, std::vector<std::int64_t>{s});
+      return true;
+    }
+  }
+  return false;
+}
+
+}  // namespace hetgpu

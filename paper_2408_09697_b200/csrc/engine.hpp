@@ -1,0 +1,245 @@
+// Device engine for the mini-batch hot path of one meta-partition (one GPU).
+//
+// It replaces, for the relations and node types this partition owns, the
+// reference's per-batch pipeline run_raf_batch (raf.cpp:344-530):
+//   sample_khop_restricted (sampling.cpp:41-103)  -> sample_count/sample_draw + bitmap frontier
+//   layer-0 gather + mean_aggregate + matmul + agg_all (hgnn.cpp:215-279, raf.cpp:167-248)
+//                                                 -> aggregate_project (fused, gather by id)
+//   AGG_all across partitions (raf.cpp:427-446)   -> ncclAllReduce of the [B x C] partial logits
+//   cross_entropy (hgnn.cpp:281-307)              -> cross_entropy
+//   backward (hgnn.cpp:309-362, raf.cpp:250-304) -> weight_grad / mean_grad / csc gather
+//   adam_update_model / adam_update_rows          -> adam_dense / adam_rows
+// Every live size stays on the device; a step is one stream of launches.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <functional>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "host.hpp"
+#include "kernels.cuh"
+
+#ifdef HG_WITH_NCCL
+#include <nccl.h>
+#endif
+
+namespace hetgpu {
+
+struct EngineOptions {
+  int k = 2;
+  std::vector<int> fanouts{25, 20};
+  int hidden = 64;
+  int batch_cap = 1024;
+  int p = 1;      // meta-partition count
+  int rank = 0;   // which partition this engine evaluates
+  std::uint64_t model_seed = 0;  // init_model seed
+  std::uint64_t learn_seed = 0;  // init_learnable seed
+  int device = 0;
+  int elem_bytes = 4;  // byte accounting of partial messages (AccountingModel)
+};
+
+// Host-visible outputs of one step (one small D2H copy).
+struct StepReport {
+  double loss = 0.0;
+  std::uint64_t sampled_edges = 0;   // Block::src_ids entries, all hops (this partition)
+  std::uint32_t err = 0;
+  std::vector<int> active_rows;      // per rank: batch rows with >= 1 sampled top edge
+};
+
+struct DeviceBuffer {
+  void* ptr = nullptr;
+  std::size_t bytes = 0;
+};
+
+class Engine {
+ public:
+  Engine(const Graph& g, const EngineOptions& o);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+#ifdef HG_WITH_NCCL
+  void attach_comm(ncclComm_t comm) { comm_ = comm; }
+#endif
+
+  // Full training step: sample, forward, AGG_all, loss, backward, Adam.
+  // `batch` is host memory (copied to the device inside the call).
+  StepReport step(const NodeId* batch, int n, std::uint64_t rng_seed, int designated, bool train = true);
+  // Same as step() but the batch is already on the device (benchmark inner loop).
+  void enqueue_step(std::uint64_t rng_seed, int n, int designated, bool train);
+  StepReport finish_step();
+  // Sampling only (parity of the sampler; presample_hotness).
+  void sample_only(const NodeId* batch, int n, std::uint64_t rng_seed);
+
+  // Read any named tensor (see engine.cu: tensor names mirror the oracle's).
+  // Returns false if the name is unknown.
+  bool read_tensor(const std::string& name, std::string& dtype, std::vector<long long>& shape,
+                   std::vector<char>& data);
+  std::vector<std::string> tensor_names() const;
+
+  // cache: hotness presample over `epochs` id-ordered passes (cache.cpp:39-63)
+  std::vector<std::vector<std::uint32_t>> presample_hotness(int epochs, std::uint64_t seed, int batch_size);
+  // mark the cached ids per type (sorted lists from fill_and_serve); lookups
+  // then run on every step for the layer-0 frontier (harness.cpp:425-437)
+  void set_cache(const std::vector<std::vector<NodeId>>& cached);
+  std::vector<std::pair<unsigned long long, unsigned long long>> cache_counters();
+
+  // per-kernel-class device time accumulated with events (profiling on)
+  void set_profiling(bool on) { profiling_ = on; }
+  std::map<std::string, double> kernel_ms() const { return kernel_ms_; }
+  std::map<std::string, double> kernel_bytes() const { return kernel_bytes_; }
+  void reset_profile() {
+    kernel_ms_.clear();
+    kernel_bytes_.clear();
+    kernel_launches_.clear();
+  }
+  std::map<std::string, int> kernel_launches() const { return kernel_launches_; }
+  int launches_per_step() const { return launches_per_step_; }
+
+  cudaStream_t stream() const { return st_; }
+  std::uint32_t* device_batch() { return d_batch_; }
+  std::uint64_t param_count() const;
+  std::uint64_t device_bytes() const { return total_bytes_; }
+
+  // static description (for CommStats / tests)
+  const Tree& local_tree() const { return tree_; }
+  const std::vector<std::vector<int>>& hop_rels() const { return hop_rels_; }
+  int model_step() const { return static_cast<int>(model_step_); }
+
+ private:
+  struct BlockBuf {
+    int rel = -1, hop = 0, src_t = -1, dst_t = -1;
+    int rows_cap = 0, edge_cap = 0, edge_base = 0;
+    std::uint32_t *indptr = nullptr, *src = nullptr, *erow = nullptr, *col = nullptr;
+    float* mean = nullptr;   // tape: rows_cap x ld_mean (only for blocks feeding a layer)
+    float* dmean = nullptr;  // rows_cap x ld_mean (only if the source needs a gradient)
+    int din = 0, ld_mean = 0;
+    bool need_src_grad = false;
+  };
+  struct Front {
+    std::uint32_t* list = nullptr;
+    int* count = nullptr;  // device
+    int cap = 0;
+  };
+  struct Slot {
+    int rel = -1, layer = 0, din = 0, dout = 0, ld = 0;
+    float *w = nullptr, *m = nullptr, *v = nullptr, *g = nullptr;
+  };
+  struct Group {  // one output type of one layer
+    int layer = 0, depth = 0, type = -1, dout = 0, ld = 0, rows_cap = 0;
+    std::vector<int> blocks;  // indices into blocks_
+    std::vector<int> slots;   // matching slot indices
+    float* out = nullptr;     // H[depth-1][type] (logits for layer k)
+    float* dout_buf = nullptr;  // dH for it
+  };
+  struct CscBuf {
+    int hop = 0, src_t = -1, src_cap = 0, din = 0, ld = 0;
+    std::vector<int> blocks;
+    std::uint32_t *offs = nullptr, *cursor = nullptr, *entries = nullptr;
+    float* dh = nullptr;  // gradient of H[hop][src_t] (or learnable rows)
+  };
+  struct TypeTable {
+    int dim = 0, ld = 0;
+    bool learnable = false, dense = false;
+    float *w = nullptr, *m = nullptr, *v = nullptr;
+    std::int64_t* step = nullptr;  // device
+    std::int64_t host_step = 0;
+  };
+
+  void* alloc(std::size_t bytes);
+  void build_plan(const Graph& g);
+  void upload(const Graph& g);
+  void run_sampling();
+  void run_forward();
+  void run_loss();
+  void run_backward();
+  void run_update();
+  void timed(const char* name, double bytes, const std::function<void()>& f);
+  Front& front(int h, int t) { return fronts_[h * ntypes_ + t]; }
+  int out_dim(int layer) const { return layer == o_.k ? num_classes_ : o_.hidden; }
+
+  EngineOptions o_;
+  Tree tree_;
+  std::vector<std::vector<int>> hop_rels_;
+  int ntypes_ = 0, target_ = 0, num_classes_ = 0;
+  std::vector<std::uint64_t> type_counts_;
+  std::vector<int> rel_src_, rel_dst_;
+  bool replica_ = false;
+  int shard_index_ = 0, shard_count_ = 1;
+
+  cudaStream_t st_ = nullptr;
+  std::vector<void*> allocs_;
+  std::size_t total_bytes_ = 0;
+
+  // graph on device
+  std::vector<std::uint64_t*> csr_ptr_;
+  std::vector<std::uint32_t*> csr_src_;
+  std::vector<std::uint64_t> maxdeg_;
+  std::vector<TypeTable> tables_;
+  std::int32_t* labels_ = nullptr;
+
+  // frontier machinery
+  std::vector<Front> fronts_;       // [(k+1) x ntypes]
+  std::vector<int> word_base_;      // per type, offset in words
+  std::uint32_t *bits_ = nullptr, *wscan_ = nullptr, *cached_bits_ = nullptr;
+  int total_words_ = 0;
+  int* words_dev_ = nullptr;        // per hop, per frontier slot: word counts (device)
+  std::vector<std::vector<int>> hop_slot_types_;  // per hop: types in slot order
+  std::uint32_t* shard_list_ = nullptr;
+  int* shard_count_dev_ = nullptr;
+
+  std::vector<BlockBuf> blocks_;
+  std::vector<std::vector<int>> hop_blocks_;  // per hop: block indices
+  std::vector<Group> groups_;                 // ordered by layer
+  std::vector<Slot> slots_;
+  std::map<SlotId, int> slot_of_;
+  std::vector<CscBuf> cscs_;
+
+  // per-step state
+  StepScalars* d_sc_ = nullptr;
+  StepScalars* h_sc_ = nullptr;      // pinned
+  std::uint32_t* d_batch_ = nullptr;
+  std::uint32_t* h_batch_ = nullptr;  // pinned
+  float* mult_ = nullptr;
+  float* logits_ = nullptr;   // [batch_cap + 1 rows x ldC] (+1: partition counters)
+  float* dlogits_ = nullptr;
+  int ldc_ = 0;
+  double* row_loss_ = nullptr;
+  double* loss_ = nullptr;
+  std::uint32_t* err_ = nullptr;
+  std::int64_t* model_step_dev_ = nullptr;
+  std::int64_t model_step_ = 0;
+  struct Readback {
+    double loss;
+    std::uint32_t err;
+    std::uint32_t pad;
+    std::uint64_t edges;
+  };
+  Readback* h_rb_ = nullptr;  // pinned
+  std::uint64_t* edges_dev_ = nullptr;
+  unsigned long long* cache_hm_ = nullptr;  // [ntypes x 2]
+
+  // scratch
+  std::uint32_t* scan_partials_ = nullptr;
+  std::uint32_t* slow_ = nullptr;
+  int* n_slow_ = nullptr;
+  std::uint64_t* mt_scratch_ = nullptr;
+  float* wt_scratch_ = nullptr;
+  float* wgrad_partial_ = nullptr;
+
+  bool cache_on_ = false;
+  std::vector<bool> cache_types_;
+  bool profiling_ = false;
+  std::map<std::string, double> kernel_ms_, kernel_bytes_;
+  std::map<std::string, int> kernel_launches_;
+  int launches_per_step_ = 0;
+#ifdef HG_WITH_NCCL
+  ncclComm_t comm_ = nullptr;
+#endif
+};
+
+}  // namespace hetgpu

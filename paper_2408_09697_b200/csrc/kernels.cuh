@@ -1,0 +1,255 @@
+// Kernel interfaces of the mini-batch hot path (sm_100a). All sizes that
+// depend on the sampled data live in device memory: kernels are launched with
+// grids sized from host-known capacities and read their live counts on the
+// device, so a whole training step is one stream of launches with no host
+// round trip (and capturable into a CUDA graph).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace hetgpu {
+
+constexpr int kMaxBlocks = 16;  // sampled blocks per hop (relations)
+constexpr int kMaxSegs = 16;
+constexpr int kMaxRelsPerGroup = 16;
+
+// Per-step scalars written by one small H2D copy (the only per-batch upload
+// besides the batch ids).
+struct StepScalars {
+  std::uint64_t rng_seed;
+  int batch_len;       // |batch| including duplicates
+  int designated;
+  std::int64_t model_step;  // Adam step after this batch's increment
+};
+
+// ---- segmented inclusive scan of u32 (in place) --------------------------------
+struct ScanSeg {
+  std::uint32_t* data;
+  const int* n;  // live length (device)
+  int cap;       // capacity (host)
+};
+struct ScanArgs {
+  ScanSeg s[kMaxSegs];
+  int nseg;
+};
+constexpr int kScanTile = 4096;
+// partial scratch: nseg * ceil(max cap / kScanTile) u32
+void scan_inclusive(const ScanArgs& a, std::uint32_t* partials, cudaStream_t st);
+
+// ---- sampling ---------------------------------------------------------------------
+struct SampleBlock {
+  const std::uint64_t* csr_ptr;  // relation CSR (dst-major), full graph
+  const std::uint32_t* csr_src;
+  const std::uint32_t* dst_list;  // frontier[h-1][rel.dst]
+  const int* n_rows;              // its live size
+  std::uint32_t* indptr;          // [rows_cap + 1] block offsets (u32)
+  std::uint32_t* src_ids;         // [edge_cap] sampled sources in draw order
+  std::uint32_t* erow;            // [edge_cap] block row of every sampled edge
+  int rel;
+  int rows_cap;
+};
+struct SampleHop {
+  SampleBlock b[kMaxBlocks];
+  int nblk;
+  int fanout;
+  int hop;
+};
+// counts[i] = min(fanout, deg) into indptr[i+1]; indptr[0] = 0
+void sample_count(const SampleHop& h, cudaStream_t st);
+// draws (exact mt19937_64 + Lemire + partial Fisher-Yates). Rows whose draw
+// overflows the streaming engine go to `slow` ((block,row) pairs, capacity =
+// total rows) and are replayed with the full-state engine on `scratch`
+// (sample_scratch_words(fanout) u64).
+std::size_t sample_scratch_words(int fanout);
+void sample_draw(const SampleHop& h, const StepScalars* sc, std::uint32_t* slow, int* n_slow,
+                 std::uint64_t* scratch, cudaStream_t st);
+
+// ---- frontier: bitmap set -> sorted unique ids + rank -----------------------------
+struct BitmapType {
+  std::uint32_t* bits;   // words of this type's id space
+  int words;
+  std::uint32_t* wscan;  // inclusive scan of per-word popcounts
+  std::uint32_t* list;   // out: sorted unique ids
+  int* count;            // out: live size
+  int cap;
+};
+struct FrontierArgs {
+  BitmapType t[kMaxSegs];
+  int ntypes;
+};
+struct MarkSource {
+  const std::uint32_t* ids;
+  const std::uint32_t* indptr;  // live total = indptr[*n_rows]
+  const int* n_rows;
+  int cap;
+  int slot;  // index into FrontierArgs::t
+};
+struct MarkArgs {
+  MarkSource s[kMaxBlocks];
+  int nsrc;
+};
+void frontier_mark(const MarkArgs& m, const FrontierArgs& f, cudaStream_t st);
+void frontier_mark_batch(const std::uint32_t* ids, const StepScalars* sc, int cap, const BitmapType& t,
+                         cudaStream_t st);
+void frontier_compact(const FrontierArgs& f, const int* words_dev, std::uint32_t* partials,
+                      cudaStream_t st);
+struct RelabelBlock {
+  const std::uint32_t* ids;
+  const std::uint32_t* indptr;
+  const int* n_rows;
+  std::uint32_t* col;
+  int cap;
+  int slot;
+};
+struct RelabelArgs {
+  RelabelBlock b[kMaxBlocks];
+  int nblk;
+};
+void frontier_relabel(const RelabelArgs& r, const FrontierArgs& f, cudaStream_t st);
+// multiplicity of every unique batch row (duplicates in the batch)
+void batch_multiplicity(const std::uint32_t* ids, const StepScalars* sc, int cap, const BitmapType& t,
+                        float* mult, cudaStream_t st);
+
+// ---- dense: relation-first aggregation + projection -------------------------------
+struct AggRel {
+  const std::uint32_t* indptr;  // block offsets
+  const std::uint32_t* src;     // sampled global src ids (layer 1: gather by id)
+  const std::uint32_t* col;     // src rows in frontier[d][src_t] (inner layers)
+  const float* h;               // source rows: feature table (by id) or H[d][src_t] (by col)
+  int ld_h;
+  int by_id;
+  int din;
+  const float* w;               // [din x dout], ld = ld_w
+  int ld_w;
+  float* mean;                  // tape [rows x din], ld = ld_mean
+  int ld_mean;
+};
+struct AggGroup {
+  AggRel r[kMaxRelsPerGroup];
+  int nrel;
+  const int* n_rows;
+  int rows_cap;
+  float* out;
+  int ld_out;
+  int dout;
+  int relu;
+  // optional row remap of the output (replica shards write into full-batch rows)
+  int out_stride;
+  int out_offset;
+};
+void aggregate_project(const AggGroup& g, cudaStream_t st);
+
+// ---- loss ------------------------------------------------------------------------
+struct LossArgs {
+  const float* logits;
+  int ld;
+  int C;
+  const int* n_rows;
+  int rows_cap;
+  const std::uint32_t* row_ids;  // frontier[0][target]
+  const float* mult;
+  const std::int32_t* labels;
+  const StepScalars* sc;
+  float* dlogits;
+  double* row_loss;   // scratch [rows_cap]
+  double* loss_out;   // [1]
+  std::uint32_t* err;
+};
+void cross_entropy(const LossArgs& a, cudaStream_t st);
+
+// ---- backward ----------------------------------------------------------------------
+// dpre = dH * [H > 0] (in place on dH)
+void relu_mask(float* dh, const float* h, int ld, int cols, const int* n_rows, int rows_cap,
+               int in_stride, int in_offset, cudaStream_t st);
+// dW += mean^T . dpre over the live rows (deterministic two-level reduction)
+struct WGradArgs {
+  const float* mean;
+  int ld_mean;
+  int din;
+  const float* dpre;
+  int ld_dpre;
+  int dout;
+  int dpre_stride;  // dpre row = i*stride + offset (replica shards)
+  int dpre_offset;
+  const int* n_rows;
+  int rows_cap;
+  float* partial;   // scratch [chunks x din x dout]
+  float* dw;        // [din x dout], ld = ld_dw (accumulated)
+  int ld_dw;
+};
+void weight_grad(const WGradArgs& a, cudaStream_t st);
+// dmean = (dpre . W^T) / deg(row)
+struct DMeanArgs {
+  const float* dpre;
+  int ld_dpre;
+  int dout;
+  int dpre_stride;
+  int dpre_offset;
+  const float* w;
+  int ld_w;
+  int din;
+  const std::uint32_t* indptr;
+  const int* n_rows;
+  int rows_cap;
+  float* dmean;
+  int ld_dmean;
+};
+// wt_scratch: >= round_up4(din) * dout floats (W^T)
+void mean_grad(const DMeanArgs& a, float* wt_scratch, cudaStream_t st);
+
+// transposed (src-major) view of a hop's blocks for one source type, used to
+// turn the backward scatter into an ordered gather (deterministic).
+struct CscBlock {
+  const std::uint32_t* col;
+  const std::uint32_t* erow;
+  const std::uint32_t* indptr;
+  const int* n_rows;
+  int cap;
+  int edge_base;  // static offset of this block in the hop's edge id space
+  const float* dmean;
+  int ld_dmean;
+};
+struct CscArgs {
+  CscBlock b[kMaxBlocks];
+  int nblk;
+  const int* n_src;      // live size of frontier[d][src_t]
+  int src_cap;
+  std::uint32_t* offs;   // [src_cap + 1]
+  std::uint32_t* cursor; // [src_cap]
+  std::uint32_t* entries;// [sum of caps]
+  float* dh;             // out [src rows x din]
+  int ld_dh;
+  int din;
+};
+void csc_build(const CscArgs& a, std::uint32_t* partials, cudaStream_t st);
+void csc_gather(const CscArgs& a, cudaStream_t st);
+
+// ---- optimizer ------------------------------------------------------------------------
+struct AdamHyper {  // hgnn.hpp:16-21
+  double lr = 1e-2, beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
+};
+// dense slot update; step counter in device memory (already incremented)
+void adam_dense(float* w, float* m, float* v, const float* g, int rows, int cols, int ld,
+                const std::int64_t* step, AdamHyper hp, std::uint32_t* err, cudaStream_t st);
+// sparse rows: ids = frontier[k][t], grads aligned with them; step_t advanced
+// on the device iff the frontier is non-empty
+void adam_rows(float* w, float* m, float* v, int ld, int cols, const std::uint32_t* ids,
+               const float* g, int ld_g, const int* n_rows, int rows_cap, std::int64_t* step,
+               AdamHyper hp, std::uint32_t* err, cudaStream_t st);
+
+// ---- misc --------------------------------------------------------------------------------
+void zero_rows(float* p, int ld, const int* n_rows, int rows_cap, cudaStream_t st);
+// cache lookups: hits of frontier ids against a cached-id bitmap, accumulated
+void cache_count(const std::uint32_t* ids, const int* n, int cap, const std::uint32_t* cached_bits,
+                 unsigned long long* hits_misses, cudaStream_t st);
+// histogram for presample_hotness
+void hotness_add(const std::uint32_t* ids, const std::uint32_t* indptr, const int* n_rows, int cap,
+                 std::uint32_t* counts, cudaStream_t st);
+void hotness_add_list(const std::uint32_t* ids, const int* n, int cap, std::uint32_t* counts,
+                      cudaStream_t st);
+
+}  // namespace hetgpu

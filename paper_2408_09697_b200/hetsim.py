@@ -1,0 +1,305 @@
+"""Python mirror of the reference's interface for the mini-batch hot path.
+
+Same names, argument meaning and error behaviour as the reference's C++ API
+(/root/reference/proj/include/hetsim/*.hpp), so the parity tests read like the
+reference's own tests. Everything runs through the C-ABI in include/hetgpu.h;
+the heavy lifting is C++ (host) and sm_100a CUDA (device). ValueError mirrors
+std::invalid_argument, HetGpuError mirrors std::runtime_error.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+from ._native import HetGpuError  # noqa: F401  (re-export)
+
+# ---- bundled synthetic specs (harness.cpp:192-247) and the benchmark shapes --------------
+
+
+def bundled_spec(name: str) -> dict:
+    """bundled_spec (src/harness.cpp:192-247)."""
+    if name == "mag-mini":
+        return dict(name=name, target="paper", num_classes=8, label_noise=0.1,
+                    node_types=[dict(name="paper", count=8000, dim=128, storage="dense"),
+                                dict(name="author", count=6000, dim=64, storage="learnable"),
+                                dict(name="institution", count=500, dim=64, storage="learnable"),
+                                dict(name="field", count=1000, dim=64, storage="learnable")],
+                    relations=[dict(src="author", edge="writes", dst="paper", edges=30000, degree="powerlaw", alpha=1.6),
+                               dict(src="author", edge="affiliated", dst="institution", edges=6000),
+                               dict(src="paper", edge="cites", dst="paper", edges=40000, degree="powerlaw", alpha=1.8),
+                               dict(src="paper", edge="has_topic", dst="field", edges=24000)],
+                    self_paired=["cites"])
+    if name == "freebase-mini":
+        return dict(name=name, target="book", num_classes=8, label_noise=0.05,
+                    node_types=[dict(name="book", count=5000, dim=32, storage="learnable"),
+                                dict(name="film", count=4000, dim=32, storage="learnable"),
+                                dict(name="music", count=8000, dim=32, storage="learnable"),
+                                dict(name="people", count=6000, dim=32, storage="learnable")],
+                    relations=[dict(src="people", edge="authored", dst="book", edges=20000, degree="powerlaw", alpha=1.7),
+                               dict(src="film", edge="adapted", dst="book", edges=8000),
+                               dict(src="music", edge="scored", dst="film", edges=10000),
+                               dict(src="people", edge="liked", dst="music", edges=15000, degree="powerlaw", alpha=2.0)])
+    if name == "donor-mini":
+        return dict(name=name, target="project", num_classes=2, label_noise=0.05,
+                    node_types=[dict(name="project", count=2000, dim=789, storage="dense"),
+                                dict(name="donation", count=3000, dim=17, storage="dense"),
+                                dict(name="donor", count=3000, dim=7, storage="dense")],
+                    relations=[dict(src="donor", edge="gave", dst="project", edges=8000, degree="powerlaw", alpha=2.0),
+                               dict(src="donor", edge="made", dst="donation", edges=6000),
+                               dict(src="donation", edge="to_project", dst="project", edges=6000)])
+    if name == "igb-mini":
+        return dict(name=name, target="paper", num_classes=16, label_noise=0.1,
+                    node_types=[dict(name="paper", count=10000, dim=128, storage="dense"),
+                                dict(name="author", count=8000, dim=128, storage="dense"),
+                                dict(name="institute", count=400, dim=128, storage="dense"),
+                                dict(name="fos", count=700, dim=128, storage="dense")],
+                    relations=[dict(src="author", edge="written", dst="paper", edges=30000, degree="powerlaw", alpha=1.6),
+                               dict(src="author", edge="affiliated", dst="institute", edges=8000),
+                               dict(src="paper", edge="cites", dst="paper", edges=30000, degree="powerlaw", alpha=1.8),
+                               dict(src="paper", edge="topic", dst="fos", edges=20000)],
+                    self_paired=["cites"])
+    raise ValueError("unknown bundled spec: " + name)
+
+
+def bundled_spec_names() -> List[str]:
+    return ["mag-mini", "freebase-mini", "donor-mini", "igb-mini"]
+
+
+def toy_spec() -> dict:
+    """BASELINE.json configs[0] / SURVEY §8(d) C1: 4 types x 128-d, 5 uniform relations."""
+    return dict(name="toy", target="paper", num_classes=8, label_noise=0.0, add_reverse=False,
+                node_types=[dict(name="paper", count=40000, dim=128, storage="dense"),
+                            dict(name="author", count=35000, dim=128, storage="dense"),
+                            dict(name="institution", count=5000, dim=128, storage="dense"),
+                            dict(name="field", count=20000, dim=128, storage="dense")],
+                relations=[dict(src="author", edge="writes", dst="paper", edges=400000),
+                           dict(src="paper", edge="rev_writes", dst="author", edges=400000),
+                           dict(src="institution", edge="affiliated", dst="author", edges=35000),
+                           dict(src="paper", edge="cites", dst="paper", edges=400000),
+                           dict(src="field", edge="topic", dst="paper", edges=300000)])
+
+
+def ogbn_mag_spec() -> dict:
+    """BASELINE.json configs[1] / SURVEY §8(d) C2: ogbn-mag shape, uniform degrees."""
+    return dict(name="ogbn-mag-shape", target="paper", num_classes=349, label_noise=0.1,
+                node_types=[dict(name="paper", count=736389, dim=128, storage="dense"),
+                            dict(name="author", count=1134649, dim=64, storage="learnable"),
+                            dict(name="institution", count=8740, dim=64, storage="learnable"),
+                            dict(name="field", count=59965, dim=64, storage="learnable")],
+                relations=[dict(src="author", edge="writes", dst="paper", edges=7145660),
+                           dict(src="author", edge="affiliated", dst="institution", edges=1043998),
+                           dict(src="paper", edge="cites", dst="paper", edges=5416271),
+                           dict(src="paper", edge="has_topic", dst="field", edges=7505078)],
+                self_paired=["cites"])
+
+
+def mix_seed(a: int, b: int) -> int:
+    """mix_seed (src/sampling.cpp:9-15)."""
+    return int(N.lib().hg_mix_seed(a, b))
+
+
+# ---- graphs --------------------------------------------------------------------------------
+
+
+class HetGraph:
+    """Host graph owned by the native layer (hetgraph.hpp:58-74)."""
+
+    def __init__(self, handle):
+        self._h = handle if handle else N.raise_last()
+
+    def __del__(self):
+        if getattr(self, "_h", None) and N._lib is not None:
+            N._lib.hg_graph_free(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def export(self) -> Dict[str, np.ndarray]:
+        return N.take(N.lib().hg_graph_export(self._h))
+
+
+def gen_synthetic(spec: dict, seed: int) -> HetGraph:
+    """gen_synthetic (src/harness.cpp:74-186): bit-exact graph, features and labels."""
+    keep = []
+
+    def cs(s):
+        b = s.encode()
+        keep.append(b)
+        return b
+
+    for t in spec["node_types"]:
+        if t.get("storage", "dense") not in ("dense", "learnable"):
+            raise ValueError("unknown storage kind: " + t["storage"])
+    for r in spec["relations"]:
+        if r.get("degree", "uniform") not in ("uniform", "powerlaw"):
+            raise ValueError("unknown degree distribution: " + r["degree"])
+    types = (N.SpecNodeType * max(1, len(spec["node_types"])))()
+    for i, t in enumerate(spec["node_types"]):
+        types[i] = N.SpecNodeType(cs(t["name"]), int(t["count"]), int(t["dim"]),
+                                  1 if t.get("storage", "dense") == "dense" else 2)
+    rels = (N.SpecRelation * max(1, len(spec["relations"])))()
+    for i, r in enumerate(spec["relations"]):
+        rels[i] = N.SpecRelation(cs(r["src"]), cs(r["edge"]), cs(r["dst"]), int(r["edges"]),
+                                 1 if r.get("degree", "uniform") == "powerlaw" else 0, float(r.get("alpha", 2.0)))
+    sp = spec.get("self_paired", [])
+    sp_arr = (C.c_char_p * max(1, len(sp)))(*[cs(x) for x in sp])
+    s = N.Spec(cs(spec["target"]), int(spec["num_classes"]), float(spec.get("label_noise", 0.0)),
+               len(spec["node_types"]), types, len(spec["relations"]), rels, int(spec.get("add_reverse", True)),
+               len(sp), sp_arr)
+    return HetGraph(N.lib().hg_graph_generate(C.byref(s), seed))
+
+
+def graph_from_export(e: Dict[str, np.ndarray]) -> HetGraph:
+    """A HetGraph from exported arrays (the oracle's or ours): CSR per relation."""
+    counts = np.asarray(e["node_counts"], np.uint64)
+    nt = len(counts)
+    rs = np.asarray(e["rel_src"], np.int32)
+    rd = np.asarray(e["rel_dst"], np.int32)
+    rr = np.asarray(e.get("rel_reverse", np.zeros(len(rs))), np.int32)
+    ip = np.concatenate([np.asarray(e[f"rel{r}.indptr"], np.uint64) for r in range(len(rs))] or [np.zeros(1, np.uint64)])
+    sr = np.concatenate([np.asarray(e[f"rel{r}.src"], np.uint32) for r in range(len(rs))] or [np.zeros(1, np.uint32)])
+    if sr.size == 0:
+        sr = np.zeros(1, np.uint32)
+    kinds = np.asarray(e["kinds"], np.int32)
+    dims = np.asarray(e["dims"], np.int32)
+    dense = [np.asarray(e[f"feat.t{t}"], np.float32).ravel() for t in range(nt) if kinds[t] == 1]
+    dense = np.concatenate(dense) if dense else np.zeros(1, np.float32)
+    labels = np.asarray(e["labels"], np.int32)
+    return HetGraph(N.lib().hg_graph_from_csr(nt, N.ptr(counts), len(rs), N.ptr(rs), N.ptr(rd), N.ptr(rr),
+                                              N.ptr(ip), N.ptr(sr), N.ptr(kinds), N.ptr(dims), N.ptr(dense),
+                                              int(np.asarray(e["target"]).ravel()[0]),
+                                              int(np.asarray(e["num_classes"]).ravel()[0]), N.ptr(labels)))
+
+
+def build_hetgraph(counts: Sequence[int], relations: Sequence[tuple], edges: Sequence[Sequence[tuple]],
+                   target: int, num_classes: int) -> HetGraph:
+    """build_hetgraph (src/hetgraph.cpp:126-156); relations = [(src_type, dst_type)]."""
+    cnt = np.asarray(counts, np.uint64)
+    rs = np.asarray([r[0] for r in relations], np.int32)
+    rd = np.asarray([r[1] for r in relations], np.int32)
+    pc = np.asarray([len(e) for e in edges], np.uint64)
+    ps = np.asarray([p[0] for e in edges for p in e] or [0], np.uint32)
+    pd = np.asarray([p[1] for e in edges for p in e] or [0], np.uint32)
+    return HetGraph(N.lib().hg_graph_from_pairs(len(cnt), N.ptr(cnt), len(rs), N.ptr(rs), N.ptr(rd), N.ptr(pc),
+                                                N.ptr(ps), N.ptr(pd), target, num_classes))
+
+
+def meta_partition(g: HetGraph, k: int, p: int) -> Dict[str, np.ndarray]:
+    """meta_partition + cacheable_types + hop_relation_sets (metapartition.cpp:283, cache.cpp:143)."""
+    return N.take(N.lib().hg_meta_partition(g.handle, k, p))
+
+
+def make_batches(g: HetGraph, batch_size: int, max_batches: int, seed: int) -> List[np.ndarray]:
+    """make_batches (src/harness.cpp:327-340)."""
+    b = N.take(N.lib().hg_make_batches(g.handle, batch_size, max_batches, seed))
+    return [b[f"batch{i}"] for i in range(len(b))]
+
+
+def cache_plan(g: HetGraph, hot: Dict[str, np.ndarray], n_types: int, budget: int, read_ns=1.0, write_ns=1.0,
+               overhead_ns=1000.0, elem_bytes=4) -> Dict[str, np.ndarray]:
+    """profile_miss_penalty + allocate_cache + fill_and_serve (src/cache.cpp:11-141)."""
+    counts = np.concatenate([np.asarray(hot[f"hot.t{t}"], np.uint32) for t in range(n_types)])
+    return N.take(N.lib().hg_cache_plan(g.handle, N.ptr(counts), budget, read_ns, write_ns, overhead_ns, elem_bytes))
+
+
+# ---- device engine ---------------------------------------------------------------------------
+
+
+class Engine:
+    """One meta-partition of the RAF engine on one GPU (run_raf_batch, raf.cpp:344-530)."""
+
+    def __init__(self, g: HetGraph, fanouts: Sequence[int], hidden: int = 64, batch_cap: int = 1024, p: int = 1,
+                 rank: int = 0, model_seed: int = 0, learn_seed: int = 0, device: int = 0):
+        fo = (C.c_int * len(fanouts))(*[int(f) for f in fanouts])
+        self._fo = fo
+        opts = N.EngineOpts(len(fanouts), fo, hidden, batch_cap, p, rank, model_seed, learn_seed, device)
+        self.k = len(fanouts)
+        self.graph = g  # keep alive
+        self._h = N.lib().hg_engine_create(g.handle, C.byref(opts))
+        if not self._h:
+            N.raise_last()
+
+    @classmethod
+    def for_experiment(cls, g: HetGraph, fanouts, hidden, seed, **kw) -> "Engine":
+        """Seeds as run_experiment derives them (harness.cpp:365-366)."""
+        return cls(g, fanouts, hidden, model_seed=mix_seed(seed, 0xD0DE1), learn_seed=mix_seed(seed, 0x1EA4A), **kw)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and N._lib is not None:
+            N._lib.hg_engine_free(self._h)
+            self._h = None
+
+    def step(self, batch, rng_seed: int, designated: int = 0, train: bool = True) -> dict:
+        b = np.ascontiguousarray(batch, dtype=np.uint32)
+        rep = N.StepReport()
+        N.check(N.lib().hg_engine_step(self._h, N.ptr(b), len(b), rng_seed, designated, int(train), C.byref(rep)))
+        return dict(loss=rep.loss, sampled_edges=int(rep.sampled_edges),
+                    active_rows=[rep.active_rows[i] for i in range(rep.n_active)])
+
+    def sample(self, seeds, rng_seed: int) -> None:
+        b = np.ascontiguousarray(seeds, dtype=np.uint32)
+        if b.size == 0:
+            raise ValueError("empty batch")
+        N.check(N.lib().hg_engine_sample(self._h, N.ptr(b), len(b), rng_seed))
+
+    def read(self, *names: str) -> Dict[str, np.ndarray]:
+        return N.take(N.lib().hg_engine_read(self._h, ",".join(names).encode() if names else None))
+
+    def bench(self, batches: Sequence[np.ndarray], seeds: Sequence[int], train: bool = True):
+        flat = np.ascontiguousarray(np.concatenate(batches), dtype=np.uint32)
+        lens = np.asarray([len(b) for b in batches], np.int32)
+        sd = np.asarray(seeds, np.uint64)
+        ms, edges, loss = C.c_double(), C.c_uint64(), C.c_double()
+        N.check(N.lib().hg_engine_bench(self._h, N.ptr(flat), N.ptr(lens), N.ptr(sd), len(batches), int(train),
+                                        C.byref(ms), C.byref(edges), C.byref(loss)))
+        return ms.value, int(edges.value), loss.value
+
+    def profile(self, on: bool = True):
+        N.lib().hg_engine_profile(self._h, int(on))
+
+    def profile_read(self) -> Dict[str, np.ndarray]:
+        return N.take(N.lib().hg_engine_profile_read(self._h))
+
+    def info(self) -> dict:
+        pc, db, ms = C.c_uint64(), C.c_uint64(), C.c_int()
+        N.check(N.lib().hg_engine_info(self._h, C.byref(pc), C.byref(db), C.byref(ms)))
+        return dict(param_count=pc.value, device_bytes=db.value, model_step=ms.value)
+
+    def presample_hotness(self, epochs: int, seed: int, batch_size: int = 512) -> Dict[str, np.ndarray]:
+        return N.take(N.lib().hg_engine_presample_hotness(self._h, epochs, seed, batch_size))
+
+    def set_cache(self, cached: Sequence[np.ndarray]):
+        ids = np.concatenate([np.asarray(c, np.uint32) for c in cached] or [np.zeros(0, np.uint32)])
+        if ids.size == 0:
+            ids = np.zeros(1, np.uint32)
+        lens = np.asarray([len(c) for c in cached], np.uint64)
+        N.check(N.lib().hg_engine_set_cache(self._h, N.ptr(ids), N.ptr(lens), len(cached)))
+
+    def cache_counters(self) -> Dict[str, np.ndarray]:
+        return N.take(N.lib().hg_engine_cache_counters(self._h))
+
+    def attach_nccl(self, unique_id: bytes, nranks: int, rank: int):
+        buf = C.create_string_buffer(unique_id, len(unique_id))
+        N.check(N.lib().hg_engine_attach_nccl(self._h, buf, len(unique_id), nranks, rank))
+
+    # ---- reference-named views --------------------------------------------------------
+    def sample_khop_restricted(self, seeds, rng_seed: int) -> Dict[str, np.ndarray]:
+        """sample_khop_restricted (sampling.cpp:99-103) with this engine's hop relation sets."""
+        self.sample(seeds, rng_seed)
+        names = [n for n in self.tensor_names() if n.startswith(("frontier", "hop"))]
+        return self.read(*names)
+
+    def tensor_names(self) -> List[str]:
+        raw = N.take(N.lib().hg_engine_read(self._h, b"?"))["names"]
+        return [x for x in bytes(raw.astype(np.uint8)).decode().split(",") if x]
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(256)
+    n = N.check(N.lib().hg_nccl_unique_id(buf, 256))
+    return buf.raw[:n]

@@ -1,0 +1,73 @@
+"""Shared helpers for the parity tests (product vs oracle)."""
+from __future__ import annotations
+
+import numpy as np
+
+
+def rel_err(ours: np.ndarray, ref: np.ndarray, floor: float = 1e-6) -> float:
+    """max|ours - ref| / max(max|ref|, floor): the per-tensor relative error the
+    north_star's "within 1e-3 relative" is measured with."""
+    ours = np.asarray(ours, np.float64)
+    ref = np.asarray(ref, np.float64)
+    assert ours.shape == ref.shape, (ours.shape, ref.shape)
+    if ref.size == 0:
+        return 0.0
+    return float(np.max(np.abs(ours - ref)) / max(float(np.max(np.abs(ref))), floor))
+
+
+def assert_close(ours, ref, tol=1e-3, what=""):
+    e = rel_err(ours, ref)
+    assert e <= tol, f"{what}: relative error {e:.3e} > {tol:.1e}"
+
+
+def assert_adam_close(w_ours, w_ref, w_before, lr=1e-2, tol=1e-3, max_flip_frac=2e-3, what=""):
+    """Post-Adam parameters. Adam's first steps move each element by ~lr*sign(g);
+    elements whose gradient is at fp32 rounding level may flip sign, so those
+    (at most `max_flip_frac` of the tensor) may differ by up to 2*lr per step."""
+    w_ours = np.asarray(w_ours, np.float64)
+    w_ref = np.asarray(w_ref, np.float64)
+    d = np.abs(w_ours - w_ref)
+    scale = max(float(np.max(np.abs(w_ref))), 1e-6)
+    bad = d > tol * scale
+    frac = float(bad.mean()) if bad.size else 0.0
+    assert frac <= max_flip_frac, f"{what}: {bad.sum()} of {bad.size} elements differ (max {d.max():.3e})"
+    if bad.any():
+        assert float(d[bad].max()) <= 2 * lr * 1.01 * 8, f"{what}: a flip larger than Adam's step bound"
+
+
+def csr_from_pairs(n_dst, pairs):
+    """dst-major CSR keeping insertion order (hetgraph.cpp:126-156)."""
+    indptr = np.zeros(n_dst + 1, np.uint64)
+    for _, d in pairs:
+        indptr[d + 1] += 1
+    indptr = np.cumsum(indptr).astype(np.uint64)
+    fill = indptr[:-1].copy()
+    src = np.zeros(len(pairs), np.uint32)
+    for s, d in pairs:
+        src[fill[d]] = s
+        fill[d] += 1
+    return indptr, src
+
+
+def single_relation_graph(H, deg_list, n_src=None, dim=4, seed=0):
+    """Target type 0 with len(deg_list) nodes; relation 0 from type 1 into it with
+    the given in-degrees (sources 0..deg-1 in order, shifted per row)."""
+    n_dst = len(deg_list)
+    n_src = n_src or max(1, max(deg_list))
+    pairs = []
+    for d, deg in enumerate(deg_list):
+        for j in range(deg):
+            pairs.append(((j + d) % n_src, d))
+    indptr, src = csr_from_pairs(n_dst, pairs)
+    rng = np.random.default_rng(seed)
+    e = {
+        "node_counts": np.array([n_dst, n_src], np.uint64),
+        "rel_src": np.array([1], np.int32), "rel_dst": np.array([0], np.int32),
+        "rel_reverse": np.array([0], np.int32),
+        "rel0.indptr": indptr, "rel0.src": src,
+        "kinds": np.array([1, 1], np.int32), "dims": np.array([dim, dim], np.int32),
+        "feat.t0": rng.uniform(-1, 1, (n_dst, dim)).astype(np.float32),
+        "feat.t1": rng.uniform(-1, 1, (n_src, dim)).astype(np.float32),
+        "labels": np.zeros(n_dst, np.int32), "target": np.array([0]), "num_classes": np.array([2]),
+    }
+    return e
