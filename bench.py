@@ -1,0 +1,313 @@
+"""Benchmark of the Heta mini-batch hot path on B200 (BASELINE.json metric:
+RGCN epoch time & sampled-edges/s, ogbn-mag shape).
+
+Workload (configs[1]): ogbn-mag-shaped synthetic HetG (736,389 paper / 1,134,649
+author / 8,740 institution / 59,965 field; 36.8M edges with reverses; uniform
+degrees), 2-layer RGCN hidden 64, fanout [25, 20], batch 1024 per GPU,
+meta-partitioned over N GPUs (p = N) with the AGG_all exchange over NCCL.
+A step = one training batch: sample -> gather/aggregate/project -> AGG_all ->
+loss -> backward -> Adam (model + learnable rows).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Under torchrun (N > 1) every rank runs one partition; rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+SEED = 1
+FANOUTS = [25, 20]
+HIDDEN = 64
+BATCH_PER_GPU = 1024
+EPOCH_BATCHES = 720  # ceil(736,389 / 1024): one epoch of the target type at N=1
+METRIC = "sampled-edges/s (2-layer RGCN training, ogbn-mag shape)"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """SM clocks + throttle reasons polled through NVML every ~2 ms during the
+    timed region (nvidia-smi's 100 ms floor is longer than a short region)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.stop = threading.Event()
+        self.thread = None
+        self.max_mhz = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def poll():
+                while not self.stop.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.rows.append((sm, rs))
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.thread = None
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        if self.thread:
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({name for _, rs in self.rows for name, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------------------------
+def cpu_baseline_sample(n_threads, n_batches, graph_ref=None):
+    """The reference (oracle/_ref, compiled from /root/reference) on the host's
+    cores: `n_threads` concurrent run_raf_batch calls on distinct C2 batches.
+    Returns (edges/s, sample description, seconds)."""
+    from oracle import ref as R
+    from paper_2408_09697_b200 import hetsim as H
+    g = graph_ref or R.RefGraph.from_spec(H.ogbn_mag_spec(), SEED)
+    r = g.bench_raf(2, HIDDEN, 1, SEED, BATCH_PER_GPU, FANOUTS, 0, n_batches, n_threads)
+    secs = float(r["seconds"][0])
+    edges = int(r["edges"].sum())
+    return edges / secs, f"{n_batches} run_raf_batch calls (batch 1024, p=1) on {n_threads} threads", secs, g
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU implementation of the path
+    (oracle/_ref) on this box's host cores, same metric/config/unit."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import ref as R
+    if not R.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libhetsim_ref.so not built"}))
+        return
+    threads = os.cpu_count() or 1
+    g = None
+    for _ in range(args.warmup_ref):
+        _, _, _, g = cpu_baseline_sample(threads, threads, g)
+    vals, secs = [], []
+    edges_total, time_total = 0.0, 0.0
+    for _ in range(args.steps):
+        v, sample, s, g = cpu_baseline_sample(threads, threads, g)
+        vals.append(v)
+        secs.append(s)
+        edges_total += v * s
+        time_total += s
+    value = edges_total / time_total
+    ms_per_batch = 1000.0 * time_total / (threads * args.steps)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup_ref, "ms_per_step": 1000.0 * time_total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C2 ogbn-mag-shape RGCN-2 hidden 64 fanout [25,20] batch 1024 (p=1 on CPU)",
+                   "batch_per_step": threads, "graph_seed": SEED},
+        "epoch_time_s": EPOCH_BATCHES * ms_per_batch / 1000.0 / threads,
+        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": threads, "kind": "reference",
+                         "sample": f"{threads} concurrent run_raf_batch calls per step"},
+        "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------------
+def run_b200(args):
+    import torch
+    from paper_2408_09697_b200 import hetsim as H
+
+    world, rank, local = dist_env()
+    n = world
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    batch = BATCH_PER_GPU * n
+
+    t0 = time.time()
+    g = H.gen_synthetic(H.ogbn_mag_spec(), SEED)
+    t_gen = time.time() - t0
+    eng = H.Engine.for_experiment(g, FANOUTS, HIDDEN, SEED, batch_cap=batch, p=n, rank=rank, device=local)
+    if world > 1:
+        import torch.distributed as dist
+        uid = [H.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        eng.attach_nccl(uid[0], world, rank)
+    total_steps = args.warmup + args.steps
+    need = 2 * total_steps + 2
+    batches = H.make_batches(g, batch, 0, H.mix_seed(SEED, 0xBA7C))
+    while len(batches) < need:
+        batches += batches
+    seeds = [H.mix_seed(SEED, 0xB000 + i) for i in range(need)]
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def reduce(x, op):
+        if world == 1:
+            return x
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=op)
+        return float(t.item())
+
+    import torch.distributed as tdist
+    MAX = tdist.ReduceOp.MAX if world > 1 else None
+    SUM = tdist.ReduceOp.SUM if world > 1 else None
+
+    launches = eng.count_launches(len(batches[0]), True)
+    # warm-up (also JIT-free: everything is precompiled sm_100a)
+    eng.bench(batches[:args.warmup], seeds[:args.warmup], train=True)
+
+    # ---- device-resident timed region: K steps back to back (CUDA-graph replay)
+    sl = slice(args.warmup, args.warmup + args.steps)
+    barrier()
+    with ClockSampler(local) as clk:
+        ms, _, loss = eng.bench(batches[sl], seeds[sl], train=True)
+    barrier()
+    # ---- profiled pass over the same batches: every kernel class bracketed by
+    # CUDA events on the engine's stream (eager launches, no graph)
+    eng.profile(True)
+    prof_steps = min(args.steps, 50)
+    psl = slice(args.warmup, args.warmup + prof_steps)
+    eng.bench(batches[psl], seeds[psl], train=True)
+    prof = eng.profile_read()
+    eng.profile(False)
+    ms_max = reduce(ms, MAX)
+    # sampled edges of the timed steps, summed over ranks (re-derived per step below)
+    edges_rank = 0
+    # ---- end-to-end through the public API: host batch in, loss out, every step
+    e2e_sl = slice(args.warmup + args.steps, args.warmup + 2 * args.steps)
+    barrier()
+    te = time.perf_counter()
+    for b, s in zip(batches[e2e_sl], seeds[e2e_sl]):
+        rep = eng.step(b, s, 0, train=True)
+        edges_rank += rep["sampled_edges"]
+    barrier()
+    e2e_s = reduce(time.perf_counter() - te, MAX)
+    e2e_edges = reduce(float(edges_rank), SUM)
+    # device-timed steps sampled the same kind of batches; count their edges exactly
+    # by replaying the sampler only (cheap) on this rank
+    dev_edges = 0
+    for b, s in zip(batches[sl], seeds[sl]):
+        eng.sample(b, s)
+        dev_edges += int(eng.read("sampled_edges")["sampled_edges"][0])
+    dev_edges = reduce(float(dev_edges), SUM)
+
+    if rank != 0:
+        if world > 1:
+            tdist.destroy_process_group()
+        return
+
+    value = dev_edges / (ms_max / 1000.0)
+    e2e_value = e2e_edges / e2e_s
+    peak, peak_kind = load_peaks()
+    # dominant kernel: the largest share of the step's device time
+    classes = {k.split(".")[1]: float(v[0]) for k, v in prof.items() if k.endswith(".ms")}
+    launches_by = {k.split(".")[1]: int(v[0]) for k, v in prof.items() if k.endswith(".launches")}
+    alg = prof["alg_bytes"]
+    alg_by = {"sample": alg[0], "aggregate": alg[1], "aggregate_top": alg[2]}
+    dom = max(classes, key=classes.get)
+    roof_kernel = dom if dom in alg_by else max(alg_by, key=lambda k: classes.get(k, 0.0))
+    per_launch_bytes = alg_by[roof_kernel] / max(1, launches_by.get(roof_kernel, 1))
+    per_launch_ms = classes[roof_kernel] / max(1, launches_by.get(roof_kernel, 1))
+    achieved = per_launch_bytes / (per_launch_ms / 1000.0) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": n, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "C2 ogbn-mag-shape (BASELINE configs[1]) 2-layer RGCN hidden 64, fanout [25,20]",
+                   "global_batch": batch, "batch_per_gpu": BATCH_PER_GPU, "parallelism": f"meta-partition p={n}",
+                   "graph_seed": SEED, "l2": "not flushed: tables 1.3 GB + CSR 0.3 GB >> 126 MB L2, new rows every step"},
+        "epoch_time_s": (ms_max / args.steps) * EPOCH_BATCHES / n / 1000.0,
+        "sampled_edges_per_step": dev_edges / args.steps,
+        "gpu_launches": launches * args.steps,
+        "launches_per_step": launches,
+        "clocks": clk.summary(),
+        "e2e": {"value": e2e_value, "unit": "edges/s", "h2d_bytes_per_step": 4 * batch + 32,
+                "d2h_bytes_per_step": 24, "ms_per_step": 1000.0 * e2e_s / args.steps},
+        "roofline": {"bound": "hbm", "kernel": roof_kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "alg_bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms},
+        "kernel_share": {k: v / max(1e-9, sum(classes.values())) for k, v in sorted(classes.items())},
+        "kernel_us_per_step_eager": {k: 1000.0 * v / prof_steps for k, v in sorted(classes.items())},
+        "final_loss": loss,
+        "setup_s": {"graph_gen": t_gen},
+    }
+    if not args.no_cpu_baseline and n == 1:
+        threads = os.cpu_count() or 1
+        v, sample, secs, _ = cpu_baseline_sample(threads, threads)
+        line["cpu_baseline"] = {"value": v, "unit": "edges/s", "cores": threads, "kind": "reference",
+                                "sample": sample + f" ({secs:.1f} s)"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        tdist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--warmup-ref", type=int, default=0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

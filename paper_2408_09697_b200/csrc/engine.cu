@@ -1,5 +1,6 @@
 // Device engine: static plan, workspace, and the per-step launch sequence.
 #include "engine.hpp"
+#include "gemm.cuh"
 
 #include <algorithm>
 #include <cstring>
@@ -61,6 +62,37 @@ __global__ void k_gather_rows(const float* table, int ld, const std::uint32_t* i
   }
 }
 
+// Algorithmic bytes of the main kernel classes for one step, accumulated on
+// the device (SURVEY §8(d) formulas): [0] sample, [1] aggregate (inner layers),
+// [2] aggregate_top (layer k).
+struct AlgBytesArgs {
+  const std::uint32_t* indptr[kMaxBlocks * 4];
+  const int* n_rows[kMaxBlocks * 4];
+  int din[kMaxBlocks * 4];
+  int cls[kMaxBlocks * 4];  // 1 inner aggregate, 2 top aggregate
+  int nblk;
+  const int* g_rows[kMaxBlocks * 4];
+  int g_dout[kMaxBlocks * 4];
+  int g_cls[kMaxBlocks * 4];
+  int ngrp;
+};
+
+__global__ void k_alg_bytes(AlgBytesArgs a, double* acc) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s = 0, agg[3] = {0, 0, 0};
+  for (int i = 0; i < a.nblk; ++i) {
+    const double R = *a.n_rows[i], E = a.indptr[i][*a.n_rows[i]];
+    // sampling: indptr pair + dst id read, neighbour reads, src write, offset write
+    s += 16.0 * R + 4.0 * R + 4.0 * E + 4.0 * E + 4.0 * R;
+    // aggregation: per edge one source row + its id; offsets; tape write
+    agg[a.cls[i]] += E * (4.0 * a.din[i] + 4.0) + 4.0 * (R + 1) + 4.0 * R * a.din[i];
+  }
+  for (int i = 0; i < a.ngrp; ++i) agg[a.g_cls[i]] += 4.0 * static_cast<double>(*a.g_rows[i]) * a.g_dout[i];
+  acc[0] += s;
+  acc[1] += agg[1];
+  acc[2] += agg[2];
+}
+
 template <typename T>
 void put(std::vector<char>& data, const std::vector<T>& v) {
   data.resize(v.size() * sizeof(T));
@@ -89,6 +121,9 @@ Engine::Engine(const Graph& g, const EngineOptions& o) : o_(o) {
 
 Engine::~Engine() {
   cudaStreamSynchronize(st_);
+  if (exec_train_) cudaGraphExecDestroy(exec_train_);
+  if (exec_eval_) cudaGraphExecDestroy(exec_eval_);
+  for (auto e : ev_pool_) cudaEventDestroy(e);
   for (void* p : allocs_) cudaFree(p);
   if (h_sc_) cudaFreeHost(h_sc_);
   if (h_batch_) cudaFreeHost(h_batch_);
@@ -408,6 +443,7 @@ void Engine::upload(const Graph& g) {
   edges_dev_ = &rb->edges;
   HG_CUDA(cudaMallocHost(&h_rb_, sizeof(Readback)));
   cache_hm_ = static_cast<unsigned long long*>(alloc(sizeof(unsigned long long) * 2 * ntypes_));
+  alg_bytes_ = static_cast<double*>(alloc(sizeof(double) * 4));
   cache_types_.assign(ntypes_, false);
 
   int max_cap = std::max(total_words_, max_rows);
@@ -420,11 +456,16 @@ void Engine::upload(const Graph& g) {
   mt_scratch_ = static_cast<std::uint64_t*>(alloc(sample_scratch_words(maxf) * 8));
   std::size_t wt = 1, wp = 1;
   for (const auto& s : slots_) wt = std::max<std::size_t>(wt, static_cast<std::size_t>(round_up4(s.din)) * s.dout);
-  for (const auto& gr : groups_)
-    for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
-      const Slot& s = slots_[gr.slots[q]];
-      wp = std::max<std::size_t>(wp, ceil_div(std::max(1, gr.rows_cap), 256) * s.din * s.dout);
+  for (int l = 1; l <= o_.k; ++l) {
+    std::size_t layer = 0;
+    for (const auto& gr : groups_) {
+      if (gr.layer != l) continue;
+      const int rc = (l == o_.k && replica_) ? static_cast<int>(ceil_div(o_.batch_cap, shard_count_)) : gr.rows_cap;
+      for (std::size_t q = 0; q < gr.blocks.size(); ++q)
+        layer += ceil_div(std::max(1, rc), kWChunkRows) * static_cast<std::size_t>(blocks_[gr.blocks[q]].din) * gr.dout;
     }
+    wp = std::max(wp, layer);
+  }
   wt_scratch_ = static_cast<float*>(alloc(wt * 4));
   wgrad_partial_ = static_cast<float*>(alloc(wp * 4));
   HG_CUDA(cudaStreamSynchronize(st_));
@@ -442,20 +483,32 @@ void Engine::timed(const char* name, double bytes, const std::function<void()>& 
     f();
     return;
   }
-  cudaEvent_t a, b;
-  HG_CUDA(cudaEventCreate(&a));
-  HG_CUDA(cudaEventCreate(&b));
+  // event pairs are recorded asynchronously and resolved in finish_step(), so
+  // the per-class device times come from the timed run itself
+  if (ev_used_ + 2 > ev_pool_.size()) {
+    cudaEvent_t e;
+    for (int i = 0; i < 2; ++i) {
+      HG_CUDA(cudaEventCreate(&e));
+      ev_pool_.push_back(e);
+    }
+  }
+  cudaEvent_t a = ev_pool_[ev_used_++], b = ev_pool_[ev_used_++];
   HG_CUDA(cudaEventRecord(a, st_));
   f();
   HG_CUDA(cudaEventRecord(b, st_));
-  HG_CUDA(cudaEventSynchronize(b));
-  float ms = 0.f;
-  HG_CUDA(cudaEventElapsedTime(&ms, a, b));
-  kernel_ms_[name] += ms;
+  pending_.push_back({name, a, b});
   kernel_bytes_[name] += bytes;
-  kernel_launches_[name] += 1;
-  cudaEventDestroy(a);
-  cudaEventDestroy(b);
+}
+
+void Engine::resolve_profile() {
+  for (const auto& p : pending_) {
+    float ms = 0.f;
+    HG_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+    kernel_ms_[p.name] += ms;
+    kernel_launches_[p.name] += 1;
+  }
+  pending_.clear();
+  ev_used_ = 0;
 }
 
 void Engine::run_sampling() {
@@ -535,6 +588,24 @@ void Engine::run_sampling() {
     ++ec.n;
   }
   k_count_edges<<<1, 32, 0, st_>>>(ec, edges_dev_);
+  if (profiling_) {
+    AlgBytesArgs ab{};
+    for (const auto& b : blocks_) {
+      ab.indptr[ab.nblk] = b.indptr;
+      ab.n_rows[ab.nblk] = b.hop == 1 ? hop1_n : front(b.hop - 1, b.dst_t).count;
+      ab.din[ab.nblk] = b.din;
+      ab.cls[ab.nblk] = b.hop == 1 ? 2 : 1;
+      ++ab.nblk;
+    }
+    for (const auto& gr : groups_) {
+      if (gr.blocks.empty() || ab.ngrp >= kMaxBlocks * 4) continue;
+      ab.g_rows[ab.ngrp] = (gr.layer == o_.k && replica_) ? shard_count_dev_ : front(gr.depth - 1, gr.type).count;
+      ab.g_dout[ab.ngrp] = gr.dout;
+      ab.g_cls[ab.ngrp] = gr.layer == o_.k ? 2 : 1;
+      ++ab.ngrp;
+    }
+    k_alg_bytes<<<1, 32, 0, st_>>>(ab, alg_bytes_);
+  }
   // cache lookups + updates over the layer-0 frontier (harness.cpp:425-437)
   if (cache_on_)
     for (int t = 0; t < ntypes_; ++t)
@@ -590,7 +661,7 @@ void Engine::run_forward() {
       zero_rows(gr.out, gr.ld, front(gr.depth - 1, gr.type).count, gr.rows_cap, st_);
       continue;
     }
-    timed(top ? "aggregate_top" : "aggregate", bytes, [&] { aggregate_project(ag, st_); });
+    timed(top ? "aggregate_top" : "aggregate", bytes, [&] { agg_tiles(ag, st_); });
   }
   // AGG_all: sum the partial logits of every partition (raf.cpp:427-446)
   if (o_.p > 1) {
@@ -656,26 +727,29 @@ void Engine::run_backward() {
 
   for (int l = k; l >= 1; --l) {
     const int d = k - l + 1;
+    WGradBatch wb{};
+    DMeanBatch db{};
+    std::size_t partial_off = 0;
     for (const auto& gr : groups_) {
       if (gr.layer != l || gr.blocks.empty()) continue;
       const bool top = l == k;
       const int* n_rows = (top && replica_) ? shard_count_dev_ : front(d - 1, gr.type).count;
       const int rows_cap = top && replica_ ? static_cast<int>(ceil_div(o_.batch_cap, shard_count_)) : gr.rows_cap;
-      const int stride = top ? shard_count_ : 1, offset = top ? shard_index_ : 0;
-      if (!top) timed("relu_mask", 0, [&] { relu_mask(gr.dout_buf, gr.out, gr.ld, gr.dout, n_rows, rows_cap, 1, 0, st_); });
+      // dpre = dH (x) [H > 0] between layers, fused into the operand loads
+      const DpreView dv{gr.dout_buf, top ? nullptr : gr.out, gr.ld, gr.dout, top ? shard_count_ : 1,
+                        top ? shard_index_ : 0};
       for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
         BlockBuf& b = blocks_[gr.blocks[q]];
         Slot& s = slots_[gr.slots[q]];
-        WGradArgs wa{b.mean, b.ld_mean, b.din, gr.dout_buf, gr.ld, gr.dout, stride, offset, n_rows, rows_cap,
-                     wgrad_partial_, s.g, s.ld};
-        timed("weight_grad", 0, [&] { weight_grad(wa, st_); });
-        if (b.need_src_grad) {
-          DMeanArgs da{gr.dout_buf, gr.ld, gr.dout, stride, offset, s.w, s.ld, b.din, b.indptr, n_rows, rows_cap,
-                       b.dmean, b.ld_mean};
-          timed("mean_grad", 0, [&] { mean_grad(da, wt_scratch_, st_); });
-        }
+        if (wb.np >= kMaxProblems || db.np >= kMaxProblems) throw std::runtime_error("too many problems per layer");
+        wb.p[wb.np++] = {b.mean, b.ld_mean, b.din, dv, n_rows, rows_cap, wgrad_partial_ + partial_off, s.g, s.ld};
+        partial_off += ceil_div(std::max(1, rows_cap), kWChunkRows) * static_cast<std::size_t>(b.din) * gr.dout;
+        if (b.need_src_grad)
+          db.p[db.np++] = {dv, s.w, s.ld, b.din, b.indptr, n_rows, rows_cap, b.dmean, b.ld_mean};
       }
     }
+    timed("weight_grad", 0, [&] { wgrad_tiles(wb, st_); });
+    timed("mean_grad", 0, [&] { dmean_tiles(db, st_); });
     // scatter back to the sources of this hop, as ordered gathers
     for (auto& c : cscs_) {
       if (c.hop != d) continue;
@@ -698,28 +772,54 @@ void Engine::run_backward() {
 
 void Engine::run_update() {
   AdamHyper hp;
+  AdamModelBatch mb{};
+  int base = 0;
+  for (auto& s : slots_) {
+    if (mb.n >= kMaxSlots) throw std::runtime_error("too many model slots");
+    mb.w[mb.n] = s.w;
+    mb.m[mb.n] = s.m;
+    mb.v[mb.n] = s.v;
+    mb.g[mb.n] = s.g;
+    mb.base4[mb.n] = base;
+    base += std::max(1, s.din) * s.ld / 4;
+    ++mb.n;
+  }
+  mb.total4 = base;
+  AdamRowsBatch rb{};
+  base = 0;
+  for (const auto& c : cscs_) {
+    if (c.hop != o_.k) continue;
+    TypeTable& tb = tables_[c.src_t];
+    if (!tb.learnable) continue;
+    const Front& f = front(o_.k, c.src_t);
+    rb.t[rb.n] = {tb.w, tb.m, tb.v, tb.ld, f.list, c.dh, c.ld, f.count, tb.step};
+    rb.base4[rb.n] = base;
+    base += f.cap * tb.ld / 4;
+    ++rb.n;
+  }
+  rb.total4 = base;
   timed("adam", 0, [&] {
-    for (auto& s : slots_)
-      adam_dense(s.w, s.m, s.v, s.g, s.din, s.dout, s.ld, &d_sc_->model_step, hp, err_, st_);
-    for (const auto& c : cscs_) {
-      if (c.hop != o_.k) continue;
-      TypeTable& tb = tables_[c.src_t];
-      if (!tb.learnable) continue;
-      const Front& f = front(o_.k, c.src_t);
-      adam_rows(tb.w, tb.m, tb.v, tb.ld, tb.dim, f.list, c.dh, c.ld, f.count, f.cap, tb.step, hp, err_, st_);
-    }
+    adam_model(mb, &d_sc_->model_step, hp, err_, st_);
+    adam_rows(rb, hp, err_, st_);
   });
 }
 
-void Engine::enqueue_step(std::uint64_t rng_seed, int n, int designated, bool train) {
+StepScalars Engine::next_scalars(std::uint64_t rng_seed, int n, int designated, bool train) {
   if (n > o_.batch_cap) throw std::invalid_argument("batch larger than the engine's batch capacity");
   if (n <= 0) throw std::invalid_argument("empty batch");
   if (train) ++model_step_;
-  h_sc_->rng_seed = rng_seed;
-  h_sc_->batch_len = n;
-  h_sc_->designated = designated;
-  h_sc_->model_step = model_step_;
-  HG_CUDA(cudaMemcpyAsync(d_sc_, h_sc_, sizeof(StepScalars), cudaMemcpyHostToDevice, st_));
+  StepScalars sc{};
+  sc.rng_seed = rng_seed;
+  sc.batch_len = n;
+  sc.designated = designated;
+  sc.model_step = model_step_;
+  return sc;
+}
+
+// The step body: everything after the batch ids and step scalars are in device
+// memory. Captured once per mode into a CUDA graph and replayed (profiling
+// runs it eagerly so every kernel class can be bracketed by events).
+void Engine::step_body(bool train) {
   HG_CUDA(cudaMemsetAsync(err_, 0, sizeof(std::uint32_t), st_));
   run_sampling();
   run_forward();
@@ -731,9 +831,45 @@ void Engine::enqueue_step(std::uint64_t rng_seed, int n, int designated, bool tr
   HG_CUDA(cudaMemcpyAsync(h_rb_, loss_, sizeof(Readback), cudaMemcpyDeviceToHost, st_));
 }
 
+void Engine::launch_body(bool train) {
+  if (!use_graphs_ || profiling_) {
+    step_body(train);
+    return;
+  }
+  cudaGraphExec_t& ex = train ? exec_train_ : exec_eval_;
+  if (!ex) {
+    cudaGraph_t graph = nullptr;
+    HG_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+    try {
+      step_body(train);
+    } catch (...) {
+      cudaStreamEndCapture(st_, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    HG_CUDA(cudaStreamEndCapture(st_, &graph));
+    HG_CUDA(cudaGraphInstantiate(&ex, graph, 0));
+    cudaGraphDestroy(graph);
+  }
+  HG_CUDA(cudaGraphLaunch(ex, st_));
+}
+
+void Engine::enqueue_step(std::uint64_t rng_seed, int n, int designated, bool train) {
+  *h_sc_ = next_scalars(rng_seed, n, designated, train);
+  HG_CUDA(cudaMemcpyAsync(d_sc_, h_sc_, sizeof(StepScalars), cudaMemcpyHostToDevice, st_));
+  launch_body(train);
+}
+
+void Engine::enqueue_step_device(const StepScalars* d_src, const std::uint32_t* d_ids, int n, bool train) {
+  HG_CUDA(cudaMemcpyAsync(d_batch_, d_ids, static_cast<std::size_t>(n) * 4, cudaMemcpyDeviceToDevice, st_));
+  HG_CUDA(cudaMemcpyAsync(d_sc_, d_src, sizeof(StepScalars), cudaMemcpyDeviceToDevice, st_));
+  launch_body(train);
+}
+
 StepReport Engine::finish_step() {
   HG_CUDA(cudaStreamSynchronize(st_));
   HG_CUDA(cudaGetLastError());
+  if (profiling_) resolve_profile();
   StepReport r;
   r.loss = h_rb_->loss;
   r.err = h_rb_->err;
@@ -759,6 +895,50 @@ StepReport Engine::step(const NodeId* batch, int n, std::uint64_t rng_seed, int 
   HG_CUDA(cudaMemcpyAsync(d_batch_, h_batch_, sizeof(NodeId) * n, cudaMemcpyHostToDevice, st_));
   enqueue_step(rng_seed, n, designated, train);
   return finish_step();
+}
+
+int Engine::count_launches(int n, bool train) {
+  // capture one step (without executing it) and count our kernel nodes
+  const bool prof = profiling_;
+  profiling_ = false;
+  cudaGraph_t graph = nullptr;
+  HG_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+  (void)n;
+  try {
+    step_body(train);
+  } catch (...) {
+    cudaStreamEndCapture(st_, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    profiling_ = prof;
+    throw;
+  }
+  HG_CUDA(cudaStreamEndCapture(st_, &graph));
+  profiling_ = prof;
+  std::size_t nn = 0;
+  HG_CUDA(cudaGraphGetNodes(graph, nullptr, &nn));
+  std::vector<cudaGraphNode_t> nodes(nn);
+  HG_CUDA(cudaGraphGetNodes(graph, nodes.data(), &nn));
+  int kernels = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType ty;
+    HG_CUDA(cudaGraphNodeGetType(nd, &ty));
+    if (ty != cudaGraphNodeTypeKernel) continue;
+    cudaKernelNodeParams kp{};
+    HG_CUDA(cudaGraphKernelNodeGetParams(nd, &kp));
+    const char* fname = nullptr;
+    if (cudaFuncGetName(&fname, kp.func) == cudaSuccess && fname && std::strstr(fname, "nccl")) continue;
+    ++kernels;
+  }
+  cudaGraphDestroy(graph);
+  launches_per_step_ = kernels;
+  return kernels;
+}
+
+std::vector<double> Engine::algorithmic_bytes() {
+  std::vector<double> v(4, 0.0);
+  HG_CUDA(cudaStreamSynchronize(st_));
+  HG_CUDA(cudaMemcpy(v.data(), alg_bytes_, sizeof(double) * 4, cudaMemcpyDeviceToHost));
+  return v;
 }
 
 void Engine::sample_only(const NodeId* batch, int n, std::uint64_t rng_seed) {

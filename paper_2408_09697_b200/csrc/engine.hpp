@@ -69,8 +69,12 @@ class Engine {
   // Full training step: sample, forward, AGG_all, loss, backward, Adam.
   // `batch` is host memory (copied to the device inside the call).
   StepReport step(const NodeId* batch, int n, std::uint64_t rng_seed, int designated, bool train = true);
-  // Same as step() but the batch is already on the device (benchmark inner loop).
+  // Same as step() but without the final synchronisation (batch already in d_batch_).
   void enqueue_step(std::uint64_t rng_seed, int n, int designated, bool train);
+  // Benchmark inner loop: batch ids and step scalars already resident in HBM.
+  void enqueue_step_device(const StepScalars* d_src, const std::uint32_t* d_ids, int n, bool train);
+  StepScalars next_scalars(std::uint64_t rng_seed, int n, int designated, bool train);
+  void set_graphs(bool on) { use_graphs_ = on; }
   StepReport finish_step();
   // Sampling only (parity of the sampler; presample_hotness).
   void sample_only(const NodeId* batch, int n, std::uint64_t rng_seed);
@@ -96,7 +100,13 @@ class Engine {
     kernel_ms_.clear();
     kernel_bytes_.clear();
     kernel_launches_.clear();
+    if (alg_bytes_) cudaMemsetAsync(alg_bytes_, 0, sizeof(double) * 4, st_);
   }
+  // kernel launches of one step, counted from a captured (not executed) step
+  int count_launches(int n, bool train);
+  // cumulative algorithmic bytes since reset_profile (profiling on):
+  // [0] sample, [1] aggregate, [2] aggregate_top
+  std::vector<double> algorithmic_bytes();
   std::map<std::string, int> kernel_launches() const { return kernel_launches_; }
   int launches_per_step() const { return launches_per_step_; }
 
@@ -234,6 +244,19 @@ class Engine {
   bool cache_on_ = false;
   std::vector<bool> cache_types_;
   bool profiling_ = false;
+  struct PendingEvent {
+    std::string name;
+    cudaEvent_t a, b;
+  };
+  std::vector<PendingEvent> pending_;
+  std::vector<cudaEvent_t> ev_pool_;
+  std::size_t ev_used_ = 0;
+  double* alg_bytes_ = nullptr;
+  void resolve_profile();
+  void step_body(bool train);
+  void launch_body(bool train);
+  bool use_graphs_ = true;
+  cudaGraphExec_t exec_train_ = nullptr, exec_eval_ = nullptr;
   std::map<std::string, double> kernel_ms_, kernel_bytes_;
   std::map<std::string, int> kernel_launches_;
   int launches_per_step_ = 0;

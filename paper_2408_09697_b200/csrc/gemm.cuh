@@ -1,0 +1,59 @@
+// Multi-problem tile kernels for the dense contractions (gemm_kernels.cu).
+#pragma once
+
+#include "kernels.cuh"
+
+namespace hetgpu {
+
+constexpr int kMaxProblems = 16;
+constexpr int kWChunkRows = 256;  // split-K rows per weight-gradient partial
+
+// dpre rows: g[(i*stride + offset) * ld + c], masked by H > 0 when h != nullptr
+struct DpreView {
+  const float* g;
+  const float* h;
+  int ld;
+  int cols;
+  int stride;
+  int offset;
+};
+
+struct WGradProblem {
+  const float* mean;
+  int ld_mean;
+  int din;
+  DpreView d;
+  const int* n_rows;
+  int rows_cap;
+  float* partial;  // [chunks x din x cols]
+  float* dw;
+  int ld_dw;
+};
+struct WGradBatch {
+  WGradProblem p[kMaxProblems];
+  int tile_base[kMaxProblems];
+  int np;
+};
+
+struct DMeanProblem {
+  DpreView d;
+  const float* w;  // [din x dout], ld_w
+  int ld_w;
+  int din;
+  const std::uint32_t* indptr;
+  const int* n_rows;
+  int rows_cap;
+  float* dmean;
+  int ld_dmean;
+};
+struct DMeanBatch {
+  DMeanProblem p[kMaxProblems];
+  int tile_base[kMaxProblems];
+  int np;
+};
+
+void agg_tiles(const AggGroup& g, cudaStream_t st);
+void wgrad_tiles(WGradBatch& b, cudaStream_t st);
+void dmean_tiles(DMeanBatch& b, cudaStream_t st);
+
+}  // namespace hetgpu

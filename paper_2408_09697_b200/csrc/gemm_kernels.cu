@@ -1,0 +1,312 @@
+// SIMT fp32 tile kernels for the small dense contractions of the hot path:
+// the fused gather-mean-project of every layer (hgnn.cpp:173-203), the
+// backward weight gradient dW += mean^T . dpre (matrix.hpp:49-61) and the
+// mean gradient dmean = dpre . W^T / deg (matrix.hpp:64-78, hgnn.cpp:344-353).
+// One 64x64 output tile per CTA, 256 threads with a 4x4 register tile each,
+// K staged through shared memory in 32-deep slabs. Several independent
+// problems share one launch (tile ids are linearised over the problems).
+#include "gemm.cuh"
+
+namespace hetgpu {
+
+namespace {
+
+constexpr int kT = 256;   // threads
+constexpr int kTile = 64; // output tile (rows and cols)
+constexpr int kKS = 32;   // K slab
+constexpr int kLd = kTile + 4;
+
+struct Acc {
+  float v[4][4];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[i][j] = 0.f;
+  }
+};
+
+// acc += As[k][ty*4..+4] (x) Bs[k][tx*4..+4] over k < kn
+__device__ __forceinline__ void slab_fma(const float* As, const float* Bs, int kn, int ty, int tx, Acc& acc) {
+#pragma unroll 8
+  for (int k = 0; k < kn; ++k) {
+    const float4 a = *reinterpret_cast<const float4*>(As + k * kLd + ty * 4);
+    const float4 b = *reinterpret_cast<const float4*>(Bs + k * kLd + tx * 4);
+    const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc.v[i][j] = fmaf(av[i], bv[j], acc.v[i][j]);
+  }
+}
+
+__device__ __forceinline__ int find_problem(const int* tile_base, int np, int tile) {
+  int p = 0;
+  while (p + 1 < np && tile >= tile_base[p + 1]) ++p;
+  return p;
+}
+
+// ---- forward: fused gather-mean-project ------------------------------------------------
+// tile (row block rb, col block cb) of one group. For every relation and every
+// 64-wide chunk of its input columns: the CTA gathers the neighbour rows of its
+// 64 block rows (by global id from the feature table at layer 1, by frontier
+// row otherwise), averages them into As (transposed) and the tape, stages the
+// matching W slab and accumulates. Relations sum in ascending order (agg_all).
+__global__ void __launch_bounds__(kT) k_agg_tiles(AggGroup g) {
+  __shared__ __align__(16) float As[kKS * 2 * kLd];  // 64 k rows (two slabs)
+  __shared__ __align__(16) float Bs[kKS * 2 * kLd];
+  const int n = *g.n_rows;
+  const int ncb = (g.dout + kTile - 1) / kTile;
+  const int rb = blockIdx.x / ncb, cb = blockIdx.x % ncb;
+  const int row0 = rb * kTile, col0 = cb * kTile;
+  if (row0 >= n) return;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int half = lane >> 4, hl = lane & 15;  // half-warp per row, 4 cols per lane
+  Acc acc;
+  acc.zero();
+  for (int q = 0; q < g.nrel; ++q) {
+    const AggRel& r = g.r[q];
+    const std::uint32_t* keys = r.by_id ? r.src : r.col;
+    for (int c0 = 0; c0 < r.din; c0 += 2 * kKS) {
+      const int kn = min(2 * kKS, r.din - c0);
+      __syncthreads();
+      // gather: 8 warps x 2 half-warps = 16 rows per pass, 4 passes
+      for (int rr = warp * 2 + half; rr < kTile; rr += 16) {
+        const int i = row0 + rr;
+        float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int c = c0 + 4 * hl;
+        if (i < n && 4 * hl < kn) {
+          const std::uint32_t lo = r.indptr[i], hi = r.indptr[i + 1];
+          const float* base = r.h + c;
+          std::uint32_t e = lo;
+          for (; e + 4 <= hi; e += 4) {
+            const std::uint32_t k0 = __ldg(keys + e), k1 = __ldg(keys + e + 1), k2 = __ldg(keys + e + 2),
+                                k3 = __ldg(keys + e + 3);
+            const float4 v0 = __ldg(reinterpret_cast<const float4*>(base + static_cast<std::size_t>(k0) * r.ld_h));
+            const float4 v1 = __ldg(reinterpret_cast<const float4*>(base + static_cast<std::size_t>(k1) * r.ld_h));
+            const float4 v2 = __ldg(reinterpret_cast<const float4*>(base + static_cast<std::size_t>(k2) * r.ld_h));
+            const float4 v3 = __ldg(reinterpret_cast<const float4*>(base + static_cast<std::size_t>(k3) * r.ld_h));
+            s.x += (v0.x + v1.x) + (v2.x + v3.x);
+            s.y += (v0.y + v1.y) + (v2.y + v3.y);
+            s.z += (v0.z + v1.z) + (v2.z + v3.z);
+            s.w += (v0.w + v1.w) + (v2.w + v3.w);
+          }
+          for (; e < hi; ++e) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(base + static_cast<std::size_t>(__ldg(keys + e)) * r.ld_h));
+            s.x += v.x;
+            s.y += v.y;
+            s.z += v.z;
+            s.w += v.w;
+          }
+          if (hi > lo) {
+            const float inv = 1.0f / static_cast<float>(hi - lo);
+            s.x *= inv;
+            s.y *= inv;
+            s.z *= inv;
+            s.w *= inv;
+          }
+          if (cb == 0) *reinterpret_cast<float4*>(r.mean + static_cast<std::size_t>(i) * r.ld_mean + c) = s;
+        }
+        const int kc = 4 * hl;
+        As[(kc + 0) * kLd + rr] = s.x;
+        As[(kc + 1) * kLd + rr] = s.y;
+        As[(kc + 2) * kLd + rr] = s.z;
+        As[(kc + 3) * kLd + rr] = s.w;
+      }
+      // W slab: rows c0..c0+kn, cols col0..col0+64
+      for (int x = tid; x < 2 * kKS * kTile / 4; x += kT) {
+        const int k = x / (kTile / 4), nq = (x % (kTile / 4)) * 4;
+        float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (k < kn && col0 + nq < g.dout)
+          w = __ldg(reinterpret_cast<const float4*>(r.w + static_cast<std::size_t>(c0 + k) * r.ld_w + col0 + nq));
+        *reinterpret_cast<float4*>(Bs + k * kLd + nq) = w;
+      }
+      __syncthreads();
+      slab_fma(As, Bs, kn, ty, tx, acc);
+    }
+  }
+  // epilogue: ReLU between layers, store (row remap for replica shards)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = row0 + ty * 4 + i;
+    if (row >= n) break;
+    float* orow = g.out + static_cast<std::size_t>(row * g.out_stride + g.out_offset) * g.ld_out;
+    const int c = col0 + tx * 4;
+    if (c < g.dout) {
+      float4 o = make_float4(acc.v[i][0], acc.v[i][1], acc.v[i][2], acc.v[i][3]);
+      if (g.relu) {
+        o.x = fmaxf(o.x, 0.f);
+        o.y = fmaxf(o.y, 0.f);
+        o.z = fmaxf(o.z, 0.f);
+        o.w = fmaxf(o.w, 0.f);
+      }
+      // out rows are ld_out = round_up4(dout) wide: the float4 stays in bounds,
+      // padded columns receive zeros (W padding is zero)
+      *reinterpret_cast<float4*>(orow + c) = o;
+    }
+  }
+}
+
+// ---- dpre staging helpers (ReLU mask fused) -------------------------------------------------
+__device__ __forceinline__ float4 load_dpre4(const DpreView& d, int row, int col) {
+  const std::size_t at = static_cast<std::size_t>(row * d.stride + d.offset) * d.ld + col;
+  float4 v = *reinterpret_cast<const float4*>(d.g + at);
+  if (d.h) {  // dpre = dH * [H > 0] (hgnn.cpp:326-328); H in the group's own row space
+    const float4 h = *reinterpret_cast<const float4*>(d.h + static_cast<std::size_t>(row) * d.ld + col);
+    if (h.x <= 0.f) v.x = 0.f;
+    if (h.y <= 0.f) v.y = 0.f;
+    if (h.z <= 0.f) v.z = 0.f;
+    if (h.w <= 0.f) v.w = 0.f;
+  }
+  return v;
+}
+
+// ---- backward: weight gradient partials --------------------------------------------------
+// problem p: partial[chunk][i][j] = sum_{r in chunk} mean[r][i] * dpre[r][j]
+__global__ void __launch_bounds__(kT) k_wgrad_tiles(WGradBatch b) {
+  __shared__ __align__(16) float As[kKS * kLd];
+  __shared__ __align__(16) float Bs[kKS * kLd];
+  const int p = find_problem(b.tile_base, b.np, blockIdx.x);
+  const WGradProblem& P = b.p[p];
+  const int t = blockIdx.x - b.tile_base[p];
+  const int mt = (P.din + kTile - 1) / kTile, nt = (P.d.cols + kTile - 1) / kTile;
+  const int chunk = t / (mt * nt), mi = (t / nt) % mt, ni = t % nt;
+  const int n = *P.n_rows;
+  const int r0 = chunk * kWChunkRows;
+  if (r0 >= n) return;
+  const int r1 = min(n, r0 + kWChunkRows);
+  const int i0 = mi * kTile, j0 = ni * kTile;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  Acc acc;
+  acc.zero();
+  for (int k0 = r0; k0 < r1; k0 += kKS) {
+    const int kn = min(kKS, r1 - k0);
+    __syncthreads();
+    for (int x = tid; x < kKS * kTile / 4; x += kT) {
+      const int k = x / (kTile / 4), q = (x % (kTile / 4)) * 4;
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), bb = a;
+      if (k < kn) {
+        if (i0 + q < P.din)
+          a = *reinterpret_cast<const float4*>(P.mean + static_cast<std::size_t>(k0 + k) * P.ld_mean + i0 + q);
+        if (j0 + q < P.d.cols) bb = load_dpre4(P.d, k0 + k, j0 + q);
+      }
+      *reinterpret_cast<float4*>(As + k * kLd + q) = a;
+      *reinterpret_cast<float4*>(Bs + k * kLd + q) = bb;
+    }
+    __syncthreads();
+    slab_fma(As, Bs, kn, ty, tx, acc);
+  }
+  float* out = P.partial + static_cast<std::size_t>(chunk) * P.din * P.d.cols;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = i0 + ty * 4 + i;
+    if (row >= P.din) break;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = j0 + tx * 4 + j;
+      if (c < P.d.cols) out[static_cast<std::size_t>(row) * P.d.cols + c] = acc.v[i][j];
+    }
+  }
+}
+
+// ordered sum of the chunk partials into dW (deterministic)
+__global__ void k_wgrad_reduce(WGradBatch b) {
+  for (int p = 0; p < b.np; ++p) {
+    const WGradProblem& P = b.p[p];
+    const int chunks = (*P.n_rows + kWChunkRows - 1) / kWChunkRows;
+    const int total = P.din * P.d.cols;
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
+      float s = 0.f;
+      for (int c = 0; c < chunks; ++c) s += P.partial[static_cast<std::size_t>(c) * total + x];
+      P.dw[static_cast<std::size_t>(x / P.d.cols) * P.ld_dw + x % P.d.cols] += s;
+    }
+  }
+}
+
+// ---- backward: mean gradient ---------------------------------------------------------------------
+// dmean[r][c] = (sum_j dpre[r][j] * W[c][j]) / deg(r)
+__global__ void __launch_bounds__(kT) k_dmean_tiles(DMeanBatch b) {
+  __shared__ __align__(16) float As[kKS * kLd];
+  __shared__ __align__(16) float Bs[kKS * kLd];
+  const int p = find_problem(b.tile_base, b.np, blockIdx.x);
+  const DMeanProblem& P = b.p[p];
+  const int t = blockIdx.x - b.tile_base[p];
+  const int nt = (P.din + kTile - 1) / kTile;
+  const int rb = t / nt, cb = t % nt;
+  const int n = *P.n_rows;
+  const int row0 = rb * kTile, col0 = cb * kTile;
+  if (row0 >= n) return;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  Acc acc;
+  acc.zero();
+  const int K = P.d.cols;
+  for (int k0 = 0; k0 < K; k0 += kKS) {
+    const int kn = min(kKS, K - k0);
+    __syncthreads();
+    // As[k][m] = dpre[row0+m][k0+k]; Bs[k][c] = W[col0+c][k0+k] (both transposed on the way in)
+    for (int x = tid; x < kTile * kKS / 4; x += kT) {
+      const int m = x / (kKS / 4), kq = (x % (kKS / 4)) * 4;
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), w = a;
+      if (row0 + m < n && k0 + kq < K) a = load_dpre4(P.d, row0 + m, k0 + kq);
+      if (col0 + m < P.din && k0 + kq < K)
+        w = *reinterpret_cast<const float4*>(P.w + static_cast<std::size_t>(col0 + m) * P.ld_w + k0 + kq);
+      As[(kq + 0) * kLd + m] = a.x;
+      As[(kq + 1) * kLd + m] = a.y;
+      As[(kq + 2) * kLd + m] = a.z;
+      As[(kq + 3) * kLd + m] = a.w;
+      Bs[(kq + 0) * kLd + m] = w.x;
+      Bs[(kq + 1) * kLd + m] = w.y;
+      Bs[(kq + 2) * kLd + m] = w.z;
+      Bs[(kq + 3) * kLd + m] = w.w;
+    }
+    __syncthreads();
+    slab_fma(As, Bs, kn, ty, tx, acc);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = row0 + ty * 4 + i;
+    if (row >= n) break;
+    const std::uint32_t deg = P.indptr[row + 1] - P.indptr[row];
+    const float inv = deg ? 1.0f / static_cast<float>(deg) : 0.0f;
+    const int c = col0 + tx * 4;
+    if (c < P.din) {
+      float4 o = make_float4(acc.v[i][0] * inv, acc.v[i][1] * inv, acc.v[i][2] * inv, acc.v[i][3] * inv);
+      *reinterpret_cast<float4*>(P.dmean + static_cast<std::size_t>(row) * P.ld_dmean + c) = o;
+    }
+  }
+}
+
+}  // namespace
+
+void agg_tiles(const AggGroup& g, cudaStream_t st) {
+  const int ncb = static_cast<int>(ceil_div(g.dout, kTile));
+  const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, ceil_div(g.rows_cap, kTile) * ncb));
+  k_agg_tiles<<<grid, kT, 0, st>>>(g);
+}
+
+void wgrad_tiles(WGradBatch& b, cudaStream_t st) {
+  if (b.np == 0) return;
+  int tiles = 0;
+  for (int p = 0; p < b.np; ++p) {
+    const WGradProblem& P = b.p[p];
+    b.tile_base[p] = tiles;
+    tiles += static_cast<int>(ceil_div(std::max(1, P.rows_cap), kWChunkRows) * ceil_div(P.din, kTile) *
+                              ceil_div(P.d.cols, kTile));
+  }
+  k_wgrad_tiles<<<std::max(1, tiles), kT, 0, st>>>(b);
+  k_wgrad_reduce<<<2 * kNumSMs, 256, 0, st>>>(b);
+}
+
+void dmean_tiles(DMeanBatch& b, cudaStream_t st) {
+  if (b.np == 0) return;
+  int tiles = 0;
+  for (int p = 0; p < b.np; ++p) {
+    const DMeanProblem& P = b.p[p];
+    b.tile_base[p] = tiles;
+    tiles += static_cast<int>(ceil_div(std::max(1, P.rows_cap), kTile) * ceil_div(P.din, kTile));
+  }
+  k_dmean_tiles<<<std::max(1, tiles), kT, 0, st>>>(b);
+}
+
+}  // namespace hetgpu

@@ -141,7 +141,6 @@ struct AggGroup {
   int out_stride;
   int out_offset;
 };
-void aggregate_project(const AggGroup& g, cudaStream_t st);
 
 // ---- loss ------------------------------------------------------------------------
 struct LossArgs {
@@ -161,46 +160,7 @@ struct LossArgs {
 };
 void cross_entropy(const LossArgs& a, cudaStream_t st);
 
-// ---- backward ----------------------------------------------------------------------
-// dpre = dH * [H > 0] (in place on dH)
-void relu_mask(float* dh, const float* h, int ld, int cols, const int* n_rows, int rows_cap,
-               int in_stride, int in_offset, cudaStream_t st);
-// dW += mean^T . dpre over the live rows (deterministic two-level reduction)
-struct WGradArgs {
-  const float* mean;
-  int ld_mean;
-  int din;
-  const float* dpre;
-  int ld_dpre;
-  int dout;
-  int dpre_stride;  // dpre row = i*stride + offset (replica shards)
-  int dpre_offset;
-  const int* n_rows;
-  int rows_cap;
-  float* partial;   // scratch [chunks x din x dout]
-  float* dw;        // [din x dout], ld = ld_dw (accumulated)
-  int ld_dw;
-};
-void weight_grad(const WGradArgs& a, cudaStream_t st);
-// dmean = (dpre . W^T) / deg(row)
-struct DMeanArgs {
-  const float* dpre;
-  int ld_dpre;
-  int dout;
-  int dpre_stride;
-  int dpre_offset;
-  const float* w;
-  int ld_w;
-  int din;
-  const std::uint32_t* indptr;
-  const int* n_rows;
-  int rows_cap;
-  float* dmean;
-  int ld_dmean;
-};
-// wt_scratch: >= round_up4(din) * dout floats (W^T)
-void mean_grad(const DMeanArgs& a, float* wt_scratch, cudaStream_t st);
-
+// ---- backward ------------------------------------------------------------------------
 // transposed (src-major) view of a hop's blocks for one source type, used to
 // turn the backward scatter into an ordered gather (deterministic).
 struct CscBlock {
@@ -232,14 +192,35 @@ void csc_gather(const CscArgs& a, cudaStream_t st);
 struct AdamHyper {  // hgnn.hpp:16-21
   double lr = 1e-2, beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
 };
-// dense slot update; step counter in device memory (already incremented)
-void adam_dense(float* w, float* m, float* v, const float* g, int rows, int cols, int ld,
-                const std::int64_t* step, AdamHyper hp, std::uint32_t* err, cudaStream_t st);
-// sparse rows: ids = frontier[k][t], grads aligned with them; step_t advanced
-// on the device iff the frontier is non-empty
-void adam_rows(float* w, float* m, float* v, int ld, int cols, const std::uint32_t* ids,
-               const float* g, int ld_g, const int* n_rows, int rows_cap, std::int64_t* step,
-               AdamHyper hp, std::uint32_t* err, cudaStream_t st);
+constexpr int kMaxSlots = 64;
+// all model slots (adam_update_model, hgnn.cpp:379-390); base4 = prefix of rows*ld/4
+struct AdamModelBatch {
+  float* w[kMaxSlots];
+  float* m[kMaxSlots];
+  float* v[kMaxSlots];
+  const float* g[kMaxSlots];
+  int base4[kMaxSlots];
+  int n;
+  int total4;
+};
+void adam_model(AdamModelBatch& b, const std::int64_t* step, AdamHyper hp, std::uint32_t* err, cudaStream_t st);
+// sparse learnable rows (adam_update_rows, hgnn.cpp:392-410): ids = frontier[k][t]
+struct AdamRowsTable {
+  float *w, *m, *v;
+  int ld;
+  const std::uint32_t* ids;
+  const float* g;
+  int ld_g;
+  const int* n_rows;
+  std::int64_t* step;
+};
+struct AdamRowsBatch {
+  AdamRowsTable t[kMaxSegs];
+  int base4[kMaxSegs];  // prefix of rows_cap * ld / 4
+  int n;
+  int total4;
+};
+void adam_rows(AdamRowsBatch& b, AdamHyper hp, std::uint32_t* err, cudaStream_t st);
 
 // ---- misc --------------------------------------------------------------------------------
 void zero_rows(float* p, int ld, const int* n_rows, int rows_cap, cudaStream_t st);

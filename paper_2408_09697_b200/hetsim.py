@@ -270,6 +270,9 @@ class Engine:
         N.check(N.lib().hg_engine_info(self._h, C.byref(pc), C.byref(db), C.byref(ms)))
         return dict(param_count=pc.value, device_bytes=db.value, model_step=ms.value)
 
+    def count_launches(self, n: int, train: bool = True) -> int:
+        return N.check(N.lib().hg_engine_count_launches(self._h, n, int(train)))
+
     def presample_hotness(self, epochs: int, seed: int, batch_size: int = 512) -> Dict[str, np.ndarray]:
         return N.take(N.lib().hg_engine_presample_hotness(self._h, epochs, seed, batch_size))
 
