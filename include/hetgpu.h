@@ -147,6 +147,9 @@ void hg_engine_profile(hg_engine* e, int on);
  * bytes [sample, aggregate, aggregate_top, 0] since profiling was switched on */
 hg_bundle* hg_engine_profile_read(hg_engine* e);
 int hg_engine_info(hg_engine* e, uint64_t* param_count, uint64_t* device_bytes, int* model_step);
+/* options: "retain_grads" (keep learnable-row gradients readable as grad.f.*; default 1),
+ * "graphs" (replay the step as a CUDA graph; default 1) */
+int hg_engine_set_option(hg_engine* e, const char* name, int value);
 /* kernel launches of one step (a captured, never executed step; NCCL kernels excluded) */
 int hg_engine_count_launches(hg_engine* e, int n, int train);
 

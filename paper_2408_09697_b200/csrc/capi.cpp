@@ -422,6 +422,19 @@ int hg_engine_info(hg_engine* e, uint64_t* param_count, uint64_t* device_bytes, 
   });
 }
 
+int hg_engine_set_option(hg_engine* e, const char* name, int value) {
+  return guard<int>(-1, [&] {
+    const std::string n(name ? name : "");
+    if (n == "retain_grads")
+      e->e->set_retain_grads(value != 0);
+    else if (n == "graphs")
+      e->e->set_graphs(value != 0);
+    else
+      throw std::invalid_argument("unknown engine option: " + n);
+    return 0;
+  });
+}
+
 int hg_engine_count_launches(hg_engine* e, int n, int train) {
   return guard<int>(-1, [&] { return e->e->count_launches(n, train != 0); });
 }

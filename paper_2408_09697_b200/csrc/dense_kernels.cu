@@ -79,97 +79,6 @@ void cross_entropy(const LossArgs& a, cudaStream_t st) {
 
 namespace {
 
-__global__ void k_csc_count(CscArgs a) {
-  const CscBlock& b = a.b[blockIdx.y];
-  const std::uint32_t total = b.indptr[*b.n_rows];
-  for (std::uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x)
-    atomicAdd(a.offs + b.col[e], 1u);
-}
-
-__global__ void k_csc_fill(CscArgs a) {
-  const CscBlock& b = a.b[blockIdx.y];
-  const std::uint32_t total = b.indptr[*b.n_rows];
-  for (std::uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-    const std::uint32_t c = b.col[e];
-    const std::uint32_t pos = atomicAdd(a.cursor + c, 1u);
-    a.entries[a.offs[c] - 1 - pos] = static_cast<std::uint32_t>(b.edge_base) + e;
-  }
-}
-
-// make every segment ascending in (block, edge): deterministic summation order
-__global__ void k_csc_sort(CscArgs a) {
-  const int n = *a.n_src;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
-    const std::uint32_t lo = c ? a.offs[c - 1] : 0u, hi = a.offs[c];
-    for (std::uint32_t x = lo + 1; x < hi; ++x) {
-      const std::uint32_t v = a.entries[x];
-      std::uint32_t y = x;
-      while (y > lo && a.entries[y - 1] > v) {
-        a.entries[y] = a.entries[y - 1];
-        --y;
-      }
-      a.entries[y] = v;
-    }
-  }
-}
-
-// one warp per source row: dh[c] = sum over its sampled edges of dmean[row(e)]
-__global__ void __launch_bounds__(256) k_csc_gather(CscArgs a) {
-  const int n = *a.n_src;
-  const int lane = threadIdx.x & 31;
-  const int warps = gridDim.x * (blockDim.x / 32);
-  for (int c = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); c < n; c += warps) {
-    const std::uint32_t lo = c ? a.offs[c - 1] : 0u, hi = a.offs[c];
-    for (int c0 = 0; c0 < a.din; c0 += 128) {
-      const int f = c0 + 4 * lane;
-      if (f >= round_up4(a.din)) continue;
-      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (std::uint32_t x = lo; x < hi; ++x) {
-        const std::uint32_t id = a.entries[x];
-        int bi = 0;
-        while (bi + 1 < a.nblk && id >= static_cast<std::uint32_t>(a.b[bi + 1].edge_base)) ++bi;
-        const CscBlock& b = a.b[bi];
-        const std::uint32_t row = b.erow[id - b.edge_base];
-        const float4 v = *reinterpret_cast<const float4*>(b.dmean + static_cast<std::size_t>(row) * b.ld_dmean + f);
-        s.x += v.x;
-        s.y += v.y;
-        s.z += v.z;
-        s.w += v.w;
-      }
-      *reinterpret_cast<float4*>(a.dh + static_cast<std::size_t>(c) * a.ld_dh + f) = s;
-    }
-  }
-}
-
-}  // namespace
-
-void csc_build(const CscArgs& a, std::uint32_t* partials, cudaStream_t st) {
-  HG_CUDA(cudaMemsetAsync(a.offs, 0, sizeof(std::uint32_t) * (a.src_cap + 1), st));
-  HG_CUDA(cudaMemsetAsync(a.cursor, 0, sizeof(std::uint32_t) * (a.src_cap + 1), st));
-  int cap = 1;
-  for (int i = 0; i < a.nblk; ++i) cap = std::max(cap, a.b[i].cap);
-  dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, 256), 4 * kNumSMs)), a.nblk);
-  k_csc_count<<<grid, 256, 0, st>>>(a);
-  ScanArgs sa{};
-  sa.nseg = 1;
-  sa.s[0] = {a.offs, a.n_src, a.src_cap};
-  scan_inclusive(sa, partials, st);
-  k_csc_fill<<<grid, 256, 0, st>>>(a);
-  const unsigned g2 = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
-                                                                          ceil_div(a.src_cap, 256), 4 * kNumSMs)));
-  k_csc_sort<<<g2, 256, 0, st>>>(a);
-}
-
-void csc_gather(const CscArgs& a, cudaStream_t st) {
-  const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(
-      1, std::min<std::uint64_t>(ceil_div(a.src_cap, 8), 8 * kNumSMs)));
-  k_csc_gather<<<grid, 256, 0, st>>>(a);
-}
-
-// ---- Adam ---------------------------------------------------------------------------------------
-
-namespace {
-
 __device__ __forceinline__ void adam4(float4& w, float4& m, float4& v, const float4 g, double bc1, double bc2,
                                       const AdamHyper& hp, std::uint32_t* err) {
   // moments and update in f64 like the reference (hgnn.cpp:364-377); fp32 storage
@@ -191,6 +100,115 @@ __device__ __forceinline__ void adam4(float4& w, float4& m, float4& v, const flo
     wp[j] = static_cast<float>(wp[j] - hp.lr * (md / bc1) / (sqrt(vd / bc2) + hp.eps));
   }
 }
+
+
+__global__ void k_csc_fill(CscHop h) {
+  const CscEdges& b = h.b[blockIdx.y];
+  const CscType& t = h.t[b.type];
+  const std::uint32_t total = b.indptr[*b.n_rows];
+  for (std::uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const std::uint32_t c = b.col[e];
+    const std::uint32_t pos = atomicAdd(t.cursor + c, 1u);
+    t.entries[t.offs[c] - 1 - pos] = static_cast<std::uint32_t>(b.edge_base) + e;
+  }
+}
+
+// make every segment ascending in (block, edge): deterministic summation order
+__global__ void k_csc_sort(CscHop h) {
+  const CscType& t = h.t[blockIdx.y];
+  const int n = *t.n_src;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+    const std::uint32_t lo = c ? t.offs[c - 1] : 0u, hi = t.offs[c];
+    for (std::uint32_t x = lo + 1; x < hi; ++x) {
+      const std::uint32_t v = t.entries[x];
+      std::uint32_t y = x;
+      while (y > lo && t.entries[y - 1] > v) {
+        t.entries[y] = t.entries[y - 1];
+        --y;
+      }
+      t.entries[y] = v;
+    }
+  }
+}
+
+// one half-warp per (source row, 64-column chunk): ordered sum of the dmean rows
+// of its sampled edges; learnable leaves apply Adam to their table row directly
+__global__ void __launch_bounds__(256) k_csc_gather(CscHop h, AdamHyper hp, std::uint32_t* err) {
+  __shared__ double bc[kMaxSegs][2];
+  if (threadIdx.x < h.nt) {
+    const CscType& t = h.t[threadIdx.x];
+    const double st = t.step ? static_cast<double>(*t.step) : 1.0;
+    bc[threadIdx.x][0] = 1.0 - pow(hp.beta1, st);
+    bc[threadIdx.x][1] = 1.0 - pow(hp.beta2, st);
+  }
+  __syncthreads();
+  const int hl = threadIdx.x & 15;
+  const int halves = gridDim.x * (blockDim.x >> 4);
+  for (int ty = 0; ty < h.nt; ++ty) {
+    const CscType& t = h.t[ty];
+    const int n = *t.n_src;
+    const int nch = (t.din + 63) / 64;
+    for (int item = blockIdx.x * (blockDim.x >> 4) + (threadIdx.x >> 4); item < n * nch; item += halves) {
+      const int c = item / nch;
+      const int f = (item % nch) * 64 + 4 * hl;
+      if (f >= t.ld_dh) continue;
+      const std::uint32_t lo = c ? t.offs[c - 1] : 0u, hi = t.offs[c];
+      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (std::uint32_t x = lo; x < hi; ++x) {
+        const std::uint32_t id = t.entries[x];
+        int bi = 0;
+        while (bi + 1 < h.nb && id >= static_cast<std::uint32_t>(h.b[bi + 1].edge_base)) ++bi;
+        const CscEdges& b = h.b[bi];
+        const std::uint32_t row = b.erow[id - b.edge_base];
+        const float4 v = *reinterpret_cast<const float4*>(b.dmean + static_cast<std::size_t>(row) * b.ld_dmean + f);
+        s.x += v.x;
+        s.y += v.y;
+        s.z += v.z;
+        s.w += v.w;
+      }
+      if (t.dh) *reinterpret_cast<float4*>(t.dh + static_cast<std::size_t>(c) * t.ld_dh + f) = s;
+      if (t.w) {
+        const std::size_t at = static_cast<std::size_t>(t.ids[c]) * t.ld_w + f;
+        float4 w = *reinterpret_cast<float4*>(t.w + at);
+        float4 m = *reinterpret_cast<float4*>(t.m + at);
+        float4 v = *reinterpret_cast<float4*>(t.v + at);
+        adam4(w, m, v, s, bc[ty][0], bc[ty][1], hp, err);
+        *reinterpret_cast<float4*>(t.w + at) = w;
+        *reinterpret_cast<float4*>(t.m + at) = m;
+        *reinterpret_cast<float4*>(t.v + at) = v;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+void csc_prepare(const CscHop& h, std::uint32_t* partials, cudaStream_t st) {
+  if (h.nt == 0) return;
+  ScanArgs sa{};
+  sa.nseg = h.nt;
+  for (int i = 0; i < h.nt; ++i) sa.s[i] = {h.t[i].offs, h.t[i].n_src, h.t[i].src_cap};
+  scan_inclusive(sa, partials, st);
+  int cap = 1, scap = 1;
+  for (int i = 0; i < h.nb; ++i) cap = std::max(cap, h.b[i].cap);
+  for (int i = 0; i < h.nt; ++i) scap = std::max(scap, h.t[i].src_cap);
+  dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, 256), 4 * kNumSMs)), h.nb);
+  k_csc_fill<<<grid, 256, 0, st>>>(h);
+  dim3 g2(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(scap, 256), 4 * kNumSMs)), h.nt);
+  k_csc_sort<<<g2, 256, 0, st>>>(h);
+}
+
+void csc_gather(const CscHop& h, AdamHyper hp, std::uint32_t* err, cudaStream_t st) {
+  if (h.nt == 0) return;
+  int items = 0;
+  for (int i = 0; i < h.nt; ++i) items += h.t[i].src_cap * static_cast<int>(ceil_div(h.t[i].din, 64));
+  const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(items, 16), 16 * kNumSMs)));
+  k_csc_gather<<<grid, 256, 0, st>>>(h, hp, err);
+}
+
+// ---- Adam ---------------------------------------------------------------------------------------
+
+namespace {
 
 // every model slot in one launch: flat [rows x ld] arrays (padding is zero
 // in w, m, v and g, so updating it is a no-op)
@@ -261,6 +279,29 @@ __global__ void k_zero_rows(float* p, int ld, const int* n_rows) {
 }
 
 }  // namespace
+
+namespace {
+struct BumpArgs {
+  std::int64_t* step[kMaxSegs];
+  const int* n[kMaxSegs];
+  int count;
+};
+__global__ void k_bump_list(BumpArgs a) {
+  const int t = threadIdx.x;
+  if (t < a.count && *a.n[t] > 0) ++*a.step[t];
+}
+}  // namespace
+
+void bump_steps(const std::int64_t* const* steps, const int* const* counts, int n, cudaStream_t st) {
+  if (n == 0) return;
+  BumpArgs a{};
+  for (int i = 0; i < n && i < kMaxSegs; ++i) {
+    a.step[i] = const_cast<std::int64_t*>(steps[i]);
+    a.n[i] = counts[i];
+  }
+  a.count = n;
+  k_bump_list<<<1, 32, 0, st>>>(a);
+}
 
 void adam_model(AdamModelBatch& b, const std::int64_t* step, AdamHyper hp, std::uint32_t* err, cudaStream_t st) {
   if (b.n == 0) return;

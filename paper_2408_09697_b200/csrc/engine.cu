@@ -416,9 +416,26 @@ void Engine::upload(const Graph& g) {
       gr.out = static_cast<float*>(alloc(static_cast<std::size_t>(std::max(1, gr.rows_cap)) * gr.ld * 4));
     }
   }
+  // transposed views: per hop one contiguous offs/cursor region (one memset each)
+  csc_region_.assign(o_.k + 1, {nullptr, nullptr, 0});
+  for (int h = 1; h <= o_.k; ++h) {
+    std::size_t words = 0;
+    for (const auto& c : cscs_)
+      if (c.hop == h) words += static_cast<std::size_t>(c.src_cap) + 1;
+    if (!words) continue;
+    auto& reg = csc_region_[h];
+    reg.words = words;
+    reg.offs = static_cast<std::uint32_t*>(alloc(words * 4));
+    reg.cursor = static_cast<std::uint32_t*>(alloc(words * 4));
+    std::size_t at = 0;
+    for (auto& c : cscs_) {
+      if (c.hop != h) continue;
+      c.offs = reg.offs + at;
+      c.cursor = reg.cursor + at;
+      at += static_cast<std::size_t>(c.src_cap) + 1;
+    }
+  }
   for (auto& c : cscs_) {
-    c.offs = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(c.src_cap + 1) * 4));
-    c.cursor = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(c.src_cap + 1) * 4));
     std::size_t ent = 0;
     for (int bi : c.blocks) ent = std::max<std::size_t>(ent, blocks_[bi].edge_base + blocks_[bi].edge_cap);
     c.entries = static_cast<std::uint32_t*>(alloc(ent * 4));
@@ -572,14 +589,25 @@ void Engine::run_sampling() {
     for (int q = 0; q < sh.nblk; ++q) {
       const BlockBuf& b = blocks_[hop_blocks_[h][q]];
       ma.s[ma.nsrc++] = {b.src, b.indptr, sh.b[q].n_rows, b.edge_cap, slot_of_type[b.src_t]};
-      ra.b[ra.nblk++] = {b.src, b.indptr, sh.b[q].n_rows, b.col, b.edge_cap, slot_of_type[b.src_t]};
+      std::uint32_t* cnt = nullptr;
+      if (b.need_src_grad)
+        for (const auto& c : cscs_)
+          if (c.hop == h && c.src_t == b.src_t) cnt = c.offs;
+      ra.b[ra.nblk++] = {b.src, b.indptr, sh.b[q].n_rows, b.col, b.edge_cap, slot_of_type[b.src_t], cnt};
     }
     HG_CUDA(cudaMemsetAsync(bits_, 0, static_cast<std::size_t>(total_words_) * 4, st_));
+    if (csc_region_[h].words) {
+      HG_CUDA(cudaMemsetAsync(csc_region_[h].offs, 0, csc_region_[h].words * 4, st_));
+      HG_CUDA(cudaMemsetAsync(csc_region_[h].cursor, 0, csc_region_[h].words * 4, st_));
+    }
     timed("frontier", 0, [&] {
       frontier_mark(ma, fa, st_);
       frontier_compact(fa, words_dev_ + h * kMaxSegs, scan_partials_, st_);
       frontier_relabel(ra, fa, st_);
     });
+    // transposed views of this hop (independent of the forward values)
+    const CscHop ch = csc_hop(h);
+    timed("csc_build", 0, [&] { csc_prepare(ch, scan_partials_, st_); });
   }
   EdgeCountArgs ec{};
   for (const auto& b : blocks_) {
@@ -597,13 +625,6 @@ void Engine::run_sampling() {
       ab.cls[ab.nblk] = b.hop == 1 ? 2 : 1;
       ++ab.nblk;
     }
-    for (const auto& gr : groups_) {
-      if (gr.blocks.empty() || ab.ngrp >= kMaxBlocks * 4) continue;
-      ab.g_rows[ab.ngrp] = (gr.layer == o_.k && replica_) ? shard_count_dev_ : front(gr.depth - 1, gr.type).count;
-      ab.g_dout[ab.ngrp] = gr.dout;
-      ab.g_cls[ab.ngrp] = gr.layer == o_.k ? 2 : 1;
-      ++ab.ngrp;
-    }
     k_alg_bytes<<<1, 32, 0, st_>>>(ab, alg_bytes_);
   }
   // cache lookups + updates over the layer-0 frontier (harness.cpp:425-437)
@@ -618,50 +639,62 @@ void Engine::run_forward() {
   const int k = o_.k;
   // AGG_all buffer: rows beyond the live batch and the counter row stay zero
   HG_CUDA(cudaMemsetAsync(logits_, 0, static_cast<std::size_t>(o_.batch_cap + 1) * ldc_ * 4, st_));
-  for (const auto& gr : groups_) {
-    AggGroup ag{};
-    ag.nrel = static_cast<int>(gr.blocks.size());
-    const bool top = gr.layer == k;
-    ag.n_rows = (top && replica_) ? shard_count_dev_ : front(gr.depth - 1, gr.type).count;
-    ag.rows_cap = top && replica_ ? static_cast<int>(ceil_div(o_.batch_cap, shard_count_)) : gr.rows_cap;
-    ag.out = gr.out;
-    ag.ld_out = gr.ld;
-    ag.dout = gr.dout;
-    ag.relu = gr.layer < k ? 1 : 0;
-    ag.out_stride = top ? shard_count_ : 1;
-    ag.out_offset = top ? shard_index_ : 0;
+  for (int l = 1; l <= k; ++l) {
+    const int d = k - l + 1;
+    const bool top = l == k;
+    // (1) relation-first mean aggregation of every block of hop d: one launch;
+    // layer 1 reads the feature / learnable tables by global id (fused gather)
+    MeanBatch mb{};
     double bytes = 0;
-    for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
-      const BlockBuf& b = blocks_[gr.blocks[q]];
-      const Slot& s = slots_[gr.slots[q]];
-      AggRel& r = ag.r[q];
-      r.indptr = b.indptr;
-      r.src = b.src;
-      r.col = b.col;
+    for (int bi : hop_blocks_[d]) {
+      const BlockBuf& b = blocks_[bi];
+      MeanBlock& m = mb.b[mb.nb++];
+      m.indptr = b.indptr;
       if (b.hop == k) {
-        r.h = tables_[b.src_t].w;
-        r.ld_h = tables_[b.src_t].ld;
-        r.by_id = 1;
+        m.keys = b.src;
+        m.h = tables_[b.src_t].w;
+        m.ld_h = tables_[b.src_t].ld;
       } else {
         const Group* sg = nullptr;
         for (const auto& g2 : groups_)
           if (g2.depth - 1 == b.hop && g2.type == b.src_t) sg = &g2;
-        r.h = sg->out;
-        r.ld_h = sg->ld;
-        r.by_id = 0;
+        m.keys = b.col;
+        m.h = sg->out;
+        m.ld_h = sg->ld;
       }
-      r.din = b.din;
-      r.w = s.w;
-      r.ld_w = s.ld;
-      r.mean = b.mean;
-      r.ld_mean = b.ld_mean;
+      m.din = b.din;
+      m.n_rows = b.hop == 1 ? (replica_ ? shard_count_dev_ : front(0, target_).count) : front(b.hop - 1, b.dst_t).count;
+      m.rows_cap = b.rows_cap;
+      m.mean = b.mean;
+      m.ld_mean = b.ld_mean;
     }
-    if (gr.blocks.empty() && !top) {
-      // no relation into this type at this depth: zero embedding
-      zero_rows(gr.out, gr.ld, front(gr.depth - 1, gr.type).count, gr.rows_cap, st_);
-      continue;
+    timed(top ? "aggregate_top" : "aggregate", bytes, [&] { gather_mean(mb, st_); });
+    // (2) per-relation projection summed over the relations into each type (agg_all)
+    ProjBatch pb{};
+    for (const auto& gr : groups_) {
+      if (gr.layer != l) continue;
+      if (gr.blocks.empty()) {
+        if (!top) zero_rows(gr.out, gr.ld, front(gr.depth - 1, gr.type).count, gr.rows_cap, st_);
+        continue;
+      }
+      if (pb.ng >= 4 || gr.blocks.size() > 8) throw std::runtime_error("projection batch too large");
+      ProjGroup& pg = pb.g[pb.ng++];
+      pg.nrel = static_cast<int>(gr.blocks.size());
+      pg.n_rows = (top && replica_) ? shard_count_dev_ : front(gr.depth - 1, gr.type).count;
+      pg.rows_cap = top && replica_ ? static_cast<int>(ceil_div(o_.batch_cap, shard_count_)) : gr.rows_cap;
+      pg.out = gr.out;
+      pg.ld_out = gr.ld;
+      pg.dout = gr.dout;
+      pg.relu = top ? 0 : 1;
+      pg.out_stride = top ? shard_count_ : 1;
+      pg.out_offset = top ? shard_index_ : 0;
+      for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
+        const BlockBuf& b = blocks_[gr.blocks[q]];
+        const Slot& s = slots_[gr.slots[q]];
+        pg.r[q] = {b.mean, b.ld_mean, b.din, s.w, s.ld};
+      }
     }
-    timed(top ? "aggregate_top" : "aggregate", bytes, [&] { agg_tiles(ag, st_); });
+    timed(top ? "project_top" : "project", 0, [&] { project_tiles(pb, st_); });
   }
   // AGG_all: sum the partial logits of every partition (raf.cpp:427-446)
   if (o_.p > 1) {
@@ -704,24 +737,16 @@ void Engine::run_loss() {
 
 void Engine::run_backward() {
   const int k = o_.k;
-  // transposed views of the blocks whose sources need gradients
-  for (auto& c : cscs_) {
-    CscArgs a{};
-    for (int bi : c.blocks) {
-      const BlockBuf& b = blocks_[bi];
-      a.b[a.nblk++] = {b.col, b.erow, b.indptr, b.hop == 1 ? (replica_ ? shard_count_dev_ : front(0, target_).count)
-                                                              : front(b.hop - 1, b.dst_t).count,
-                       b.edge_cap, b.edge_base, b.dmean, b.ld_mean};
-    }
-    a.n_src = front(c.hop, c.src_t).count;
-    a.src_cap = c.src_cap;
-    a.offs = c.offs;
-    a.cursor = c.cursor;
-    a.entries = c.entries;
-    a.dh = c.dh;
-    a.ld_dh = c.ld;
-    a.din = c.din;
-    timed("csc_build", 0, [&] { csc_build(a, scan_partials_, st_); });
+  // learnable layer-0 tables advance their Adam step before the fused row update
+  {
+    std::vector<const std::int64_t*> steps;
+    std::vector<const int*> counts;
+    for (const auto& c : cscs_)
+      if (c.hop == k && tables_[c.src_t].learnable) {
+        steps.push_back(tables_[c.src_t].step);
+        counts.push_back(front(k, c.src_t).count);
+      }
+    bump_steps(steps.data(), counts.data(), static_cast<int>(steps.size()), st_);
   }
   for (auto& s : slots_) HG_CUDA(cudaMemsetAsync(s.g, 0, static_cast<std::size_t>(std::max(1, s.din)) * s.ld * 4, st_));
 
@@ -750,24 +775,55 @@ void Engine::run_backward() {
     }
     timed("weight_grad", 0, [&] { wgrad_tiles(wb, st_); });
     timed("mean_grad", 0, [&] { dmean_tiles(db, st_); });
-    // scatter back to the sources of this hop, as ordered gathers
-    for (auto& c : cscs_) {
-      if (c.hop != d) continue;
-      CscArgs a{};
-      for (int bi : c.blocks) {
-        const BlockBuf& b = blocks_[bi];
-        a.b[a.nblk++] = {b.col, b.erow, b.indptr, nullptr, b.edge_cap, b.edge_base, b.dmean, b.ld_mean};
-      }
-      a.n_src = front(c.hop, c.src_t).count;
-      a.src_cap = c.src_cap;
-      a.offs = c.offs;
-      a.entries = c.entries;
-      a.dh = c.dh;
-      a.ld_dh = c.ld;
-      a.din = c.din;
-      timed("csc_gather", 0, [&] { csc_gather(a, st_); });
+    // scatter back to the sources of this hop, as ordered gathers (learnable
+    // layer-0 rows get their Adam update in the same pass)
+    const CscHop ch = csc_hop(d);
+    AdamHyper hp;
+    timed("csc_gather", 0, [&] { csc_gather(ch, hp, err_, st_); });
+  }
+}
+
+CscHop Engine::csc_hop(int h) {
+  CscHop ch{};
+  std::vector<int> slot(ntypes_, -1);
+  for (const auto& c : cscs_) {
+    if (c.hop != h) continue;
+    slot[c.src_t] = ch.nt;
+    CscType& t = ch.t[ch.nt++];
+    t.offs = c.offs;
+    t.cursor = c.cursor;
+    t.entries = c.entries;
+    t.n_src = front(h, c.src_t).count;
+    t.src_cap = c.src_cap;
+    const bool leaf_learnable = h == o_.k && tables_[c.src_t].learnable;
+    t.dh = (!leaf_learnable || retain_grads_) ? c.dh : nullptr;
+    t.ld_dh = c.ld;
+    t.din = c.din;
+    if (leaf_learnable) {
+      const TypeTable& tb = tables_[c.src_t];
+      t.w = tb.w;
+      t.m = tb.m;
+      t.v = tb.v;
+      t.ld_w = tb.ld;
+      t.ids = front(h, c.src_t).list;
+      t.step = tb.step;
     }
   }
+  for (int bi : hop_blocks_[h]) {
+    const BlockBuf& b = blocks_[bi];
+    if (!b.need_src_grad || slot[b.src_t] < 0) continue;
+    CscEdges& e = ch.b[ch.nb++];
+    e.col = b.col;
+    e.erow = b.erow;
+    e.indptr = b.indptr;
+    e.n_rows = b.hop == 1 ? (replica_ ? shard_count_dev_ : front(0, target_).count) : front(b.hop - 1, b.dst_t).count;
+    e.cap = b.edge_cap;
+    e.edge_base = b.edge_base;
+    e.type = slot[b.src_t];
+    e.dmean = b.dmean;
+    e.ld_dmean = b.ld_mean;
+  }
+  return ch;
 }
 
 void Engine::run_update() {
@@ -785,23 +841,7 @@ void Engine::run_update() {
     ++mb.n;
   }
   mb.total4 = base;
-  AdamRowsBatch rb{};
-  base = 0;
-  for (const auto& c : cscs_) {
-    if (c.hop != o_.k) continue;
-    TypeTable& tb = tables_[c.src_t];
-    if (!tb.learnable) continue;
-    const Front& f = front(o_.k, c.src_t);
-    rb.t[rb.n] = {tb.w, tb.m, tb.v, tb.ld, f.list, c.dh, c.ld, f.count, tb.step};
-    rb.base4[rb.n] = base;
-    base += f.cap * tb.ld / 4;
-    ++rb.n;
-  }
-  rb.total4 = base;
-  timed("adam", 0, [&] {
-    adam_model(mb, &d_sc_->model_step, hp, err_, st_);
-    adam_rows(rb, hp, err_, st_);
-  });
+  timed("adam", 0, [&] { adam_model(mb, &d_sc_->model_step, hp, err_, st_); });
 }
 
 StepScalars Engine::next_scalars(std::uint64_t rng_seed, int n, int designated, bool train) {

@@ -75,6 +75,14 @@ class Engine {
   void enqueue_step_device(const StepScalars* d_src, const std::uint32_t* d_ids, int n, bool train);
   StepScalars next_scalars(std::uint64_t rng_seed, int n, int designated, bool train);
   void set_graphs(bool on) { use_graphs_ = on; }
+  // keep the learnable-row gradients in memory (grad.f.* tensors); the bench
+  // turns this off so the sparse Adam update consumes them in registers
+  void set_retain_grads(bool on) {
+    if (on != retain_grads_) {
+      retain_grads_ = on;
+      drop_graphs();
+    }
+  }
   StepReport finish_step();
   // Sampling only (parity of the sampler; presample_hotness).
   void sample_only(const NodeId* batch, int n, std::uint64_t rng_seed);
@@ -256,6 +264,18 @@ class Engine {
   void step_body(bool train);
   void launch_body(bool train);
   bool use_graphs_ = true;
+  bool retain_grads_ = true;
+  struct CscRegion {
+    std::uint32_t *offs, *cursor;
+    std::size_t words;
+  };
+  std::vector<CscRegion> csc_region_;
+  CscHop csc_hop(int h);
+  void drop_graphs() {
+    if (exec_train_) cudaGraphExecDestroy(exec_train_);
+    if (exec_eval_) cudaGraphExecDestroy(exec_eval_);
+    exec_train_ = exec_eval_ = nullptr;
+  }
   cudaGraphExec_t exec_train_ = nullptr, exec_eval_ = nullptr;
   std::map<std::string, double> kernel_ms_, kernel_bytes_;
   std::map<std::string, int> kernel_launches_;

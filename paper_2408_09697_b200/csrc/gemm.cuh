@@ -53,6 +53,50 @@ struct DMeanBatch {
 };
 
 void agg_tiles(const AggGroup& g, cudaStream_t st);
+
+// ---- split forward: gather-mean of every block of a hop, then projection ------------------
+struct MeanBlock {
+  const std::uint32_t* indptr;
+  const std::uint32_t* keys;  // global ids (by_id) or frontier rows
+  const float* h;
+  int ld_h;
+  int din;
+  const int* n_rows;
+  int rows_cap;
+  float* mean;
+  int ld_mean;
+};
+struct MeanBatch {
+  MeanBlock b[kMaxBlocks];
+  int item_base[kMaxBlocks + 1];  // prefix of rows_cap * ceil(din/64)
+  int nb;
+};
+void gather_mean(MeanBatch& m, cudaStream_t st);
+
+struct ProjRel {
+  const float* mean;
+  int ld_mean;
+  int din;
+  const float* w;
+  int ld_w;
+};
+struct ProjGroup {
+  ProjRel r[8];
+  int nrel;
+  const int* n_rows;
+  int rows_cap;
+  float* out;
+  int ld_out;
+  int dout;
+  int relu;
+  int out_stride, out_offset;
+};
+struct ProjBatch {
+  ProjGroup g[4];
+  int tile_base[5];
+  int ng;
+};
+void project_tiles(ProjBatch& p, cudaStream_t st);
 void wgrad_tiles(WGradBatch& b, cudaStream_t st);
 void dmean_tiles(DMeanBatch& b, cudaStream_t st);
 

@@ -277,7 +277,139 @@ __global__ void __launch_bounds__(kT) k_dmean_tiles(DMeanBatch b) {
   }
 }
 
+// ---- gather-mean: one warp per (row, 128-column chunk), 8 edges in flight ----------------
+__global__ void __launch_bounds__(256) k_gather_mean(MeanBatch m) {
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); item < m.item_base[m.nb]; item += warps) {
+    int b = 0;
+    while (b + 1 < m.nb && item >= m.item_base[b + 1]) ++b;
+    const MeanBlock& B = m.b[b];
+    const int nch = (B.din + 127) / 128;
+    const int local = item - m.item_base[b];
+    const int i = local / nch, c = (local % nch) * 128 + 4 * lane;
+    if (i >= *B.n_rows || c >= B.ld_mean) continue;
+    const std::uint32_t lo = B.indptr[i], hi = B.indptr[i + 1];
+    const float* base = B.h + c;
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    std::uint32_t e = lo;
+    for (; e + 8 <= hi; e += 8) {
+      std::uint32_t kk[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) kk[q] = __ldg(B.keys + e + q);
+      float4 v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = __ldg(reinterpret_cast<const float4*>(base + static_cast<std::size_t>(kk[q]) * B.ld_h));
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        s.x += v[q].x;
+        s.y += v[q].y;
+        s.z += v[q].z;
+        s.w += v[q].w;
+      }
+    }
+    for (; e < hi; ++e) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(base + static_cast<std::size_t>(__ldg(B.keys + e)) * B.ld_h));
+      s.x += v.x;
+      s.y += v.y;
+      s.z += v.z;
+      s.w += v.w;
+    }
+    if (hi > lo) {
+      const float inv = 1.0f / static_cast<float>(hi - lo);
+      s.x *= inv;
+      s.y *= inv;
+      s.z *= inv;
+      s.w *= inv;
+    }
+    *reinterpret_cast<float4*>(B.mean + static_cast<std::size_t>(i) * B.ld_mean + c) = s;
+  }
+}
+
+// ---- projection: out = sum_r mean_r . W_r (agg_all over relations), ReLU ------------------
+__global__ void __launch_bounds__(kT) k_project_tiles(ProjBatch pb) {
+  __shared__ __align__(16) float As[kKS * kLd];
+  __shared__ __align__(16) float Bs[kKS * kLd];
+  const int gi = find_problem(pb.tile_base, pb.ng, blockIdx.x);
+  const ProjGroup& g = pb.g[gi];
+  const int t = blockIdx.x - pb.tile_base[gi];
+  const int ncb = (g.dout + kTile - 1) / kTile;
+  const int rb = t / ncb, cb = t % ncb;
+  const int n = *g.n_rows;
+  const int row0 = rb * kTile, col0 = cb * kTile;
+  if (row0 >= n) return;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  Acc acc;
+  acc.zero();
+  for (int q = 0; q < g.nrel; ++q) {
+    const ProjRel& r = g.r[q];
+    for (int k0 = 0; k0 < r.din; k0 += kKS) {
+      const int kn = min(kKS, r.din - k0);
+      __syncthreads();
+      for (int x = tid; x < kTile * kKS / 4; x += kT) {
+        const int m = x / (kKS / 4), kq = (x % (kKS / 4)) * 4;
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row0 + m < n && kq < kn)
+          a = *reinterpret_cast<const float4*>(r.mean + static_cast<std::size_t>(row0 + m) * r.ld_mean + k0 + kq);
+        As[(kq + 0) * kLd + m] = a.x;
+        As[(kq + 1) * kLd + m] = a.y;
+        As[(kq + 2) * kLd + m] = a.z;
+        As[(kq + 3) * kLd + m] = a.w;
+      }
+      for (int x = tid; x < kKS * kTile / 4; x += kT) {
+        const int k = x / (kTile / 4), nq = (x % (kTile / 4)) * 4;
+        float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (k < kn && col0 + nq < g.dout)
+          w = __ldg(reinterpret_cast<const float4*>(r.w + static_cast<std::size_t>(k0 + k) * r.ld_w + col0 + nq));
+        *reinterpret_cast<float4*>(Bs + k * kLd + nq) = w;
+      }
+      __syncthreads();
+      slab_fma(As, Bs, kn, ty, tx, acc);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = row0 + ty * 4 + i;
+    if (row >= n) break;
+    float* orow = g.out + static_cast<std::size_t>(row * g.out_stride + g.out_offset) * g.ld_out;
+    const int c = col0 + tx * 4;
+    if (c < g.dout) {
+      float4 o = make_float4(acc.v[i][0], acc.v[i][1], acc.v[i][2], acc.v[i][3]);
+      if (g.relu) {
+        o.x = fmaxf(o.x, 0.f);
+        o.y = fmaxf(o.y, 0.f);
+        o.z = fmaxf(o.z, 0.f);
+        o.w = fmaxf(o.w, 0.f);
+      }
+      *reinterpret_cast<float4*>(orow + c) = o;
+    }
+  }
+}
+
 }  // namespace
+
+void gather_mean(MeanBatch& m, cudaStream_t st) {
+  if (m.nb == 0) return;
+  int items = 0;
+  for (int b = 0; b < m.nb; ++b) {
+    m.item_base[b] = items;
+    items += m.b[b].rows_cap * static_cast<int>(ceil_div(m.b[b].din, 128));
+  }
+  m.item_base[m.nb] = items;
+  const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(items, 8), 16 * kNumSMs)));
+  k_gather_mean<<<grid, 256, 0, st>>>(m);
+}
+
+void project_tiles(ProjBatch& p, cudaStream_t st) {
+  if (p.ng == 0) return;
+  int tiles = 0;
+  for (int g = 0; g < p.ng; ++g) {
+    p.tile_base[g] = tiles;
+    tiles += static_cast<int>(ceil_div(std::max(1, p.g[g].rows_cap), kTile) * ceil_div(p.g[g].dout, kTile));
+  }
+  p.tile_base[p.ng] = tiles;
+  k_project_tiles<<<std::max(1, tiles), kT, 0, st>>>(p);
+}
 
 void agg_tiles(const AggGroup& g, cudaStream_t st) {
   const int ncb = static_cast<int>(ceil_div(g.dout, kTile));

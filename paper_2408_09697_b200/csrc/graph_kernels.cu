@@ -330,8 +330,11 @@ __global__ void __launch_bounds__(kFrontThreads) k_relabel(RelabelArgs r, Fronti
   const RelabelBlock& b = r.b[blockIdx.y];
   const std::uint32_t total = b.indptr[*b.n_rows];
   const BitmapType& t = f.t[b.slot];
-  for (std::uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x)
-    b.col[e] = bitmap_rank(t, b.ids[e]);
+  for (std::uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const std::uint32_t c = bitmap_rank(t, b.ids[e]);
+    b.col[e] = c;
+    if (b.csc_count) atomicAdd(b.csc_count + c, 1u);
+  }
 }
 
 __global__ void __launch_bounds__(kFrontThreads) k_batch_mult(const std::uint32_t* ids, const StepScalars* sc,

@@ -104,6 +104,7 @@ struct RelabelBlock {
   std::uint32_t* col;
   int cap;
   int slot;
+  std::uint32_t* csc_count;  // optional: per-source-row edge counts for the transposed view
 };
 struct RelabelArgs {
   RelabelBlock b[kMaxBlocks];
@@ -161,32 +162,45 @@ struct LossArgs {
 void cross_entropy(const LossArgs& a, cudaStream_t st);
 
 // ---- backward ------------------------------------------------------------------------
-// transposed (src-major) view of a hop's blocks for one source type, used to
-// turn the backward scatter into an ordered gather (deterministic).
-struct CscBlock {
+// Transposed (src-major) view of one hop's blocks per source type: turns the
+// backward scatter (hgnn.cpp:344-353) into an ordered gather (deterministic).
+// Counts come from the relabel kernel; csc_prepare scans, fills and sorts
+// every segment by (block, edge); csc_gather sums dmean rows per source row and,
+// for learnable layer-0 types, applies the sparse Adam row update in place
+// (adam_update_rows, hgnn.cpp:392-410) without materialising the gradient.
+struct CscType {
+  std::uint32_t* offs;     // [src_cap + 1]: counts, then inclusive prefix
+  std::uint32_t* cursor;   // [src_cap]
+  std::uint32_t* entries;  // edge ids (edge_base + e) grouped by source row
+  const int* n_src;
+  int src_cap;
+  float* dh;               // gradient rows (nullptr: not materialised)
+  int ld_dh;
+  int din;
+  // fused Adam (learnable leaf types only; w == nullptr otherwise)
+  float *w, *m, *v;
+  int ld_w;
+  const std::uint32_t* ids;  // frontier[k][t]: global row of every source row
+  const std::int64_t* step;
+};
+struct CscEdges {
   const std::uint32_t* col;
   const std::uint32_t* erow;
   const std::uint32_t* indptr;
   const int* n_rows;
   int cap;
-  int edge_base;  // static offset of this block in the hop's edge id space
+  int edge_base;
+  int type;  // index into CscHop::t
   const float* dmean;
   int ld_dmean;
 };
-struct CscArgs {
-  CscBlock b[kMaxBlocks];
-  int nblk;
-  const int* n_src;      // live size of frontier[d][src_t]
-  int src_cap;
-  std::uint32_t* offs;   // [src_cap + 1]
-  std::uint32_t* cursor; // [src_cap]
-  std::uint32_t* entries;// [sum of caps]
-  float* dh;             // out [src rows x din]
-  int ld_dh;
-  int din;
+struct CscHop {
+  CscType t[kMaxSegs];
+  int nt;
+  CscEdges b[kMaxBlocks];
+  int nb;
 };
-void csc_build(const CscArgs& a, std::uint32_t* partials, cudaStream_t st);
-void csc_gather(const CscArgs& a, cudaStream_t st);
+void csc_prepare(const CscHop& h, std::uint32_t* partials, cudaStream_t st);
 
 // ---- optimizer ------------------------------------------------------------------------
 struct AdamHyper {  // hgnn.hpp:16-21
@@ -221,6 +235,10 @@ struct AdamRowsBatch {
   int total4;
 };
 void adam_rows(AdamRowsBatch& b, AdamHyper hp, std::uint32_t* err, cudaStream_t st);
+// gather (+ fused sparse Adam for learnable leaves) of every type of one hop
+void csc_gather(const CscHop& h, AdamHyper hp, std::uint32_t* err, cudaStream_t st);
+// per table: step += 1 iff it has gradient rows (hgnn.cpp:392-394)
+void bump_steps(const std::int64_t* const* steps, const int* const* counts, int n, cudaStream_t st);
 
 // ---- misc --------------------------------------------------------------------------------
 void zero_rows(float* p, int ld, const int* n_rows, int rows_cap, cudaStream_t st);

@@ -270,6 +270,9 @@ class Engine:
         N.check(N.lib().hg_engine_info(self._h, C.byref(pc), C.byref(db), C.byref(ms)))
         return dict(param_count=pc.value, device_bytes=db.value, model_step=ms.value)
 
+    def set_option(self, name: str, value) -> None:
+        N.check(N.lib().hg_engine_set_option(self._h, name.encode(), int(value)))
+
     def count_launches(self, n: int, train: bool = True) -> int:
         return N.check(N.lib().hg_engine_count_launches(self._h, n, int(train)))
 
