@@ -183,12 +183,12 @@ __global__ void __launch_bounds__(256) k_csc_gather(CscHop h, AdamHyper hp, std:
 
 }  // namespace
 
-void csc_prepare(const CscHop& h, std::uint32_t* partials, cudaStream_t st) {
+void csc_prepare(const CscHop& h, LbScratch& lb, cudaStream_t st) {
   if (h.nt == 0) return;
   ScanArgs sa{};
   sa.nseg = h.nt;
   for (int i = 0; i < h.nt; ++i) sa.s[i] = {h.t[i].offs, h.t[i].n_src, h.t[i].src_cap};
-  scan_inclusive(sa, partials, st);
+  scan_inclusive(sa, lb, st);
   int cap = 1, scap = 1;
   for (int i = 0; i < h.nb; ++i) cap = std::max(cap, h.b[i].cap);
   for (int i = 0; i < h.nt; ++i) scap = std::max(scap, h.t[i].src_cap);

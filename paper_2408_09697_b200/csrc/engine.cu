@@ -465,7 +465,18 @@ void Engine::upload(const Graph& g) {
 
   int max_cap = std::max(total_words_, max_rows);
   for (const auto& c : cscs_) max_cap = std::max(max_cap, c.src_cap + 1);
-  scan_partials_ = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(kMaxSegs) * (ceil_div(max_cap, kScanTile) + 1) * 4));
+  {
+    // look-back scratch: enough tiles for the largest single-pass launch
+    std::size_t tiles = ceil_div(total_words_, 1024) + kMaxSegs;
+    for (int h = 1; h <= o_.k; ++h) {
+      std::size_t t = 0;
+      for (int bi : hop_blocks_[h]) t += ceil_div(std::max(1, blocks_[bi].rows_cap), 256) + 1;
+      tiles = std::max(tiles, t);
+    }
+    tiles = std::max<std::size_t>(tiles, kMaxSegs * (ceil_div(max_cap, kScanTile) + 1));
+    lb_.cap = static_cast<int>(tiles);
+    lb_.mem = static_cast<unsigned long long*>(alloc((tiles + 1) * 8));
+  }
   slow_ = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(total_rows + 1) * 8));
   n_slow_ = static_cast<int*>(alloc(sizeof(int)));
   int maxf = 1;
@@ -539,7 +550,7 @@ void Engine::run_sampling() {
   HG_CUDA(cudaMemsetAsync(mult_, 0, static_cast<std::size_t>(o_.batch_cap) * 4, st_));
   timed("frontier", 0, [&] {
     frontier_mark_batch(d_batch_, d_sc_, o_.batch_cap, f0.t[0], st_);
-    frontier_compact(f0, words_dev_, scan_partials_, st_);
+    frontier_compact(f0, lb_, st_);
     batch_multiplicity(d_batch_, d_sc_, o_.batch_cap, f0.t[0], mult_, st_);
   });
   const std::uint32_t* hop1_rows = front(0, target_).list;
@@ -568,13 +579,7 @@ void Engine::run_sampling() {
       s.rel = b.rel;
       s.rows_cap = b.rows_cap;
     }
-    ScanArgs sa{};
-    for (int q = 0; q < sh.nblk; ++q) sa.s[sa.nseg++] = {sh.b[q].indptr + 1, sh.b[q].n_rows, sh.b[q].rows_cap};
-    timed("sample", 0, [&] {
-      sample_count(sh, st_);
-      scan_inclusive(sa, scan_partials_, st_);
-      sample_draw(sh, d_sc_, slow_, n_slow_, mt_scratch_, st_);
-    });
+    timed("sample", 0, [&] { sample_hop(sh, d_sc_, slow_, n_slow_, mt_scratch_, lb_, st_); });
 
     // frontier[h][t]: bitmap of every sampled source, compacted in id order
     FrontierArgs fa{};
@@ -602,12 +607,12 @@ void Engine::run_sampling() {
     }
     timed("frontier", 0, [&] {
       frontier_mark(ma, fa, st_);
-      frontier_compact(fa, words_dev_ + h * kMaxSegs, scan_partials_, st_);
+      frontier_compact(fa, lb_, st_);
       frontier_relabel(ra, fa, st_);
     });
     // transposed views of this hop (independent of the forward values)
     const CscHop ch = csc_hop(h);
-    timed("csc_build", 0, [&] { csc_prepare(ch, scan_partials_, st_); });
+    timed("csc_build", 0, [&] { csc_prepare(ch, lb_, st_); });
   }
   EdgeCountArgs ec{};
   for (const auto& b : blocks_) {

@@ -242,7 +242,7 @@ class Engine {
   unsigned long long* cache_hm_ = nullptr;  // [ntypes x 2]
 
   // scratch
-  std::uint32_t* scan_partials_ = nullptr;
+  LbScratch lb_;
   std::uint32_t* slow_ = nullptr;
   int* n_slow_ = nullptr;
   std::uint64_t* mt_scratch_ = nullptr;

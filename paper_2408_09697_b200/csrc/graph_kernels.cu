@@ -43,76 +43,97 @@ __device__ __forceinline__ std::uint32_t block_incl_scan(std::uint32_t v, std::u
   return x;
 }
 
-__global__ void __launch_bounds__(kScanThreads) scan_tile_sums(ScanArgs a, std::uint32_t* partials,
-                                                               int tiles_stride) {
-  const ScanSeg& s = a.s[blockIdx.y];
-  const int n = *s.n;
-  const int base = blockIdx.x * kScanTile;
-  if (base >= n) return;
-  std::uint32_t sum = 0;
-  for (int i = threadIdx.x; i < kScanTile; i += kScanThreads) {
-    const int idx = base + i;
-    if (idx < n) sum += s.data[idx];
-  }
-  std::uint32_t tot;
-  block_incl_scan<kScanThreads>(sum, &tot);
-  if (threadIdx.x == 0) partials[blockIdx.y * tiles_stride + blockIdx.x] = tot;
+// Decoupled look-back (single-pass prefix): tiles take dynamic ticket ids in
+// launch order, publish their aggregate, then walk back until a tile that has
+// published its inclusive prefix. Flag and value share one 64-bit word.
+constexpr unsigned long long kLbAgg = 1ull << 32, kLbPre = 2ull << 32;
+
+__device__ __forceinline__ unsigned long long lb_load(const unsigned long long* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
 }
 
-__global__ void __launch_bounds__(kScanThreads) scan_partials(ScanArgs a, std::uint32_t* partials,
-                                                              int tiles_stride) {
-  const ScanSeg& s = a.s[blockIdx.x];
-  const int n = *s.n;
-  const int tiles = (n + kScanTile - 1) / kScanTile;
-  std::uint32_t carry = 0;
-  std::uint32_t* p = partials + blockIdx.x * tiles_stride;
-  for (int b = 0; b < tiles; b += kScanThreads) {
-    const int i = b + threadIdx.x;
-    const std::uint32_t v = i < tiles ? p[i] : 0u;
-    std::uint32_t tot;
-    const std::uint32_t incl = block_incl_scan<kScanThreads>(v, &tot);
-    if (i < tiles) p[i] = carry + incl - v;  // exclusive tile prefix
-    carry += tot;
+// thread 0 only: exclusive prefix of tile t inside its segment state array
+__device__ __forceinline__ std::uint32_t lb_prefix(unsigned long long* st, int t, std::uint32_t agg) {
+  if (t == 0) {
+    atomicExch(st, kLbPre | agg);
+    return 0;
   }
+  atomicExch(st + t, kLbAgg | agg);
+  std::uint32_t excl = 0;
+  int j = t - 1;
+  while (true) {
+    const unsigned long long v = lb_load(st + j);
+    const unsigned long long flag = v >> 32;
+    if (flag == 0) continue;
+    excl += static_cast<std::uint32_t>(v);
+    if (flag == 2) break;
+    --j;
+  }
+  atomicExch(st + t, kLbPre | (excl + agg));
+  return excl;
 }
 
-__global__ void __launch_bounds__(kScanThreads) scan_apply(ScanArgs a, const std::uint32_t* partials,
-                                                           int tiles_stride) {
-  const ScanSeg& s = a.s[blockIdx.y];
-  const int n = *s.n;
-  const int base = blockIdx.x * kScanTile;
-  if (base >= n) return;
-  // each thread owns kScanPer consecutive elements
-  const int first = base + threadIdx.x * kScanPer;
+// ticket -> (segment, tile) over per-segment tile counts (tile_base prefix)
+__device__ __forceinline__ int seg_of(const int* base, int nseg, int ticket) {
+  int s = 0;
+  while (s + 1 < nseg && ticket >= base[s + 1]) ++s;
+  return s;
+}
+
+struct LbLayout {
+  int base[kMaxSegs + 1];  // per segment: first ticket / first state slot
+  int nseg;
+};
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_lb(ScanArgs a, LbLayout L, unsigned long long* state,
+                                                          int* ticket) {
+  __shared__ int s_tile;
+  __shared__ std::uint32_t s_prefix;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
+  __syncthreads();
+  const int tk = s_tile;
+  if (tk >= L.base[L.nseg]) return;
+  const int sg = seg_of(L.base, L.nseg, tk);
+  const int t = tk - L.base[sg];
+  const ScanSeg& S = a.s[sg];
+  const int n = *S.n;
+  const int first = t * kScanTile + threadIdx.x * kScanPer;
+  if (t * kScanTile >= n) return;  // beyond the live data: nobody waits on it
   std::uint32_t v[kScanPer];
   std::uint32_t local = 0;
 #pragma unroll
   for (int j = 0; j < kScanPer; ++j) {
     const int idx = first + j;
-    v[j] = idx < n ? s.data[idx] : 0u;
+    v[j] = idx < n ? S.data[idx] : 0u;
     local += v[j];
   }
-  std::uint32_t incl = block_incl_scan<kScanThreads>(local, nullptr);
-  std::uint32_t run = partials[blockIdx.y * tiles_stride + blockIdx.x] + incl - local;
+  std::uint32_t tot;
+  const std::uint32_t incl = block_incl_scan<kScanThreads>(local, &tot);
+  if (threadIdx.x == 0) s_prefix = lb_prefix(state + L.base[sg], t, tot);
+  __syncthreads();
+  std::uint32_t run = s_prefix + incl - local;
 #pragma unroll
   for (int j = 0; j < kScanPer; ++j) {
     const int idx = first + j;
     run += v[j];
-    if (idx < n) s.data[idx] = run;
+    if (idx < n) S.data[idx] = run;
   }
 }
 
 }  // namespace
 
-void scan_inclusive(const ScanArgs& a, std::uint32_t* partials, cudaStream_t st) {
+void scan_inclusive(const ScanArgs& a, LbScratch& lb, cudaStream_t st) {
   if (a.nseg == 0) return;
-  int max_cap = 1;
-  for (int i = 0; i < a.nseg; ++i) max_cap = max(max_cap, a.s[i].cap);
-  const int tiles = static_cast<int>(ceil_div(max_cap, kScanTile));
-  dim3 grid(tiles, a.nseg);
-  scan_tile_sums<<<grid, kScanThreads, 0, st>>>(a, partials, tiles);
-  scan_partials<<<a.nseg, kScanThreads, 0, st>>>(a, partials, tiles);
-  scan_apply<<<grid, kScanThreads, 0, st>>>(a, partials, tiles);
+  LbLayout L{};
+  L.nseg = a.nseg;
+  int tiles = 0;
+  for (int i = 0; i < a.nseg; ++i) {
+    L.base[i] = tiles;
+    tiles += static_cast<int>(ceil_div(std::max(1, a.s[i].cap), kScanTile));
+  }
+  L.base[a.nseg] = tiles;
+  lb.reset(tiles, st);
+  k_scan_lb<<<tiles, kScanThreads, 0, st>>>(a, L, lb.state, lb.ticket);
 }
 
 // ---- sampling -------------------------------------------------------------------------
@@ -120,25 +141,55 @@ void scan_inclusive(const ScanArgs& a, std::uint32_t* partials, cudaStream_t st)
 namespace {
 
 constexpr int kSampleThreads = 256;
-constexpr int kMapCap = 64;       // displaced-position map held in local memory
 constexpr int kSlowThreads = 4096;  // concurrent slow-path rows (global scratch)
-
-__global__ void __launch_bounds__(kSampleThreads) k_sample_count(SampleHop h) {
-  const SampleBlock& b = h.b[blockIdx.y];
-  const int n = *b.n_rows;
-  const std::uint64_t fo = static_cast<std::uint64_t>(h.fanout);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const std::uint32_t d = b.dst_list[i];
-    const std::uint64_t deg = b.csr_ptr[d + 1] - b.csr_ptr[d];
-    b.indptr[i + 1] = static_cast<std::uint32_t>(deg < fo ? deg : fo);
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) b.indptr[0] = 0;
-}
 
 // Partial Fisher-Yates over [0, deg) with a sparse map of displaced positions
 // (sampling.cpp:29-37 keeps a dense O(deg) index array). Position p holds p
 // unless overridden; position i is final once drawn, so only the j side needs
-// remembering. Returns false if a streaming engine ran dry (caller replays).
+// remembering. The map lives in registers (fully unrolled, MAXF entries).
+// Returns false if the streaming engine ran dry (caller replays on MtFull).
+template <int MAXF, typename Eng>
+__device__ __forceinline__ bool draw_row_reg(Eng& eng, std::uint64_t deg, int fanout, const std::uint32_t* nbr,
+                                             std::uint32_t* out) {
+  std::uint32_t mpos[MAXF], mval[MAXF];
+#pragma unroll
+  for (int q = 0; q < MAXF; ++q) {
+    mpos[q] = 0xffffffffu;
+    mval[q] = 0u;
+  }
+  int nmap = 0;
+  for (int i = 0; i < fanout; ++i) {
+    std::uint64_t off;
+    if (!lemire(eng, deg - static_cast<std::uint64_t>(i), off)) return false;
+    const std::uint32_t ii = static_cast<std::uint32_t>(i);
+    const std::uint32_t jpos = static_cast<std::uint32_t>(i + off);
+    std::uint32_t vi = ii, vj = jpos;
+    bool found = false;
+#pragma unroll
+    for (int q = 0; q < MAXF; ++q) {
+      if (mpos[q] == ii) vi = mval[q];
+      if (mpos[q] == jpos) {
+        vj = mval[q];
+        found = true;
+      }
+    }
+    if (jpos != ii) {
+#pragma unroll
+      for (int q = 0; q < MAXF; ++q) {
+        const bool hit = found ? mpos[q] == jpos : q == nmap;
+        if (hit) {
+          mpos[q] = jpos;
+          mval[q] = vi;
+        }
+      }
+      if (!found) ++nmap;
+    }
+    out[i] = nbr[vj];
+  }
+  return true;
+}
+
+// generic (memory-backed map) variant for the slow path
 template <typename Eng>
 __device__ bool draw_row(Eng& eng, std::uint64_t deg, int fanout, const std::uint32_t* nbr,
                          std::uint32_t* out, std::uint32_t* mpos, std::uint32_t* mval) {
@@ -169,59 +220,74 @@ __device__ bool draw_row(Eng& eng, std::uint64_t deg, int fanout, const std::uin
   return true;
 }
 
-__global__ void __launch_bounds__(kSampleThreads) k_sample_draw(SampleHop h, const StepScalars* sc,
-                                                                std::uint32_t* slow, int* n_slow) {
-  const SampleBlock& b = h.b[blockIdx.y];
+// One CTA = one tile of 256 rows of one block. Counts -> CTA scan -> look-back
+// for the tile's offset -> block offsets written -> copy-all rows (warp-
+// cooperative, coalesced) and RNG rows (one lane each, map in registers).
+template <int MAXF>
+__global__ void __launch_bounds__(kSampleThreads) k_sample_fused(SampleHop h, LbLayout L, const StepScalars* sc,
+                                                                 unsigned long long* state, int* ticket,
+                                                                 std::uint32_t* slow, int* n_slow) {
+  __shared__ int s_tile;
+  __shared__ std::uint32_t s_prefix;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
+  __syncthreads();
+  const int tk = s_tile;
+  if (tk >= L.base[L.nseg]) return;
+  const int bi = seg_of(L.base, L.nseg, tk);
+  const int t = tk - L.base[bi];
+  const SampleBlock& b = h.b[bi];
   const int n = *b.n_rows;
+  const int base = t * kSampleThreads;
+  if (base >= n) return;
+  const int i = base + threadIdx.x;
+  const bool live = i < n;
   const std::uint64_t fo = static_cast<std::uint64_t>(h.fanout);
-  const std::uint64_t rng_seed = sc->rng_seed;
-  const std::uint64_t rel_key = (static_cast<std::uint64_t>(h.hop) << 32) | static_cast<std::uint64_t>(b.rel);
+  std::uint32_t d = 0, cnt = 0;
+  std::uint64_t lo = 0, deg = 0;
+  if (live) {
+    d = b.dst_list[i];
+    lo = b.csr_ptr[d];
+    deg = b.csr_ptr[d + 1] - lo;
+    cnt = static_cast<std::uint32_t>(deg < fo ? deg : fo);
+  }
+  std::uint32_t tot;
+  const std::uint32_t incl = block_incl_scan<kSampleThreads>(cnt, &tot);
+  if (threadIdx.x == 0) s_prefix = lb_prefix(state + L.base[bi], t, tot);
+  __syncthreads();
+  const std::uint32_t o = s_prefix + incl - cnt;
+  if (live) b.indptr[i + 1] = o + cnt;
+  if (i == 0) b.indptr[0] = 0;
+
   const int lane = threadIdx.x & 31;
-  const int stride = gridDim.x * blockDim.x;
-  for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
-    const int i = base + threadIdx.x;
-    const bool live = i < n;
-    std::uint32_t d = 0, o = 0, cnt = 0;
-    std::uint64_t lo = 0, deg = 0;
-    if (live) {
-      d = b.dst_list[i];
-      lo = b.csr_ptr[d];
-      deg = b.csr_ptr[d + 1] - lo;
-      o = b.indptr[i];
-      cnt = b.indptr[i + 1] - o;
+  unsigned live_mask = __ballot_sync(0xffffffffu, live);
+  const unsigned copy_mask = __ballot_sync(0xffffffffu, live && deg <= fo);
+  while (live_mask) {
+    const int sl = __ffs(live_mask) - 1;
+    live_mask &= live_mask - 1;
+    const std::uint64_t rlo = __shfl_sync(0xffffffffu, lo, sl);
+    const std::uint32_t ro = __shfl_sync(0xffffffffu, o, sl);
+    const std::uint32_t rc = __shfl_sync(0xffffffffu, cnt, sl);
+    const std::uint32_t row = static_cast<std::uint32_t>(base + (threadIdx.x & ~31) + sl);
+    const bool copy = (copy_mask >> sl) & 1u;
+    for (std::uint32_t e = lane; e < rc; e += 32) {
+      b.erow[ro + e] = row;
+      if (copy) b.src_ids[ro + e] = b.csr_src[rlo + e];
     }
-    // warp-cooperative, coalesced writes: the row index of every edge, and the
-    // copy-all rows (deg <= fanout) in CSR order (sampling.cpp:22-25)
-    unsigned live_mask = __ballot_sync(0xffffffffu, live);
-    const unsigned copy_mask = __ballot_sync(0xffffffffu, live && deg <= fo);
-    while (live_mask) {
-      const int sl = __ffs(live_mask) - 1;
-      live_mask &= live_mask - 1;
-      const std::uint64_t rlo = __shfl_sync(0xffffffffu, lo, sl);
-      const std::uint32_t ro = __shfl_sync(0xffffffffu, o, sl);
-      const std::uint32_t rc = __shfl_sync(0xffffffffu, cnt, sl);
-      const std::uint32_t row = static_cast<std::uint32_t>(base + (threadIdx.x & ~31) + sl);
-      const bool copy = (copy_mask >> sl) & 1u;
-      for (std::uint32_t e = lane; e < rc; e += 32) {
-        b.erow[ro + e] = row;
-        if (copy) b.src_ids[ro + e] = b.csr_src[rlo + e];
-      }
+  }
+  if (live && deg > fo) {
+    bool done = false;
+    if (h.fanout <= MAXF) {
+      const std::uint64_t rel_key = (static_cast<std::uint64_t>(h.hop) << 32) | static_cast<std::uint64_t>(b.rel);
+      MtStream eng;
+      eng.seed(dmix_seed(sc->rng_seed, dmix_seed(rel_key, d)));
+      done = draw_row_reg<MAXF>(eng, deg, h.fanout, b.csr_src + lo, b.src_ids + o);
     }
-    if (live && deg > fo) {
-      bool done = false;
-      if (h.fanout <= kMapCap) {
-        std::uint32_t mpos[kMapCap], mval[kMapCap];
-        MtStream eng;
-        eng.seed(dmix_seed(rng_seed, dmix_seed(rel_key, d)));
-        done = draw_row(eng, deg, h.fanout, b.csr_src + lo, b.src_ids + o, mpos, mval);
-      }
-      if (!done) {
-        // more than 156 engine outputs (Lemire rejections) or a fanout above
-        // the local map: replay on the full-state engine in a second pass
-        const int q = atomicAdd(n_slow, 1);
-        slow[2 * q] = blockIdx.y;
-        slow[2 * q + 1] = static_cast<std::uint32_t>(i);
-      }
+    if (!done) {
+      // more than 156 engine outputs (Lemire rejections) or a fanout above the
+      // register map: replay on the full-state engine in a second pass
+      const int q = atomicAdd(n_slow, 1);
+      slow[2 * q] = static_cast<std::uint32_t>(bi);
+      slow[2 * q + 1] = static_cast<std::uint32_t>(i);
     }
   }
 }
@@ -249,26 +315,29 @@ __global__ void __launch_bounds__(128) k_sample_slow(SampleHop h, const StepScal
 
 }  // namespace
 
-void sample_count(const SampleHop& h, cudaStream_t st) {
-  if (h.nblk == 0) return;
-  int cap = 1;
-  for (int i = 0; i < h.nblk; ++i) cap = max(cap, h.b[i].rows_cap);
-  dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, kSampleThreads), 4 * kNumSMs)), h.nblk);
-  k_sample_count<<<grid, kSampleThreads, 0, st>>>(h);
-}
-
 std::size_t sample_scratch_words(int fanout) {
   return static_cast<std::size_t>(kSlowThreads) * (312 + static_cast<std::size_t>(fanout));
 }
 
-void sample_draw(const SampleHop& h, const StepScalars* sc, std::uint32_t* slow, int* n_slow,
-                 std::uint64_t* scratch, cudaStream_t st) {
+void sample_hop(const SampleHop& h, const StepScalars* sc, std::uint32_t* slow, int* n_slow,
+                std::uint64_t* scratch, LbScratch& lb, cudaStream_t st) {
   if (h.nblk == 0) return;
-  int cap = 1;
-  for (int i = 0; i < h.nblk; ++i) cap = max(cap, h.b[i].rows_cap);
+  LbLayout L{};
+  L.nseg = h.nblk;
+  int tiles = 0;
+  for (int i = 0; i < h.nblk; ++i) {
+    L.base[i] = tiles;
+    tiles += static_cast<int>(ceil_div(std::max(1, h.b[i].rows_cap), kSampleThreads));
+  }
+  L.base[h.nblk] = tiles;
+  lb.reset(tiles, st);
   HG_CUDA(cudaMemsetAsync(n_slow, 0, sizeof(int), st));
-  dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, kSampleThreads), 4 * kNumSMs)), h.nblk);
-  k_sample_draw<<<grid, kSampleThreads, 0, st>>>(h, sc, slow, n_slow);
+  if (h.fanout <= 16)
+    k_sample_fused<16><<<tiles, kSampleThreads, 0, st>>>(h, L, sc, lb.state, lb.ticket, slow, n_slow);
+  else if (h.fanout <= 32)
+    k_sample_fused<32><<<tiles, kSampleThreads, 0, st>>>(h, L, sc, lb.state, lb.ticket, slow, n_slow);
+  else
+    k_sample_fused<64><<<tiles, kSampleThreads, 0, st>>>(h, L, sc, lb.state, lb.ticket, slow, n_slow);
   k_sample_slow<<<kSlowThreads / 128, 128, 0, st>>>(h, sc, slow, n_slow, scratch);
 }
 
@@ -298,24 +367,49 @@ __global__ void __launch_bounds__(kFrontThreads) k_mark_batch(const std::uint32_
   }
 }
 
-__global__ void __launch_bounds__(kFrontThreads) k_popc(FrontierArgs f) {
-  const BitmapType& t = f.t[blockIdx.y];
-  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < t.words; w += gridDim.x * blockDim.x)
-    t.wscan[w] = __popc(t.bits[w]);
-}
+constexpr int kWordsPerThread = 4;
+constexpr int kWordsPerTile = kFrontThreads * kWordsPerThread;
 
-__global__ void __launch_bounds__(kFrontThreads) k_emit(FrontierArgs f) {
-  const BitmapType& t = f.t[blockIdx.y];
-  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < t.words; w += gridDim.x * blockDim.x) {
-    std::uint32_t bits = t.bits[w];
-    const std::uint32_t incl = t.wscan[w];
-    std::uint32_t at = incl - __popc(bits);
-    while (bits) {
-      const int j = __ffs(bits) - 1;
-      bits &= bits - 1;
-      t.list[at++] = static_cast<std::uint32_t>(w) * 32u + static_cast<std::uint32_t>(j);
+// popcount of 1024 words per tile -> CTA scan -> look-back -> inclusive word
+// prefix (the rank structure) and the sorted ids of the set bits
+__global__ void __launch_bounds__(kFrontThreads) k_compact(FrontierArgs f, LbLayout L, unsigned long long* state,
+                                                           int* ticket) {
+  __shared__ int s_tile;
+  __shared__ std::uint32_t s_prefix;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
+  __syncthreads();
+  const int tk = s_tile;
+  if (tk >= L.base[L.nseg]) return;
+  const int ti = seg_of(L.base, L.nseg, tk);
+  const int t = tk - L.base[ti];
+  const BitmapType& T = f.t[ti];
+  const int w0 = t * kWordsPerTile + threadIdx.x * kWordsPerThread;
+  std::uint32_t bits[kWordsPerThread];
+  std::uint32_t local = 0;
+#pragma unroll
+  for (int j = 0; j < kWordsPerThread; ++j) {
+    bits[j] = w0 + j < T.words ? T.bits[w0 + j] : 0u;
+    local += __popc(bits[j]);
+  }
+  std::uint32_t tot;
+  const std::uint32_t incl = block_incl_scan<kFrontThreads>(local, &tot);
+  if (threadIdx.x == 0) s_prefix = lb_prefix(state + L.base[ti], t, tot);
+  __syncthreads();
+  std::uint32_t at = s_prefix + incl - local;
+#pragma unroll
+  for (int j = 0; j < kWordsPerThread; ++j) {
+    const int w = w0 + j;
+    if (w >= T.words) break;
+    std::uint32_t b = bits[j];
+    const std::uint32_t start = at;
+    while (b) {
+      const int q = __ffs(b) - 1;
+      b &= b - 1;
+      T.list[at++] = static_cast<std::uint32_t>(w) * 32u + static_cast<std::uint32_t>(q);
     }
-    if (w == t.words - 1) *t.count = static_cast<int>(incl);
+    T.wscan[w] = at;  // inclusive prefix through word w
+    (void)start;
+    if (w == T.words - 1) *T.count = static_cast<int>(at);
   }
 }
 
@@ -360,17 +454,18 @@ void frontier_mark_batch(const std::uint32_t* ids, const StepScalars* sc, int ca
   k_mark_batch<<<grid, kFrontThreads, 0, st>>>(ids, sc, t.bits);
 }
 
-void frontier_compact(const FrontierArgs& f, const int* words_dev, std::uint32_t* partials, cudaStream_t st) {
+void frontier_compact(const FrontierArgs& f, LbScratch& lb, cudaStream_t st) {
   if (f.ntypes == 0) return;
-  int maxw = 1;
-  for (int i = 0; i < f.ntypes; ++i) maxw = max(maxw, f.t[i].words);
-  dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(maxw, kFrontThreads), 8 * kNumSMs)), f.ntypes);
-  k_popc<<<grid, kFrontThreads, 0, st>>>(f);
-  ScanArgs sa{};
-  sa.nseg = f.ntypes;
-  for (int i = 0; i < f.ntypes; ++i) sa.s[i] = {f.t[i].wscan, words_dev + i, f.t[i].words};
-  scan_inclusive(sa, partials, st);
-  k_emit<<<grid, kFrontThreads, 0, st>>>(f);
+  LbLayout L{};
+  L.nseg = f.ntypes;
+  int tiles = 0;
+  for (int i = 0; i < f.ntypes; ++i) {
+    L.base[i] = tiles;
+    tiles += static_cast<int>(ceil_div(std::max(1, f.t[i].words), kWordsPerTile));
+  }
+  L.base[f.ntypes] = tiles;
+  lb.reset(tiles, st);
+  k_compact<<<tiles, kFrontThreads, 0, st>>>(f, L, lb.state, lb.ticket);
 }
 
 void frontier_relabel(const RelabelArgs& r, const FrontierArgs& f, cudaStream_t st) {

@@ -37,8 +37,22 @@ struct ScanArgs {
   int nseg;
 };
 constexpr int kScanTile = 4096;
-// partial scratch: nseg * ceil(max cap / kScanTile) u32
-void scan_inclusive(const ScanArgs& a, std::uint32_t* partials, cudaStream_t st);
+// look-back scratch for the single-pass scans: word 0 is the ticket counter,
+// words 1.. the per-tile (flag, value) states; reset with one memset per use
+struct LbScratch {
+  unsigned long long* mem = nullptr;
+  int cap = 0;  // tiles
+  unsigned long long* state = nullptr;
+  int* ticket = nullptr;
+  void reset(int tiles, cudaStream_t st) {
+    if (tiles > cap) throw std::runtime_error("look-back scratch too small");
+    ticket = reinterpret_cast<int*>(mem);
+    state = mem + 1;
+    HG_CUDA(cudaMemsetAsync(mem, 0, (static_cast<std::size_t>(tiles) + 1) * 8, st));
+  }
+};
+// single-pass (decoupled look-back) segmented inclusive scan
+void scan_inclusive(const ScanArgs& a, LbScratch& lb, cudaStream_t st);
 
 // ---- sampling ---------------------------------------------------------------------
 struct SampleBlock {
@@ -58,15 +72,14 @@ struct SampleHop {
   int fanout;
   int hop;
 };
-// counts[i] = min(fanout, deg) into indptr[i+1]; indptr[0] = 0
-void sample_count(const SampleHop& h, cudaStream_t st);
-// draws (exact mt19937_64 + Lemire + partial Fisher-Yates). Rows whose draw
-// overflows the streaming engine go to `slow` ((block,row) pairs, capacity =
-// total rows) and are replayed with the full-state engine on `scratch`
-// (sample_scratch_words(fanout) u64).
+// One pass per hop: per-row counts min(fanout, deg), the block offsets (single-pass
+// scan) and the draws (exact mt19937_64 + Lemire + partial Fisher-Yates). Rows
+// whose draw overflows the streaming engine go to `slow` ((block,row) pairs,
+// capacity = total rows) and are replayed with the full-state engine on
+// `scratch` (sample_scratch_words(fanout) u64).
 std::size_t sample_scratch_words(int fanout);
-void sample_draw(const SampleHop& h, const StepScalars* sc, std::uint32_t* slow, int* n_slow,
-                 std::uint64_t* scratch, cudaStream_t st);
+void sample_hop(const SampleHop& h, const StepScalars* sc, std::uint32_t* slow, int* n_slow,
+                std::uint64_t* scratch, LbScratch& lb, cudaStream_t st);
 
 // ---- frontier: bitmap set -> sorted unique ids + rank -----------------------------
 struct BitmapType {
@@ -95,8 +108,8 @@ struct MarkArgs {
 void frontier_mark(const MarkArgs& m, const FrontierArgs& f, cudaStream_t st);
 void frontier_mark_batch(const std::uint32_t* ids, const StepScalars* sc, int cap, const BitmapType& t,
                          cudaStream_t st);
-void frontier_compact(const FrontierArgs& f, const int* words_dev, std::uint32_t* partials,
-                      cudaStream_t st);
+// popcount + single-pass scan + emit of every type's bitmap (sorted unique ids)
+void frontier_compact(const FrontierArgs& f, LbScratch& lb, cudaStream_t st);
 struct RelabelBlock {
   const std::uint32_t* ids;
   const std::uint32_t* indptr;
@@ -200,7 +213,7 @@ struct CscHop {
   CscEdges b[kMaxBlocks];
   int nb;
 };
-void csc_prepare(const CscHop& h, std::uint32_t* partials, cudaStream_t st);
+void csc_prepare(const CscHop& h, LbScratch& lb, cudaStream_t st);
 
 // ---- optimizer ------------------------------------------------------------------------
 struct AdamHyper {  // hgnn.hpp:16-21
