@@ -79,28 +79,43 @@ void cross_entropy(const LossArgs& a, cudaStream_t st) {
 
 namespace {
 
-__device__ __forceinline__ void adam4(float4& w, float4& m, float4& v, const float4 g, double bc1, double bc2,
-                                      const AdamHyper& hp, std::uint32_t* err) {
-  // moments and update in f64 like the reference (hgnn.cpp:364-377); fp32 storage
+// Adam (hgnn.cpp:364-377) in fp32 with the bias corrections folded into two
+// per-step scalars computed in f64: w -= a * m / (sqrt(v * b) + eps) with
+// a = lr / (1 - beta1^t), b = 1 / (1 - beta2^t)
+struct AdamStep {
+  float a, b, c1, c2, beta1, beta2, eps;
+};
+__device__ __forceinline__ AdamStep adam_step_of(const AdamHyper& hp, double t) {
+  AdamStep s;
+  s.a = static_cast<float>(hp.lr / (1.0 - pow(hp.beta1, t)));
+  s.b = static_cast<float>(1.0 / (1.0 - pow(hp.beta2, t)));
+  s.beta1 = static_cast<float>(hp.beta1);
+  s.beta2 = static_cast<float>(hp.beta2);
+  s.c1 = static_cast<float>(1.0 - hp.beta1);
+  s.c2 = static_cast<float>(1.0 - hp.beta2);
+  s.eps = static_cast<float>(hp.eps);
+  return s;
+}
+__device__ __forceinline__ void adam4(float4& w, float4& m, float4& v, const float4 g, const AdamStep& k,
+                                      std::uint32_t* err) {
   float* wp = &w.x;
   float* mp = &m.x;
   float* vp = &v.x;
   const float gv[4] = {g.x, g.y, g.z, g.w};
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const double gi = gv[j];
+    const float gi = gv[j];
     if (!isfinite(gi)) {
       atomicOr(err, 4u);
       continue;
     }
-    const double md = hp.beta1 * mp[j] + (1.0 - hp.beta1) * gi;
-    const double vd = hp.beta2 * vp[j] + (1.0 - hp.beta2) * gi * gi;
-    mp[j] = static_cast<float>(md);
-    vp[j] = static_cast<float>(vd);
-    wp[j] = static_cast<float>(wp[j] - hp.lr * (md / bc1) / (sqrt(vd / bc2) + hp.eps));
+    const float md = fmaf(k.beta1, mp[j], k.c1 * gi);
+    const float vd = fmaf(k.beta2, vp[j], k.c2 * gi * gi);
+    mp[j] = md;
+    vp[j] = vd;
+    wp[j] -= k.a * md / (sqrtf(vd * k.b) + k.eps);
   }
 }
-
 
 __global__ void k_csc_fill(CscHop h) {
   const CscEdges& b = h.b[blockIdx.y];
@@ -134,12 +149,10 @@ __global__ void k_csc_sort(CscHop h) {
 // one half-warp per (source row, 64-column chunk): ordered sum of the dmean rows
 // of its sampled edges; learnable leaves apply Adam to their table row directly
 __global__ void __launch_bounds__(256) k_csc_gather(CscHop h, AdamHyper hp, std::uint32_t* err) {
-  __shared__ double bc[kMaxSegs][2];
+  __shared__ AdamStep ks[kMaxSegs];
   if (threadIdx.x < h.nt) {
     const CscType& t = h.t[threadIdx.x];
-    const double st = t.step ? static_cast<double>(*t.step) : 1.0;
-    bc[threadIdx.x][0] = 1.0 - pow(hp.beta1, st);
-    bc[threadIdx.x][1] = 1.0 - pow(hp.beta2, st);
+    ks[threadIdx.x] = adam_step_of(hp, t.step ? static_cast<double>(*t.step) : 1.0);
   }
   __syncthreads();
   const int hl = threadIdx.x & 15;
@@ -154,17 +167,33 @@ __global__ void __launch_bounds__(256) k_csc_gather(CscHop h, AdamHyper hp, std:
       if (f >= t.ld_dh) continue;
       const std::uint32_t lo = c ? t.offs[c - 1] : 0u, hi = t.offs[c];
       float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (std::uint32_t x = lo; x < hi; ++x) {
-        const std::uint32_t id = t.entries[x];
-        int bi = 0;
-        while (bi + 1 < h.nb && id >= static_cast<std::uint32_t>(h.b[bi + 1].edge_base)) ++bi;
-        const CscEdges& b = h.b[bi];
-        const std::uint32_t row = b.erow[id - b.edge_base];
-        const float4 v = *reinterpret_cast<const float4*>(b.dmean + static_cast<std::size_t>(row) * b.ld_dmean + f);
-        s.x += v.x;
-        s.y += v.y;
-        s.z += v.z;
-        s.w += v.w;
+      // up to 4 edges in flight: entry ids, then block rows, then dmean rows
+      for (std::uint32_t x0 = lo; x0 < hi; x0 += 4) {
+        const int cnt = min(4u, hi - x0);
+        const float* rowp[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          rowp[q] = nullptr;
+          if (q < cnt) {
+            const std::uint32_t id = __ldg(t.entries + x0 + q);
+            int bi = 0;
+            while (bi + 1 < h.nb && id >= static_cast<std::uint32_t>(h.b[bi + 1].edge_base)) ++bi;
+            const CscEdges& b = h.b[bi];
+            const std::uint32_t row = __ldg(b.erow + (id - b.edge_base));
+            rowp[q] = b.dmean + static_cast<std::size_t>(row) * b.ld_dmean + f;
+          }
+        }
+        float4 v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          v[q] = q < cnt ? *reinterpret_cast<const float4*>(rowp[q]) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          s.x += v[q].x;
+          s.y += v[q].y;
+          s.z += v[q].z;
+          s.w += v[q].w;
+        }
       }
       if (t.dh) *reinterpret_cast<float4*>(t.dh + static_cast<std::size_t>(c) * t.ld_dh + f) = s;
       if (t.w) {
@@ -172,7 +201,7 @@ __global__ void __launch_bounds__(256) k_csc_gather(CscHop h, AdamHyper hp, std:
         float4 w = *reinterpret_cast<float4*>(t.w + at);
         float4 m = *reinterpret_cast<float4*>(t.m + at);
         float4 v = *reinterpret_cast<float4*>(t.v + at);
-        adam4(w, m, v, s, bc[ty][0], bc[ty][1], hp, err);
+        adam4(w, m, v, s, ks[ty], err);
         *reinterpret_cast<float4*>(t.w + at) = w;
         *reinterpret_cast<float4*>(t.m + at) = m;
         *reinterpret_cast<float4*>(t.v + at) = v;
@@ -214,12 +243,8 @@ namespace {
 // in w, m, v and g, so updating it is a no-op)
 __global__ void __launch_bounds__(256) k_adam_model(AdamModelBatch b, const std::int64_t* step, AdamHyper hp,
                                                     std::uint32_t* err) {
-  __shared__ double bc[2];
-  if (threadIdx.x == 0) {
-    const double t = static_cast<double>(*step);
-    bc[0] = 1.0 - pow(hp.beta1, t);
-    bc[1] = 1.0 - pow(hp.beta2, t);
-  }
+  __shared__ AdamStep ks;
+  if (threadIdx.x == 0) ks = adam_step_of(hp, static_cast<double>(*step));
   __syncthreads();
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < b.total4; x += gridDim.x * blockDim.x) {
     int s = 0;
@@ -229,7 +254,7 @@ __global__ void __launch_bounds__(256) k_adam_model(AdamModelBatch b, const std:
     float4 m = *reinterpret_cast<float4*>(b.m[s] + off);
     float4 v = *reinterpret_cast<float4*>(b.v[s] + off);
     const float4 g = *reinterpret_cast<const float4*>(b.g[s] + off);
-    adam4(w, m, v, g, bc[0], bc[1], hp, err);
+    adam4(w, m, v, g, ks, err);
     *reinterpret_cast<float4*>(b.w[s] + off) = w;
     *reinterpret_cast<float4*>(b.m[s] + off) = m;
     *reinterpret_cast<float4*>(b.v[s] + off) = v;
@@ -244,12 +269,8 @@ __global__ void k_bump_steps(AdamRowsBatch b) {
 
 // sparse learnable rows of every table in one launch: one float4 per thread
 __global__ void __launch_bounds__(256) k_adam_rows(AdamRowsBatch b, AdamHyper hp, std::uint32_t* err) {
-  __shared__ double bc[kMaxSegs][2];
-  if (threadIdx.x < b.n) {
-    const double t = static_cast<double>(*b.t[threadIdx.x].step);
-    bc[threadIdx.x][0] = 1.0 - pow(hp.beta1, t);
-    bc[threadIdx.x][1] = 1.0 - pow(hp.beta2, t);
-  }
+  __shared__ AdamStep ks[kMaxSegs];
+  if (threadIdx.x < b.n) ks[threadIdx.x] = adam_step_of(hp, static_cast<double>(*b.t[threadIdx.x].step));
   __syncthreads();
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < b.total4; x += gridDim.x * blockDim.x) {
     int s = 0;
@@ -264,7 +285,7 @@ __global__ void __launch_bounds__(256) k_adam_rows(AdamRowsBatch b, AdamHyper hp
     float4 m = *reinterpret_cast<float4*>(T.m + at);
     float4 v = *reinterpret_cast<float4*>(T.v + at);
     const float4 g = *reinterpret_cast<const float4*>(T.g + static_cast<std::size_t>(i) * T.ld_g + c);
-    adam4(w, m, v, g, bc[s][0], bc[s][1], hp, err);
+    adam4(w, m, v, g, ks[s], err);
     *reinterpret_cast<float4*>(T.w + at) = w;
     *reinterpret_cast<float4*>(T.m + at) = m;
     *reinterpret_cast<float4*>(T.v + at) = v;

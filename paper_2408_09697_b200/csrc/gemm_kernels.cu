@@ -210,17 +210,31 @@ __global__ void __launch_bounds__(kT) k_wgrad_tiles(WGradBatch b) {
   }
 }
 
-// ordered sum of the chunk partials into dW (deterministic)
-__global__ void k_wgrad_reduce(WGradBatch b) {
-  for (int p = 0; p < b.np; ++p) {
-    const WGradProblem& P = b.p[p];
-    const int chunks = (*P.n_rows + kWChunkRows - 1) / kWChunkRows;
-    const int total = P.din * P.d.cols;
-    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
-      float s = 0.f;
-      for (int c = 0; c < chunks; ++c) s += P.partial[static_cast<std::size_t>(c) * total + x];
-      P.dw[static_cast<std::size_t>(x / P.d.cols) * P.ld_dw + x % P.d.cols] += s;
+// ordered sum of the chunk partials into dW (deterministic): one thread per
+// output element of every problem, chunks summed in order, 8 loads in flight
+__global__ void __launch_bounds__(256) k_wgrad_reduce(WGradBatch b, int total_out) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < total_out; x += gridDim.x * blockDim.x) {
+    int p = 0, base = 0;
+    while (p + 1 < b.np && x >= base + b.p[p].din * b.p[p].d.cols) {
+      base += b.p[p].din * b.p[p].d.cols;
+      ++p;
     }
+    const WGradProblem& P = b.p[p];
+    const int total = P.din * P.d.cols;
+    const int o = x - base;
+    const int chunks = (*P.n_rows + kWChunkRows - 1) / kWChunkRows;
+    const float* src = P.partial + o;
+    float s = 0.f;
+    int c = 0;
+    for (; c + 8 <= chunks; c += 8) {
+      float v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = src[static_cast<std::size_t>(c + q) * total];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s += v[q];
+    }
+    for (; c < chunks; ++c) s += src[static_cast<std::size_t>(c) * total];
+    P.dw[static_cast<std::size_t>(o / P.d.cols) * P.ld_dw + o % P.d.cols] += s;
   }
 }
 
@@ -277,17 +291,18 @@ __global__ void __launch_bounds__(kT) k_dmean_tiles(DMeanBatch b) {
   }
 }
 
-// ---- gather-mean: one warp per (row, 128-column chunk), 8 edges in flight ----------------
+// ---- gather-mean: 16 lanes x float4 per (row, 64-column chunk); a warp carries
+// two such items, 8 edges in flight per lane ---------------------------------------------------
 __global__ void __launch_bounds__(256) k_gather_mean(MeanBatch m) {
-  const int lane = threadIdx.x & 31;
-  const int warps = gridDim.x * (blockDim.x >> 5);
-  for (int item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); item < m.item_base[m.nb]; item += warps) {
+  const int hl = threadIdx.x & 15;
+  const int halves = gridDim.x * (blockDim.x >> 4);
+  for (int item = blockIdx.x * (blockDim.x >> 4) + (threadIdx.x >> 4); item < m.item_base[m.nb]; item += halves) {
     int b = 0;
     while (b + 1 < m.nb && item >= m.item_base[b + 1]) ++b;
     const MeanBlock& B = m.b[b];
-    const int nch = (B.din + 127) / 128;
+    const int nch = (B.din + 63) / 64;
     const int local = item - m.item_base[b];
-    const int i = local / nch, c = (local % nch) * 128 + 4 * lane;
+    const int i = local / nch, c = (local % nch) * 64 + 4 * hl;
     if (i >= *B.n_rows || c >= B.ld_mean) continue;
     const std::uint32_t lo = B.indptr[i], hi = B.indptr[i + 1];
     const float* base = B.h + c;
@@ -393,10 +408,10 @@ void gather_mean(MeanBatch& m, cudaStream_t st) {
   int items = 0;
   for (int b = 0; b < m.nb; ++b) {
     m.item_base[b] = items;
-    items += m.b[b].rows_cap * static_cast<int>(ceil_div(m.b[b].din, 128));
+    items += m.b[b].rows_cap * static_cast<int>(ceil_div(m.b[b].din, 64));
   }
   m.item_base[m.nb] = items;
-  const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(items, 8), 16 * kNumSMs)));
+  const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(items, 16), 16 * kNumSMs)));
   k_gather_mean<<<grid, 256, 0, st>>>(m);
 }
 
@@ -427,7 +442,9 @@ void wgrad_tiles(WGradBatch& b, cudaStream_t st) {
                               ceil_div(P.d.cols, kTile));
   }
   k_wgrad_tiles<<<std::max(1, tiles), kT, 0, st>>>(b);
-  k_wgrad_reduce<<<2 * kNumSMs, 256, 0, st>>>(b);
+  int total_out = 0;
+  for (int p = 0; p < b.np; ++p) total_out += b.p[p].din * b.p[p].d.cols;
+  k_wgrad_reduce<<<static_cast<unsigned>(ceil_div(total_out, 256)), 256, 0, st>>>(b, total_out);
 }
 
 void dmean_tiles(DMeanBatch& b, cudaStream_t st) {

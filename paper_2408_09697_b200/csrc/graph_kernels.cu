@@ -52,24 +52,36 @@ __device__ __forceinline__ unsigned long long lb_load(const unsigned long long* 
   return *reinterpret_cast<const volatile unsigned long long*>(p);
 }
 
-// thread 0 only: exclusive prefix of tile t inside its segment state array
+// warp 0 only (all 32 lanes): exclusive prefix of tile t inside its segment
+// state array. The warp inspects 32 predecessors at once: the nearest one with
+// an inclusive prefix ends the walk, aggregates in between are summed; a
+// predecessor that has published nothing yet makes the warp re-read.
 __device__ __forceinline__ std::uint32_t lb_prefix(unsigned long long* st, int t, std::uint32_t agg) {
+  const int lane = threadIdx.x & 31;
   if (t == 0) {
-    atomicExch(st, kLbPre | agg);
+    if (lane == 0) atomicExch(st, kLbPre | agg);
     return 0;
   }
-  atomicExch(st + t, kLbAgg | agg);
+  if (lane == 0) atomicExch(st + t, kLbAgg | agg);
   std::uint32_t excl = 0;
-  int j = t - 1;
+  int hi = t - 1;  // window [hi-31, hi]
   while (true) {
-    const unsigned long long v = lb_load(st + j);
+    const int j = hi - lane;
+    const unsigned long long v = j >= 0 ? lb_load(st + j) : kLbPre;  // virtual prefix 0 before tile 0
     const unsigned long long flag = v >> 32;
-    if (flag == 0) continue;
-    excl += static_cast<std::uint32_t>(v);
-    if (flag == 2) break;
-    --j;
+    const unsigned waiting = __ballot_sync(0xffffffffu, flag == 0);
+    const unsigned prefix = __ballot_sync(0xffffffffu, flag == 2);
+    // lanes up to the nearest prefix (lowest lane with flag 2) must all be ready
+    const int stop = prefix ? __ffs(prefix) - 1 : 31;
+    const unsigned needed = stop == 31 ? 0xffffffffu : ((1u << (stop + 1)) - 1u);
+    if (waiting & needed) continue;  // spin on the same window
+    std::uint32_t part = lane <= stop ? static_cast<std::uint32_t>(v) : 0u;
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    excl += part;
+    if (prefix) break;
+    hi -= 32;
   }
-  atomicExch(st + t, kLbPre | (excl + agg));
+  if (lane == 0) atomicExch(st + t, kLbPre | (excl + agg));
   return excl;
 }
 
@@ -109,7 +121,10 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lb(ScanArgs a, LbLayout L
   }
   std::uint32_t tot;
   const std::uint32_t incl = block_incl_scan<kScanThreads>(local, &tot);
-  if (threadIdx.x == 0) s_prefix = lb_prefix(state + L.base[sg], t, tot);
+  if (threadIdx.x < 32) {
+    const std::uint32_t p = lb_prefix(state + L.base[sg], t, tot);
+    if (threadIdx.x == 0) s_prefix = p;
+  }
   __syncthreads();
   std::uint32_t run = s_prefix + incl - local;
 #pragma unroll
@@ -146,17 +161,15 @@ constexpr int kSlowThreads = 4096;  // concurrent slow-path rows (global scratch
 // Partial Fisher-Yates over [0, deg) with a sparse map of displaced positions
 // (sampling.cpp:29-37 keeps a dense O(deg) index array). Position p holds p
 // unless overridden; position i is final once drawn, so only the j side needs
-// remembering. The map lives in registers (fully unrolled, MAXF entries).
-// Returns false if the streaming engine ran dry (caller replays on MtFull).
+// remembering. The map is a per-lane list in shared memory laid out
+// [slot][lane] (conflict-free), O(1) insert; a 64-bit filter of the inserted
+// positions lets most lookups skip the scan. Returns false if the streaming
+// engine ran dry (the caller replays the row on MtFull).
 template <int MAXF, typename Eng>
-__device__ __forceinline__ bool draw_row_reg(Eng& eng, std::uint64_t deg, int fanout, const std::uint32_t* nbr,
-                                             std::uint32_t* out) {
-  std::uint32_t mpos[MAXF], mval[MAXF];
-#pragma unroll
-  for (int q = 0; q < MAXF; ++q) {
-    mpos[q] = 0xffffffffu;
-    mval[q] = 0u;
-  }
+__device__ __forceinline__ bool draw_row_smem(Eng& eng, std::uint64_t deg, int fanout, const std::uint32_t* nbr,
+                                              std::uint32_t* out, std::uint32_t* mpos, std::uint32_t* mval) {
+  // mpos/mval point at this lane's column: element q at [q * kSampleThreads]
+  unsigned long long filt = 0ull;
   int nmap = 0;
   for (int i = 0; i < fanout; ++i) {
     std::uint64_t off;
@@ -164,28 +177,29 @@ __device__ __forceinline__ bool draw_row_reg(Eng& eng, std::uint64_t deg, int fa
     const std::uint32_t ii = static_cast<std::uint32_t>(i);
     const std::uint32_t jpos = static_cast<std::uint32_t>(i + off);
     std::uint32_t vi = ii, vj = jpos;
-    bool found = false;
-#pragma unroll
-    for (int q = 0; q < MAXF; ++q) {
-      if (mpos[q] == ii) vi = mval[q];
-      if (mpos[q] == jpos) {
-        vj = mval[q];
-        found = true;
+    int slot_j = -1;
+    const bool maybe_i = (filt >> (ii & 63u)) & 1ull, maybe_j = (filt >> (jpos & 63u)) & 1ull;
+    if (maybe_i || maybe_j) {
+      for (int q = 0; q < nmap; ++q) {
+        const std::uint32_t pq = mpos[q * kSampleThreads];
+        if (pq == ii) vi = mval[q * kSampleThreads];
+        if (pq == jpos) {
+          vj = mval[q * kSampleThreads];
+          slot_j = q;
+        }
       }
     }
     if (jpos != ii) {
-#pragma unroll
-      for (int q = 0; q < MAXF; ++q) {
-        const bool hit = found ? mpos[q] == jpos : q == nmap;
-        if (hit) {
-          mpos[q] = jpos;
-          mval[q] = vi;
-        }
+      if (slot_j < 0) {
+        slot_j = nmap++;
+        mpos[slot_j * kSampleThreads] = jpos;
+        filt |= 1ull << (jpos & 63u);
       }
-      if (!found) ++nmap;
+      mval[slot_j * kSampleThreads] = vi;
     }
     out[i] = nbr[vj];
   }
+  (void)MAXF;
   return true;
 }
 
@@ -229,6 +243,7 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_fused(SampleHop h, Lb
                                                                  std::uint32_t* slow, int* n_slow) {
   __shared__ int s_tile;
   __shared__ std::uint32_t s_prefix;
+  extern __shared__ std::uint32_t s_map[];  // 2 * MAXF * kSampleThreads words (dynamic)
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
   __syncthreads();
   const int tk = s_tile;
@@ -252,26 +267,46 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_fused(SampleHop h, Lb
   }
   std::uint32_t tot;
   const std::uint32_t incl = block_incl_scan<kSampleThreads>(cnt, &tot);
-  if (threadIdx.x == 0) s_prefix = lb_prefix(state + L.base[bi], t, tot);
+  if (threadIdx.x < 32) {
+    const std::uint32_t p = lb_prefix(state + L.base[bi], t, tot);
+    if (threadIdx.x == 0) s_prefix = p;
+  }
   __syncthreads();
   const std::uint32_t o = s_prefix + incl - cnt;
   if (live) b.indptr[i + 1] = o + cnt;
   if (i == 0) b.indptr[0] = 0;
 
+  // Warp-flattened writes: the warp's 32 consecutive rows own one contiguous
+  // output range, so every lane takes independent edges q = lane, lane+32, ...
+  // (row found by a shuffle binary search over the warp's inclusive counts):
+  // the row index of every edge, and the copy-all rows (deg <= fanout) in CSR
+  // order (sampling.cpp:22-25). Loads are independent across lanes.
   const int lane = threadIdx.x & 31;
-  unsigned live_mask = __ballot_sync(0xffffffffu, live);
   const unsigned copy_mask = __ballot_sync(0xffffffffu, live && deg <= fo);
-  while (live_mask) {
-    const int sl = __ffs(live_mask) - 1;
-    live_mask &= live_mask - 1;
-    const std::uint64_t rlo = __shfl_sync(0xffffffffu, lo, sl);
-    const std::uint32_t ro = __shfl_sync(0xffffffffu, o, sl);
-    const std::uint32_t rc = __shfl_sync(0xffffffffu, cnt, sl);
-    const std::uint32_t row = static_cast<std::uint32_t>(base + (threadIdx.x & ~31) + sl);
-    const bool copy = (copy_mask >> sl) & 1u;
-    for (std::uint32_t e = lane; e < rc; e += 32) {
-      b.erow[ro + e] = row;
-      if (copy) b.src_ids[ro + e] = b.csr_src[rlo + e];
+  std::uint32_t wincl = cnt;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const std::uint32_t y = __shfl_up_sync(0xffffffffu, wincl, off);
+    if (lane >= off) wincl += y;
+  }
+  const std::uint32_t wtotal = __shfl_sync(0xffffffffu, wincl, 31);
+  const std::uint32_t o0 = __shfl_sync(0xffffffffu, o, 0);
+  const std::uint32_t row_base = static_cast<std::uint32_t>(base + (threadIdx.x & ~31));
+  for (std::uint32_t q0 = 0; q0 < wtotal; q0 += 32) {  // warp-uniform trip count
+    const std::uint32_t q = q0 + lane;
+    int r = 0;  // smallest lane r with wincl[r] > q
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+      const std::uint32_t v = __shfl_sync(0xffffffffu, wincl, r + step - 1);
+      if (v <= q) r += step;
+    }
+    r = min(r, 31);
+    const std::uint32_t rincl = __shfl_sync(0xffffffffu, wincl, r);
+    const std::uint32_t rcnt = __shfl_sync(0xffffffffu, cnt, r);
+    const std::uint64_t rlo = __shfl_sync(0xffffffffu, lo, r);
+    if (q < wtotal) {
+      b.erow[o0 + q] = row_base + static_cast<std::uint32_t>(r);
+      if ((copy_mask >> r) & 1u) b.src_ids[o0 + q] = b.csr_src[rlo + (q - (rincl - rcnt))];
     }
   }
   if (live && deg > fo) {
@@ -280,7 +315,8 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_fused(SampleHop h, Lb
       const std::uint64_t rel_key = (static_cast<std::uint64_t>(h.hop) << 32) | static_cast<std::uint64_t>(b.rel);
       MtStream eng;
       eng.seed(dmix_seed(sc->rng_seed, dmix_seed(rel_key, d)));
-      done = draw_row_reg<MAXF>(eng, deg, h.fanout, b.csr_src + lo, b.src_ids + o);
+      done = draw_row_smem<MAXF>(eng, deg, h.fanout, b.csr_src + lo, b.src_ids + o, s_map + threadIdx.x,
+                                 s_map + MAXF * kSampleThreads + threadIdx.x);
     }
     if (!done) {
       // more than 156 engine outputs (Lemire rejections) or a fanout above the
@@ -332,12 +368,18 @@ void sample_hop(const SampleHop& h, const StepScalars* sc, std::uint32_t* slow, 
   L.base[h.nblk] = tiles;
   lb.reset(tiles, st);
   HG_CUDA(cudaMemsetAsync(n_slow, 0, sizeof(int), st));
+  // the shared-memory map holds up to MAXF displaced positions per lane
+  static bool attr_set = false;
+  const int smem16 = 2 * 16 * kSampleThreads * 4, smem32 = 2 * 32 * kSampleThreads * 4;
+  if (!attr_set) {
+    HG_CUDA(cudaFuncSetAttribute(k_sample_fused<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem16));
+    HG_CUDA(cudaFuncSetAttribute(k_sample_fused<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem32));
+    attr_set = true;
+  }
   if (h.fanout <= 16)
-    k_sample_fused<16><<<tiles, kSampleThreads, 0, st>>>(h, L, sc, lb.state, lb.ticket, slow, n_slow);
-  else if (h.fanout <= 32)
-    k_sample_fused<32><<<tiles, kSampleThreads, 0, st>>>(h, L, sc, lb.state, lb.ticket, slow, n_slow);
+    k_sample_fused<16><<<tiles, kSampleThreads, smem16, st>>>(h, L, sc, lb.state, lb.ticket, slow, n_slow);
   else
-    k_sample_fused<64><<<tiles, kSampleThreads, 0, st>>>(h, L, sc, lb.state, lb.ticket, slow, n_slow);
+    k_sample_fused<32><<<tiles, kSampleThreads, smem32, st>>>(h, L, sc, lb.state, lb.ticket, slow, n_slow);
   k_sample_slow<<<kSlowThreads / 128, 128, 0, st>>>(h, sc, slow, n_slow, scratch);
 }
 
@@ -393,7 +435,10 @@ __global__ void __launch_bounds__(kFrontThreads) k_compact(FrontierArgs f, LbLay
   }
   std::uint32_t tot;
   const std::uint32_t incl = block_incl_scan<kFrontThreads>(local, &tot);
-  if (threadIdx.x == 0) s_prefix = lb_prefix(state + L.base[ti], t, tot);
+  if (threadIdx.x < 32) {
+    const std::uint32_t p = lb_prefix(state + L.base[ti], t, tot);
+    if (threadIdx.x == 0) s_prefix = p;
+  }
   __syncthreads();
   std::uint32_t at = s_prefix + incl - local;
 #pragma unroll
