@@ -89,6 +89,8 @@ hg_graph* hg_graph_from_pairs(int n_types, const uint64_t* counts, int n_rels, c
 void hg_graph_free(hg_graph* g);
 /* node_counts, labels, rel_src/rel_dst/rel_reverse, rel{r}.indptr, rel{r}.src, feat.t{t}, kinds, dims */
 hg_bundle* hg_graph_export(const hg_graph* g);
+/* schema only (no edges or features): node_counts, kinds, dims, target, num_classes, rel_src, rel_dst */
+hg_bundle* hg_graph_schema(const hg_graph* g);
 
 /* ---- planning (host; meta-partitioner stays on the CPU) ------------------------------- */
 /* meta_partition (src/metapartition.cpp:283-295) + cacheable_types (src/cache.cpp:143-177)
@@ -121,6 +123,12 @@ typedef struct {
 } hg_step_report;
 
 hg_engine* hg_engine_create(const hg_graph* g, const hg_engine_opts* opts);
+/* Sampler-only engine for sample_khop (hop_rel_flat == NULL: every relation at
+ * every hop; src/sampling.cpp:94-97) and sample_khop_restricted (per-hop allowed
+ * relation lists, concatenated, hop_rel_counts[h] entries each; sampling.cpp:99-103).
+ * Use hg_engine_sample + hg_engine_read; hg_engine_step is rejected. */
+hg_engine* hg_sampler_create(const hg_graph* g, const int* fanouts, int k, const int* hop_rel_flat,
+                             const int* hop_rel_counts, int batch_cap, int device);
 void hg_engine_free(hg_engine* e);
 
 /* One RAF training batch: run_raf_batch (src/raf.cpp:344-530) followed by

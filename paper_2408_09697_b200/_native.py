@@ -73,6 +73,8 @@ def lib():
             "hg_graph_from_pairs": ([i32, vp, i32, vp, vp, vp, vp, vp, i32, i32], vp),
             "hg_graph_free": ([vp], None),
             "hg_graph_export": ([vp], vp),
+            "hg_graph_schema": ([vp], vp),
+            "hg_sampler_create": ([vp, vp, i32, vp, vp, i32, i32], vp),
             "hg_meta_partition": ([vp, i32, i32], vp),
             "hg_make_batches": ([vp, i32, i32, u64], vp),
             "hg_engine_create": ([vp, C.POINTER(EngineOpts)], vp),

@@ -177,6 +177,32 @@ hg_graph* hg_graph_from_pairs(int n_types, const uint64_t* counts, int n_rels, c
 
 void hg_graph_free(hg_graph* g) { delete g; }
 
+hg_bundle* hg_graph_schema(const hg_graph* h) {
+  return guard<hg_bundle*>(nullptr, [&] {
+    const Graph& g = h->g;
+    auto* b = new hg_bundle;
+    std::vector<std::uint64_t> counts;
+    std::vector<int> kinds, dims, rs, rd;
+    for (const auto& t : g.types) {
+      counts.push_back(t.count);
+      kinds.push_back(static_cast<int>(t.storage));
+      dims.push_back(t.dim);
+    }
+    for (int r = 0; r < g.num_rels(); ++r) {
+      rs.push_back(g.rels[r].src_type);
+      rd.push_back(g.rels[r].dst_type);
+    }
+    b->add("node_counts", "<u8", counts);
+    b->add("kinds", "<i4", kinds);
+    b->add("dims", "<i4", dims);
+    b->add("target", "<i8", std::vector<long long>{g.target});
+    b->add("num_classes", "<i8", std::vector<long long>{g.num_classes});
+    b->add("rel_src", "<i4", rs);
+    b->add("rel_dst", "<i4", rd);
+    return b;
+  });
+}
+
 hg_bundle* hg_graph_export(const hg_graph* h) {
   return guard<hg_bundle*>(nullptr, [&] {
     const Graph& g = h->g;
@@ -275,6 +301,31 @@ hg_engine* hg_engine_create(const hg_graph* g, const hg_engine_opts* o) {
     eo.model_seed = o->model_seed;
     eo.learn_seed = o->learn_seed;
     eo.device = o->device;
+    auto* h = new hg_engine;
+    h->e = std::make_unique<Engine>(g->g, eo);
+    return h;
+  });
+}
+
+hg_engine* hg_sampler_create(const hg_graph* g, const int* fanouts, int k, const int* hop_rel_flat,
+                             const int* hop_rel_counts, int batch_cap, int device) {
+  return guard<hg_engine*>(nullptr, [&] {
+    if (k < 1 || !fanouts) throw std::invalid_argument("fanouts must be non-empty");
+    EngineOptions eo;
+    eo.k = k;
+    eo.fanouts = ivec(fanouts, k);
+    eo.batch_cap = batch_cap;
+    eo.device = device;
+    eo.sample_only = true;
+    if (!hop_rel_flat || !hop_rel_counts) {
+      eo.all_relations = true;
+    } else {
+      int at = 0;
+      for (int h = 0; h < k; ++h) {
+        eo.hop_relations.emplace_back(hop_rel_flat + at, hop_rel_flat + at + hop_rel_counts[h]);
+        at += hop_rel_counts[h];
+      }
+    }
     auto* h = new hg_engine;
     h->e = std::make_unique<Engine>(g->g, eo);
     return h;

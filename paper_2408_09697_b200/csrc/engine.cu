@@ -171,6 +171,23 @@ void Engine::build_plan(const Graph& g) {
     }
   }
   hop_rels_ = hop_relations(tree_, k);
+  if (o_.sample_only) {
+    // the reference filters relations by membership and walks them ascending
+    // (sampling.cpp:64-68): the effective per-hop set is sorted and unique
+    hop_rels_.assign(k, {});
+    for (int h = 0; h < k; ++h) {
+      if (o_.all_relations) {
+        for (int r = 0; r < g.num_rels(); ++r) hop_rels_[h].push_back(r);
+        continue;
+      }
+      if (static_cast<int>(o_.hop_relations.size()) != k)
+        throw std::invalid_argument("hop_relations must have one entry per hop");
+      for (int r : o_.hop_relations[h])
+        if (r >= 0 && r < g.num_rels()) hop_rels_[h].push_back(r);
+      std::sort(hop_rels_[h].begin(), hop_rels_[h].end());
+      hop_rels_[h].erase(std::unique(hop_rels_[h].begin(), hop_rels_[h].end()), hop_rels_[h].end());
+    }
+  }
 
   // max in-degree per relation tightens the edge capacities
   maxdeg_.assign(g.num_rels(), 0);
@@ -213,6 +230,11 @@ void Engine::build_plan(const Graph& g) {
       throw std::invalid_argument("too many relations in one hop");
   }
 
+  for (auto& b : blocks_) {
+    b.din = b.hop == k ? g.types[b.src_t].dim : o_.hidden;
+    b.ld_mean = round_up4(std::max(1, b.din));
+  }
+  if (o_.sample_only) return;
   // model slots present in the (local) tree: W_{r,l}, l = k - depth + 1 (hgnn.cpp:39-62)
   const ModelInit mi = init_model(g, tree_, o_.hidden, o_.model_seed);
   for (const auto& [id, w] : mi.weights) {
@@ -305,6 +327,7 @@ void Engine::upload(const Graph& g) {
   }
   // feature / learnable tables of the leaf types (layer-0 inputs)
   tables_.assign(ntypes_, TypeTable{});
+  if (!o_.sample_only) {
   std::vector<bool> leaf(ntypes_, false);
   for (const auto& b : blocks_)
     if (b.hop == k) leaf[b.src_t] = true;
@@ -353,6 +376,7 @@ void Engine::upload(const Graph& g) {
     HG_CUDA(cudaMemcpyAsync(s.w, host.data(), bytes, cudaMemcpyHostToDevice, st_));
     HG_CUDA(cudaStreamSynchronize(st_));
   }
+  }  // !sample_only
 
   // frontier machinery: one bitmap region for all types
   word_base_.assign(ntypes_ + 1, 0);
@@ -397,7 +421,7 @@ void Engine::upload(const Graph& g) {
     b.src = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(b.edge_cap) * 4));
     b.erow = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(b.edge_cap) * 4));
     b.col = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(b.edge_cap) * 4));
-    b.mean = static_cast<float*>(alloc(static_cast<std::size_t>(b.rows_cap) * b.ld_mean * 4));
+    if (!o_.sample_only) b.mean = static_cast<float*>(alloc(static_cast<std::size_t>(b.rows_cap) * b.ld_mean * 4));
     if (b.need_src_grad) b.dmean = static_cast<float*>(alloc(static_cast<std::size_t>(b.rows_cap) * b.ld_mean * 4));
     max_rows = std::max(max_rows, b.rows_cap + 1);
     total_rows += b.rows_cap;
@@ -932,6 +956,7 @@ StepReport Engine::finish_step() {
 }
 
 StepReport Engine::step(const NodeId* batch, int n, std::uint64_t rng_seed, int designated, bool train) {
+  if (o_.sample_only) throw std::invalid_argument("a sampler engine has no model to step");
   if (n > o_.batch_cap) throw std::invalid_argument("batch larger than the engine's batch capacity");
   for (int i = 0; i < n; ++i)
     if (batch[i] >= type_counts_[target_])

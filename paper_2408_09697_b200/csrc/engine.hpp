@@ -40,6 +40,11 @@ struct EngineOptions {
   std::uint64_t learn_seed = 0;  // init_learnable seed
   int device = 0;
   int elem_bytes = 4;  // byte accounting of partial messages (AccountingModel)
+  // sampler-only engines (sample_khop / sample_khop_restricted, sampling.cpp:94-103):
+  // explicit per-hop relation sets replace the metatree's; no model state is built
+  bool sample_only = false;
+  bool all_relations = false;                  // sample_khop: every relation at every hop
+  std::vector<std::vector<int>> hop_relations; // sample_khop_restricted: allowed set per hop
 };
 
 // Host-visible outputs of one step (one small D2H copy).

@@ -305,6 +305,44 @@ class Engine:
         return [x for x in bytes(raw.astype(np.uint8)).decode().split(",") if x]
 
 
+class Sampler:
+    """Device sampler for sample_khop / sample_khop_restricted (sampling.cpp:94-103):
+    explicit per-hop relation sets (None = every relation at every hop)."""
+
+    def __init__(self, g: HetGraph, fanouts: Sequence[int], hop_relations: Optional[Sequence[Sequence[int]]] = None,
+                 batch_cap: int = 1024, device: int = 0):
+        if len(fanouts) == 0:
+            raise ValueError("fanouts must be non-empty")
+        fo = np.asarray(fanouts, np.int32)
+        self.k = len(fanouts)
+        self.graph = g
+        if hop_relations is None:
+            flat = cnt = None
+        else:
+            if len(hop_relations) != len(fanouts):
+                raise ValueError("hop_relations must have one entry per hop")
+            flat = np.asarray([r for h in hop_relations for r in h] or [-1], np.int32)
+            cnt = np.asarray([len(h) for h in hop_relations], np.int32)
+        self._h = N.lib().hg_sampler_create(g.handle, N.ptr(fo), len(fo), N.ptr(flat), N.ptr(cnt), batch_cap, device)
+        if not self._h:
+            N.raise_last()
+
+    def __del__(self):
+        if getattr(self, "_h", None) and N._lib is not None:
+            N._lib.hg_engine_free(self._h)
+            self._h = None
+
+    def sample(self, seeds, rng_seed: int) -> Dict[str, np.ndarray]:
+        """frontier{h}.t{t} and hop{h}.rel{r}.{dst_ids,indptr,src_ids} of one call."""
+        b = np.ascontiguousarray(seeds, dtype=np.uint32)
+        if b.size == 0:
+            raise ValueError("empty batch")
+        N.check(N.lib().hg_engine_sample(self._h, N.ptr(b), len(b), rng_seed))
+        names = [x for x in bytes(N.take(N.lib().hg_engine_read(self._h, b"?"))["names"].astype(np.uint8)).decode()
+                 .split(",") if x.startswith(("frontier", "hop")) and not x.endswith(".col")]
+        return N.take(N.lib().hg_engine_read(self._h, ",".join(names).encode()))
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(256)
     n = N.check(N.lib().hg_nccl_unique_id(buf, 256))
