@@ -213,7 +213,7 @@ void Engine::build_plan(const Graph& g) {
       b.src_t = rel_src_[r];
       b.dst_t = rel_dst_[r];
       b.rows_cap = front(h - 1, b.dst_t).cap;
-      if (h == 1 && replica_) b.rows_cap = static_cast<int>(ceil_div(o_.batch_cap, shard_count_));
+      if (h == 1 && replica_ && b.dst_t == target_) b.rows_cap = static_cast<int>(ceil_div(o_.batch_cap, shard_count_));
       const std::uint64_t per_row = std::min<std::uint64_t>(o_.fanouts[h - 1], maxdeg_[r]);
       const std::uint64_t ec = std::max<std::uint64_t>(1, static_cast<std::uint64_t>(b.rows_cap) * per_row);
       if (ec > 0x7fffffffULL) throw std::invalid_argument("block edge capacity exceeds 2^31");
@@ -577,14 +577,9 @@ void Engine::run_sampling() {
     frontier_compact(f0, lb_, st_);
     batch_multiplicity(d_batch_, d_sc_, o_.batch_cap, f0.t[0], mult_, st_);
   });
-  const std::uint32_t* hop1_rows = front(0, target_).list;
-  const int* hop1_n = front(0, target_).count;
-  if (replica_) {
+  if (replica_)
     k_shard_rows<<<4, 256, 0, st_>>>(front(0, target_).list, front(0, target_).count, shard_index_, shard_count_,
                                      shard_list_, shard_count_dev_);
-    hop1_rows = shard_list_;
-    hop1_n = shard_count_dev_;
-  }
 
   for (int h = 1; h <= k; ++h) {
     SampleHop sh{};
@@ -595,8 +590,8 @@ void Engine::run_sampling() {
       SampleBlock& s = sh.b[sh.nblk++];
       s.csr_ptr = csr_ptr_[b.rel];
       s.csr_src = csr_src_[b.rel];
-      s.dst_list = h == 1 ? hop1_rows : front(h - 1, b.dst_t).list;
-      s.n_rows = h == 1 ? hop1_n : front(h - 1, b.dst_t).count;
+      s.dst_list = block_dst(b);
+      s.n_rows = block_rows(b);
       s.indptr = b.indptr;
       s.src_ids = b.src;
       s.erow = b.erow;
@@ -641,7 +636,7 @@ void Engine::run_sampling() {
   EdgeCountArgs ec{};
   for (const auto& b : blocks_) {
     ec.indptr[ec.n] = b.indptr;
-    ec.n_rows[ec.n] = b.hop == 1 ? hop1_n : front(b.hop - 1, b.dst_t).count;
+    ec.n_rows[ec.n] = block_rows(b);
     ++ec.n;
   }
   k_count_edges<<<1, 32, 0, st_>>>(ec, edges_dev_);
@@ -649,7 +644,7 @@ void Engine::run_sampling() {
     AlgBytesArgs ab{};
     for (const auto& b : blocks_) {
       ab.indptr[ab.nblk] = b.indptr;
-      ab.n_rows[ab.nblk] = b.hop == 1 ? hop1_n : front(b.hop - 1, b.dst_t).count;
+      ab.n_rows[ab.nblk] = block_rows(b);
       ab.din[ab.nblk] = b.din;
       ab.cls[ab.nblk] = b.hop == 1 ? 2 : 1;
       ++ab.nblk;
@@ -692,7 +687,7 @@ void Engine::run_forward() {
         m.ld_h = sg->ld;
       }
       m.din = b.din;
-      m.n_rows = b.hop == 1 ? (replica_ ? shard_count_dev_ : front(0, target_).count) : front(b.hop - 1, b.dst_t).count;
+      m.n_rows = block_rows(b);
       m.rows_cap = b.rows_cap;
       m.mean = b.mean;
       m.ld_mean = b.ld_mean;
@@ -845,7 +840,7 @@ CscHop Engine::csc_hop(int h) {
     e.col = b.col;
     e.erow = b.erow;
     e.indptr = b.indptr;
-    e.n_rows = b.hop == 1 ? (replica_ ? shard_count_dev_ : front(0, target_).count) : front(b.hop - 1, b.dst_t).count;
+    e.n_rows = block_rows(b);
     e.cap = b.edge_cap;
     e.edge_base = b.edge_base;
     e.type = slot[b.src_t];
@@ -1049,7 +1044,7 @@ std::vector<std::vector<std::uint32_t>> Engine::presample_hotness(int epochs, st
       // +1 per seed, +1 per sampled source occurrence (cache.cpp:51-56)
       hotness_add_list(front(0, target_).list, front(0, target_).count, o_.batch_cap, counts[target_], st_);
       for (const auto& b : blocks_)
-        hotness_add(b.src, b.indptr, b.hop == 1 ? front(0, target_).count : front(b.hop - 1, b.dst_t).count,
+        hotness_add(b.src, b.indptr, block_rows(b),
                     b.edge_cap, counts[b.src_t], st_);
       // pinned staging buffers are reused: wait before the next batch
       HG_CUDA(cudaStreamSynchronize(st_));
@@ -1160,7 +1155,7 @@ bool Engine::read_tensor(const std::string& name, std::string& dtype, std::vecto
     return true;
   };
   auto n_rows_of_block = [&](const BlockBuf& b) {
-    if (b.hop == 1 && replica_) return dev_int(shard_count_dev_);
+    if (b.hop == 1 && b.dst_t == target_ && replica_) return dev_int(shard_count_dev_);
     return dev_int(front(b.hop - 1, b.dst_t).count);
   };
   for (int h = 0; h <= k; ++h)
@@ -1176,7 +1171,7 @@ bool Engine::read_tensor(const std::string& name, std::string& dtype, std::vecto
     std::uint32_t total = 0;
     HG_CUDA(cudaMemcpy(&total, b.indptr + n, 4, cudaMemcpyDeviceToHost));
     if (name == p + ".dst_ids")
-      return u32s(b.hop == 1 ? (replica_ ? shard_list_ : front(0, target_).list) : front(b.hop - 1, b.dst_t).list, n);
+      return u32s(block_dst(b), n);
     if (name == p + ".indptr") return u32s(b.indptr, n + 1);
     if (name == p + ".src_ids") return u32s(b.src, total);
     if (name == p + ".col") return u32s(b.col, total);

@@ -183,6 +183,16 @@ class Engine {
   void run_update();
   void timed(const char* name, double bytes, const std::function<void()>& f);
   Front& front(int h, int t) { return fronts_[h * ntypes_ + t]; }
+  // destination rows of a block: frontier[hop-1][dst type]; hop-1 blocks into the
+  // target read the replica's shard of the batch when the partition is a replica
+  const int* block_rows(const BlockBuf& b) {
+    if (b.hop == 1 && b.dst_t == target_ && replica_) return shard_count_dev_;
+    return front(b.hop - 1, b.dst_t).count;
+  }
+  const std::uint32_t* block_dst(const BlockBuf& b) {
+    if (b.hop == 1 && b.dst_t == target_ && replica_) return shard_list_;
+    return front(b.hop - 1, b.dst_t).list;
+  }
   int out_dim(int layer) const { return layer == o_.k ? num_classes_ : o_.hidden; }
 
   EngineOptions o_;
