@@ -156,8 +156,13 @@ void hg_engine_profile(hg_engine* e, int on);
 hg_bundle* hg_engine_profile_read(hg_engine* e);
 int hg_engine_info(hg_engine* e, uint64_t* param_count, uint64_t* device_bytes, int* model_step);
 /* options: "retain_grads" (keep learnable-row gradients readable as grad.f.*; default 1),
- * "graphs" (replay the step as a CUDA graph; default 1) */
+ * "graphs" (replay the step as a CUDA graph; default 1), "umma" (dense contractions on
+ * tcgen05 tensor cores, 3xTF32; 0 = SIMT fp32 tiles for A/B checks; default 1) */
 int hg_engine_set_option(hg_engine* e, const char* name, int value);
+/* Device self-test of the tcgen05 contractions against the fp32 SIMT tiles on random
+ * problems: cases = n_cases x (rows, nrel, din, dout); err = [n_cases x 3] relative
+ * errors of (projection, mean gradient, weight gradient). */
+hg_bundle* hg_selftest_contractions(const int* cases, int n_cases, int device);
 /* kernel launches of one step (a captured, never executed step; NCCL kernels excluded) */
 int hg_engine_count_launches(hg_engine* e, int n, int train);
 

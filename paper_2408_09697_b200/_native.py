@@ -88,6 +88,7 @@ def lib():
             "hg_engine_profile_read": ([vp], vp),
             "hg_engine_info": ([vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_int)], i32),
             "hg_engine_count_launches": ([vp, i32, i32], i32),
+            "hg_selftest_contractions": ([vp, i32, i32], vp),
             "hg_engine_set_option": ([vp, C.c_char_p, i32], i32),
             "hg_engine_presample_hotness": ([vp, i32, u64, i32], vp),
             "hg_cache_plan": ([vp, vp, u64, C.c_double, C.c_double, C.c_double, i32], vp),

@@ -9,6 +9,7 @@
 
 #include "../../include/hetgpu.h"
 #include "engine.hpp"
+#include "gemm.cuh"
 #include "host.hpp"
 
 #ifdef HG_WITH_NCCL
@@ -480,9 +481,25 @@ int hg_engine_set_option(hg_engine* e, const char* name, int value) {
       e->e->set_retain_grads(value != 0);
     else if (n == "graphs")
       e->e->set_graphs(value != 0);
+    else if (n == "umma")
+      e->e->set_umma(value != 0);
     else
       throw std::invalid_argument("unknown engine option: " + n);
     return 0;
+  });
+}
+
+hg_bundle* hg_selftest_contractions(const int* cases, int n_cases, int device) {
+  return guard<hg_bundle*>(nullptr, [&] {
+    HG_CUDA(cudaSetDevice(device));
+    std::vector<std::vector<int>> cs;
+    for (int i = 0; i < n_cases; ++i) cs.push_back({cases[4 * i], cases[4 * i + 1], cases[4 * i + 2], cases[4 * i + 3]});
+    const auto errs = selftest_contractions(cs);
+    std::vector<double> flat;
+    for (const auto& e : errs) flat.insert(flat.end(), e.begin(), e.end());
+    auto* b = new hg_bundle;
+    b->add("err", "<f8", flat, {static_cast<long long>(errs.size()), 3});
+    return b;
   });
 }
 

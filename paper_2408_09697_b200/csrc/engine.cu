@@ -718,7 +718,7 @@ void Engine::run_forward() {
         pg.r[q] = {b.mean, b.ld_mean, b.din, s.w, s.ld};
       }
     }
-    timed(top ? "project_top" : "project", 0, [&] { project_tiles(pb, st_); });
+    timed(top ? "project_top" : "project", 0, [&] { use_umma_ ? project_umma(pb, st_) : project_tiles(pb, st_); });
   }
   // AGG_all: sum the partial logits of every partition (raf.cpp:427-446)
   if (o_.p > 1) {
@@ -797,8 +797,8 @@ void Engine::run_backward() {
           db.p[db.np++] = {dv, s.w, s.ld, b.din, b.indptr, n_rows, rows_cap, b.dmean, b.ld_mean};
       }
     }
-    timed("weight_grad", 0, [&] { wgrad_tiles(wb, st_); });
-    timed("mean_grad", 0, [&] { dmean_tiles(db, st_); });
+    timed("weight_grad", 0, [&] { use_umma_ ? wgrad_umma(wb, st_) : wgrad_tiles(wb, st_); });
+    timed("mean_grad", 0, [&] { use_umma_ ? dmean_umma(db, st_) : dmean_tiles(db, st_); });
     // scatter back to the sources of this hop, as ordered gathers (learnable
     // layer-0 rows get their Adam update in the same pass)
     const CscHop ch = csc_hop(d);

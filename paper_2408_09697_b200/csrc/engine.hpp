@@ -80,6 +80,12 @@ class Engine {
   void enqueue_step_device(const StepScalars* d_src, const std::uint32_t* d_ids, int n, bool train);
   StepScalars next_scalars(std::uint64_t rng_seed, int n, int designated, bool train);
   void set_graphs(bool on) { use_graphs_ = on; }
+  void set_umma(bool on) {
+    if (on != use_umma_) {
+      use_umma_ = on;
+      drop_graphs();
+    }
+  }
   // keep the learnable-row gradients in memory (grad.f.* tensors); the bench
   // turns this off so the sparse Adam update consumes them in registers
   void set_retain_grads(bool on) {
@@ -279,6 +285,7 @@ class Engine {
   void step_body(bool train);
   void launch_body(bool train);
   bool use_graphs_ = true;
+  bool use_umma_ = true;  // tcgen05 contractions (0: SIMT fp32 tiles, kept for A/B checks)
   bool retain_grads_ = true;
   struct CscRegion {
     std::uint32_t *offs, *cursor;

@@ -1,6 +1,8 @@
 // Multi-problem tile kernels for the dense contractions (gemm_kernels.cu).
 #pragma once
 
+#include <vector>
+
 #include "kernels.cuh"
 
 namespace hetgpu {
@@ -99,5 +101,16 @@ struct ProjBatch {
 void project_tiles(ProjBatch& p, cudaStream_t st);
 void wgrad_tiles(WGradBatch& b, cudaStream_t st);
 void dmean_tiles(DMeanBatch& b, cudaStream_t st);
+// ordered (deterministic) sum of the split-K weight-gradient partials into dW
+void wgrad_reduce(WGradBatch& b, cudaStream_t st);
+
+// tcgen05 (kind::tf32, 3xTF32 split) versions of the three contractions (umma_kernels.cu)
+void project_umma(ProjBatch& p, cudaStream_t st);
+void wgrad_umma(WGradBatch& b, cudaStream_t st);
+void dmean_umma(DMeanBatch& b, cudaStream_t st);
+
+// self-test (selftest.cu): cases (rows, nrel, din, dout) -> {project, dmean, wgrad}
+// max|tcgen05 - fp32 tiles| / max|fp32 tiles|
+std::vector<std::vector<double>> selftest_contractions(const std::vector<std::vector<int>>& cases);
 
 }  // namespace hetgpu

@@ -442,9 +442,13 @@ void wgrad_tiles(WGradBatch& b, cudaStream_t st) {
                               ceil_div(P.d.cols, kTile));
   }
   k_wgrad_tiles<<<std::max(1, tiles), kT, 0, st>>>(b);
+  wgrad_reduce(b, st);
+}
+
+void wgrad_reduce(WGradBatch& b, cudaStream_t st) {
   int total_out = 0;
   for (int p = 0; p < b.np; ++p) total_out += b.p[p].din * b.p[p].d.cols;
-  k_wgrad_reduce<<<static_cast<unsigned>(ceil_div(total_out, 256)), 256, 0, st>>>(b, total_out);
+  if (total_out > 0) k_wgrad_reduce<<<static_cast<unsigned>(ceil_div(total_out, 256)), 256, 0, st>>>(b, total_out);
 }
 
 void dmean_tiles(DMeanBatch& b, cudaStream_t st) {

@@ -166,8 +166,8 @@ constexpr int kSlowThreads = 4096;  // concurrent slow-path rows (global scratch
 // positions lets most lookups skip the scan. Returns false if the streaming
 // engine ran dry (the caller replays the row on MtFull).
 template <int MAXF, typename Eng>
-__device__ __forceinline__ bool draw_row_smem(Eng& eng, std::uint64_t deg, int fanout, const std::uint32_t* nbr,
-                                              std::uint32_t* out, std::uint32_t* mpos, std::uint32_t* mval) {
+__device__ __forceinline__ bool draw_positions_smem(Eng& eng, std::uint64_t deg, int fanout, std::uint32_t* out,
+                                                    std::uint32_t* mpos, std::uint32_t* mval) {
   // mpos/mval point at this lane's column: element q at [q * kSampleThreads]
   unsigned long long filt = 0ull;
   int nmap = 0;
@@ -197,7 +197,7 @@ __device__ __forceinline__ bool draw_row_smem(Eng& eng, std::uint64_t deg, int f
       }
       mval[slot_j * kSampleThreads] = vi;
     }
-    out[i] = nbr[vj];
+    out[i] = vj;  // position in the CSR row; the warp gathers the ids afterwards
   }
   (void)MAXF;
   return true;
@@ -276,13 +276,36 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_fused(SampleHop h, Lb
   if (live) b.indptr[i + 1] = o + cnt;
   if (i == 0) b.indptr[0] = 0;
 
-  // Warp-flattened writes: the warp's 32 consecutive rows own one contiguous
-  // output range, so every lane takes independent edges q = lane, lane+32, ...
-  // (row found by a shuffle binary search over the warp's inclusive counts):
-  // the row index of every edge, and the copy-all rows (deg <= fanout) in CSR
-  // order (sampling.cpp:22-25). Loads are independent across lanes.
+  // Phase 1 — RNG rows (deg > fanout): one lane per row runs the exact
+  // mt19937_64 + Lemire + partial Fisher-Yates and records the drawn CSR
+  // positions in its output slots. Rows that overflow the streaming engine (or
+  // the shared-memory map) go to the slow list and are skipped below.
+  bool rng_ok = false;
+  if (live && deg > fo) {
+    if (h.fanout <= MAXF) {
+      const std::uint64_t rel_key = (static_cast<std::uint64_t>(h.hop) << 32) | static_cast<std::uint64_t>(b.rel);
+      MtStream eng;
+      eng.seed(dmix_seed(sc->rng_seed, dmix_seed(rel_key, d)));
+      rng_ok = draw_positions_smem<MAXF>(eng, deg, h.fanout, b.src_ids + o, s_map + threadIdx.x,
+                                         s_map + MAXF * kSampleThreads + threadIdx.x);
+    }
+    if (!rng_ok) {
+      const int q = atomicAdd(n_slow, 1);
+      slow[2 * q] = static_cast<std::uint32_t>(bi);
+      slow[2 * q + 1] = static_cast<std::uint32_t>(i);
+    }
+  }
+  __syncwarp();
+
+  // Phase 2 — warp-flattened gather: the warp's 32 consecutive rows own one
+  // contiguous output range, so lane l takes edges q = l, l+32, ... (row found
+  // by a shuffle binary search over the warp's inclusive counts). Copy-all rows
+  // (sampling.cpp:22-25) read the CSR slice in order; RNG rows read the drawn
+  // positions back. kUnroll edges per lane are resolved first and their loads
+  // issued together, so a lane keeps several independent DRAM reads in flight.
   const int lane = threadIdx.x & 31;
-  const unsigned copy_mask = __ballot_sync(0xffffffffu, live && deg <= fo);
+  const unsigned take_mask = __ballot_sync(0xffffffffu, live && (deg <= fo || rng_ok));
+  const unsigned rng_mask = __ballot_sync(0xffffffffu, rng_ok);
   std::uint32_t wincl = cnt;
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
@@ -292,38 +315,43 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_fused(SampleHop h, Lb
   const std::uint32_t wtotal = __shfl_sync(0xffffffffu, wincl, 31);
   const std::uint32_t o0 = __shfl_sync(0xffffffffu, o, 0);
   const std::uint32_t row_base = static_cast<std::uint32_t>(base + (threadIdx.x & ~31));
-  for (std::uint32_t q0 = 0; q0 < wtotal; q0 += 32) {  // warp-uniform trip count
-    const std::uint32_t q = q0 + lane;
-    int r = 0;  // smallest lane r with wincl[r] > q
+  constexpr int kUnroll = 4;
+  for (std::uint32_t q0 = 0; q0 < wtotal; q0 += 32 * kUnroll) {  // warp-uniform trip count
+    std::uint32_t at[kUnroll], pos[kUnroll];
+    std::uint64_t rlo[kUnroll];
+    int rr[kUnroll];
+    bool ok[kUnroll], rng[kUnroll];
 #pragma unroll
-    for (int step = 16; step > 0; step >>= 1) {
-      const std::uint32_t v = __shfl_sync(0xffffffffu, wincl, r + step - 1);
-      if (v <= q) r += step;
+    for (int u = 0; u < kUnroll; ++u) {
+      const std::uint32_t q = q0 + 32 * u + lane;
+      int r = 0;  // smallest lane r with wincl[r] > q
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const std::uint32_t v = __shfl_sync(0xffffffffu, wincl, r + step - 1);
+        if (v <= q) r += step;
+      }
+      r = min(r, 31);
+      const std::uint32_t rincl = __shfl_sync(0xffffffffu, wincl, r);
+      const std::uint32_t rcnt = __shfl_sync(0xffffffffu, cnt, r);
+      rlo[u] = __shfl_sync(0xffffffffu, lo, r);
+      rr[u] = r;
+      at[u] = o0 + q;
+      ok[u] = q < wtotal && ((take_mask >> r) & 1u);
+      rng[u] = (rng_mask >> r) & 1u;
+      pos[u] = q - (rincl - rcnt);
     }
-    r = min(r, 31);
-    const std::uint32_t rincl = __shfl_sync(0xffffffffu, wincl, r);
-    const std::uint32_t rcnt = __shfl_sync(0xffffffffu, cnt, r);
-    const std::uint64_t rlo = __shfl_sync(0xffffffffu, lo, r);
-    if (q < wtotal) {
-      b.erow[o0 + q] = row_base + static_cast<std::uint32_t>(r);
-      if ((copy_mask >> r) & 1u) b.src_ids[o0 + q] = b.csr_src[rlo + (q - (rincl - rcnt))];
-    }
-  }
-  if (live && deg > fo) {
-    bool done = false;
-    if (h.fanout <= MAXF) {
-      const std::uint64_t rel_key = (static_cast<std::uint64_t>(h.hop) << 32) | static_cast<std::uint64_t>(b.rel);
-      MtStream eng;
-      eng.seed(dmix_seed(sc->rng_seed, dmix_seed(rel_key, d)));
-      done = draw_row_smem<MAXF>(eng, deg, h.fanout, b.csr_src + lo, b.src_ids + o, s_map + threadIdx.x,
-                                 s_map + MAXF * kSampleThreads + threadIdx.x);
-    }
-    if (!done) {
-      // more than 156 engine outputs (Lemire rejections) or a fanout above the
-      // register map: replay on the full-state engine in a second pass
-      const int q = atomicAdd(n_slow, 1);
-      slow[2 * q] = static_cast<std::uint32_t>(bi);
-      slow[2 * q + 1] = static_cast<std::uint32_t>(i);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (ok[u] && rng[u]) pos[u] = b.src_ids[at[u]];
+    std::uint32_t val[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (ok[u]) val[u] = __ldg(b.csr_src + rlo[u] + pos[u]);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const std::uint32_t q = q0 + 32 * u + lane;
+      if (q < wtotal) b.erow[o0 + q] = row_base + static_cast<std::uint32_t>(rr[u]);
+      if (ok[u]) b.src_ids[at[u]] = val[u];
     }
   }
 }

@@ -109,3 +109,45 @@ def test_raf_training_trajectory(H, ref, name):
         if n.startswith("final.learn.t") and "post.learn.t" + n.split(".t")[-1] in got:
             key = "post.learn.t" + n.split(".t")[-1]
             assert_adam_close(got[key], want[n], None, max_flip_frac=5e-3, what=f"{name}: {key}")
+
+
+@pytest.mark.parametrize("name", ["mag-mini", "donor-mini"])
+def test_tensor_core_contractions_match_fp32_tiles(H, name):
+    # The tcgen05 (3xTF32) projection / weight-grad / mean-grad kernels against
+    # the SIMT fp32 tile kernels on identical inputs: fp32-level agreement
+    # (tf32 split error ~2^-21), far inside the 1e-3 parity budget.
+    g = H.gen_synthetic(H.bundled_spec(name), 4)
+    batch = list(range(0, 600, 2))
+    outs = []
+    for umma in (0, 1):
+        eng = H.Engine(g, [10, 5], hidden=32, batch_cap=512, model_seed=5, learn_seed=6)
+        eng.set_option("umma", umma)
+        eng.step(batch, 99, 0, train=True)
+        # H2.* (layer-0 learnable rows) and post.* are read after Adam, whose
+        # +-lr steps flip for gradients at rounding level: compared separately
+        names = [n for n in eng.tensor_names()
+                 if n.startswith(("H0", "H1", "logits", "dlogits", "grad.w.", "grad.f."))]
+        outs.append(eng.read(*names))
+    simt, tc = outs
+    for n in simt:
+        if n.endswith(".ids"):
+            assert np.array_equal(simt[n], tc[n]), n
+        else:
+            assert_close(tc[n], simt[n], 2e-5, f"{name}: {n} (tcgen05 vs fp32 tiles)")
+
+
+def test_tensor_core_tile_shapes():
+    # every tile width (32/64/128 columns, multi-tile 349), partial row tiles,
+    # K chunk counts (din not a multiple of 4 / 32), 1-3 relations per group,
+    # split-K chunk edges (255/256/257 rows): tcgen05 vs fp32 tiles
+    import ctypes as C
+    from paper_2408_09697_b200 import _native as N
+    cases = []
+    for rows in (1, 7, 128, 257, 1000):
+        for nrel, din, dout in ((1, 2, 3), (2, 5, 8), (3, 17, 33), (1, 32, 64), (2, 64, 64), (3, 128, 64),
+                                (1, 64, 349), (2, 100, 100), (1, 128, 128), (3, 64, 349)):
+            cases.append((rows, nrel, din, dout))
+    arr = np.asarray(cases, np.int32).ravel()
+    err = N.take(N.lib().hg_selftest_contractions(N.ptr(arr), len(cases), 0))["err"]
+    bad = [(cases[i], err[i].tolist()) for i in range(len(cases)) if not np.all(err[i] < 2e-5)]
+    assert not bad, bad[:8]
