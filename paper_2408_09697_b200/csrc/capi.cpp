@@ -334,8 +334,11 @@ hg_engine* hg_sampler_create(const hg_graph* g, const int* fanouts, int k, const
 }
 
 void hg_engine_free(hg_engine* e) {
+  if (!e) return;
+  // the engine first: its captured step graphs hold NCCL work on the communicator
+  e->e.reset();
 #ifdef HG_WITH_NCCL
-  if (e && e->comm) ncclCommDestroy(e->comm);
+  if (e->comm) ncclCommDestroy(e->comm);
 #endif
   delete e;
 }

@@ -63,34 +63,44 @@ __global__ void k_gather_rows(const float* table, int ld, const std::uint32_t* i
 }
 
 // Algorithmic bytes of the main kernel classes for one step, accumulated on
-// the device (SURVEY §8(d) formulas): [0] sample, [1] aggregate (inner layers),
-// [2] aggregate_top (layer k).
+// the device (SURVEY §8(d) formulas): [0] sample, [1] aggregate (layer 1, hop-k
+// blocks), [2] aggregate_top (hop-1 blocks), [3] csc_gather (backward gather +
+// fused sparse Adam).
 struct AlgBytesArgs {
   const std::uint32_t* indptr[kMaxBlocks * 4];
   const int* n_rows[kMaxBlocks * 4];
   int din[kMaxBlocks * 4];
   int cls[kMaxBlocks * 4];  // 1 inner aggregate, 2 top aggregate
   int nblk;
-  const int* g_rows[kMaxBlocks * 4];
-  int g_dout[kMaxBlocks * 4];
-  int g_cls[kMaxBlocks * 4];
-  int ngrp;
+  int grad[kMaxBlocks * 4];  // block feeds a source gradient (its edges are gathered by csc_gather)
+  // csc_gather per (hop, source type): live source rows, row width, bytes per row
+  const int* c_rows[kMaxBlocks * 4];
+  int c_din[kMaxBlocks * 4];
+  int c_row_bytes_mult[kMaxBlocks * 4];  // 1: dH write; 6: fused Adam (w, m, v read + write); 7: both
+  int ncsc;
 };
 
 __global__ void k_alg_bytes(AlgBytesArgs a, double* acc) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double s = 0, agg[3] = {0, 0, 0};
+  double s = 0, agg[3] = {0, 0, 0}, csc = 0;
   for (int i = 0; i < a.nblk; ++i) {
     const double R = *a.n_rows[i], E = a.indptr[i][*a.n_rows[i]];
     // sampling: indptr pair + dst id read, neighbour reads, src write, offset write
     s += 16.0 * R + 4.0 * R + 4.0 * E + 4.0 * E + 4.0 * R;
     // aggregation: per edge one source row + its id; offsets; tape write
     agg[a.cls[i]] += E * (4.0 * a.din[i] + 4.0) + 4.0 * (R + 1) + 4.0 * R * a.din[i];
+    // backward gather: per edge one dmean row + the edge id
+    if (a.grad[i]) csc += E * (4.0 * a.din[i] + 4.0);
   }
-  for (int i = 0; i < a.ngrp; ++i) agg[a.g_cls[i]] += 4.0 * static_cast<double>(*a.g_rows[i]) * a.g_dout[i];
+  // per source row: segment offsets + the gradient row (or the fused Adam row update)
+  for (int i = 0; i < a.ncsc; ++i) {
+    const double n = *a.c_rows[i];
+    csc += 4.0 * (n + 1) + n * 4.0 * a.c_din[i] * a.c_row_bytes_mult[i];
+  }
   acc[0] += s;
   acc[1] += agg[1];
   acc[2] += agg[2];
+  acc[3] += csc;
 }
 
 template <typename T>
@@ -647,7 +657,15 @@ void Engine::run_sampling() {
       ab.n_rows[ab.nblk] = block_rows(b);
       ab.din[ab.nblk] = b.din;
       ab.cls[ab.nblk] = b.hop == 1 ? 2 : 1;
+      ab.grad[ab.nblk] = b.need_src_grad ? 1 : 0;
       ++ab.nblk;
+    }
+    for (const auto& c : cscs_) {
+      const bool leaf_learnable = c.hop == o_.k && tables_[c.src_t].learnable;
+      ab.c_rows[ab.ncsc] = front(c.hop, c.src_t).count;
+      ab.c_din[ab.ncsc] = c.din;
+      ab.c_row_bytes_mult[ab.ncsc] = leaf_learnable ? (retain_grads_ ? 7 : 6) : 1;
+      ++ab.ncsc;
     }
     k_alg_bytes<<<1, 32, 0, st_>>>(ab, alg_bytes_);
   }
@@ -730,7 +748,7 @@ void Engine::run_forward() {
     k_active_rows<<<1, 256, 0, st_>>>(ec, replica_ ? shard_count_dev_ : front(0, target_).count,
                                       logits_ + static_cast<std::size_t>(o_.batch_cap) * ldc_ + o_.rank);
 #ifdef HG_WITH_NCCL
-    if (comm_) {
+    if (comm_ && !counting_) {
       timed("agg_all", static_cast<double>(o_.batch_cap + 1) * ldc_ * 4, [&] {
         if (ncclAllReduce(logits_, logits_, static_cast<std::size_t>(o_.batch_cap + 1) * ldc_, ncclFloat, ncclSum,
                           comm_, st_) != ncclSuccess)
@@ -964,8 +982,11 @@ StepReport Engine::step(const NodeId* batch, int n, std::uint64_t rng_seed, int 
 
 int Engine::count_launches(int n, bool train) {
   // capture one step (without executing it) and count our kernel nodes
+  // the collective is left out of this capture: a captured-but-never-launched
+  // NCCL call would desynchronise the ranks (NCCL kernels are not counted anyway)
   const bool prof = profiling_;
   profiling_ = false;
+  counting_ = true;
   cudaGraph_t graph = nullptr;
   HG_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
   (void)n;
@@ -975,10 +996,12 @@ int Engine::count_launches(int n, bool train) {
     cudaStreamEndCapture(st_, &graph);
     if (graph) cudaGraphDestroy(graph);
     profiling_ = prof;
+    counting_ = false;
     throw;
   }
   HG_CUDA(cudaStreamEndCapture(st_, &graph));
   profiling_ = prof;
+  counting_ = false;
   std::size_t nn = 0;
   HG_CUDA(cudaGraphGetNodes(graph, nullptr, &nn));
   std::vector<cudaGraphNode_t> nodes(nn);

@@ -124,7 +124,7 @@ class Engine {
   // kernel launches of one step, counted from a captured (not executed) step
   int count_launches(int n, bool train);
   // cumulative algorithmic bytes since reset_profile (profiling on):
-  // [0] sample, [1] aggregate, [2] aggregate_top
+  // [0] sample, [1] aggregate, [2] aggregate_top, [3] csc_gather
   std::vector<double> algorithmic_bytes();
   std::map<std::string, int> kernel_launches() const { return kernel_launches_; }
   int launches_per_step() const { return launches_per_step_; }
@@ -285,7 +285,8 @@ class Engine {
   void step_body(bool train);
   void launch_body(bool train);
   bool use_graphs_ = true;
-  bool use_umma_ = true;  // tcgen05 contractions (0: SIMT fp32 tiles, kept for A/B checks)
+  bool use_umma_ = true;
+  bool counting_ = false;  // count_launches capture in progress (no collectives)  // tcgen05 contractions (0: SIMT fp32 tiles, kept for A/B checks)
   bool retain_grads_ = true;
   struct CscRegion {
     std::uint32_t *offs, *cursor;

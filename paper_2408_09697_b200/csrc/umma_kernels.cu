@@ -22,7 +22,8 @@ namespace hetgpu {
 
 namespace {
 
-constexpr int kUT = 128;             // threads per CTA
+constexpr int kUT = 256;             // threads per CTA (8 warps: 2 per TMEM lane quadrant)
+constexpr int kAV = 128 * 32 / 4 / kUT;  // A float4 per thread per chunk
 constexpr int kATile = 128 * 128;    // bytes of one 128 x 32 fp32 operand tile
 
 template <int NT>
@@ -162,8 +163,8 @@ __global__ void __launch_bounds__(kUT) k_umma(UmmaArgs<Batch> args) {
   const std::uint32_t tmem = *tmem_slot;
 
   // ---- operand loaders ------------------------------------------------------------------------
-  constexpr int kBV = NT / 16;  // B float4 per thread
-  float4 ra[8], rb[kBV];
+  constexpr int kBV = NT * 32 / 4 / kUT;  // B float4 per thread per chunk
+  float4 ra[kAV], rb[kBV];
   auto load = [&](int ch) {
     if constexpr (MODE == kProject) {
       const ProjGroup& g = args.b.g[p];
@@ -174,8 +175,8 @@ __global__ void __launch_bounds__(kUT) k_umma(UmmaArgs<Batch> args) {
       }
       const ProjRel& r = g.r[q];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {  // A: mean rows, K-contiguous
-        const int m = (tid >> 3) + 16 * i, k = k0 + (tid & 7) * 4, row = c.row0 + m;
+      for (int i = 0; i < kAV; ++i) {  // A: mean rows, K-contiguous
+        const int m = (tid >> 3) + (kUT / 8) * i, k = k0 + (tid & 7) * 4, row = c.row0 + m;
         ra[i] = (row < c.n_live && k < r.ld_mean)
                     ? __ldg(reinterpret_cast<const float4*>(r.mean + static_cast<std::size_t>(row) * r.ld_mean + k))
                     : f4zero();
@@ -191,13 +192,13 @@ __global__ void __launch_bounds__(kUT) k_umma(UmmaArgs<Batch> args) {
       const DMeanProblem& P = args.b.p[p];
       const int cols4 = (P.d.cols + 3) & ~3;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {  // A: dpre rows (ReLU mask, row remap), K-contiguous
-        const int m = (tid >> 3) + 16 * i, k = ch * 32 + (tid & 7) * 4, row = c.row0 + m;
+      for (int i = 0; i < kAV; ++i) {  // A: dpre rows (ReLU mask, row remap), K-contiguous
+        const int m = (tid >> 3) + (kUT / 8) * i, k = ch * 32 + (tid & 7) * 4, row = c.row0 + m;
         ra[i] = (row < c.n_live && k < cols4) ? load_dpre(P.d, row, k) : f4zero();
       }
 #pragma unroll
       for (int i = 0; i < kBV; ++i) {  // B[n=c][k=j] = W[c][j]: K-contiguous
-        const int n = c.n0 + (tid >> 3) + 16 * i, k = ch * 32 + (tid & 7) * 4;
+        const int n = c.n0 + (tid >> 3) + (kUT / 8) * i, k = ch * 32 + (tid & 7) * 4;
         rb[i] = (n < P.din && k < P.ld_w)
                     ? __ldg(reinterpret_cast<const float4*>(P.w + static_cast<std::size_t>(n) * P.ld_w + k))
                     : f4zero();
@@ -206,8 +207,8 @@ __global__ void __launch_bounds__(kUT) k_umma(UmmaArgs<Batch> args) {
       const WGradProblem& P = args.b.p[p];
       const int cols4 = (P.d.cols + 3) & ~3;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {  // A[m=c][k=row] = mean[row][c]: M-contiguous
-        const int k = (tid >> 5) + 4 * i, m = c.m0 + (tid & 31) * 4, row = c.row0 + ch * 32 + k;
+      for (int i = 0; i < kAV; ++i) {  // A[m=c][k=row] = mean[row][c]: M-contiguous
+        const int k = (tid >> 5) + (kUT / 32) * i, m = c.m0 + (tid & 31) * 4, row = c.row0 + ch * 32 + k;
         ra[i] = (row < c.n_live && m < P.ld_mean)
                     ? *reinterpret_cast<const float4*>(P.mean + static_cast<std::size_t>(row) * P.ld_mean + m)
                     : f4zero();
@@ -223,10 +224,10 @@ __global__ void __launch_bounds__(kUT) k_umma(UmmaArgs<Batch> args) {
     std::uint8_t *ahi = st, *alo = st + kATile, *bhi = st + 2 * kATile, *blo = bhi + UStage<NT>::kB;
     if constexpr (Majors<MODE>::a) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) st_mn(ahi, alo, (tid & 31) * 4, (tid >> 5) + 4 * i, UStage<NT>::kSboA, ra[i]);
+      for (int i = 0; i < kAV; ++i) st_mn(ahi, alo, (tid & 31) * 4, (tid >> 5) + (kUT / 32) * i, UStage<NT>::kSboA, ra[i]);
     } else {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) st_kc(ahi, alo, (tid >> 3) + 16 * i, (tid & 7) * 4, ra[i]);
+      for (int i = 0; i < kAV; ++i) st_kc(ahi, alo, (tid >> 3) + (kUT / 8) * i, (tid & 7) * 4, ra[i]);
     }
     if constexpr (Majors<MODE>::b) {
 #pragma unroll
@@ -236,7 +237,7 @@ __global__ void __launch_bounds__(kUT) k_umma(UmmaArgs<Batch> args) {
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < kBV; ++i) st_kc(bhi, blo, (tid >> 3) + 16 * i, (tid & 7) * 4, rb[i]);
+      for (int i = 0; i < kBV; ++i) st_kc(bhi, blo, (tid >> 3) + (kUT / 8) * i, (tid & 7) * 4, rb[i]);
     }
   };
 
@@ -283,10 +284,14 @@ __global__ void __launch_bounds__(kUT) k_umma(UmmaArgs<Batch> args) {
   umma::fence_after_sync();
 
   // ---- epilogue: TMEM -> registers -> global ------------------------------------------------------
-  const int m = warp * 32 + lane;  // tile row owned by this thread
-  const std::uint32_t trow = tmem + (static_cast<std::uint32_t>(warp * 32) << 16);
+  // warp w reads TMEM lane quadrant (w % 4) = tile rows 32(w%4)..+31, columns
+  // [(w / 4) * NT / 2, ...) : the two warps of a quadrant split the columns
+  constexpr int kHalves = kUT / 128;
+  const int quad = warp & 3, half = warp >> 2;
+  const int m = quad * 32 + lane;  // tile row owned by this thread
+  const std::uint32_t trow = tmem + (static_cast<std::uint32_t>(quad * 32) << 16);
 #pragma unroll 1
-  for (int c0 = 0; c0 < NT; c0 += 16) {
+  for (int c0 = half * (NT / kHalves); c0 < (half + 1) * (NT / kHalves); c0 += 16) {
     float v[16];
     umma::tmem_ld16(trow + c0, v);
     if constexpr (MODE == kProject) {

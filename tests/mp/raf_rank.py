@@ -1,0 +1,49 @@
+"""One rank of a multi-GPU RAF run (one meta-partition per GPU, AGG_all over
+NCCL). Launched by tests/test_gpu_multi.py as N processes; rank 0 publishes the
+NCCL unique id through a file and writes the per-batch losses and active-row
+counts (the PartialAgg row counts, raf.cpp:418-446) to an .npz."""
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    name, seed, p, rank, id_path, out_path, n_batches, bsz = sys.argv[1:9]
+    seed, p, rank, n_batches, bsz = int(seed), int(p), int(rank), int(n_batches), int(bsz)
+    from paper_2408_09697_b200 import hetsim as H
+    g = H.gen_synthetic(H.bundled_spec(name), seed)
+    eng = H.Engine.for_experiment(g, [25, 20], 32, seed, batch_cap=bsz, p=p, rank=rank, device=rank)
+    if rank == 0:
+        uid = H.nccl_unique_id()
+        with open(id_path + ".tmp", "wb") as f:
+            f.write(uid)
+        os.replace(id_path + ".tmp", id_path)
+    else:
+        t0 = time.time()
+        while not os.path.exists(id_path):
+            if time.time() - t0 > 120:
+                raise RuntimeError("no NCCL id from rank 0")
+            time.sleep(0.05)
+        uid = open(id_path, "rb").read()
+    if os.environ.get("HG_NO_GRAPHS"):
+        eng.set_option("graphs", 0)
+    print(f"rank {rank}: attaching", flush=True)
+    eng.attach_nccl(uid, p, rank)
+    print(f"rank {rank}: attached", flush=True)
+    batches = H.make_batches(g, bsz, n_batches, H.mix_seed(seed, 0xBA7C))
+    losses, active = [], []
+    for i, b in enumerate(batches):
+        rep = eng.step(b, H.mix_seed(seed, 0xB000 + i), i % p)
+        print(f"rank {rank}: batch {i} loss {rep['loss']:.6f}", flush=True)
+        losses.append(rep["loss"])
+        active.append(rep["active_rows"])
+    np.savez(out_path, losses=np.asarray(losses), active=np.asarray(active, np.int64))
+
+
+if __name__ == "__main__":
+    main()
