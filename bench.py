@@ -187,6 +187,9 @@ def run_b200(args):
         dist.broadcast_object_list(uid, src=0)
         dbg("attaching nccl")
         eng.attach_nccl(uid[0], world, rank)
+        handles = [None] * world
+        dist.all_gather_object(handles, eng.replica_handle())
+        eng.attach_replicas(handles)
         dbg("attached")
     total_steps = args.warmup + args.steps
     need = 2 * total_steps + 2

@@ -184,6 +184,13 @@ hg_bundle* hg_engine_cache_counters(hg_engine* e);
 /* ---- multi-GPU: AGG_all over NCCL (one engine per rank) --------------------------------- */
 int hg_nccl_unique_id(void* out, int cap);
 int hg_engine_attach_nccl(hg_engine* e, const void* unique_id, int id_bytes, int nranks, int rank);
+/* Replica groups (p larger than the number of sub-metatrees; metapartition.cpp:206-236):
+ * hg_engine_replica_handle writes this engine's CUDA IPC handle of its gradient-exchange
+ * arena (returns its size; 0 if the partition has no replicas). Every rank passes the
+ * handles of all ranks (nranks x handle_bytes, rank order; any bytes for ranks without
+ * replicas) to hg_engine_attach_replicas after hg_engine_attach_nccl. */
+int hg_engine_replica_handle(hg_engine* e, void* out, int cap);
+int hg_engine_attach_replicas(hg_engine* e, const void* handles, int handle_bytes, int nranks);
 
 #ifdef __cplusplus
 }

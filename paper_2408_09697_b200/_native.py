@@ -96,6 +96,8 @@ def lib():
             "hg_engine_cache_counters": ([vp], vp),
             "hg_nccl_unique_id": ([vp, i32], i32),
             "hg_engine_attach_nccl": ([vp, vp, i32, i32, i32], i32),
+            "hg_engine_replica_handle": ([vp, vp, i32], i32),
+            "hg_engine_attach_replicas": ([vp, vp, i32, i32], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)

@@ -25,6 +25,7 @@ struct hg_engine {
   std::unique_ptr<Engine> e;
 #ifdef HG_WITH_NCCL
   ncclComm_t comm = nullptr;
+  ncclComm_t rcomm = nullptr;  // replica group (ncclCommSplit of comm)
 #endif
 };
 struct hg_bundle {
@@ -338,6 +339,7 @@ void hg_engine_free(hg_engine* e) {
   // the engine first: its captured step graphs hold NCCL work on the communicator
   e->e.reset();
 #ifdef HG_WITH_NCCL
+  if (e->rcomm) ncclCommDestroy(e->rcomm);
   if (e->comm) ncclCommDestroy(e->comm);
 #endif
   delete e;
@@ -614,6 +616,26 @@ int hg_nccl_unique_id(void* out, int cap) {
   });
 }
 
+int hg_engine_replica_handle(hg_engine* e, void* out, int cap) {
+  return guard<int>(-1, [&] {
+    const std::vector<char> h = e->e->replica_handle();
+    if (static_cast<int>(h.size()) > cap) throw std::invalid_argument("handle buffer too small");
+    if (!h.empty()) std::memcpy(out, h.data(), h.size());
+    return static_cast<int>(h.size());
+  });
+}
+
+int hg_engine_attach_replicas(hg_engine* e, const void* handles, int handle_bytes, int nranks) {
+  return guard<int>(-1, [&] {
+    std::vector<std::vector<char>> hs(nranks);
+    const char* p = static_cast<const char*>(handles);
+    for (int r = 0; r < nranks; ++r) hs[r].assign(p + static_cast<std::size_t>(r) * handle_bytes,
+                                                 p + static_cast<std::size_t>(r + 1) * handle_bytes);
+    e->e->attach_replicas(hs);
+    return 0;
+  });
+}
+
 int hg_engine_attach_nccl(hg_engine* e, const void* unique_id, int id_bytes, int nranks, int rank) {
   return guard<int>(-1, [&] {
 #ifdef HG_WITH_NCCL
@@ -621,7 +643,13 @@ int hg_engine_attach_nccl(hg_engine* e, const void* unique_id, int id_bytes, int
     if (id_bytes != static_cast<int>(sizeof(id))) throw std::invalid_argument("bad unique id size");
     std::memcpy(&id, unique_id, sizeof(id));
     if (ncclCommInitRank(&e->comm, nranks, id, rank) != ncclSuccess) throw std::runtime_error("ncclCommInitRank failed");
-    e->e->attach_comm(e->comm);
+    // every rank joins the split (collective); replicas of one sub-metatree set
+    // share a colour, the others opt out
+    const int color = e->e->replica_color();
+    if (ncclCommSplit(e->comm, color >= 0 ? color : NCCL_SPLIT_NOCOLOR, e->e->replica_pos(), &e->rcomm, nullptr) !=
+        ncclSuccess)
+      throw std::runtime_error("ncclCommSplit failed");
+    e->e->attach_comm(e->comm, e->rcomm);
     return 0;
 #else
     (void)e;

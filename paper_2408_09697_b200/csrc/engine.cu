@@ -134,6 +134,7 @@ Engine::~Engine() {
   if (exec_train_) cudaGraphExecDestroy(exec_train_);
   if (exec_eval_) cudaGraphExecDestroy(exec_eval_);
   for (auto e : ev_pool_) cudaEventDestroy(e);
+  for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
   for (void* p : allocs_) cudaFree(p);
   if (h_sc_) cudaFreeHost(h_sc_);
   if (h_batch_) cudaFreeHost(h_batch_);
@@ -159,6 +160,44 @@ void Engine::build_plan(const Graph& g) {
   } else {
     const Plan plan = meta_partition(sch, target_, k, o_.p);
     const Part& part = plan.parts.at(o_.rank);
+    // replica group: the partitions owning exactly this sub-metatree set
+    for (int q = 0; q < static_cast<int>(plan.parts.size()); ++q)
+      if (plan.parts[q].sub_ids == part.sub_ids) replica_group_.push_back(q);
+    std::sort(replica_group_.begin(), replica_group_.end(), [&](int a, int b) {
+      return plan.parts[a].replica_index < plan.parts[b].replica_index;
+    });
+    replica_pos_ = static_cast<int>(std::find(replica_group_.begin(), replica_group_.end(), o_.rank) -
+                                    replica_group_.begin());
+    if (replica_group_.size() > static_cast<std::size_t>(kMaxRep))
+      throw std::invalid_argument("replica group larger than supported");
+    // gradients are exchanged only inside a replica group: a weight slot or a
+    // learnable leaf type shared by two different sub-metatree sets would need a
+    // cross-group reduction, which this engine does not implement
+    {
+      std::map<std::pair<int, int>, std::vector<int>> slot_groups;
+      std::map<int, std::vector<int>> leaf_groups;
+      for (int q = 0; q < static_cast<int>(plan.parts.size()); ++q) {
+        const int color = plan.parts[q].sub_ids.empty() ? -1 : plan.parts[q].sub_ids.front();
+        std::vector<int> kids;
+        for (int sid : plan.parts[q].sub_ids) kids.push_back(plan.subs[sid].child_pos);
+        for (std::size_t p = 1; p < plan.tree.pos.size(); ++p) {
+          if (std::find(kids.begin(), kids.end(), plan.tree.root_child_ancestor(static_cast<int>(p))) == kids.end())
+            continue;
+          const TreePos& tp = plan.tree.pos[p];
+          slot_groups[{tp.rel, k - tp.depth + 1}].push_back(color);
+          if (tp.depth == k && g.types[tp.type].storage == Storage::Learnable) leaf_groups[tp.type].push_back(color);
+        }
+      }
+      auto distinct = [](std::vector<int> v) {
+        std::sort(v.begin(), v.end());
+        return std::unique(v.begin(), v.end()) - v.begin();
+      };
+      for (const auto& [key, cs] : slot_groups)
+        if (distinct(cs) > 1) throw std::runtime_error("weight slot shared by two partition groups is not supported");
+      for (const auto& [t, cs] : leaf_groups)
+        if (distinct(cs) > 1)
+          throw std::runtime_error("learnable type shared by two partition groups is not supported");
+    }
     replica_ = part.replica;
     shard_index_ = part.replica ? part.replica_index : 0;
     shard_count_ = part.replica ? part.replica_count : 1;
@@ -416,9 +455,51 @@ void Engine::upload(const Graph& g) {
     HG_CUDA(cudaMemcpyAsync(words_dev_, wd.data(), wd.size() * sizeof(int), cudaMemcpyHostToDevice, st_));
     HG_CUDA(cudaStreamSynchronize(st_));
   }
+  // replica exchange arena: frontier ids + count and gradient rows of every
+  // learnable leaf type, in one cudaMalloc so one CUDA IPC handle maps it on the
+  // peers (identical layout on every replica of the group)
+  if (replica_group_.size() > 1) {
+    std::size_t at = 0;
+    auto take = [&](std::size_t bytes) {
+      const std::size_t o = at;
+      at += (bytes + 255) & ~static_cast<std::size_t>(255);
+      return o;
+    };
+    for (const auto& c : cscs_) {
+      if (c.hop != k || !tables_[c.src_t].learnable) continue;
+      Xchg x;
+      x.t = c.src_t;
+      x.cap = front(k, c.src_t).cap;
+      x.ld = c.ld;
+      x.din = c.din;
+      x.off_count = take(sizeof(int));
+      x.off_ids = take(static_cast<std::size_t>(std::max(1, x.cap)) * 4);
+      x.off_dh = take(static_cast<std::size_t>(std::max(1, x.cap)) * x.ld * 4);
+      xchg_.push_back(x);
+    }
+    arena_bytes_ = std::max<std::size_t>(at, 256);
+    arena_ = static_cast<std::uint8_t*>(alloc(arena_bytes_));
+    for (auto& x : xchg_) {
+      Front& f = front(k, x.t);
+      f.count = reinterpret_cast<int*>(arena_ + x.off_count);
+      f.list = reinterpret_cast<std::uint32_t*>(arena_ + x.off_ids);
+      for (auto& c : cscs_)
+        if (c.hop == k && c.src_t == x.t) c.dh = reinterpret_cast<float*>(arena_ + x.off_dh);
+      x.ucap = static_cast<int>(std::min<std::uint64_t>(type_counts_[x.t],
+                                                        static_cast<std::uint64_t>(x.cap) * replica_group_.size()));
+      x.ulist = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(std::max(1, x.ucap)) * 4));
+      x.ucount = static_cast<int*>(alloc(sizeof(int)));
+      x.slot = static_cast<int*>(alloc(static_cast<std::size_t>(std::max(1, x.ucap)) * replica_group_.size() * 4));
+      x.ug = static_cast<float*>(alloc(static_cast<std::size_t>(std::max(1, x.ucap)) * x.ld * 4));
+    }
+    barrier_word_ = static_cast<float*>(alloc(16));
+    peer_arena_.assign(replica_group_.size(), nullptr);
+    peer_arena_[replica_pos_] = arena_;
+  }
   for (int h = 0; h <= k; ++h)
     for (int t = 0; t < ntypes_; ++t) {
       Front& f = front(h, t);
+      if (h == k && xchg_type(t)) continue;  // lives in the exchange arena
       f.count = static_cast<int*>(alloc(sizeof(int)));
       if (f.cap > 0) f.list = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(f.cap) * 4));
     }
@@ -473,7 +554,8 @@ void Engine::upload(const Graph& g) {
     std::size_t ent = 0;
     for (int bi : c.blocks) ent = std::max<std::size_t>(ent, blocks_[bi].edge_base + blocks_[bi].edge_cap);
     c.entries = static_cast<std::uint32_t*>(alloc(ent * 4));
-    c.dh = static_cast<float*>(alloc(static_cast<std::size_t>(std::max(1, c.src_cap)) * c.ld * 4));
+    if (!(c.hop == o_.k && xchg_type(c.src_t)))
+      c.dh = static_cast<float*>(alloc(static_cast<std::size_t>(std::max(1, c.src_cap)) * c.ld * 4));
     if (c.hop < o_.k) {
       for (auto& gr : groups_)
         if (gr.depth - 1 == c.hop && gr.type == c.src_t) gr.dout_buf = c.dh;
@@ -784,7 +866,7 @@ void Engine::run_backward() {
     std::vector<const std::int64_t*> steps;
     std::vector<const int*> counts;
     for (const auto& c : cscs_)
-      if (c.hop == k && tables_[c.src_t].learnable) {
+      if (c.hop == k && tables_[c.src_t].learnable && !xchg_type(c.src_t)) {
         steps.push_back(tables_[c.src_t].step);
         counts.push_back(front(k, c.src_t).count);
       }
@@ -823,6 +905,87 @@ void Engine::run_backward() {
     AdamHyper hp;
     timed("csc_gather", 0, [&] { csc_gather(ch, hp, err_, st_); });
   }
+  if (replica_group_.size() > 1) timed("replica_sync", 0, [&] { run_replica_merge(); });
+}
+
+// Replica group gradient synchronisation (raf.cpp:496-510 accounts it as a ring
+// all-reduce over the slots' contributors): dense weight gradients over NCCL;
+// learnable rows merged by reading every replica's (ids, rows) through peer
+// mappings of their exchange arenas, then one sparse Adam on the union.
+void Engine::run_replica_merge() {
+#ifdef HG_WITH_NCCL
+  if (!rcomm_) throw std::runtime_error("replica group without a communicator (attach_nccl first)");
+  for (std::size_t r = 0; r < peer_arena_.size(); ++r)
+    if (!peer_arena_[r]) throw std::runtime_error("replica peers not attached (attach_replicas)");
+  // 1. weight gradients; completing it also orders every replica's gradient rows
+  //    (written by its csc_gather before its all-reduce) before our reads below
+  // (a launch-count capture leaves the collectives out, see count_launches)
+  if (!counting_ && ncclGroupStart() != ncclSuccess) throw std::runtime_error("ncclGroupStart failed");
+  for (auto& sl : slots_)
+    if (!counting_)
+    if (ncclAllReduce(sl.g, sl.g, static_cast<std::size_t>(std::max(1, sl.din)) * sl.ld, ncclFloat, ncclSum, rcomm_,
+                      st_) != ncclSuccess)
+      throw std::runtime_error("ncclAllReduce (replica weight gradients) failed");
+  if (!counting_ && ncclGroupEnd() != ncclSuccess) throw std::runtime_error("ncclGroupEnd failed");
+  // 2. learnable rows: union + ordered sums, then step and Adam on the union
+  AdamRowsBatch ab{};
+  int base = 0;
+  for (auto& x : xchg_) {
+    ReplicaMerge m{};
+    m.n_rep = static_cast<int>(peer_arena_.size());
+    for (int r = 0; r < m.n_rep; ++r) {
+      m.ids[r] = reinterpret_cast<const std::uint32_t*>(peer_arena_[r] + x.off_ids);
+      m.count[r] = reinterpret_cast<const int*>(peer_arena_[r] + x.off_count);
+      m.dh[r] = reinterpret_cast<const float*>(peer_arena_[r] + x.off_dh);
+    }
+    m.ld = x.ld;
+    m.din = x.din;
+    m.u = {bits_ + word_base_[x.t], word_base_[x.t + 1] - word_base_[x.t], wscan_ + word_base_[x.t], x.ulist, x.ucount,
+           x.ucap};
+    m.slot = x.slot;
+    m.ug = x.ug;
+    replica_merge(m, lb_, st_);
+    const TypeTable& tb = tables_[x.t];
+    ab.t[ab.n] = {tb.w, tb.m, tb.v, tb.ld, x.ulist, x.ug, x.ld, x.ucount, tb.step};
+    ab.base4[ab.n] = base;
+    base += x.ucap * tb.ld / 4;
+    ++ab.n;
+  }
+  ab.total4 = base;
+  adam_rows(ab, AdamHyper{}, err_, st_);  // bumps each table's step iff its union is non-empty
+  // 3. nobody rewrites its arena (next step's sampling) before every peer read it
+  if (!counting_ && ncclAllReduce(barrier_word_, barrier_word_, 1, ncclFloat, ncclSum, rcomm_, st_) != ncclSuccess)
+    throw std::runtime_error("ncclAllReduce (replica barrier) failed");
+#else
+  throw std::runtime_error("replica groups need NCCL");
+#endif
+}
+
+std::vector<char> Engine::replica_handle() {
+  if (replica_group_.size() < 2) return {};
+  cudaIpcMemHandle_t h;
+  HG_CUDA(cudaIpcGetMemHandle(&h, arena_));
+  std::vector<char> out(sizeof(h));
+  std::memcpy(out.data(), &h, sizeof(h));
+  return out;
+}
+
+void Engine::attach_replicas(const std::vector<std::vector<char>>& handles_by_rank) {
+  if (replica_group_.size() < 2) return;
+  HG_CUDA(cudaSetDevice(o_.device));
+  for (std::size_t r = 0; r < replica_group_.size(); ++r) {
+    if (static_cast<int>(r) == replica_pos_) continue;
+    const int q = replica_group_[r];
+    if (q >= static_cast<int>(handles_by_rank.size()) || handles_by_rank[q].size() != sizeof(cudaIpcMemHandle_t))
+      throw std::invalid_argument("missing IPC handle of replica partition " + std::to_string(q));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handles_by_rank[q].data(), sizeof(h));
+    void* p = nullptr;
+    HG_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    ipc_opened_.push_back(p);
+    peer_arena_[r] = static_cast<const std::uint8_t*>(p);
+  }
+  drop_graphs();
 }
 
 CscHop Engine::csc_hop(int h) {
@@ -837,7 +1000,9 @@ CscHop Engine::csc_hop(int h) {
     t.entries = c.entries;
     t.n_src = front(h, c.src_t).count;
     t.src_cap = c.src_cap;
-    const bool leaf_learnable = h == o_.k && tables_[c.src_t].learnable;
+    // replicas merge their learnable-row gradients before Adam: keep the rows
+    const bool exchanged = h == o_.k && xchg_type(c.src_t);
+    const bool leaf_learnable = h == o_.k && tables_[c.src_t].learnable && !exchanged;
     t.dh = (!leaf_learnable || retain_grads_) ? c.dh : nullptr;
     t.ld_dh = c.ld;
     t.din = c.din;

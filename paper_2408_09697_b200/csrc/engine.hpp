@@ -68,8 +68,22 @@ class Engine {
   Engine& operator=(const Engine&) = delete;
 
 #ifdef HG_WITH_NCCL
-  void attach_comm(ncclComm_t comm) { comm_ = comm; }
+  // comm: all partitions (AGG_all); rcomm: this partition's replica group (or null)
+  void attach_comm(ncclComm_t comm, ncclComm_t rcomm) {
+    comm_ = comm;
+    rcomm_ = rcomm;
+    drop_graphs();
+  }
 #endif
+  // ---- replica groups (p > #sub-metatrees, metapartition.cpp:206-236) ----------------
+  // partitions owning the same sub-metatrees split the batch rows (raf.cpp:390-391);
+  // their weight gradients are all-reduced (NCCL) and their learnable-row gradients
+  // merged by a kernel that reads the peers' gradient rows over NVLink (IPC-mapped).
+  const std::vector<int>& replica_group() const { return replica_group_; }
+  int replica_color() const { return replica_group_.size() > 1 ? replica_group_.front() : -1; }
+  int replica_pos() const { return replica_pos_; }
+  std::vector<char> replica_handle();  // CUDA IPC handle of the exchange arena (empty: none)
+  void attach_replicas(const std::vector<std::vector<char>>& handles_by_rank);
 
   // Full training step: sample, forward, AGG_all, loss, backward, Adam.
   // `batch` is host memory (copied to the device inside the call).
@@ -305,7 +319,33 @@ class Engine {
   int launches_per_step_ = 0;
 #ifdef HG_WITH_NCCL
   ncclComm_t comm_ = nullptr;
+  ncclComm_t rcomm_ = nullptr;
 #endif
+  std::vector<int> replica_group_;  // partition ranks, ordered by replica index
+  int replica_pos_ = 0;
+  // learnable leaf types exchanged between replicas: local views into the IPC
+  // arena (frontier ids + count, gradient rows) and the merge scratch
+  struct Xchg {
+    int t = -1, cap = 0, ld = 0, din = 0;
+    std::size_t off_count = 0, off_ids = 0, off_dh = 0;  // offsets in every replica's arena
+    std::uint32_t* ulist = nullptr;
+    int* ucount = nullptr;
+    int ucap = 0;
+    int* slot = nullptr;  // [n_rep x ucap]: row of union entry u in replica r (-1: absent)
+    float* ug = nullptr;  // merged gradient rows [ucap x ld]
+  };
+  std::vector<Xchg> xchg_;
+  std::uint8_t* arena_ = nullptr;
+  std::size_t arena_bytes_ = 0;
+  std::vector<const std::uint8_t*> peer_arena_;  // per group member (self: arena_)
+  std::vector<void*> ipc_opened_;
+  float* barrier_word_ = nullptr;
+  bool xchg_type(int t) const {
+    for (const auto& x : xchg_)
+      if (x.t == t) return true;
+    return false;
+  }
+  void run_replica_merge();
 };
 
 }  // namespace hetgpu

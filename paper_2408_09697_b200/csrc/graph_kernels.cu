@@ -555,6 +555,69 @@ void batch_multiplicity(const std::uint32_t* ids, const StepScalars* sc, int cap
   k_batch_mult<<<grid, kFrontThreads, 0, st>>>(ids, sc, t, mult);
 }
 
+// ---- replica gradient merge -------------------------------------------------------------------
+
+namespace {
+
+__global__ void k_rmark(ReplicaMerge m) {
+  const int r = blockIdx.y;
+  const int n = *m.count[r];
+  const std::uint32_t* ids = m.ids[r];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const std::uint32_t id = ids[i];
+    atomicOr(m.u.bits + (id >> 5), 1u << (id & 31));
+  }
+}
+
+__global__ void k_rslot(ReplicaMerge m) {
+  const int r = blockIdx.y;
+  const int n = *m.count[r];
+  const std::uint32_t* ids = m.ids[r];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    m.slot[static_cast<std::size_t>(r) * m.u.cap + bitmap_rank(m.u, ids[i])] = i;
+}
+
+// half-warp per (union row, 64-column chunk): ordered sum over replicas
+__global__ void __launch_bounds__(256) k_rsum(ReplicaMerge m) {
+  const int hl = threadIdx.x & 15;
+  const int n = *m.u.count;
+  const int nch = (m.din + 63) / 64;
+  const int halves = gridDim.x * (blockDim.x >> 4);
+  for (int item = blockIdx.x * (blockDim.x >> 4) + (threadIdx.x >> 4); item < n * nch; item += halves) {
+    const int u = item / nch;
+    const int f = (item % nch) * 64 + 4 * hl;
+    if (f >= m.ld) continue;
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int r = 0; r < m.n_rep; ++r) {
+      const int row = m.slot[static_cast<std::size_t>(r) * m.u.cap + u];
+      if (row < 0) continue;
+      const float4 v = *reinterpret_cast<const float4*>(m.dh[r] + static_cast<std::size_t>(row) * m.ld + f);
+      s.x += v.x;
+      s.y += v.y;
+      s.z += v.z;
+      s.w += v.w;
+    }
+    *reinterpret_cast<float4*>(m.ug + static_cast<std::size_t>(u) * m.ld + f) = s;
+  }
+}
+
+}  // namespace
+
+void replica_merge(const ReplicaMerge& m, LbScratch& lb, cudaStream_t st) {
+  HG_CUDA(cudaMemsetAsync(m.u.bits, 0, static_cast<std::size_t>(m.u.words) * 4, st));
+  const dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(m.u.cap, 256), 2 * kNumSMs)), m.n_rep);
+  k_rmark<<<grid, 256, 0, st>>>(m);
+  FrontierArgs f{};
+  f.ntypes = 1;
+  f.t[0] = m.u;
+  frontier_compact(f, lb, st);
+  HG_CUDA(cudaMemsetAsync(m.slot, 0xFF, static_cast<std::size_t>(m.n_rep) * m.u.cap * sizeof(int), st));
+  k_rslot<<<grid, 256, 0, st>>>(m);
+  const unsigned g2 = static_cast<unsigned>(
+      std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(m.u.cap * ceil_div(m.din, 64), 16), 16 * kNumSMs)));
+  k_rsum<<<g2, 256, 0, st>>>(m);
+}
+
 // ---- cache / hotness counters -------------------------------------------------------------
 
 namespace {

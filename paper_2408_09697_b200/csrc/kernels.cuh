@@ -253,6 +253,25 @@ void csc_gather(const CscHop& h, AdamHyper hp, std::uint32_t* err, cudaStream_t 
 // per table: step += 1 iff it has gradient rows (hgnn.cpp:392-394)
 void bump_steps(const std::int64_t* const* steps, const int* const* counts, int n, cudaStream_t st);
 
+// ---- replica groups: merge of the learnable-row gradients of every replica ----------
+// ids/count/dh of replica r may live in a peer GPU's memory (CUDA IPC over NVLink).
+// Union of the replicas' sorted id lists (bitmap + compaction, sorted), then per
+// union row the ordered sum over replicas (r = 0..n-1) of their gradient rows:
+// deterministic and identical on every replica, so the replicated tables stay equal.
+constexpr int kMaxRep = 8;
+struct ReplicaMerge {
+  const std::uint32_t* ids[kMaxRep];
+  const int* count[kMaxRep];
+  const float* dh[kMaxRep];
+  int n_rep;
+  int ld;       // row stride of dh and ug
+  int din;
+  BitmapType u; // union over the type's id space: list = union ids, count = union size
+  int* slot;    // [n_rep x u.cap]
+  float* ug;    // [u.cap x ld] merged gradient rows
+};
+void replica_merge(const ReplicaMerge& m, LbScratch& lb, cudaStream_t st);
+
 // ---- misc --------------------------------------------------------------------------------
 void zero_rows(float* p, int ld, const int* n_rows, int rows_cap, cudaStream_t st);
 // cache lookups: hits of frontier ids against a cached-id bitmap, accumulated

@@ -293,6 +293,19 @@ class Engine:
         buf = C.create_string_buffer(unique_id, len(unique_id))
         N.check(N.lib().hg_engine_attach_nccl(self._h, buf, len(unique_id), nranks, rank))
 
+    def replica_handle(self) -> bytes:
+        """CUDA IPC handle of this partition's gradient-exchange arena (b"" without replicas)."""
+        buf = C.create_string_buffer(128)
+        n = N.check(N.lib().hg_engine_replica_handle(self._h, buf, 128))
+        return buf.raw[:n]
+
+    def attach_replicas(self, handles: Sequence[bytes]):
+        """Map the replica peers' exchange arenas (handles of every rank, rank order)."""
+        size = max([len(h) for h in handles] + [1])
+        flat = b"".join(h.ljust(size, b"\0") for h in handles)
+        buf = C.create_string_buffer(flat, len(flat))
+        N.check(N.lib().hg_engine_attach_replicas(self._h, buf, size, len(handles)))
+
     # ---- reference-named views --------------------------------------------------------
     def sample_khop_restricted(self, seeds, rng_seed: int) -> Dict[str, np.ndarray]:
         """sample_khop_restricted (sampling.cpp:99-103) with this engine's hop relation sets."""
@@ -341,6 +354,18 @@ class Sampler:
         names = [x for x in bytes(N.take(N.lib().hg_engine_read(self._h, b"?"))["names"].astype(np.uint8)).decode()
                  .split(",") if x.startswith(("frontier", "hop")) and not x.endswith(".col")]
         return N.take(N.lib().hg_engine_read(self._h, ",".join(names).encode()))
+
+
+def agg_all_comm_bytes(active_rows: Sequence[int], designated: int, num_classes: int, elem_bytes: int = 4,
+                       header_bytes: int = 32) -> Dict[str, int]:
+    """CommStats of one batch's AGG_all exchange (raf.cpp:427-466, payload_bytes
+    raf.cpp:113-115): every partition q != designated with at least one active
+    row sends a PartialAgg of rows x C elements and receives the mirrored
+    PartialGrad. `active_rows` is the per-partition list a step reports."""
+    sent = [header_bytes + int(a) * num_classes * elem_bytes
+            for q, a in enumerate(active_rows) if q != designated and int(a) > 0]
+    return {"messages": 2 * len(sent), "partial_agg_bytes": sum(sent), "partial_grad_bytes": sum(sent),
+            "total_bytes": 2 * sum(sent)}
 
 
 def nccl_unique_id() -> bytes:

@@ -35,14 +35,29 @@ def main():
     print(f"rank {rank}: attaching", flush=True)
     eng.attach_nccl(uid, p, rank)
     print(f"rank {rank}: attached", flush=True)
+    # replica groups: publish this rank's IPC handle, map the peers'
+    hpath = f"{id_path}.h{rank}"
+    with open(hpath + ".tmp", "wb") as f:
+        f.write(eng.replica_handle())
+    os.replace(hpath + ".tmp", hpath)
+    t0 = time.time()
+    while not all(os.path.exists(f"{id_path}.h{r}") for r in range(p)):
+        if time.time() - t0 > 120:
+            raise RuntimeError("missing replica handles")
+        time.sleep(0.05)
+    eng.attach_replicas([open(f"{id_path}.h{r}", "rb").read() for r in range(p)])
     batches = H.make_batches(g, bsz, n_batches, H.mix_seed(seed, 0xBA7C))
     losses, active = [], []
     for i, b in enumerate(batches):
         rep = eng.step(b, H.mix_seed(seed, 0xB000 + i), i % p)
+        if i == 0:
+            g0 = eng.read(*[n for n in eng.tensor_names() if n.startswith(("grad.w.", "grad.f."))])
         print(f"rank {rank}: batch {i} loss {rep['loss']:.6f}", flush=True)
         losses.append(rep["loss"])
         active.append(rep["active_rows"])
-    np.savez(out_path, losses=np.asarray(losses), active=np.asarray(active, np.int64))
+    post = eng.read(*[n for n in eng.tensor_names() if n.startswith(("post.r", "post.learn.t", "post.learn_step.t"))])
+    np.savez(out_path, losses=np.asarray(losses), active=np.asarray(active, np.int64),
+             **{"T:" + k: v for k, v in post.items()}, **{"G:" + k: v for k, v in g0.items()})
 
 
 if __name__ == "__main__":
