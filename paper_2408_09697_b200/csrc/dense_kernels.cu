@@ -195,6 +195,13 @@ __global__ void __launch_bounds__(256) k_csc_gather(CscHop h, AdamHyper hp, std:
           s.w += v[q].w;
         }
       }
+      if (t.relu_h) {
+        const float4 h = *reinterpret_cast<const float4*>(t.relu_h + static_cast<std::size_t>(c) * t.ld_h + f);
+        if (h.x <= 0.f) s.x = 0.f;
+        if (h.y <= 0.f) s.y = 0.f;
+        if (h.z <= 0.f) s.z = 0.f;
+        if (h.w <= 0.f) s.w = 0.f;
+      }
       if (t.dh) *reinterpret_cast<float4*>(t.dh + static_cast<std::size_t>(c) * t.ld_dh + f) = s;
       if (t.w) {
         const std::size_t at = static_cast<std::size_t>(t.ids[c]) * t.ld_w + f;

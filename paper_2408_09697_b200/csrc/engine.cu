@@ -885,8 +885,8 @@ void Engine::run_backward() {
       const int* n_rows = (top && replica_) ? shard_count_dev_ : front(d - 1, gr.type).count;
       const int rows_cap = top && replica_ ? static_cast<int>(ceil_div(o_.batch_cap, shard_count_)) : gr.rows_cap;
       // dpre = dH (x) [H > 0] between layers, fused into the operand loads
-      const DpreView dv{gr.dout_buf, top ? nullptr : gr.out, gr.ld, gr.dout, top ? shard_count_ : 1,
-                        top ? shard_index_ : 0};
+      // dpre = dH * [H > 0]: the mask was applied when csc_gather wrote dH
+      const DpreView dv{gr.dout_buf, nullptr, gr.ld, gr.dout, top ? shard_count_ : 1, top ? shard_index_ : 0};
       for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
         BlockBuf& b = blocks_[gr.blocks[q]];
         Slot& s = slots_[gr.slots[q]];
@@ -1006,6 +1006,12 @@ CscHop Engine::csc_hop(int h) {
     t.dh = (!leaf_learnable || retain_grads_) ? c.dh : nullptr;
     t.ld_dh = c.ld;
     t.din = c.din;
+    if (h < o_.k)  // inner type: its forward output H[h][t] masks the stored gradient
+      for (const auto& gr : groups_)
+        if (gr.depth - 1 == h && gr.type == c.src_t) {
+          t.relu_h = gr.out;
+          t.ld_h = gr.ld;
+        }
     if (leaf_learnable) {
       const TypeTable& tb = tables_[c.src_t];
       t.w = tb.w;

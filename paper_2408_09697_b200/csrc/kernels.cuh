@@ -195,6 +195,10 @@ struct CscType {
   int ld_w;
   const std::uint32_t* ids;  // frontier[k][t]: global row of every source row
   const std::int64_t* step;
+  // inner types: dH is stored already masked by the ReLU of its forward output
+  // (dpre = dH * [H > 0], hgnn.cpp:326-328), so the backward contractions read it plain
+  const float* relu_h;
+  int ld_h;
 };
 struct CscEdges {
   const std::uint32_t* col;

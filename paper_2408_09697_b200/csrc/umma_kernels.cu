@@ -8,13 +8,16 @@
 // accumulated in fp32 (3xTF32), which keeps fp32-level accuracy (the north
 // star's 1e-3 tolerance is for fp32 accumulate).
 //
-// One CTA = 128 threads = one 128-row output tile x NT columns. Per 32-wide K
-// chunk every thread loads its float4s from global memory (coalesced), splits
-// them and stores hi/lo into 128B-swizzled K-major tiles; thread 0 issues the
-// 4 k-steps x 3 MMAs and commits them to the stage's mbarrier. Two smem stages:
-// the global loads of chunk c+1 are in flight while the tensor core runs chunk
-// c. The epilogue reads TMEM with tcgen05.ld (warp w owns TMEM lanes 32w..32w+31,
-// i.e. tile rows) and applies the fused ReLU / 1/deg scaling / row remap.
+// One CTA = 256 threads = one 128-row output tile x NT columns. Operands are
+// staged per 32-wide K chunk in a 4-deep ring: every thread cp.async-copies its
+// 16-byte pieces of raw fp32 straight into the canonical UMMA layout (K-major
+// 128B-swizzled, or MN-major SW128_32B for row-contiguous sources that the
+// tensor core reads transposed), zero-filling rows / columns outside the live
+// extent; chunks are prefetched 2 ahead. The raw tile is the "hi" operand (the
+// tensor core reads the top 19 bits), one elementwise pass writes lo = x -
+// trunc(x), and thread 0 issues 4 k-steps x 3 MMAs and commits them to the
+// stage's mbarrier. The epilogue reads TMEM with tcgen05.ld (warps w and w+4 own
+// TMEM lane quadrant w%4) and applies the fused ReLU / 1/deg scaling / row remap.
 #include "gemm.cuh"
 #include "umma.cuh"
 
@@ -23,14 +26,17 @@ namespace hetgpu {
 namespace {
 
 constexpr int kUT = 256;             // threads per CTA (8 warps: 2 per TMEM lane quadrant)
-constexpr int kAV = 128 * 32 / 4 / kUT;  // A float4 per thread per chunk
 constexpr int kATile = 128 * 128;    // bytes of one 128 x 32 fp32 operand tile
+
+constexpr int kRing = 4;   // raw (hi) operand stages
+constexpr int kAhead = 2;  // chunks prefetched ahead of the one being multiplied
 
 template <int NT>
 struct UStage {
   static constexpr int kB = NT * 128;
-  static constexpr int kBytes = 2 * kATile + 2 * kB;  // A hi, A lo, B hi, B lo
-  static constexpr int kSmem = 2 * kBytes + 1024 + 64;  // two stages + alignment + barriers
+  static constexpr int kHi = kATile + kB;              // one raw stage: A, B
+  static constexpr int kLo = kATile + kB;              // one lo stage: A, B
+  static constexpr int kSmem = kRing * kHi + 2 * kLo + 1024 + 128;  // + alignment + barriers
   static constexpr int kTmemCols = NT <= 32 ? 32 : NT <= 64 ? 64 : NT <= 128 ? 128 : 256;
   static constexpr std::uint32_t kSboA = 128 / 32 * umma::kMnLbo;  // MN-major A: 4-row K-group stride
   static constexpr std::uint32_t kSboB = NT / 32 * umma::kMnLbo;   // MN-major B: 4-row K-group stride
@@ -39,42 +45,19 @@ struct UStage {
 // A = mean[row][c], B = dpre[row][j] are row-contiguous -> MN-major tiles
 template <int MODE> struct Majors;
 
-__device__ __forceinline__ float4 f4zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
 
-// K-contiguous float4 (4 consecutive k of row r) -> hi/lo tiles
-__device__ __forceinline__ void st_kc(std::uint8_t* hi, std::uint8_t* lo, int r, int kq, float4 v) {
-  float4 h, l;
-  umma::split_tf32(v.x, h.x, l.x);
-  umma::split_tf32(v.y, h.y, l.y);
-  umma::split_tf32(v.z, h.z, l.z);
-  umma::split_tf32(v.w, h.w, l.w);
-  const std::uint32_t off = umma::sw128_chunk(r, kq >> 2);
-  *reinterpret_cast<float4*>(hi + off) = h;
-  *reinterpret_cast<float4*>(lo + off) = l;
+// 16-byte async copy global -> shared; src_bytes = 0 zero-fills (outside the live extent)
+__device__ __forceinline__ void cp16(std::uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
 }
-// M/N-contiguous float4 (elements m..m+3 at one k) -> MN-major hi/lo tiles
-__device__ __forceinline__ void st_mn(std::uint8_t* hi, std::uint8_t* lo, int m, int k, std::uint32_t sbo, float4 v) {
-  float4 h, l;
-  umma::split_tf32(v.x, h.x, l.x);
-  umma::split_tf32(v.y, h.y, l.y);
-  umma::split_tf32(v.z, h.z, l.z);
-  umma::split_tf32(v.w, h.w, l.w);
-  const std::uint32_t off = umma::sw128b32_mn(m, k, sbo);
-  *reinterpret_cast<float4*>(hi + off) = h;
-  *reinterpret_cast<float4*>(lo + off) = l;
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_ahead() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(kAhead) : "memory");
 }
-
-__device__ __forceinline__ float4 load_dpre(const DpreView& d, int row, int col) {
-  const std::size_t at = static_cast<std::size_t>(row * d.stride + d.offset) * d.ld + col;
-  float4 v = *reinterpret_cast<const float4*>(d.g + at);
-  if (d.h) {  // dpre = dH * [H > 0] (hgnn.cpp:326-328)
-    const float4 h = *reinterpret_cast<const float4*>(d.h + static_cast<std::size_t>(row) * d.ld + col);
-    if (h.x <= 0.f) v.x = 0.f;
-    if (h.y <= 0.f) v.y = 0.f;
-    if (h.z <= 0.f) v.z = 0.f;
-    if (h.w <= 0.f) v.w = 0.f;
-  }
-  return v;
+// dpre rows (row remap for replica shards); the ReLU mask was applied upstream
+__device__ __forceinline__ const float* dpre_ptr(const DpreView& d, int row, int col) {
+  return d.g + static_cast<std::size_t>(row * d.stride + d.offset) * d.ld + col;
 }
 
 __device__ __forceinline__ int find_tile(const int* base, int n, int tile) {
@@ -112,8 +95,10 @@ __global__ void __launch_bounds__(kUT) k_umma(UmmaArgs<Batch> args) {
   extern __shared__ std::uint8_t smem_raw[];
   std::uint8_t* smem = reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
                                                         ~static_cast<std::uintptr_t>(1023));
-  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + 2 * UStage<NT>::kBytes);
-  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 2);
+  std::uint8_t* hi_ring = smem;                                  // kRing x (A, B)
+  std::uint8_t* lo_ring = smem + kRing * UStage<NT>::kHi;        // 2 x (A, B)
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(lo_ring + 2 * UStage<NT>::kLo);  // per hi stage
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + kRing);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   // ---- tile lookup ----------------------------------------------------------------------
@@ -152,8 +137,7 @@ __global__ void __launch_bounds__(kUT) k_umma(UmmaArgs<Batch> args) {
 
   // ---- setup: barriers, TMEM ---------------------------------------------------------------
   if (tid == 0) {
-    umma::mbar_init(umma::smem_u32(&bars[0]), 1);
-    umma::mbar_init(umma::smem_u32(&bars[1]), 1);
+    for (int i = 0; i < kRing; ++i) umma::mbar_init(umma::smem_u32(&bars[i]), 1);
     umma::fence_mbar_init();
   }
   if (warp == 0) umma::tmem_alloc(umma::smem_u32(tmem_slot), UStage<NT>::kTmemCols);
@@ -162,10 +146,12 @@ __global__ void __launch_bounds__(kUT) k_umma(UmmaArgs<Batch> args) {
   umma::fence_after_sync();
   const std::uint32_t tmem = *tmem_slot;
 
-  // ---- operand loaders ------------------------------------------------------------------------
-  constexpr int kBV = NT * 32 / 4 / kUT;  // B float4 per thread per chunk
-  float4 ra[kAV], rb[kBV];
-  auto load = [&](int ch) {
+  // ---- staging: cp.async of chunk ch's raw fp32 into hi stage `slot` ----------------------------
+  constexpr int kAV = 128 * 32 / 4 / kUT;  // A 16-byte pieces per thread per chunk
+  constexpr int kBV = NT * 32 / 4 / kUT;   // B 16-byte pieces per thread per chunk
+  auto issue = [&](int ch, int slot) {
+    std::uint8_t* st = hi_ring + slot * UStage<NT>::kHi;
+    const std::uint32_t a_s = umma::smem_u32(st), b_s = a_s + kATile;
     if constexpr (MODE == kProject) {
       const ProjGroup& g = args.b.g[p];
       int q = 0, k0 = ch * 32;
@@ -175,73 +161,68 @@ __global__ void __launch_bounds__(kUT) k_umma(UmmaArgs<Batch> args) {
       }
       const ProjRel& r = g.r[q];
 #pragma unroll
-      for (int i = 0; i < kAV; ++i) {  // A: mean rows, K-contiguous
-        const int m = (tid >> 3) + (kUT / 8) * i, k = k0 + (tid & 7) * 4, row = c.row0 + m;
-        ra[i] = (row < c.n_live && k < r.ld_mean)
-                    ? __ldg(reinterpret_cast<const float4*>(r.mean + static_cast<std::size_t>(row) * r.ld_mean + k))
-                    : f4zero();
+      for (int i = 0; i < kAV; ++i) {  // A = mean rows, K-major
+        const int m = (tid >> 3) + (kUT / 8) * i, kq = (tid & 7) * 4, k = k0 + kq, row = c.row0 + m;
+        const bool ok = row < c.n_live && k < r.ld_mean;
+        cp16(a_s + umma::sw128_chunk(m, kq >> 2), ok ? r.mean + static_cast<std::size_t>(row) * r.ld_mean + k : r.mean, ok);
       }
 #pragma unroll
-      for (int i = 0; i < kBV; ++i) {  // B[n][k] = W[k][n]: N-contiguous
-        const int f = tid + kUT * i, k = f / (NT / 4), n = c.n0 + (f % (NT / 4)) * 4, kk = k0 + k;
-        rb[i] = (kk < r.din && n < r.ld_w)
-                    ? __ldg(reinterpret_cast<const float4*>(r.w + static_cast<std::size_t>(kk) * r.ld_w + n))
-                    : f4zero();
+      for (int i = 0; i < kBV; ++i) {  // B[n][k] = W[k][n], MN-major
+        const int f = tid + kUT * i, k = f / (NT / 4), nq = (f % (NT / 4)) * 4, kk = k0 + k, n = c.n0 + nq;
+        const bool ok = kk < r.din && n < r.ld_w;
+        cp16(b_s + umma::sw128b32_mn(nq, k, UStage<NT>::kSboB), ok ? r.w + static_cast<std::size_t>(kk) * r.ld_w + n : r.w, ok);
       }
     } else if constexpr (MODE == kDMean) {
       const DMeanProblem& P = args.b.p[p];
       const int cols4 = (P.d.cols + 3) & ~3;
 #pragma unroll
-      for (int i = 0; i < kAV; ++i) {  // A: dpre rows (ReLU mask, row remap), K-contiguous
-        const int m = (tid >> 3) + (kUT / 8) * i, k = ch * 32 + (tid & 7) * 4, row = c.row0 + m;
-        ra[i] = (row < c.n_live && k < cols4) ? load_dpre(P.d, row, k) : f4zero();
+      for (int i = 0; i < kAV; ++i) {  // A = dpre rows, K-major
+        const int m = (tid >> 3) + (kUT / 8) * i, kq = (tid & 7) * 4, k = ch * 32 + kq, row = c.row0 + m;
+        const bool ok = row < c.n_live && k < cols4;
+        cp16(a_s + umma::sw128_chunk(m, kq >> 2), ok ? dpre_ptr(P.d, row, k) : P.d.g, ok);
       }
 #pragma unroll
-      for (int i = 0; i < kBV; ++i) {  // B[n=c][k=j] = W[c][j]: K-contiguous
-        const int n = c.n0 + (tid >> 3) + (kUT / 8) * i, k = ch * 32 + (tid & 7) * 4;
-        rb[i] = (n < P.din && k < P.ld_w)
-                    ? __ldg(reinterpret_cast<const float4*>(P.w + static_cast<std::size_t>(n) * P.ld_w + k))
-                    : f4zero();
+      for (int i = 0; i < kBV; ++i) {  // B[n=c][k=j] = W[c][j], K-major
+        const int nl = (tid >> 3) + (kUT / 8) * i, kq = (tid & 7) * 4, n = c.n0 + nl, k = ch * 32 + kq;
+        const bool ok = n < P.din && k < P.ld_w;
+        cp16(b_s + umma::sw128_chunk(nl, kq >> 2), ok ? P.w + static_cast<std::size_t>(n) * P.ld_w + k : P.w, ok);
       }
     } else {
       const WGradProblem& P = args.b.p[p];
       const int cols4 = (P.d.cols + 3) & ~3;
 #pragma unroll
-      for (int i = 0; i < kAV; ++i) {  // A[m=c][k=row] = mean[row][c]: M-contiguous
-        const int k = (tid >> 5) + (kUT / 32) * i, m = c.m0 + (tid & 31) * 4, row = c.row0 + ch * 32 + k;
-        ra[i] = (row < c.n_live && m < P.ld_mean)
-                    ? *reinterpret_cast<const float4*>(P.mean + static_cast<std::size_t>(row) * P.ld_mean + m)
-                    : f4zero();
+      for (int i = 0; i < kAV; ++i) {  // A[m=c][k=row] = mean[row][c], MN-major
+        const int k = (tid >> 5) + (kUT / 32) * i, mq = (tid & 31) * 4, m = c.m0 + mq, row = c.row0 + ch * 32 + k;
+        const bool ok = row < c.n_live && m < P.ld_mean;
+        cp16(a_s + umma::sw128b32_mn(mq, k, UStage<NT>::kSboA),
+             ok ? P.mean + static_cast<std::size_t>(row) * P.ld_mean + m : P.mean, ok);
       }
 #pragma unroll
-      for (int i = 0; i < kBV; ++i) {  // B[n=j][k=row] = dpre[row][j]: N-contiguous
-        const int f = tid + kUT * i, k = f / (NT / 4), n = c.n0 + (f % (NT / 4)) * 4, row = c.row0 + ch * 32 + k;
-        rb[i] = (row < c.n_live && n < cols4) ? load_dpre(P.d, row, n) : f4zero();
+      for (int i = 0; i < kBV; ++i) {  // B[n=j][k=row] = dpre[row][j], MN-major
+        const int f = tid + kUT * i, k = f / (NT / 4), nq = (f % (NT / 4)) * 4, n = c.n0 + nq,
+                  row = c.row0 + ch * 32 + k;
+        const bool ok = row < c.n_live && n < cols4;
+        cp16(b_s + umma::sw128b32_mn(nq, k, UStage<NT>::kSboB), ok ? dpre_ptr(P.d, row, n) : P.d.g, ok);
       }
     }
   };
-  auto store = [&](std::uint8_t* st) {
-    std::uint8_t *ahi = st, *alo = st + kATile, *bhi = st + 2 * kATile, *blo = bhi + UStage<NT>::kB;
-    if constexpr (Majors<MODE>::a) {
+  // lo = x - trunc_tf32(x) over the raw stage (elementwise: layout-agnostic)
+  auto make_lo = [&](int hslot, int lslot) {
+    const float4* src = reinterpret_cast<const float4*>(hi_ring + hslot * UStage<NT>::kHi);
+    float4* dst = reinterpret_cast<float4*>(lo_ring + lslot * UStage<NT>::kLo);
 #pragma unroll
-      for (int i = 0; i < kAV; ++i) st_mn(ahi, alo, (tid & 31) * 4, (tid >> 5) + (kUT / 32) * i, UStage<NT>::kSboA, ra[i]);
-    } else {
-#pragma unroll
-      for (int i = 0; i < kAV; ++i) st_kc(ahi, alo, (tid >> 3) + (kUT / 8) * i, (tid & 7) * 4, ra[i]);
-    }
-    if constexpr (Majors<MODE>::b) {
-#pragma unroll
-      for (int i = 0; i < kBV; ++i) {
-        const int f = tid + kUT * i;
-        st_mn(bhi, blo, (f % (NT / 4)) * 4, f / (NT / 4), UStage<NT>::kSboB, rb[i]);
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < kBV; ++i) st_kc(bhi, blo, (tid >> 3) + (kUT / 8) * i, (tid & 7) * 4, rb[i]);
+    for (int i = 0; i < (UStage<NT>::kHi / 16) / kUT; ++i) {
+      const float4 x = src[tid + kUT * i];
+      float4 h, l;
+      umma::split_tf32(x.x, h.x, l.x);
+      umma::split_tf32(x.y, h.y, l.y);
+      umma::split_tf32(x.z, h.z, l.z);
+      umma::split_tf32(x.w, h.w, l.w);
+      dst[tid + kUT * i] = l;
     }
   };
 
-  // ---- main loop: two stages, MMAs of chunk c overlap the loads of chunk c+1 -------------------
+  // ---- main loop ---------------------------------------------------------------------------------
   constexpr std::uint32_t kIdesc = umma::idesc_tf32(128, NT, Majors<MODE>::a, Majors<MODE>::b);
   auto desc_a = [&](std::uint32_t base, int kk) {
     return Majors<MODE>::a ? umma::desc_mn_sw128_32b(base + 2 * kk * UStage<NT>::kSboA, UStage<NT>::kSboA)
@@ -251,36 +232,34 @@ __global__ void __launch_bounds__(kUT) k_umma(UmmaArgs<Batch> args) {
     return Majors<MODE>::b ? umma::desc_mn_sw128_32b(base + 2 * kk * UStage<NT>::kSboB, UStage<NT>::kSboB)
                            : umma::desc_k_sw128(base + 32u * kk);
   };
-  std::uint32_t phase[2] = {0u, 0u};
-  load(0);
+  for (int j = 0; j < kAhead; ++j) {
+    if (j < c.nch) issue(j, j);
+    cp_commit();
+  }
   for (int ch = 0; ch < c.nch; ++ch) {
-    const int s = ch & 1;
-    std::uint8_t* st = smem + s * UStage<NT>::kBytes;
-    if (ch >= 2) {
-      umma::mbar_wait(umma::smem_u32(&bars[s]), phase[s]);
-      phase[s] ^= 1u;
-    }
-    store(st);
-    if (ch + 1 < c.nch) load(ch + 1);
+    // MMAs of chunk ch-2 read hi stage (ch+2)%4 and lo stage ch%2: both free after them
+    if (ch >= 2) umma::mbar_wait(umma::smem_u32(&bars[(ch - 2) % kRing]), ((ch - 2) / kRing) & 1);
+    if (ch + kAhead < c.nch) issue(ch + kAhead, (ch + kAhead) % kRing);
+    cp_commit();
+    cp_wait_ahead();  // this thread's pieces of chunk ch have landed
+    __syncthreads();  // ... and everybody else's
+    make_lo(ch % kRing, ch & 1);
     umma::fence_async_smem();
     __syncthreads();
     if (tid == 0) {
       umma::fence_after_sync();
-      const std::uint32_t a_hi = umma::smem_u32(st), a_lo = a_hi + kATile;
-      const std::uint32_t b_hi = a_hi + 2 * kATile, b_lo = b_hi + UStage<NT>::kB;
+      const std::uint32_t a_hi = umma::smem_u32(hi_ring + (ch % kRing) * UStage<NT>::kHi), b_hi = a_hi + kATile;
+      const std::uint32_t a_lo = umma::smem_u32(lo_ring + (ch & 1) * UStage<NT>::kLo), b_lo = a_lo + kATile;
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {  // 8 tf32 of K per MMA
         umma::mma_tf32(tmem, desc_a(a_hi, kk), desc_b(b_hi, kk), kIdesc, (ch > 0 || kk > 0) ? 1u : 0u);
         umma::mma_tf32(tmem, desc_a(a_hi, kk), desc_b(b_lo, kk), kIdesc, 1u);
         umma::mma_tf32(tmem, desc_a(a_lo, kk), desc_b(b_hi, kk), kIdesc, 1u);
       }
-      umma::commit(umma::smem_u32(&bars[s]));
+      umma::commit(umma::smem_u32(&bars[ch % kRing]));
     }
   }
-  {
-    const int s = (c.nch - 1) & 1;
-    umma::mbar_wait(umma::smem_u32(&bars[s]), phase[s]);
-  }
+  umma::mbar_wait(umma::smem_u32(&bars[(c.nch - 1) % kRing]), ((c.nch - 1) / kRing) & 1);
   umma::fence_after_sync();
 
   // ---- epilogue: TMEM -> registers -> global ------------------------------------------------------
