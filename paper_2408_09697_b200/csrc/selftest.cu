@@ -92,10 +92,10 @@ std::vector<std::vector<double>> selftest_contractions(const std::vector<std::ve
       }
       errs.push_back(rel(res[1], res[0]));
     }
-    // ---- mean gradient: dmean = (dpre * [H > 0]) . W^T / deg
+    // ---- mean gradient: dmean = dpre . W^T / deg (dpre arrives ReLU-masked)
     {
-      float* g = d.up(rnd(gen, rows, dout, ldo));
-      float* h = d.up(rnd(gen, rows, dout, ldo));
+      float* g = d.up(rnd(gen, rows, dout, ldo, 0.3f));
+      float* h = nullptr;
       std::vector<std::uint32_t> ip(rows + 1, 0);
       for (int i = 0; i < rows; ++i) ip[i + 1] = ip[i] + (i % 7);
       std::uint32_t* indptr = d.up(ip);

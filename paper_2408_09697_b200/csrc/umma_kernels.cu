@@ -378,6 +378,8 @@ void project_umma(ProjBatch& pb, cudaStream_t st) {
 
 void dmean_umma(DMeanBatch& b, cudaStream_t st) {
   if (b.np == 0) return;
+  for (int q = 0; q < b.np; ++q)
+    if (b.p[q].d.h) throw std::invalid_argument("tcgen05 mean gradient expects an already masked dpre");
   UmmaArgs<DMeanBatch> a{};
   a.b = b;
   a.np = b.np;
@@ -395,6 +397,8 @@ void dmean_umma(DMeanBatch& b, cudaStream_t st) {
 
 void wgrad_umma(WGradBatch& b, cudaStream_t st) {
   if (b.np == 0) return;
+  for (int q = 0; q < b.np; ++q)
+    if (b.p[q].d.h) throw std::invalid_argument("tcgen05 weight gradient expects an already masked dpre");
   UmmaArgs<WGradBatch> a{};
   a.b = b;
   a.np = b.np;
