@@ -23,6 +23,13 @@ constexpr int kNumSMs = 148;
 __host__ __device__ inline std::uint64_t ceil_div(std::uint64_t a, std::uint64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int round_up4(int x) { return (x + 3) & ~3; }
 
+// tf32 residual x - trunc_tf32(x): the "lo" operand of the 3xTF32 tensor-core
+// products (the tensor core reads the top 19 bits of the raw fp32 as "hi")
+__device__ __forceinline__ float tf32_lo(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+__device__ __forceinline__ float4 tf32_lo4(float4 v) {
+  return make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
+}
+
 // ---- exact restatement of the reference's sampler arithmetic ------------------
 // splitmix64 finaliser (sampling.cpp:9-15)
 __device__ __forceinline__ std::uint64_t dmix_seed(std::uint64_t a, std::uint64_t b) {

@@ -159,6 +159,7 @@ class Engine {
     int rows_cap = 0, edge_cap = 0, edge_base = 0;
     std::uint32_t *indptr = nullptr, *src = nullptr, *erow = nullptr, *col = nullptr;
     float* mean = nullptr;   // tape: rows_cap x ld_mean (only for blocks feeding a layer)
+    float* mean_lo = nullptr;  // its tf32 residual (tensor-core operand)
     float* dmean = nullptr;  // rows_cap x ld_mean (only if the source needs a gradient)
     int din = 0, ld_mean = 0;
     bool need_src_grad = false;
@@ -171,6 +172,7 @@ class Engine {
   struct Slot {
     int rel = -1, layer = 0, din = 0, dout = 0, ld = 0;
     float *w = nullptr, *m = nullptr, *v = nullptr, *g = nullptr;
+    float* w_lo = nullptr;  // tf32 residual of w, refreshed by every Adam step
   };
   struct Group {  // one output type of one layer
     int layer = 0, depth = 0, type = -1, dout = 0, ld = 0, rows_cap = 0;
@@ -178,12 +180,14 @@ class Engine {
     std::vector<int> slots;   // matching slot indices
     float* out = nullptr;     // H[depth-1][type] (logits for layer k)
     float* dout_buf = nullptr;  // dH for it
+    float* dout_lo = nullptr;   // its tf32 residual
   };
   struct CscBuf {
     int hop = 0, src_t = -1, src_cap = 0, din = 0, ld = 0;
     std::vector<int> blocks;
     std::uint32_t *offs = nullptr, *cursor = nullptr, *entries = nullptr;
     float* dh = nullptr;  // gradient of H[hop][src_t] (or learnable rows)
+    float* dh_lo = nullptr;  // tf32 residual of dh (inner types: the next layer's dpre)
   };
   struct TypeTable {
     int dim = 0, ld = 0;
@@ -260,6 +264,7 @@ class Engine {
   float* mult_ = nullptr;
   float* logits_ = nullptr;   // [batch_cap + 1 rows x ldC] (+1: partition counters)
   float* dlogits_ = nullptr;
+  float* dlogits_lo_ = nullptr;
   int ldc_ = 0;
   double* row_loss_ = nullptr;
   double* loss_ = nullptr;

@@ -18,6 +18,7 @@ struct DpreView {
   int cols;
   int stride;
   int offset;
+  const float* g_lo;  // tf32 residual of g (x - trunc_tf32(x)) for the 3xTF32 tensor-core path
 };
 
 struct WGradProblem {
@@ -30,6 +31,7 @@ struct WGradProblem {
   float* partial;  // [chunks x din x cols]
   float* dw;
   int ld_dw;
+  const float* mean_lo;
 };
 struct WGradBatch {
   WGradProblem p[kMaxProblems];
@@ -47,6 +49,7 @@ struct DMeanProblem {
   int rows_cap;
   float* dmean;
   int ld_dmean;
+  const float* w_lo;
 };
 struct DMeanBatch {
   DMeanProblem p[kMaxProblems];
@@ -67,6 +70,7 @@ struct MeanBlock {
   int rows_cap;
   float* mean;
   int ld_mean;
+  float* mean_lo;  // optional tf32 residual of the tape (rows up to the next 32 zero-filled)
 };
 struct MeanBatch {
   MeanBlock b[kMaxBlocks];
@@ -81,6 +85,8 @@ struct ProjRel {
   int din;
   const float* w;
   int ld_w;
+  const float* mean_lo;
+  const float* w_lo;
 };
 struct ProjGroup {
   ProjRel r[8];

@@ -303,7 +303,17 @@ __global__ void __launch_bounds__(256) k_gather_mean(MeanBatch m) {
     const int nch = (B.din + 63) / 64;
     const int local = item - m.item_base[b];
     const int i = local / nch, c = (local % nch) * 64 + 4 * hl;
-    if (i >= *B.n_rows || c >= B.ld_mean) continue;
+    const int n = *B.n_rows;
+    if (c >= B.ld_mean) continue;
+    if (i >= n) {
+      // zero tail up to the next 32-row boundary: the tensor-core weight gradient
+      // streams whole 32-row K chunks of the tape
+      if (B.mean_lo && i < ((n + 31) & ~31)) {
+        *reinterpret_cast<float4*>(B.mean + static_cast<std::size_t>(i) * B.ld_mean + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+        *reinterpret_cast<float4*>(B.mean_lo + static_cast<std::size_t>(i) * B.ld_mean + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      continue;
+    }
     const std::uint32_t lo = B.indptr[i], hi = B.indptr[i + 1];
     const float* base = B.h + c;
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -338,6 +348,7 @@ __global__ void __launch_bounds__(256) k_gather_mean(MeanBatch m) {
       s.w *= inv;
     }
     *reinterpret_cast<float4*>(B.mean + static_cast<std::size_t>(i) * B.ld_mean + c) = s;
+    if (B.mean_lo) *reinterpret_cast<float4*>(B.mean_lo + static_cast<std::size_t>(i) * B.ld_mean + c) = tf32_lo4(s);
   }
 }
 

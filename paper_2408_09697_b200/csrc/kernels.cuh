@@ -171,6 +171,7 @@ struct LossArgs {
   double* row_loss;   // scratch [rows_cap]
   double* loss_out;   // [1]
   std::uint32_t* err;
+  float* dlogits_lo;  // optional tf32 residual of dlogits
 };
 void cross_entropy(const LossArgs& a, cudaStream_t st);
 
@@ -199,6 +200,7 @@ struct CscType {
   // (dpre = dH * [H > 0], hgnn.cpp:326-328), so the backward contractions read it plain
   const float* relu_h;
   int ld_h;
+  float* dh_lo;  // optional tf32 residual of dh
 };
 struct CscEdges {
   const std::uint32_t* col;
@@ -226,6 +228,7 @@ struct AdamHyper {  // hgnn.hpp:16-21
 constexpr int kMaxSlots = 64;
 // all model slots (adam_update_model, hgnn.cpp:379-390); base4 = prefix of rows*ld/4
 struct AdamModelBatch {
+  float* w_lo[kMaxSlots];  // optional tf32 residual of the updated weights
   float* w[kMaxSlots];
   float* m[kMaxSlots];
   float* v[kMaxSlots];

@@ -81,6 +81,35 @@ __device__ __forceinline__ std::uint64_t desc_mn_sw128_32b(std::uint32_t saddr, 
   d |= static_cast<std::uint64_t>(1) << 61;                   // SWIZZLE_128B_BASE32B
   return d;
 }
+// The same MN-major layout as written by TMA boxes of 32 (M/N) x 32 (K) fp32
+// with CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B: each box is 32 K-rows of 128 bytes
+// (4-row groups SBO = 512 bytes apart), consecutive M/N atoms LBO = 4096 apart.
+__device__ __forceinline__ std::uint64_t desc_mn_tma(std::uint32_t saddr) {
+  std::uint64_t d = 0;
+  d |= static_cast<std::uint64_t>((saddr & 0x3FFFFu) >> 4);
+  d |= static_cast<std::uint64_t>(4096 >> 4) << 16;  // LBO: next 32-element M/N box
+  d |= static_cast<std::uint64_t>(512 >> 4) << 32;   // SBO: next 4-row K group
+  d |= static_cast<std::uint64_t>(1) << 46;
+  d |= static_cast<std::uint64_t>(1) << 61;          // SWIZZLE_128B_BASE32B
+  return d;
+}
+
+// ---- TMA ----------------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_expect_tx(std::uint32_t bar, std::uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+// 2-D tiled bulk tensor copy global -> shared, completion counted on `bar`
+__device__ __forceinline__ void tma_load_2d(std::uint32_t dst, const void* tmap, int c0, int c1, std::uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+}
+
 // byte offset of elements (m..m+3, k) (m % 4 == 0) in such a tile
 __device__ __forceinline__ std::uint32_t sw128b32_mn(int m, int k, std::uint32_t sbo) {
   return static_cast<std::uint32_t>((k >> 2) * sbo + (m >> 5) * kMnLbo + (k & 3) * 128 +

@@ -1,23 +1,29 @@
 // The dense contractions of the hot path on the 5th-generation tensor cores
-// (tcgen05.mma kind::tf32, accumulators in TMEM), replacing the reference's
-// naive f64 loops:
+// (tcgen05.mma kind::tf32, accumulators in TMEM, operands by TMA), replacing
+// the reference's naive f64 loops:
 //   projection   out   = sum_r mean_r . W_r  (+ReLU)     matmul + agg_all, hgnn.cpp:189-203, 267-272
 //   mean grad    dmean = (dpre . W^T) / deg              matmul_nt, matrix.hpp:64-78; hgnn.cpp:337-353
 //   weight grad  dW   += mean^T . dpre  (split-K)        matmul_tn_acc, matrix.hpp:49-61; hgnn.cpp:334
-// Parity: operands are split x = hi + lo in tf32 and hi.hi + hi.lo + lo.hi is
-// accumulated in fp32 (3xTF32), which keeps fp32-level accuracy (the north
-// star's 1e-3 tolerance is for fp32 accumulate).
+// Parity: every operand x is carried as hi = x (the tensor core reads its top
+// 19 bits) plus lo = x - trunc_tf32(x), written by the producing kernel; the
+// sum hi.hi + hi.lo + lo.hi accumulated in fp32 (3xTF32) keeps fp32-level
+// accuracy (the north star's 1e-3 tolerance is for fp32 accumulate).
 //
-// One CTA = 256 threads = one 128-row output tile x NT columns. Operands are
-// staged per 32-wide K chunk in a 4-deep ring: every thread cp.async-copies its
-// 16-byte pieces of raw fp32 straight into the canonical UMMA layout (K-major
-// 128B-swizzled, or MN-major SW128_32B for row-contiguous sources that the
-// tensor core reads transposed), zero-filling rows / columns outside the live
-// extent; chunks are prefetched 2 ahead. The raw tile is the "hi" operand (the
-// tensor core reads the top 19 bits), one elementwise pass writes lo = x -
-// trunc(x), and thread 0 issues 4 k-steps x 3 MMAs and commits them to the
-// stage's mbarrier. The epilogue reads TMEM with tcgen05.ld (warps w and w+4 own
-// TMEM lane quadrant w%4) and applies the fused ReLU / 1/deg scaling / row remap.
+// One CTA = 128 threads = one 128-row output tile x NT columns, warp-specialised:
+// warp 0 (one lane) streams 32-wide K chunks of A hi/lo and B hi/lo through a
+// kStages-deep shared-memory ring with 2-D TMA loads (K-major tiles with the
+// 128-byte swizzle; row-contiguous operands the tensor core reads transposed as
+// MN-major SW128_32B tiles); warp 1 (one lane) issues 4 k-steps x 3 MMAs per chunk
+// and commits them to the stage's "empty" barrier; all four warps then drain TMEM
+// with tcgen05.ld (warp w owns TMEM lanes 32w..32w+31) and apply the fused ReLU /
+// 1/deg scaling / row remap. Rows and columns outside a tensor's extent are
+// zero-filled by TMA; rows beyond the live count inside the extent are either
+// never stored (projection, mean gradient) or zero in the tape (weight gradient).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
 #include "gemm.cuh"
 #include "umma.cuh"
 
@@ -25,39 +31,38 @@ namespace hetgpu {
 
 namespace {
 
-constexpr int kUT = 256;             // threads per CTA (8 warps: 2 per TMEM lane quadrant)
-constexpr int kATile = 128 * 128;    // bytes of one 128 x 32 fp32 operand tile
-
-constexpr int kRing = 4;   // raw (hi) operand stages
-constexpr int kAhead = 2;  // chunks prefetched ahead of the one being multiplied
+constexpr int kUT = 128;           // threads per CTA (4 warps = 4 TMEM lane quadrants)
+constexpr int kATile = 128 * 128;  // bytes of one 128 x 32 fp32 operand tile
+constexpr int kMaxMaps = 128;
 
 template <int NT>
 struct UStage {
   static constexpr int kB = NT * 128;
-  static constexpr int kHi = kATile + kB;              // one raw stage: A, B
-  static constexpr int kLo = kATile + kB;              // one lo stage: A, B
-  static constexpr int kSmem = kRing * kHi + 2 * kLo + 1024 + 128;  // + alignment + barriers
+  static constexpr int kBytes = 2 * kATile + 2 * kB;  // A hi, A lo, B hi, B lo
+  static constexpr int kStages = NT <= 64 ? 4 : 3;
+  static constexpr int kSmem = kStages * kBytes + 1024 + 128;
   static constexpr int kTmemCols = NT <= 32 ? 32 : NT <= 64 ? 64 : NT <= 128 ? 128 : 256;
-  static constexpr std::uint32_t kSboA = 128 / 32 * umma::kMnLbo;  // MN-major A: 4-row K-group stride
-  static constexpr std::uint32_t kSboB = NT / 32 * umma::kMnLbo;   // MN-major B: 4-row K-group stride
 };
-// operand majors per mode: projection B = W[k][n] and the weight gradient's
-// A = mean[row][c], B = dpre[row][j] are row-contiguous -> MN-major tiles
+
+enum Mode { kProject = 0, kDMean = 1, kWGrad = 2 };
+// operand majors: projection B = W[k][n] and the weight gradient's A = mean[row][c],
+// B = dpre[row][j] are row-contiguous -> MN-major tiles the tensor core transposes
 template <int MODE> struct Majors;
+template <> struct Majors<kProject> { static constexpr int a = 0, b = 1; };
+template <> struct Majors<kDMean> { static constexpr int a = 0, b = 0; };
+template <> struct Majors<kWGrad> { static constexpr int a = 1, b = 1; };
 
-
-// 16-byte async copy global -> shared; src_bytes = 0 zero-fills (outside the live extent)
-__device__ __forceinline__ void cp16(std::uint32_t dst, const void* src, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
-               : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_wait_ahead() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(kAhead) : "memory");
-}
-// dpre rows (row remap for replica shards); the ReLU mask was applied upstream
-__device__ __forceinline__ const float* dpre_ptr(const DpreView& d, int row, int col) {
-  return d.g + static_cast<std::size_t>(row * d.stride + d.offset) * d.ld + col;
+template <typename Batch>
+struct alignas(64) UmmaArgs {
+  CUtensorMap maps[kMaxMaps];  // [A hi, A lo, B hi, B lo] per (problem[, relation])
+  Batch b;
+  int tile_base[kMaxProblems + 1];
+  int n_tiles[kMaxProblems];  // column tiles per problem
+  int m_tiles[kMaxProblems];  // weight gradient: din tiles per problem
+  int np;
+};
+__host__ __device__ constexpr int map_index(int mode, int p, int r, int which) {
+  return mode == kProject ? (p * 8 + r) * 4 + which : p * 4 + which;
 }
 
 __device__ __forceinline__ int find_tile(const int* base, int n, int tile) {
@@ -66,78 +71,53 @@ __device__ __forceinline__ int find_tile(const int* base, int n, int tile) {
   return p;
 }
 
-enum Mode { kProject = 0, kDMean = 1, kWGrad = 2 };
-template <> struct Majors<kProject> { static constexpr int a = 0, b = 1; };
-template <> struct Majors<kDMean> { static constexpr int a = 0, b = 0; };
-template <> struct Majors<kWGrad> { static constexpr int a = 1, b = 1; };
-
-template <typename Batch>
-struct UmmaArgs {
-  Batch b;
-  int tile_base[kMaxProblems + 1];
-  int n_tiles[kMaxProblems];  // column tiles per problem
-  int m_tiles[kMaxProblems];  // wgrad: din tiles per problem
-  int np;
-};
-
-// Per-CTA description of the tile being computed, filled by the mode.
-struct TileCtx {
-  int mode;
-  int p;          // problem / group index
-  int row0;       // first output row (project/dmean) or first K row (wgrad)
-  int m0, n0;     // wgrad: first din row; all: first output column
-  int nch;        // K chunks
-  int n_live;     // live rows
-};
-
 template <int NT, int MODE, typename Batch>
-__global__ void __launch_bounds__(kUT) k_umma(UmmaArgs<Batch> args) {
+__global__ void __launch_bounds__(kUT) k_umma(const __grid_constant__ UmmaArgs<Batch> args) {
+  constexpr int S = UStage<NT>::kStages;
   extern __shared__ std::uint8_t smem_raw[];
   std::uint8_t* smem = reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
                                                         ~static_cast<std::uintptr_t>(1023));
-  std::uint8_t* hi_ring = smem;                                  // kRing x (A, B)
-  std::uint8_t* lo_ring = smem + kRing * UStage<NT>::kHi;        // 2 x (A, B)
-  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(lo_ring + 2 * UStage<NT>::kLo);  // per hi stage
-  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + kRing);
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + S * UStage<NT>::kBytes);
+  std::uint64_t* empty = full + S;
+  std::uint64_t* done = empty + S;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(done + 1);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  // ---- tile lookup ----------------------------------------------------------------------
+  // ---- tile of this CTA -----------------------------------------------------------------
   const int p = find_tile(args.tile_base, args.np, blockIdx.x);
   const int t = blockIdx.x - args.tile_base[p];
   const int ntl = args.n_tiles[p];
-  TileCtx c{};
-  c.mode = MODE;
-  c.p = p;
+  int row0 = 0, m0 = 0, n0 = 0, nch = 0, n_live = 0;
   if constexpr (MODE == kProject) {
     const ProjGroup& g = args.b.g[p];
-    c.n_live = *g.n_rows;
-    c.row0 = (t / ntl) * 128;
-    c.n0 = (t % ntl) * NT;
-    int nch = 0;
+    n_live = *g.n_rows;
+    row0 = (t / ntl) * 128;
+    n0 = (t % ntl) * NT;
     for (int q = 0; q < g.nrel; ++q) nch += (g.r[q].din + 31) / 32;
-    c.nch = nch;
   } else if constexpr (MODE == kDMean) {
     const DMeanProblem& P = args.b.p[p];
-    c.n_live = *P.n_rows;
-    c.row0 = (t / ntl) * 128;
-    c.n0 = (t % ntl) * NT;
-    c.nch = (P.d.cols + 31) / 32;
+    n_live = *P.n_rows;
+    row0 = (t / ntl) * 128;
+    n0 = (t % ntl) * NT;
+    nch = (P.d.cols + 31) / 32;
   } else {
     const WGradProblem& P = args.b.p[p];
-    c.n_live = *P.n_rows;
+    n_live = *P.n_rows;
     const int mt = args.m_tiles[p];
-    const int chunk = t / (mt * ntl);
-    c.m0 = ((t / ntl) % mt) * 128;
-    c.n0 = (t % ntl) * NT;
-    c.row0 = chunk * kWChunkRows;
-    c.nch = (min(kWChunkRows, c.n_live - c.row0) + 31) / 32;
+    m0 = ((t / ntl) % mt) * 128;
+    n0 = (t % ntl) * NT;
+    row0 = (t / (mt * ntl)) * kWChunkRows;
+    if (row0 < n_live) nch = (min(kWChunkRows, n_live - row0) + 31) / 32;
   }
-  if (MODE != kWGrad && c.row0 >= c.n_live) return;
-  if (MODE == kWGrad && c.row0 >= c.n_live) return;
+  if (row0 >= n_live) return;
 
   // ---- setup: barriers, TMEM ---------------------------------------------------------------
   if (tid == 0) {
-    for (int i = 0; i < kRing; ++i) umma::mbar_init(umma::smem_u32(&bars[i]), 1);
+    for (int i = 0; i < S; ++i) {
+      umma::mbar_init(umma::smem_u32(&full[i]), 1);
+      umma::mbar_init(umma::smem_u32(&empty[i]), 1);
+    }
+    umma::mbar_init(umma::smem_u32(done), 1);
     umma::fence_mbar_init();
   }
   if (warp == 0) umma::tmem_alloc(umma::smem_u32(tmem_slot), UStage<NT>::kTmemCols);
@@ -146,141 +126,91 @@ __global__ void __launch_bounds__(kUT) k_umma(UmmaArgs<Batch> args) {
   umma::fence_after_sync();
   const std::uint32_t tmem = *tmem_slot;
 
-  // ---- staging: cp.async of chunk ch's raw fp32 into hi stage `slot` ----------------------------
-  constexpr int kAV = 128 * 32 / 4 / kUT;  // A 16-byte pieces per thread per chunk
-  constexpr int kBV = NT * 32 / 4 / kUT;   // B 16-byte pieces per thread per chunk
-  auto issue = [&](int ch, int slot) {
-    std::uint8_t* st = hi_ring + slot * UStage<NT>::kHi;
-    const std::uint32_t a_s = umma::smem_u32(st), b_s = a_s + kATile;
-    if constexpr (MODE == kProject) {
-      const ProjGroup& g = args.b.g[p];
-      int q = 0, k0 = ch * 32;
-      while (q + 1 < g.nrel && k0 >= ((g.r[q].din + 31) / 32) * 32) {
-        k0 -= ((g.r[q].din + 31) / 32) * 32;
-        ++q;
-      }
-      const ProjRel& r = g.r[q];
-#pragma unroll
-      for (int i = 0; i < kAV; ++i) {  // A = mean rows, K-major
-        const int m = (tid >> 3) + (kUT / 8) * i, kq = (tid & 7) * 4, k = k0 + kq, row = c.row0 + m;
-        const bool ok = row < c.n_live && k < r.ld_mean;
-        cp16(a_s + umma::sw128_chunk(m, kq >> 2), ok ? r.mean + static_cast<std::size_t>(row) * r.ld_mean + k : r.mean, ok);
-      }
-#pragma unroll
-      for (int i = 0; i < kBV; ++i) {  // B[n][k] = W[k][n], MN-major
-        const int f = tid + kUT * i, k = f / (NT / 4), nq = (f % (NT / 4)) * 4, kk = k0 + k, n = c.n0 + nq;
-        const bool ok = kk < r.din && n < r.ld_w;
-        cp16(b_s + umma::sw128b32_mn(nq, k, UStage<NT>::kSboB), ok ? r.w + static_cast<std::size_t>(kk) * r.ld_w + n : r.w, ok);
-      }
-    } else if constexpr (MODE == kDMean) {
-      const DMeanProblem& P = args.b.p[p];
-      const int cols4 = (P.d.cols + 3) & ~3;
-#pragma unroll
-      for (int i = 0; i < kAV; ++i) {  // A = dpre rows, K-major
-        const int m = (tid >> 3) + (kUT / 8) * i, kq = (tid & 7) * 4, k = ch * 32 + kq, row = c.row0 + m;
-        const bool ok = row < c.n_live && k < cols4;
-        cp16(a_s + umma::sw128_chunk(m, kq >> 2), ok ? dpre_ptr(P.d, row, k) : P.d.g, ok);
-      }
-#pragma unroll
-      for (int i = 0; i < kBV; ++i) {  // B[n=c][k=j] = W[c][j], K-major
-        const int nl = (tid >> 3) + (kUT / 8) * i, kq = (tid & 7) * 4, n = c.n0 + nl, k = ch * 32 + kq;
-        const bool ok = n < P.din && k < P.ld_w;
-        cp16(b_s + umma::sw128_chunk(nl, kq >> 2), ok ? P.w + static_cast<std::size_t>(n) * P.ld_w + k : P.w, ok);
-      }
-    } else {
-      const WGradProblem& P = args.b.p[p];
-      const int cols4 = (P.d.cols + 3) & ~3;
-#pragma unroll
-      for (int i = 0; i < kAV; ++i) {  // A[m=c][k=row] = mean[row][c], MN-major
-        const int k = (tid >> 5) + (kUT / 32) * i, mq = (tid & 31) * 4, m = c.m0 + mq, row = c.row0 + ch * 32 + k;
-        const bool ok = row < c.n_live && m < P.ld_mean;
-        cp16(a_s + umma::sw128b32_mn(mq, k, UStage<NT>::kSboA),
-             ok ? P.mean + static_cast<std::size_t>(row) * P.ld_mean + m : P.mean, ok);
-      }
-#pragma unroll
-      for (int i = 0; i < kBV; ++i) {  // B[n=j][k=row] = dpre[row][j], MN-major
-        const int f = tid + kUT * i, k = f / (NT / 4), nq = (f % (NT / 4)) * 4, n = c.n0 + nq,
-                  row = c.row0 + ch * 32 + k;
-        const bool ok = row < c.n_live && n < cols4;
-        cp16(b_s + umma::sw128b32_mn(nq, k, UStage<NT>::kSboB), ok ? dpre_ptr(P.d, row, n) : P.d.g, ok);
+  if (warp == 0 && lane == 0) {
+    // ===== TMA producer =====
+    for (int ch = 0; ch < nch; ++ch) {
+      const int s = ch % S;
+      if (ch >= S) umma::mbar_wait(umma::smem_u32(&empty[s]), ((ch / S) - 1) & 1);
+      const std::uint32_t bar = umma::smem_u32(&full[s]);
+      umma::mbar_expect_tx(bar, UStage<NT>::kBytes);
+      const std::uint32_t a_hi = umma::smem_u32(smem + s * UStage<NT>::kBytes), a_lo = a_hi + kATile;
+      const std::uint32_t b_hi = a_hi + 2 * kATile, b_lo = b_hi + UStage<NT>::kB;
+      if constexpr (MODE == kProject) {
+        const ProjGroup& g = args.b.g[p];
+        int q = 0, k0 = ch * 32;
+        while (q + 1 < g.nrel && k0 >= ((g.r[q].din + 31) / 32) * 32) {
+          k0 -= ((g.r[q].din + 31) / 32) * 32;
+          ++q;
+        }
+        const CUtensorMap* M = &args.maps[map_index(MODE, p, q, 0)];
+        umma::tma_load_2d(a_hi, M + 0, k0, row0, bar);  // A = mean rows, K-major
+        umma::tma_load_2d(a_lo, M + 1, k0, row0, bar);
+        for (int j = 0; j < NT / 32; ++j) {  // B = W[k][n] boxes of 32 n x 32 k
+          umma::tma_load_2d(b_hi + j * 4096, M + 2, n0 + 32 * j, k0, bar);
+          umma::tma_load_2d(b_lo + j * 4096, M + 3, n0 + 32 * j, k0, bar);
+        }
+      } else if constexpr (MODE == kDMean) {
+        const CUtensorMap* M = &args.maps[map_index(MODE, p, 0, 0)];
+        umma::tma_load_2d(a_hi, M + 0, ch * 32, row0, bar);  // A = dpre rows, K-major
+        umma::tma_load_2d(a_lo, M + 1, ch * 32, row0, bar);
+        umma::tma_load_2d(b_hi, M + 2, ch * 32, n0, bar);    // B = W rows c, K-major
+        umma::tma_load_2d(b_lo, M + 3, ch * 32, n0, bar);
+      } else {
+        const CUtensorMap* M = &args.maps[map_index(MODE, p, 0, 0)];
+        const int r = row0 + ch * 32;
+        for (int j = 0; j < 4; ++j) {  // A = mean[row][c]: boxes of 32 c x 32 rows
+          umma::tma_load_2d(a_hi + j * 4096, M + 0, m0 + 32 * j, r, bar);
+          umma::tma_load_2d(a_lo + j * 4096, M + 1, m0 + 32 * j, r, bar);
+        }
+        for (int j = 0; j < NT / 32; ++j) {  // B = dpre[row][j]: boxes of 32 j x 32 rows
+          umma::tma_load_2d(b_hi + j * 4096, M + 2, n0 + 32 * j, r, bar);
+          umma::tma_load_2d(b_lo + j * 4096, M + 3, n0 + 32 * j, r, bar);
+        }
       }
     }
-  };
-  // lo = x - trunc_tf32(x) over the raw stage (elementwise: layout-agnostic)
-  auto make_lo = [&](int hslot, int lslot) {
-    const float4* src = reinterpret_cast<const float4*>(hi_ring + hslot * UStage<NT>::kHi);
-    float4* dst = reinterpret_cast<float4*>(lo_ring + lslot * UStage<NT>::kLo);
-#pragma unroll
-    for (int i = 0; i < (UStage<NT>::kHi / 16) / kUT; ++i) {
-      const float4 x = src[tid + kUT * i];
-      float4 h, l;
-      umma::split_tf32(x.x, h.x, l.x);
-      umma::split_tf32(x.y, h.y, l.y);
-      umma::split_tf32(x.z, h.z, l.z);
-      umma::split_tf32(x.w, h.w, l.w);
-      dst[tid + kUT * i] = l;
-    }
-  };
-
-  // ---- main loop ---------------------------------------------------------------------------------
-  constexpr std::uint32_t kIdesc = umma::idesc_tf32(128, NT, Majors<MODE>::a, Majors<MODE>::b);
-  auto desc_a = [&](std::uint32_t base, int kk) {
-    return Majors<MODE>::a ? umma::desc_mn_sw128_32b(base + 2 * kk * UStage<NT>::kSboA, UStage<NT>::kSboA)
-                           : umma::desc_k_sw128(base + 32u * kk);
-  };
-  auto desc_b = [&](std::uint32_t base, int kk) {
-    return Majors<MODE>::b ? umma::desc_mn_sw128_32b(base + 2 * kk * UStage<NT>::kSboB, UStage<NT>::kSboB)
-                           : umma::desc_k_sw128(base + 32u * kk);
-  };
-  for (int j = 0; j < kAhead; ++j) {
-    if (j < c.nch) issue(j, j);
-    cp_commit();
-  }
-  for (int ch = 0; ch < c.nch; ++ch) {
-    // MMAs of chunk ch-2 read hi stage (ch+2)%4 and lo stage ch%2: both free after them
-    if (ch >= 2) umma::mbar_wait(umma::smem_u32(&bars[(ch - 2) % kRing]), ((ch - 2) / kRing) & 1);
-    if (ch + kAhead < c.nch) issue(ch + kAhead, (ch + kAhead) % kRing);
-    cp_commit();
-    cp_wait_ahead();  // this thread's pieces of chunk ch have landed
-    __syncthreads();  // ... and everybody else's
-    make_lo(ch % kRing, ch & 1);
-    umma::fence_async_smem();
-    __syncthreads();
-    if (tid == 0) {
+  } else if (warp == 1 && lane == 0) {
+    // ===== MMA issuer =====
+    constexpr std::uint32_t kIdesc = umma::idesc_tf32(128, NT, Majors<MODE>::a, Majors<MODE>::b);
+    auto dsc = [](bool mn, std::uint32_t base, int kk) {
+      return mn ? umma::desc_mn_tma(base + 1024u * kk) : umma::desc_k_sw128(base + 32u * kk);
+    };
+    for (int ch = 0; ch < nch; ++ch) {
+      const int s = ch % S;
+      umma::mbar_wait(umma::smem_u32(&full[s]), (ch / S) & 1);
       umma::fence_after_sync();
-      const std::uint32_t a_hi = umma::smem_u32(hi_ring + (ch % kRing) * UStage<NT>::kHi), b_hi = a_hi + kATile;
-      const std::uint32_t a_lo = umma::smem_u32(lo_ring + (ch & 1) * UStage<NT>::kLo), b_lo = a_lo + kATile;
+      const std::uint32_t a_hi = umma::smem_u32(smem + s * UStage<NT>::kBytes), a_lo = a_hi + kATile;
+      const std::uint32_t b_hi = a_hi + 2 * kATile, b_lo = b_hi + UStage<NT>::kB;
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {  // 8 tf32 of K per MMA
-        umma::mma_tf32(tmem, desc_a(a_hi, kk), desc_b(b_hi, kk), kIdesc, (ch > 0 || kk > 0) ? 1u : 0u);
-        umma::mma_tf32(tmem, desc_a(a_hi, kk), desc_b(b_lo, kk), kIdesc, 1u);
-        umma::mma_tf32(tmem, desc_a(a_lo, kk), desc_b(b_hi, kk), kIdesc, 1u);
+        const std::uint64_t ah = dsc(Majors<MODE>::a, a_hi, kk), al = dsc(Majors<MODE>::a, a_lo, kk);
+        const std::uint64_t bh = dsc(Majors<MODE>::b, b_hi, kk), bl = dsc(Majors<MODE>::b, b_lo, kk);
+        umma::mma_tf32(tmem, ah, bh, kIdesc, (ch > 0 || kk > 0) ? 1u : 0u);
+        umma::mma_tf32(tmem, ah, bl, kIdesc, 1u);
+        umma::mma_tf32(tmem, al, bh, kIdesc, 1u);
       }
-      umma::commit(umma::smem_u32(&bars[ch % kRing]));
+      umma::commit(umma::smem_u32(&empty[s]));  // frees the stage once these MMAs are done
     }
+    umma::commit(umma::smem_u32(done));  // accumulator complete
   }
-  umma::mbar_wait(umma::smem_u32(&bars[(c.nch - 1) % kRing]), ((c.nch - 1) / kRing) & 1);
+  __syncwarp();
+  umma::mbar_wait(umma::smem_u32(done), 0);
   umma::fence_after_sync();
 
-  // ---- epilogue: TMEM -> registers -> global ------------------------------------------------------
-  // warp w reads TMEM lane quadrant (w % 4) = tile rows 32(w%4)..+31, columns
-  // [(w / 4) * NT / 2, ...) : the two warps of a quadrant split the columns
-  constexpr int kHalves = kUT / 128;
-  const int quad = warp & 3, half = warp >> 2;
-  const int m = quad * 32 + lane;  // tile row owned by this thread
-  const std::uint32_t trow = tmem + (static_cast<std::uint32_t>(quad * 32) << 16);
+  // ---- epilogue: TMEM -> registers -> global ---------------------------------------------------
+  const int m = warp * 32 + lane;  // tile row owned by this thread
+  const std::uint32_t trow = tmem + (static_cast<std::uint32_t>(warp * 32) << 16);
 #pragma unroll 1
-  for (int c0 = half * (NT / kHalves); c0 < (half + 1) * (NT / kHalves); c0 += 16) {
+  for (int c0 = 0; c0 < NT; c0 += 16) {
     float v[16];
     umma::tmem_ld16(trow + c0, v);
     if constexpr (MODE == kProject) {
       const ProjGroup& g = args.b.g[p];
-      const int row = c.row0 + m;
-      if (row < c.n_live) {
+      const int row = row0 + m;
+      if (row < n_live) {
         float* orow = g.out + static_cast<std::size_t>(row * g.out_stride + g.out_offset) * g.ld_out;
 #pragma unroll
         for (int j = 0; j < 16; j += 4) {
-          const int col = c.n0 + c0 + j;
+          const int col = n0 + c0 + j;
           if (col < g.ld_out) {
             float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
             if (g.relu) {
@@ -295,14 +225,14 @@ __global__ void __launch_bounds__(kUT) k_umma(UmmaArgs<Batch> args) {
       }
     } else if constexpr (MODE == kDMean) {
       const DMeanProblem& P = args.b.p[p];
-      const int row = c.row0 + m;
-      if (row < c.n_live) {
+      const int row = row0 + m;
+      if (row < n_live) {
         const std::uint32_t deg = P.indptr[row + 1] - P.indptr[row];
         const float inv = deg ? 1.0f / static_cast<float>(deg) : 0.0f;
         float* orow = P.dmean + static_cast<std::size_t>(row) * P.ld_dmean;
 #pragma unroll
         for (int j = 0; j < 16; j += 4) {
-          const int col = c.n0 + c0 + j;
+          const int col = n0 + c0 + j;
           if (col < P.ld_dmean)
             *reinterpret_cast<float4*>(orow + col) =
                 make_float4(v[j] * inv, v[j + 1] * inv, v[j + 2] * inv, v[j + 3] * inv);
@@ -310,13 +240,13 @@ __global__ void __launch_bounds__(kUT) k_umma(UmmaArgs<Batch> args) {
       }
     } else {
       const WGradProblem& P = args.b.p[p];
-      const int row = c.m0 + m;  // din index
+      const int row = m0 + m;  // din index
       if (row < P.din) {
-        const int chunk = c.row0 / kWChunkRows;
+        const int chunk = row0 / kWChunkRows;
         float* out = P.partial + (static_cast<std::size_t>(chunk) * P.din + row) * P.d.cols;
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const int col = c.n0 + c0 + j;
+          const int col = n0 + c0 + j;
           if (col < P.d.cols) out[col] = v[j];
         }
       }
@@ -325,6 +255,37 @@ __global__ void __launch_bounds__(kUT) k_umma(UmmaArgs<Batch> args) {
   umma::fence_before_sync();
   __syncthreads();
   if (warp == 0) umma::tmem_dealloc(tmem, UStage<NT>::kTmemCols);
+}
+
+// ---- host side: tensor maps ----------------------------------------------------------------------
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    HG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// fp32 row-major [rows x cols] with `row_stride` elements between rows, read in
+// boxes of 32 columns x box_rows rows
+void encode(CUtensorMap* m, const float* base, std::uint64_t cols, std::uint64_t rows, std::uint64_t row_stride,
+            std::uint32_t box_rows, bool mn_major) {
+  if (!base) throw std::invalid_argument("tensor-core operand without a tf32 residual buffer");
+  const cuuint64_t dims[2] = {cols, std::max<std::uint64_t>(1, rows)};
+  const cuuint64_t strides[1] = {row_stride * 4};
+  const cuuint32_t box[2] = {32, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
 }
 
 template <int NT, int MODE, typename Batch>
@@ -338,8 +299,8 @@ void launch(UmmaArgs<Batch>& a, int tiles, cudaStream_t st) {
   k_umma<NT, MODE, Batch><<<tiles, kUT, UStage<NT>::kSmem, st>>>(a);
 }
 
-// column tile width for an output of `cols` columns (multiples of 32 for the
-// MN-major atoms); wider outputs take several 128-wide tiles (349 classes -> 3)
+// column tile width (multiples of 32 for the MN-major boxes); wider outputs take
+// several 128-wide tiles (349 classes -> 3)
 int pick_nt(int cols) {
   if (cols <= 32) return 32;
   if (cols <= 64) return 64;
@@ -359,18 +320,30 @@ void dispatch(UmmaArgs<Batch>& a, int nt, int tiles, cudaStream_t st) {
 }  // namespace
 
 // All problems of one launch share one column-tile width (the widest needed).
+// The tensor maps are encoded on the host per launch and travel in the kernel
+// parameters (a captured CUDA graph keeps them).
 void project_umma(ProjBatch& pb, cudaStream_t st) {
   if (pb.ng == 0) return;
-  UmmaArgs<ProjBatch> a{};
+  static thread_local UmmaArgs<ProjBatch> a;
+  a = UmmaArgs<ProjBatch>{};
   a.b = pb;
   a.np = pb.ng;
   int nt = 32;
   for (int g = 0; g < pb.ng; ++g) nt = std::max(nt, pick_nt(pb.g[g].ld_out));
   int tiles = 0;
   for (int g = 0; g < pb.ng; ++g) {
+    const ProjGroup& G = pb.g[g];
     a.tile_base[g] = tiles;
-    a.n_tiles[g] = static_cast<int>(ceil_div(pb.g[g].ld_out, nt));
-    tiles += static_cast<int>(ceil_div(std::max(1, pb.g[g].rows_cap), 128)) * a.n_tiles[g];
+    a.n_tiles[g] = static_cast<int>(ceil_div(G.ld_out, nt));
+    tiles += static_cast<int>(ceil_div(std::max(1, G.rows_cap), 128)) * a.n_tiles[g];
+    for (int r = 0; r < G.nrel; ++r) {
+      const ProjRel& R = G.r[r];
+      CUtensorMap* M = &a.maps[map_index(kProject, g, r, 0)];
+      encode(M + 0, R.mean, R.ld_mean, G.rows_cap, R.ld_mean, 128, false);
+      encode(M + 1, R.mean_lo, R.ld_mean, G.rows_cap, R.ld_mean, 128, false);
+      encode(M + 2, R.w, R.ld_w, R.din, R.ld_w, 32, true);
+      encode(M + 3, R.w_lo, R.ld_w, R.din, R.ld_w, 32, true);
+    }
   }
   a.tile_base[pb.ng] = tiles;
   dispatch<kProject>(a, nt, tiles, st);
@@ -378,18 +351,26 @@ void project_umma(ProjBatch& pb, cudaStream_t st) {
 
 void dmean_umma(DMeanBatch& b, cudaStream_t st) {
   if (b.np == 0) return;
-  for (int q = 0; q < b.np; ++q)
-    if (b.p[q].d.h) throw std::invalid_argument("tcgen05 mean gradient expects an already masked dpre");
-  UmmaArgs<DMeanBatch> a{};
+  static thread_local UmmaArgs<DMeanBatch> a;
+  a = UmmaArgs<DMeanBatch>{};
   a.b = b;
   a.np = b.np;
   int nt = 32;
   for (int q = 0; q < b.np; ++q) nt = std::max(nt, pick_nt(b.p[q].ld_dmean));
   int tiles = 0;
   for (int q = 0; q < b.np; ++q) {
+    const DMeanProblem& P = b.p[q];
+    if (P.d.h) throw std::invalid_argument("tcgen05 mean gradient expects an already masked dpre");
     a.tile_base[q] = tiles;
-    a.n_tiles[q] = static_cast<int>(ceil_div(b.p[q].ld_dmean, nt));
-    tiles += static_cast<int>(ceil_div(std::max(1, b.p[q].rows_cap), 128)) * a.n_tiles[q];
+    a.n_tiles[q] = static_cast<int>(ceil_div(P.ld_dmean, nt));
+    tiles += static_cast<int>(ceil_div(std::max(1, P.rows_cap), 128)) * a.n_tiles[q];
+    CUtensorMap* M = &a.maps[map_index(kDMean, q, 0, 0)];
+    const std::size_t off = static_cast<std::size_t>(P.d.offset) * P.d.ld;
+    const std::uint64_t rstride = static_cast<std::uint64_t>(P.d.stride) * P.d.ld;
+    encode(M + 0, P.d.g + off, P.d.ld, P.rows_cap, rstride, 128, false);
+    encode(M + 1, P.d.g_lo ? P.d.g_lo + off : nullptr, P.d.ld, P.rows_cap, rstride, 128, false);
+    encode(M + 2, P.w, P.ld_w, P.din, P.ld_w, nt, false);
+    encode(M + 3, P.w_lo, P.ld_w, P.din, P.ld_w, nt, false);
   }
   a.tile_base[b.np] = tiles;
   dispatch<kDMean>(a, nt, tiles, st);
@@ -397,9 +378,8 @@ void dmean_umma(DMeanBatch& b, cudaStream_t st) {
 
 void wgrad_umma(WGradBatch& b, cudaStream_t st) {
   if (b.np == 0) return;
-  for (int q = 0; q < b.np; ++q)
-    if (b.p[q].d.h) throw std::invalid_argument("tcgen05 weight gradient expects an already masked dpre");
-  UmmaArgs<WGradBatch> a{};
+  static thread_local UmmaArgs<WGradBatch> a;
+  a = UmmaArgs<WGradBatch>{};
   a.b = b;
   a.np = b.np;
   int nt = 32;
@@ -407,10 +387,18 @@ void wgrad_umma(WGradBatch& b, cudaStream_t st) {
   int tiles = 0;
   for (int q = 0; q < b.np; ++q) {
     const WGradProblem& P = b.p[q];
+    if (P.d.h) throw std::invalid_argument("tcgen05 weight gradient expects an already masked dpre");
     a.tile_base[q] = tiles;
     a.n_tiles[q] = static_cast<int>(ceil_div(P.d.cols, nt));
     a.m_tiles[q] = static_cast<int>(ceil_div(P.din, 128));
     tiles += static_cast<int>(ceil_div(std::max(1, P.rows_cap), kWChunkRows)) * a.m_tiles[q] * a.n_tiles[q];
+    CUtensorMap* M = &a.maps[map_index(kWGrad, q, 0, 0)];
+    const std::size_t off = static_cast<std::size_t>(P.d.offset) * P.d.ld;
+    const std::uint64_t rstride = static_cast<std::uint64_t>(P.d.stride) * P.d.ld;
+    encode(M + 0, P.mean, P.ld_mean, P.rows_cap, P.ld_mean, 32, true);
+    encode(M + 1, P.mean_lo, P.ld_mean, P.rows_cap, P.ld_mean, 32, true);
+    encode(M + 2, P.d.g + off, P.d.ld, P.rows_cap, rstride, 32, true);
+    encode(M + 3, P.d.g_lo ? P.d.g_lo + off : nullptr, P.d.ld, P.rows_cap, rstride, 32, true);
   }
   a.tile_base[b.np] = tiles;
   dispatch<kWGrad>(a, nt, tiles, st);
