@@ -117,6 +117,9 @@ Engine::Engine(const Graph& g, const EngineOptions& o) : o_(o) {
   if (o.k < 1) throw std::invalid_argument("fanouts must be non-empty");
   HG_CUDA(cudaSetDevice(o.device));
   HG_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  HG_CUDA(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking));
+  fork_ev_.resize(16);
+  for (auto& e : fork_ev_) HG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   ntypes_ = g.num_types();
   target_ = g.target;
   num_classes_ = g.num_classes;
@@ -135,11 +138,30 @@ Engine::~Engine() {
   if (exec_eval_) cudaGraphExecDestroy(exec_eval_);
   for (auto e : ev_pool_) cudaEventDestroy(e);
   for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
+  cudaStreamSynchronize(st2_);
+  for (auto e : fork_ev_) cudaEventDestroy(e);
   for (void* p : allocs_) cudaFree(p);
   if (h_sc_) cudaFreeHost(h_sc_);
   if (h_batch_) cudaFreeHost(h_batch_);
   if (h_rb_) cudaFreeHost(h_rb_);
+  cudaStreamDestroy(st2_);
   cudaStreamDestroy(st_);
+}
+
+void Engine::fork() {
+  if (side() == st_) return;
+  if (fork_used_ >= static_cast<int>(fork_ev_.size())) throw std::runtime_error("fork events exhausted");
+  cudaEvent_t e = fork_ev_[fork_used_++];
+  HG_CUDA(cudaEventRecord(e, st_));
+  HG_CUDA(cudaStreamWaitEvent(st2_, e, 0));
+}
+
+void Engine::join() {
+  if (side() == st_) return;
+  if (fork_used_ >= static_cast<int>(fork_ev_.size())) throw std::runtime_error("fork events exhausted");
+  cudaEvent_t e = fork_ev_[fork_used_++];
+  HG_CUDA(cudaEventRecord(e, st2_));
+  HG_CUDA(cudaStreamWaitEvent(st_, e, 0));
 }
 
 void* Engine::alloc(std::size_t bytes) {
@@ -611,6 +633,8 @@ void Engine::upload(const Graph& g) {
     tiles = std::max<std::size_t>(tiles, kMaxSegs * (ceil_div(max_cap, kScanTile) + 1));
     lb_.cap = static_cast<int>(tiles);
     lb_.mem = static_cast<unsigned long long*>(alloc((tiles + 1) * 8));
+    lb2_.cap = static_cast<int>(tiles);
+    lb2_.mem = static_cast<unsigned long long*>(alloc((tiles + 1) * 8));
   }
   slow_ = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(total_rows + 1) * 8));
   n_slow_ = static_cast<int*>(alloc(sizeof(int)));
@@ -730,19 +754,26 @@ void Engine::run_sampling() {
           if (c.hop == h && c.src_t == b.src_t) cnt = c.offs;
       ra.b[ra.nblk++] = {b.src, b.indptr, sh.b[q].n_rows, b.col, b.edge_cap, slot_of_type[b.src_t], cnt};
     }
-    HG_CUDA(cudaMemsetAsync(bits_, 0, static_cast<std::size_t>(total_words_) * 4, st_));
+    // the last hop's frontier is not needed by the forward pass (layer 1 reads
+    // its sources by global id): it and every transposed view run on the side
+    // stream, overlapping the next hop's sampling and the forward
+    if (h == k) fork();
+    cudaStream_t fs = h == k ? side() : st_;
+    LbScratch& flb = h == k && fs != st_ ? lb2_ : lb_;
+    HG_CUDA(cudaMemsetAsync(bits_, 0, static_cast<std::size_t>(total_words_) * 4, fs));
     if (csc_region_[h].words) {
-      HG_CUDA(cudaMemsetAsync(csc_region_[h].offs, 0, csc_region_[h].words * 4, st_));
-      HG_CUDA(cudaMemsetAsync(csc_region_[h].cursor, 0, csc_region_[h].words * 4, st_));
+      HG_CUDA(cudaMemsetAsync(csc_region_[h].offs, 0, csc_region_[h].words * 4, fs));
+      HG_CUDA(cudaMemsetAsync(csc_region_[h].cursor, 0, csc_region_[h].words * 4, fs));
     }
     timed("frontier", 0, [&] {
-      frontier_mark(ma, fa, st_);
-      frontier_compact(fa, lb_, st_);
-      frontier_relabel(ra, fa, st_);
+      frontier_mark(ma, fa, fs);
+      frontier_compact(fa, flb, fs);
+      frontier_relabel(ra, fa, fs);
     });
     // transposed views of this hop (independent of the forward values)
+    if (h < k) fork();
     const CscHop ch = csc_hop(h);
-    timed("csc_build", 0, [&] { csc_prepare(ch, lb_, st_); });
+    timed("csc_build", 0, [&] { csc_prepare(ch, side() == st_ ? lb_ : lb2_, side()); });
   }
   EdgeCountArgs ec{};
   for (const auto& b : blocks_) {
@@ -775,7 +806,7 @@ void Engine::run_sampling() {
     for (int t = 0; t < ntypes_; ++t)
       if (cache_types_[t] && front(k, t).cap > 0)
         cache_count(front(k, t).list, front(k, t).count, front(k, t).cap, cached_bits_ + word_base_[t],
-                    cache_hm_ + 2 * t, st_);
+                    cache_hm_ + 2 * t, side());
 }
 
 void Engine::run_forward() {
@@ -882,6 +913,7 @@ void Engine::run_loss() {
 
 void Engine::run_backward() {
   const int k = o_.k;
+  join();  // the hop-k frontier and the transposed views (side stream)
   // learnable layer-0 tables advance their Adam step before the fused row update
   {
     std::vector<const std::int64_t*> steps;
@@ -920,7 +952,10 @@ void Engine::run_backward() {
           db.p[db.np++] = {dv, s.w, s.ld, b.din, b.indptr, n_rows, rows_cap, b.dmean, b.ld_mean, s.w_lo};
       }
     }
-    timed("weight_grad", 0, [&] { use_umma_ ? wgrad_umma(wb, st_) : wgrad_tiles(wb, st_); });
+    // dpre of this layer is complete on st_: the weight gradient runs beside the
+    // mean gradient and the next backward gather
+    fork();
+    timed("weight_grad", 0, [&] { use_umma_ ? wgrad_umma(wb, side()) : wgrad_tiles(wb, side()); });
     timed("mean_grad", 0, [&] { use_umma_ ? dmean_umma(db, st_) : dmean_tiles(db, st_); });
     // scatter back to the sources of this hop, as ordered gathers (learnable
     // layer-0 rows get their Adam update in the same pass)
@@ -928,6 +963,7 @@ void Engine::run_backward() {
     AdamHyper hp;
     timed("csc_gather", 0, [&] { csc_gather(ch, hp, err_, st_); });
   }
+  join();  // weight gradients
   if (replica_group_.size() > 1) timed("replica_sync", 0, [&] { run_replica_merge(); });
 }
 
@@ -1098,6 +1134,7 @@ StepScalars Engine::next_scalars(std::uint64_t rng_seed, int n, int designated, 
 // memory. Captured once per mode into a CUDA graph and replayed (profiling
 // runs it eagerly so every kernel class can be bracketed by events).
 void Engine::step_body(bool train) {
+  fork_used_ = 0;
   HG_CUDA(cudaMemsetAsync(err_, 0, sizeof(std::uint32_t), st_));
   run_sampling();
   run_forward();
@@ -1106,6 +1143,7 @@ void Engine::step_body(bool train) {
     run_backward();
     run_update();
   }
+  join();  // nothing of this step may remain on the side stream
   HG_CUDA(cudaMemcpyAsync(h_rb_, loss_, sizeof(Readback), cudaMemcpyDeviceToHost, st_));
 }
 
@@ -1236,7 +1274,9 @@ void Engine::sample_only(const NodeId* batch, int n, std::uint64_t rng_seed) {
   h_sc_->rng_seed = rng_seed;
   h_sc_->batch_len = n;
   HG_CUDA(cudaMemcpyAsync(d_sc_, h_sc_, sizeof(StepScalars), cudaMemcpyHostToDevice, st_));
+  fork_used_ = 0;
   run_sampling();
+  join();
   HG_CUDA(cudaStreamSynchronize(st_));
   HG_CUDA(cudaGetLastError());
 }
@@ -1259,7 +1299,9 @@ std::vector<std::vector<std::uint32_t>> Engine::presample_hotness(int epochs, st
       h_sc_->rng_seed = rs;
       h_sc_->batch_len = static_cast<int>(batch.size());
       HG_CUDA(cudaMemcpyAsync(d_sc_, h_sc_, sizeof(StepScalars), cudaMemcpyHostToDevice, st_));
+      fork_used_ = 0;
       run_sampling();
+      join();
       // +1 per seed, +1 per sampled source occurrence (cache.cpp:51-56)
       hotness_add_list(front(0, target_).list, front(0, target_).count, o_.batch_cap, counts[target_], st_);
       for (const auto& b : blocks_)

@@ -94,6 +94,12 @@ class Engine {
   void enqueue_step_device(const StepScalars* d_src, const std::uint32_t* d_ids, int n, bool train);
   StepScalars next_scalars(std::uint64_t rng_seed, int n, int designated, bool train);
   void set_graphs(bool on) { use_graphs_ = on; }
+  void set_side_stream(bool on) {
+    if (on != use_side_) {
+      use_side_ = on;
+      drop_graphs();
+    }
+  }
   void set_umma(bool on) {
     if (on != use_umma_) {
       use_umma_ = on;
@@ -229,6 +235,17 @@ class Engine {
   int shard_index_ = 0, shard_count_ = 1;
 
   cudaStream_t st_ = nullptr;
+  // side stream for work off the critical path (captured as parallel graph
+  // branches): the hop-k frontier + transposed views overlap the forward pass,
+  // weight gradients overlap the mean gradients and backward gathers
+  cudaStream_t st2_ = nullptr;
+  std::vector<cudaEvent_t> fork_ev_;
+  int fork_used_ = 0;
+  LbScratch lb2_;  // look-back scratch of the side stream
+  bool use_side_ = true;
+  cudaStream_t side() const { return (profiling_ || !use_side_) ? st_ : st2_; }
+  void fork();  // side stream waits for everything queued on st_ so far
+  void join();  // st_ waits for everything queued on the side stream so far
   std::vector<void*> allocs_;
   std::size_t total_bytes_ = 0;
 
