@@ -288,14 +288,13 @@ __global__ void __launch_bounds__(256) k_adam_rows(AdamRowsBatch b, AdamHyper hp
   __shared__ AdamStep ks[kMaxSegs];
   if (threadIdx.x < b.n) ks[threadIdx.x] = adam_step_of(hp, static_cast<double>(*b.t[threadIdx.x].step));
   __syncthreads();
-  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < b.total4; x += gridDim.x * blockDim.x) {
-    int s = 0;
-    while (s + 1 < b.n && x >= b.base4[s + 1]) ++s;
+  // per table, only its live rows (capacities can be far larger than the union)
+  for (int s = 0; s < b.n; ++s) {
     const AdamRowsTable& T = b.t[s];
-    const int q = x - b.base4[s];
     const int per_row = T.ld / 4;
-    const int i = q / per_row, c = (q % per_row) * 4;
-    if (i >= *T.n_rows) continue;
+    const int total = *T.n_rows * per_row;
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
+    const int i = x / per_row, c = (x % per_row) * 4;
     const std::size_t at = static_cast<std::size_t>(T.ids[i]) * T.ld + c;
     float4 w = *reinterpret_cast<float4*>(T.w + at);
     float4 m = *reinterpret_cast<float4*>(T.m + at);
@@ -305,6 +304,7 @@ __global__ void __launch_bounds__(256) k_adam_rows(AdamRowsBatch b, AdamHyper hp
     *reinterpret_cast<float4*>(T.w + at) = w;
     *reinterpret_cast<float4*>(T.m + at) = m;
     *reinterpret_cast<float4*>(T.v + at) = v;
+    }
   }
 }
 

@@ -964,7 +964,7 @@ void Engine::run_backward() {
     timed("csc_gather", 0, [&] { csc_gather(ch, hp, err_, st_); });
   }
   join();  // weight gradients
-  if (replica_group_.size() > 1) timed("replica_sync", 0, [&] { run_replica_merge(); });
+  if (replica_group_.size() > 1) run_replica_merge();
 }
 
 // Replica group gradient synchronisation (raf.cpp:496-510 accounts it as a ring
@@ -979,13 +979,15 @@ void Engine::run_replica_merge() {
   // 1. weight gradients; completing it also orders every replica's gradient rows
   //    (written by its csc_gather before its all-reduce) before our reads below
   // (a launch-count capture leaves the collectives out, see count_launches)
-  if (!counting_ && ncclGroupStart() != ncclSuccess) throw std::runtime_error("ncclGroupStart failed");
-  for (auto& sl : slots_)
-    if (!counting_)
-    if (ncclAllReduce(sl.g, sl.g, static_cast<std::size_t>(std::max(1, sl.din)) * sl.ld, ncclFloat, ncclSum, rcomm_,
-                      st_) != ncclSuccess)
-      throw std::runtime_error("ncclAllReduce (replica weight gradients) failed");
-  if (!counting_ && ncclGroupEnd() != ncclSuccess) throw std::runtime_error("ncclGroupEnd failed");
+  timed("replica_wgrad", 0, [&] {
+    if (counting_) return;
+    if (ncclGroupStart() != ncclSuccess) throw std::runtime_error("ncclGroupStart failed");
+    for (auto& sl : slots_)
+      if (ncclAllReduce(sl.g, sl.g, static_cast<std::size_t>(std::max(1, sl.din)) * sl.ld, ncclFloat, ncclSum, rcomm_,
+                        st_) != ncclSuccess)
+        throw std::runtime_error("ncclAllReduce (replica weight gradients) failed");
+    if (ncclGroupEnd() != ncclSuccess) throw std::runtime_error("ncclGroupEnd failed");
+  });
   // 2. learnable rows: union + ordered sums, then step and Adam on the union
   AdamRowsBatch ab{};
   int base = 0;
@@ -1003,7 +1005,9 @@ void Engine::run_replica_merge() {
            x.ucap};
     m.slot = x.slot;
     m.ug = x.ug;
-    replica_merge(m, lb_, st_);
+    timed("replica_union", 0, [&] { replica_union(m, lb_, st_); });
+    timed("replica_slots", 0, [&] { replica_slots(m, st_); });
+    timed("replica_sum", 0, [&] { replica_sum(m, st_); });
     const TypeTable& tb = tables_[x.t];
     ab.t[ab.n] = {tb.w, tb.m, tb.v, tb.ld, x.ulist, x.ug, x.ld, x.ucount, tb.step};
     ab.base4[ab.n] = base;
@@ -1011,10 +1015,13 @@ void Engine::run_replica_merge() {
     ++ab.n;
   }
   ab.total4 = base;
-  adam_rows(ab, AdamHyper{}, err_, st_);  // bumps each table's step iff its union is non-empty
+  // bumps each table's step iff its union is non-empty
+  timed("replica_adam", 0, [&] { adam_rows(ab, AdamHyper{}, err_, st_); });
   // 3. nobody rewrites its arena (next step's sampling) before every peer read it
-  if (!counting_ && ncclAllReduce(barrier_word_, barrier_word_, 1, ncclFloat, ncclSum, rcomm_, st_) != ncclSuccess)
-    throw std::runtime_error("ncclAllReduce (replica barrier) failed");
+  timed("replica_barrier", 0, [&] {
+    if (!counting_ && ncclAllReduce(barrier_word_, barrier_word_, 1, ncclFloat, ncclSum, rcomm_, st_) != ncclSuccess)
+      throw std::runtime_error("ncclAllReduce (replica barrier) failed");
+  });
 #else
   throw std::runtime_error("replica groups need NCCL");
 #endif

@@ -603,7 +603,7 @@ __global__ void __launch_bounds__(256) k_rsum(ReplicaMerge m) {
 
 }  // namespace
 
-void replica_merge(const ReplicaMerge& m, LbScratch& lb, cudaStream_t st) {
+void replica_union(const ReplicaMerge& m, LbScratch& lb, cudaStream_t st) {
   HG_CUDA(cudaMemsetAsync(m.u.bits, 0, static_cast<std::size_t>(m.u.words) * 4, st));
   const dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(m.u.cap, 256), 2 * kNumSMs)), m.n_rep);
   k_rmark<<<grid, 256, 0, st>>>(m);
@@ -611,11 +611,21 @@ void replica_merge(const ReplicaMerge& m, LbScratch& lb, cudaStream_t st) {
   f.ntypes = 1;
   f.t[0] = m.u;
   frontier_compact(f, lb, st);
+}
+void replica_slots(const ReplicaMerge& m, cudaStream_t st) {
   HG_CUDA(cudaMemsetAsync(m.slot, 0xFF, static_cast<std::size_t>(m.n_rep) * m.u.cap * sizeof(int), st));
+  const dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(m.u.cap, 256), 2 * kNumSMs)), m.n_rep);
   k_rslot<<<grid, 256, 0, st>>>(m);
+}
+void replica_sum(const ReplicaMerge& m, cudaStream_t st) {
   const unsigned g2 = static_cast<unsigned>(
       std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(m.u.cap * ceil_div(m.din, 64), 16), 16 * kNumSMs)));
   k_rsum<<<g2, 256, 0, st>>>(m);
+}
+void replica_merge(const ReplicaMerge& m, LbScratch& lb, cudaStream_t st) {
+  replica_union(m, lb, st);
+  replica_slots(m, st);
+  replica_sum(m, st);
 }
 
 // ---- cache / hotness counters -------------------------------------------------------------

@@ -278,6 +278,10 @@ struct ReplicaMerge {
   float* ug;    // [u.cap x ld] merged gradient rows
 };
 void replica_merge(const ReplicaMerge& m, LbScratch& lb, cudaStream_t st);
+// its three stages: union (bitmap + compaction), per-replica row slots, ordered sums
+void replica_union(const ReplicaMerge& m, LbScratch& lb, cudaStream_t st);
+void replica_slots(const ReplicaMerge& m, cudaStream_t st);
+void replica_sum(const ReplicaMerge& m, cudaStream_t st);
 
 // ---- misc --------------------------------------------------------------------------------
 void zero_rows(float* p, int ld, const int* n_rows, int rows_cap, cudaStream_t st);
