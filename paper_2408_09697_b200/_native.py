@@ -12,7 +12,8 @@ from typing import Dict
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhetgpu.so")
+# HETGPU_LIB: an alternative build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("HETGPU_LIB") or os.path.join(HERE, "libhetgpu.so")
 
 _lib = None
 
