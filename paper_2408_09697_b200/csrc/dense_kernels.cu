@@ -124,18 +124,22 @@ __device__ __forceinline__ void adam4(float4& w, float4& m, float4& v, const flo
   }
 }
 
+// entries hold the packed (block, destination row) of every sampled edge
+// (block index in the top 4 bits): the backward gather reads dmean rows directly
+constexpr int kRowBits = 28;
 __global__ void k_csc_fill(CscHop h) {
-  const CscEdges& b = h.b[blockIdx.y];
+  const int bi = blockIdx.y;
+  const CscEdges& b = h.b[bi];
   const CscType& t = h.t[b.type];
   const std::uint32_t total = b.indptr[*b.n_rows];
   for (std::uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
     const std::uint32_t c = b.col[e];
     const std::uint32_t pos = atomicAdd(t.cursor + c, 1u);
-    t.entries[t.offs[c] - 1 - pos] = static_cast<std::uint32_t>(b.edge_base) + e;
+    t.entries[t.offs[c] - 1 - pos] = (static_cast<std::uint32_t>(bi) << kRowBits) | b.erow[e];
   }
 }
 
-// make every segment ascending in (block, edge): deterministic summation order
+// make every segment ascending in (block, row): deterministic summation order
 __global__ void k_csc_sort(CscHop h) {
   const CscType& t = h.t[blockIdx.y];
   const int n = *t.n_src;
@@ -174,7 +178,7 @@ __global__ void __launch_bounds__(256) k_csc_gather(CscHop h, AdamHyper hp, std:
       if (f >= t.ld_dh) continue;
       const std::uint32_t lo = c ? t.offs[c - 1] : 0u, hi = t.offs[c];
       float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-      // up to 4 edges in flight: entry ids, then block rows, then dmean rows
+      // up to 4 edges in flight: packed entries, then dmean rows
       for (std::uint32_t x0 = lo; x0 < hi; x0 += 4) {
         const int cnt = min(4u, hi - x0);
         const float* rowp[4];
@@ -182,12 +186,9 @@ __global__ void __launch_bounds__(256) k_csc_gather(CscHop h, AdamHyper hp, std:
         for (int q = 0; q < 4; ++q) {
           rowp[q] = nullptr;
           if (q < cnt) {
-            const std::uint32_t id = __ldg(t.entries + x0 + q);
-            int bi = 0;
-            while (bi + 1 < h.nb && id >= static_cast<std::uint32_t>(h.b[bi + 1].edge_base)) ++bi;
-            const CscEdges& b = h.b[bi];
-            const std::uint32_t row = __ldg(b.erow + (id - b.edge_base));
-            rowp[q] = b.dmean + static_cast<std::size_t>(row) * b.ld_dmean + f;
+            const std::uint32_t key = __ldg(t.entries + x0 + q);  // packed (block, row)
+            const CscEdges& b = h.b[key >> kRowBits];
+            rowp[q] = b.dmean + static_cast<std::size_t>(key & ((1u << kRowBits) - 1)) * b.ld_dmean + f;
           }
         }
         float4 v[4];

@@ -288,6 +288,7 @@ void Engine::build_plan(const Graph& g) {
       const std::uint64_t per_row = std::min<std::uint64_t>(o_.fanouts[h - 1], maxdeg_[r]);
       const std::uint64_t ec = std::max<std::uint64_t>(1, static_cast<std::uint64_t>(b.rows_cap) * per_row);
       if (ec > 0x7fffffffULL) throw std::invalid_argument("block edge capacity exceeds 2^31");
+      if (b.rows_cap >= (1 << 28)) throw std::invalid_argument("block row capacity exceeds 2^28");
       b.edge_cap = static_cast<int>(ec);
       b.edge_base = edge_base;
       edge_base += b.edge_cap;

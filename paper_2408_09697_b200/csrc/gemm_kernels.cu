@@ -317,14 +317,18 @@ __global__ void __launch_bounds__(256) k_gather_mean(MeanBatch m) {
     const std::uint32_t lo = B.indptr[i], hi = B.indptr[i + 1];
     const float* base = B.h + c;
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-    std::uint32_t e = lo;
-    for (; e + 8 <= hi; e += 8) {
+    // batches of 8 neighbours (the last one predicated): one key round trip and
+    // one row round trip per batch, summed in edge order
+    for (std::uint32_t e = lo; e < hi; e += 8) {
+      const std::uint32_t cnt = min(8u, hi - e);
       std::uint32_t kk[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) kk[q] = __ldg(B.keys + e + q);
+      for (int q = 0; q < 8; ++q) kk[q] = q < cnt ? __ldg(B.keys + e + q) : 0u;
       float4 v[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = __ldg(reinterpret_cast<const float4*>(base + static_cast<std::size_t>(kk[q]) * B.ld_h));
+      for (int q = 0; q < 8; ++q)
+        v[q] = q < cnt ? __ldg(reinterpret_cast<const float4*>(base + static_cast<std::size_t>(kk[q]) * B.ld_h))
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         s.x += v[q].x;
@@ -332,13 +336,6 @@ __global__ void __launch_bounds__(256) k_gather_mean(MeanBatch m) {
         s.z += v[q].z;
         s.w += v[q].w;
       }
-    }
-    for (; e < hi; ++e) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(base + static_cast<std::size_t>(__ldg(B.keys + e)) * B.ld_h));
-      s.x += v.x;
-      s.y += v.y;
-      s.z += v.z;
-      s.w += v.w;
     }
     if (hi > lo) {
       const float inv = 1.0f / static_cast<float>(hi - lo);

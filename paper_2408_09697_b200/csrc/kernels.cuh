@@ -185,7 +185,7 @@ void cross_entropy(const LossArgs& a, cudaStream_t st);
 struct CscType {
   std::uint32_t* offs;     // [src_cap + 1]: counts, then inclusive prefix
   std::uint32_t* cursor;   // [src_cap]
-  std::uint32_t* entries;  // edge ids (edge_base + e) grouped by source row
+  std::uint32_t* entries;  // packed (block << 28 | destination row) of every edge, grouped by source row
   const int* n_src;
   int src_cap;
   float* dh;               // gradient rows (nullptr: not materialised)
