@@ -356,6 +356,24 @@ class Sampler:
         return N.take(N.lib().hg_engine_read(self._h, ",".join(names).encode()))
 
 
+def cache_stats(counters: Dict[str, np.ndarray], kinds: Sequence[int], transfer_ns: Sequence[float]) -> List[dict]:
+    """CacheState accounting (cache.cpp:87-113, hook harness.cpp:425-437) from the
+    engine's per-type lookup counters: every layer-0 frontier id is looked up,
+    and learnable types (kind 2) are also updated, which counts a second
+    hit/miss; each miss adds the type's transfer penalty."""
+    out = []
+    for t, kind in enumerate(kinds):
+        key = f"cache.t{t}"
+        if key not in counters:
+            continue
+        hits, misses = (int(x) for x in counters[key])
+        mult = 2 if int(kind) == 2 else 1
+        h, m = hits * mult, misses * mult
+        out.append(dict(type=t, hits=h, misses=m, hit_rate=h / (h + m) if h + m else 0.0,
+                        penalty_ns=m * float(transfer_ns[t])))
+    return out
+
+
 def agg_all_comm_bytes(active_rows: Sequence[int], designated: int, num_classes: int, elem_bytes: int = 4,
                        header_bytes: int = 32) -> Dict[str, int]:
     """CommStats of one batch's AGG_all exchange (raf.cpp:427-466, payload_bytes

@@ -151,3 +151,20 @@ def test_tensor_core_tile_shapes():
     err = N.take(N.lib().hg_selftest_contractions(N.ptr(arr), len(cases), 0))["err"]
     bad = [(cases[i], err[i].tolist()) for i in range(len(cases)) if not np.all(err[i] < 2e-5)]
     assert not bad, bad[:8]
+
+
+def test_toy_config_run_experiment(H, ref):
+    # BASELINE configs[0]: 4 types x 128-d dense, 5 uniform
+    # relations without reverses, fanout [10,10], hidden 64, batch 1024: the
+    # per-batch losses of the reference's run_experiment, batch by batch
+    spec = H.toy_spec()
+    seed, nb = 1, 3
+    cfg = {"spec": spec, "partitioner": "meta", "p": 1, "engine": "raf", "fanouts": [10, 10], "hidden": 64,
+           "batch_size": 1024, "epochs": 1, "max_batches_per_epoch": nb, "seed": seed}
+    stats, _, ok = ref.run_experiment(cfg)
+    assert ok
+    g = H.gen_synthetic(spec, seed)
+    eng = H.Engine.for_experiment(g, [10, 10], 64, seed, batch_cap=1024)
+    batches = H.make_batches(g, 1024, nb, H.mix_seed(seed, 0xBA7C))
+    losses = [eng.step(b, H.mix_seed(seed, 0xB000 + i), 0)["loss"] for i, b in enumerate(batches)]
+    np.testing.assert_allclose(losses, [b["loss"] for b in stats["batches"]], rtol=1e-3, atol=0)
