@@ -246,7 +246,11 @@ def run_b200(args):
     e2e_sl = slice(args.warmup + args.steps, args.warmup + 2 * args.steps)
     barrier()
     te = time.perf_counter()
-    for b, s in zip(batches[e2e_sl], seeds[e2e_sl]):
+    e2e_b, e2e_s = batches[e2e_sl], seeds[e2e_sl]
+    eng.prefetch(e2e_b[0], e2e_s[0])
+    for i, (b, s) in enumerate(zip(e2e_b, e2e_s)):
+        if i + 1 < len(e2e_b):
+            eng.prefetch(e2e_b[i + 1], e2e_s[i + 1])  # sampled while batch i trains
         rep = eng.step(b, s, 0, train=True)
         edges_rank += rep["sampled_edges"]
     barrier()

@@ -137,6 +137,11 @@ void hg_engine_free(hg_engine* e);
  * train = 0 runs forward + loss only. */
 int hg_engine_step(hg_engine* e, const uint32_t* batch, int n, uint64_t rng_seed, int designated,
                    int train, hg_step_report* out);
+/* Sampling depends only on (graph, batch, rng_seed): hg_engine_prefetch samples a future
+ * batch into the engine's second sample slot on its sampling stream and returns at once;
+ * a later hg_engine_step with the same (batch, rng_seed) trains on it, so the sampling of
+ * batch i+1 overlaps the training of batch i. At most two batches may be in flight. */
+int hg_engine_prefetch(hg_engine* e, const uint32_t* batch, int n, uint64_t rng_seed);
 /* sample_khop_restricted (src/sampling.cpp:99-103) with the engine's hop relation sets. */
 int hg_engine_sample(hg_engine* e, const uint32_t* batch, int n, uint64_t rng_seed);
 /* Named device tensors after the last call (comma-separated names, NULL = all):

@@ -373,6 +373,11 @@ class RafEngine {
     out.active_rows.assign(r.active_rows, r.active_rows + r.n_active);
     return out;
   }
+  // sample a future batch now (second sample slot, sampling stream); the next
+  // run_raf_batch with the same (batch, rng_seed) trains on it meanwhile
+  void prefetch(std::span<const NodeId> batch, std::uint64_t rng_seed) {
+    detail::check(hg_engine_prefetch(e_.get(), batch.data(), static_cast<int>(batch.size()), rng_seed));
+  }
   // device tensors by name (hetgpu.h hg_engine_read), widened like the reference's Matrix
   detail::Bundle read(const std::string& names) { return detail::Bundle(hg_engine_read(e_.get(), names.c_str())); }
   // presample_hotness (cache.cpp:39-63): per type, visit counts over `epochs` id-ordered passes

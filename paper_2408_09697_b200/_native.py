@@ -82,6 +82,7 @@ def lib():
             "hg_engine_free": ([vp], None),
             "hg_engine_step": ([vp, vp, i32, u64, i32, i32, C.POINTER(StepReport)], i32),
             "hg_engine_sample": ([vp, vp, i32, u64], i32),
+            "hg_engine_prefetch": ([vp, vp, i32, u64], i32),
             "hg_engine_read": ([vp, C.c_char_p], vp),
             "hg_engine_bench": ([vp, vp, vp, vp, i32, i32, C.POINTER(C.c_double), C.POINTER(C.c_uint64),
                                  C.POINTER(C.c_double)], i32),

@@ -360,6 +360,13 @@ int hg_engine_step(hg_engine* e, const uint32_t* batch, int n, uint64_t rng_seed
   });
 }
 
+int hg_engine_prefetch(hg_engine* e, const uint32_t* batch, int n, uint64_t rng_seed) {
+  return guard<int>(-1, [&] {
+    e->e->prefetch(batch, n, rng_seed);
+    return 0;
+  });
+}
+
 int hg_engine_sample(hg_engine* e, const uint32_t* batch, int n, uint64_t rng_seed) {
   return guard<int>(-1, [&] {
     e->e->sample_only(batch, n, rng_seed);
@@ -422,14 +429,18 @@ int hg_engine_bench(hg_engine* e, const uint32_t* batches, const int* lens, cons
     cudaEvent_t a, b;
     HG_CUDA(cudaEventCreate(&a));
     HG_CUDA(cudaEventCreate(&b));
-    HG_CUDA(cudaStreamSynchronize(en.stream()));
+    en.quiesce();
     HG_CUDA(cudaEventRecord(a, en.stream()));
-    std::size_t off = 0;
+    HG_CUDA(cudaStreamWaitEvent(en.sample_stream(), a, 0));  // sampling is inside the timed region
+    std::vector<std::size_t> off(n_steps + 1, 0);
+    for (int i = 0; i < n_steps; ++i) off[i + 1] = off[i] + lens[i];
     std::uint64_t edges = 0;
     double loss = 0.0;
+    // batch i+1 is sampled (sampling stream) while batch i trains
+    if (n_steps > 0) en.prefetch_device(d_all + off[0], lens[0], d_sc + 0);
     for (int i = 0; i < n_steps; ++i) {
-      en.enqueue_step_device(d_sc + i, d_all + off, lens[i], train != 0);
-      off += lens[i];
+      if (i + 1 < n_steps) en.prefetch_device(d_all + off[i + 1], lens[i + 1], d_sc + i + 1);
+      en.train_device(d_sc + i, train != 0);
     }
     HG_CUDA(cudaEventRecord(b, en.stream()));
     HG_CUDA(cudaEventSynchronize(b));

@@ -118,6 +118,11 @@ Engine::Engine(const Graph& g, const EngineOptions& o) : o_(o) {
   HG_CUDA(cudaSetDevice(o.device));
   HG_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
   HG_CUDA(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking));
+  HG_CUDA(cudaStreamCreateWithFlags(&st_s_, cudaStreamNonBlocking));
+  for (int sl = 0; sl < 2; ++sl) {
+    HG_CUDA(cudaEventCreateWithFlags(&ev_sampled_[sl], cudaEventDisableTiming));
+    HG_CUDA(cudaEventCreateWithFlags(&ev_trained_[sl], cudaEventDisableTiming));
+  }
   fork_ev_.resize(16);
   for (auto& e : fork_ev_) HG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   ntypes_ = g.num_types();
@@ -134,16 +139,24 @@ Engine::Engine(const Graph& g, const EngineOptions& o) : o_(o) {
 
 Engine::~Engine() {
   cudaStreamSynchronize(st_);
-  if (exec_train_) cudaGraphExecDestroy(exec_train_);
-  if (exec_eval_) cudaGraphExecDestroy(exec_eval_);
+  drop_graphs();
   for (auto e : ev_pool_) cudaEventDestroy(e);
   for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
   cudaStreamSynchronize(st2_);
   for (auto e : fork_ev_) cudaEventDestroy(e);
   for (void* p : allocs_) cudaFree(p);
-  if (h_sc_) cudaFreeHost(h_sc_);
-  if (h_batch_) cudaFreeHost(h_batch_);
-  if (h_rb_) cudaFreeHost(h_rb_);
+  for (int sl = 0; sl < 2; ++sl) {
+    if (h_sc_slot_[sl]) cudaFreeHost(h_sc_slot_[sl]);
+    if (h_batch_slot_[sl]) cudaFreeHost(h_batch_slot_[sl]);
+    if (h_rb_slot_[sl]) cudaFreeHost(h_rb_slot_[sl]);
+    if (ev_sampled_[sl]) cudaEventDestroy(ev_sampled_[sl]);
+    if (ev_trained_[sl]) cudaEventDestroy(ev_trained_[sl]);
+  }
+  if (h_tsc_) cudaFreeHost(h_tsc_);
+  if (st_s_) {
+    cudaStreamSynchronize(st_s_);
+    cudaStreamDestroy(st_s_);
+  }
   cudaStreamDestroy(st2_);
   cudaStreamDestroy(st_);
 }
@@ -154,10 +167,12 @@ void Engine::fork() {
   cudaEvent_t e = fork_ev_[fork_used_++];
   HG_CUDA(cudaEventRecord(e, st_));
   HG_CUDA(cudaStreamWaitEvent(st2_, e, 0));
+  side_open_ = true;
 }
 
 void Engine::join() {
-  if (side() == st_) return;
+  if (side() == st_ || !side_open_) return;  // nothing was forked since the last join
+  side_open_ = false;
   if (fork_used_ >= static_cast<int>(fork_ev_.size())) throw std::runtime_error("fork events exhausted");
   cudaEvent_t e = fork_ev_[fork_used_++];
   HG_CUDA(cudaEventRecord(e, st2_));
@@ -465,8 +480,10 @@ void Engine::upload(const Graph& g) {
   for (int t = 0; t < ntypes_; ++t)
     word_base_[t + 1] = word_base_[t] + static_cast<int>(ceil_div(type_counts_[t], 32));
   total_words_ = std::max(1, word_base_[ntypes_]);
-  bits_ = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(total_words_) * 4));
-  wscan_ = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(total_words_) * 4));
+  for (int sl = 0; sl < 2; ++sl) {
+    bits_slot_[sl] = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(total_words_) * 4));
+    wscan_slot_[sl] = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(total_words_) * 4));
+  }
   cached_bits_ = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(total_words_) * 4));
   // static per-hop frontier slot layout: slot i of hop h is the i-th distinct
   // source type of that hop's blocks (hop 0: the target)
@@ -505,17 +522,16 @@ void Engine::upload(const Graph& g) {
       x.cap = front(k, c.src_t).cap;
       x.ld = c.ld;
       x.din = c.din;
-      x.off_count = take(sizeof(int));
-      x.off_ids = take(static_cast<std::size_t>(std::max(1, x.cap)) * 4);
+      for (int sl = 0; sl < 2; ++sl) {
+        x.off_count[sl] = take(sizeof(int));
+        x.off_ids[sl] = take(static_cast<std::size_t>(std::max(1, x.cap)) * 4);
+      }
       x.off_dh = take(static_cast<std::size_t>(std::max(1, x.cap)) * x.ld * 4);
       xchg_.push_back(x);
     }
     arena_bytes_ = std::max<std::size_t>(at, 256);
     arena_ = static_cast<std::uint8_t*>(alloc(arena_bytes_));
     for (auto& x : xchg_) {
-      Front& f = front(k, x.t);
-      f.count = reinterpret_cast<int*>(arena_ + x.off_count);
-      f.list = reinterpret_cast<std::uint32_t*>(arena_ + x.off_ids);
       for (auto& c : cscs_)
         if (c.hop == k && c.src_t == x.t) c.dh = reinterpret_cast<float*>(arena_ + x.off_dh);
       x.ucap = static_cast<int>(std::min<std::uint64_t>(type_counts_[x.t],
@@ -529,22 +545,34 @@ void Engine::upload(const Graph& g) {
     peer_arena_.assign(replica_group_.size(), nullptr);
     peer_arena_[replica_pos_] = arena_;
   }
-  for (int h = 0; h <= k; ++h)
-    for (int t = 0; t < ntypes_; ++t) {
-      Front& f = front(h, t);
-      if (h == k && xchg_type(t)) continue;  // lives in the exchange arena
-      f.count = static_cast<int*>(alloc(sizeof(int)));
-      if (f.cap > 0) f.list = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(f.cap) * 4));
-    }
-  shard_list_ = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(o_.batch_cap) * 4));
-  shard_count_dev_ = static_cast<int*>(alloc(sizeof(int)));
+  for (int sl = 0; sl < 2; ++sl) {
+    fronts_slot_[sl] = fronts_;  // capacities
+    for (int h = 0; h <= k; ++h)
+      for (int t = 0; t < ntypes_; ++t) {
+        Front& f = fronts_slot_[sl][h * ntypes_ + t];
+        if (h == k && xchg_type(t)) {  // lives in the exchange arena
+          for (const auto& x : xchg_)
+            if (x.t == t) {
+              f.count = reinterpret_cast<int*>(arena_ + x.off_count[sl]);
+              f.list = reinterpret_cast<std::uint32_t*>(arena_ + x.off_ids[sl]);
+            }
+          continue;
+        }
+        f.count = static_cast<int*>(alloc(sizeof(int)));
+        if (f.cap > 0) f.list = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(f.cap) * 4));
+      }
+    shard_list_slot_[sl] = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(o_.batch_cap) * 4));
+    shard_count_slot_[sl] = static_cast<int*>(alloc(sizeof(int)));
+  }
 
   int max_rows = 1, total_rows = 0;
   for (auto& b : blocks_) {
-    b.indptr = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(b.rows_cap + 1) * 4));
-    b.src = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(b.edge_cap) * 4));
-    b.erow = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(b.edge_cap) * 4));
-    b.col = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(b.edge_cap) * 4));
+    for (int sl = 0; sl < 2; ++sl) {
+      b.s_indptr[sl] = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(b.rows_cap + 1) * 4));
+      b.s_src[sl] = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(b.edge_cap) * 4));
+      b.s_erow[sl] = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(b.edge_cap) * 4));
+      b.s_col[sl] = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(b.edge_cap) * 4));
+    }
     if (!o_.sample_only) {
       b.mean = static_cast<float*>(alloc(static_cast<std::size_t>(b.rows_cap) * b.ld_mean * 4));
       b.mean_lo = static_cast<float*>(alloc(static_cast<std::size_t>(b.rows_cap) * b.ld_mean * 4));
@@ -570,28 +598,30 @@ void Engine::upload(const Graph& g) {
     }
   }
   // transposed views: per hop one contiguous offs/cursor region (one memset each)
-  csc_region_.assign(o_.k + 1, {nullptr, nullptr, 0});
-  for (int h = 1; h <= o_.k; ++h) {
-    std::size_t words = 0;
-    for (const auto& c : cscs_)
-      if (c.hop == h) words += static_cast<std::size_t>(c.src_cap) + 1;
-    if (!words) continue;
-    auto& reg = csc_region_[h];
-    reg.words = words;
-    reg.offs = static_cast<std::uint32_t*>(alloc(words * 4));
-    reg.cursor = static_cast<std::uint32_t*>(alloc(words * 4));
-    std::size_t at = 0;
-    for (auto& c : cscs_) {
-      if (c.hop != h) continue;
-      c.offs = reg.offs + at;
-      c.cursor = reg.cursor + at;
-      at += static_cast<std::size_t>(c.src_cap) + 1;
+  for (int sl = 0; sl < 2; ++sl) {
+    csc_region_slot_[sl].assign(o_.k + 1, {nullptr, nullptr, 0});
+    for (int h = 1; h <= o_.k; ++h) {
+      std::size_t words = 0;
+      for (const auto& c : cscs_)
+        if (c.hop == h) words += static_cast<std::size_t>(c.src_cap) + 1;
+      if (!words) continue;
+      auto& reg = csc_region_slot_[sl][h];
+      reg.words = words;
+      reg.offs = static_cast<std::uint32_t*>(alloc(words * 4));
+      reg.cursor = static_cast<std::uint32_t*>(alloc(words * 4));
+      std::size_t at = 0;
+      for (auto& c : cscs_) {
+        if (c.hop != h) continue;
+        c.s_offs[sl] = reg.offs + at;
+        c.s_cursor[sl] = reg.cursor + at;
+        at += static_cast<std::size_t>(c.src_cap) + 1;
+      }
     }
   }
   for (auto& c : cscs_) {
     std::size_t ent = 0;
     for (int bi : c.blocks) ent = std::max<std::size_t>(ent, blocks_[bi].edge_base + blocks_[bi].edge_cap);
-    c.entries = static_cast<std::uint32_t*>(alloc(ent * 4));
+    for (int sl = 0; sl < 2; ++sl) c.s_entries[sl] = static_cast<std::uint32_t*>(alloc(ent * 4));
     if (!(c.hop == o_.k && xchg_type(c.src_t)))
       c.dh = static_cast<float*>(alloc(static_cast<std::size_t>(std::max(1, c.src_cap)) * c.ld * 4));
     if (c.hop < o_.k) {
@@ -605,18 +635,20 @@ void Engine::upload(const Graph& g) {
   }
 
   // per-step state and scratch
-  d_sc_ = static_cast<StepScalars*>(alloc(sizeof(StepScalars)));
-  HG_CUDA(cudaMallocHost(&h_sc_, sizeof(StepScalars)));
-  std::memset(h_sc_, 0, sizeof(StepScalars));
-  d_batch_ = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(o_.batch_cap) * 4));
-  HG_CUDA(cudaMallocHost(&h_batch_, static_cast<std::size_t>(o_.batch_cap) * 4));
-  mult_ = static_cast<float*>(alloc(static_cast<std::size_t>(o_.batch_cap) * 4));
+  for (int sl = 0; sl < 2; ++sl) {
+    d_sc_slot_[sl] = static_cast<StepScalars*>(alloc(sizeof(StepScalars)));
+    HG_CUDA(cudaMallocHost(&h_sc_slot_[sl], sizeof(StepScalars)));
+    std::memset(h_sc_slot_[sl], 0, sizeof(StepScalars));
+    d_batch_slot_[sl] = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(o_.batch_cap) * 4));
+    HG_CUDA(cudaMallocHost(&h_batch_slot_[sl], static_cast<std::size_t>(o_.batch_cap) * 4));
+    mult_slot_[sl] = static_cast<float*>(alloc(static_cast<std::size_t>(o_.batch_cap) * 4));
+    rb_slot_[sl] = static_cast<Readback*>(alloc(sizeof(Readback)));
+    HG_CUDA(cudaMallocHost(&h_rb_slot_[sl], sizeof(Readback)));
+  }
+  d_tsc_ = static_cast<StepScalars*>(alloc(sizeof(StepScalars)));
+  HG_CUDA(cudaMallocHost(&h_tsc_, sizeof(StepScalars)));
+  std::memset(h_tsc_, 0, sizeof(StepScalars));
   row_loss_ = static_cast<double*>(alloc(static_cast<std::size_t>(o_.batch_cap) * 8));
-  auto* rb = static_cast<Readback*>(alloc(sizeof(Readback)));
-  loss_ = &rb->loss;
-  err_ = &rb->err;
-  edges_dev_ = &rb->edges;
-  HG_CUDA(cudaMallocHost(&h_rb_, sizeof(Readback)));
   cache_hm_ = static_cast<unsigned long long*>(alloc(sizeof(unsigned long long) * 2 * ntypes_));
   alg_bytes_ = static_cast<double*>(alloc(sizeof(double) * 4));
   cache_types_.assign(ntypes_, false);
@@ -657,6 +689,37 @@ void Engine::upload(const Graph& g) {
   wt_scratch_ = static_cast<float*>(alloc(wt * 4));
   wgrad_partial_ = static_cast<float*>(alloc(wp * 4));
   HG_CUDA(cudaStreamSynchronize(st_));
+  bind_slot(0);
+}
+
+void Engine::bind_slot(int s) {
+  bound_ = s;
+  fronts_ = fronts_slot_[s];
+  bits_ = bits_slot_[s];
+  wscan_ = wscan_slot_[s];
+  shard_list_ = shard_list_slot_[s];
+  shard_count_dev_ = shard_count_slot_[s];
+  for (auto& b : blocks_) {
+    b.indptr = b.s_indptr[s];
+    b.src = b.s_src[s];
+    b.erow = b.s_erow[s];
+    b.col = b.s_col[s];
+  }
+  for (auto& c : cscs_) {
+    c.offs = c.s_offs[s];
+    c.cursor = c.s_cursor[s];
+    c.entries = c.s_entries[s];
+  }
+  csc_region_ = csc_region_slot_[s];
+  d_sc_ = d_sc_slot_[s];
+  h_sc_ = h_sc_slot_[s];
+  d_batch_ = d_batch_slot_[s];
+  h_batch_ = h_batch_slot_[s];
+  mult_ = mult_slot_[s];
+  loss_ = &rb_slot_[s]->loss;
+  err_ = &rb_slot_[s]->err;
+  edges_dev_ = &rb_slot_[s]->edges;
+  h_rb_ = h_rb_slot_[s];
 }
 
 std::uint64_t Engine::param_count() const {
@@ -699,22 +762,22 @@ void Engine::resolve_profile() {
   ev_used_ = 0;
 }
 
-void Engine::run_sampling() {
+void Engine::run_sampling(cudaStream_t ss) {
   const int k = o_.k;
   // frontier[0][target] = sorted unique batch (bitmap), with multiplicities
   FrontierArgs f0{};
   f0.ntypes = 1;
   f0.t[0] = {bits_ + word_base_[target_], word_base_[target_ + 1] - word_base_[target_], wscan_ + word_base_[target_],
              front(0, target_).list, front(0, target_).count, front(0, target_).cap};
-  HG_CUDA(cudaMemsetAsync(bits_, 0, static_cast<std::size_t>(total_words_) * 4, st_));
-  HG_CUDA(cudaMemsetAsync(mult_, 0, static_cast<std::size_t>(o_.batch_cap) * 4, st_));
+  HG_CUDA(cudaMemsetAsync(bits_, 0, static_cast<std::size_t>(total_words_) * 4, ss));
+  HG_CUDA(cudaMemsetAsync(mult_, 0, static_cast<std::size_t>(o_.batch_cap) * 4, ss));
   timed("frontier", 0, [&] {
-    frontier_mark_batch(d_batch_, d_sc_, o_.batch_cap, f0.t[0], st_);
-    frontier_compact(f0, lb_, st_);
-    batch_multiplicity(d_batch_, d_sc_, o_.batch_cap, f0.t[0], mult_, st_);
+    frontier_mark_batch(d_batch_, d_sc_, o_.batch_cap, f0.t[0], ss);
+    frontier_compact(f0, lb_, ss);
+    batch_multiplicity(d_batch_, d_sc_, o_.batch_cap, f0.t[0], mult_, ss);
   });
   if (replica_)
-    k_shard_rows<<<4, 256, 0, st_>>>(front(0, target_).list, front(0, target_).count, shard_index_, shard_count_,
+    k_shard_rows<<<4, 256, 0, ss>>>(front(0, target_).list, front(0, target_).count, shard_index_, shard_count_,
                                      shard_list_, shard_count_dev_);
 
   for (int h = 1; h <= k; ++h) {
@@ -734,7 +797,7 @@ void Engine::run_sampling() {
       s.rel = b.rel;
       s.rows_cap = b.rows_cap;
     }
-    timed("sample", 0, [&] { sample_hop(sh, d_sc_, slow_, n_slow_, mt_scratch_, lb_, st_); });
+    timed("sample", 0, [&] { sample_hop(sh, d_sc_, slow_, n_slow_, mt_scratch_, lb_, ss); });
 
     // frontier[h][t]: bitmap of every sampled source, compacted in id order
     FrontierArgs fa{};
@@ -755,26 +818,19 @@ void Engine::run_sampling() {
           if (c.hop == h && c.src_t == b.src_t) cnt = c.offs;
       ra.b[ra.nblk++] = {b.src, b.indptr, sh.b[q].n_rows, b.col, b.edge_cap, slot_of_type[b.src_t], cnt};
     }
-    // the last hop's frontier is not needed by the forward pass (layer 1 reads
-    // its sources by global id): it and every transposed view run on the side
-    // stream, overlapping the next hop's sampling and the forward
-    if (h == k) fork();
-    cudaStream_t fs = h == k ? side() : st_;
-    LbScratch& flb = h == k && fs != st_ ? lb2_ : lb_;
-    HG_CUDA(cudaMemsetAsync(bits_, 0, static_cast<std::size_t>(total_words_) * 4, fs));
+    HG_CUDA(cudaMemsetAsync(bits_, 0, static_cast<std::size_t>(total_words_) * 4, ss));
     if (csc_region_[h].words) {
-      HG_CUDA(cudaMemsetAsync(csc_region_[h].offs, 0, csc_region_[h].words * 4, fs));
-      HG_CUDA(cudaMemsetAsync(csc_region_[h].cursor, 0, csc_region_[h].words * 4, fs));
+      HG_CUDA(cudaMemsetAsync(csc_region_[h].offs, 0, csc_region_[h].words * 4, ss));
+      HG_CUDA(cudaMemsetAsync(csc_region_[h].cursor, 0, csc_region_[h].words * 4, ss));
     }
     timed("frontier", 0, [&] {
-      frontier_mark(ma, fa, fs);
-      frontier_compact(fa, flb, fs);
-      frontier_relabel(ra, fa, fs);
+      frontier_mark(ma, fa, ss);
+      frontier_compact(fa, lb_, ss);
+      frontier_relabel(ra, fa, ss);
     });
     // transposed views of this hop (independent of the forward values)
-    if (h < k) fork();
     const CscHop ch = csc_hop(h);
-    timed("csc_build", 0, [&] { csc_prepare(ch, side() == st_ ? lb_ : lb2_, side()); });
+    timed("csc_build", 0, [&] { csc_prepare(ch, lb_, ss); });
   }
   EdgeCountArgs ec{};
   for (const auto& b : blocks_) {
@@ -782,7 +838,7 @@ void Engine::run_sampling() {
     ec.n_rows[ec.n] = block_rows(b);
     ++ec.n;
   }
-  k_count_edges<<<1, 32, 0, st_>>>(ec, edges_dev_);
+  k_count_edges<<<1, 32, 0, ss>>>(ec, edges_dev_);
   if (profiling_) {
     AlgBytesArgs ab{};
     for (const auto& b : blocks_) {
@@ -800,14 +856,14 @@ void Engine::run_sampling() {
       ab.c_row_bytes_mult[ab.ncsc] = leaf_learnable ? (retain_grads_ ? 7 : 6) : 1;
       ++ab.ncsc;
     }
-    k_alg_bytes<<<1, 32, 0, st_>>>(ab, alg_bytes_);
+    k_alg_bytes<<<1, 32, 0, ss>>>(ab, alg_bytes_);
   }
   // cache lookups + updates over the layer-0 frontier (harness.cpp:425-437)
   if (cache_on_)
     for (int t = 0; t < ntypes_; ++t)
       if (cache_types_[t] && front(k, t).cap > 0)
         cache_count(front(k, t).list, front(k, t).count, front(k, t).cap, cached_bits_ + word_base_[t],
-                    cache_hm_ + 2 * t, side());
+                    cache_hm_ + 2 * t, ss);
 }
 
 void Engine::run_forward() {
@@ -903,7 +959,7 @@ void Engine::run_loss() {
   la.row_ids = front(0, target_).list;
   la.mult = mult_;
   la.labels = labels_;
-  la.sc = d_sc_;
+  la.sc = d_tsc_;  // batch_len of the step being trained
   la.dlogits = dlogits_;
   la.dlogits_lo = dlogits_lo_;
   la.row_loss = row_loss_;
@@ -914,7 +970,6 @@ void Engine::run_loss() {
 
 void Engine::run_backward() {
   const int k = o_.k;
-  join();  // the hop-k frontier and the transposed views (side stream)
   // learnable layer-0 tables advance their Adam step before the fused row update
   {
     std::vector<const std::int64_t*> steps;
@@ -996,8 +1051,8 @@ void Engine::run_replica_merge() {
     ReplicaMerge m{};
     m.n_rep = static_cast<int>(peer_arena_.size());
     for (int r = 0; r < m.n_rep; ++r) {
-      m.ids[r] = reinterpret_cast<const std::uint32_t*>(peer_arena_[r] + x.off_ids);
-      m.count[r] = reinterpret_cast<const int*>(peer_arena_[r] + x.off_count);
+      m.ids[r] = reinterpret_cast<const std::uint32_t*>(peer_arena_[r] + x.off_ids[bound_]);
+      m.count[r] = reinterpret_cast<const int*>(peer_arena_[r] + x.off_count[bound_]);
       m.dh[r] = reinterpret_cast<const float*>(peer_arena_[r] + x.off_dh);
     }
     m.ld = x.ld;
@@ -1006,7 +1061,7 @@ void Engine::run_replica_merge() {
            x.ucap};
     m.slot = x.slot;
     m.ug = x.ug;
-    timed("replica_union", 0, [&] { replica_union(m, lb_, st_); });
+    timed("replica_union", 0, [&] { replica_union(m, lb2_, st_); });  // lb_ belongs to the sampling stream
     timed("replica_slots", 0, [&] { replica_slots(m, st_); });
     timed("replica_sum", 0, [&] { replica_sum(m, st_); });
     const TypeTable& tb = tables_[x.t];
@@ -1123,7 +1178,75 @@ void Engine::run_update() {
     ++mb.n;
   }
   mb.total4 = base;
-  timed("adam", 0, [&] { adam_model(mb, &d_sc_->model_step, hp, err_, st_); });
+  timed("adam", 0, [&] { adam_model(mb, &d_tsc_->model_step, hp, err_, st_); });
+}
+
+
+// Sampling of the bound slot: everything that depends only on (graph, batch,
+// rng_seed). Training of the bound slot: forward, AGG_all, loss, backward, Adam
+// and the readback. Each is captured once per slot into a CUDA graph and replayed
+// (profiling runs them eagerly on st_ so every kernel class can be bracketed).
+void Engine::sample_body(cudaStream_t ss) {
+  HG_CUDA(cudaMemsetAsync(err_, 0, sizeof(std::uint32_t), ss));
+  run_sampling(ss);
+}
+
+void Engine::train_body(bool train) {
+  fork_used_ = 0;
+  side_open_ = false;
+  run_forward();
+  run_loss();
+  if (train) {
+    run_backward();
+    run_update();
+  }
+  join();  // nothing of this step may remain on the side stream
+  HG_CUDA(cudaMemcpyAsync(h_rb_, loss_, sizeof(Readback), cudaMemcpyDeviceToHost, st_));
+}
+
+void Engine::step_body(bool train) {
+  sample_body(st_);
+  train_body(train);
+}
+
+namespace {
+template <typename F>
+void capture(cudaGraphExec_t& ex, cudaStream_t st, F&& body) {
+  cudaGraph_t graph = nullptr;
+  HG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  try {
+    body();
+  } catch (...) {
+    cudaStreamEndCapture(st, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    throw;
+  }
+  HG_CUDA(cudaStreamEndCapture(st, &graph));
+  HG_CUDA(cudaGraphInstantiate(&ex, graph, 0));
+  cudaGraphDestroy(graph);
+}
+}  // namespace
+
+void Engine::enqueue_sample(int s) {
+  bind_slot(s);
+  cudaStream_t ss = sstream();
+  if (!use_graphs_ || profiling_) {
+    sample_body(ss);
+    return;
+  }
+  if (!exec_sample_[s]) capture(exec_sample_[s], ss, [&] { sample_body(ss); });
+  HG_CUDA(cudaGraphLaunch(exec_sample_[s], ss));
+}
+
+void Engine::enqueue_train(int s, bool train) {
+  bind_slot(s);
+  if (!use_graphs_ || profiling_) {
+    train_body(train);
+    return;
+  }
+  cudaGraphExec_t& ex = train ? exec_train_[s] : exec_eval_[s];
+  if (!ex) capture(ex, st_, [&] { train_body(train); });
+  HG_CUDA(cudaGraphLaunch(ex, st_));
 }
 
 StepScalars Engine::next_scalars(std::uint64_t rng_seed, int n, int designated, bool train) {
@@ -1138,62 +1261,58 @@ StepScalars Engine::next_scalars(std::uint64_t rng_seed, int n, int designated, 
   return sc;
 }
 
-// The step body: everything after the batch ids and step scalars are in device
-// memory. Captured once per mode into a CUDA graph and replayed (profiling
-// runs it eagerly so every kernel class can be bracketed by events).
-void Engine::step_body(bool train) {
-  fork_used_ = 0;
-  HG_CUDA(cudaMemsetAsync(err_, 0, sizeof(std::uint32_t), st_));
-  run_sampling();
-  run_forward();
-  run_loss();
-  if (train) {
-    run_backward();
-    run_update();
-  }
-  join();  // nothing of this step may remain on the side stream
-  HG_CUDA(cudaMemcpyAsync(h_rb_, loss_, sizeof(Readback), cudaMemcpyDeviceToHost, st_));
+void Engine::prefetch(const NodeId* batch, int n, std::uint64_t rng_seed) {
+  if (o_.sample_only) throw std::invalid_argument("a sampler engine has no model to step");
+  if (n > o_.batch_cap) throw std::invalid_argument("batch larger than the engine's batch capacity");
+  if (n <= 0) throw std::invalid_argument("empty batch");
+  for (int i = 0; i < n; ++i)
+    if (batch[i] >= type_counts_[target_])
+      throw std::invalid_argument("seed node id out of range: " + std::to_string(batch[i]));
+  if (pending_slots_.size() >= 2) throw std::runtime_error("two batches already prefetched: step one first");
+  const int s = next_slot_;
+  next_slot_ ^= 1;
+  cudaStream_t ss = sstream();
+  // the slot is free once the step that last trained on it is done
+  HG_CUDA(cudaStreamWaitEvent(ss, ev_trained_[s], 0));
+  HG_CUDA(cudaStreamSynchronize(ss));  // the slot's pinned staging buffers are reusable
+  std::memcpy(h_batch_slot_[s], batch, sizeof(NodeId) * n);
+  *h_sc_slot_[s] = StepScalars{rng_seed, n, 0, 0};
+  HG_CUDA(cudaMemcpyAsync(d_batch_slot_[s], h_batch_slot_[s], sizeof(NodeId) * n, cudaMemcpyHostToDevice, ss));
+  HG_CUDA(cudaMemcpyAsync(d_sc_slot_[s], h_sc_slot_[s], sizeof(StepScalars), cudaMemcpyHostToDevice, ss));
+  enqueue_sample(s);
+  HG_CUDA(cudaEventRecord(ev_sampled_[s], ss));
+  pending_slots_.push_back({s, rng_seed, std::vector<NodeId>(batch, batch + n)});
 }
 
-void Engine::launch_body(bool train) {
-  if (!use_graphs_ || profiling_) {
-    step_body(train);
-    return;
-  }
-  cudaGraphExec_t& ex = train ? exec_train_ : exec_eval_;
-  if (!ex) {
-    cudaGraph_t graph = nullptr;
-    HG_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
-    try {
-      step_body(train);
-    } catch (...) {
-      cudaStreamEndCapture(st_, &graph);
-      if (graph) cudaGraphDestroy(graph);
-      throw;
-    }
-    HG_CUDA(cudaStreamEndCapture(st_, &graph));
-    HG_CUDA(cudaGraphInstantiate(&ex, graph, 0));
-    cudaGraphDestroy(graph);
-  }
-  HG_CUDA(cudaGraphLaunch(ex, st_));
+void Engine::prefetch_device(const std::uint32_t* d_ids, int n, const StepScalars* d_ss) {
+  if (pending_slots_.size() >= 2) throw std::runtime_error("two batches already prefetched: step one first");
+  const int s = next_slot_;
+  next_slot_ ^= 1;
+  cudaStream_t ss = sstream();
+  HG_CUDA(cudaStreamWaitEvent(ss, ev_trained_[s], 0));
+  HG_CUDA(cudaMemcpyAsync(d_batch_slot_[s], d_ids, static_cast<std::size_t>(n) * 4, cudaMemcpyDeviceToDevice, ss));
+  HG_CUDA(cudaMemcpyAsync(d_sc_slot_[s], d_ss, sizeof(StepScalars), cudaMemcpyDeviceToDevice, ss));
+  enqueue_sample(s);
+  HG_CUDA(cudaEventRecord(ev_sampled_[s], ss));
+  pending_slots_.push_back({s, 0, {}});
 }
 
-void Engine::enqueue_step(std::uint64_t rng_seed, int n, int designated, bool train) {
-  *h_sc_ = next_scalars(rng_seed, n, designated, train);
-  HG_CUDA(cudaMemcpyAsync(d_sc_, h_sc_, sizeof(StepScalars), cudaMemcpyHostToDevice, st_));
-  launch_body(train);
-}
-
-void Engine::enqueue_step_device(const StepScalars* d_src, const std::uint32_t* d_ids, int n, bool train) {
-  HG_CUDA(cudaMemcpyAsync(d_batch_, d_ids, static_cast<std::size_t>(n) * 4, cudaMemcpyDeviceToDevice, st_));
-  HG_CUDA(cudaMemcpyAsync(d_sc_, d_src, sizeof(StepScalars), cudaMemcpyDeviceToDevice, st_));
-  launch_body(train);
+void Engine::train_device(const StepScalars* d_ts, bool train) {
+  if (pending_slots_.empty()) throw std::runtime_error("no sampled batch to train");
+  const int s = pending_slots_.front().slot;
+  pending_slots_.erase(pending_slots_.begin());
+  HG_CUDA(cudaMemcpyAsync(d_tsc_, d_ts, sizeof(StepScalars), cudaMemcpyDeviceToDevice, st_));
+  HG_CUDA(cudaStreamWaitEvent(st_, ev_sampled_[s], 0));
+  enqueue_train(s, train);
+  HG_CUDA(cudaEventRecord(ev_trained_[s], st_));
+  last_trained_ = s;
 }
 
 StepReport Engine::finish_step() {
   HG_CUDA(cudaStreamSynchronize(st_));
   HG_CUDA(cudaGetLastError());
   if (profiling_) resolve_profile();
+  bind_slot(last_trained_);
   StepReport r;
   r.loss = h_rb_->loss;
   r.err = h_rb_->err;
@@ -1212,13 +1331,25 @@ StepReport Engine::finish_step() {
 
 StepReport Engine::step(const NodeId* batch, int n, std::uint64_t rng_seed, int designated, bool train) {
   if (o_.sample_only) throw std::invalid_argument("a sampler engine has no model to step");
-  if (n > o_.batch_cap) throw std::invalid_argument("batch larger than the engine's batch capacity");
-  for (int i = 0; i < n; ++i)
-    if (batch[i] >= type_counts_[target_])
-      throw std::invalid_argument("seed node id out of range: " + std::to_string(batch[i]));
-  std::memcpy(h_batch_, batch, sizeof(NodeId) * n);
-  HG_CUDA(cudaMemcpyAsync(d_batch_, h_batch_, sizeof(NodeId) * n, cudaMemcpyHostToDevice, st_));
-  enqueue_step(rng_seed, n, designated, train);
+  // use the prefetched slot if it holds exactly this batch; otherwise sample now
+  const bool hit = !pending_slots_.empty() && pending_slots_.front().rng_seed == rng_seed &&
+                   pending_slots_.front().batch.size() == static_cast<std::size_t>(n) &&
+                   std::equal(batch, batch + n, pending_slots_.front().batch.begin());
+  if (!hit) {
+    if (!pending_slots_.empty()) {  // a stale prefetch: drop it (its slot is rewritten later)
+      HG_CUDA(cudaStreamSynchronize(sstream()));
+      pending_slots_.clear();
+    }
+    prefetch(batch, n, rng_seed);
+  }
+  const int s = pending_slots_.front().slot;
+  pending_slots_.erase(pending_slots_.begin());
+  *h_tsc_ = next_scalars(rng_seed, n, designated, train);
+  HG_CUDA(cudaMemcpyAsync(d_tsc_, h_tsc_, sizeof(StepScalars), cudaMemcpyHostToDevice, st_));
+  HG_CUDA(cudaStreamWaitEvent(st_, ev_sampled_[s], 0));
+  enqueue_train(s, train);
+  HG_CUDA(cudaEventRecord(ev_trained_[s], st_));
+  last_trained_ = s;
   return finish_step();
 }
 
@@ -1277,21 +1408,31 @@ void Engine::sample_only(const NodeId* batch, int n, std::uint64_t rng_seed) {
   for (int i = 0; i < n; ++i)
     if (batch[i] >= type_counts_[target_])
       throw std::invalid_argument("seed node id out of range: " + std::to_string(batch[i]));
+  quiesce();
+  bind_slot(0);
   std::memcpy(h_batch_, batch, sizeof(NodeId) * n);
   HG_CUDA(cudaMemcpyAsync(d_batch_, h_batch_, sizeof(NodeId) * n, cudaMemcpyHostToDevice, st_));
   h_sc_->rng_seed = rng_seed;
   h_sc_->batch_len = n;
   HG_CUDA(cudaMemcpyAsync(d_sc_, h_sc_, sizeof(StepScalars), cudaMemcpyHostToDevice, st_));
-  fork_used_ = 0;
-  run_sampling();
-  join();
+  sample_body(st_);
   HG_CUDA(cudaStreamSynchronize(st_));
   HG_CUDA(cudaGetLastError());
+}
+
+// finish everything in flight and forget prefetched batches (their slots are reused)
+void Engine::quiesce() {
+  HG_CUDA(cudaStreamSynchronize(st_s_));
+  HG_CUDA(cudaStreamSynchronize(st_));
+  pending_slots_.clear();
+  next_slot_ = 0;
 }
 
 // ---------------------------------------------------------------------------------------------
 std::vector<std::vector<std::uint32_t>> Engine::presample_hotness(int epochs, std::uint64_t seed, int batch_size) {
   if (batch_size > o_.batch_cap) throw std::invalid_argument("presample batch larger than the batch capacity");
+  quiesce();
+  bind_slot(0);
   std::vector<std::uint32_t*> counts(ntypes_, nullptr);
   for (int t = 0; t < ntypes_; ++t) counts[t] = static_cast<std::uint32_t*>(alloc(type_counts_[t] * 4));
   const std::uint64_t n_target = type_counts_[target_];
@@ -1307,9 +1448,7 @@ std::vector<std::vector<std::uint32_t>> Engine::presample_hotness(int epochs, st
       h_sc_->rng_seed = rs;
       h_sc_->batch_len = static_cast<int>(batch.size());
       HG_CUDA(cudaMemcpyAsync(d_sc_, h_sc_, sizeof(StepScalars), cudaMemcpyHostToDevice, st_));
-      fork_used_ = 0;
-      run_sampling();
-      join();
+      run_sampling(st_);
       // +1 per seed, +1 per sampled source occurrence (cache.cpp:51-56)
       hotness_add_list(front(0, target_).list, front(0, target_).count, o_.batch_cap, counts[target_], st_);
       for (const auto& b : blocks_)

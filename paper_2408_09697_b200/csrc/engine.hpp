@@ -86,13 +86,20 @@ class Engine {
   void attach_replicas(const std::vector<std::vector<char>>& handles_by_rank);
 
   // Full training step: sample, forward, AGG_all, loss, backward, Adam.
-  // `batch` is host memory (copied to the device inside the call).
+  // `batch` is host memory (copied to the device inside the call). If the same
+  // (batch, rng_seed) was handed to prefetch() before, its sampled blocks are used.
   StepReport step(const NodeId* batch, int n, std::uint64_t rng_seed, int designated, bool train = true);
-  // Same as step() but without the final synchronisation (batch already in d_batch_).
-  void enqueue_step(std::uint64_t rng_seed, int n, int designated, bool train);
-  // Benchmark inner loop: batch ids and step scalars already resident in HBM.
-  void enqueue_step_device(const StepScalars* d_src, const std::uint32_t* d_ids, int n, bool train);
+  // Sampling is a pure function of (graph, batch, rng_seed): prefetch() samples a
+  // future batch into the other of two sample slots on the sampling stream, so it
+  // runs while the current step trains (at most two batches in flight).
+  void prefetch(const NodeId* batch, int n, std::uint64_t rng_seed);
+  // Benchmark inner loop, inputs resident in HBM: sample a batch into the next
+  // slot (d_ss: its sampling scalars), then train the oldest sampled slot.
+  void prefetch_device(const std::uint32_t* d_ids, int n, const StepScalars* d_ss);
+  void train_device(const StepScalars* d_ts, bool train);
   StepScalars next_scalars(std::uint64_t rng_seed, int n, int designated, bool train);
+  cudaStream_t sample_stream() const { return st_s_; }
+  void quiesce();  // finish everything in flight, drop prefetched batches
   void set_graphs(bool on) { use_graphs_ = on; }
   void set_side_stream(bool on) {
     if (on != use_side_) {
@@ -114,7 +121,7 @@ class Engine {
       drop_graphs();
     }
   }
-  StepReport finish_step();
+  StepReport finish_step();  // waits for the last trained step and reads its report
   // Sampling only (parity of the sampler; presample_hotness).
   void sample_only(const NodeId* batch, int n, std::uint64_t rng_seed);
 
@@ -163,7 +170,8 @@ class Engine {
   struct BlockBuf {
     int rel = -1, hop = 0, src_t = -1, dst_t = -1;
     int rows_cap = 0, edge_cap = 0, edge_base = 0;
-    std::uint32_t *indptr = nullptr, *src = nullptr, *erow = nullptr, *col = nullptr;
+    std::uint32_t *indptr = nullptr, *src = nullptr, *erow = nullptr, *col = nullptr;  // bound sample slot
+    std::uint32_t *s_indptr[2] = {}, *s_src[2] = {}, *s_erow[2] = {}, *s_col[2] = {};
     float* mean = nullptr;   // tape: rows_cap x ld_mean (only for blocks feeding a layer)
     float* mean_lo = nullptr;  // its tf32 residual (tensor-core operand)
     float* dmean = nullptr;  // rows_cap x ld_mean (only if the source needs a gradient)
@@ -191,7 +199,8 @@ class Engine {
   struct CscBuf {
     int hop = 0, src_t = -1, src_cap = 0, din = 0, ld = 0;
     std::vector<int> blocks;
-    std::uint32_t *offs = nullptr, *cursor = nullptr, *entries = nullptr;
+    std::uint32_t *offs = nullptr, *cursor = nullptr, *entries = nullptr;  // bound sample slot
+    std::uint32_t *s_offs[2] = {}, *s_cursor[2] = {}, *s_entries[2] = {};
     float* dh = nullptr;  // gradient of H[hop][src_t] (or learnable rows)
     float* dh_lo = nullptr;  // tf32 residual of dh (inner types: the next layer's dpre)
   };
@@ -206,7 +215,7 @@ class Engine {
   void* alloc(std::size_t bytes);
   void build_plan(const Graph& g);
   void upload(const Graph& g);
-  void run_sampling();
+  void run_sampling(cudaStream_t ss);  // everything of one sample slot, on stream ss
   void run_forward();
   void run_loss();
   void run_backward();
@@ -241,6 +250,7 @@ class Engine {
   cudaStream_t st2_ = nullptr;
   std::vector<cudaEvent_t> fork_ev_;
   int fork_used_ = 0;
+  bool side_open_ = false;  // the side stream has work forked since the last join
   LbScratch lb2_;  // look-back scratch of the side stream
   bool use_side_ = true;
   cudaStream_t side() const { return (profiling_ || !use_side_) ? st_ : st2_; }
@@ -256,8 +266,40 @@ class Engine {
   std::vector<TypeTable> tables_;
   std::int32_t* labels_ = nullptr;
 
+  // ---- two sample slots: everything sampling writes exists twice; bind_slot(s)
+  // points the working pointers below at slot s (host-side rebinding: each
+  // captured graph is for one slot)
+  void bind_slot(int s);
+  int bound_ = 0;
+  std::vector<Front> fronts_slot_[2];
+  std::uint32_t *bits_slot_[2] = {}, *wscan_slot_[2] = {};
+  std::uint32_t* shard_list_slot_[2] = {};
+  int* shard_count_slot_[2] = {};
+  StepScalars *d_sc_slot_[2] = {}, *h_sc_slot_[2] = {};
+  std::uint32_t *d_batch_slot_[2] = {}, *h_batch_slot_[2] = {};
+  float* mult_slot_[2] = {};
+  struct Readback;
+  Readback *rb_slot_[2] = {}, *h_rb_slot_[2] = {};
+  // slots sampled and not trained yet (FIFO), with the host batch they hold
+  struct Pending {
+    int slot;
+    std::uint64_t rng_seed;
+    std::vector<NodeId> batch;
+  };
+  std::vector<Pending> pending_slots_;
+  int next_slot_ = 0, last_trained_ = 0;
+  cudaStream_t st_s_ = nullptr;  // sampling stream
+  cudaEvent_t ev_sampled_[2] = {}, ev_trained_[2] = {};
+  StepScalars* d_tsc_ = nullptr;  // scalars of the step being trained
+  StepScalars* h_tsc_ = nullptr;  // pinned
+  cudaStream_t sstream() const { return profiling_ ? st_ : st_s_; }
+  void enqueue_sample(int s);   // graph or eager sampling of slot s on sstream()
+  void enqueue_train(int s, bool train);
+  void sample_body(cudaStream_t ss);
+  void train_body(bool train);
+
   // frontier machinery
-  std::vector<Front> fronts_;       // [(k+1) x ntypes]
+  std::vector<Front> fronts_;       // [(k+1) x ntypes], bound slot
   std::vector<int> word_base_;      // per type, offset in words
   std::uint32_t *bits_ = nullptr, *wscan_ = nullptr, *cached_bits_ = nullptr;
   int total_words_ = 0;
@@ -294,7 +336,7 @@ class Engine {
     std::uint32_t pad;
     std::uint64_t edges;
   };
-  Readback* h_rb_ = nullptr;  // pinned
+  Readback* h_rb_ = nullptr;  // pinned, bound slot
   std::uint64_t* edges_dev_ = nullptr;
   unsigned long long* cache_hm_ = nullptr;  // [ntypes x 2]
 
@@ -318,8 +360,7 @@ class Engine {
   std::size_t ev_used_ = 0;
   double* alg_bytes_ = nullptr;
   void resolve_profile();
-  void step_body(bool train);
-  void launch_body(bool train);
+  void step_body(bool train);  // sample_body + train_body on st_ (launch counting)
   bool use_graphs_ = true;
   bool use_umma_ = true;
   bool counting_ = false;  // count_launches capture in progress (no collectives)  // tcgen05 contractions (0: SIMT fp32 tiles, kept for A/B checks)
@@ -328,14 +369,18 @@ class Engine {
     std::uint32_t *offs, *cursor;
     std::size_t words;
   };
-  std::vector<CscRegion> csc_region_;
+  std::vector<CscRegion> csc_region_;  // bound slot
+  std::vector<CscRegion> csc_region_slot_[2];
   CscHop csc_hop(int h);
   void drop_graphs() {
-    if (exec_train_) cudaGraphExecDestroy(exec_train_);
-    if (exec_eval_) cudaGraphExecDestroy(exec_eval_);
-    exec_train_ = exec_eval_ = nullptr;
+    for (int s = 0; s < 2; ++s) {
+      if (exec_train_[s]) cudaGraphExecDestroy(exec_train_[s]);
+      if (exec_eval_[s]) cudaGraphExecDestroy(exec_eval_[s]);
+      if (exec_sample_[s]) cudaGraphExecDestroy(exec_sample_[s]);
+      exec_train_[s] = exec_eval_[s] = exec_sample_[s] = nullptr;
+    }
   }
-  cudaGraphExec_t exec_train_ = nullptr, exec_eval_ = nullptr;
+  cudaGraphExec_t exec_train_[2] = {}, exec_eval_[2] = {}, exec_sample_[2] = {};
   std::map<std::string, double> kernel_ms_, kernel_bytes_;
   std::map<std::string, int> kernel_launches_;
   int launches_per_step_ = 0;
@@ -349,7 +394,7 @@ class Engine {
   // arena (frontier ids + count, gradient rows) and the merge scratch
   struct Xchg {
     int t = -1, cap = 0, ld = 0, din = 0;
-    std::size_t off_count = 0, off_ids = 0, off_dh = 0;  // offsets in every replica's arena
+    std::size_t off_count[2] = {}, off_ids[2] = {}, off_dh = 0;  // offsets in every replica's arena (per slot)
     std::uint32_t* ulist = nullptr;
     int* ucount = nullptr;
     int ucap = 0;

@@ -241,6 +241,13 @@ class Engine:
         return dict(loss=rep.loss, sampled_edges=int(rep.sampled_edges),
                     active_rows=[rep.active_rows[i] for i in range(rep.n_active)])
 
+    def prefetch(self, batch, rng_seed: int) -> None:
+        """Sample a future batch now (sampling stream, second sample slot); the
+        step() with the same (batch, rng_seed) then trains on it while the
+        next prefetch samples. Keeps the numbers identical to an unprefetched step."""
+        b = np.ascontiguousarray(batch, dtype=np.uint32)
+        N.check(N.lib().hg_engine_prefetch(self._h, N.ptr(b), len(b), rng_seed))
+
     def sample(self, seeds, rng_seed: int) -> None:
         b = np.ascontiguousarray(seeds, dtype=np.uint32)
         if b.size == 0:

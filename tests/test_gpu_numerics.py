@@ -168,3 +168,29 @@ def test_toy_config_run_experiment(H, ref):
     batches = H.make_batches(g, 1024, nb, H.mix_seed(seed, 0xBA7C))
     losses = [eng.step(b, H.mix_seed(seed, 0xB000 + i), 0)["loss"] for i, b in enumerate(batches)]
     np.testing.assert_allclose(losses, [b["loss"] for b in stats["batches"]], rtol=1e-3, atol=0)
+
+
+def test_prefetch_pipeline_is_bit_identical(H):
+    # sampling batch i+1 (second sample slot, sampling stream) while batch i
+    # trains must not change a single bit of the training trajectory
+    g = H.gen_synthetic(H.bundled_spec("mag-mini"), 5)
+    batches = H.make_batches(g, 128, 6, H.mix_seed(5, 0xBA7C))
+    seeds = [H.mix_seed(5, 0xB000 + i) for i in range(len(batches))]
+    plain = H.Engine.for_experiment(g, [25, 20], 32, 5, batch_cap=128)
+    ref_losses = [plain.step(b, s)["loss"] for b, s in zip(batches, seeds)]
+    piped = H.Engine.for_experiment(g, [25, 20], 32, 5, batch_cap=128)
+    piped.prefetch(batches[0], seeds[0])
+    losses = []
+    for i, (b, s) in enumerate(zip(batches, seeds)):
+        if i + 1 < len(batches):
+            piped.prefetch(batches[i + 1], seeds[i + 1])
+        losses.append(piped.step(b, s)["loss"])
+    assert losses == ref_losses
+    names = [n for n in plain.tensor_names() if n.startswith("post.")]
+    a, b = plain.read(*names), piped.read(*names)
+    for n in names:
+        assert np.array_equal(a[n], b[n]), n
+    # a step whose batch was not prefetched still samples it (stale prefetch dropped)
+    piped.prefetch(batches[1], seeds[1])
+    r = piped.step(batches[2], seeds[2])
+    assert np.isfinite(r["loss"])
