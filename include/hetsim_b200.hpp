@@ -391,6 +391,23 @@ class RafEngine {
   void attach_nccl(const std::vector<char>& unique_id, int nranks, int rank) {
     detail::check(hg_engine_attach_nccl(e_.get(), unique_id.data(), static_cast<int>(unique_id.size()), nranks, rank));
   }
+  // replica groups (p > #sub-metatrees): this rank's CUDA IPC handle of its gradient
+  // exchange arena (empty without replicas); every rank then maps all ranks' handles
+  std::vector<char> replica_handle() {
+    std::vector<char> h(128);
+    const int n = detail::check(hg_engine_replica_handle(e_.get(), h.data(), static_cast<int>(h.size())));
+    h.resize(n);
+    return h;
+  }
+  void attach_replicas(const std::vector<std::vector<char>>& handles_by_rank) {
+    std::size_t size = 1;
+    for (const auto& h : handles_by_rank) size = std::max(size, h.size());
+    std::vector<char> flat(size * handles_by_rank.size(), 0);
+    for (std::size_t r = 0; r < handles_by_rank.size(); ++r)
+      std::copy(handles_by_rank[r].begin(), handles_by_rank[r].end(), flat.begin() + r * size);
+    detail::check(hg_engine_attach_replicas(e_.get(), flat.data(), static_cast<int>(size),
+                                            static_cast<int>(handles_by_rank.size())));
+  }
   hg_engine* handle() const { return e_.get(); }
 
  private:
