@@ -664,16 +664,21 @@ void Engine::upload(const Graph& g) {
       tiles = std::max(tiles, t);
     }
     tiles = std::max<std::size_t>(tiles, kMaxSegs * (ceil_div(max_cap, kScanTile) + 1));
-    lb_.cap = static_cast<int>(tiles);
-    lb_.mem = static_cast<unsigned long long*>(alloc((tiles + 1) * 8));
+    for (int sl = 0; sl < 2; ++sl) {
+      lb_slot_[sl].cap = static_cast<int>(tiles);
+      lb_slot_[sl].mem = static_cast<unsigned long long*>(alloc((tiles + 1) * 8));
+    }
     lb2_.cap = static_cast<int>(tiles);
     lb2_.mem = static_cast<unsigned long long*>(alloc((tiles + 1) * 8));
   }
-  slow_ = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(total_rows + 1) * 8));
-  n_slow_ = static_cast<int*>(alloc(sizeof(int)));
+  for (int sl = 0; sl < 2; ++sl) {
+    slow_slot_[sl] = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(total_rows + 1) * 8));
+    n_slow_slot_[sl] = static_cast<int*>(alloc(sizeof(int)));
+  }
   int maxf = 1;
   for (int f : o_.fanouts) maxf = std::max(maxf, f);
-  mt_scratch_ = static_cast<std::uint64_t*>(alloc(sample_scratch_words(maxf) * 8));
+  for (int sl = 0; sl < 2; ++sl)
+    mt_scratch_slot_[sl] = static_cast<std::uint64_t*>(alloc(sample_scratch_words(maxf) * 8));
   std::size_t wt = 1, wp = 1;
   for (const auto& s : slots_) wt = std::max<std::size_t>(wt, static_cast<std::size_t>(round_up4(s.din)) * s.dout);
   for (int l = 1; l <= o_.k; ++l) {
@@ -720,6 +725,10 @@ void Engine::bind_slot(int s) {
   err_ = &rb_slot_[s]->err;
   edges_dev_ = &rb_slot_[s]->edges;
   h_rb_ = h_rb_slot_[s];
+  lb_ = lb_slot_[s];  // sampling scratch: two slots can sample concurrently
+  slow_ = slow_slot_[s];
+  n_slow_ = n_slow_slot_[s];
+  mt_scratch_ = mt_scratch_slot_[s];
 }
 
 std::uint64_t Engine::param_count() const {
@@ -829,8 +838,10 @@ void Engine::run_sampling(cudaStream_t ss) {
       frontier_relabel(ra, fa, ss);
     });
     // transposed views of this hop (independent of the forward values)
-    const CscHop ch = csc_hop(h);
-    timed("csc_build", 0, [&] { csc_prepare(ch, lb_, ss); });
+    if (!presampling_) {
+      const CscHop ch = csc_hop(h);
+      timed("csc_build", 0, [&] { csc_prepare(ch, lb_, ss); });
+    }
   }
   EdgeCountArgs ec{};
   for (const auto& b : blocks_) {
@@ -859,7 +870,7 @@ void Engine::run_sampling(cudaStream_t ss) {
     k_alg_bytes<<<1, 32, 0, ss>>>(ab, alg_bytes_);
   }
   // cache lookups + updates over the layer-0 frontier (harness.cpp:425-437)
-  if (cache_on_)
+  if (cache_on_ && !presampling_)
     for (int t = 0; t < ntypes_; ++t)
       if (cache_types_[t] && front(k, t).cap > 0)
         cache_count(front(k, t).list, front(k, t).count, front(k, t).cap, cached_bits_ + word_base_[t],
@@ -1429,40 +1440,91 @@ void Engine::quiesce() {
 }
 
 // ---------------------------------------------------------------------------------------------
+// presample_hotness (cache.cpp:39-63): `epochs` passes over the target ids in id
+// order, batch_size per batch, rng seed mix_seed(seed, epoch); +1 per seed and
+// per sampled source occurrence. All batch ids and scalars are uploaded once;
+// every batch is one replay of a captured graph (sampling without the transposed
+// views + histogram) on one stream, with no host round trip between batches.
 std::vector<std::vector<std::uint32_t>> Engine::presample_hotness(int epochs, std::uint64_t seed, int batch_size) {
   if (batch_size > o_.batch_cap) throw std::invalid_argument("presample batch larger than the batch capacity");
+  if (batch_size <= 0) throw std::invalid_argument("presample batch size must be positive");
   quiesce();
   bind_slot(0);
-  std::vector<std::uint32_t*> counts(ntypes_, nullptr);
-  for (int t = 0; t < ntypes_; ++t) counts[t] = static_cast<std::uint32_t*>(alloc(type_counts_[t] * 4));
-  const std::uint64_t n_target = type_counts_[target_];
-  std::vector<NodeId> batch;
-  for (int e = 0; e < epochs; ++e) {
-    const std::uint64_t rs = mix_seed(seed, static_cast<std::uint64_t>(e));
-    for (std::uint64_t lo = 0; lo < n_target; lo += batch_size) {
-      batch.clear();
-      for (std::uint64_t v = lo; v < std::min<std::uint64_t>(lo + batch_size, n_target); ++v)
-        batch.push_back(static_cast<NodeId>(v));
-      std::memcpy(h_batch_, batch.data(), batch.size() * 4);
-      HG_CUDA(cudaMemcpyAsync(d_batch_, h_batch_, batch.size() * 4, cudaMemcpyHostToDevice, st_));
-      h_sc_->rng_seed = rs;
-      h_sc_->batch_len = static_cast<int>(batch.size());
-      HG_CUDA(cudaMemcpyAsync(d_sc_, h_sc_, sizeof(StepScalars), cudaMemcpyHostToDevice, st_));
-      run_sampling(st_);
-      // +1 per seed, +1 per sampled source occurrence (cache.cpp:51-56)
-      hotness_add_list(front(0, target_).list, front(0, target_).count, o_.batch_cap, counts[target_], st_);
-      for (const auto& b : blocks_)
-        hotness_add(b.src, b.indptr, block_rows(b),
-                    b.edge_cap, counts[b.src_t], st_);
-      // pinned staging buffers are reused: wait before the next batch
-      HG_CUDA(cudaStreamSynchronize(st_));
-    }
+  if (hot_counts_.empty()) {
+    hot_counts_.assign(ntypes_, nullptr);
+    for (int t = 0; t < ntypes_; ++t) hot_counts_[t] = static_cast<std::uint32_t*>(alloc(type_counts_[t] * 4));
   }
+  for (int t = 0; t < ntypes_; ++t)
+    HG_CUDA(cudaMemsetAsync(hot_counts_[t], 0, type_counts_[t] * 4, st_));
+  const std::uint64_t n_target = type_counts_[target_];
+  std::vector<NodeId> ids(n_target);
+  for (std::uint64_t v = 0; v < n_target; ++v) ids[v] = static_cast<NodeId>(v);
+  std::vector<StepScalars> sc;
+  std::vector<std::uint64_t> lo_of;
+  for (int e = 0; e < epochs; ++e)
+    for (std::uint64_t lo = 0; lo < n_target; lo += batch_size) {
+      sc.push_back(StepScalars{mix_seed(seed, static_cast<std::uint64_t>(e)),
+                               static_cast<int>(std::min<std::uint64_t>(batch_size, n_target - lo)), 0, 0});
+      lo_of.push_back(lo);
+    }
+  NodeId* d_ids = nullptr;
+  StepScalars* d_sc = nullptr;
+  HG_CUDA(cudaMalloc(&d_ids, std::max<std::size_t>(4, ids.size() * 4)));
+  HG_CUDA(cudaMalloc(&d_sc, std::max<std::size_t>(1, sc.size()) * sizeof(StepScalars)));
+  HG_CUDA(cudaMemcpyAsync(d_ids, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice, st_));
+  HG_CUDA(cudaMemcpyAsync(d_sc, sc.data(), sc.size() * sizeof(StepScalars), cudaMemcpyHostToDevice, st_));
+  // batches alternate between the two sample slots, each on its own stream
+  // (histogram counters are atomics, order-independent)
+  HG_CUDA(cudaStreamSynchronize(st_));
+  cudaStream_t sts[2] = {st_, st_s_};
+  auto body = [&](cudaStream_t ss) {
+    presampling_ = true;
+    run_sampling(ss);
+    presampling_ = false;
+    // +1 per seed, +1 per sampled source occurrence (cache.cpp:51-56)
+    hotness_add_list(front(0, target_).list, front(0, target_).count, o_.batch_cap, hot_counts_[target_], ss);
+    for (const auto& b : blocks_) hotness_add(b.src, b.indptr, block_rows(b), b.edge_cap, hot_counts_[b.src_t], ss);
+  };
+  cudaGraphExec_t ex[2] = {nullptr, nullptr};
+  auto release = [&] {
+    for (auto& e : ex)
+      if (e) cudaGraphExecDestroy(e);
+    cudaFree(d_ids);
+    cudaFree(d_sc);
+  };
+  try {
+    if (use_graphs_ && !profiling_)
+      for (int sl = 0; sl < 2; ++sl) {
+        bind_slot(sl);
+        capture(ex[sl], sts[sl], [&] { body(sts[sl]); });
+      }
+    for (std::size_t i = 0; i < sc.size(); ++i) {
+      const int sl = static_cast<int>(i & 1);
+      bind_slot(sl);
+      HG_CUDA(cudaMemcpyAsync(d_batch_, d_ids + lo_of[i], static_cast<std::size_t>(sc[i].batch_len) * 4,
+                              cudaMemcpyDeviceToDevice, sts[sl]));
+      HG_CUDA(cudaMemcpyAsync(d_sc_, d_sc + i, sizeof(StepScalars), cudaMemcpyDeviceToDevice, sts[sl]));
+      if (ex[sl])
+        HG_CUDA(cudaGraphLaunch(ex[sl], sts[sl]));
+      else
+        body(sts[sl]);
+    }
+    HG_CUDA(cudaStreamSynchronize(st_));
+    HG_CUDA(cudaStreamSynchronize(st_s_));
+  } catch (...) {
+    release();
+    throw;
+  }
+  for (auto& e : ex)
+    if (e) cudaGraphExecDestroy(e);
+  cudaFree(d_ids);
+  cudaFree(d_sc);
+  bind_slot(0);
   std::vector<std::vector<std::uint32_t>> out(ntypes_);
   for (int t = 0; t < ntypes_; ++t) {
     out[t].resize(type_counts_[t]);
     if (!out[t].empty())
-      HG_CUDA(cudaMemcpy(out[t].data(), counts[t], out[t].size() * 4, cudaMemcpyDeviceToHost));
+      HG_CUDA(cudaMemcpy(out[t].data(), hot_counts_[t], out[t].size() * 4, cudaMemcpyDeviceToHost));
   }
   return out;
 }

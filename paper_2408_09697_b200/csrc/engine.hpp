@@ -251,6 +251,8 @@ class Engine {
   std::vector<cudaEvent_t> fork_ev_;
   int fork_used_ = 0;
   bool side_open_ = false;  // the side stream has work forked since the last join
+  bool presampling_ = false;  // run_sampling for presample_hotness: no transposed views, no cache lookups
+  std::vector<std::uint32_t*> hot_counts_;  // presample_hotness histograms (allocated once)
   LbScratch lb2_;  // look-back scratch of the side stream
   bool use_side_ = true;
   cudaStream_t side() const { return (profiling_ || !use_side_) ? st_ : st2_; }
@@ -280,6 +282,10 @@ class Engine {
   float* mult_slot_[2] = {};
   struct Readback;
   Readback *rb_slot_[2] = {}, *h_rb_slot_[2] = {};
+  LbScratch lb_slot_[2];
+  std::uint32_t* slow_slot_[2] = {};
+  int* n_slow_slot_[2] = {};
+  std::uint64_t* mt_scratch_slot_[2] = {};
   // slots sampled and not trained yet (FIFO), with the host batch they hold
   struct Pending {
     int slot;
