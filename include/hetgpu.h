@@ -86,6 +86,11 @@ hg_graph* hg_graph_from_pairs(int n_types, const uint64_t* counts, int n_rels, c
                               const int* rel_dst, const uint64_t* pair_counts, const uint32_t* pair_src,
                               const uint32_t* pair_dst, int target, int num_classes);
 
+/* HGC1 container (save_container / load_container, src/container.cpp:47-154): the
+ * writer produces the reference's exact bytes; failures are runtime_error. */
+hg_graph* hg_graph_load(const char* path);
+int hg_graph_save(const hg_graph* g, const char* path);
+
 void hg_graph_free(hg_graph* g);
 /* node_counts, labels, rel_src/rel_dst/rel_reverse, rel{r}.indptr, rel{r}.src, feat.t{t}, kinds, dims */
 hg_bundle* hg_graph_export(const hg_graph* g);

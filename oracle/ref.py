@@ -50,6 +50,8 @@ def lib():
             "ref_graph_random": [u64, i32, i32, i32],
             "ref_graph_bundled": [C.c_char_p, u64],
             "ref_graph_spec": [C.c_char_p, u64],
+            "ref_graph_load": [C.c_char_p],
+            "ref_graph_save": [vp, C.c_char_p],
             "ref_graph_build": [i32, vp, i32, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, vp],
             "ref_graph_export": [vp],
             "ref_meta_partition": [vp, i32, i32],
@@ -143,6 +145,13 @@ class RefGraph:
         return cls(lib().ref_graph_build(len(counts), _ptr(counts), len(rels), _ptr(rs), _ptr(rd),
                                          _ptr(ec), _ptr(es), _ptr(ed), target, num_classes,
                                          _ptr(lab), _ptr(kd), _ptr(dm), _ptr(dv)))
+
+    @classmethod
+    def load(cls, path: str) -> "RefGraph":
+        return cls(lib().ref_graph_load(str(path).encode()))
+
+    def save(self, path: str) -> None:
+        _take(lib().ref_graph_save(self.h, str(path).encode()))
 
     def export(self) -> Dict[str, np.ndarray]:
         return _take(lib().ref_graph_export(self.h))

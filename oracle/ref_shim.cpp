@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "hetsim/cache.hpp"
+#include "hetsim/container.hpp"
 #include "hetsim/harness.hpp"
 #include "hetsim/hgnn.hpp"
 #include "hetsim/metapartition.hpp"
@@ -181,6 +182,24 @@ void* ref_graph_bundled(const char* name, unsigned long long seed) {
     auto* s = new Session;
     s->g = gen_synthetic(bundled_spec(name), seed);
     return s;
+  });
+}
+
+// load_container / save_container (container.cpp:47-154)
+void* ref_graph_load(const char* path) {
+  return guarded([&]() -> void* {
+    auto* s = new Session;
+    s->g = load_container(path);
+    return s;
+  });
+}
+
+void* ref_graph_save(void* sp, const char* path) {
+  return guarded([&]() -> void* {
+    save_container(static_cast<Session*>(sp)->g, path);
+    auto* b = new Bundle;
+    b->put_u64("ok", std::vector<std::uint64_t>{1});
+    return b;
   });
 }
 

@@ -73,6 +73,8 @@ def lib():
             "hg_graph_from_csr": ([i32, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp], vp),
             "hg_graph_from_pairs": ([i32, vp, i32, vp, vp, vp, vp, vp, i32, i32], vp),
             "hg_graph_free": ([vp], None),
+            "hg_graph_load": ([C.c_char_p], vp),
+            "hg_graph_save": ([vp, C.c_char_p], i32),
             "hg_graph_export": ([vp], vp),
             "hg_graph_schema": ([vp], vp),
             "hg_sampler_create": ([vp, vp, i32, vp, vp, i32, i32], vp),

@@ -177,6 +177,21 @@ hg_graph* hg_graph_from_pairs(int n_types, const uint64_t* counts, int n_rels, c
   });
 }
 
+hg_graph* hg_graph_load(const char* path) {
+  return guard<hg_graph*>(nullptr, [&] {
+    auto* h = new hg_graph;
+    h->g = load_container(path ? path : "");
+    return h;
+  });
+}
+
+int hg_graph_save(const hg_graph* g, const char* path) {
+  return guard<int>(-1, [&] {
+    save_container(g->g, path ? path : "");
+    return 0;
+  });
+}
+
 void hg_graph_free(hg_graph* g) { delete g; }
 
 hg_bundle* hg_graph_schema(const hg_graph* h) {

@@ -102,6 +102,11 @@ struct Spec {
 
 Graph generate(const Spec& spec, std::uint64_t seed);
 
+// ---- HGC1 container (container.hpp:8-19; container.cpp:47-154) -----------------
+std::string container_header(const Graph& g);  // the reference's exact JSON header
+void save_container(const Graph& g, const std::string& path);
+Graph load_container(const std::string& path);
+
 // Builds the dst-major adjacency of every relation from (src, dst) pairs in
 // insertion order (hetgraph.cpp:126-156). Features start Absent.
 Graph assemble(std::vector<std::string> type_names, std::vector<std::uint64_t> counts,

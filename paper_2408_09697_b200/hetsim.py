@@ -154,6 +154,16 @@ def gen_synthetic(spec: dict, seed: int) -> HetGraph:
     return HetGraph(N.lib().hg_graph_generate(C.byref(s), seed))
 
 
+def load_container(path: str) -> HetGraph:
+    """load_container (src/container.cpp:92-154): an HGC1 file."""
+    return HetGraph(N.lib().hg_graph_load(str(path).encode()))
+
+
+def save_container(g: HetGraph, path: str) -> None:
+    """save_container (src/container.cpp:47-90): byte-identical to the reference's writer."""
+    N.check(N.lib().hg_graph_save(g.handle, str(path).encode()))
+
+
 def graph_from_export(e: Dict[str, np.ndarray]) -> HetGraph:
     """A HetGraph from exported arrays (the oracle's or ours): CSR per relation."""
     counts = np.asarray(e["node_counts"], np.uint64)
