@@ -181,6 +181,13 @@ inline HetGraph build_hetgraph(const std::vector<std::uint64_t>& node_counts,
                                       pd.data(), target, num_classes));
 }
 
+// load_container / save_container (container.cpp:47-154): HGC1 files, byte-identical
+// to the reference writer; failures throw std::runtime_error
+inline HetGraph load_container(const std::string& path) { return HetGraph(hg_graph_load(path.c_str())); }
+inline void save_container(const HetGraph& g, const std::string& path) {
+  detail::check(hg_graph_save(g.handle(), path.c_str()));
+}
+
 // make_batches (harness.cpp:327-340)
 inline std::vector<std::vector<NodeId>> make_batches(const HetGraph& g, int batch_size, int max_batches,
                                                      std::uint64_t seed) {
