@@ -809,9 +809,22 @@ void Engine::run_sampling(cudaStream_t ss) {
     timed("sample", 0, [&] { sample_hop(sh, d_sc_, slow_, n_slow_, mt_scratch_, lb_, ss); });
 
     // frontier[h][t]: bitmap of every sampled source, compacted in id order
+    // The last hop's frontier of a type is needed only for its gradient rows
+    // (learnable leaves: the transposed view and the sparse Adam ids): layer 1
+    // reads its sources by global id. Lean mode (no retained gradients, no cache
+    // lookups) skips the other types' mark/compact/relabel; presampling needs
+    // none of them.
+    const bool lean = h == k && (presampling_ || (!retain_grads_ && !cache_on_));
+    auto wanted = [&](int t) {
+      if (!lean || presampling_) return !presampling_ || h < k;
+      for (const auto& c : cscs_)
+        if (c.hop == k && c.src_t == t) return true;
+      return false;
+    };
     FrontierArgs fa{};
     std::vector<int> slot_of_type(ntypes_, -1);
     for (int t : hop_slot_types_[h]) {
+      if (!wanted(t)) continue;
       slot_of_type[t] = fa.ntypes;
       fa.t[fa.ntypes++] = {bits_ + word_base_[t], word_base_[t + 1] - word_base_[t], wscan_ + word_base_[t],
                            front(h, t).list, front(h, t).count, front(h, t).cap};
@@ -820,6 +833,7 @@ void Engine::run_sampling(cudaStream_t ss) {
     RelabelArgs ra{};
     for (int q = 0; q < sh.nblk; ++q) {
       const BlockBuf& b = blocks_[hop_blocks_[h][q]];
+      if (slot_of_type[b.src_t] < 0) continue;
       ma.s[ma.nsrc++] = {b.src, b.indptr, sh.b[q].n_rows, b.edge_cap, slot_of_type[b.src_t]};
       std::uint32_t* cnt = nullptr;
       if (b.need_src_grad)
@@ -1537,6 +1551,7 @@ void Engine::set_cache(const std::vector<std::vector<NodeId>>& cached) {
   HG_CUDA(cudaMemset(cache_hm_, 0, sizeof(unsigned long long) * 2 * ntypes_));
   cache_on_ = true;
   for (int t = 0; t < ntypes_; ++t) cache_types_[t] = t < static_cast<int>(cached.size());
+  drop_graphs();  // the captured steps did not look the frontier up
 }
 
 std::vector<std::pair<unsigned long long, unsigned long long>> Engine::cache_counters() {
