@@ -1,5 +1,6 @@
 // extern "C" boundary (include/hetgpu.h): converts C arguments into the host
 // layer / engine calls and C++ exceptions into return codes + last error.
+#include <cstdlib>
 #include <algorithm>
 #include <cstring>
 #include <map>
@@ -451,13 +452,33 @@ int hg_engine_bench(hg_engine* e, const uint32_t* batches, const int* lens, cons
     for (int i = 0; i < n_steps; ++i) off[i + 1] = off[i] + lens[i];
     std::uint64_t edges = 0;
     double loss = 0.0;
-    // batch i+1 is sampled (sampling stream) while batch i trains
-    if (n_steps > 0) en.prefetch_device(d_all + off[0], lens[0], d_sc + 0);
-    for (int i = 0; i < n_steps; ++i) {
-      if (i + 1 < n_steps) en.prefetch_device(d_all + off[i + 1], lens[i + 1], d_sc + i + 1);
-      en.train_device(d_sc + i, train != 0);
+    // HG_BENCH_PHASE (diagnostics only): "sample" times the sampling graphs alone,
+    // "serial" runs sampling and training back to back without overlap
+    const char* phase_env = std::getenv("HG_BENCH_PHASE");
+    const std::string phase = phase_env ? phase_env : "";
+    if (phase == "sample") {
+      for (int i = 0; i < n_steps; ++i) {
+        en.prefetch_device(d_all + off[i], lens[i], d_sc + i);
+        en.drop_pending();
+      }
+      HG_CUDA(cudaEventRecord(b, en.sample_stream()));
+    } else if (phase == "serial") {
+      for (int i = 0; i < n_steps; ++i) {
+        en.prefetch_device(d_all + off[i], lens[i], d_sc + i);
+        en.train_device(d_sc + i, train != 0);
+        HG_CUDA(cudaEventRecord(b, en.stream()));
+        HG_CUDA(cudaStreamWaitEvent(en.sample_stream(), b, 0));
+      }
+      HG_CUDA(cudaEventRecord(b, en.stream()));
+    } else {
+      // batch i+1 is sampled (sampling stream) while batch i trains
+      if (n_steps > 0) en.prefetch_device(d_all + off[0], lens[0], d_sc + 0);
+      for (int i = 0; i < n_steps; ++i) {
+        if (i + 1 < n_steps) en.prefetch_device(d_all + off[i + 1], lens[i + 1], d_sc + i + 1);
+        en.train_device(d_sc + i, train != 0);
+      }
+      HG_CUDA(cudaEventRecord(b, en.stream()));
     }
-    HG_CUDA(cudaEventRecord(b, en.stream()));
     HG_CUDA(cudaEventSynchronize(b));
     float ms = 0.f;
     HG_CUDA(cudaEventElapsedTime(&ms, a, b));

@@ -657,7 +657,7 @@ void Engine::upload(const Graph& g) {
   for (const auto& c : cscs_) max_cap = std::max(max_cap, c.src_cap + 1);
   {
     // look-back scratch: enough tiles for the largest single-pass launch
-    std::size_t tiles = ceil_div(total_words_, 1024) + kMaxSegs;
+    std::size_t tiles = ceil_div(total_words_, kCompactWordsPerTile) + kMaxSegs;
     for (int h = 1; h <= o_.k; ++h) {
       std::size_t t = 0;
       for (int bi : hop_blocks_[h]) t += ceil_div(std::max(1, blocks_[bi].rows_cap), 256) + 1;
@@ -803,10 +803,10 @@ void Engine::run_sampling(cudaStream_t ss) {
       s.indptr = b.indptr;
       s.src_ids = b.src;
       s.erow = b.erow;
+      s.mark_bits = nullptr;
       s.rel = b.rel;
       s.rows_cap = b.rows_cap;
     }
-    timed("sample", 0, [&] { sample_hop(sh, d_sc_, slow_, n_slow_, mt_scratch_, lb_, ss); });
 
     // frontier[h][t]: bitmap of every sampled source, compacted in id order
     // The last hop's frontier of a type is needed only for its gradient rows
@@ -829,25 +829,25 @@ void Engine::run_sampling(cudaStream_t ss) {
       fa.t[fa.ntypes++] = {bits_ + word_base_[t], word_base_[t + 1] - word_base_[t], wscan_ + word_base_[t],
                            front(h, t).list, front(h, t).count, front(h, t).cap};
     }
-    MarkArgs ma{};
     RelabelArgs ra{};
     for (int q = 0; q < sh.nblk; ++q) {
       const BlockBuf& b = blocks_[hop_blocks_[h][q]];
       if (slot_of_type[b.src_t] < 0) continue;
-      ma.s[ma.nsrc++] = {b.src, b.indptr, sh.b[q].n_rows, b.edge_cap, slot_of_type[b.src_t]};
+      sh.b[q].mark_bits = bits_ + word_base_[b.src_t];  // the sampler marks frontier[h] as it emits
       std::uint32_t* cnt = nullptr;
       if (b.need_src_grad)
         for (const auto& c : cscs_)
           if (c.hop == h && c.src_t == b.src_t) cnt = c.offs;
       ra.b[ra.nblk++] = {b.src, b.indptr, sh.b[q].n_rows, b.col, b.edge_cap, slot_of_type[b.src_t], cnt};
     }
+    // frontier[h-1]'s bitmap is dead once its relabel / transposed views are enqueued
     HG_CUDA(cudaMemsetAsync(bits_, 0, static_cast<std::size_t>(total_words_) * 4, ss));
+    timed("sample", 0, [&] { sample_hop(sh, d_sc_, slow_, n_slow_, mt_scratch_, lb_, ss); });
     if (csc_region_[h].words) {
       HG_CUDA(cudaMemsetAsync(csc_region_[h].offs, 0, csc_region_[h].words * 4, ss));
       HG_CUDA(cudaMemsetAsync(csc_region_[h].cursor, 0, csc_region_[h].words * 4, ss));
     }
     timed("frontier", 0, [&] {
-      frontier_mark(ma, fa, ss);
       frontier_compact(fa, lb_, ss);
       frontier_relabel(ra, fa, ss);
     });

@@ -100,6 +100,7 @@ class Engine {
   StepScalars next_scalars(std::uint64_t rng_seed, int n, int designated, bool train);
   cudaStream_t sample_stream() const { return st_s_; }
   void quiesce();  // finish everything in flight, drop prefetched batches
+  void drop_pending() { pending_slots_.clear(); }  // bench phase timing: sampled slots never trained
   void set_graphs(bool on) { use_graphs_ = on; }
   void set_side_stream(bool on) {
     if (on != use_side_) {

@@ -353,6 +353,12 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_fused(SampleHop h, Lb
       if (q < wtotal) b.erow[o0 + q] = row_base + static_cast<std::uint32_t>(rr[u]);
       if (ok[u]) b.src_ids[at[u]] = val[u];
     }
+    // frontier mark fused here (the ids are in registers): one atomicOr per edge
+    if (b.mark_bits) {
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u)
+        if (ok[u]) atomicOr(b.mark_bits + (val[u] >> 5), 1u << (val[u] & 31));
+    }
   }
 }
 
@@ -373,7 +379,10 @@ __global__ void __launch_bounds__(128) k_sample_slow(SampleHop h, const StepScal
     const std::uint64_t rel_key = (static_cast<std::uint64_t>(h.hop) << 32) | static_cast<std::uint64_t>(b.rel);
     MtFull eng{x, 0};
     eng.seed(dmix_seed(sc->rng_seed, dmix_seed(rel_key, d)));
-    draw_row(eng, deg, h.fanout, b.csr_src + lo, b.src_ids + b.indptr[i], mpos, mval);
+    std::uint32_t* out = b.src_ids + b.indptr[i];
+    draw_row(eng, deg, h.fanout, b.csr_src + lo, out, mpos, mval);
+    if (b.mark_bits)
+      for (int e = 0; e < h.fanout; ++e) atomicOr(b.mark_bits + (out[e] >> 5), 1u << (out[e] & 31));
   }
 }
 
@@ -417,16 +426,6 @@ namespace {
 
 constexpr int kFrontThreads = 256;
 
-__global__ void __launch_bounds__(kFrontThreads) k_mark(MarkArgs m, FrontierArgs f) {
-  const MarkSource& s = m.s[blockIdx.y];
-  const std::uint32_t total = s.indptr[*s.n_rows];
-  std::uint32_t* bits = f.t[s.slot].bits;
-  for (std::uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-    const std::uint32_t id = s.ids[e];
-    atomicOr(bits + (id >> 5), 1u << (id & 31));
-  }
-}
-
 __global__ void __launch_bounds__(kFrontThreads) k_mark_batch(const std::uint32_t* ids,
                                                               const StepScalars* sc,
                                                               std::uint32_t* bits) {
@@ -437,8 +436,9 @@ __global__ void __launch_bounds__(kFrontThreads) k_mark_batch(const std::uint32_
   }
 }
 
-constexpr int kWordsPerThread = 4;
+constexpr int kWordsPerThread = 1;  // short per-thread emission loops; more tiles in flight
 constexpr int kWordsPerTile = kFrontThreads * kWordsPerThread;
+static_assert(kWordsPerTile == kCompactWordsPerTile, "look-back scratch sizing");
 
 // popcount of 1024 words per tile -> CTA scan -> look-back -> inclusive word
 // prefix (the rank structure) and the sorted ids of the set bits
@@ -512,14 +512,6 @@ __global__ void __launch_bounds__(kFrontThreads) k_batch_mult(const std::uint32_
 }
 
 }  // namespace
-
-void frontier_mark(const MarkArgs& m, const FrontierArgs& f, cudaStream_t st) {
-  if (m.nsrc == 0) return;
-  int cap = 1;
-  for (int i = 0; i < m.nsrc; ++i) cap = max(cap, m.s[i].cap);
-  dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, kFrontThreads), 4 * kNumSMs)), m.nsrc);
-  k_mark<<<grid, kFrontThreads, 0, st>>>(m, f);
-}
 
 void frontier_mark_batch(const std::uint32_t* ids, const StepScalars* sc, int cap, const BitmapType& t,
                          cudaStream_t st) {

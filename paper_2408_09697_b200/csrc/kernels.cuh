@@ -51,6 +51,8 @@ struct LbScratch {
     HG_CUDA(cudaMemsetAsync(mem, 0, (static_cast<std::size_t>(tiles) + 1) * 8, st));
   }
 };
+// bitmap words per frontier-compaction tile (one word per thread)
+constexpr int kCompactWordsPerTile = 256;
 // single-pass (decoupled look-back) segmented inclusive scan
 void scan_inclusive(const ScanArgs& a, LbScratch& lb, cudaStream_t st);
 
@@ -63,6 +65,7 @@ struct SampleBlock {
   std::uint32_t* indptr;          // [rows_cap + 1] block offsets (u32)
   std::uint32_t* src_ids;         // [edge_cap] sampled sources in draw order
   std::uint32_t* erow;            // [edge_cap] block row of every sampled edge
+  std::uint32_t* mark_bits;       // frontier[h][src type] bitmap (marked as sampled), or null
   int rel;
   int rows_cap;
 };
@@ -94,18 +97,6 @@ struct FrontierArgs {
   BitmapType t[kMaxSegs];
   int ntypes;
 };
-struct MarkSource {
-  const std::uint32_t* ids;
-  const std::uint32_t* indptr;  // live total = indptr[*n_rows]
-  const int* n_rows;
-  int cap;
-  int slot;  // index into FrontierArgs::t
-};
-struct MarkArgs {
-  MarkSource s[kMaxBlocks];
-  int nsrc;
-};
-void frontier_mark(const MarkArgs& m, const FrontierArgs& f, cudaStream_t st);
 void frontier_mark_batch(const std::uint32_t* ids, const StepScalars* sc, int cap, const BitmapType& t,
                          cudaStream_t st);
 // popcount + single-pass scan + emit of every type's bitmap (sorted unique ids)
