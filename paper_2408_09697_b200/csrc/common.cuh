@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 namespace hetgpu {
 
@@ -19,6 +20,33 @@ namespace hetgpu {
 
 constexpr int kWarp = 32;
 constexpr int kNumSMs = 148;
+
+// ---- programmatic dependent launch (PDL) --------------------------------------
+// The step is a chain of short dependent kernels. Launched through launch_pdl, a
+// kernel's CTAs become resident while its predecessor drains (once every
+// predecessor CTA has passed pdl_trigger) and park in pdl_wait, which returns
+// when the predecessor grid has completed and its writes are visible. Every
+// kernel calls pdl_wait before touching anything an earlier kernel produced;
+// outside a PDL launch both instructions are no-ops.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_enter() { pdl_wait(); }
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  HG_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 
 __host__ __device__ inline std::uint64_t ceil_div(std::uint64_t a, std::uint64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int round_up4(int x) { return (x + 3) & ~3; }

@@ -20,6 +20,7 @@ constexpr int kThreads = 256;
 namespace {
 
 __global__ void __launch_bounds__(kThreads) k_cross_entropy(LossArgs a) {
+  pdl_enter();
   const int n = *a.n_rows;
   const int lane = threadIdx.x & 31;
   const int warps = gridDim.x * (kThreads / 32);
@@ -61,6 +62,7 @@ __global__ void __launch_bounds__(kThreads) k_cross_entropy(LossArgs a) {
 
 // ordered single-CTA reduction: fixed per-thread striding and a fixed tree
 __global__ void __launch_bounds__(1024) k_sum_rows(const double* v, const int* n, double* out) {
+  pdl_enter();
   __shared__ double part[1024];
   double s = 0.0;
   for (int i = threadIdx.x; i < *n; i += 1024) s += v[i];
@@ -78,8 +80,8 @@ __global__ void __launch_bounds__(1024) k_sum_rows(const double* v, const int* n
 void cross_entropy(const LossArgs& a, cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(
       1, std::min<std::uint64_t>(ceil_div(a.rows_cap, kThreads / 32), 4 * kNumSMs)));
-  k_cross_entropy<<<grid, kThreads, 0, st>>>(a);
-  k_sum_rows<<<1, 1024, 0, st>>>(a.row_loss, a.n_rows, a.loss_out);
+  launch_pdl(k_cross_entropy, grid, kThreads, 0, st, a);
+  launch_pdl(k_sum_rows, 1, 1024, 0, st, a.row_loss, a.n_rows, a.loss_out);
 }
 
 // ---- transposed gather for the backward scatter ------------------------------------------------
@@ -128,6 +130,7 @@ __device__ __forceinline__ void adam4(float4& w, float4& m, float4& v, const flo
 // (block index in the top 4 bits): the backward gather reads dmean rows directly
 constexpr int kRowBits = 28;
 __global__ void k_csc_fill(CscHop h) {
+  pdl_enter();
   const int bi = blockIdx.y;
   const CscEdges& b = h.b[bi];
   const CscType& t = h.t[b.type];
@@ -141,6 +144,7 @@ __global__ void k_csc_fill(CscHop h) {
 
 // make every segment ascending in (block, row): deterministic summation order
 __global__ void k_csc_sort(CscHop h) {
+  pdl_enter();
   const CscType& t = h.t[blockIdx.y];
   const int n = *t.n_src;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
@@ -160,6 +164,7 @@ __global__ void k_csc_sort(CscHop h) {
 // one half-warp per (source row, 64-column chunk): ordered sum of the dmean rows
 // of its sampled edges; learnable leaves apply Adam to their table row directly
 __global__ void __launch_bounds__(256) k_csc_gather(CscHop h, AdamHyper hp, std::uint32_t* err) {
+  pdl_enter();
   __shared__ AdamStep ks[kMaxSegs];
   if (threadIdx.x < h.nt) {
     const CscType& t = h.t[threadIdx.x];
@@ -238,9 +243,9 @@ void csc_prepare(const CscHop& h, LbScratch& lb, cudaStream_t st) {
   for (int i = 0; i < h.nb; ++i) cap = std::max(cap, h.b[i].cap);
   for (int i = 0; i < h.nt; ++i) scap = std::max(scap, h.t[i].src_cap);
   dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, 256), 4 * kNumSMs)), h.nb);
-  k_csc_fill<<<grid, 256, 0, st>>>(h);
+  launch_pdl(k_csc_fill, grid, 256, 0, st, h);
   dim3 g2(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(scap, 256), 4 * kNumSMs)), h.nt);
-  k_csc_sort<<<g2, 256, 0, st>>>(h);
+  launch_pdl(k_csc_sort, g2, 256, 0, st, h);
 }
 
 void csc_gather(const CscHop& h, AdamHyper hp, std::uint32_t* err, cudaStream_t st) {
@@ -248,7 +253,7 @@ void csc_gather(const CscHop& h, AdamHyper hp, std::uint32_t* err, cudaStream_t 
   int items = 0;
   for (int i = 0; i < h.nt; ++i) items += h.t[i].src_cap * static_cast<int>(ceil_div(h.t[i].din, 64));
   const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(items, 16), 16 * kNumSMs)));
-  k_csc_gather<<<grid, 256, 0, st>>>(h, hp, err);
+  launch_pdl(k_csc_gather, grid, 256, 0, st, h, hp, err);
 }
 
 // ---- Adam ---------------------------------------------------------------------------------------
@@ -259,6 +264,7 @@ namespace {
 // in w, m, v and g, so updating it is a no-op)
 __global__ void __launch_bounds__(256) k_adam_model(AdamModelBatch b, const std::int64_t* step, AdamHyper hp,
                                                     std::uint32_t* err) {
+  pdl_enter();
   __shared__ AdamStep ks;
   if (threadIdx.x == 0) ks = adam_step_of(hp, static_cast<double>(*step));
   __syncthreads();
@@ -280,12 +286,14 @@ __global__ void __launch_bounds__(256) k_adam_model(AdamModelBatch b, const std:
 
 // per table: step += 1 iff it has gradient rows this batch (hgnn.cpp:392-394)
 __global__ void k_bump_steps(AdamRowsBatch b) {
+  pdl_enter();
   const int t = threadIdx.x;
   if (t < b.n && *b.t[t].n_rows > 0) ++*b.t[t].step;
 }
 
 // sparse learnable rows of every table in one launch: one float4 per thread
 __global__ void __launch_bounds__(256) k_adam_rows(AdamRowsBatch b, AdamHyper hp, std::uint32_t* err) {
+  pdl_enter();
   __shared__ AdamStep ks[kMaxSegs];
   if (threadIdx.x < b.n) ks[threadIdx.x] = adam_step_of(hp, static_cast<double>(*b.t[threadIdx.x].step));
   __syncthreads();
@@ -310,6 +318,7 @@ __global__ void __launch_bounds__(256) k_adam_rows(AdamRowsBatch b, AdamHyper hp
 }
 
 __global__ void k_zero_rows(float* p, int ld, const int* n_rows) {
+  pdl_enter();
   const std::size_t total = static_cast<std::size_t>(*n_rows) * ld;
   for (std::size_t x = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; x < total;
        x += static_cast<std::size_t>(gridDim.x) * blockDim.x)
@@ -325,6 +334,7 @@ struct BumpArgs {
   int count;
 };
 __global__ void k_bump_list(BumpArgs a) {
+  pdl_enter();
   const int t = threadIdx.x;
   if (t < a.count && *a.n[t] > 0) ++*a.step[t];
 }
@@ -338,28 +348,28 @@ void bump_steps(const std::int64_t* const* steps, const int* const* counts, int 
     a.n[i] = counts[i];
   }
   a.count = n;
-  k_bump_list<<<1, 32, 0, st>>>(a);
+  launch_pdl(k_bump_list, 1, 32, 0, st, a);
 }
 
 void adam_model(AdamModelBatch& b, const std::int64_t* step, AdamHyper hp, std::uint32_t* err, cudaStream_t st) {
   if (b.n == 0) return;
   const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
                                                                             ceil_div(b.total4, 256), 4 * kNumSMs)));
-  k_adam_model<<<grid, 256, 0, st>>>(b, step, hp, err);
+  launch_pdl(k_adam_model, grid, 256, 0, st, b, step, hp, err);
 }
 
 void adam_rows(AdamRowsBatch& b, AdamHyper hp, std::uint32_t* err, cudaStream_t st) {
   if (b.n == 0) return;
-  k_bump_steps<<<1, 32, 0, st>>>(b);
+  launch_pdl(k_bump_steps, 1, 32, 0, st, b);
   const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
                                                                             ceil_div(b.total4, 256), 8 * kNumSMs)));
-  k_adam_rows<<<grid, 256, 0, st>>>(b, hp, err);
+  launch_pdl(k_adam_rows, grid, 256, 0, st, b, hp, err);
 }
 
 void zero_rows(float* p, int ld, const int* n_rows, int rows_cap, cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(
       1, std::min<std::uint64_t>(ceil_div(static_cast<std::uint64_t>(rows_cap) * ld, 256), 4 * kNumSMs)));
-  k_zero_rows<<<grid, 256, 0, st>>>(p, ld, n_rows);
+  launch_pdl(k_zero_rows, grid, 256, 0, st, p, ld, n_rows);
 }
 
 }  // namespace hetgpu

@@ -13,6 +13,7 @@ namespace {
 
 __global__ void k_shard_rows(const std::uint32_t* full, const int* n_full, int index, int count,
                              std::uint32_t* shard, int* n_shard) {
+  pdl_enter();
   const int n = *n_full;
   const int m = n > index ? (n - index + count - 1) / count : 0;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x)
@@ -27,6 +28,7 @@ struct EdgeCountArgs {
 };
 
 __global__ void k_count_edges(EdgeCountArgs a, std::uint64_t* out) {
+  pdl_enter();
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     std::uint64_t s = 0;
     for (int i = 0; i < a.n; ++i) s += a.indptr[i][*a.n_rows[i]];
@@ -38,6 +40,7 @@ __global__ void k_count_edges(EdgeCountArgs a, std::uint64_t* out) {
 // (the bucket's `active` set, raf.cpp:418-419); stored as a float counter in
 // the partition's slot of the AGG_all buffer
 __global__ void k_active_rows(EdgeCountArgs a, const int* n_rows, float* slot) {
+  pdl_enter();
   __shared__ int total;
   if (threadIdx.x == 0) total = 0;
   __syncthreads();
@@ -55,6 +58,7 @@ __global__ void k_active_rows(EdgeCountArgs a, const int* n_rows, float* slot) {
 
 __global__ void k_gather_rows(const float* table, int ld, const std::uint32_t* ids, const int* n, int cols,
                               float* out) {
+  pdl_enter();
   const int total = *n * cols;
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
     const int i = x / cols, c = x % cols;
@@ -81,6 +85,7 @@ struct AlgBytesArgs {
 };
 
 __global__ void k_alg_bytes(AlgBytesArgs a, double* acc) {
+  pdl_enter();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double s = 0, agg[3] = {0, 0, 0}, csc = 0;
   for (int i = 0; i < a.nblk; ++i) {
@@ -786,7 +791,7 @@ void Engine::run_sampling(cudaStream_t ss) {
     batch_multiplicity(d_batch_, d_sc_, o_.batch_cap, f0.t[0], mult_, ss);
   });
   if (replica_)
-    k_shard_rows<<<4, 256, 0, ss>>>(front(0, target_).list, front(0, target_).count, shard_index_, shard_count_,
+    launch_pdl(k_shard_rows, 4, 256, 0, ss, front(0, target_).list, front(0, target_).count, shard_index_, shard_count_,
                                      shard_list_, shard_count_dev_);
 
   for (int h = 1; h <= k; ++h) {
@@ -863,7 +868,7 @@ void Engine::run_sampling(cudaStream_t ss) {
     ec.n_rows[ec.n] = block_rows(b);
     ++ec.n;
   }
-  k_count_edges<<<1, 32, 0, ss>>>(ec, edges_dev_);
+  launch_pdl(k_count_edges, 1, 32, 0, ss, ec, edges_dev_);
   if (profiling_) {
     AlgBytesArgs ab{};
     for (const auto& b : blocks_) {
@@ -881,7 +886,7 @@ void Engine::run_sampling(cudaStream_t ss) {
       ab.c_row_bytes_mult[ab.ncsc] = leaf_learnable ? (retain_grads_ ? 7 : 6) : 1;
       ++ab.ncsc;
     }
-    k_alg_bytes<<<1, 32, 0, ss>>>(ab, alg_bytes_);
+    launch_pdl(k_alg_bytes, 1, 32, 0, ss, ab, alg_bytes_);
   }
   // cache lookups + updates over the layer-0 frontier (harness.cpp:425-437)
   if (cache_on_ && !presampling_)
@@ -960,7 +965,7 @@ void Engine::run_forward() {
       ec.indptr[ec.n] = blocks_[bi].indptr;
       ++ec.n;
     }
-    k_active_rows<<<1, 256, 0, st_>>>(ec, replica_ ? shard_count_dev_ : front(0, target_).count,
+    launch_pdl(k_active_rows, 1, 256, 0, st_, ec, replica_ ? shard_count_dev_ : front(0, target_).count,
                                       logits_ + static_cast<std::size_t>(o_.batch_cap) * ldc_ + o_.rank);
 #ifdef HG_WITH_NCCL
     if (comm_ && !counting_) {
@@ -1677,7 +1682,7 @@ bool Engine::read_tensor(const std::string& name, std::string& dtype, std::vecto
       const int n = dev_int(f.count);
       float* tmp = nullptr;
       HG_CUDA(cudaMalloc(&tmp, std::max<std::size_t>(16, static_cast<std::size_t>(n) * tables_[t].dim * 4)));
-      if (n) k_gather_rows<<<64, 256, 0, st_>>>(tables_[t].w, tables_[t].ld, f.list, f.count, tables_[t].dim, tmp);
+      if (n) launch_pdl(k_gather_rows, 64, 256, 0, st_, tables_[t].w, tables_[t].ld, f.list, f.count, tables_[t].dim, tmp);
       HG_CUDA(cudaStreamSynchronize(st_));
       mat(tmp, n, tables_[t].dim, tables_[t].dim);
       cudaFree(tmp);

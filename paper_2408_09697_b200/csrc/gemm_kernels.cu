@@ -53,6 +53,7 @@ __device__ __forceinline__ int find_problem(const int* tile_base, int np, int ti
 // row otherwise), averages them into As (transposed) and the tape, stages the
 // matching W slab and accumulates. Relations sum in ascending order (agg_all).
 __global__ void __launch_bounds__(kT) k_agg_tiles(AggGroup g) {
+  pdl_enter();
   __shared__ __align__(16) float As[kKS * 2 * kLd];  // 64 k rows (two slabs)
   __shared__ __align__(16) float Bs[kKS * 2 * kLd];
   const int n = *g.n_rows;
@@ -165,6 +166,7 @@ __device__ __forceinline__ float4 load_dpre4(const DpreView& d, int row, int col
 // ---- backward: weight gradient partials --------------------------------------------------
 // problem p: partial[chunk][i][j] = sum_{r in chunk} mean[r][i] * dpre[r][j]
 __global__ void __launch_bounds__(kT) k_wgrad_tiles(WGradBatch b) {
+  pdl_enter();
   __shared__ __align__(16) float As[kKS * kLd];
   __shared__ __align__(16) float Bs[kKS * kLd];
   const int p = find_problem(b.tile_base, b.np, blockIdx.x);
@@ -213,6 +215,7 @@ __global__ void __launch_bounds__(kT) k_wgrad_tiles(WGradBatch b) {
 // ordered sum of the chunk partials into dW (deterministic): one thread per
 // output element of every problem, chunks summed in order, 8 loads in flight
 __global__ void __launch_bounds__(256) k_wgrad_reduce(WGradBatch b, int total_out) {
+  pdl_enter();
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < total_out; x += gridDim.x * blockDim.x) {
     int p = 0, base = 0;
     while (p + 1 < b.np && x >= base + b.p[p].din * b.p[p].d.cols) {
@@ -241,6 +244,7 @@ __global__ void __launch_bounds__(256) k_wgrad_reduce(WGradBatch b, int total_ou
 // ---- backward: mean gradient ---------------------------------------------------------------------
 // dmean[r][c] = (sum_j dpre[r][j] * W[c][j]) / deg(r)
 __global__ void __launch_bounds__(kT) k_dmean_tiles(DMeanBatch b) {
+  pdl_enter();
   __shared__ __align__(16) float As[kKS * kLd];
   __shared__ __align__(16) float Bs[kKS * kLd];
   const int p = find_problem(b.tile_base, b.np, blockIdx.x);
@@ -294,6 +298,7 @@ __global__ void __launch_bounds__(kT) k_dmean_tiles(DMeanBatch b) {
 // ---- gather-mean: 16 lanes x float4 per (row, 64-column chunk); a warp carries
 // two such items, 8 edges in flight per lane ---------------------------------------------------
 __global__ void __launch_bounds__(256) k_gather_mean(MeanBatch m) {
+  pdl_enter();
   const int hl = threadIdx.x & 15;
   const int halves = gridDim.x * (blockDim.x >> 4);
   for (int item = blockIdx.x * (blockDim.x >> 4) + (threadIdx.x >> 4); item < m.item_base[m.nb]; item += halves) {
@@ -351,6 +356,7 @@ __global__ void __launch_bounds__(256) k_gather_mean(MeanBatch m) {
 
 // ---- projection: out = sum_r mean_r . W_r (agg_all over relations), ReLU ------------------
 __global__ void __launch_bounds__(kT) k_project_tiles(ProjBatch pb) {
+  pdl_enter();
   __shared__ __align__(16) float As[kKS * kLd];
   __shared__ __align__(16) float Bs[kKS * kLd];
   const int gi = find_problem(pb.tile_base, pb.ng, blockIdx.x);
@@ -420,7 +426,7 @@ void gather_mean(MeanBatch& m, cudaStream_t st) {
   }
   m.item_base[m.nb] = items;
   const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(items, 16), 16 * kNumSMs)));
-  k_gather_mean<<<grid, 256, 0, st>>>(m);
+  launch_pdl(k_gather_mean, grid, 256, 0, st, m);
 }
 
 void project_tiles(ProjBatch& p, cudaStream_t st) {
@@ -431,13 +437,13 @@ void project_tiles(ProjBatch& p, cudaStream_t st) {
     tiles += static_cast<int>(ceil_div(std::max(1, p.g[g].rows_cap), kTile) * ceil_div(p.g[g].dout, kTile));
   }
   p.tile_base[p.ng] = tiles;
-  k_project_tiles<<<std::max(1, tiles), kT, 0, st>>>(p);
+  launch_pdl(k_project_tiles, std::max(1, tiles), kT, 0, st, p);
 }
 
 void agg_tiles(const AggGroup& g, cudaStream_t st) {
   const int ncb = static_cast<int>(ceil_div(g.dout, kTile));
   const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, ceil_div(g.rows_cap, kTile) * ncb));
-  k_agg_tiles<<<grid, kT, 0, st>>>(g);
+  launch_pdl(k_agg_tiles, grid, kT, 0, st, g);
 }
 
 void wgrad_tiles(WGradBatch& b, cudaStream_t st) {
@@ -449,14 +455,14 @@ void wgrad_tiles(WGradBatch& b, cudaStream_t st) {
     tiles += static_cast<int>(ceil_div(std::max(1, P.rows_cap), kWChunkRows) * ceil_div(P.din, kTile) *
                               ceil_div(P.d.cols, kTile));
   }
-  k_wgrad_tiles<<<std::max(1, tiles), kT, 0, st>>>(b);
+  launch_pdl(k_wgrad_tiles, std::max(1, tiles), kT, 0, st, b);
   wgrad_reduce(b, st);
 }
 
 void wgrad_reduce(WGradBatch& b, cudaStream_t st) {
   int total_out = 0;
   for (int p = 0; p < b.np; ++p) total_out += b.p[p].din * b.p[p].d.cols;
-  if (total_out > 0) k_wgrad_reduce<<<static_cast<unsigned>(ceil_div(total_out, 256)), 256, 0, st>>>(b, total_out);
+  if (total_out > 0) launch_pdl(k_wgrad_reduce, static_cast<unsigned>(ceil_div(total_out, 256)), 256, 0, st, b, total_out);
 }
 
 void dmean_tiles(DMeanBatch& b, cudaStream_t st) {
@@ -467,7 +473,7 @@ void dmean_tiles(DMeanBatch& b, cudaStream_t st) {
     b.tile_base[p] = tiles;
     tiles += static_cast<int>(ceil_div(std::max(1, P.rows_cap), kTile) * ceil_div(P.din, kTile));
   }
-  k_dmean_tiles<<<std::max(1, tiles), kT, 0, st>>>(b);
+  launch_pdl(k_dmean_tiles, std::max(1, tiles), kT, 0, st, b);
 }
 
 }  // namespace hetgpu

@@ -99,6 +99,7 @@ struct LbLayout {
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_lb(ScanArgs a, LbLayout L, unsigned long long* state,
                                                           int* ticket) {
+  pdl_enter();
   __shared__ int s_tile;
   __shared__ std::uint32_t s_prefix;
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
@@ -148,7 +149,7 @@ void scan_inclusive(const ScanArgs& a, LbScratch& lb, cudaStream_t st) {
   }
   L.base[a.nseg] = tiles;
   lb.reset(tiles, st);
-  k_scan_lb<<<tiles, kScanThreads, 0, st>>>(a, L, lb.state, lb.ticket);
+  launch_pdl(k_scan_lb, tiles, kScanThreads, 0, st, a, L, lb.state, lb.ticket);
 }
 
 // ---- sampling -------------------------------------------------------------------------
@@ -241,6 +242,7 @@ template <int MAXF>
 __global__ void __launch_bounds__(kSampleThreads) k_sample_fused(SampleHop h, LbLayout L, const StepScalars* sc,
                                                                  unsigned long long* state, int* ticket,
                                                                  std::uint32_t* slow, int* n_slow) {
+  pdl_enter();
   __shared__ int s_tile;
   __shared__ std::uint32_t s_prefix;
   extern __shared__ std::uint32_t s_map[];  // 2 * MAXF * kSampleThreads words (dynamic)
@@ -365,6 +367,7 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_fused(SampleHop h, Lb
 __global__ void __launch_bounds__(128) k_sample_slow(SampleHop h, const StepScalars* sc,
                                                      const std::uint32_t* slow, const int* n_slow,
                                                      std::uint64_t* scratch) {
+  pdl_enter();
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   std::uint64_t* x = scratch + static_cast<std::size_t>(tid) * (312 + h.fanout);
   std::uint32_t* mpos = reinterpret_cast<std::uint32_t*>(x + 312);
@@ -414,10 +417,10 @@ void sample_hop(const SampleHop& h, const StepScalars* sc, std::uint32_t* slow, 
     attr_set = true;
   }
   if (h.fanout <= 16)
-    k_sample_fused<16><<<tiles, kSampleThreads, smem16, st>>>(h, L, sc, lb.state, lb.ticket, slow, n_slow);
+    launch_pdl(k_sample_fused<16>, tiles, kSampleThreads, smem16, st, h, L, sc, lb.state, lb.ticket, slow, n_slow);
   else
-    k_sample_fused<32><<<tiles, kSampleThreads, smem32, st>>>(h, L, sc, lb.state, lb.ticket, slow, n_slow);
-  k_sample_slow<<<kSlowThreads / 128, 128, 0, st>>>(h, sc, slow, n_slow, scratch);
+    launch_pdl(k_sample_fused<32>, tiles, kSampleThreads, smem32, st, h, L, sc, lb.state, lb.ticket, slow, n_slow);
+  launch_pdl(k_sample_slow, kSlowThreads / 128, 128, 0, st, h, sc, slow, n_slow, scratch);
 }
 
 // ---- frontier ---------------------------------------------------------------------------
@@ -429,6 +432,7 @@ constexpr int kFrontThreads = 256;
 __global__ void __launch_bounds__(kFrontThreads) k_mark_batch(const std::uint32_t* ids,
                                                               const StepScalars* sc,
                                                               std::uint32_t* bits) {
+  pdl_enter();
   const int n = sc->batch_len;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     const std::uint32_t id = ids[e];
@@ -444,6 +448,7 @@ static_assert(kWordsPerTile == kCompactWordsPerTile, "look-back scratch sizing")
 // prefix (the rank structure) and the sorted ids of the set bits
 __global__ void __launch_bounds__(kFrontThreads) k_compact(FrontierArgs f, LbLayout L, unsigned long long* state,
                                                            int* ticket) {
+  pdl_enter();
   __shared__ int s_tile;
   __shared__ std::uint32_t s_prefix;
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
@@ -494,6 +499,7 @@ __device__ __forceinline__ std::uint32_t bitmap_rank(const BitmapType& t, std::u
 }
 
 __global__ void __launch_bounds__(kFrontThreads) k_relabel(RelabelArgs r, FrontierArgs f) {
+  pdl_enter();
   const RelabelBlock& b = r.b[blockIdx.y];
   const std::uint32_t total = b.indptr[*b.n_rows];
   const BitmapType& t = f.t[b.slot];
@@ -506,6 +512,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_relabel(RelabelArgs r, Fronti
 
 __global__ void __launch_bounds__(kFrontThreads) k_batch_mult(const std::uint32_t* ids, const StepScalars* sc,
                                                               BitmapType t, float* mult) {
+  pdl_enter();
   const int n = sc->batch_len;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x)
     atomicAdd(mult + bitmap_rank(t, ids[e]), 1.0f);
@@ -516,7 +523,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_batch_mult(const std::uint32_
 void frontier_mark_batch(const std::uint32_t* ids, const StepScalars* sc, int cap, const BitmapType& t,
                          cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, kFrontThreads), kNumSMs));
-  k_mark_batch<<<grid, kFrontThreads, 0, st>>>(ids, sc, t.bits);
+  launch_pdl(k_mark_batch, grid, kFrontThreads, 0, st, ids, sc, t.bits);
 }
 
 void frontier_compact(const FrontierArgs& f, LbScratch& lb, cudaStream_t st) {
@@ -530,7 +537,7 @@ void frontier_compact(const FrontierArgs& f, LbScratch& lb, cudaStream_t st) {
   }
   L.base[f.ntypes] = tiles;
   lb.reset(tiles, st);
-  k_compact<<<tiles, kFrontThreads, 0, st>>>(f, L, lb.state, lb.ticket);
+  launch_pdl(k_compact, tiles, kFrontThreads, 0, st, f, L, lb.state, lb.ticket);
 }
 
 void frontier_relabel(const RelabelArgs& r, const FrontierArgs& f, cudaStream_t st) {
@@ -538,13 +545,13 @@ void frontier_relabel(const RelabelArgs& r, const FrontierArgs& f, cudaStream_t 
   int cap = 1;
   for (int i = 0; i < r.nblk; ++i) cap = max(cap, r.b[i].cap);
   dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, kFrontThreads), 4 * kNumSMs)), r.nblk);
-  k_relabel<<<grid, kFrontThreads, 0, st>>>(r, f);
+  launch_pdl(k_relabel, grid, kFrontThreads, 0, st, r, f);
 }
 
 void batch_multiplicity(const std::uint32_t* ids, const StepScalars* sc, int cap, const BitmapType& t,
                         float* mult, cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, kFrontThreads), kNumSMs));
-  k_batch_mult<<<grid, kFrontThreads, 0, st>>>(ids, sc, t, mult);
+  launch_pdl(k_batch_mult, grid, kFrontThreads, 0, st, ids, sc, t, mult);
 }
 
 // ---- replica gradient merge -------------------------------------------------------------------
@@ -552,6 +559,7 @@ void batch_multiplicity(const std::uint32_t* ids, const StepScalars* sc, int cap
 namespace {
 
 __global__ void k_rmark(ReplicaMerge m) {
+  pdl_enter();
   const int r = blockIdx.y;
   const int n = *m.count[r];
   const std::uint32_t* ids = m.ids[r];
@@ -562,6 +570,7 @@ __global__ void k_rmark(ReplicaMerge m) {
 }
 
 __global__ void k_rslot(ReplicaMerge m) {
+  pdl_enter();
   const int r = blockIdx.y;
   const int n = *m.count[r];
   const std::uint32_t* ids = m.ids[r];
@@ -571,6 +580,7 @@ __global__ void k_rslot(ReplicaMerge m) {
 
 // half-warp per (union row, 64-column chunk): ordered sum over replicas
 __global__ void __launch_bounds__(256) k_rsum(ReplicaMerge m) {
+  pdl_enter();
   const int hl = threadIdx.x & 15;
   const int n = *m.u.count;
   const int nch = (m.din + 63) / 64;
@@ -598,7 +608,7 @@ __global__ void __launch_bounds__(256) k_rsum(ReplicaMerge m) {
 void replica_union(const ReplicaMerge& m, LbScratch& lb, cudaStream_t st) {
   HG_CUDA(cudaMemsetAsync(m.u.bits, 0, static_cast<std::size_t>(m.u.words) * 4, st));
   const dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(m.u.cap, 256), 2 * kNumSMs)), m.n_rep);
-  k_rmark<<<grid, 256, 0, st>>>(m);
+  launch_pdl(k_rmark, grid, 256, 0, st, m);
   FrontierArgs f{};
   f.ntypes = 1;
   f.t[0] = m.u;
@@ -607,12 +617,12 @@ void replica_union(const ReplicaMerge& m, LbScratch& lb, cudaStream_t st) {
 void replica_slots(const ReplicaMerge& m, cudaStream_t st) {
   HG_CUDA(cudaMemsetAsync(m.slot, 0xFF, static_cast<std::size_t>(m.n_rep) * m.u.cap * sizeof(int), st));
   const dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(m.u.cap, 256), 2 * kNumSMs)), m.n_rep);
-  k_rslot<<<grid, 256, 0, st>>>(m);
+  launch_pdl(k_rslot, grid, 256, 0, st, m);
 }
 void replica_sum(const ReplicaMerge& m, cudaStream_t st) {
   const unsigned g2 = static_cast<unsigned>(
       std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(m.u.cap * ceil_div(m.din, 64), 16), 16 * kNumSMs)));
-  k_rsum<<<g2, 256, 0, st>>>(m);
+  launch_pdl(k_rsum, g2, 256, 0, st, m);
 }
 void replica_merge(const ReplicaMerge& m, LbScratch& lb, cudaStream_t st) {
   replica_union(m, lb, st);
@@ -626,6 +636,7 @@ namespace {
 
 __global__ void k_cache_count(const std::uint32_t* ids, const int* n, const std::uint32_t* cached,
                               unsigned long long* hm) {
+  pdl_enter();
   const int total = *n;
   unsigned long long hit = 0, miss = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
@@ -648,12 +659,14 @@ __global__ void k_cache_count(const std::uint32_t* ids, const int* n, const std:
 
 __global__ void k_hot_add(const std::uint32_t* ids, const std::uint32_t* indptr, const int* n_rows,
                           std::uint32_t* counts) {
+  pdl_enter();
   const std::uint32_t total = indptr[*n_rows];
   for (std::uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x)
     atomicAdd(counts + ids[e], 1u);
 }
 
 __global__ void k_hot_add_list(const std::uint32_t* ids, const int* n, std::uint32_t* counts) {
+  pdl_enter();
   const int total = *n;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x)
     atomicAdd(counts + ids[e], 1u);
@@ -664,18 +677,18 @@ __global__ void k_hot_add_list(const std::uint32_t* ids, const int* n, std::uint
 void cache_count(const std::uint32_t* ids, const int* n, int cap, const std::uint32_t* cached_bits,
                  unsigned long long* hm, cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, 256), 2 * kNumSMs));
-  k_cache_count<<<std::max(grid, 1u), 256, 0, st>>>(ids, n, cached_bits, hm);
+  launch_pdl(k_cache_count, std::max(grid, 1u), 256, 0, st, ids, n, cached_bits, hm);
 }
 
 void hotness_add(const std::uint32_t* ids, const std::uint32_t* indptr, const int* n_rows, int cap,
                  std::uint32_t* counts, cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, 256), 4 * kNumSMs));
-  k_hot_add<<<std::max(grid, 1u), 256, 0, st>>>(ids, indptr, n_rows, counts);
+  launch_pdl(k_hot_add, std::max(grid, 1u), 256, 0, st, ids, indptr, n_rows, counts);
 }
 
 void hotness_add_list(const std::uint32_t* ids, const int* n, int cap, std::uint32_t* counts, cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, 256), 2 * kNumSMs));
-  k_hot_add_list<<<std::max(grid, 1u), 256, 0, st>>>(ids, n, counts);
+  launch_pdl(k_hot_add_list, std::max(grid, 1u), 256, 0, st, ids, n, counts);
 }
 
 }  // namespace hetgpu

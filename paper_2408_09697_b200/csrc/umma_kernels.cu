@@ -73,6 +73,7 @@ __device__ __forceinline__ int find_tile(const int* base, int n, int tile) {
 
 template <int NT, int MODE, typename Batch>
 __global__ void __launch_bounds__(kUT) k_umma(const __grid_constant__ UmmaArgs<Batch> args) {
+  pdl_enter();
   constexpr int S = UStage<NT>::kStages;
   extern __shared__ std::uint8_t smem_raw[];
   std::uint8_t* smem = reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
@@ -296,7 +297,7 @@ void launch(UmmaArgs<Batch>& a, int tiles, cudaStream_t st) {
                                  UStage<NT>::kSmem));
     attr = true;
   }
-  k_umma<NT, MODE, Batch><<<tiles, kUT, UStage<NT>::kSmem, st>>>(a);
+  launch_pdl(k_umma<NT, MODE, Batch>, tiles, kUT, UStage<NT>::kSmem, st, a);
 }
 
 // column tile width (multiples of 32 for the MN-major boxes); wider outputs take
