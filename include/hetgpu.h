@@ -125,6 +125,16 @@ typedef struct {
   uint64_t sampled_edges;
   int n_active; /* entries filled in active_rows (p > 1) */
   int active_rows[64];
+  /* ExecutionReport bookkeeping (raf.hpp:66-77). sync_bytes is this rank's replica
+   * group's share of the ring all-reduce model (raf.cpp:496-510); summing it over
+   * the ranks with sync_leader = 1 gives the reference's run-wide number. */
+  uint64_t sync_bytes;
+  int sync_leader;
+  int message_bound_ok; /* check_comm_bounds (raf.cpp:662-676) */
+  int target_only_ok;   /* cross_ids_target_only (raf.cpp:511-514) */
+  int n_boundary;       /* entries filled in boundary_counts (= p) */
+  uint64_t boundary_cut_edges;   /* raf.cpp:521-528 */
+  uint64_t boundary_counts[64];  /* structural_boundaries (raf.cpp:306-340), per worker */
 } hg_step_report;
 
 hg_engine* hg_engine_create(const hg_graph* g, const hg_engine_opts* opts);
@@ -167,7 +177,8 @@ hg_bundle* hg_engine_profile_read(hg_engine* e);
 int hg_engine_info(hg_engine* e, uint64_t* param_count, uint64_t* device_bytes, int* model_step);
 /* options: "retain_grads" (keep learnable-row gradients readable as grad.f.*; default 1),
  * "graphs" (replay the step as a CUDA graph; default 1), "umma" (dense contractions on
- * tcgen05 tensor cores, 3xTF32; 0 = SIMT fp32 tiles for A/B checks; default 1) */
+ * tcgen05 tensor cores, 3xTF32; 0 = SIMT fp32 tiles for A/B checks; default 1),
+ * "elem_bytes" (AccountingModel::elem_bytes of the sync_bytes model: 2, 4 or 8; default 4) */
 int hg_engine_set_option(hg_engine* e, const char* name, int value);
 /* Device self-test of the tcgen05 contractions against the fp32 SIMT tiles on random
  * problems: cases = n_cases x (rows, nrel, din, dout); err = [n_cases x 3] relative

@@ -355,6 +355,12 @@ struct ExecutionReport {
   double loss = 0.0;
   std::uint64_t sampled_edges = 0;     // Block::src_ids entries over all hops (this partition)
   std::vector<int> active_rows;        // per rank (p > 1): rows of the AGG_all partial (raf.cpp:418-446)
+  std::uint64_t sync_bytes = 0;        // this rank's replica group's share (raf.cpp:496-510)
+  bool sync_leader = true;             // sum sync_bytes over leaders for the run-wide figure
+  std::vector<std::uint64_t> boundary_counts;  // structural, per worker (raf.cpp:306-340)
+  std::uint64_t boundary_cut_edges = 0;        // raf.cpp:521-528
+  bool cross_ids_target_only = true;
+  bool message_bound_ok = true;        // check_comm_bounds (raf.cpp:662-676)
 };
 
 class RafEngine {
@@ -378,6 +384,12 @@ class RafEngine {
     out.loss = r.loss;
     out.sampled_edges = r.sampled_edges;
     out.active_rows.assign(r.active_rows, r.active_rows + r.n_active);
+    out.sync_bytes = r.sync_bytes;
+    out.sync_leader = r.sync_leader != 0;
+    out.boundary_counts.assign(r.boundary_counts, r.boundary_counts + r.n_boundary);
+    out.boundary_cut_edges = r.boundary_cut_edges;
+    out.cross_ids_target_only = r.target_only_ok != 0;
+    out.message_bound_ok = r.message_bound_ok != 0;
     return out;
   }
   // sample a future batch now (second sample slot, sampling stream); the next

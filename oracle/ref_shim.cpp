@@ -445,7 +445,8 @@ void* ref_raf_train(void* sp, int k, int hidden, int p, unsigned long long seed,
     const auto fo = to_vec(fanouts, k);
     auto* b = new Bundle;
     std::vector<double> losses;
-    std::vector<std::uint64_t> bytes, sync;
+    std::vector<std::uint64_t> bytes, sync, bound_ok, target_ok;
+    const int n_rel = static_cast<int>(g.relations.size());
     int off = 0;
     for (int i = 0; i < n_batches; ++i) {
       std::vector<NodeId> batch(batches_flat + off, batches_flat + off + batch_counts[i]);
@@ -455,7 +456,12 @@ void* ref_raf_train(void* sp, int k, int hidden, int p, unsigned long long seed,
       losses.push_back(rep.loss);
       bytes.push_back(rep.stats.total_bytes());
       sync.push_back(rep.sync_bytes);
+      const CommBoundVerdict v = check_comm_bounds(rep, n_rel, view.meta);  // as harness.cpp:411
+      bound_ok.push_back(v.message_bound_ok ? 1 : 0);
+      target_ok.push_back(v.target_only_ok ? 1 : 0);
       if (i == 0) {
+        b->put_u64("boundary_counts", rep.boundary_counts);
+        b->put_u64("boundary_cut_edges", {rep.boundary_cut_edges});
         b->put_matrix("b0.logits", rep.logits);
         put_grads(*b, rep.grads, "b0.grad");
         std::vector<std::uint64_t> dirs;
@@ -475,6 +481,8 @@ void* ref_raf_train(void* sp, int k, int hidden, int p, unsigned long long seed,
     b->put_f64("losses", losses);
     b->put_u64("bytes", bytes);
     b->put_u64("sync_bytes", sync);
+    b->put_u64("message_bound_ok", bound_ok);
+    b->put_u64("target_only_ok", target_ok);
     put_model(*b, model, "final");
     for (const auto& [t, tab] : store.tables) {
       b->put_matrix("final.learn.t" + std::to_string(t), tab.w);

@@ -46,7 +46,9 @@ class EngineOpts(C.Structure):
 
 class StepReport(C.Structure):
     _fields_ = [("loss", C.c_double), ("sampled_edges", C.c_uint64), ("n_active", C.c_int),
-                ("active_rows", C.c_int * 64)]
+                ("active_rows", C.c_int * 64), ("sync_bytes", C.c_uint64), ("sync_leader", C.c_int),
+                ("message_bound_ok", C.c_int), ("target_only_ok", C.c_int), ("n_boundary", C.c_int),
+                ("boundary_cut_edges", C.c_uint64), ("boundary_counts", C.c_uint64 * 64)]
 
 
 def lib():

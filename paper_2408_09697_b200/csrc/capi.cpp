@@ -293,6 +293,17 @@ hg_bundle* hg_meta_partition(const hg_graph* h, int k, int p) {
     }
     const auto hr = hop_relations(plan.tree, k);
     for (int i = 0; i < k; ++i) b->add("hop_rels" + std::to_string(i + 1), "<i4", hr[i]);
+    // batch-invariant RAF bookkeeping of this plan (raf.cpp:306-340, 496-503, 521-528)
+    const RafAccounting a = plan_accounting(g, plan);
+    b->add("raf.boundary_counts", "<u8", a.boundary_counts);
+    b->add("raf.boundary_cut_edges", "<u8", std::vector<std::uint64_t>{a.boundary_cut_edges});
+    std::vector<int> slot_rows;  // (rel, layer, n_contributors) per slot
+    for (const auto& [id, who] : a.slot_contributors) {
+      slot_rows.push_back(id.rel);
+      slot_rows.push_back(id.layer);
+      slot_rows.push_back(static_cast<int>(who.size()));
+    }
+    b->add("raf.slot_contributors", "<i4", slot_rows);
     return b;
   });
 }
@@ -371,6 +382,13 @@ int hg_engine_step(hg_engine* e, const uint32_t* batch, int n, uint64_t rng_seed
       out->sampled_edges = r.sampled_edges;
       out->n_active = static_cast<int>(std::min<std::size_t>(64, r.active_rows.size()));
       for (int i = 0; i < out->n_active; ++i) out->active_rows[i] = r.active_rows[i];
+      out->sync_bytes = r.sync_bytes;
+      out->sync_leader = r.sync_leader ? 1 : 0;
+      out->message_bound_ok = r.message_bound_ok ? 1 : 0;
+      out->target_only_ok = r.target_only_ok ? 1 : 0;
+      out->boundary_cut_edges = r.boundary_cut_edges;
+      out->n_boundary = static_cast<int>(std::min<std::size_t>(64, r.boundary_counts.size()));
+      for (int i = 0; i < out->n_boundary; ++i) out->boundary_counts[i] = r.boundary_counts[i];
     }
     return 0;
   });
@@ -535,6 +553,8 @@ int hg_engine_set_option(hg_engine* e, const char* name, int value) {
       e->e->set_graphs(value != 0);
     else if (n == "umma")
       e->e->set_umma(value != 0);
+    else if (n == "elem_bytes")
+      e->e->set_elem_bytes(value);
     else
       throw std::invalid_argument("unknown engine option: " + n);
     return 0;

@@ -56,6 +56,28 @@ __global__ void k_active_rows(EdgeCountArgs a, const int* n_rows, float* slot) {
   if (threadIdx.x == 0) *slot = static_cast<float>(total);
 }
 
+// learnable-row part of sync_bytes for a replica group (raf.cpp:504-510): per
+// exchanged type, s = replicas with a non-empty leaf frontier (its
+// feat_contributors), rows = the union the merge just built
+struct FeatSyncArgs {
+  const int* ucount[kMaxSegs];
+  const int* count[kMaxSegs][kMaxRep];
+  int dim[kMaxSegs];
+  int nt, n_rep, elem;
+};
+__global__ void k_feat_sync(FeatSyncArgs a, std::uint64_t* out) {
+  pdl_enter();
+  std::uint64_t bytes = 0;
+  for (int t = 0; t < a.nt; ++t) {
+    std::uint64_t s = 0;
+    for (int r = 0; r < a.n_rep; ++r) s += *a.count[t][r] > 0 ? 1 : 0;
+    if (s < 2) continue;
+    const std::uint64_t n = static_cast<std::uint64_t>(*a.ucount[t]) * static_cast<std::uint64_t>(a.dim[t]);
+    bytes += 2ull * n * static_cast<std::uint64_t>(a.elem) * (s - 1) / s;
+  }
+  *out = bytes;
+}
+
 __global__ void k_gather_rows(const float* table, int ld, const std::uint32_t* ids, const int* n, int cols,
                               float* out) {
   pdl_enter();
@@ -197,10 +219,13 @@ void* Engine::alloc(std::size_t bytes) {
 void Engine::build_plan(const Graph& g) {
   const Schema sch = schema_of(g);
   const int k = o_.k;
+  n_rel_ = g.num_rels();
   if (o_.p <= 1) {
     tree_ = bfs_tree(sch, target_, k);
+    acct_ = raf_accounting(g, tree_, std::vector<std::vector<int>>(tree_.pos.at(0).children.size(), {0}), 1);
   } else {
     const Plan plan = meta_partition(sch, target_, k, o_.p);
+    acct_ = plan_accounting(g, plan);  // run_experiment's view: raf_view_from_plan
     const Part& part = plan.parts.at(o_.rank);
     // replica group: the partitions owning exactly this sub-metatree set
     for (int q = 0; q < static_cast<int>(plan.parts.size()); ++q)
@@ -729,6 +754,7 @@ void Engine::bind_slot(int s) {
   loss_ = &rb_slot_[s]->loss;
   err_ = &rb_slot_[s]->err;
   edges_dev_ = &rb_slot_[s]->edges;
+  feat_sync_dev_ = &rb_slot_[s]->feat_sync;
   h_rb_ = h_rb_slot_[s];
   lb_ = lb_slot_[s];  // sampling scratch: two slots can sample concurrently
   slow_ = slow_slot_[s];
@@ -1101,6 +1127,19 @@ void Engine::run_replica_merge() {
     ++ab.n;
   }
   ab.total4 = base;
+  {
+    FeatSyncArgs fs{};
+    fs.n_rep = static_cast<int>(peer_arena_.size());
+    fs.elem = elem_bytes_;
+    for (auto& x : xchg_) {
+      fs.ucount[fs.nt] = x.ucount;
+      for (int r = 0; r < fs.n_rep; ++r)
+        fs.count[fs.nt][r] = reinterpret_cast<const int*>(peer_arena_[r] + x.off_count[bound_]);
+      fs.dim[fs.nt] = tables_[x.t].dim;
+      ++fs.nt;
+    }
+    launch_pdl(k_feat_sync, 1, 1, 0, st_, fs, feat_sync_dev_);
+  }
   // bumps each table's step iff its union is non-empty
   timed("replica_adam", 0, [&] { adam_rows(ab, AdamHyper{}, err_, st_); });
   // 3. nobody rewrites its arena (next step's sampling) before every peer read it
@@ -1287,6 +1326,7 @@ StepScalars Engine::next_scalars(std::uint64_t rng_seed, int n, int designated, 
   sc.rng_seed = rng_seed;
   sc.batch_len = n;
   sc.designated = designated;
+  last_designated_ = designated;
   sc.model_step = model_step_;
   return sc;
 }
@@ -1356,7 +1396,34 @@ StepReport Engine::finish_step() {
                        cudaMemcpyDeviceToHost));
     for (int q = 0; q < o_.p; ++q) r.active_rows.push_back(static_cast<int>(row[q]));
   }
+  // ExecutionReport bookkeeping. Only the AGG_all partials cross workers, one
+  // PartialAgg per non-designated worker with active rows (raf.cpp:427-446), all
+  // of the target type, so cross_ids_target_only holds and check_comm_bounds
+  // compares that one message against num_relations x boundary_counts[sender].
+  r.boundary_counts = acct_.boundary_counts;
+  r.boundary_cut_edges = acct_.boundary_cut_edges;
+  for (std::size_t q = 0; q < r.active_rows.size(); ++q)
+    if (static_cast<int>(q) != last_designated_ && r.active_rows[q] > 0 &&
+        1ull > static_cast<std::uint64_t>(n_rel_) * acct_.boundary_counts.at(q))
+      r.message_bound_ok = false;
+  r.sync_bytes = model_sync_bytes() + h_rb_->feat_sync;
+  r.sync_leader = replica_pos_ == 0;
   return r;
+}
+
+std::uint64_t Engine::model_sync_bytes() const {
+  // slot part of sync_bytes (raf.cpp:496-503) for the slots this rank contributes to
+  std::uint64_t bytes = 0;
+  for (const auto& [id, who] : acct_.slot_contributors) {
+    const std::uint64_t s = who.size();
+    if (s < 2 || std::find(who.begin(), who.end(), o_.rank) == who.end()) continue;
+    for (const auto& sl : slots_)
+      if (sl.rel == id.rel && sl.layer == id.layer) {
+        const std::uint64_t n = static_cast<std::uint64_t>(sl.din) * static_cast<std::uint64_t>(sl.dout);
+        bytes += 2ull * n * static_cast<std::uint64_t>(elem_bytes_) * (s - 1) / s;
+      }
+  }
+  return bytes;
 }
 
 StepReport Engine::step(const NodeId* batch, int n, std::uint64_t rng_seed, int designated, bool train) {

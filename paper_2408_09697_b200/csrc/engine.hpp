@@ -53,6 +53,13 @@ struct StepReport {
   std::uint64_t sampled_edges = 0;   // Block::src_ids entries, all hops (this partition)
   std::uint32_t err = 0;
   std::vector<int> active_rows;      // per rank: batch rows with >= 1 sampled top edge
+  // ExecutionReport bookkeeping (raf.hpp:66-77), see Engine::accounting
+  std::uint64_t sync_bytes = 0;      // this rank's replica group: ring all-reduce model (raf.cpp:496-510)
+  bool sync_leader = true;           // sum sync_bytes over leaders = the reference's run-wide number
+  std::vector<std::uint64_t> boundary_counts;  // per worker (raf.cpp:306-340)
+  std::uint64_t boundary_cut_edges = 0;        // raf.cpp:521-528
+  bool message_bound_ok = true;      // check_comm_bounds (raf.cpp:662-676)
+  bool target_only_ok = true;        // only target-type rows cross workers (raf.cpp:511-514)
 };
 
 struct DeviceBuffer {
@@ -123,6 +130,11 @@ class Engine {
     }
   }
   StepReport finish_step();  // waits for the last trained step and reads its report
+  // payload element width of the accounting model (AccountingModel::elem_bytes, raf.hpp:15-19)
+  void set_elem_bytes(int b) {
+    if (b != 2 && b != 4 && b != 8) throw std::invalid_argument("elem_bytes must be 2, 4 or 8");
+    elem_bytes_ = b;
+  }
   // Sampling only (parity of the sampler; presample_hotness).
   void sample_only(const NodeId* batch, int n, std::uint64_t rng_seed);
 
@@ -342,9 +354,17 @@ class Engine {
     std::uint32_t err;
     std::uint32_t pad;
     std::uint64_t edges;
+    std::uint64_t feat_sync;  // learnable-row part of sync_bytes (replica groups)
   };
+  // batch-invariant RAF bookkeeping of the whole plan (host, once)
+  RafAccounting acct_;
+  int elem_bytes_ = 4;
+  int n_rel_ = 0;
+  std::uint64_t model_sync_bytes() const;
   Readback* h_rb_ = nullptr;  // pinned, bound slot
   std::uint64_t* edges_dev_ = nullptr;
+  std::uint64_t* feat_sync_dev_ = nullptr;
+  int last_designated_ = 0;
   unsigned long long* cache_hm_ = nullptr;  // [ntypes x 2]
 
   // scratch

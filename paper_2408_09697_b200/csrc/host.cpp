@@ -5,6 +5,7 @@
 #include <cmath>
 #include <numeric>
 #include <random>
+#include <set>
 
 namespace hetgpu {
 
@@ -247,6 +248,65 @@ std::vector<int> Plan::owners_of_sub(int sub_id) const {
   for (std::size_t i = 0; i < parts.size(); ++i)
     if (contains(parts[i].sub_ids, sub_id)) out.push_back(static_cast<int>(i));
   return out;
+}
+
+RafAccounting raf_accounting(const Graph& g, const Tree& t, const std::vector<std::vector<int>>& top_owners, int p) {
+  RafAccounting a;
+  a.boundary_counts.assign(static_cast<std::size_t>(std::max(p, 1)), 0);
+  const auto& root_kids = t.pos.at(0).children;
+  if (top_owners.size() != root_kids.size()) throw std::invalid_argument("one owner list per root child expected");
+  auto owners_of = [&](int pos) -> const std::vector<int>& {
+    const int anc = t.root_child_ancestor(pos);
+    for (std::size_t ci = 0; ci < root_kids.size(); ++ci)
+      if (root_kids[ci] == anc) return top_owners[ci];
+    throw std::logic_error("position outside every root subtree");
+  };
+  // sender-side boundary per worker: the parent-type nodes with at least one
+  // in-edge of a crossing (depth-1) relation, as a set over (type, node)
+  std::vector<std::vector<std::uint64_t>> marks(a.boundary_counts.size());
+  for (std::size_t pos = 1; pos < t.pos.size(); ++pos) {
+    const TreePos& tp = t.pos[pos];
+    const std::vector<int>& own = owners_of(static_cast<int>(pos));
+    std::set<int> who(own.begin(), own.end());
+    auto& c = a.slot_contributors[SlotId{tp.rel, t.k - tp.depth + 1}];
+    for (int w : c) who.insert(w);
+    c.assign(who.begin(), who.end());
+    if (tp.depth == t.k && g.types[tp.type].storage == Storage::Learnable) {
+      auto& lo = a.leaf_owners[tp.type];
+      std::set<int> lw(lo.begin(), lo.end());
+      lw.insert(own.begin(), own.end());
+      lo.assign(lw.begin(), lw.end());
+    }
+    if (tp.depth != 1) continue;  // meta plans: inner positions never cross workers
+    const Adjacency& adj = g.rels[tp.rel].adj;
+    a.boundary_cut_edges += adj.sources.size();
+    const int parent_type = t.pos[tp.parent].type;
+    const std::uint64_t n = g.types[parent_type].count;
+    for (int w : own) {
+      auto& m = marks[w];
+      if (m.empty()) m.assign(static_cast<std::size_t>((n + 63) / 64), 0);  // one parent type: the root
+      for (std::uint64_t v = 0; v < n; ++v)
+        if (adj.offsets[v + 1] > adj.offsets[v]) m[v >> 6] |= 1ull << (v & 63);
+    }
+  }
+  for (std::size_t w = 0; w < marks.size(); ++w)
+    for (std::uint64_t x : marks[w]) a.boundary_counts[w] += static_cast<std::uint64_t>(__builtin_popcountll(x));
+  return a;
+}
+
+RafAccounting plan_accounting(const Graph& g, const Plan& plan) {
+  std::vector<std::vector<int>> top;
+  for (int c : plan.tree.pos.at(0).children) {
+    bool found = false;
+    for (const auto& sub : plan.subs)
+      if (sub.child_pos == c) {
+        top.push_back(plan.owners_of_sub(sub.id));
+        found = true;
+        break;
+      }
+    if (!found) throw std::invalid_argument("plan has no sub-metatree for a root child");
+  }
+  return raf_accounting(g, plan.tree, top, plan.p);
 }
 
 Schema schema_of(const Graph& g) {

@@ -210,6 +210,24 @@ ModelInit init_model(const Graph& g, const Tree& t, int hidden, std::uint64_t se
 // Learnable tables: uniform in [-1/sqrt(d), 1/sqrt(d)] per type (hgnn.cpp:64-81).
 std::map<int, std::vector<double>> init_learnable(const Graph& g, std::uint64_t seed);
 
+// ---- batch-invariant RAF bookkeeping ---------------------
+// run_raf_batch recomputes these every batch although they depend only on the
+// plan: structural_boundaries (raf.cpp:306-340), boundary_cut_edges
+// (raf.cpp:521-528) and the contributor sets behind the slot part of
+// sync_bytes (raf.cpp:217, 414, 496-503). Meta view: a depth-1 position is the
+// only crossing kind; a slot's contributors are the owners of the root children
+// whose subtrees hold a position with that (relation, layer).
+struct RafAccounting {
+  std::vector<std::uint64_t> boundary_counts;          // per worker
+  std::uint64_t boundary_cut_edges = 0;
+  std::map<SlotId, std::vector<int>> slot_contributors;  // ascending worker ids
+  std::map<int, std::vector<int>> leaf_owners;           // learnable leaf type -> possible contributors
+};
+// top_owners[ci]: owning workers of root child ci (tree.pos[0].children order)
+RafAccounting raf_accounting(const Graph& g, const Tree& t, const std::vector<std::vector<int>>& top_owners, int p);
+// the same for a meta plan's view (raf_view_from_plan, raf.cpp:43-57)
+RafAccounting plan_accounting(const Graph& g, const Plan& plan);
+
 // make_batches (harness.cpp:327-340): shuffled target ids in batch_size chunks.
 std::vector<std::vector<NodeId>> make_batches(const Graph& g, int batch_size, int max_batches,
                                               std::uint64_t seed);

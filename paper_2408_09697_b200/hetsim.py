@@ -248,8 +248,15 @@ class Engine:
         b = np.ascontiguousarray(batch, dtype=np.uint32)
         rep = N.StepReport()
         N.check(N.lib().hg_engine_step(self._h, N.ptr(b), len(b), rng_seed, designated, int(train), C.byref(rep)))
+        # ExecutionReport fields (raf.hpp:66-77); sync_bytes is this rank's replica
+        # group's share: sum it over the ranks whose sync_leader is set
         return dict(loss=rep.loss, sampled_edges=int(rep.sampled_edges),
-                    active_rows=[rep.active_rows[i] for i in range(rep.n_active)])
+                    active_rows=[rep.active_rows[i] for i in range(rep.n_active)],
+                    sync_bytes=int(rep.sync_bytes), sync_leader=bool(rep.sync_leader),
+                    message_bound_ok=bool(rep.message_bound_ok), target_only_ok=bool(rep.target_only_ok),
+                    cross_ids_target_only=bool(rep.target_only_ok),
+                    boundary_counts=[int(rep.boundary_counts[i]) for i in range(rep.n_boundary)],
+                    boundary_cut_edges=int(rep.boundary_cut_edges))
 
     def prefetch(self, batch, rng_seed: int) -> None:
         """Sample a future batch now (sampling stream, second sample slot); the

@@ -193,6 +193,10 @@ int main() {
       const double rel = std::fabs(brep.loss - rrep.loss) / std::fabs(rrep.loss);
       std::printf("batch %zu loss ref %.9f b200 %.9f rel %.2e\n", i, rrep.loss, brep.loss, rel);
       EXPECT(rel < 1e-3, "run_raf_batch loss within 1e-3");
+      EXPECT(brep.boundary_counts == rrep.boundary_counts, "ExecutionReport::boundary_counts");
+      EXPECT(brep.boundary_cut_edges == rrep.boundary_cut_edges, "ExecutionReport::boundary_cut_edges");
+      EXPECT(brep.sync_bytes == rrep.sync_bytes, "ExecutionReport::sync_bytes");
+      EXPECT(brep.cross_ids_target_only == rrep.cross_ids_target_only, "ExecutionReport::cross_ids_target_only");
     }
   }
 

@@ -47,7 +47,7 @@ def main():
         time.sleep(0.05)
     eng.attach_replicas([open(f"{id_path}.h{r}", "rb").read() for r in range(p)])
     batches = H.make_batches(g, bsz, n_batches, H.mix_seed(seed, 0xBA7C))
-    losses, active = [], []
+    losses, active, sync, lead, bound_ok, target_ok = [], [], [], [], [], []
     for i, b in enumerate(batches):
         rep = eng.step(b, H.mix_seed(seed, 0xB000 + i), i % p)
         if i == 0:
@@ -55,8 +55,16 @@ def main():
         print(f"rank {rank}: batch {i} loss {rep['loss']:.6f}", flush=True)
         losses.append(rep["loss"])
         active.append(rep["active_rows"])
+        sync.append(rep["sync_bytes"])
+        lead.append(int(rep["sync_leader"]))
+        bound_ok.append(int(rep["message_bound_ok"]))
+        target_ok.append(int(rep["target_only_ok"]))
+        boundary = (rep["boundary_counts"], rep["boundary_cut_edges"])
     post = eng.read(*[n for n in eng.tensor_names() if n.startswith(("post.r", "post.learn.t", "post.learn_step.t"))])
     np.savez(out_path, losses=np.asarray(losses), active=np.asarray(active, np.int64),
+             sync=np.asarray(sync, np.uint64), lead=np.asarray(lead), bound_ok=np.asarray(bound_ok),
+             target_ok=np.asarray(target_ok), boundary=np.asarray(boundary[0], np.uint64),
+             cut_edges=np.asarray([boundary[1]], np.uint64),
              **{"T:" + k: v for k, v in post.items()}, **{"G:" + k: v for k, v in g0.items()})
 
 

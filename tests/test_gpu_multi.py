@@ -80,3 +80,14 @@ def test_raf_multi_gpu_matches_reference(ref, name, p):
     for i in range(n_batches):
         got_bytes = H.agg_all_comm_bytes(act[i], i % p, C)["total_bytes"]
         assert got_bytes == int(want["bytes"][i]), (i, got_bytes, int(want["bytes"][i]))
+    # ExecutionReport bookkeeping (raf.hpp:66-77): the ring-model sync bytes of
+    # replicated slots and learnable rows (raf.cpp:496-510) summed over replica-group
+    # leaders, structural boundaries and cut edges, and the check_comm_bounds verdicts
+    for i in range(n_batches):
+        got_sync = sum(int(res[r]["sync"][i]) for r in range(p) if res[r]["lead"][i])
+        assert got_sync == int(want["sync_bytes"][i]), (i, got_sync, int(want["sync_bytes"][i]))
+    for r in range(p):
+        assert np.array_equal(res[r]["boundary"], want["boundary_counts"]), r
+        assert int(res[r]["cut_edges"][0]) == int(want["boundary_cut_edges"][0])
+        assert np.array_equal(res[r]["bound_ok"], want["message_bound_ok"].astype(res[r]["bound_ok"].dtype))
+        assert np.array_equal(res[r]["target_ok"], want["target_only_ok"].astype(res[r]["target_ok"].dtype))

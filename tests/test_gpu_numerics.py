@@ -166,8 +166,14 @@ def test_toy_config_run_experiment(H, ref):
     g = H.gen_synthetic(spec, seed)
     eng = H.Engine.for_experiment(g, [10, 10], 64, seed, batch_cap=1024)
     batches = H.make_batches(g, 1024, nb, H.mix_seed(seed, 0xBA7C))
-    losses = [eng.step(b, H.mix_seed(seed, 0xB000 + i), 0)["loss"] for i, b in enumerate(batches)]
-    np.testing.assert_allclose(losses, [b["loss"] for b in stats["batches"]], rtol=1e-3, atol=0)
+    reps = [eng.step(b, H.mix_seed(seed, 0xB000 + i), 0) for i, b in enumerate(batches)]
+    np.testing.assert_allclose([r["loss"] for r in reps], [b["loss"] for b in stats["batches"]], rtol=1e-3, atol=0)
+    # the per-batch stats entry of run_experiment (harness.cpp:410-446)
+    for r, want in zip(reps, stats["batches"]):
+        assert r["boundary_counts"] == want["boundary_counts"]
+        assert r["sync_bytes"] == want["sync_bytes"] and r["sync_leader"]
+        assert r["message_bound_ok"] == want["message_bound_ok"]
+        assert r["target_only_ok"] == want["target_only_ok"]
 
 
 def test_prefetch_pipeline_is_bit_identical(H):

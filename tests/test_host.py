@@ -148,6 +148,25 @@ def test_plans_match_reference(H, ref, p):
                 assert np.array_equal(want[key], got[key]), (s, k, p, key)
 
 
+@pytest.mark.parametrize("p", [1, 2, 4, 8])
+def test_raf_bookkeeping_matches_reference(H, ref, p):
+    # batch-invariant ExecutionReport fields computed once per plan (SURVEY 8(f)
+    # item 3): structural_boundaries (raf.cpp:306-340) and boundary_cut_edges
+    # (raf.cpp:521-528) equal what run_raf_batch reports for a real batch
+    for name in H.bundled_spec_names():
+        g = H.gen_synthetic(H.bundled_spec(name), 5)
+        batch = H.make_batches(g, 32, 1, H.mix_seed(5, 0xBA7C))[0]
+        want = ref.RefGraph.bundled(name, 5).raf_train(2, 16, p, 5, [list(batch)], [5, 5])
+        got = H.meta_partition(g, 2, p)
+        assert np.array_equal(got["raf.boundary_counts"], want["boundary_counts"]), (name, p)
+        assert int(got["raf.boundary_cut_edges"][0]) == int(want["boundary_cut_edges"][0]), (name, p)
+        assert int(want["message_bound_ok"][0]) == 1 and int(want["target_only_ok"][0]) == 1
+        contrib = got["raf.slot_contributors"].reshape(-1, 3)
+        assert contrib[:, 2].min() >= 1 and contrib[:, 2].max() <= p
+        if p == 1:
+            assert int(want["sync_bytes"][0]) == 0 and contrib[:, 2].max() == 1
+
+
 def test_make_batches_matches_reference_shuffle(H, ref):
     g = H.gen_synthetic(H.bundled_spec("mag-mini"), 5)
     batches = H.make_batches(g, 256, 0, H.mix_seed(5, 0xBA7C))
