@@ -218,6 +218,8 @@ def run_b200(args):
     SUM = tdist.ReduceOp.SUM if world > 1 else None
 
     eng.set_option("retain_grads", 0)  # learnable-row grads feed Adam in registers
+    if os.environ.get("HG_SHARD_MERGE", "0") != "0":  # A/B: replica merge sharded by id
+        eng.set_option("shard_merge", 1)
     launches = eng.count_launches(len(batches[0]), True)
     dbg(f"launches {launches}")
     # warm-up (also JIT-free: everything is precompiled sm_100a)
@@ -313,6 +315,8 @@ def run_b200(args):
                      "alg_bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms,
                      "kernels": {k: roof_of(k) for k in alg_by}},
         "kernel_share": {k: v / max(1e-9, sum(classes.values())) for k, v in sorted(classes.items())},
+        # eager profiled pass (events around every kernel class, rank 0): device us per step
+        "kernel_us_per_step": {k: round(v * 1000.0 / prof_steps, 2) for k, v in sorted(classes.items())},
         "kernel_us_per_step_eager": {k: 1000.0 * v / prof_steps for k, v in sorted(classes.items())},
         "final_loss": loss,
         "setup_s": {"graph_gen": t_gen},

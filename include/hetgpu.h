@@ -178,7 +178,9 @@ int hg_engine_info(hg_engine* e, uint64_t* param_count, uint64_t* device_bytes, 
 /* options: "retain_grads" (keep learnable-row gradients readable as grad.f.*; default 1),
  * "graphs" (replay the step as a CUDA graph; default 1), "umma" (dense contractions on
  * tcgen05 tensor cores, 3xTF32; 0 = SIMT fp32 tiles for A/B checks; default 1),
- * "elem_bytes" (AccountingModel::elem_bytes of the sync_bytes model: 2, 4 or 8; default 4) */
+ * "elem_bytes" (AccountingModel::elem_bytes of the sync_bytes model: 2, 4 or 8; default 4),
+ * "shard_merge" (replica groups: each replica Adam-updates only its id shard of the merged
+ * learnable rows and stores them into every copy; default 0) */
 int hg_engine_set_option(hg_engine* e, const char* name, int value);
 /* Device self-test of the tcgen05 contractions against the fp32 SIMT tiles on random
  * problems: cases = n_cases x (rows, nrel, din, dout); err = [n_cases x 3] relative
@@ -206,9 +208,10 @@ hg_bundle* hg_engine_cache_counters(hg_engine* e);
 int hg_nccl_unique_id(void* out, int cap);
 int hg_engine_attach_nccl(hg_engine* e, const void* unique_id, int id_bytes, int nranks, int rank);
 /* Replica groups (p larger than the number of sub-metatrees; metapartition.cpp:206-236):
- * hg_engine_replica_handle writes this engine's CUDA IPC handle of its gradient-exchange
- * arena (returns its size; 0 if the partition has no replicas). Every rank passes the
- * handles of all ranks (nranks x handle_bytes, rank order; any bytes for ranks without
+ * hg_engine_replica_handle writes this engine's CUDA IPC handles (its gradient-exchange
+ * arena, then its copy of every exchanged learnable table; returns the byte count, 0 if
+ * the partition has no replicas). Every rank passes the handles of all ranks (nranks x
+ * handle_bytes, rank order, each zero-padded to handle_bytes; any bytes for ranks without
  * replicas) to hg_engine_attach_replicas after hg_engine_attach_nccl. */
 int hg_engine_replica_handle(hg_engine* e, void* out, int cap);
 int hg_engine_attach_replicas(hg_engine* e, const void* handles, int handle_bytes, int nranks);

@@ -413,7 +413,7 @@ class RafEngine {
   // replica groups (p > #sub-metatrees): this rank's CUDA IPC handle of its gradient
   // exchange arena (empty without replicas); every rank then maps all ranks' handles
   std::vector<char> replica_handle() {
-    std::vector<char> h(128);
+    std::vector<char> h(4096);
     const int n = detail::check(hg_engine_replica_handle(e_.get(), h.data(), static_cast<int>(h.size())));
     h.resize(n);
     return h;

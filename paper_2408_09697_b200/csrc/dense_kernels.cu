@@ -338,7 +338,65 @@ __global__ void k_bump_list(BumpArgs a) {
   const int t = threadIdx.x;
   if (t < a.count && *a.n[t] > 0) ++*a.step[t];
 }
+// half-warp per (union row of this shard, 64-column chunk): replicas' rows
+// summed in replica order (hgnn.cpp:83-113 accumulate), then Adam on the table
+// row (hgnn.cpp:392-410). The shard owns the row's m / v; its new w is stored
+// into every replica's copy of the table (NVLink stores to the peers).
+__global__ void __launch_bounds__(256) k_rsum_adam(ReplicaMerge m, ReplicaAdam a, AdamHyper hp,
+                                                   std::uint32_t* err) {
+  pdl_enter();
+  __shared__ AdamStep ks;
+  if (threadIdx.x == 0) ks = adam_step_of(hp, static_cast<double>(*a.step));
+  __syncthreads();
+  const int hl = threadIdx.x & 15;
+  const int n = *m.u.count;
+  const int nch = (m.din + 63) / 64;
+  const int halves = gridDim.x * (blockDim.x >> 4);
+  for (int item = blockIdx.x * (blockDim.x >> 4) + (threadIdx.x >> 4); item < n * nch; item += halves) {
+    const int u = item / nch;
+    const int f = (item % nch) * 64 + 4 * hl;
+    if (f >= m.ld) continue;
+    const std::size_t at = static_cast<std::size_t>(m.u.list[u]) * a.ld_w + f;
+    float4 w = *reinterpret_cast<const float4*>(a.w + at);
+    float4 mm = *reinterpret_cast<const float4*>(a.m + at);
+    float4 v = *reinterpret_cast<const float4*>(a.v + at);
+    float4 part[kMaxRep];
+#pragma unroll
+    for (int r = 0; r < kMaxRep; ++r) {
+      part[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < m.n_rep) {
+        const int row = m.slot[static_cast<std::size_t>(r) * m.u.cap + u];
+        if (row >= 0) part[r] = *reinterpret_cast<const float4*>(m.dh[r] + static_cast<std::size_t>(row) * m.ld + f);
+      }
+    }
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < kMaxRep; ++r) {
+      if (r >= m.n_rep) break;
+      s.x += part[r].x;
+      s.y += part[r].y;
+      s.z += part[r].z;
+      s.w += part[r].w;
+    }
+    if (m.ug) *reinterpret_cast<float4*>(m.ug + static_cast<std::size_t>(u) * m.ld + f) = s;
+    adam4(w, mm, v, s, ks, err);
+    *reinterpret_cast<float4*>(a.m + at) = mm;
+    *reinterpret_cast<float4*>(a.v + at) = v;
+#pragma unroll
+    for (int r = 0; r < kMaxRep; ++r)
+      if (r < a.n_rep) *reinterpret_cast<float4*>(a.peer_w[r] + at) = w;
+  }
+  if (a.n_rep > 1) __threadfence_system();  // peers read their tables after the replica barrier
+}
+
 }  // namespace
+
+void replica_sum_adam(const ReplicaMerge& m, const ReplicaAdam& a, AdamHyper hp, std::uint32_t* err,
+                      cudaStream_t st) {
+  const unsigned grid = static_cast<unsigned>(
+      std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(m.u.cap * ceil_div(m.din, 64), 16), 16 * kNumSMs)));
+  launch_pdl(k_rsum_adam, grid, 256, 0, st, m, a, hp, err);
+}
 
 void bump_steps(const std::int64_t* const* steps, const int* const* counts, int n, cudaStream_t st) {
   if (n == 0) return;

@@ -570,6 +570,9 @@ void Engine::upload(const Graph& g) {
       x.ucount = static_cast<int*>(alloc(sizeof(int)));
       x.slot = static_cast<int*>(alloc(static_cast<std::size_t>(std::max(1, x.ucap)) * replica_group_.size() * 4));
       x.ug = static_cast<float*>(alloc(static_cast<std::size_t>(std::max(1, x.ucap)) * x.ld * 4));
+      x.utotal = static_cast<int*>(alloc(sizeof(int)));
+      x.peer_w.assign(replica_group_.size(), nullptr);
+      x.peer_w[replica_pos_] = tables_[x.t].w;
     }
     barrier_word_ = static_cast<float*>(alloc(16));
     peer_arena_.assign(replica_group_.size(), nullptr);
@@ -1100,9 +1103,11 @@ void Engine::run_replica_merge() {
         throw std::runtime_error("ncclAllReduce (replica weight gradients) failed");
     if (ncclGroupEnd() != ncclSuccess) throw std::runtime_error("ncclGroupEnd failed");
   });
-  // 2. learnable rows: union + ordered sums, then step and Adam on the union
-  AdamRowsBatch ab{};
-  int base = 0;
+  // 2. learnable rows: union + per-replica row slots, then step and the fused
+  //    ordered sum + Adam over the union
+  std::vector<ReplicaMerge> merges;
+  std::vector<const std::int64_t*> steps;
+  std::vector<const int*> ucounts;
   for (auto& x : xchg_) {
     ReplicaMerge m{};
     m.n_rep = static_cast<int>(peer_arena_.size());
@@ -1116,23 +1121,40 @@ void Engine::run_replica_merge() {
     m.u = {bits_ + word_base_[x.t], word_base_[x.t + 1] - word_base_[x.t], wscan_ + word_base_[x.t], x.ulist, x.ucount,
            x.ucap};
     m.slot = x.slot;
-    m.ug = x.ug;
+    m.ug = nullptr;
+    // sharded: this replica merges and Adam-updates only the ids of its shard and
+    // stores the new rows into every copy; unsharded: every replica updates the
+    // whole union in its own copy (measured faster on B200 at p=4, the default)
+    m.shard = shard_merge_ ? replica_pos_ : 0;
+    m.nshard = shard_merge_ ? m.n_rep : 1;
+    m.total = x.utotal;
     timed("replica_union", 0, [&] { replica_union(m, lb2_, st_); });  // lb_ belongs to the sampling stream
     timed("replica_slots", 0, [&] { replica_slots(m, st_); });
-    timed("replica_sum", 0, [&] { replica_sum(m, st_); });
-    const TypeTable& tb = tables_[x.t];
-    ab.t[ab.n] = {tb.w, tb.m, tb.v, tb.ld, x.ulist, x.ug, x.ld, x.ucount, tb.step};
-    ab.base4[ab.n] = base;
-    base += x.ucap * tb.ld / 4;
-    ++ab.n;
+    merges.push_back(m);
+    steps.push_back(tables_[x.t].step);
+    ucounts.push_back(x.utotal);  // the step moves iff the whole union is non-empty
   }
-  ab.total4 = base;
+  // each table's step += 1 iff its union is non-empty (hgnn.cpp:392-394)
+  bump_steps(steps.data(), ucounts.data(), static_cast<int>(steps.size()), st_);
+  timed("replica_adam", 0, [&] {
+    for (std::size_t i = 0; i < merges.size(); ++i) {
+      const TypeTable& tb = tables_[xchg_[i].t];
+      ReplicaAdam ra{tb.w, tb.m, tb.v, tb.ld, tb.step, {}, merges[i].n_rep};
+      if (shard_merge_) {
+        for (int r = 0; r < ra.n_rep; ++r) ra.peer_w[r] = xchg_[i].peer_w[r];
+      } else {
+        ra.n_rep = 1;
+        ra.peer_w[0] = tb.w;
+      }
+      replica_sum_adam(merges[i], ra, AdamHyper{}, err_, st_);
+    }
+  });
   {
     FeatSyncArgs fs{};
     fs.n_rep = static_cast<int>(peer_arena_.size());
     fs.elem = elem_bytes_;
     for (auto& x : xchg_) {
-      fs.ucount[fs.nt] = x.ucount;
+      fs.ucount[fs.nt] = x.utotal;
       for (int r = 0; r < fs.n_rep; ++r)
         fs.count[fs.nt][r] = reinterpret_cast<const int*>(peer_arena_[r] + x.off_count[bound_]);
       fs.dim[fs.nt] = tables_[x.t].dim;
@@ -1140,8 +1162,6 @@ void Engine::run_replica_merge() {
     }
     launch_pdl(k_feat_sync, 1, 1, 0, st_, fs, feat_sync_dev_);
   }
-  // bumps each table's step iff its union is non-empty
-  timed("replica_adam", 0, [&] { adam_rows(ab, AdamHyper{}, err_, st_); });
   // 3. nobody rewrites its arena (next step's sampling) before every peer read it
   timed("replica_barrier", 0, [&] {
     if (!counting_ && ncclAllReduce(barrier_word_, barrier_word_, 1, ncclFloat, ncclSum, rcomm_, st_) != ncclSuccess)
@@ -1152,12 +1172,18 @@ void Engine::run_replica_merge() {
 #endif
 }
 
+// IPC handles of this replica's exchange arena, then of its copy of every
+// exchanged learnable table (the sharded merge writes updated rows into them)
 std::vector<char> Engine::replica_handle() {
   if (replica_group_.size() < 2) return {};
-  cudaIpcMemHandle_t h;
-  HG_CUDA(cudaIpcGetMemHandle(&h, arena_));
-  std::vector<char> out(sizeof(h));
-  std::memcpy(out.data(), &h, sizeof(h));
+  std::vector<const void*> bases{arena_};
+  for (const auto& x : xchg_) bases.push_back(tables_[x.t].w);
+  std::vector<char> out(bases.size() * sizeof(cudaIpcMemHandle_t));
+  for (std::size_t i = 0; i < bases.size(); ++i) {
+    cudaIpcMemHandle_t h;
+    HG_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(bases[i])));
+    std::memcpy(out.data() + i * sizeof(h), &h, sizeof(h));
+  }
   return out;
 }
 
@@ -1167,14 +1193,19 @@ void Engine::attach_replicas(const std::vector<std::vector<char>>& handles_by_ra
   for (std::size_t r = 0; r < replica_group_.size(); ++r) {
     if (static_cast<int>(r) == replica_pos_) continue;
     const int q = replica_group_[r];
-    if (q >= static_cast<int>(handles_by_rank.size()) || handles_by_rank[q].size() != sizeof(cudaIpcMemHandle_t))
+    const std::size_t want = (1 + xchg_.size()) * sizeof(cudaIpcMemHandle_t);
+    if (q >= static_cast<int>(handles_by_rank.size()) || handles_by_rank[q].size() < want)
       throw std::invalid_argument("missing IPC handle of replica partition " + std::to_string(q));
-    cudaIpcMemHandle_t h;
-    std::memcpy(&h, handles_by_rank[q].data(), sizeof(h));
-    void* p = nullptr;
-    HG_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
-    ipc_opened_.push_back(p);
-    peer_arena_[r] = static_cast<const std::uint8_t*>(p);
+    auto open = [&](std::size_t i) {
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, handles_by_rank[q].data() + i * sizeof(h), sizeof(h));
+      void* p = nullptr;
+      HG_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      ipc_opened_.push_back(p);
+      return p;
+    };
+    peer_arena_[r] = static_cast<const std::uint8_t*>(open(0));
+    for (std::size_t i = 0; i < xchg_.size(); ++i) xchg_[i].peer_w[r] = static_cast<float*>(open(1 + i));
   }
   drop_graphs();
 }
@@ -1783,6 +1814,8 @@ bool Engine::read_tensor(const std::string& name, std::string& dtype, std::vecto
     if (name == p + ".ids") return u32s(f.list, dev_int(f.count));
     if (name == p + ".rows") return mat(c.dh, dev_int(f.count), c.din, c.ld);
   }
+  for (const auto& x : xchg_)  // replica groups: the merged union of the last step
+    if (name == "merge.t" + std::to_string(x.t) + ".union") return u32s(x.ulist, dev_int(x.ucount));
   for (int t = 0; t < ntypes_; ++t) {
     const TypeTable& tb = tables_[t];
     if (!tb.learnable) continue;

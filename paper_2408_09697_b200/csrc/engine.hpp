@@ -131,6 +131,12 @@ class Engine {
   }
   StepReport finish_step();  // waits for the last trained step and reads its report
   // payload element width of the accounting model (AccountingModel::elem_bytes, raf.hpp:15-19)
+  void set_shard_merge(bool on) {
+    if (on != shard_merge_) {
+      shard_merge_ = on;
+      drop_graphs();
+    }
+  }
   void set_elem_bytes(int b) {
     if (b != 2 && b != 4 && b != 8) throw std::invalid_argument("elem_bytes must be 2, 4 or 8");
     elem_bytes_ = b;
@@ -359,6 +365,7 @@ class Engine {
   // batch-invariant RAF bookkeeping of the whole plan (host, once)
   RafAccounting acct_;
   int elem_bytes_ = 4;
+  bool shard_merge_ = false;  // replica merge: each replica updates only its id shard
   int n_rel_ = 0;
   std::uint64_t model_sync_bytes() const;
   Readback* h_rb_ = nullptr;  // pinned, bound slot
@@ -427,6 +434,8 @@ class Engine {
     int ucap = 0;
     int* slot = nullptr;  // [n_rep x ucap]: row of union entry u in replica r (-1: absent)
     float* ug = nullptr;  // merged gradient rows [ucap x ld]
+    int* utotal = nullptr;  // size of the whole union (every shard)
+    std::vector<float*> peer_w;  // per group member: its copy of this table (self: ours)
   };
   std::vector<Xchg> xchg_;
   std::uint8_t* arena_ = nullptr;

@@ -569,67 +569,91 @@ __global__ void k_rmark(ReplicaMerge m) {
   }
 }
 
+// bits of word w whose id is in shard s of n (id % n == s)
+__device__ __forceinline__ std::uint32_t shard_mask(std::uint32_t w, int s, int n) {
+  if (n == 1) return 0xFFFFFFFFu;
+  std::uint32_t mask = 0;
+  const int o = static_cast<int>((static_cast<std::uint64_t>(w) * 32u) % static_cast<std::uint64_t>(n));
+  int first = s - o;  // first bit j with (o + j) % n == s
+  if (first < 0) first += n;
+  for (int j = first; j < 32; j += n) mask |= 1u << j;
+  return mask;
+}
+
 __global__ void k_rslot(ReplicaMerge m) {
   pdl_enter();
   const int r = blockIdx.y;
   const int n = *m.count[r];
   const std::uint32_t* ids = m.ids[r];
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    m.slot[static_cast<std::size_t>(r) * m.u.cap + bitmap_rank(m.u, ids[i])] = i;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const std::uint32_t id = ids[i];
+    if (static_cast<int>(id % static_cast<std::uint32_t>(m.nshard)) != m.shard) continue;
+    const std::uint32_t w = id >> 5;
+    const std::uint32_t bits = m.u.bits[w] & shard_mask(w, m.shard, m.nshard);
+    const std::uint32_t rank = m.u.wscan[w] - __popc(bits) + __popc(bits & ((1u << (id & 31)) - 1u));
+    m.slot[static_cast<std::size_t>(r) * m.u.cap + rank] = i;
+  }
 }
 
-// half-warp per (union row, 64-column chunk): ordered sum over replicas
-__global__ void __launch_bounds__(256) k_rsum(ReplicaMerge m) {
+// union compaction restricted to this shard's ids (rank structure over the
+// shard's bits) plus the size of the whole union
+__global__ void __launch_bounds__(kFrontThreads) k_shard_compact(ReplicaMerge m, LbLayout L,
+                                                                 unsigned long long* state, int* ticket) {
   pdl_enter();
-  const int hl = threadIdx.x & 15;
-  const int n = *m.u.count;
-  const int nch = (m.din + 63) / 64;
-  const int halves = gridDim.x * (blockDim.x >> 4);
-  for (int item = blockIdx.x * (blockDim.x >> 4) + (threadIdx.x >> 4); item < n * nch; item += halves) {
-    const int u = item / nch;
-    const int f = (item % nch) * 64 + 4 * hl;
-    if (f >= m.ld) continue;
-    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int r = 0; r < m.n_rep; ++r) {
-      const int row = m.slot[static_cast<std::size_t>(r) * m.u.cap + u];
-      if (row < 0) continue;
-      const float4 v = *reinterpret_cast<const float4*>(m.dh[r] + static_cast<std::size_t>(row) * m.ld + f);
-      s.x += v.x;
-      s.y += v.y;
-      s.z += v.z;
-      s.w += v.w;
-    }
-    *reinterpret_cast<float4*>(m.ug + static_cast<std::size_t>(u) * m.ld + f) = s;
+  __shared__ int s_tile;
+  __shared__ std::uint32_t s_prefix;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
+  __syncthreads();
+  const int t = s_tile;
+  if (t >= L.base[L.nseg]) return;
+  const BitmapType& T = m.u;
+  const int w = t * kFrontThreads + threadIdx.x;
+  const std::uint32_t all = w < T.words ? T.bits[w] : 0u;
+  const std::uint32_t mine = all & shard_mask(static_cast<std::uint32_t>(w), m.shard, m.nshard);
+  const std::uint32_t local = __popc(mine);
+  std::uint32_t tot;
+  const std::uint32_t incl = block_incl_scan<kFrontThreads>(local, &tot);
+  if (threadIdx.x < 32) {
+    const std::uint32_t p = lb_prefix(state, t, tot);
+    if (threadIdx.x == 0) s_prefix = p;
   }
+  // whole-union size: warp-aggregated popcounts
+  int c = __popc(all);
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(m.total, c);
+  __syncthreads();
+  if (w >= T.words) return;
+  std::uint32_t at = s_prefix + incl - local;
+  std::uint32_t b = mine;
+  while (b) {
+    const int q = __ffs(b) - 1;
+    b &= b - 1;
+    for (int r = 0; r < m.n_rep; ++r) m.slot[static_cast<std::size_t>(r) * T.cap + at] = -1;  // k_rslot fills
+    T.list[at++] = static_cast<std::uint32_t>(w) * 32u + static_cast<std::uint32_t>(q);
+  }
+  T.wscan[w] = at;
+  if (w == T.words - 1) *T.count = static_cast<int>(at);
 }
 
 }  // namespace
 
 void replica_union(const ReplicaMerge& m, LbScratch& lb, cudaStream_t st) {
   HG_CUDA(cudaMemsetAsync(m.u.bits, 0, static_cast<std::size_t>(m.u.words) * 4, st));
+  HG_CUDA(cudaMemsetAsync(m.total, 0, sizeof(int), st));
   const dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(m.u.cap, 256), 2 * kNumSMs)), m.n_rep);
   launch_pdl(k_rmark, grid, 256, 0, st, m);
-  FrontierArgs f{};
-  f.ntypes = 1;
-  f.t[0] = m.u;
-  frontier_compact(f, lb, st);
+  LbLayout L{};
+  L.nseg = 1;
+  L.base[0] = 0;
+  L.base[1] = static_cast<int>(ceil_div(std::max(1, m.u.words), kFrontThreads));
+  lb.reset(L.base[1], st);
+  launch_pdl(k_shard_compact, L.base[1], kFrontThreads, 0, st, m, L, lb.state, lb.ticket);
 }
 void replica_slots(const ReplicaMerge& m, cudaStream_t st) {
-  HG_CUDA(cudaMemsetAsync(m.slot, 0xFF, static_cast<std::size_t>(m.n_rep) * m.u.cap * sizeof(int), st));
+  // slots of this shard's union rows were reset to -1 by the compaction
   const dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(m.u.cap, 256), 2 * kNumSMs)), m.n_rep);
   launch_pdl(k_rslot, grid, 256, 0, st, m);
 }
-void replica_sum(const ReplicaMerge& m, cudaStream_t st) {
-  const unsigned g2 = static_cast<unsigned>(
-      std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(m.u.cap * ceil_div(m.din, 64), 16), 16 * kNumSMs)));
-  launch_pdl(k_rsum, g2, 256, 0, st, m);
-}
-void replica_merge(const ReplicaMerge& m, LbScratch& lb, cudaStream_t st) {
-  replica_union(m, lb, st);
-  replica_slots(m, st);
-  replica_sum(m, st);
-}
-
 // ---- cache / hotness counters -------------------------------------------------------------
 
 namespace {

@@ -264,15 +264,28 @@ struct ReplicaMerge {
   int n_rep;
   int ld;       // row stride of dh and ug
   int din;
-  BitmapType u; // union over the type's id space: list = union ids, count = union size
+  BitmapType u; // union over the type's id space: list/count/wscan = this shard's ids
   int* slot;    // [n_rep x u.cap]
   float* ug;    // [u.cap x ld] merged gradient rows
+  int shard, nshard;  // ids with id % nshard == shard are merged (and Adam-updated) here
+  int* total;         // size of the whole union (all shards)
 };
-void replica_merge(const ReplicaMerge& m, LbScratch& lb, cudaStream_t st);
-// its three stages: union (bitmap + compaction), per-replica row slots, ordered sums
+// stages: union (bitmap of every replica's ids, compaction of this shard's) and
+// per-replica row slots of the shard's union rows
 void replica_union(const ReplicaMerge& m, LbScratch& lb, cudaStream_t st);
 void replica_slots(const ReplicaMerge& m, cudaStream_t st);
-void replica_sum(const ReplicaMerge& m, cudaStream_t st);
+// ordered sum fused with the sparse Adam of the union rows (one pass instead of
+// sum -> ug -> adam_rows); ug is still written when m.ug is set (retained grads).
+// The table's step must already be bumped (bump_steps).
+struct ReplicaAdam {
+  float *w, *m, *v;
+  int ld_w;
+  const std::int64_t* step;
+  float* peer_w[kMaxRep];  // every replica's copy of the table (IPC-mapped; ours included)
+  int n_rep;
+};
+void replica_sum_adam(const ReplicaMerge& m, const ReplicaAdam& a, AdamHyper hp, std::uint32_t* err,
+                      cudaStream_t st);
 
 // ---- misc --------------------------------------------------------------------------------
 void zero_rows(float* p, int ld, const int* n_rows, int rows_cap, cudaStream_t st);

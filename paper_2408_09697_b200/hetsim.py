@@ -319,8 +319,8 @@ class Engine:
 
     def replica_handle(self) -> bytes:
         """CUDA IPC handle of this partition's gradient-exchange arena (b"" without replicas)."""
-        buf = C.create_string_buffer(128)
-        n = N.check(N.lib().hg_engine_replica_handle(self._h, buf, 128))
+        buf = C.create_string_buffer(4096)
+        n = N.check(N.lib().hg_engine_replica_handle(self._h, buf, 4096))
         return buf.raw[:n]
 
     def attach_replicas(self, handles: Sequence[bytes]):

@@ -32,6 +32,8 @@ def main():
         uid = open(id_path, "rb").read()
     if os.environ.get("HG_NO_GRAPHS"):
         eng.set_option("graphs", 0)
+    if os.environ.get("HG_SHARD_MERGE", "0") != "0":  # replica merge sharded by id (peer stores)
+        eng.set_option("shard_merge", 1)
     print(f"rank {rank}: attaching", flush=True)
     eng.attach_nccl(uid, p, rank)
     print(f"rank {rank}: attached", flush=True)

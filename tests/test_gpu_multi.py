@@ -24,8 +24,9 @@ def n_gpus():
         return 0
 
 
-@pytest.mark.parametrize("name,p", [("mag-mini", 2), ("mag-mini", 4), ("igb-mini", 4)])
-def test_raf_multi_gpu_matches_reference(ref, name, p):
+@pytest.mark.parametrize("name,p,shard", [("mag-mini", 2, 0), ("mag-mini", 4, 0), ("igb-mini", 4, 0),
+                                          ("mag-mini", 4, 1)])
+def test_raf_multi_gpu_matches_reference(ref, name, p, shard):
     # p = 4 > 3 sub-metatrees: one sub-metatree is replicated, its replicas split
     # the batch and synchronise weight gradients (NCCL) and learnable rows
     # (peer-mapped merge) before Adam
@@ -36,7 +37,8 @@ def test_raf_multi_gpu_matches_reference(ref, name, p):
         idp = os.path.join(td, "nccl.id")
         procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "mp", "raf_rank.py"), name, str(seed), str(p),
                                    str(r), idp, os.path.join(td, f"r{r}.npz"), str(n_batches), str(bsz)],
-                                  stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True) for r in range(p)]
+                                  stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True,
+                                  env=dict(os.environ, HG_SHARD_MERGE=str(shard))) for r in range(p)]
         outs = [pr.communicate(timeout=300)[0] for pr in procs]
         for pr, o in zip(procs, outs):
             assert pr.returncode == 0, o[-3000:]
