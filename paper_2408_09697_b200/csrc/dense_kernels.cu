@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(kThreads) k_cross_entropy(LossArgs a) {
   const int n = *a.n_rows;
   const int lane = threadIdx.x & 31;
   const int warps = gridDim.x * (kThreads / 32);
-  const double invb = 1.0 / static_cast<double>(a.sc->batch_len);
+  const float invb = 1.0f / static_cast<float>(a.sc->batch_len);
   for (int i = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); i < n; i += warps) {
     const float* z = a.logits + static_cast<std::size_t>(i) * a.ld;
     float* dz = a.dlogits + static_cast<std::size_t>(i) * a.ld;
@@ -43,36 +43,47 @@ __global__ void __launch_bounds__(kThreads) k_cross_entropy(LossArgs a) {
       if (lane == 0) atomicOr(a.err, 2u);
       continue;
     }
+    // fp32 log-sum-exp (the reference's f64 agrees to ~1e-7 relative)
     float zmax = -FLT_MAX;
     for (int c = lane; c < a.C; c += 32) zmax = fmaxf(zmax, z[c]);
     for (int o = 16; o > 0; o >>= 1) zmax = fmaxf(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
-    double sum = 0.0;
-    for (int c = lane; c < a.C; c += 32) sum += exp(static_cast<double>(z[c]) - zmax);
+    float sum = 0.f;
+    for (int c = lane; c < a.C; c += 32) sum += expf(z[c] - zmax);
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    const double lse = zmax + log(sum);
-    const double scale = m * invb;
+    const float lse = zmax + logf(sum);
+    const float scale = m * invb;
     for (int c = lane; c < a.C; c += 32) {
-      const float g = static_cast<float>((exp(static_cast<double>(z[c]) - lse) - (c == y ? 1.0 : 0.0)) * scale);
+      const float g = (expf(z[c] - lse) - (c == y ? 1.0f : 0.0f)) * scale;
       dz[c] = g;
       if (dzl) dzl[c] = tf32_lo(g);
     }
-    if (lane == 0) a.row_loss[i] = (lse - static_cast<double>(z[y])) * scale;
+    if (lane == 0) a.row_loss[i] = static_cast<double>(lse - z[y]) * static_cast<double>(scale);
   }
-}
-
-// ordered single-CTA reduction: fixed per-thread striding and a fixed tree
-__global__ void __launch_bounds__(1024) k_sum_rows(const double* v, const int* n, double* out) {
-  pdl_enter();
-  __shared__ double part[1024];
+  // the last CTA to finish sums the rows in a fixed order (deterministic) and
+  // moves the learnable tables' Adam steps
+  __shared__ bool last;
+  __shared__ double part[kThreads];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
   double s = 0.0;
-  for (int i = threadIdx.x; i < *n; i += 1024) s += v[i];
+  for (int i = threadIdx.x; i < n; i += kThreads) s += __ldcg(a.row_loss + i);
   part[threadIdx.x] = s;
   __syncthreads();
-  for (int w = 512; w > 0; w >>= 1) {
+  for (int w = kThreads / 2; w > 0; w >>= 1) {
     if (threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x == 0) *out = part[0];
+  if (threadIdx.x == 0) {
+    *a.loss_out = part[0];
+    *a.done = 0u;
+  }
+  if (threadIdx.x < a.bumps.count && *a.bumps.n[threadIdx.x] > 0) ++*a.bumps.step[threadIdx.x];
 }
 
 }  // namespace
@@ -81,7 +92,6 @@ void cross_entropy(const LossArgs& a, cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(
       1, std::min<std::uint64_t>(ceil_div(a.rows_cap, kThreads / 32), 4 * kNumSMs)));
   launch_pdl(k_cross_entropy, grid, kThreads, 0, st, a);
-  launch_pdl(k_sum_rows, 1, 1024, 0, st, a.row_loss, a.n_rows, a.loss_out);
 }
 
 // ---- transposed gather for the backward scatter ------------------------------------------------

@@ -2,6 +2,7 @@
 #include "engine.hpp"
 #include "gemm.cuh"
 
+#include <cstdio>
 #include <algorithm>
 #include <cstring>
 #include <functional>
@@ -143,9 +144,14 @@ Engine::Engine(const Graph& g, const EngineOptions& o) : o_(o) {
   if (static_cast<int>(o.fanouts.size()) != o.k) throw std::invalid_argument("fanout count must equal the model depth");
   if (o.k < 1) throw std::invalid_argument("fanouts must be non-empty");
   HG_CUDA(cudaSetDevice(o.device));
-  HG_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
-  HG_CUDA(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking));
-  HG_CUDA(cudaStreamCreateWithFlags(&st_s_, cudaStreamNonBlocking));
+  // the sampling stream (batch i+1) gets the highest priority so that its
+  // latency-bound chain is never starved by the bandwidth-bound training
+  // kernels (measured +1%; prioritising training instead costs 6%)
+  int least = 0, greatest = 0;
+  HG_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  HG_CUDA(cudaStreamCreateWithPriority(&st_, cudaStreamNonBlocking, least));
+  HG_CUDA(cudaStreamCreateWithPriority(&st2_, cudaStreamNonBlocking, least));
+  HG_CUDA(cudaStreamCreateWithPriority(&st_s_, cudaStreamNonBlocking, greatest));
   for (int sl = 0; sl < 2; ++sl) {
     HG_CUDA(cudaEventCreateWithFlags(&ev_sampled_[sl], cudaEventDisableTiming));
     HG_CUDA(cudaEventCreateWithFlags(&ev_trained_[sl], cudaEventDisableTiming));
@@ -682,6 +688,7 @@ void Engine::upload(const Graph& g) {
   HG_CUDA(cudaMallocHost(&h_tsc_, sizeof(StepScalars)));
   std::memset(h_tsc_, 0, sizeof(StepScalars));
   row_loss_ = static_cast<double*>(alloc(static_cast<std::size_t>(o_.batch_cap) * 8));
+  loss_done_ = static_cast<unsigned*>(alloc(sizeof(unsigned)));
   cache_hm_ = static_cast<unsigned long long*>(alloc(sizeof(unsigned long long) * 2 * ntypes_));
   alg_bytes_ = static_cast<double*>(alloc(sizeof(double) * 4));
   cache_types_.assign(ntypes_, false);
@@ -1008,8 +1015,19 @@ void Engine::run_forward() {
   }
 }
 
-void Engine::run_loss() {
+void Engine::run_loss(bool train) {
   LossArgs la{};
+  la.done = loss_done_;
+  if (train) {
+    // learnable layer-0 tables advance their Adam step before the fused row
+    // update of the backward pass; the loss kernel's last CTA does it
+    for (const auto& c : cscs_)
+      if (c.hop == o_.k && tables_[c.src_t].learnable && !xchg_type(c.src_t) && la.bumps.count < kMaxSegs) {
+        la.bumps.step[la.bumps.count] = tables_[c.src_t].step;
+        la.bumps.n[la.bumps.count] = front(o_.k, c.src_t).count;
+        ++la.bumps.count;
+      }
+  }
   la.logits = logits_;
   la.ld = ldc_;
   la.C = num_classes_;
@@ -1029,17 +1047,10 @@ void Engine::run_loss() {
 
 void Engine::run_backward() {
   const int k = o_.k;
-  // learnable layer-0 tables advance their Adam step before the fused row update
-  {
-    std::vector<const std::int64_t*> steps;
-    std::vector<const int*> counts;
-    for (const auto& c : cscs_)
-      if (c.hop == k && tables_[c.src_t].learnable && !xchg_type(c.src_t)) {
-        steps.push_back(tables_[c.src_t].step);
-        counts.push_back(front(k, c.src_t).count);
-      }
-    bump_steps(steps.data(), counts.data(), static_cast<int>(steps.size()), st_);
-  }
+  // (the layer-0 tables' steps were bumped by the loss kernel.) Every slot's weight
+  // gradient is overwritten by its reduction; the zeroing below is kept because
+  // it delays the side-stream weight gradients behind the critical mean-gradient
+  // chain (measured: 1.89G vs 1.77G sampled-edges/s without it)
   for (auto& s : slots_) HG_CUDA(cudaMemsetAsync(s.g, 0, static_cast<std::size_t>(std::max(1, s.din)) * s.ld * 4, st_));
 
   for (int l = k; l >= 1; --l) {
@@ -1295,7 +1306,7 @@ void Engine::train_body(bool train) {
   fork_used_ = 0;
   side_open_ = false;
   run_forward();
-  run_loss();
+  run_loss(train);
   if (train) {
     run_backward();
     run_update();
@@ -1322,7 +1333,7 @@ void capture(cudaGraphExec_t& ex, cudaStream_t st, F&& body) {
     throw;
   }
   HG_CUDA(cudaStreamEndCapture(st, &graph));
-  HG_CUDA(cudaGraphInstantiate(&ex, graph, 0));
+  HG_CUDA(cudaGraphInstantiate(&ex, graph, cudaGraphInstantiateFlagUseNodePriority));
   cudaGraphDestroy(graph);
 }
 }  // namespace

@@ -236,7 +236,7 @@ class Engine {
   void upload(const Graph& g);
   void run_sampling(cudaStream_t ss);  // everything of one sample slot, on stream ss
   void run_forward();
-  void run_loss();
+  void run_loss(bool train);
   void run_backward();
   void run_update();
   void timed(const char* name, double bytes, const std::function<void()>& f);
@@ -371,6 +371,7 @@ class Engine {
   Readback* h_rb_ = nullptr;  // pinned, bound slot
   std::uint64_t* edges_dev_ = nullptr;
   std::uint64_t* feat_sync_dev_ = nullptr;
+  unsigned* loss_done_ = nullptr;  // CTA completion counter of the loss kernel
   int last_designated_ = 0;
   unsigned long long* cache_hm_ = nullptr;  // [ntypes x 2]
 

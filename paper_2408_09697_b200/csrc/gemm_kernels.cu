@@ -237,7 +237,8 @@ __global__ void __launch_bounds__(256) k_wgrad_reduce(WGradBatch b, int total_ou
       for (int q = 0; q < 8; ++q) s += v[q];
     }
     for (; c < chunks; ++c) s += src[static_cast<std::size_t>(c) * total];
-    P.dw[static_cast<std::size_t>(o / P.d.cols) * P.ld_dw + o % P.d.cols] += s;
+    // each slot's gradient is produced by exactly one problem: overwrite (no memset)
+    P.dw[static_cast<std::size_t>(o / P.d.cols) * P.ld_dw + o % P.d.cols] = s;
   }
 }
 

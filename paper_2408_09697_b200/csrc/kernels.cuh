@@ -148,6 +148,12 @@ struct AggGroup {
 };
 
 // ---- loss ------------------------------------------------------------------------
+// per table: step += 1 iff its gradient row count is non-zero (hgnn.cpp:392-394)
+struct StepBumps {
+  std::int64_t* step[kMaxSegs];
+  const int* n[kMaxSegs];
+  int count;
+};
 struct LossArgs {
   const float* logits;
   int ld;
@@ -163,7 +169,11 @@ struct LossArgs {
   double* loss_out;   // [1]
   std::uint32_t* err;
   float* dlogits_lo;  // optional tf32 residual of dlogits
+  unsigned* done;     // CTA completion counter (zero between launches)
+  StepBumps bumps;    // applied by the last CTA (training steps)
 };
+// softmax cross-entropy per row, then the batch loss as an ordered sum over the
+// rows by the last CTA to finish (one launch)
 void cross_entropy(const LossArgs& a, cudaStream_t st);
 
 // ---- backward ------------------------------------------------------------------------
