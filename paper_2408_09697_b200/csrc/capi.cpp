@@ -555,6 +555,8 @@ int hg_engine_set_option(hg_engine* e, const char* name, int value) {
       e->e->set_umma(value != 0);
     else if (n == "elem_bytes")
       e->e->set_elem_bytes(value);
+    else if (n == "trace_sampler")
+      e->e->set_trace_sampler(value != 0);
     else if (n == "shard_merge")
       e->e->set_shard_merge(value != 0);
     else

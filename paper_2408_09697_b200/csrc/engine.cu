@@ -883,6 +883,11 @@ void Engine::run_sampling(cudaStream_t ss) {
     }
     // frontier[h-1]'s bitmap is dead once its relabel / transposed views are enqueued
     HG_CUDA(cudaMemsetAsync(bits_, 0, static_cast<std::size_t>(total_words_) * 4, ss));
+    if (trace_sampler_) {  // diagnostics: per-tile timestamps of this hop's sampler
+      if (!sample_trace_[h]) sample_trace_[h] = static_cast<unsigned long long*>(alloc(static_cast<std::size_t>(lb_.cap) * 64));
+      HG_CUDA(cudaMemsetAsync(sample_trace_[h], 0, static_cast<std::size_t>(lb_.cap) * 64, ss));
+      sh.trace = sample_trace_[h];
+    }
     timed("sample", 0, [&] { sample_hop(sh, d_sc_, slow_, n_slow_, mt_scratch_, lb_, ss); });
     if (csc_region_[h].words) {
       HG_CUDA(cudaMemsetAsync(csc_region_[h].offs, 0, csc_region_[h].words * 4, ss));
@@ -1825,6 +1830,15 @@ bool Engine::read_tensor(const std::string& name, std::string& dtype, std::vecto
     if (name == p + ".ids") return u32s(f.list, dev_int(f.count));
     if (name == p + ".rows") return mat(c.dh, dev_int(f.count), c.din, c.ld);
   }
+  for (int h = 1; h <= o_.k && h < 8; ++h)
+    if (sample_trace_[h] && name == "trace.sample.h" + std::to_string(h)) {
+      std::vector<unsigned long long> v(static_cast<std::size_t>(lb_.cap) * 8);
+      HG_CUDA(cudaMemcpy(v.data(), sample_trace_[h], v.size() * 8, cudaMemcpyDeviceToHost));
+      dtype = "<u8";
+      shape = {static_cast<long long>(lb_.cap), 8};
+      put(data, v);
+      return true;
+    }
   for (const auto& x : xchg_)  // replica groups: the merged union of the last step
     if (name == "merge.t" + std::to_string(x.t) + ".union") return u32s(x.ulist, dev_int(x.ucount));
   for (int t = 0; t < ntypes_; ++t) {

@@ -131,6 +131,10 @@ class Engine {
   }
   StepReport finish_step();  // waits for the last trained step and reads its report
   // payload element width of the accounting model (AccountingModel::elem_bytes, raf.hpp:15-19)
+  void set_trace_sampler(bool on) {
+    trace_sampler_ = on;
+    drop_graphs();
+  }
   void set_shard_merge(bool on) {
     if (on != shard_merge_) {
       shard_merge_ = on;
@@ -366,6 +370,8 @@ class Engine {
   RafAccounting acct_;
   int elem_bytes_ = 4;
   bool shard_merge_ = false;  // replica merge: each replica updates only its id shard
+  bool trace_sampler_ = false;  // diagnostics: per-tile sampler timestamps
+  unsigned long long* sample_trace_[8] = {};
   int n_rel_ = 0;
   std::uint64_t model_sync_bytes() const;
   Readback* h_rb_ = nullptr;  // pinned, bound slot

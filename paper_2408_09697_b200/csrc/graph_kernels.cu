@@ -159,48 +159,57 @@ namespace {
 constexpr int kSampleThreads = 256;
 constexpr int kSlowThreads = 4096;  // concurrent slow-path rows (global scratch)
 
-// Partial Fisher-Yates over [0, deg) with a sparse map of displaced positions
-// (sampling.cpp:29-37 keeps a dense O(deg) index array). Position p holds p
-// unless overridden; position i is final once drawn, so only the j side needs
-// remembering. The map is a per-lane list in shared memory laid out
-// [slot][lane] (conflict-free), O(1) insert; a 64-bit filter of the inserted
-// positions lets most lookups skip the scan. Returns false if the streaming
-// engine ran dry (the caller replays the row on MtFull).
-template <int MAXF, typename Eng>
-__device__ __forceinline__ bool draw_positions_smem(Eng& eng, std::uint64_t deg, int fanout, std::uint32_t* out,
-                                                    std::uint32_t* mpos, std::uint32_t* mval) {
-  // mpos/mval point at this lane's column: element q at [q * kSampleThreads]
-  unsigned long long filt = 0ull;
-  int nmap = 0;
-  for (int i = 0; i < fanout; ++i) {
-    std::uint64_t off;
-    if (!lemire(eng, deg - static_cast<std::uint64_t>(i), off)) return false;
-    const std::uint32_t ii = static_cast<std::uint32_t>(i);
-    const std::uint32_t jpos = static_cast<std::uint32_t>(i + off);
-    std::uint32_t vi = ii, vj = jpos;
-    int slot_j = -1;
-    const bool maybe_i = (filt >> (ii & 63u)) & 1ull, maybe_j = (filt >> (jpos & 63u)) & 1ull;
-    if (maybe_i || maybe_j) {
-      for (int q = 0; q < nmap; ++q) {
-        const std::uint32_t pq = mpos[q * kSampleThreads];
-        if (pq == ii) vi = mval[q * kSampleThreads];
-        if (pq == jpos) {
-          vj = mval[q * kSampleThreads];
-          slot_j = q;
-        }
-      }
+// Same draws with the dependency chain cut short. The mt19937_64 outputs
+// j < fanout need only x[j], x[j+1] and x[j+156] of the seeding recurrence
+// (first twist), so after the 156-step seeding two independent step chains
+// produce all outputs; each output's Lemire offset depends only on it and on
+// deg - i (assuming no rejection: a product below the range, probability
+// ~deg/2^64, sends the row to the exact slow path). The partial Fisher-Yates
+// is then resolved per draw without sequential swaps: the value at position p
+// before swap i is p unless an earlier swap k < i moved position k onto p
+// (j_k == p, the latest such k), in which case it is the value position k held
+// before swap k (sampling.cpp:28-37). jcol: this lane's column of MAXF words.
+template <int MAXF>
+__device__ __forceinline__ bool draw_positions_fast(std::uint64_t seed, std::uint64_t deg, int fanout,
+                                                    std::uint32_t* out) {
+  std::uint64_t xa = seed, xa1 = Mt64::step(seed, 1), xb = xa1;
+#pragma unroll 4
+  for (std::uint32_t i = 2; i <= 156; ++i) xb = Mt64::step(xb, i);
+  bool exact = true;
+  std::uint32_t jr[MAXF];  // j_q = q + offset_q, in registers (the loops below are unrolled)
+#pragma unroll
+  for (int q = 0; q < MAXF; ++q) {
+    jr[q] = 0xFFFFFFFFu;
+    if (q < fanout) {
+      const std::uint64_t t = Mt64::temper(Mt64::twist(xa, xa1, xb));
+      const std::uint64_t range = deg - static_cast<std::uint64_t>(q);
+      exact &= t * range >= range;  // otherwise Lemire may reject: replay exactly
+      jr[q] = static_cast<std::uint32_t>(q + __umul64hi(t, range));
+      xa = xa1;
+      xa1 = Mt64::step(xa1, static_cast<std::uint32_t>(q) + 2u);
+      xb = Mt64::step(xb, static_cast<std::uint32_t>(q) + 157u);
     }
-    if (jpos != ii) {
-      if (slot_j < 0) {
-        slot_j = nmap++;
-        mpos[slot_j * kSampleThreads] = jpos;
-        filt |= 1ull << (jpos & 63u);
-      }
-      mval[slot_j * kSampleThreads] = vi;
-    }
-    out[i] = vj;  // position in the CSR row; the warp gathers the ids afterwards
   }
-  (void)MAXF;
+  if (!exact) return false;
+#pragma unroll
+  for (int i = 0; i < MAXF; ++i) {
+    if (i < fanout) {
+      std::uint32_t p = jr[i];
+      int found = -1;  // latest earlier swap that moved a position onto p
+#pragma unroll
+      for (int q = 0; q < i; ++q)
+        if (jr[q] == p) found = q;
+      while (found >= 0) {  // rare: follow the chain of displaced positions
+        const int k = found;
+        p = static_cast<std::uint32_t>(k);
+        found = -1;
+#pragma unroll
+        for (int q = 0; q < MAXF; ++q)
+          if (q < k && jr[q] == p) found = q;
+      }
+      out[i] = p;  // position in the CSR row; the warp gathers the ids afterwards
+    }
+  }
   return true;
 }
 
@@ -245,7 +254,6 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_fused(SampleHop h, Lb
   pdl_enter();
   __shared__ int s_tile;
   __shared__ std::uint32_t s_prefix;
-  extern __shared__ std::uint32_t s_map[];  // 2 * MAXF * kSampleThreads words (dynamic)
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
   __syncthreads();
   const int tk = s_tile;
@@ -256,6 +264,8 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_fused(SampleHop h, Lb
   const int n = *b.n_rows;
   const int base = t * kSampleThreads;
   if (base >= n) return;
+  unsigned long long t0 = 0;
+  if (h.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   const int i = base + threadIdx.x;
   const bool live = i < n;
   const std::uint64_t fo = static_cast<std::uint64_t>(h.fanout);
@@ -277,6 +287,8 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_fused(SampleHop h, Lb
   const std::uint32_t o = s_prefix + incl - cnt;
   if (live) b.indptr[i + 1] = o + cnt;
   if (i == 0) b.indptr[0] = 0;
+  unsigned long long t1 = 0;
+  if (h.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
 
   // Phase 1 — RNG rows (deg > fanout): one lane per row runs the exact
   // mt19937_64 + Lemire + partial Fisher-Yates and records the drawn CSR
@@ -286,10 +298,8 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_fused(SampleHop h, Lb
   if (live && deg > fo) {
     if (h.fanout <= MAXF) {
       const std::uint64_t rel_key = (static_cast<std::uint64_t>(h.hop) << 32) | static_cast<std::uint64_t>(b.rel);
-      MtStream eng;
-      eng.seed(dmix_seed(sc->rng_seed, dmix_seed(rel_key, d)));
-      rng_ok = draw_positions_smem<MAXF>(eng, deg, h.fanout, b.src_ids + o, s_map + threadIdx.x,
-                                         s_map + MAXF * kSampleThreads + threadIdx.x);
+      rng_ok = draw_positions_fast<MAXF>(dmix_seed(sc->rng_seed, dmix_seed(rel_key, d)), deg, h.fanout,
+                                         b.src_ids + o);
     }
     if (!rng_ok) {
       const int q = atomicAdd(n_slow, 1);
@@ -298,6 +308,20 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_fused(SampleHop h, Lb
     }
   }
   __syncwarp();
+  if (h.trace) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t2, smid;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(*reinterpret_cast<unsigned*>(&smid)));
+      unsigned long long* r = h.trace + static_cast<std::size_t>(tk) * 8;
+      r[0] = t0;
+      r[1] = t1;
+      r[2] = t2;
+      r[4] = static_cast<unsigned long long>(bi);
+      r[5] = smid & 0xffffffffull;
+    }
+  }
 
   // Phase 2 — warp-flattened gather: the warp's 32 consecutive rows own one
   // contiguous output range, so lane l takes edges q = l, l+32, ... (row found
@@ -362,6 +386,14 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_fused(SampleHop h, Lb
         if (ok[u]) atomicOr(b.mark_bits + (val[u] >> 5), 1u << (val[u] & 31));
     }
   }
+  if (h.trace) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t3;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t3));
+      h.trace[static_cast<std::size_t>(tk) * 8 + 3] = t3;
+    }
+  }
 }
 
 __global__ void __launch_bounds__(128) k_sample_slow(SampleHop h, const StepScalars* sc,
@@ -408,18 +440,10 @@ void sample_hop(const SampleHop& h, const StepScalars* sc, std::uint32_t* slow, 
   L.base[h.nblk] = tiles;
   lb.reset(tiles, st);
   HG_CUDA(cudaMemsetAsync(n_slow, 0, sizeof(int), st));
-  // the shared-memory map holds up to MAXF displaced positions per lane
-  static bool attr_set = false;
-  const int smem16 = 2 * 16 * kSampleThreads * 4, smem32 = 2 * 32 * kSampleThreads * 4;
-  if (!attr_set) {
-    HG_CUDA(cudaFuncSetAttribute(k_sample_fused<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem16));
-    HG_CUDA(cudaFuncSetAttribute(k_sample_fused<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem32));
-    attr_set = true;
-  }
   if (h.fanout <= 16)
-    launch_pdl(k_sample_fused<16>, tiles, kSampleThreads, smem16, st, h, L, sc, lb.state, lb.ticket, slow, n_slow);
+    launch_pdl(k_sample_fused<16>, tiles, kSampleThreads, 0, st, h, L, sc, lb.state, lb.ticket, slow, n_slow);
   else
-    launch_pdl(k_sample_fused<32>, tiles, kSampleThreads, smem32, st, h, L, sc, lb.state, lb.ticket, slow, n_slow);
+    launch_pdl(k_sample_fused<32>, tiles, kSampleThreads, 0, st, h, L, sc, lb.state, lb.ticket, slow, n_slow);
   launch_pdl(k_sample_slow, kSlowThreads / 128, 128, 0, st, h, sc, slow, n_slow, scratch);
 }
 

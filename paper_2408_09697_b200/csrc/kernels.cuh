@@ -74,6 +74,9 @@ struct SampleHop {
   int nblk;
   int fanout;
   int hop;
+  // diagnostics (null normally): per tile [start, scanned, drawn, end] %globaltimer
+  // ns, the segment, and the SM
+  unsigned long long* trace;
 };
 // One pass per hop: per-row counts min(fanout, deg), the block offsets (single-pass
 // scan) and the draws (exact mt19937_64 + Lemire + partial Fisher-Yates). Rows
