@@ -285,14 +285,26 @@ def run_b200(args):
     # is reported beside them, not as the roofline kernel.
     alg_by = {"aggregate": alg[1], "csc_gather": alg[3], "aggregate_top": alg[2], "sample": alg[0]}
 
+    def traffic_of(k):
+        # DRAM bytes per launch of the roofline kernel from the committed ncu --set
+        # full capture (profiles/r01_traffic.json); ncu is never run inside the bench
+        try:
+            with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+                return int(json.load(f)[k]["dram_bytes_per_launch"])
+        except Exception:
+            return None
+
     def roof_of(k):
         pl_bytes = alg_by[k] / max(1, launches_by.get(k, 1))
         pl_ms = classes.get(k, 0.0) / max(1, launches_by.get(k, 1))
         ach = pl_bytes / (pl_ms / 1000.0) / 1e9 if pl_ms > 0 else 0.0
         return {"achieved": ach, "frac": ach / peak_hbm, "alg_bytes_per_launch": pl_bytes, "ms_per_launch": pl_ms,
+                "traffic": traffic_of(k),
                 "share": classes.get(k, 0.0) / max(1e-9, sum(classes.values()))}
 
     peak_hbm = load_peaks()[0]
+
+
     roof_kernel = max(("aggregate", "csc_gather"), key=lambda k: classes.get(k, 0.0))
     r0 = roof_of(roof_kernel)
     per_launch_bytes, per_launch_ms, achieved = r0["alg_bytes_per_launch"], r0["ms_per_launch"], r0["achieved"]
@@ -311,13 +323,12 @@ def run_b200(args):
         "e2e": {"value": e2e_value, "unit": "edges/s", "h2d_bytes_per_step": 4 * batch + 32,
                 "d2h_bytes_per_step": 24, "ms_per_step": 1000.0 * e2e_s / args.steps},
         "roofline": {"bound": "hbm", "kernel": roof_kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "frac": achieved / peak, "traffic": traffic_of(roof_kernel), "traffic_source": "profiles/r01_traffic.json (ncu --set full)", "peak_kind": peak_kind,
                      "alg_bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms,
                      "kernels": {k: roof_of(k) for k in alg_by}},
         "kernel_share": {k: v / max(1e-9, sum(classes.values())) for k, v in sorted(classes.items())},
         # eager profiled pass (events around every kernel class, rank 0): device us per step
         "kernel_us_per_step": {k: round(v * 1000.0 / prof_steps, 2) for k, v in sorted(classes.items())},
-        "kernel_us_per_step_eager": {k: 1000.0 * v / prof_steps for k, v in sorted(classes.items())},
         "final_loss": loss,
         "setup_s": {"graph_gen": t_gen},
     }
