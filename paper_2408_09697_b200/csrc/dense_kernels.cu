@@ -352,6 +352,7 @@ __global__ void k_bump_list(BumpArgs a) {
 // summed in replica order (hgnn.cpp:83-113 accumulate), then Adam on the table
 // row (hgnn.cpp:392-410). The shard owns the row's m / v; its new w is stored
 // into every replica's copy of the table (NVLink stores to the peers).
+template <int R>  // replicas in the group (register footprint: R float4 partials)
 __global__ void __launch_bounds__(256) k_rsum_adam(ReplicaMerge m, ReplicaAdam a, AdamHyper hp,
                                                    std::uint32_t* err) {
   pdl_enter();
@@ -366,23 +367,23 @@ __global__ void __launch_bounds__(256) k_rsum_adam(ReplicaMerge m, ReplicaAdam a
     const int u = item / nch;
     const int f = (item % nch) * 64 + 4 * hl;
     if (f >= m.ld) continue;
+    // independent loads first: the replicas' row slots and the union id, then the
+    // replicas' gradient rows (peers over NVLink) and the table row state
+    int rows[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) rows[r] = r < m.n_rep ? m.slot[static_cast<std::size_t>(r) * m.u.cap + u] : -1;
     const std::size_t at = static_cast<std::size_t>(m.u.list[u]) * a.ld_w + f;
+    float4 part[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      part[r] = rows[r] >= 0 ? *reinterpret_cast<const float4*>(m.dh[r] + static_cast<std::size_t>(rows[r]) * m.ld + f)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
     float4 w = *reinterpret_cast<const float4*>(a.w + at);
     float4 mm = *reinterpret_cast<const float4*>(a.m + at);
     float4 v = *reinterpret_cast<const float4*>(a.v + at);
-    float4 part[kMaxRep];
-#pragma unroll
-    for (int r = 0; r < kMaxRep; ++r) {
-      part[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (r < m.n_rep) {
-        const int row = m.slot[static_cast<std::size_t>(r) * m.u.cap + u];
-        if (row >= 0) part[r] = *reinterpret_cast<const float4*>(m.dh[r] + static_cast<std::size_t>(row) * m.ld + f);
-      }
-    }
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int r = 0; r < kMaxRep; ++r) {
-      if (r >= m.n_rep) break;
+    for (int r = 0; r < R; ++r) {  // replica order
       s.x += part[r].x;
       s.y += part[r].y;
       s.z += part[r].z;
@@ -393,7 +394,7 @@ __global__ void __launch_bounds__(256) k_rsum_adam(ReplicaMerge m, ReplicaAdam a
     *reinterpret_cast<float4*>(a.m + at) = mm;
     *reinterpret_cast<float4*>(a.v + at) = v;
 #pragma unroll
-    for (int r = 0; r < kMaxRep; ++r)
+    for (int r = 0; r < R; ++r)
       if (r < a.n_rep) *reinterpret_cast<float4*>(a.peer_w[r] + at) = w;
   }
   if (a.n_rep > 1) __threadfence_system();  // peers read their tables after the replica barrier
@@ -405,7 +406,13 @@ void replica_sum_adam(const ReplicaMerge& m, const ReplicaAdam& a, AdamHyper hp,
                       cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>(
       std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(m.u.cap * ceil_div(m.din, 64), 16), 16 * kNumSMs)));
-  launch_pdl(k_rsum_adam, grid, 256, 0, st, m, a, hp, err);
+  switch (m.n_rep) {
+    case 1: launch_pdl(k_rsum_adam<1>, grid, 256, 0, st, m, a, hp, err); break;
+    case 2: launch_pdl(k_rsum_adam<2>, grid, 256, 0, st, m, a, hp, err); break;
+    case 3: launch_pdl(k_rsum_adam<3>, grid, 256, 0, st, m, a, hp, err); break;
+    case 4: launch_pdl(k_rsum_adam<4>, grid, 256, 0, st, m, a, hp, err); break;
+    default: launch_pdl(k_rsum_adam<kMaxRep>, grid, 256, 0, st, m, a, hp, err); break;
+  }
 }
 
 void bump_steps(const std::int64_t* const* steps, const int* const* counts, int n, cudaStream_t st) {
