@@ -5,7 +5,11 @@
 #include <cmath>
 #include <numeric>
 #include <random>
+#include <atomic>
+#include <exception>
+#include <functional>
 #include <set>
+#include <thread>
 
 namespace hetgpu {
 
@@ -30,6 +34,30 @@ bool contains(const std::vector<T>& v, const T& x) {
 
 // Counting-sort the pairs of one relation into dst-major order, keeping the
 // insertion order inside every destination row.
+// Runs independent tasks on up to hardware_concurrency host threads; the first
+// exception (in task order) is rethrown after all tasks finish.
+void run_parallel(std::vector<std::function<void()>>& tasks) {
+  const std::size_t nthreads =
+      std::max<std::size_t>(1, std::min<std::size_t>(tasks.size(), std::thread::hardware_concurrency()));
+  std::vector<std::exception_ptr> errs(tasks.size());
+  std::atomic<std::size_t> next{0};
+  auto worker = [&] {
+    for (std::size_t i = next++; i < tasks.size(); i = next++) {
+      try {
+        tasks[i]();
+      } catch (...) {
+        errs[i] = std::current_exception();
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (std::size_t t = 1; t < nthreads; ++t) pool.emplace_back(worker);
+  worker();
+  for (auto& t : pool) t.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
+
 Adjacency dst_major(std::uint64_t n_dst, const std::vector<std::pair<NodeId, NodeId>>& pairs) {
   Adjacency a;
   a.offsets.assign(n_dst + 1, 0);
@@ -80,18 +108,21 @@ Graph assemble(std::vector<std::string> type_names, std::vector<std::uint64_t> c
     g.types.push_back(std::move(nt));
   }
   g.edge_type_names = std::move(edge_names);
-  for (std::size_t r = 0; r < rel_src.size(); ++r) {
-    RelationInfo rel;
-    rel.src_type = rel_src[r];
-    rel.edge_type = static_cast<int>(r);
-    rel.dst_type = rel_dst[r];
-    const std::uint64_t ns = counts[rel.src_type], nd = counts[rel.dst_type];
-    for (const auto& pr : pairs[r])
-      if (pr.first >= ns || pr.second >= nd)
-        throw std::invalid_argument("edge endpoint out of range in relation " + std::to_string(r));
-    rel.adj = dst_major(nd, pairs[r]);
-    g.rels.push_back(std::move(rel));
-  }
+  g.rels.resize(rel_src.size());
+  std::vector<std::function<void()>> tasks;
+  for (std::size_t r = 0; r < rel_src.size(); ++r)
+    tasks.emplace_back([&, r] {
+      RelationInfo& rel = g.rels[r];
+      rel.src_type = rel_src[r];
+      rel.edge_type = static_cast<int>(r);
+      rel.dst_type = rel_dst[r];
+      const std::uint64_t ns = counts[rel.src_type], nd = counts[rel.dst_type];
+      for (const auto& pr : pairs[r])
+        if (pr.first >= ns || pr.second >= nd)
+          throw std::invalid_argument("edge endpoint out of range in relation " + std::to_string(r));
+      rel.adj = dst_major(nd, pairs[r]);
+    });
+  run_parallel(tasks);
   g.target = target;
   g.num_classes = num_classes;
   g.labels.assign(counts[target], -1);
@@ -102,32 +133,44 @@ void append_reverse(Graph& g, const std::vector<int>& self_paired) {
   for (const auto& r : g.rels)
     if (r.reverse) throw std::invalid_argument("graph already contains reverse relations");
   const std::size_t n_fwd = g.rels.size();
+  std::vector<std::size_t> todo;
+  std::vector<int> name_idx;
   for (std::size_t r = 0; r < n_fwd; ++r) {
     if (contains(self_paired, static_cast<int>(r))) continue;
     const std::string name = "rev_" + g.edge_type_names[g.rels[r].edge_type];
     if (contains(g.edge_type_names, name))
       throw std::invalid_argument("reverse edge type name already exists: " + name);
     g.edge_type_names.push_back(name);
-    // transpose: rows become the old sources, each listing old destinations
-    // in ascending destination order
-    const Adjacency& fwd = g.rels[r].adj;
-    const std::uint64_t n_new_dst = g.types[g.rels[r].src_type].count;
-    Adjacency t;
-    t.offsets.assign(n_new_dst + 1, 0);
-    for (NodeId s : fwd.sources) ++t.offsets[s + 1];
-    std::partial_sum(t.offsets.begin(), t.offsets.end(), t.offsets.begin());
-    t.sources.resize(fwd.sources.size());
-    std::vector<std::uint64_t> fill(t.offsets.begin(), t.offsets.end() - 1);
-    const std::uint64_t n_old_dst = fwd.offsets.size() - 1;
-    for (std::uint64_t d = 0; d < n_old_dst; ++d)
-      for (std::uint64_t e = fwd.offsets[d]; e < fwd.offsets[d + 1]; ++e)
-        t.sources[fill[fwd.sources[e]]++] = static_cast<NodeId>(d);
+    todo.push_back(r);
+    name_idx.push_back(static_cast<int>(g.edge_type_names.size()) - 1);
+  }
+  // transposes (independent per relation, built on host threads): rows become
+  // the old sources, each listing old destinations in ascending order
+  std::vector<Adjacency> tr(todo.size());
+  std::vector<std::function<void()>> tasks;
+  for (std::size_t i = 0; i < todo.size(); ++i)
+    tasks.emplace_back([&, i] {
+      const Adjacency& fwd = g.rels[todo[i]].adj;
+      const std::uint64_t n_new_dst = g.types[g.rels[todo[i]].src_type].count;
+      Adjacency& t = tr[i];
+      t.offsets.assign(n_new_dst + 1, 0);
+      for (NodeId s : fwd.sources) ++t.offsets[s + 1];
+      std::partial_sum(t.offsets.begin(), t.offsets.end(), t.offsets.begin());
+      t.sources.resize(fwd.sources.size());
+      std::vector<std::uint64_t> fill(t.offsets.begin(), t.offsets.end() - 1);
+      const std::uint64_t n_old_dst = fwd.offsets.size() - 1;
+      for (std::uint64_t d = 0; d < n_old_dst; ++d)
+        for (std::uint64_t e = fwd.offsets[d]; e < fwd.offsets[d + 1]; ++e)
+          t.sources[fill[fwd.sources[e]]++] = static_cast<NodeId>(d);
+    });
+  run_parallel(tasks);
+  for (std::size_t i = 0; i < todo.size(); ++i) {
     RelationInfo rev;
-    rev.src_type = g.rels[r].dst_type;
-    rev.dst_type = g.rels[r].src_type;
-    rev.edge_type = static_cast<int>(g.edge_type_names.size()) - 1;
+    rev.src_type = g.rels[todo[i]].dst_type;
+    rev.dst_type = g.rels[todo[i]].src_type;
+    rev.edge_type = name_idx[i];
     rev.reverse = true;
-    rev.adj = std::move(t);
+    rev.adj = std::move(tr[i]);
     g.rels.push_back(std::move(rev));
   }
 }
@@ -165,9 +208,17 @@ Graph generate(const Spec& spec, std::uint64_t seed) {
     const SpecRelation& sr = spec.relations[ri];
     if (contains(edge_names, sr.edge)) throw std::invalid_argument("duplicate edge type name: " + sr.edge);
     edge_names.push_back(sr.edge);
-    const int s = index_of(names, sr.src), d = index_of(names, sr.dst);
-    rs.push_back(s);
-    rd.push_back(d);
+    rs.push_back(index_of(names, sr.src));
+    rd.push_back(index_of(names, sr.dst));
+  }
+  // Every stochastic part draws from its own mt19937_64 stream (per relation
+  // mix_seed(seed, 0x9e0 + ri), per feature type mix_seed(seed, 0xf0 + t), the
+  // labels mix_seed(seed, 0x1abe1); harness.cpp:113-166), so the streams run on
+  // separate host threads with bit-identical results.
+  std::vector<std::function<void()>> tasks;
+  for (std::size_t ri = 0; ri < spec.relations.size(); ++ri) tasks.emplace_back([&, ri] {
+    const SpecRelation& sr = spec.relations[ri];
+    const int s = rs[ri], d = rd[ri];
     std::mt19937_64 eng(mix_seed(seed, 0x9e0ULL + ri));
     std::uniform_int_distribution<std::uint64_t> src_pick(0, counts[s] - 1);
     auto& out = pairs[ri];
@@ -200,27 +251,36 @@ Graph generate(const Spec& spec, std::uint64_t seed) {
         for (std::uint64_t e = 0; e < deg[dd]; ++e)
           out.emplace_back(static_cast<NodeId>(src_pick(eng)), static_cast<NodeId>(dd));
     }
-  }
+  });
+  std::vector<std::vector<float>> dense(spec.node_types.size());
+  for (std::size_t t = 0; t < spec.node_types.size(); ++t)
+    if (spec.node_types[t].storage == Storage::Dense)
+      tasks.emplace_back([&, t] {
+        std::mt19937_64 eng(mix_seed(seed, 0xf0ULL + t));
+        std::uniform_real_distribution<double> u(-1.0, 1.0);
+        dense[t].resize(spec.node_types[t].count * static_cast<std::uint64_t>(spec.node_types[t].dim));
+        for (float& x : dense[t]) x = static_cast<float>(u(eng));
+      });
+  std::vector<std::int32_t> labels(counts[tgt]);
+  tasks.emplace_back([&] {
+    std::mt19937_64 leng(mix_seed(seed, 0x1abe1ULL));
+    std::uniform_real_distribution<double> coin(0.0, 1.0);
+    std::uniform_int_distribution<int> any_class(0, spec.num_classes - 1);
+    for (NodeId v = 0; v < counts[tgt]; ++v) {
+      labels[v] = static_cast<std::int32_t>(v % spec.num_classes);
+      if (coin(leng) < spec.label_noise) labels[v] = any_class(leng);
+    }
+  });
+  run_parallel(tasks);
 
   Graph g = assemble(names, counts, edge_names, rs, rd, pairs, tgt, spec.num_classes);
   for (std::size_t t = 0; t < spec.node_types.size(); ++t) {
     NodeTypeInfo& nt = g.types[t];
     nt.dim = spec.node_types[t].dim;
     nt.storage = spec.node_types[t].storage;
-    if (nt.storage == Storage::Dense) {
-      std::mt19937_64 eng(mix_seed(seed, 0xf0ULL + t));
-      std::uniform_real_distribution<double> u(-1.0, 1.0);
-      nt.dense.resize(nt.count * static_cast<std::uint64_t>(nt.dim));
-      for (float& x : nt.dense) x = static_cast<float>(u(eng));
-    }
+    if (nt.storage == Storage::Dense) nt.dense = std::move(dense[t]);
   }
-  std::mt19937_64 leng(mix_seed(seed, 0x1abe1ULL));
-  std::uniform_real_distribution<double> coin(0.0, 1.0);
-  std::uniform_int_distribution<int> any_class(0, spec.num_classes - 1);
-  for (NodeId v = 0; v < g.types[tgt].count; ++v) {
-    g.labels[v] = static_cast<std::int32_t>(v % spec.num_classes);
-    if (coin(leng) < spec.label_noise) g.labels[v] = any_class(leng);
-  }
+  g.labels = std::move(labels);
   if (spec.add_reverse) {
     std::vector<int> paired;
     for (const auto& n : spec.self_paired) {
