@@ -1017,6 +1017,7 @@ void Engine::run_forward() {
       });
     }
 #endif
+    if (training_ && replica_group_.size() > 1) replica_prepare();
   }
 }
 
@@ -1119,50 +1120,28 @@ void Engine::run_replica_merge() {
         throw std::runtime_error("ncclAllReduce (replica weight gradients) failed");
     if (ncclGroupEnd() != ncclSuccess) throw std::runtime_error("ncclGroupEnd failed");
   });
-  // 2. learnable rows: union + per-replica row slots, then step and the fused
-  //    ordered sum + Adam over the union
-  std::vector<ReplicaMerge> merges;
+  // 2. learnable rows: the union and row slots were built by replica_prepare
+  //    (side stream, during the loss and backward pass; joined before this).
+  //    Step, then the fused ordered sum + Adam over the union.
   std::vector<const std::int64_t*> steps;
   std::vector<const int*> ucounts;
   for (auto& x : xchg_) {
-    ReplicaMerge m{};
-    m.n_rep = static_cast<int>(peer_arena_.size());
-    for (int r = 0; r < m.n_rep; ++r) {
-      m.ids[r] = reinterpret_cast<const std::uint32_t*>(peer_arena_[r] + x.off_ids[bound_]);
-      m.count[r] = reinterpret_cast<const int*>(peer_arena_[r] + x.off_count[bound_]);
-      m.dh[r] = reinterpret_cast<const float*>(peer_arena_[r] + x.off_dh);
-    }
-    m.ld = x.ld;
-    m.din = x.din;
-    m.u = {bits_ + word_base_[x.t], word_base_[x.t + 1] - word_base_[x.t], wscan_ + word_base_[x.t], x.ulist, x.ucount,
-           x.ucap};
-    m.slot = x.slot;
-    m.ug = nullptr;
-    // sharded: this replica merges and Adam-updates only the ids of its shard and
-    // stores the new rows into every copy; unsharded: every replica updates the
-    // whole union in its own copy (measured faster on B200 at p=4, the default)
-    m.shard = shard_merge_ ? replica_pos_ : 0;
-    m.nshard = shard_merge_ ? m.n_rep : 1;
-    m.total = x.utotal;
-    timed("replica_union", 0, [&] { replica_union(m, lb2_, st_); });  // lb_ belongs to the sampling stream
-    timed("replica_slots", 0, [&] { replica_slots(m, st_); });
-    merges.push_back(m);
     steps.push_back(tables_[x.t].step);
     ucounts.push_back(x.utotal);  // the step moves iff the whole union is non-empty
   }
   // each table's step += 1 iff its union is non-empty (hgnn.cpp:392-394)
   bump_steps(steps.data(), ucounts.data(), static_cast<int>(steps.size()), st_);
   timed("replica_adam", 0, [&] {
-    for (std::size_t i = 0; i < merges.size(); ++i) {
+    for (std::size_t i = 0; i < merges_.size(); ++i) {
       const TypeTable& tb = tables_[xchg_[i].t];
-      ReplicaAdam ra{tb.w, tb.m, tb.v, tb.ld, tb.step, {}, merges[i].n_rep};
+      ReplicaAdam ra{tb.w, tb.m, tb.v, tb.ld, tb.step, {}, merges_[i].n_rep};
       if (shard_merge_) {
         for (int r = 0; r < ra.n_rep; ++r) ra.peer_w[r] = xchg_[i].peer_w[r];
       } else {
         ra.n_rep = 1;
         ra.peer_w[0] = tb.w;
       }
-      replica_sum_adam(merges[i], ra, AdamHyper{}, err_, st_);
+      replica_sum_adam(merges_[i], ra, AdamHyper{}, err_, st_);
     }
   });
   {
@@ -1186,6 +1165,41 @@ void Engine::run_replica_merge() {
 #else
   throw std::runtime_error("replica groups need NCCL");
 #endif
+}
+
+// Replica groups, first half of the merge: the union of the replicas' leaf ids
+// and each replica's row slots. It reads only the replicas' sampled ids and
+// counts, which exist on every replica once the AGG_all all-reduce has run, so
+// it is enqueued on the side stream right after it and overlaps the loss and
+// the backward pass (the gradient rows are read only after the replicas'
+// weight-gradient all-reduce, in run_replica_merge).
+void Engine::replica_prepare() {
+  merges_.clear();
+  fork();
+  for (auto& x : xchg_) {
+    ReplicaMerge m{};
+    m.n_rep = static_cast<int>(peer_arena_.size());
+    for (int r = 0; r < m.n_rep; ++r) {
+      m.ids[r] = reinterpret_cast<const std::uint32_t*>(peer_arena_[r] + x.off_ids[bound_]);
+      m.count[r] = reinterpret_cast<const int*>(peer_arena_[r] + x.off_count[bound_]);
+      m.dh[r] = reinterpret_cast<const float*>(peer_arena_[r] + x.off_dh);
+    }
+    m.ld = x.ld;
+    m.din = x.din;
+    m.u = {bits_ + word_base_[x.t], word_base_[x.t + 1] - word_base_[x.t], wscan_ + word_base_[x.t], x.ulist, x.ucount,
+           x.ucap};
+    m.slot = x.slot;
+    m.ug = nullptr;
+    // sharded: this replica merges and Adam-updates only the ids of its shard and
+    // stores the new rows into every copy; unsharded: every replica updates the
+    // whole union in its own copy (measured faster on B200 at p=4, the default)
+    m.shard = shard_merge_ ? replica_pos_ : 0;
+    m.nshard = shard_merge_ ? m.n_rep : 1;
+    m.total = x.utotal;
+    timed("replica_union", 0, [&] { replica_union(m, lb2_, side()); });
+    timed("replica_slots", 0, [&] { replica_slots(m, side()); });
+    merges_.push_back(m);
+  }
 }
 
 // IPC handles of this replica's exchange arena, then of its copy of every
@@ -1310,6 +1324,7 @@ void Engine::sample_body(cudaStream_t ss) {
 void Engine::train_body(bool train) {
   fork_used_ = 0;
   side_open_ = false;
+  training_ = train;
   run_forward();
   run_loss(train);
   if (train) {

@@ -456,6 +456,9 @@ class Engine {
     return false;
   }
   void run_replica_merge();
+  void replica_prepare();
+  std::vector<ReplicaMerge> merges_;  // built by replica_prepare for run_replica_merge
+  bool training_ = false;
 };
 
 }  // namespace hetgpu

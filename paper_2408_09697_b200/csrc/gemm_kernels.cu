@@ -298,6 +298,10 @@ __global__ void __launch_bounds__(kT) k_dmean_tiles(DMeanBatch b) {
 
 // ---- gather-mean: 16 lanes x float4 per (row, 64-column chunk); a warp carries
 // two such items, 8 edges in flight per lane ---------------------------------------------------
+#ifndef HG_GATHER_BATCH
+#define HG_GATHER_BATCH 8
+#endif
+constexpr int kGatherBatch = HG_GATHER_BATCH;  // neighbour rows in flight per lane
 __global__ void __launch_bounds__(256) k_gather_mean(MeanBatch m) {
   pdl_enter();
   const int hl = threadIdx.x & 15;
@@ -325,18 +329,18 @@ __global__ void __launch_bounds__(256) k_gather_mean(MeanBatch m) {
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
     // batches of 8 neighbours (the last one predicated): one key round trip and
     // one row round trip per batch, summed in edge order
-    for (std::uint32_t e = lo; e < hi; e += 8) {
-      const std::uint32_t cnt = min(8u, hi - e);
-      std::uint32_t kk[8];
+    for (std::uint32_t e = lo; e < hi; e += kGatherBatch) {
+      const std::uint32_t cnt = min(static_cast<std::uint32_t>(kGatherBatch), hi - e);
+      std::uint32_t kk[kGatherBatch];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) kk[q] = q < cnt ? __ldg(B.keys + e + q) : 0u;
-      float4 v[8];
+      for (int q = 0; q < kGatherBatch; ++q) kk[q] = q < cnt ? __ldg(B.keys + e + q) : 0u;
+      float4 v[kGatherBatch];
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
+      for (int q = 0; q < kGatherBatch; ++q)
         v[q] = q < cnt ? __ldg(reinterpret_cast<const float4*>(base + static_cast<std::size_t>(kk[q]) * B.ld_h))
                        : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < kGatherBatch; ++q) {
         s.x += v[q].x;
         s.y += v[q].y;
         s.z += v[q].z;
