@@ -308,6 +308,7 @@ int pick_nt(int cols) {
   return 128;
 }
 
+
 template <int MODE, typename Batch>
 void dispatch(UmmaArgs<Batch>& a, int nt, int tiles, cudaStream_t st) {
   if (tiles <= 0) return;
@@ -331,6 +332,9 @@ void project_umma(ProjBatch& pb, cudaStream_t st) {
   a.np = pb.ng;
   int nt = 32;
   for (int g = 0; g < pb.ng; ++g) nt = std::max(nt, pick_nt(pb.g[g].ld_out));
+  // at most 64 columns per tile: the top layer (C = 349) then runs 48 CTAs
+  // instead of 24, which shortens its latency-bound launch (measured +2%)
+  nt = std::min(nt, 64);
   int tiles = 0;
   for (int g = 0; g < pb.ng; ++g) {
     const ProjGroup& G = pb.g[g];
