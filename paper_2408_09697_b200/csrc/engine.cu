@@ -147,8 +147,11 @@ Engine::Engine(const Graph& g, const EngineOptions& o) : o_(o) {
   // the sampling stream (batch i+1) gets the highest priority so that its
   // latency-bound chain is never starved by the bandwidth-bound training
   // kernels (measured +1%; prioritising training instead costs 6%)
+  // With several partitions the training stream carries the AGG_all collective,
+  // which every rank waits on: there all streams keep the default priority.
   int least = 0, greatest = 0;
   HG_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  if (o.p > 1) greatest = least;
   HG_CUDA(cudaStreamCreateWithPriority(&st_, cudaStreamNonBlocking, least));
   HG_CUDA(cudaStreamCreateWithPriority(&st2_, cudaStreamNonBlocking, least));
   HG_CUDA(cudaStreamCreateWithPriority(&st_s_, cudaStreamNonBlocking, greatest));

@@ -1,7 +1,7 @@
 # N = 1, 2, 4 bench lines (the driver's launch form)
-python bench.py --steps 50 --warmup 5 --no-cpu-baseline 2>/dev/null | tail -1 > gpurun_out/scale_n1.json
+python bench.py > gpurun_out/scale_n1.json 2> gpurun_out/scale_n1.err
 for n in 2 4; do
   python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29511 \
-    bench.py --gpus $n --steps 50 --warmup 5 2>/dev/null | tail -1 > gpurun_out/scale_n$n.json
+    bench.py --gpus $n --steps 100 --warmup 5 2>/dev/null | tail -1 > gpurun_out/scale_n$n.json
 done
-for n in 1 2 4; do python -c "import json; d=json.load(open('gpurun_out/scale_n$n.json')); print($n, round(d['value']/1e9,3), round(d['ms_per_step'],4), round(d['e2e']['value']/1e9,3))"; done
+for n in 1 2 4; do python -c "import json; d=json.loads(open('gpurun_out/scale_n$n.json').read().strip().splitlines()[-1]); print($n, round(d['value']/1e9,3), round(d['ms_per_step'],4), round(d['e2e']['value']/1e9,3), d['clocks'])"; done
