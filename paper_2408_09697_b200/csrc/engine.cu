@@ -1088,10 +1088,35 @@ void Engine::run_backward() {
       }
     }
     // dpre of this layer is complete on st_: the weight gradient runs beside the
-    // mean gradient and the next backward gather
+    // mean gradient and the next backward gather. Without replicas (nothing to
+    // all-reduce) each slot's Adam is fused into its gradient reduction, which
+    // then waits for this layer's mean gradient (the last reader of W_l).
+    const bool fuse_adam = fused_model_adam();
+    if (fuse_adam) {
+      wb.defer_reduce = 1;
+      wb.step = &d_tsc_->model_step;
+      wb.err = err_;
+      for (int q = 0; q < wb.np; ++q)
+        for (const auto& gr : groups_) {
+          if (gr.layer != l || gr.blocks.empty()) continue;
+          for (std::size_t j = 0; j < gr.slots.size(); ++j) {
+            const Slot& sl = slots_[gr.slots[j]];
+            if (wb.p[q].dw == sl.g) {
+              wb.p[q].w = sl.w;
+              wb.p[q].m = sl.m;
+              wb.p[q].v = sl.v;
+              wb.p[q].w_lo = sl.w_lo;
+            }
+          }
+        }
+    }
     fork();
     timed("weight_grad", 0, [&] { use_umma_ ? wgrad_umma(wb, side()) : wgrad_tiles(wb, side()); });
     timed("mean_grad", 0, [&] { use_umma_ ? dmean_umma(db, st_) : dmean_tiles(db, st_); });
+    if (fuse_adam) {
+      fork();  // the side stream waits for the mean gradient, then reduces + updates
+      timed("weight_grad", 0, [&] { wgrad_reduce(wb, side()); });
+    }
     // scatter back to the sources of this hop, as ordered gathers (learnable
     // layer-0 rows get their Adam update in the same pass)
     const CscHop ch = csc_hop(d);
@@ -1296,6 +1321,7 @@ CscHop Engine::csc_hop(int h) {
 }
 
 void Engine::run_update() {
+  if (fused_model_adam()) return;  // applied by the weight-gradient reductions
   AdamHyper hp;
   AdamModelBatch mb{};
   int base = 0;

@@ -457,6 +457,7 @@ class Engine {
   }
   void run_replica_merge();
   void replica_prepare();
+  bool fused_model_adam() const { return replica_group_.size() <= 1; }
   std::vector<ReplicaMerge> merges_;  // built by replica_prepare for run_replica_merge
   bool training_ = false;
 };

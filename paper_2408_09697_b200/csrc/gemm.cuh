@@ -32,11 +32,18 @@ struct WGradProblem {
   float* dw;
   int ld_dw;
   const float* mean_lo;
+  // optional Adam of the slot fused into the reduction (stride ld_dw): each
+  // gradient element is final there, so it is applied to w / m / v at once
+  float *w, *m, *v, *w_lo;
 };
 struct WGradBatch {
   WGradProblem p[kMaxProblems];
   int tile_base[kMaxProblems];
   int np;
+  int defer_reduce;            // the caller runs wgrad_reduce itself (after an event)
+  const std::int64_t* step;    // model Adam step (fused update)
+  AdamHyper hp;
+  std::uint32_t* err;
 };
 
 struct DMeanProblem {

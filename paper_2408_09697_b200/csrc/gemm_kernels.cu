@@ -5,6 +5,7 @@
 // One 64x64 output tile per CTA, 256 threads with a 4x4 register tile each,
 // K staged through shared memory in 32-deep slabs. Several independent
 // problems share one launch (tile ids are linearised over the problems).
+#include "adam.cuh"
 #include "gemm.cuh"
 
 namespace hetgpu {
@@ -216,6 +217,11 @@ __global__ void __launch_bounds__(kT) k_wgrad_tiles(WGradBatch b) {
 // output element of every problem, chunks summed in order, 8 loads in flight
 __global__ void __launch_bounds__(256) k_wgrad_reduce(WGradBatch b, int total_out) {
   pdl_enter();
+  __shared__ AdamStep ks;
+  if (b.step) {
+    if (threadIdx.x == 0) ks = adam_step_of(b.hp, static_cast<double>(*b.step));
+    __syncthreads();
+  }
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < total_out; x += gridDim.x * blockDim.x) {
     int p = 0, base = 0;
     while (p + 1 < b.np && x >= base + b.p[p].din * b.p[p].d.cols) {
@@ -238,7 +244,16 @@ __global__ void __launch_bounds__(256) k_wgrad_reduce(WGradBatch b, int total_ou
     }
     for (; c < chunks; ++c) s += src[static_cast<std::size_t>(c) * total];
     // each slot's gradient is produced by exactly one problem: overwrite (no memset)
-    P.dw[static_cast<std::size_t>(o / P.d.cols) * P.ld_dw + o % P.d.cols] = s;
+    const std::size_t at = static_cast<std::size_t>(o / P.d.cols) * P.ld_dw + o % P.d.cols;
+    P.dw[at] = s;
+    if (P.w) {  // adam_update_model for this element (hgnn.cpp:379-390)
+      float w = P.w[at], m = P.m[at], v = P.v[at];
+      adam1(w, m, v, s, ks, b.err);
+      P.w[at] = w;
+      P.m[at] = m;
+      P.v[at] = v;
+      if (P.w_lo) P.w_lo[at] = tf32_lo(w);
+    }
   }
 }
 
@@ -461,7 +476,7 @@ void wgrad_tiles(WGradBatch& b, cudaStream_t st) {
                               ceil_div(P.d.cols, kTile));
   }
   launch_pdl(k_wgrad_tiles, std::max(1, tiles), kT, 0, st, b);
-  wgrad_reduce(b, st);
+  if (!b.defer_reduce) wgrad_reduce(b, st);
 }
 
 void wgrad_reduce(WGradBatch& b, cudaStream_t st) {

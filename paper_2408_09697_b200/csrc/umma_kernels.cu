@@ -407,7 +407,7 @@ void wgrad_umma(WGradBatch& b, cudaStream_t st) {
   }
   a.tile_base[b.np] = tiles;
   dispatch<kWGrad>(a, nt, tiles, st);
-  wgrad_reduce(b, st);
+  if (!b.defer_reduce) wgrad_reduce(b, st);
 }
 
 }  // namespace hetgpu
