@@ -8,6 +8,10 @@
 #include "adam.cuh"
 #include "gemm.cuh"
 
+#ifndef HG_GATHER_WAVES
+#define HG_GATHER_WAVES 16  // CTAs per SM of the gather grids (8 resident: two waves)
+#endif
+
 namespace hetgpu {
 
 namespace {
@@ -445,7 +449,7 @@ void gather_mean(MeanBatch& m, cudaStream_t st) {
     items += m.b[b].rows_cap * static_cast<int>(ceil_div(m.b[b].din, 64));
   }
   m.item_base[m.nb] = items;
-  const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(items, 16), 16 * kNumSMs)));
+  const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(items, 16), HG_GATHER_WAVES * kNumSMs)));
   launch_pdl(k_gather_mean, grid, 256, 0, st, m);
 }
 

@@ -1,4 +1,6 @@
-one() { python bench.py --steps 30 --warmup 5 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); k=d['kernel_us_per_step']; print('$HG_NT_CAP', round(d['value']/1e9,4), round(d['ms_per_step'],4), 'proj', k.get('project'), k.get('project_top'), 'dmean', k.get('mean_grad'), 'wgrad', k.get('weight_grad'))"; }
+one() { HETGPU_LIB=$1 python bench.py --steps 30 --warmup 5 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); r=d['roofline']['kernels']; print('$2', round(d['value']/1e9,4), round(d['ms_per_step'],4), round(d['e2e']['value']/1e9,4), 'agg', round(r['aggregate']['frac'],3), 'csc', round(r['csc_gather']['frac'],3))"; }
 for i in 1 2; do
-  for c in 128,128,128 64,128,128 32,128,128 128,32,128 128,128,64 64,32,64; do HG_NT_CAP=$c one; done
+  one paper_2408_09697_b200/libhetgpu.so w16
+  one paper_2408_09697_b200/libhetgpu_w8.so w8
+  one paper_2408_09697_b200/libhetgpu_w24.so w24
 done
