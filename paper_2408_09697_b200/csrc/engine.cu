@@ -158,6 +158,7 @@ Engine::Engine(const Graph& g, const EngineOptions& o) : o_(o) {
   for (int sl = 0; sl < 2; ++sl) {
     HG_CUDA(cudaEventCreateWithFlags(&ev_sampled_[sl], cudaEventDisableTiming));
     HG_CUDA(cudaEventCreateWithFlags(&ev_trained_[sl], cudaEventDisableTiming));
+    HG_CUDA(cudaEventCreateWithFlags(&ev_staged_[sl], cudaEventDisableTiming));
   }
   fork_ev_.resize(16);
   for (auto& e : fork_ev_) HG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -186,6 +187,7 @@ Engine::~Engine() {
     if (h_batch_slot_[sl]) cudaFreeHost(h_batch_slot_[sl]);
     if (h_rb_slot_[sl]) cudaFreeHost(h_rb_slot_[sl]);
     if (ev_sampled_[sl]) cudaEventDestroy(ev_sampled_[sl]);
+    if (ev_staged_[sl]) cudaEventDestroy(ev_staged_[sl]);
     if (ev_trained_[sl]) cudaEventDestroy(ev_trained_[sl]);
   }
   if (h_tsc_) cudaFreeHost(h_tsc_);
@@ -1435,11 +1437,14 @@ void Engine::prefetch(const NodeId* batch, int n, std::uint64_t rng_seed) {
   cudaStream_t ss = sstream();
   // the slot is free once the step that last trained on it is done
   HG_CUDA(cudaStreamWaitEvent(ss, ev_trained_[s], 0));
-  HG_CUDA(cudaStreamSynchronize(ss));  // the slot's pinned staging buffers are reusable
+  // the slot's pinned staging buffers are reusable once their previous copies
+  // ran (not the whole sampling stream: the other slot may still be sampling)
+  HG_CUDA(cudaEventSynchronize(ev_staged_[s]));
   std::memcpy(h_batch_slot_[s], batch, sizeof(NodeId) * n);
   *h_sc_slot_[s] = StepScalars{rng_seed, n, 0, 0};
   HG_CUDA(cudaMemcpyAsync(d_batch_slot_[s], h_batch_slot_[s], sizeof(NodeId) * n, cudaMemcpyHostToDevice, ss));
   HG_CUDA(cudaMemcpyAsync(d_sc_slot_[s], h_sc_slot_[s], sizeof(StepScalars), cudaMemcpyHostToDevice, ss));
+  HG_CUDA(cudaEventRecord(ev_staged_[s], ss));
   enqueue_sample(s);
   HG_CUDA(cudaEventRecord(ev_sampled_[s], ss));
   pending_slots_.push_back({s, rng_seed, std::vector<NodeId>(batch, batch + n)});

@@ -319,6 +319,7 @@ class Engine {
   int next_slot_ = 0, last_trained_ = 0;
   cudaStream_t st_s_ = nullptr;  // sampling stream
   cudaEvent_t ev_sampled_[2] = {}, ev_trained_[2] = {};
+  cudaEvent_t ev_staged_[2] = {};  // the slot's pinned batch staging copy has been consumed
   StepScalars* d_tsc_ = nullptr;  // scalars of the step being trained
   StepScalars* h_tsc_ = nullptr;  // pinned
   cudaStream_t sstream() const { return profiling_ ? st_ : st_s_; }
