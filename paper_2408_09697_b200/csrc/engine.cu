@@ -705,7 +705,7 @@ void Engine::upload(const Graph& g) {
     std::size_t tiles = ceil_div(total_words_, kCompactWordsPerTile) + kMaxSegs;
     for (int h = 1; h <= o_.k; ++h) {
       std::size_t t = 0;
-      for (int bi : hop_blocks_[h]) t += ceil_div(std::max(1, blocks_[bi].rows_cap), 256) + 1;
+      for (int bi : hop_blocks_[h]) t += ceil_div(std::max(1, blocks_[bi].rows_cap), kSampleTileRows) + 1;
       tiles = std::max(tiles, t);
     }
     tiles = std::max<std::size_t>(tiles, kMaxSegs * (ceil_div(max_cap, kScanTile) + 1));

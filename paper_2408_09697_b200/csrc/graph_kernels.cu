@@ -156,7 +156,7 @@ void scan_inclusive(const ScanArgs& a, LbScratch& lb, cudaStream_t st) {
 
 namespace {
 
-constexpr int kSampleThreads = 256;
+constexpr int kSampleThreads = kSampleTileRows;
 constexpr int kSlowThreads = 4096;  // concurrent slow-path rows (global scratch)
 
 // Same draws with the dependency chain cut short. The mt19937_64 outputs

@@ -51,6 +51,12 @@ struct LbScratch {
     HG_CUDA(cudaMemsetAsync(mem, 0, (static_cast<std::size_t>(tiles) + 1) * 8, st));
   }
 };
+// rows per sampler tile (= threads per CTA of k_sample_fused); 128 measured best
+// (the RNG-row tiles are the long pole: smaller tiles spread them over more SMs)
+#ifndef HG_SAMPLE_TILE
+#define HG_SAMPLE_TILE 128
+#endif
+constexpr int kSampleTileRows = HG_SAMPLE_TILE;
 // bitmap words per frontier-compaction tile (one word per thread)
 constexpr int kCompactWordsPerTile = 256;
 // single-pass (decoupled look-back) segmented inclusive scan
