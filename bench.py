@@ -112,6 +112,17 @@ def dist_env():
 
 
 # ---------------------------------------------------------------------------------------------
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline_sample(n_threads, n_batches, graph_ref=None):
     """The reference (oracle/_ref, compiled from /root/reference) on the host's
     cores: `n_threads` concurrent run_raf_batch calls on distinct C2 batches.
@@ -157,7 +168,7 @@ def run_reference(args):
                                "batch 1024 (run_raf_batch p=1 on CPU: sample + forward + loss + backward; the Adam updates are not timed)",
                    "batch_per_step": threads, "graph_seed": SEED},
         "epoch_time_s": EPOCH_BATCHES * ms_per_batch / 1000.0 / threads,
-        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": threads, "kind": "reference",
+        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": threads, "kind": "reference", "cpu_model": cpu_model(),
                          "sample": f"{steps} steps x {threads} concurrent run_raf_batch calls ({time_total:.1f} s)"},
         "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -335,9 +346,13 @@ def run_b200(args):
     if not args.no_cpu_baseline and n == 1:
         # bounded sample: 8 batches per host thread (~10-20 s of CPU work)
         threads = os.cpu_count() or 1
-        v, sample, secs, _ = cpu_baseline_sample(threads, 8 * threads)
+        v, sample, secs, g_ref = cpu_baseline_sample(threads, 8 * threads)
+        # the reference as shipped is single-threaded: one core, two batches
+        v1, _, secs1, _ = cpu_baseline_sample(1, 2, g_ref)
         line["cpu_baseline"] = {"value": v, "unit": "edges/s", "cores": threads, "kind": "reference",
-                                "sample": sample + f" ({secs:.1f} s)"}
+                                "sample": sample + f" ({secs:.1f} s)", "cpu_model": cpu_model(),
+                                "single_core": {"value": v1, "unit": "edges/s", "ms_per_batch": 1000.0 * secs1 / 2,
+                                                "sample": f"2 run_raf_batch calls on 1 thread ({secs1:.1f} s)"}}
     print(json.dumps(line), flush=True)
     if world > 1:
         tdist.destroy_process_group()
