@@ -16,7 +16,13 @@ def main():
     name, seed, p, rank, id_path, out_path, n_batches, bsz = sys.argv[1:9]
     seed, p, rank, n_batches, bsz = int(seed), int(p), int(rank), int(n_batches), int(bsz)
     from paper_2408_09697_b200 import hetsim as H
-    g = H.gen_synthetic(H.bundled_spec(name), seed)
+    if name.startswith("spec:"):  # a spec written by the test as JSON
+        import json
+        with open(name[len("spec:"):]) as f:
+            spec = json.load(f)
+    else:
+        spec = H.bundled_spec(name)
+    g = H.gen_synthetic(spec, seed)
     eng = H.Engine.for_experiment(g, [25, 20], 32, seed, batch_cap=bsz, p=p, rank=rank, device=rank)
     if rank == 0:
         uid = H.nccl_unique_id()

@@ -24,8 +24,21 @@ def n_gpus():
         return 0
 
 
+# one root relation: a single sub-metatree, so every rank is a replica of it
+# (groups of 3 and 4 as at p = 8 on ogbn-mag), with learnable leaves to merge
+SINGLE_ROOT = {
+    "name": "single-root", "target": "paper", "num_classes": 6, "label_noise": 0.1,
+    "node_types": [{"name": "paper", "count": 3000, "dim": 32, "storage": "dense"},
+                   {"name": "author", "count": 4000, "dim": 16, "storage": "learnable"},
+                   {"name": "field", "count": 600, "dim": 16, "storage": "learnable"}],
+    "relations": [{"src": "author", "edge": "writes", "dst": "paper", "edges": 12000},
+                  {"src": "field", "edge": "topic", "dst": "author", "edges": 6000}],
+    "self_paired": []}
+
+
 @pytest.mark.parametrize("name,p,shard", [("mag-mini", 2, 0), ("mag-mini", 4, 0), ("igb-mini", 4, 0),
-                                          ("mag-mini", 4, 1)])
+                                          ("mag-mini", 4, 1), ("single-root", 3, 0), ("single-root", 4, 0),
+                                          ("single-root", 3, 1)])
 def test_raf_multi_gpu_matches_reference(ref, name, p, shard):
     # p = 4 > 3 sub-metatrees: one sub-metatree is replicated, its replicas split
     # the batch and synchronise weight gradients (NCCL) and learnable rows
@@ -35,7 +48,13 @@ def test_raf_multi_gpu_matches_reference(ref, name, p, shard):
     seed, n_batches, bsz = 5, 6, 64
     with tempfile.TemporaryDirectory() as td:
         idp = os.path.join(td, "nccl.id")
-        procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "mp", "raf_rank.py"), name, str(seed), str(p),
+        arg = name
+        if name == "single-root":
+            import json
+            arg = "spec:" + os.path.join(td, "spec.json")
+            with open(arg[len("spec:"):], "w") as f:
+                json.dump(SINGLE_ROOT, f)
+        procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "mp", "raf_rank.py"), arg, str(seed), str(p),
                                    str(r), idp, os.path.join(td, f"r{r}.npz"), str(n_batches), str(bsz)],
                                   stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True,
                                   env=dict(os.environ, HG_SHARD_MERGE=str(shard))) for r in range(p)]
@@ -44,9 +63,10 @@ def test_raf_multi_gpu_matches_reference(ref, name, p, shard):
             assert pr.returncode == 0, o[-3000:]
         res = [np.load(os.path.join(td, f"r{r}.npz")) for r in range(p)]
     from paper_2408_09697_b200 import hetsim as H
-    g = H.gen_synthetic(H.bundled_spec(name), seed)
+    spec = SINGLE_ROOT if name == "single-root" else H.bundled_spec(name)
+    g = H.gen_synthetic(spec, seed)
     batches = H.make_batches(g, bsz, n_batches, H.mix_seed(seed, 0xBA7C))
-    rg = ref.RefGraph.bundled(name, seed)
+    rg = ref.RefGraph.from_spec(spec, seed) if name == "single-root" else ref.RefGraph.bundled(name, seed)
     want = rg.raf_train(2, 32, p, seed, [list(b) for b in batches], [25, 20])
     for r in range(p):  # every rank computes the same loss from the all-reduced logits
         np.testing.assert_allclose(res[r]["losses"], want["losses"], rtol=1e-3, atol=0)
