@@ -8,7 +8,10 @@
 namespace hetgpu {
 
 constexpr int kMaxProblems = 16;
-constexpr int kWChunkRows = 256;  // split-K rows per weight-gradient partial
+#ifndef HG_WCHUNK
+#define HG_WCHUNK 512
+#endif
+constexpr int kWChunkRows = HG_WCHUNK;  // split-K rows per weight-gradient partial (512 measured best)
 
 // dpre rows: g[(i*stride + offset) * ld + c], masked by H > 0 when h != nullptr
 struct DpreView {
