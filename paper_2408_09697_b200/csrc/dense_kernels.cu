@@ -10,6 +10,9 @@
 #include "adam.cuh"
 #include "kernels.cuh"
 
+#ifndef HG_CSC_WAVES
+#define HG_CSC_WAVES 8  // CTAs per SM of the backward-gather grid (8: one resident wave, measured best)
+#endif
 #ifndef HG_GATHER_WAVES
 #define HG_GATHER_WAVES 16  // CTAs per SM of the gather grids (8 resident: two waves)
 #endif
@@ -229,7 +232,7 @@ void csc_gather(const CscHop& h, AdamHyper hp, std::uint32_t* err, cudaStream_t 
   if (h.nt == 0) return;
   int items = 0;
   for (int i = 0; i < h.nt; ++i) items += h.t[i].src_cap * static_cast<int>(ceil_div(h.t[i].din, 64));
-  const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(items, 16), HG_GATHER_WAVES * kNumSMs)));
+  const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(items, 16), HG_CSC_WAVES * kNumSMs)));
   launch_pdl(k_csc_gather, grid, 256, 0, st, h, hp, err);
 }
 

@@ -36,13 +36,16 @@ constexpr int kATile = 128 * 128;  // bytes of one 128 x 32 fp32 operand tile
 constexpr int kMaxMaps = 128;
 
 template <int NT>
+#ifndef HG_USTAGES128
+#define HG_USTAGES128 3  // pipeline stages of the 128-column tiles
+#endif
 #ifndef HG_USTAGES
 #define HG_USTAGES 2  // pipeline stages of the <=64-column tiles (2 measured best: two CTAs per SM)
 #endif
 struct UStage {
   static constexpr int kB = NT * 128;
   static constexpr int kBytes = 2 * kATile + 2 * kB;  // A hi, A lo, B hi, B lo
-  static constexpr int kStages = NT <= 64 ? HG_USTAGES : 3;
+  static constexpr int kStages = NT <= 64 ? HG_USTAGES : HG_USTAGES128;
   static constexpr int kSmem = kStages * kBytes + 1024 + 128;
   static constexpr int kTmemCols = NT <= 32 ? 32 : NT <= 64 ? 64 : NT <= 128 ? 128 : 256;
 };
