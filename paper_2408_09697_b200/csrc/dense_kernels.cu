@@ -10,6 +10,9 @@
 #include "adam.cuh"
 #include "kernels.cuh"
 
+#ifndef HG_FRONT_WAVES
+#define HG_FRONT_WAVES 4  // x-extent (CTAs per SM) of the per-block relabel / transpose grids
+#endif
 #ifndef HG_CSC_WAVES
 #define HG_CSC_WAVES 8  // CTAs per SM of the backward-gather grid (8: one resident wave, measured best)
 #endif
@@ -222,9 +225,9 @@ void csc_prepare(const CscHop& h, LbScratch& lb, cudaStream_t st) {
   int cap = 1, scap = 1;
   for (int i = 0; i < h.nb; ++i) cap = std::max(cap, h.b[i].cap);
   for (int i = 0; i < h.nt; ++i) scap = std::max(scap, h.t[i].src_cap);
-  dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, 256), 4 * kNumSMs)), h.nb);
+  dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, 256), HG_FRONT_WAVES * kNumSMs)), h.nb);
   launch_pdl(k_csc_fill, grid, 256, 0, st, h);
-  dim3 g2(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(scap, 256), 4 * kNumSMs)), h.nt);
+  dim3 g2(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(scap, 256), HG_FRONT_WAVES * kNumSMs)), h.nt);
   launch_pdl(k_csc_sort, g2, 256, 0, st, h);
 }
 

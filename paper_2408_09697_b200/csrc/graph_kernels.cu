@@ -451,6 +451,9 @@ void sample_hop(const SampleHop& h, const StepScalars* sc, std::uint32_t* slow, 
 
 namespace {
 
+#ifndef HG_FRONT_WAVES
+#define HG_FRONT_WAVES 4  // x-extent (CTAs per SM) of the per-block relabel / transpose grids
+#endif
 constexpr int kFrontThreads = 256;
 
 __global__ void __launch_bounds__(kFrontThreads) k_mark_batch(const std::uint32_t* ids,
@@ -568,7 +571,7 @@ void frontier_relabel(const RelabelArgs& r, const FrontierArgs& f, cudaStream_t 
   if (r.nblk == 0) return;
   int cap = 1;
   for (int i = 0; i < r.nblk; ++i) cap = max(cap, r.b[i].cap);
-  dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, kFrontThreads), 4 * kNumSMs)), r.nblk);
+  dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, kFrontThreads), HG_FRONT_WAVES * kNumSMs)), r.nblk);
   launch_pdl(k_relabel, grid, kFrontThreads, 0, st, r, f);
 }
 
