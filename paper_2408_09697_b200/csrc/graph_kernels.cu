@@ -9,7 +9,13 @@ namespace hetgpu {
 
 namespace {
 
-constexpr int kScanThreads = 512;
+#ifndef HG_SAMPLE_UNROLL
+#define HG_SAMPLE_UNROLL 4  // sampled edges in flight per lane in the sampler's gather
+#endif
+#ifndef HG_SCAN_THREADS
+#define HG_SCAN_THREADS 512
+#endif
+constexpr int kScanThreads = HG_SCAN_THREADS;
 constexpr int kScanPer = kScanTile / kScanThreads;  // 8 elements per thread
 
 __device__ __forceinline__ std::uint32_t warp_incl_scan(std::uint32_t v) {
@@ -341,7 +347,7 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_fused(SampleHop h, Lb
   const std::uint32_t wtotal = __shfl_sync(0xffffffffu, wincl, 31);
   const std::uint32_t o0 = __shfl_sync(0xffffffffu, o, 0);
   const std::uint32_t row_base = static_cast<std::uint32_t>(base + (threadIdx.x & ~31));
-  constexpr int kUnroll = 4;
+  constexpr int kUnroll = HG_SAMPLE_UNROLL;
   for (std::uint32_t q0 = 0; q0 < wtotal; q0 += 32 * kUnroll) {  // warp-uniform trip count
     std::uint32_t at[kUnroll], pos[kUnroll];
     std::uint64_t rlo[kUnroll];
