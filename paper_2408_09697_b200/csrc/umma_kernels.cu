@@ -36,6 +36,9 @@ constexpr int kATile = 128 * 128;  // bytes of one 128 x 32 fp32 operand tile
 constexpr int kMaxMaps = 128;
 
 template <int NT>
+#ifndef HG_PROJ_NT
+#define HG_PROJ_NT 64  // widest projection tile
+#endif
 #ifndef HG_USTAGES128
 #define HG_USTAGES128 3  // pipeline stages of the 128-column tiles
 #endif
@@ -340,7 +343,7 @@ void project_umma(ProjBatch& pb, cudaStream_t st) {
   for (int g = 0; g < pb.ng; ++g) nt = std::max(nt, pick_nt(pb.g[g].ld_out));
   // at most 64 columns per tile: the top layer (C = 349) then runs 48 CTAs
   // instead of 24, which shortens its latency-bound launch (measured +2%)
-  nt = std::min(nt, 64);
+  nt = std::min(nt, HG_PROJ_NT);
   int tiles = 0;
   for (int g = 0; g < pb.ng; ++g) {
     const ProjGroup& G = pb.g[g];
