@@ -13,6 +13,9 @@
 #ifndef HG_FRONT_WAVES
 #define HG_FRONT_WAVES 4  // x-extent (CTAs per SM) of the per-block relabel / transpose grids
 #endif
+#ifndef HG_RSUM_WAVES
+#define HG_RSUM_WAVES 8  // CTAs per SM of the replica sum + Adam grid (8 measured best at p=4)
+#endif
 #ifndef HG_CSC_WAVES
 #define HG_CSC_WAVES 8  // CTAs per SM of the backward-gather grid (8: one resident wave, measured best)
 #endif
@@ -378,7 +381,7 @@ __global__ void __launch_bounds__(256) k_rsum_adam(ReplicaMerge m, ReplicaAdam a
 void replica_sum_adam(const ReplicaMerge& m, const ReplicaAdam& a, AdamHyper hp, std::uint32_t* err,
                       cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>(
-      std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(m.u.cap * ceil_div(m.din, 64), 16), 16 * kNumSMs)));
+      std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(m.u.cap * ceil_div(m.din, 64), 16), HG_RSUM_WAVES * kNumSMs)));
   switch (m.n_rep) {
     case 1: launch_pdl(k_rsum_adam<1>, grid, 256, 0, st, m, a, hp, err); break;
     case 2: launch_pdl(k_rsum_adam<2>, grid, 256, 0, st, m, a, hp, err); break;
