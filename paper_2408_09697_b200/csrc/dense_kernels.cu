@@ -147,6 +147,11 @@ __global__ void k_csc_sort(CscHop h) {
   }
 }
 
+#ifndef HG_CSC_BATCH
+#define HG_CSC_BATCH 2
+#endif
+constexpr int kCscBatch = HG_CSC_BATCH;  // dmean rows in flight per lane
+
 // one half-warp per (source row, 64-column chunk): ordered sum of the dmean rows
 // of its sampled edges; learnable leaves apply Adam to their table row directly
 __global__ void __launch_bounds__(256) k_csc_gather(CscHop h, AdamHyper hp, std::uint32_t* err) {
@@ -169,12 +174,12 @@ __global__ void __launch_bounds__(256) k_csc_gather(CscHop h, AdamHyper hp, std:
       if (f >= t.ld_dh) continue;
       const std::uint32_t lo = c ? t.offs[c - 1] : 0u, hi = t.offs[c];
       float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-      // up to 4 edges in flight: packed entries, then dmean rows
-      for (std::uint32_t x0 = lo; x0 < hi; x0 += 4) {
-        const int cnt = min(4u, hi - x0);
-        const float* rowp[4];
+      // up to kCscBatch edges in flight: packed entries, then dmean rows
+      for (std::uint32_t x0 = lo; x0 < hi; x0 += kCscBatch) {
+        const int cnt = min(static_cast<std::uint32_t>(kCscBatch), hi - x0);
+        const float* rowp[kCscBatch];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < kCscBatch; ++q) {
           rowp[q] = nullptr;
           if (q < cnt) {
             const std::uint32_t key = __ldg(t.entries + x0 + q);  // packed (block, row)
@@ -182,12 +187,12 @@ __global__ void __launch_bounds__(256) k_csc_gather(CscHop h, AdamHyper hp, std:
             rowp[q] = b.dmean + static_cast<std::size_t>(key & ((1u << kRowBits) - 1)) * b.ld_dmean + f;
           }
         }
-        float4 v[4];
+        float4 v[kCscBatch];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < kCscBatch; ++q)
           v[q] = q < cnt ? *reinterpret_cast<const float4*>(rowp[q]) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < kCscBatch; ++q) {
           s.x += v[q].x;
           s.y += v[q].y;
           s.z += v[q].z;

@@ -316,9 +316,9 @@ __global__ void __launch_bounds__(kT) k_dmean_tiles(DMeanBatch b) {
 }
 
 // ---- gather-mean: 16 lanes x float4 per (row, 64-column chunk); a warp carries
-// two such items, 8 edges in flight per lane ---------------------------------------------------
+// two such items, kGatherBatch edges in flight per lane ----------------------------------------
 #ifndef HG_GATHER_BATCH
-#define HG_GATHER_BATCH 8
+#define HG_GATHER_BATCH 5
 #endif
 constexpr int kGatherBatch = HG_GATHER_BATCH;  // neighbour rows in flight per lane
 __global__ void __launch_bounds__(256) k_gather_mean(MeanBatch m) {
@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(256) k_gather_mean(MeanBatch m) {
     const std::uint32_t lo = B.indptr[i], hi = B.indptr[i + 1];
     const float* base = B.h + c;
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-    // batches of 8 neighbours (the last one predicated): one key round trip and
+    // batches of kGatherBatch neighbours (the last one predicated): one key round trip and
     // one row round trip per batch, summed in edge order
     for (std::uint32_t e = lo; e < hi; e += kGatherBatch) {
       const std::uint32_t cnt = min(static_cast<std::uint32_t>(kGatherBatch), hi - e);
