@@ -20,7 +20,7 @@
 #define HG_CSC_WAVES 8  // CTAs per SM of the backward-gather grid (8: one resident wave, measured best)
 #endif
 #ifndef HG_GATHER_WAVES
-#define HG_GATHER_WAVES 16  // CTAs per SM of the gather grids (8 resident: two waves)
+#define HG_GATHER_WAVES 24  // CTAs per SM of the gather grids (8 resident: three waves)
 #endif
 
 namespace hetgpu {

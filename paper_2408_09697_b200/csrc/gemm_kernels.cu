@@ -9,7 +9,7 @@
 #include "gemm.cuh"
 
 #ifndef HG_GATHER_WAVES
-#define HG_GATHER_WAVES 16  // CTAs per SM of the gather grids (8 resident: two waves)
+#define HG_GATHER_WAVES 24  // CTAs per SM of the gather grids (8 resident: three waves)
 #endif
 
 namespace hetgpu {
