@@ -167,12 +167,56 @@ def run_reference(args):
         "config": {"workload": "C2 ogbn-mag-shape (BASELINE configs[1]) 2-layer RGCN hidden 64, fanout [25,20], "
                                "batch 1024 (run_raf_batch p=1 on CPU: sample + forward + loss + backward; the Adam updates are not timed)",
                    "batch_per_step": threads, "graph_seed": SEED},
-        "epoch_time_s": EPOCH_BATCHES * ms_per_batch / 1000.0 / threads,
+        # ms_per_batch is already the wall time per batch amortised over the threads
+        "epoch_time_s": EPOCH_BATCHES * ms_per_batch / 1000.0,
         "cpu_baseline": {"value": value, "unit": "edges/s", "cores": threads, "kind": "reference", "cpu_model": cpu_model(),
                          "sample": f"{steps} steps x {threads} concurrent run_raf_batch calls ({time_total:.1f} s)"},
         "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+TRAFFIC_FILE = "profiles/r02_traffic.json"
+
+
+def lib_digest():
+    import hashlib
+    try:
+        with open(os.path.join(ROOT, "paper_2408_09697_b200", "libhetgpu.so"), "rb") as f:
+            return hashlib.sha256(f.read()).hexdigest()[:16]
+    except OSError:
+        return None
+
+
+def load_traffic():
+    try:
+        with open(os.path.join(ROOT, TRAFFIC_FILE)) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def parity_check(H, g, g_ref, batch, rng_seed):
+    """The first timed batch on a freshly initialised engine against the reference
+    (oracle/_ref flat_step, which check_equivalence pins to run_raf_batch at p=1;
+    raf.cpp:639-660): sampled blocks bit-exact, loss and logits within 1e-3."""
+    import numpy as np
+    eng = H.Engine.for_experiment(g, FANOUTS, HIDDEN, SEED, batch_cap=BATCH_PER_GPU)
+    rep = eng.step(batch, rng_seed, 0, train=False)
+    want = g_ref.flat_step(2, HIDDEN, H.mix_seed(SEED, 0xD0DE1), H.mix_seed(SEED, 0x1EA4A), batch, FANOUTS,
+                           rng_seed, want_init=False)
+    blocks = [n for n in want if n.startswith(("frontier", "hop")) and not n.endswith(".rels")]
+    got = eng.read("logits", *blocks)
+    bit_exact = all(np.array_equal(np.asarray(got[n]).ravel(), np.asarray(want[n]).ravel()) for n in blocks)
+    lw = want["logits"]
+    err = float(np.abs(got["logits"] - lw).max() / max(1e-30, float(np.abs(lw).max())))
+    loss_ref = float(want["loss"][0])
+    loss_err = abs(rep["loss"] - loss_ref) / abs(loss_ref)
+    del eng
+    return {"ok": bool(bit_exact and err <= 1e-3 and loss_err <= 1e-3), "blocks_bit_exact": bool(bit_exact),
+            "n_block_arrays": len(blocks), "loss": rep["loss"], "loss_ref": loss_ref, "loss_rel_err": loss_err,
+            "logits_rel_err": err, "sampled_edges": rep["sampled_edges"],
+            "oracle": "oracle/_ref flat_step (the reference compiled from its sources), first timed batch, fresh init"}
 
 
 # ---------------------------------------------------------------------------------------------
@@ -269,6 +313,23 @@ def run_b200(args):
     barrier()
     e2e_s = reduce(time.perf_counter() - te, MAX)
     dbg("e2e done")
+    # ---- one real epoch through the public API (every batch of the target type once,
+    # global batch 1024 x N, host batches in, loss out), timed by the wall clock
+    ep_b = H.make_batches(g, batch, 0, H.mix_seed(SEED, 0xBA7C + 1))
+    ep_s = [H.mix_seed(SEED, 0xB000 + 10_000 + i) for i in range(len(ep_b))]
+    barrier()
+    te = time.perf_counter()
+    ep_edges = 0
+    eng.prefetch(ep_b[0], ep_s[0])
+    for i, (b, s) in enumerate(zip(ep_b, ep_s)):
+        if i + 1 < len(ep_b):
+            eng.prefetch(ep_b[i + 1], ep_s[i + 1])
+        rep = eng.step(b, s, i % n, train=True)
+        ep_edges += rep["sampled_edges"]
+    barrier()
+    ep_time = reduce(time.perf_counter() - te, MAX)
+    ep_edges = reduce(float(ep_edges), SUM)
+    dbg("epoch done")
     e2e_edges = reduce(float(edges_rank), SUM)
     # device-timed steps sampled the same kind of batches; count their edges exactly
     # by replaying the sampler only (cheap) on this rank
@@ -296,12 +357,15 @@ def run_b200(args):
     # is reported beside them, not as the roofline kernel.
     alg_by = {"aggregate": alg[1], "csc_gather": alg[3], "aggregate_top": alg[2], "sample": alg[0]}
 
+    lib_sha = lib_digest()
+    traffic_rec = load_traffic()
+
     def traffic_of(k):
-        # DRAM bytes per launch of the roofline kernel from the committed ncu --set
-        # full capture (profiles/r01_traffic.json); ncu is never run inside the bench
+        # DRAM bytes per launch of the kernel class from the committed ncu --set full
+        # capture (profiles/r02_traffic.json, stamped with the library digest it was
+        # taken on); ncu is never run inside the bench
         try:
-            with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
-                return int(json.load(f)[k]["dram_bytes_per_launch"])
+            return int(traffic_rec["kernels"][k]["dram_bytes_per_launch"])
         except Exception:
             return None
 
@@ -326,15 +390,26 @@ def run_b200(args):
         "config": {"workload": "C2 ogbn-mag-shape (BASELINE configs[1]) 2-layer RGCN hidden 64, fanout [25,20]",
                    "global_batch": batch, "batch_per_gpu": BATCH_PER_GPU, "parallelism": f"meta-partition p={n}",
                    "graph_seed": SEED, "l2": "not flushed: tables 1.3 GB + CSR 0.3 GB >> 126 MB L2, new rows every step"},
-        "epoch_time_s": (ms_max / args.steps) * EPOCH_BATCHES / n / 1000.0,
+        # a real epoch (len(ep_b) batches of 1024 x N) through Engine.prefetch + Engine.step
+        "epoch_time_s": ep_time,
+        "epoch": {"batches": len(ep_b), "sampled_edges": ep_edges, "time_s": ep_time,
+                  "edges_per_s": ep_edges / ep_time, "path": "Engine.prefetch + Engine.step, host batches",
+                  "device_extrapolated_s": (ms_max / args.steps) * len(ep_b) / 1000.0},
+        "lib_sha256_16": lib_sha,
         "sampled_edges_per_step": dev_edges / args.steps,
         "gpu_launches": launches * args.steps,
         "launches_per_step": launches,
         "clocks": clk.summary(),
+        # H2D: the batch ids + the 32-byte step-scalar record; D2H: the 24-byte readback
+        # (loss, error flags, sampled edges) and, at p > 1, the AGG_all counter row
         "e2e": {"value": e2e_value, "unit": "edges/s", "h2d_bytes_per_step": 4 * batch + 32,
-                "d2h_bytes_per_step": 24, "ms_per_step": 1000.0 * e2e_s / args.steps},
+                "d2h_bytes_per_step": 24 + (4 * ((349 + 3) // 4) if n > 1 else 0),
+                "ms_per_step": 1000.0 * e2e_s / args.steps},
         "roofline": {"bound": "hbm", "kernel": roof_kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic_of(roof_kernel), "traffic_source": "profiles/r01_traffic.json (ncu --set full)", "peak_kind": peak_kind,
+                     "frac": achieved / peak, "traffic": traffic_of(roof_kernel),
+                     "traffic_source": TRAFFIC_FILE + " (ncu --set full)",
+                     "traffic_build_match": traffic_rec.get("lib_sha256_16") == lib_sha, "peak_kind": peak_kind,
+                     "tensor_pipe_pct": traffic_rec.get("tensor_pipe_pct"),
                      "alg_bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms,
                      "kernels": {k: roof_of(k) for k in alg_by}},
         "kernel_share": {k: v / max(1e-9, sum(classes.values())) for k, v in sorted(classes.items())},
@@ -349,6 +424,7 @@ def run_b200(args):
         v, sample, secs, g_ref = cpu_baseline_sample(threads, 8 * threads)
         # the reference as shipped is single-threaded: one core, two batches
         v1, _, secs1, _ = cpu_baseline_sample(1, 2, g_ref)
+        line["parity"] = parity_check(H, g, g_ref, batches[args.warmup], seeds[args.warmup])
         line["cpu_baseline"] = {"value": v, "unit": "edges/s", "cores": threads, "kind": "reference",
                                 "sample": sample + f" ({secs:.1f} s)", "cpu_model": cpu_model(),
                                 "single_core": {"value": v1, "unit": "edges/s", "ms_per_batch": 1000.0 * secs1 / 2,

@@ -58,7 +58,7 @@ def lib():
             "ref_sample_neighbors": [vp, i32, vp, C.c_uint, i32, u64, i32, i32],
             "ref_sample_khop": [vp, vp, i32, vp, i32, u64, vp, vp],
             "ref_flat_step": [vp, i32, i32, u64, u64, vp, i32, vp, u64, i32],
-            "ref_raf_train": [vp, i32, i32, i32, u64, vp, vp, i32, vp, i32],
+            "ref_raf_train": [vp, i32, i32, i32, u64, vp, vp, i32, vp, i32, i32],
             "ref_check_equivalence": [vp, i32, i32, i32, u64, u64, vp, i32, vp, u64, i32],
             "ref_cache_sim": [vp, i32, vp, i32, u64, i32, u64, C.c_double, C.c_double, C.c_double, i32],
             "ref_run_experiment": [C.c_char_p],
@@ -172,17 +172,20 @@ class RefGraph:
                                            _ptr(flat), _ptr(cnt)))
 
     def flat_step(self, k, hidden, model_seed, learn_seed, batch, fanouts, rng_seed, want_init=True):
+        """want_init: True = initial state with full learnable tables; "rows" = the
+        learnable tables only at the rows the batch touches (init/post .learn_rows)."""
+        want_init = 2 if want_init == "rows" else int(bool(want_init))
         bt = np.asarray(batch, np.uint32)
         fo = np.asarray(fanouts, np.int32)
         return _take(lib().ref_flat_step(self.h, k, hidden, model_seed, learn_seed, _ptr(bt), len(bt),
-                                         _ptr(fo), rng_seed, int(want_init)))
+                                         _ptr(fo), rng_seed, want_init))
 
-    def raf_train(self, k, hidden, p, seed, batches, fanouts, elem_bytes=4):
+    def raf_train(self, k, hidden, p, seed, batches, fanouts, elem_bytes=4, full_tables=True):
         flat = np.asarray([v for b in batches for v in b], np.uint32)
         cnt = np.asarray([len(b) for b in batches], np.int32)
         fo = np.asarray(fanouts, np.int32)
         return _take(lib().ref_raf_train(self.h, k, hidden, p, seed, _ptr(flat), _ptr(cnt),
-                                         len(batches), _ptr(fo), elem_bytes))
+                                         len(batches), _ptr(fo), elem_bytes, int(full_tables)))
 
     def check_equivalence(self, k, hidden, p, model_seed, learn_seed, batch, fanouts, rng_seed,
                           designated):

@@ -392,10 +392,27 @@ void* ref_flat_step(void* sp, int k, int hidden, unsigned long long model_seed,
                                       g.num_classes, &dlogits);
     GradientSet grads = backward_flat(g, tree, model, tape, dlogits);
 
+    // want_init: 0 = no initial state, 1 = full learnable tables, 2 = learnable
+    // tables only at the rows this batch touches (the gradient ids): the
+    // ogbn-mag-shaped tables are ~0.6 GB each in f64.
+    const bool rows_only = want_init == 2;
+    auto rows_of = [](const Matrix& m, const std::vector<NodeId>& ids) {
+      Matrix r(ids.size(), m.cols);
+      for (std::size_t i = 0; i < ids.size(); ++i)
+        for (std::size_t c = 0; c < m.cols; ++c) r.at(i, c) = m.at(ids[i], c);
+      return r;
+    };
     auto* b = new Bundle;
     if (want_init) {
       put_model(*b, model, "init");
-      for (const auto& [t, tab] : store.tables) b->put_matrix("init.learn.t" + std::to_string(t), tab.w);
+      for (const auto& [t, tab] : store.tables) {
+        if (!rows_only) {
+          b->put_matrix("init.learn.t" + std::to_string(t), tab.w);
+        } else if (grads.feature_grads.count(t)) {
+          b->put_matrix("init.learn_rows.t" + std::to_string(t),
+                        rows_of(tab.w, grads.feature_grads.at(t).first));
+        }
+      }
     }
     put_blocks(*b, blocks, g.reg.num_node_types());
     for (int d = 0; d <= k; ++d)
@@ -416,6 +433,15 @@ void* ref_flat_step(void* sp, int k, int hidden, unsigned long long model_seed,
       adam_update_rows(store.tables.at(t), fg.first, fg.second);
     put_model(*b, model, "post");
     for (const auto& [t, tab] : store.tables) {
+      if (rows_only) {
+        if (!grads.feature_grads.count(t)) continue;
+        const auto& ids = grads.feature_grads.at(t).first;
+        b->put_matrix("post.learn_rows.t" + std::to_string(t), rows_of(tab.w, ids));
+        b->put_matrix("post.learn_m_rows.t" + std::to_string(t), rows_of(tab.m, ids));
+        b->put_matrix("post.learn_v_rows.t" + std::to_string(t), rows_of(tab.v, ids));
+        b->put_scalar_i64("post.learn_step.t" + std::to_string(t), tab.step);
+        continue;
+      }
       b->put_matrix("post.learn.t" + std::to_string(t), tab.w);
       b->put_matrix("post.learn_m.t" + std::to_string(t), tab.m);
       b->put_matrix("post.learn_v.t" + std::to_string(t), tab.v);
@@ -431,7 +457,7 @@ void* ref_flat_step(void* sp, int k, int hidden, unsigned long long model_seed,
 // The batches are given explicitly (flat + counts).
 void* ref_raf_train(void* sp, int k, int hidden, int p, unsigned long long seed,
                     const unsigned* batches_flat, const int* batch_counts, int n_batches,
-                    const int* fanouts, int elem_bytes) {
+                    const int* fanouts, int elem_bytes, int full_tables) {
   return guarded([&]() -> void* {
     const HetGraph& g = static_cast<Session*>(sp)->g;
     const Metagraph m = build_metagraph(g);
@@ -485,7 +511,7 @@ void* ref_raf_train(void* sp, int k, int hidden, int p, unsigned long long seed,
     b->put_u64("target_only_ok", target_ok);
     put_model(*b, model, "final");
     for (const auto& [t, tab] : store.tables) {
-      b->put_matrix("final.learn.t" + std::to_string(t), tab.w);
+      if (full_tables) b->put_matrix("final.learn.t" + std::to_string(t), tab.w);
       b->put_scalar_i64("final.learn_step.t" + std::to_string(t), tab.step);
     }
     b->put_scalar_i64("final.model_step", mst.step);

@@ -450,7 +450,12 @@ int hg_engine_bench(hg_engine* e, const uint32_t* batches, const int* lens, cons
   return guard<int>(-1, [&] {
     Engine& en = *e->e;
     std::size_t total = 0;
-    for (int i = 0; i < n_steps; ++i) total += lens[i];
+    for (int i = 0; i < n_steps; ++i) {
+      if (lens[i] <= 0) throw std::invalid_argument("empty batch");
+      if (lens[i] > en.batch_cap()) throw std::invalid_argument("batch larger than the engine's batch capacity");
+      en.validate_batch(batches + total, lens[i]);
+      total += lens[i];
+    }
     // inputs resident in HBM before the timed region: batch ids and per-step scalars
     std::vector<StepScalars> sc(n_steps);
     for (int i = 0; i < n_steps; ++i) sc[i] = en.next_scalars(seeds[i], lens[i], 0, train != 0);

@@ -53,8 +53,15 @@ __global__ void __launch_bounds__(kThreads) k_cross_entropy(LossArgs a) {
       if (lane == 0) a.row_loss[i] = 0.0;
       continue;
     }
-    if (y < 0 || y >= a.C) {
-      if (lane == 0) atomicOr(a.err, 2u);
+    if (y < 0 || y >= a.C) {  // never reached: the host validates labels before enqueueing
+      for (int c = lane; c < a.C; c += 32) {
+        dz[c] = 0.f;
+        if (dzl) dzl[c] = 0.f;
+      }
+      if (lane == 0) {
+        a.row_loss[i] = 0.0;
+        atomicOr(a.err, 2u);
+      }
       continue;
     }
     // fp32 log-sum-exp (the reference's f64 agrees to ~1e-7 relative)

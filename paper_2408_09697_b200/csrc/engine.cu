@@ -486,6 +486,12 @@ void Engine::upload(const Graph& g) {
     HG_CUDA(cudaMemcpyAsync(tb.w, host.data(), host.size() * 4, cudaMemcpyHostToDevice, st_));
     HG_CUDA(cudaStreamSynchronize(st_));  // host staging buffer goes out of scope
   }
+  // target ids whose label is outside [0, C): cross_entropy throws for them
+  // (hgnn.cpp:289-291), so step()/prefetch() reject such batches on the host
+  // before anything is enqueued
+  bad_labels_.clear();
+  for (std::size_t v = 0; v < g.labels.size(); ++v)
+    if (g.labels[v] < 0 || g.labels[v] >= num_classes_) bad_labels_.push_back(static_cast<NodeId>(v));
   labels_ = static_cast<std::int32_t*>(alloc(g.labels.size() * 4));
   HG_CUDA(cudaMemcpyAsync(labels_, g.labels.data(), g.labels.size() * 4, cudaMemcpyHostToDevice, st_));
 
@@ -927,9 +933,13 @@ void Engine::run_sampling(cudaStream_t ss) {
     }
     for (const auto& c : cscs_) {
       const bool leaf_learnable = c.hop == o_.k && tables_[c.src_t].learnable;
+      // the sparse Adam is fused here (w, m, v read + written: 6 row passes, +1 for a
+      // retained gradient row) unless the type is exchanged between replicas, whose
+      // Adam runs after the merge (k_rsum_adam): then only the gradient row is written
+      const bool fused_adam = leaf_learnable && !xchg_type(c.src_t);
       ab.c_rows[ab.ncsc] = front(c.hop, c.src_t).count;
       ab.c_din[ab.ncsc] = c.din;
-      ab.c_row_bytes_mult[ab.ncsc] = leaf_learnable ? (retain_grads_ ? 7 : 6) : 1;
+      ab.c_row_bytes_mult[ab.ncsc] = fused_adam ? (retain_grads_ ? 7 : 6) : 1;
       ++ab.ncsc;
     }
     launch_pdl(k_alg_bytes, 1, 32, 0, ss, ab, alg_bytes_);
@@ -1424,13 +1434,21 @@ StepScalars Engine::next_scalars(std::uint64_t rng_seed, int n, int designated, 
   return sc;
 }
 
+void Engine::validate_batch(const NodeId* batch, int n, bool labels) const {
+  for (int i = 0; i < n; ++i)
+    if (batch[i] >= type_counts_[target_])
+      throw std::invalid_argument("seed node id out of range: " + std::to_string(batch[i]));
+  if (labels && !o_.sample_only && !bad_labels_.empty())
+    for (int i = 0; i < n; ++i)
+      if (std::binary_search(bad_labels_.begin(), bad_labels_.end(), batch[i]))
+        throw std::invalid_argument("label out of range for node " + std::to_string(batch[i]));
+}
+
 void Engine::prefetch(const NodeId* batch, int n, std::uint64_t rng_seed) {
   if (o_.sample_only) throw std::invalid_argument("a sampler engine has no model to step");
   if (n > o_.batch_cap) throw std::invalid_argument("batch larger than the engine's batch capacity");
   if (n <= 0) throw std::invalid_argument("empty batch");
-  for (int i = 0; i < n; ++i)
-    if (batch[i] >= type_counts_[target_])
-      throw std::invalid_argument("seed node id out of range: " + std::to_string(batch[i]));
+  validate_batch(batch, n);
   if (pending_slots_.size() >= 2) throw std::runtime_error("two batches already prefetched: step one first");
   const int s = next_slot_;
   next_slot_ ^= 1;
@@ -1598,9 +1616,7 @@ std::vector<double> Engine::algorithmic_bytes() {
 void Engine::sample_only(const NodeId* batch, int n, std::uint64_t rng_seed) {
   if (n > o_.batch_cap) throw std::invalid_argument("batch larger than the engine's batch capacity");
   if (n <= 0) throw std::invalid_argument("empty batch");
-  for (int i = 0; i < n; ++i)
-    if (batch[i] >= type_counts_[target_])
-      throw std::invalid_argument("seed node id out of range: " + std::to_string(batch[i]));
+  validate_batch(batch, n, /*labels=*/false);
   quiesce();
   bind_slot(0);
   std::memcpy(h_batch_, batch, sizeof(NodeId) * n);

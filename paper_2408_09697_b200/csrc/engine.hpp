@@ -100,6 +100,10 @@ class Engine {
   // future batch into the other of two sample slots on the sampling stream, so it
   // runs while the current step trains (at most two batches in flight).
   void prefetch(const NodeId* batch, int n, std::uint64_t rng_seed);
+  // seed ids in range and (labels) every seed's label in [0, C): the reference's
+  // std::invalid_argument cases (sampling.cpp:44-47, hgnn.cpp:289-291), raised
+  // on the host before anything is enqueued
+  void validate_batch(const NodeId* batch, int n, bool labels = true) const;
   // Benchmark inner loop, inputs resident in HBM: sample a batch into the next
   // slot (d_ss: its sampling scalars), then train the oldest sampled slot.
   void prefetch_device(const std::uint32_t* d_ids, int n, const StepScalars* d_ss);
@@ -188,6 +192,7 @@ class Engine {
   const Tree& local_tree() const { return tree_; }
   const std::vector<std::vector<int>>& hop_rels() const { return hop_rels_; }
   int model_step() const { return static_cast<int>(model_step_); }
+  int batch_cap() const { return o_.batch_cap; }
 
  private:
   struct BlockBuf {
@@ -290,6 +295,7 @@ class Engine {
   std::vector<std::uint64_t> maxdeg_;
   std::vector<TypeTable> tables_;
   std::int32_t* labels_ = nullptr;
+  std::vector<NodeId> bad_labels_;  // target ids with labels outside [0, C), sorted
 
   // ---- two sample slots: everything sampling writes exists twice; bind_slot(s)
   // points the working pointers below at slot s (host-side rebinding: each

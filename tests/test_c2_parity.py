@@ -1,0 +1,166 @@
+"""Parity on the benched configurations themselves (BASELINE configs[1] = C2, the
+ogbn-mag-shaped synthetic graph, and configs[0] = C1, the toy graph), against the
+compiled reference (oracle/_ref):
+
+* the graph the bench trains on is the reference's gen_synthetic output, array for
+  array (harness.cpp:74-186) — CPU;
+* sampled blocks and frontiers of the first two run_experiment batches are
+  bit-exact (batch 1024, fanout [25,20]; sampling.cpp:41-103);
+* one full training step (forward tape, logits, loss, dlogits, weight and
+  learnable-row gradients, post-Adam model and learnable rows with their Adam
+  moments) within 1e-3 relative (hgnn.cpp:215-410);
+* three consecutive run_raf_batch losses and the model after three Adam steps
+  (raf.cpp:344-530, harness.cpp:400-423).
+"""
+import numpy as np
+import pytest
+
+from tests.util import assert_adam_close, assert_close
+
+TOL = 1e-3
+SEED = 1
+FANOUTS = [25, 20]
+HIDDEN = 64
+BATCH = 1024
+
+
+@pytest.fixture(scope="module")
+def c2(H, ref):
+    spec = H.ogbn_mag_spec()
+    g = H.gen_synthetic(spec, SEED)
+    rg = ref.RefGraph.from_spec(spec, SEED)
+    batches = H.make_batches(g, BATCH, 3, H.mix_seed(SEED, 0xBA7C))
+    seeds = [H.mix_seed(SEED, 0xB000 + i) for i in range(3)]
+    return g, rg, batches, seeds
+
+
+def test_c2_graph_matches_oracle(c2):
+    g, rg, _, _ = c2
+    ours, want = g.export(), rg.export()
+    names_only = {"type_names", "etype_names", "rel_etype"}  # string tables of the registry
+    assert set(want) - names_only <= set(ours), sorted(set(want) - set(ours))
+    assert any(n.startswith("feat.") for n in want) and "labels" in want
+    for n, w in want.items():
+        if n in names_only:
+            continue
+        o = ours[n]
+        if n.startswith("feat."):
+            # features are f64 in the reference and f32 tables here: the same draws, rounded once
+            assert o.dtype == np.float32 and np.array_equal(o, w.astype(np.float32)), n
+        else:
+            assert np.array_equal(np.asarray(o).ravel(), np.asarray(w).ravel()), n
+
+
+def _engine(H, g, **kw):
+    return H.Engine(g, FANOUTS, hidden=HIDDEN, batch_cap=BATCH, model_seed=H.mix_seed(SEED, 0xD0DE1),
+                    learn_seed=H.mix_seed(SEED, 0x1EA4A), **kw)
+
+
+def _check_blocks(got, want, what):
+    keys = [n for n in want if n.startswith(("frontier", "hop")) and not n.endswith(".rels")]
+    assert keys
+    for n in keys:
+        assert n in got, f"{what}: missing {n}"
+        assert np.array_equal(np.asarray(got[n]).ravel(), np.asarray(want[n]).ravel()), f"{what}: {n}"
+
+
+@pytest.mark.gpu
+def test_c2_blocks_and_train_step(H, ref, c2):
+    g, rg, batches, seeds = c2
+    eng = _engine(H, g)
+    names = eng.tensor_names()
+    blk = [n for n in names if n.startswith(("frontier", "hop")) and not n.endswith(".col")]
+    # batch 1 first (forward only): blocks and frontiers bit-exact
+    w1 = rg.flat_step(2, HIDDEN, H.mix_seed(SEED, 0xD0DE1), H.mix_seed(SEED, 0x1EA4A), batches[1], FANOUTS,
+                      seeds[1], want_init=False)
+    r1 = eng.step(batches[1], seeds[1], 0, train=False)
+    _check_blocks(eng.read(*blk), w1, "C2 batch 1")
+    assert abs(r1["loss"] - float(w1["loss"][0])) <= TOL * abs(float(w1["loss"][0]))
+    sampled = sum(len(w1[n]) for n in w1 if n.endswith(".src_ids"))
+    assert r1["sampled_edges"] == sampled
+    # batch 0: the full training step
+    want = rg.flat_step(2, HIDDEN, H.mix_seed(SEED, 0xD0DE1), H.mix_seed(SEED, 0x1EA4A), batches[0], FANOUTS,
+                        seeds[0], want_init="rows")
+    # initial model slots are the reference's init rounded to f32
+    for n in [x for x in want if x.startswith("init.r")]:
+        got_w = eng.read("post." + n[len("init."):])["post." + n[len("init."):]]
+        assert np.array_equal(got_w, want[n].astype(np.float32).astype(np.float64)), n
+    fwd = eng.step(batches[0], seeds[0], 0, train=False)
+    got = eng.read(*[n for n in names if not n.startswith(("post.", "grad."))])
+    _check_blocks(got, want, "C2 batch 0")
+    assert abs(fwd["loss"] - float(want["loss"][0])) <= TOL * abs(float(want["loss"][0]))
+    assert_close(got["logits"], want["logits"], TOL, "C2 logits")
+    assert_close(got["dlogits"], want["dlogits"], TOL, "C2 dlogits")
+    checked = 0
+    for n in want:
+        if n.startswith(("H", "mean.")):
+            assert n in got, n
+            assert_close(got[n], want[n], TOL, f"C2 {n}")
+            checked += 1
+    assert checked >= 9 + 6  # 9 relation means (6 at layer 1, 3 at layer 2) + H per (depth, type)
+    # the same batch with backward + Adam
+    rep = eng.step(batches[0], seeds[0], 0, train=True)
+    assert rep["loss"] == fwd["loss"]
+    got = eng.read(*[n for n in names if n.startswith(("grad.", "post.r", "post.learn_step"))])
+    for n in want:
+        if n.startswith("grad.w."):
+            assert_close(got[n], want[n], TOL, f"C2 {n}")
+        elif n.startswith("grad.f.") and n.endswith(".ids"):
+            assert np.array_equal(got[n], want[n]), n
+        elif n.startswith("grad.f.") and n.endswith(".rows"):
+            assert_close(got[n], want[n], TOL, f"C2 {n}")
+        elif n.startswith("post.r"):
+            assert_adam_close(got[n], want[n], None, steps=1, what=f"C2 {n}")
+        elif n.startswith("post.learn_step.t"):
+            assert int(got[n][0]) == int(want[n][0]), n
+    # learnable rows after the sparse Adam (w, m, v at the touched rows)
+    for n in want:
+        if not n.startswith("post.learn_rows.t"):
+            continue
+        t = n.split(".t")[-1]
+        ids = want[f"grad.f.t{t}.ids"].astype(np.int64)
+        full = eng.read(f"post.learn.t{t}", f"post.learn_m.t{t}", f"post.learn_v.t{t}")
+        assert_adam_close(full[f"post.learn.t{t}"][ids], want[n], None, steps=1, what=f"C2 {n}")
+        assert_close(full[f"post.learn_m.t{t}"][ids], want[f"post.learn_m_rows.t{t}"], TOL, f"C2 m.t{t}")
+        assert_close(full[f"post.learn_v.t{t}"][ids], want[f"post.learn_v_rows.t{t}"], TOL, f"C2 v.t{t}")
+
+
+@pytest.mark.gpu
+def test_c2_run_raf_batch_losses(H, ref, c2):
+    g, rg, batches, seeds = c2
+    want = rg.raf_train(2, HIDDEN, 1, SEED, [list(b) for b in batches], FANOUTS, full_tables=False)
+    eng = H.Engine.for_experiment(g, FANOUTS, HIDDEN, SEED, batch_cap=BATCH)
+    reps = [eng.step(b, s, 0) for b, s in zip(batches, seeds)]
+    np.testing.assert_allclose([r["loss"] for r in reps], want["losses"], rtol=TOL, atol=0)
+    for r, sb in zip(reps, want["sync_bytes"]):
+        assert r["sync_bytes"] == int(sb)
+    got = eng.read(*[n for n in eng.tensor_names() if n.startswith(("post.r", "post.learn_step"))])
+    for n in want:
+        if n.startswith("final.r"):
+            assert_adam_close(got["post." + n[len("final."):]], want[n], None, max_flip_frac=5e-3,
+                              steps=len(batches), what=f"C2 {n}")
+        if n.startswith("final.learn_step.t"):
+            t = n.split(".t")[-1]
+            assert int(got[f"post.learn_step.t{t}"][0]) == int(want[n][0]), n
+
+
+@pytest.mark.gpu
+def test_c1_train_step(H, ref):
+    # BASELINE configs[0]: the toy graph, fanout [10,10], one full step
+    spec = H.toy_spec()
+    g = H.gen_synthetic(spec, SEED)
+    rg = ref.RefGraph.from_spec(spec, SEED)
+    batch = H.make_batches(g, BATCH, 1, H.mix_seed(SEED, 0xBA7C))[0]
+    rs = H.mix_seed(SEED, 0xB000)
+    want = rg.flat_step(2, HIDDEN, 3, 4, batch, [10, 10], rs, want_init="rows")
+    eng = H.Engine(g, [10, 10], hidden=HIDDEN, batch_cap=BATCH, model_seed=3, learn_seed=4)
+    names = eng.tensor_names()
+    rep = eng.step(batch, rs, 0, train=True)
+    got = eng.read(*[n for n in names if not n.startswith("post.learn")])
+    _check_blocks(got, want, "C1")
+    assert abs(rep["loss"] - float(want["loss"][0])) <= TOL * abs(float(want["loss"][0]))
+    for n in want:
+        if n.startswith(("logits", "dlogits", "mean.", "grad.w.")) or (n.startswith("H") and not n.startswith("H2")):
+            assert_close(got[n], want[n], TOL, f"C1 {n}")
+        elif n.startswith("post.r"):
+            assert_adam_close(got[n], want[n], None, steps=1, what=f"C1 {n}")

@@ -89,9 +89,10 @@ def test_raf_multi_gpu_matches_reference(ref, name, p, shard):
                 assert np.array_equal(seen[n], v), f"replicas disagree on {n}"
             seen[n] = v
             if n.startswith("post.r"):
-                assert_adam_close(v, want["final." + n[len("post."):]], None, max_flip_frac=5e-3, what=f"rank {r}: {n}")
+                assert_adam_close(v, want["final." + n[len("post."):]], None, max_flip_frac=5e-3, steps=n_batches,
+                                  what=f"rank {r}: {n}")
             elif n.startswith("post.learn.t"):
-                assert_adam_close(v, want["final.learn.t" + n.split(".t")[-1]], None, max_flip_frac=5e-3,
+                assert_adam_close(v, want["final.learn.t" + n.split(".t")[-1]], None, max_flip_frac=5e-3, steps=n_batches,
                                   what=f"rank {r}: {n}")
             elif n.startswith("post.learn_step.t"):
                 assert int(v[0]) == int(want["final.learn_step.t" + n.split(".t")[-1]][0]), (r, n)

@@ -101,14 +101,16 @@ def test_raf_training_trajectory(H, ref, name):
     for n in want:
         if n.startswith("final.r"):
             key = "post." + n[len("final."):]
-            assert_adam_close(got[key], want[n], None, max_flip_frac=5e-3, what=f"{name}: {key}")
+            assert_adam_close(got[key], want[n], None, max_flip_frac=5e-3, steps=len(batches),
+                              what=f"{name}: {key}")
         if n.startswith("final.learn_step.t"):
             t = n.split(".t")[-1]
             mine = int(got[f"post.learn_step.t{t}"][0]) if f"post.learn_step.t{t}" in got else 0
             assert mine == int(want[n][0]), f"{name}: step of type {t}"
         if n.startswith("final.learn.t") and "post.learn.t" + n.split(".t")[-1] in got:
             key = "post.learn.t" + n.split(".t")[-1]
-            assert_adam_close(got[key], want[n], None, max_flip_frac=5e-3, what=f"{name}: {key}")
+            assert_adam_close(got[key], want[n], None, max_flip_frac=5e-3, steps=len(batches),
+                              what=f"{name}: {key}")
 
 
 @pytest.mark.parametrize("name", ["mag-mini", "donor-mini"])

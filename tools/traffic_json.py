@@ -1,0 +1,99 @@
+"""Per-kernel-class DRAM traffic and tensor-pipe utilisation from one `ncu --set full`
+capture of a bench step, stamped with the library digest and git head it was taken
+on (bench.py reads it as roofline.traffic and checks the stamp).
+
+    python tools/traffic_json.py gpurun_out/prof_step.ncu-rep "<ncu command>" > profiles/r02_traffic.json
+
+Classes follow bench.py's profile classes: the first k_gather_mean launch of a step
+is the layer-1 aggregation ("aggregate"), the second the top layer
+("aggregate_top"); k_csc_gather launches are averaged ("csc_gather"); the sampler
+("sample"); every k_umma instantiation is its own class (tensor pipe % reported).
+"""
+from __future__ import annotations
+
+import collections
+import csv
+import hashlib
+import io
+import json
+import os
+import re
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def rows_of(path):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True,
+                         check=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h = rows[0]
+    return [dict(zip(h, r)) for r in rows[2:]]
+
+
+def num(d, k):
+    try:
+        return float(str(d.get(k, "nan")).replace(",", ""))
+    except ValueError:
+        return float("nan")
+
+
+def short(name):
+    n = re.sub(r"(hetgpu::)?(\(anonymous namespace\)|<unnamed>)::|^void ", "", name).strip()
+    if n.endswith(")"):  # drop the parameter list (the trailing balanced group)
+        depth = 0
+        for i in range(len(n) - 1, -1, -1):
+            depth += {")": 1, "(": -1}.get(n[i], 0)
+            if depth == 0:
+                n = n[:i]
+                break
+    return n.strip()
+
+
+def main():
+    path, cmd = sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else ""
+    acc = collections.defaultdict(list)
+    gather_seen = 0
+    for d in rows_of(path):
+        nm = short(d.get("Kernel Name", "?"))
+        if nm.startswith("k_gather_mean"):
+            cls = "aggregate" if gather_seen % 2 == 0 else "aggregate_top"
+            gather_seen += 1
+        elif nm.startswith("k_csc_gather"):
+            cls = "csc_gather"
+        elif nm.startswith("k_sample_fused"):
+            cls = "sample"
+        else:
+            cls = nm
+        acc[cls].append(d)
+    out = {}
+    for cls, ds in acc.items():
+        rd = sum(num(d, "dram__bytes_read.sum") for d in ds) / len(ds)
+        wr = sum(num(d, "dram__bytes_write.sum") for d in ds) / len(ds)
+        us = sum(num(d, "gpu__time_duration.sum") for d in ds) / len(ds)
+        unit = ds[0].get("gpu__time_duration.sum", "")
+        e = {"launches": len(ds), "dram_bytes_per_launch": int(rd + wr), "read": int(rd), "write": int(wr),
+             "duration_per_launch": us,
+             "dram_pct_of_peak": sum(num(d, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed") for d in ds) / len(ds),
+             "occupancy_pct": sum(num(d, "sm__warps_active.avg.pct_of_peak_sustained_active") for d in ds) / len(ds)}
+        tp = [num(d, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active") for d in ds]
+        tp = [x for x in tp if x == x]
+        if tp and max(tp) > 0:
+            e["tensor_pipe_pct"] = sum(tp) / len(tp)
+        out[cls] = e
+    lib = os.path.join(ROOT, "paper_2408_09697_b200", "libhetgpu.so")
+    with open(lib, "rb") as f:
+        sha = hashlib.sha256(f.read()).hexdigest()[:16]
+    head = subprocess.run(["git", "-C", ROOT, "rev-parse", "--short=12", "HEAD"], capture_output=True,
+                          text=True).stdout.strip()
+    rec = {"source": cmd, "metrics": "dram__bytes_read.sum + dram__bytes_write.sum per launch; "
+                                     "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+           "duration_unit": unit, "lib_sha256_16": sha, "git_head_at_capture": head,
+           "tensor_pipe_pct": {k: round(v["tensor_pipe_pct"], 2) for k, v in out.items() if "tensor_pipe_pct" in v},
+           "kernels": out}
+    print(json.dumps(rec, indent=1))
+
+
+if __name__ == "__main__":
+    main()
