@@ -20,7 +20,9 @@ namespace hetgpu {
   } while (0)
 
 constexpr int kWarp = 32;
-constexpr int kNumSMs = 148;
+// SM count of the current device (148 on B200), for grid sizing; queried once
+// per device (cudaDevAttrMultiProcessorCount), never hard-coded
+int num_sms();
 
 // ---- programmatic dependent launch (PDL) --------------------------------------
 // The step is a chain of short dependent kernels. Launched through launch_pdl, a
@@ -95,31 +97,6 @@ struct Mt64 {
   }
 };
 
-// Streams the first 156 outputs of a freshly seeded mt19937_64 using two
-// cursors of the seeding recurrence (at j and at j+156): output j of the first
-// twist only needs the *untwisted* words x[j], x[j+1], x[j+156]. No state array.
-struct MtStream {
-  std::uint64_t xa, xa1, xb;
-  std::uint32_t j;
-  __device__ __forceinline__ void seed(std::uint64_t s) {
-    xa = s;
-    xa1 = Mt64::step(s, 1);
-    std::uint64_t x = xa1;
-    for (std::uint32_t i = 2; i <= 156; ++i) x = Mt64::step(x, i);
-    xb = x;
-    j = 0;
-  }
-  __device__ __forceinline__ bool exhausted() const { return j >= 156; }
-  __device__ __forceinline__ std::uint64_t next() {
-    const std::uint64_t t = Mt64::twist(xa, xa1, xb);
-    xa = xa1;
-    xa1 = Mt64::step(xa1, j + 2);
-    xb = Mt64::step(xb, j + 157);
-    ++j;
-    return Mt64::temper(t);
-  }
-};
-
 // Full-state engine for the (rare) rows that need more than 156 outputs.
 struct MtFull {
   std::uint64_t* x;  // 312 words of scratch
@@ -142,23 +119,16 @@ struct MtFull {
 };
 
 // uniform_int_distribution<uint64_t>(0, range-1) via Lemire's nearly
-// divisionless method with 128-bit products (uniform_int_dist.h:255-281).
-// Returns false (without consuming the decision) when a streaming engine
-// runs out of first-twist outputs; the caller then replays the row on MtFull.
-struct MtFullTag {};
-__device__ __forceinline__ bool mt_exhausted(const MtStream& e) { return e.exhausted(); }
-__device__ __forceinline__ bool mt_exhausted(const MtFull&) { return false; }
-
-template <typename Eng>
-__device__ __forceinline__ bool lemire(Eng& eng, std::uint64_t range, std::uint64_t& out) {
-  if (mt_exhausted(eng)) return false;
+// divisionless method with 128-bit products (uniform_int_dist.h:255-281), on the
+// full-state engine of the rows that need more than 156 outputs (the fast
+// sampler path resolves its draws from the first-twist outputs in registers).
+__device__ __forceinline__ bool lemire(MtFull& eng, std::uint64_t range, std::uint64_t& out) {
   std::uint64_t x = eng.next();
   std::uint64_t lo = x * range;
   std::uint64_t hi = __umul64hi(x, range);
   if (lo < range) {
     const std::uint64_t thr = (0ULL - range) % range;
     while (lo < thr) {
-      if (mt_exhausted(eng)) return false;
       x = eng.next();
       lo = x * range;
       hi = __umul64hi(x, range);

@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kThreads) k_cross_entropy(LossArgs a) {
 
 void cross_entropy(const LossArgs& a, cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(
-      1, std::min<std::uint64_t>(ceil_div(a.rows_cap, kThreads / 32), 4 * kNumSMs)));
+      1, std::min<std::uint64_t>(ceil_div(a.rows_cap, kThreads / 32), 4 * num_sms())));
   launch_pdl(k_cross_entropy, grid, kThreads, 0, st, a);
 }
 
@@ -240,9 +240,9 @@ void csc_prepare(const CscHop& h, LbScratch& lb, cudaStream_t st) {
   int cap = 1, scap = 1;
   for (int i = 0; i < h.nb; ++i) cap = std::max(cap, h.b[i].cap);
   for (int i = 0; i < h.nt; ++i) scap = std::max(scap, h.t[i].src_cap);
-  dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, 256), HG_FRONT_WAVES * kNumSMs)), h.nb);
+  dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, 256), HG_FRONT_WAVES * num_sms())), h.nb);
   launch_pdl(k_csc_fill, grid, 256, 0, st, h);
-  dim3 g2(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(scap, 256), HG_FRONT_WAVES * kNumSMs)), h.nt);
+  dim3 g2(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(scap, 256), HG_FRONT_WAVES * num_sms())), h.nt);
   launch_pdl(k_csc_sort, g2, 256, 0, st, h);
 }
 
@@ -250,7 +250,7 @@ void csc_gather(const CscHop& h, AdamHyper hp, std::uint32_t* err, cudaStream_t 
   if (h.nt == 0) return;
   int items = 0;
   for (int i = 0; i < h.nt; ++i) items += h.t[i].src_cap * static_cast<int>(ceil_div(h.t[i].din, 64));
-  const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(items, 16), HG_CSC_WAVES * kNumSMs)));
+  const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(items, 16), HG_CSC_WAVES * num_sms())));
   launch_pdl(k_csc_gather, grid, 256, 0, st, h, hp, err);
 }
 
@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(256) k_rsum_adam(ReplicaMerge m, ReplicaAdam a
 void replica_sum_adam(const ReplicaMerge& m, const ReplicaAdam& a, AdamHyper hp, std::uint32_t* err,
                       cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>(
-      std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(m.u.cap * ceil_div(m.din, 64), 16), HG_RSUM_WAVES * kNumSMs)));
+      std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(m.u.cap * ceil_div(m.din, 64), 16), HG_RSUM_WAVES * num_sms())));
   switch (m.n_rep) {
     case 1: launch_pdl(k_rsum_adam<1>, grid, 256, 0, st, m, a, hp, err); break;
     case 2: launch_pdl(k_rsum_adam<2>, grid, 256, 0, st, m, a, hp, err); break;
@@ -417,7 +417,7 @@ void bump_steps(const std::int64_t* const* steps, const int* const* counts, int 
 void adam_model(AdamModelBatch& b, const std::int64_t* step, AdamHyper hp, std::uint32_t* err, cudaStream_t st) {
   if (b.n == 0) return;
   const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
-                                                                            ceil_div(b.total4, 256), 4 * kNumSMs)));
+                                                                            ceil_div(b.total4, 256), 4 * num_sms())));
   launch_pdl(k_adam_model, grid, 256, 0, st, b, step, hp, err);
 }
 
@@ -425,13 +425,13 @@ void adam_rows(AdamRowsBatch& b, AdamHyper hp, std::uint32_t* err, cudaStream_t 
   if (b.n == 0) return;
   launch_pdl(k_bump_steps, 1, 32, 0, st, b);
   const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
-                                                                            ceil_div(b.total4, 256), 8 * kNumSMs)));
+                                                                            ceil_div(b.total4, 256), 8 * num_sms())));
   launch_pdl(k_adam_rows, grid, 256, 0, st, b, hp, err);
 }
 
 void zero_rows(float* p, int ld, const int* n_rows, int rows_cap, cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(
-      1, std::min<std::uint64_t>(ceil_div(static_cast<std::uint64_t>(rows_cap) * ld, 256), 4 * kNumSMs)));
+      1, std::min<std::uint64_t>(ceil_div(static_cast<std::uint64_t>(rows_cap) * ld, 256), 4 * num_sms())));
   launch_pdl(k_zero_rows, grid, 256, 0, st, p, ld, n_rows);
 }
 

@@ -67,8 +67,6 @@ struct DMeanBatch {
   int np;
 };
 
-void agg_tiles(const AggGroup& g, cudaStream_t st);
-
 // ---- split forward: gather-mean of every block of a hop, then projection ------------------
 struct MeanBlock {
   const std::uint32_t* indptr;

@@ -51,109 +51,6 @@ __device__ __forceinline__ int find_problem(const int* tile_base, int np, int ti
   return p;
 }
 
-// ---- forward: fused gather-mean-project ------------------------------------------------
-// tile (row block rb, col block cb) of one group. For every relation and every
-// 64-wide chunk of its input columns: the CTA gathers the neighbour rows of its
-// 64 block rows (by global id from the feature table at layer 1, by frontier
-// row otherwise), averages them into As (transposed) and the tape, stages the
-// matching W slab and accumulates. Relations sum in ascending order (agg_all).
-__global__ void __launch_bounds__(kT) k_agg_tiles(AggGroup g) {
-  pdl_enter();
-  __shared__ __align__(16) float As[kKS * 2 * kLd];  // 64 k rows (two slabs)
-  __shared__ __align__(16) float Bs[kKS * 2 * kLd];
-  const int n = *g.n_rows;
-  const int ncb = (g.dout + kTile - 1) / kTile;
-  const int rb = blockIdx.x / ncb, cb = blockIdx.x % ncb;
-  const int row0 = rb * kTile, col0 = cb * kTile;
-  if (row0 >= n) return;
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int half = lane >> 4, hl = lane & 15;  // half-warp per row, 4 cols per lane
-  Acc acc;
-  acc.zero();
-  for (int q = 0; q < g.nrel; ++q) {
-    const AggRel& r = g.r[q];
-    const std::uint32_t* keys = r.by_id ? r.src : r.col;
-    for (int c0 = 0; c0 < r.din; c0 += 2 * kKS) {
-      const int kn = min(2 * kKS, r.din - c0);
-      __syncthreads();
-      // gather: 8 warps x 2 half-warps = 16 rows per pass, 4 passes
-      for (int rr = warp * 2 + half; rr < kTile; rr += 16) {
-        const int i = row0 + rr;
-        float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-        const int c = c0 + 4 * hl;
-        if (i < n && 4 * hl < kn) {
-          const std::uint32_t lo = r.indptr[i], hi = r.indptr[i + 1];
-          const float* base = r.h + c;
-          std::uint32_t e = lo;
-          for (; e + 4 <= hi; e += 4) {
-            const std::uint32_t k0 = __ldg(keys + e), k1 = __ldg(keys + e + 1), k2 = __ldg(keys + e + 2),
-                                k3 = __ldg(keys + e + 3);
-            const float4 v0 = __ldg(reinterpret_cast<const float4*>(base + static_cast<std::size_t>(k0) * r.ld_h));
-            const float4 v1 = __ldg(reinterpret_cast<const float4*>(base + static_cast<std::size_t>(k1) * r.ld_h));
-            const float4 v2 = __ldg(reinterpret_cast<const float4*>(base + static_cast<std::size_t>(k2) * r.ld_h));
-            const float4 v3 = __ldg(reinterpret_cast<const float4*>(base + static_cast<std::size_t>(k3) * r.ld_h));
-            s.x += (v0.x + v1.x) + (v2.x + v3.x);
-            s.y += (v0.y + v1.y) + (v2.y + v3.y);
-            s.z += (v0.z + v1.z) + (v2.z + v3.z);
-            s.w += (v0.w + v1.w) + (v2.w + v3.w);
-          }
-          for (; e < hi; ++e) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(base + static_cast<std::size_t>(__ldg(keys + e)) * r.ld_h));
-            s.x += v.x;
-            s.y += v.y;
-            s.z += v.z;
-            s.w += v.w;
-          }
-          if (hi > lo) {
-            const float inv = 1.0f / static_cast<float>(hi - lo);
-            s.x *= inv;
-            s.y *= inv;
-            s.z *= inv;
-            s.w *= inv;
-          }
-          if (cb == 0) *reinterpret_cast<float4*>(r.mean + static_cast<std::size_t>(i) * r.ld_mean + c) = s;
-        }
-        const int kc = 4 * hl;
-        As[(kc + 0) * kLd + rr] = s.x;
-        As[(kc + 1) * kLd + rr] = s.y;
-        As[(kc + 2) * kLd + rr] = s.z;
-        As[(kc + 3) * kLd + rr] = s.w;
-      }
-      // W slab: rows c0..c0+kn, cols col0..col0+64
-      for (int x = tid; x < 2 * kKS * kTile / 4; x += kT) {
-        const int k = x / (kTile / 4), nq = (x % (kTile / 4)) * 4;
-        float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (k < kn && col0 + nq < g.dout)
-          w = __ldg(reinterpret_cast<const float4*>(r.w + static_cast<std::size_t>(c0 + k) * r.ld_w + col0 + nq));
-        *reinterpret_cast<float4*>(Bs + k * kLd + nq) = w;
-      }
-      __syncthreads();
-      slab_fma(As, Bs, kn, ty, tx, acc);
-    }
-  }
-  // epilogue: ReLU between layers, store (row remap for replica shards)
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int row = row0 + ty * 4 + i;
-    if (row >= n) break;
-    float* orow = g.out + static_cast<std::size_t>(row * g.out_stride + g.out_offset) * g.ld_out;
-    const int c = col0 + tx * 4;
-    if (c < g.dout) {
-      float4 o = make_float4(acc.v[i][0], acc.v[i][1], acc.v[i][2], acc.v[i][3]);
-      if (g.relu) {
-        o.x = fmaxf(o.x, 0.f);
-        o.y = fmaxf(o.y, 0.f);
-        o.z = fmaxf(o.z, 0.f);
-        o.w = fmaxf(o.w, 0.f);
-      }
-      // out rows are ld_out = round_up4(dout) wide: the float4 stays in bounds,
-      // padded columns receive zeros (W padding is zero)
-      *reinterpret_cast<float4*>(orow + c) = o;
-    }
-  }
-}
-
 // ---- dpre staging helpers (ReLU mask fused) -------------------------------------------------
 __device__ __forceinline__ float4 load_dpre4(const DpreView& d, int row, int col) {
   const std::size_t at = static_cast<std::size_t>(row * d.stride + d.offset) * d.ld + col;
@@ -449,7 +346,7 @@ void gather_mean(MeanBatch& m, cudaStream_t st) {
     items += m.b[b].rows_cap * static_cast<int>(ceil_div(m.b[b].din, 64));
   }
   m.item_base[m.nb] = items;
-  const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(items, 16), HG_GATHER_WAVES * kNumSMs)));
+  const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(items, 16), HG_GATHER_WAVES * num_sms())));
   launch_pdl(k_gather_mean, grid, 256, 0, st, m);
 }
 
@@ -462,12 +359,6 @@ void project_tiles(ProjBatch& p, cudaStream_t st) {
   }
   p.tile_base[p.ng] = tiles;
   launch_pdl(k_project_tiles, std::max(1, tiles), kT, 0, st, p);
-}
-
-void agg_tiles(const AggGroup& g, cudaStream_t st) {
-  const int ncb = static_cast<int>(ceil_div(g.dout, kTile));
-  const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, ceil_div(g.rows_cap, kTile) * ncb));
-  launch_pdl(k_agg_tiles, grid, kT, 0, st, g);
 }
 
 void wgrad_tiles(WGradBatch& b, cudaStream_t st) {

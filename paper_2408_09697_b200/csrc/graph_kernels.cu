@@ -7,6 +7,15 @@
 
 namespace hetgpu {
 
+int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  HG_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cache[dev] == 0) HG_CUDA(cudaDeviceGetAttribute(&cache[dev], cudaDevAttrMultiProcessorCount, dev));
+  return cache[dev];
+}
+
 namespace {
 
 #ifndef HG_SAMPLE_UNROLL
@@ -555,7 +564,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_batch_mult(const std::uint32_
 
 void frontier_mark_batch(const std::uint32_t* ids, const StepScalars* sc, int cap, const BitmapType& t,
                          cudaStream_t st) {
-  const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, kFrontThreads), kNumSMs));
+  const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, kFrontThreads), num_sms()));
   launch_pdl(k_mark_batch, grid, kFrontThreads, 0, st, ids, sc, t.bits);
 }
 
@@ -577,13 +586,13 @@ void frontier_relabel(const RelabelArgs& r, const FrontierArgs& f, cudaStream_t 
   if (r.nblk == 0) return;
   int cap = 1;
   for (int i = 0; i < r.nblk; ++i) cap = max(cap, r.b[i].cap);
-  dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, kFrontThreads), HG_FRONT_WAVES * kNumSMs)), r.nblk);
+  dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, kFrontThreads), HG_FRONT_WAVES * num_sms())), r.nblk);
   launch_pdl(k_relabel, grid, kFrontThreads, 0, st, r, f);
 }
 
 void batch_multiplicity(const std::uint32_t* ids, const StepScalars* sc, int cap, const BitmapType& t,
                         float* mult, cudaStream_t st) {
-  const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, kFrontThreads), kNumSMs));
+  const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, kFrontThreads), num_sms()));
   launch_pdl(k_batch_mult, grid, kFrontThreads, 0, st, ids, sc, t, mult);
 }
 
@@ -673,7 +682,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_shard_compact(ReplicaMerge m,
 void replica_union(const ReplicaMerge& m, LbScratch& lb, cudaStream_t st) {
   HG_CUDA(cudaMemsetAsync(m.u.bits, 0, static_cast<std::size_t>(m.u.words) * 4, st));
   HG_CUDA(cudaMemsetAsync(m.total, 0, sizeof(int), st));
-  const dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(m.u.cap, 256), 2 * kNumSMs)), m.n_rep);
+  const dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(m.u.cap, 256), 2 * num_sms())), m.n_rep);
   launch_pdl(k_rmark, grid, 256, 0, st, m);
   LbLayout L{};
   L.nseg = 1;
@@ -684,7 +693,7 @@ void replica_union(const ReplicaMerge& m, LbScratch& lb, cudaStream_t st) {
 }
 void replica_slots(const ReplicaMerge& m, cudaStream_t st) {
   // slots of this shard's union rows were reset to -1 by the compaction
-  const dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(m.u.cap, 256), 2 * kNumSMs)), m.n_rep);
+  const dim3 grid(static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(m.u.cap, 256), 2 * num_sms())), m.n_rep);
   launch_pdl(k_rslot, grid, 256, 0, st, m);
 }
 // ---- cache / hotness counters -------------------------------------------------------------
@@ -733,18 +742,18 @@ __global__ void k_hot_add_list(const std::uint32_t* ids, const int* n, std::uint
 
 void cache_count(const std::uint32_t* ids, const int* n, int cap, const std::uint32_t* cached_bits,
                  unsigned long long* hm, cudaStream_t st) {
-  const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, 256), 2 * kNumSMs));
+  const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, 256), 2 * num_sms()));
   launch_pdl(k_cache_count, std::max(grid, 1u), 256, 0, st, ids, n, cached_bits, hm);
 }
 
 void hotness_add(const std::uint32_t* ids, const std::uint32_t* indptr, const int* n_rows, int cap,
                  std::uint32_t* counts, cudaStream_t st) {
-  const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, 256), 4 * kNumSMs));
+  const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, 256), 4 * num_sms()));
   launch_pdl(k_hot_add, std::max(grid, 1u), 256, 0, st, ids, indptr, n_rows, counts);
 }
 
 void hotness_add_list(const std::uint32_t* ids, const int* n, int cap, std::uint32_t* counts, cudaStream_t st) {
-  const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, 256), 2 * kNumSMs));
+  const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, 256), 2 * num_sms()));
   launch_pdl(k_hot_add_list, std::max(grid, 1u), 256, 0, st, ids, n, counts);
 }
 

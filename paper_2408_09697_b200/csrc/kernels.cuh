@@ -129,32 +129,6 @@ void batch_multiplicity(const std::uint32_t* ids, const StepScalars* sc, int cap
                         float* mult, cudaStream_t st);
 
 // ---- dense: relation-first aggregation + projection -------------------------------
-struct AggRel {
-  const std::uint32_t* indptr;  // block offsets
-  const std::uint32_t* src;     // sampled global src ids (layer 1: gather by id)
-  const std::uint32_t* col;     // src rows in frontier[d][src_t] (inner layers)
-  const float* h;               // source rows: feature table (by id) or H[d][src_t] (by col)
-  int ld_h;
-  int by_id;
-  int din;
-  const float* w;               // [din x dout], ld = ld_w
-  int ld_w;
-  float* mean;                  // tape [rows x din], ld = ld_mean
-  int ld_mean;
-};
-struct AggGroup {
-  AggRel r[kMaxRelsPerGroup];
-  int nrel;
-  const int* n_rows;
-  int rows_cap;
-  float* out;
-  int ld_out;
-  int dout;
-  int relu;
-  // optional row remap of the output (replica shards write into full-batch rows)
-  int out_stride;
-  int out_offset;
-};
 
 // ---- loss ------------------------------------------------------------------------
 // per table: step += 1 iff its gradient row count is non-zero (hgnn.cpp:392-394)
