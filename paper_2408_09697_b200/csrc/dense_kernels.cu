@@ -44,11 +44,9 @@ __global__ void __launch_bounds__(kThreads) k_cross_entropy(LossArgs a) {
     float* dz = a.dlogits + static_cast<std::size_t>(i) * a.ld;
     const float m = a.mult[i];
     const std::int32_t y = a.labels[a.row_ids[i]];
-    float* dzl = a.dlogits_lo ? a.dlogits_lo + static_cast<std::size_t>(i) * a.ld : nullptr;
     if (m == 0.0f) {
       for (int c = lane; c < a.C; c += 32) {
         dz[c] = 0.f;
-        if (dzl) dzl[c] = 0.f;
       }
       if (lane == 0) a.row_loss[i] = 0.0;
       continue;
@@ -56,7 +54,6 @@ __global__ void __launch_bounds__(kThreads) k_cross_entropy(LossArgs a) {
     if (y < 0 || y >= a.C) {  // never reached: the host validates labels before enqueueing
       for (int c = lane; c < a.C; c += 32) {
         dz[c] = 0.f;
-        if (dzl) dzl[c] = 0.f;
       }
       if (lane == 0) {
         a.row_loss[i] = 0.0;
@@ -76,7 +73,6 @@ __global__ void __launch_bounds__(kThreads) k_cross_entropy(LossArgs a) {
     for (int c = lane; c < a.C; c += 32) {
       const float g = (expf(z[c] - lse) - (c == y ? 1.0f : 0.0f)) * scale;
       dz[c] = g;
-      if (dzl) dzl[c] = tf32_lo(g);
     }
     if (lane == 0) a.row_loss[i] = static_cast<double>(lse - z[y]) * static_cast<double>(scale);
   }
@@ -214,7 +210,6 @@ __global__ void __launch_bounds__(256) k_csc_gather(CscHop h, AdamHyper hp, std:
         if (h.w <= 0.f) s.w = 0.f;
       }
       if (t.dh) *reinterpret_cast<float4*>(t.dh + static_cast<std::size_t>(c) * t.ld_dh + f) = s;
-      if (t.dh_lo) *reinterpret_cast<float4*>(t.dh_lo + static_cast<std::size_t>(c) * t.ld_dh + f) = tf32_lo4(s);
       if (t.w) {
         const std::size_t at = static_cast<std::size_t>(t.ids[c]) * t.ld_w + f;
         float4 w = *reinterpret_cast<float4*>(t.w + at);
@@ -276,7 +271,6 @@ __global__ void __launch_bounds__(256) k_adam_model(AdamModelBatch b, const std:
     const float4 g = *reinterpret_cast<const float4*>(b.g[s] + off);
     adam4(w, m, v, g, ks, err);
     *reinterpret_cast<float4*>(b.w[s] + off) = w;
-    if (b.w_lo[s]) *reinterpret_cast<float4*>(b.w_lo[s] + off) = tf32_lo4(w);
     *reinterpret_cast<float4*>(b.m[s] + off) = m;
     *reinterpret_cast<float4*>(b.v[s] + off) = v;
   }

@@ -507,17 +507,7 @@ void Engine::upload(const Graph& g) {
     s.m = static_cast<float*>(alloc(bytes));
     s.v = static_cast<float*>(alloc(bytes));
     s.g = static_cast<float*>(alloc(bytes));
-    s.w_lo = static_cast<float*>(alloc(bytes));
     HG_CUDA(cudaMemcpyAsync(s.w, host.data(), bytes, cudaMemcpyHostToDevice, st_));
-    for (float& x : host) {  // tf32 residual of the initial weights
-      std::uint32_t u;
-      std::memcpy(&u, &x, 4);
-      u &= 0xFFFFE000u;
-      float hi;
-      std::memcpy(&hi, &u, 4);
-      x -= hi;
-    }
-    HG_CUDA(cudaMemcpyAsync(s.w_lo, host.data(), bytes, cudaMemcpyHostToDevice, st_));
     HG_CUDA(cudaStreamSynchronize(st_));
   }
   }  // !sample_only
@@ -625,7 +615,6 @@ void Engine::upload(const Graph& g) {
     }
     if (!o_.sample_only) {
       b.mean = static_cast<float*>(alloc(static_cast<std::size_t>(b.rows_cap) * b.ld_mean * 4));
-      b.mean_lo = static_cast<float*>(alloc(static_cast<std::size_t>(b.rows_cap) * b.ld_mean * 4));
     }
     if (b.need_src_grad) b.dmean = static_cast<float*>(alloc(static_cast<std::size_t>(b.rows_cap) * b.ld_mean * 4));
     max_rows = std::max(max_rows, b.rows_cap + 1);
@@ -635,13 +624,11 @@ void Engine::upload(const Graph& g) {
   ldc_ = round_up4(num_classes_);
   logits_ = static_cast<float*>(alloc(static_cast<std::size_t>(o_.batch_cap + 1) * ldc_ * 4));
   dlogits_ = static_cast<float*>(alloc(static_cast<std::size_t>(o_.batch_cap + 1) * ldc_ * 4));
-  dlogits_lo_ = static_cast<float*>(alloc(static_cast<std::size_t>(o_.batch_cap + 1) * ldc_ * 4));
   if (o_.p > ldc_) throw std::invalid_argument("more partitions than logit columns for the AGG_all counters");
   for (auto& gr : groups_) {
     if (gr.layer == o_.k) {
       gr.out = logits_;
       gr.dout_buf = dlogits_;
-      gr.dout_lo = dlogits_lo_;
       gr.ld = ldc_;
     } else {
       gr.out = static_cast<float*>(alloc(static_cast<std::size_t>(std::max(1, gr.rows_cap)) * gr.ld * 4));
@@ -677,9 +664,7 @@ void Engine::upload(const Graph& g) {
     if (c.hop < o_.k) {
       for (auto& gr : groups_)
         if (gr.depth - 1 == c.hop && gr.type == c.src_t) {
-          c.dh_lo = static_cast<float*>(alloc(static_cast<std::size_t>(std::max(1, c.src_cap)) * c.ld * 4));
           gr.dout_buf = c.dh;
-          gr.dout_lo = c.dh_lo;
         }
     }
   }
@@ -984,7 +969,6 @@ void Engine::run_forward() {
       m.rows_cap = b.rows_cap;
       m.mean = b.mean;
       m.ld_mean = b.ld_mean;
-      m.mean_lo = b.mean_lo;
     }
     timed(top ? "aggregate_top" : "aggregate", bytes, [&] { gather_mean(mb, st_); });
     // (2) per-relation projection summed over the relations into each type (agg_all)
@@ -1009,7 +993,7 @@ void Engine::run_forward() {
       for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
         const BlockBuf& b = blocks_[gr.blocks[q]];
         const Slot& s = slots_[gr.slots[q]];
-        pg.r[q] = {b.mean, b.ld_mean, b.din, s.w, s.ld, b.mean_lo, s.w_lo};
+        pg.r[q] = {b.mean, b.ld_mean, b.din, s.w, s.ld};
       }
     }
     timed(top ? "project_top" : "project", 0, [&] { use_umma_ ? project_umma(pb, st_) : project_tiles(pb, st_); });
@@ -1059,7 +1043,6 @@ void Engine::run_loss(bool train) {
   la.labels = labels_;
   la.sc = d_tsc_;  // batch_len of the step being trained
   la.dlogits = dlogits_;
-  la.dlogits_lo = dlogits_lo_;
   la.row_loss = row_loss_;
   la.loss_out = loss_;
   la.err = err_;
@@ -1086,17 +1069,15 @@ void Engine::run_backward() {
       const int rows_cap = top && replica_ ? static_cast<int>(ceil_div(o_.batch_cap, shard_count_)) : gr.rows_cap;
       // dpre = dH (x) [H > 0] between layers, fused into the operand loads
       // dpre = dH * [H > 0]: the mask was applied when csc_gather wrote dH
-      const DpreView dv{gr.dout_buf, nullptr, gr.ld, gr.dout, top ? shard_count_ : 1, top ? shard_index_ : 0,
-                        gr.dout_lo};
+      const DpreView dv{gr.dout_buf, nullptr, gr.ld, gr.dout, top ? shard_count_ : 1, top ? shard_index_ : 0};
       for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
         BlockBuf& b = blocks_[gr.blocks[q]];
         Slot& s = slots_[gr.slots[q]];
         if (wb.np >= kMaxProblems || db.np >= kMaxProblems) throw std::runtime_error("too many problems per layer");
-        wb.p[wb.np++] = {b.mean, b.ld_mean, b.din, dv, n_rows, rows_cap, wgrad_partial_ + partial_off, s.g, s.ld,
-                         b.mean_lo};
+        wb.p[wb.np++] = {b.mean, b.ld_mean, b.din, dv, n_rows, rows_cap, wgrad_partial_ + partial_off, s.g, s.ld};
         partial_off += ceil_div(std::max(1, rows_cap), kWChunkRows) * static_cast<std::size_t>(b.din) * gr.dout;
         if (b.need_src_grad)
-          db.p[db.np++] = {dv, s.w, s.ld, b.din, b.indptr, n_rows, rows_cap, b.dmean, b.ld_mean, s.w_lo};
+          db.p[db.np++] = {dv, s.w, s.ld, b.din, b.indptr, n_rows, rows_cap, b.dmean, b.ld_mean};
       }
     }
     // dpre of this layer is complete on st_: the weight gradient runs beside the
@@ -1117,7 +1098,6 @@ void Engine::run_backward() {
               wb.p[q].w = sl.w;
               wb.p[q].m = sl.m;
               wb.p[q].v = sl.v;
-              wb.p[q].w_lo = sl.w_lo;
             }
           }
         }
@@ -1296,7 +1276,6 @@ CscHop Engine::csc_hop(int h) {
     const bool exchanged = h == o_.k && xchg_type(c.src_t);
     const bool leaf_learnable = h == o_.k && tables_[c.src_t].learnable && !exchanged;
     t.dh = (!leaf_learnable || retain_grads_) ? c.dh : nullptr;
-    t.dh_lo = c.dh_lo;
     t.ld_dh = c.ld;
     t.din = c.din;
     if (h < o_.k)  // inner type: its forward output H[h][t] masks the stored gradient
@@ -1343,7 +1322,6 @@ void Engine::run_update() {
     mb.m[mb.n] = s.m;
     mb.v[mb.n] = s.v;
     mb.g[mb.n] = s.g;
-    mb.w_lo[mb.n] = s.w_lo;
     mb.base4[mb.n] = base;
     base += std::max(1, s.din) * s.ld / 4;
     ++mb.n;

@@ -201,7 +201,6 @@ class Engine {
     std::uint32_t *indptr = nullptr, *src = nullptr, *erow = nullptr, *col = nullptr;  // bound sample slot
     std::uint32_t *s_indptr[2] = {}, *s_src[2] = {}, *s_erow[2] = {}, *s_col[2] = {};
     float* mean = nullptr;   // tape: rows_cap x ld_mean (only for blocks feeding a layer)
-    float* mean_lo = nullptr;  // its tf32 residual (tensor-core operand)
     float* dmean = nullptr;  // rows_cap x ld_mean (only if the source needs a gradient)
     int din = 0, ld_mean = 0;
     bool need_src_grad = false;
@@ -214,7 +213,6 @@ class Engine {
   struct Slot {
     int rel = -1, layer = 0, din = 0, dout = 0, ld = 0;
     float *w = nullptr, *m = nullptr, *v = nullptr, *g = nullptr;
-    float* w_lo = nullptr;  // tf32 residual of w, refreshed by every Adam step
   };
   struct Group {  // one output type of one layer
     int layer = 0, depth = 0, type = -1, dout = 0, ld = 0, rows_cap = 0;
@@ -222,7 +220,6 @@ class Engine {
     std::vector<int> slots;   // matching slot indices
     float* out = nullptr;     // H[depth-1][type] (logits for layer k)
     float* dout_buf = nullptr;  // dH for it
-    float* dout_lo = nullptr;   // its tf32 residual
   };
   struct CscBuf {
     int hop = 0, src_t = -1, src_cap = 0, din = 0, ld = 0;
@@ -230,7 +227,6 @@ class Engine {
     std::uint32_t *offs = nullptr, *cursor = nullptr, *entries = nullptr;  // bound sample slot
     std::uint32_t *s_offs[2] = {}, *s_cursor[2] = {}, *s_entries[2] = {};
     float* dh = nullptr;  // gradient of H[hop][src_t] (or learnable rows)
-    float* dh_lo = nullptr;  // tf32 residual of dh (inner types: the next layer's dpre)
   };
   struct TypeTable {
     int dim = 0, ld = 0;
@@ -359,7 +355,6 @@ class Engine {
   float* mult_ = nullptr;
   float* logits_ = nullptr;   // [batch_cap + 1 rows x ldC] (+1: partition counters)
   float* dlogits_ = nullptr;
-  float* dlogits_lo_ = nullptr;
   int ldc_ = 0;
   double* row_loss_ = nullptr;
   double* loss_ = nullptr;

@@ -21,7 +21,6 @@ struct DpreView {
   int cols;
   int stride;
   int offset;
-  const float* g_lo;  // tf32 residual of g (x - trunc_tf32(x)) for the 3xTF32 tensor-core path
 };
 
 struct WGradProblem {
@@ -34,10 +33,9 @@ struct WGradProblem {
   float* partial;  // [chunks x din x cols]
   float* dw;
   int ld_dw;
-  const float* mean_lo;
   // optional Adam of the slot fused into the reduction (stride ld_dw): each
   // gradient element is final there, so it is applied to w / m / v at once
-  float *w, *m, *v, *w_lo;
+  float *w, *m, *v;
 };
 struct WGradBatch {
   WGradProblem p[kMaxProblems];
@@ -59,7 +57,6 @@ struct DMeanProblem {
   int rows_cap;
   float* dmean;
   int ld_dmean;
-  const float* w_lo;
 };
 struct DMeanBatch {
   DMeanProblem p[kMaxProblems];
@@ -77,8 +74,7 @@ struct MeanBlock {
   const int* n_rows;
   int rows_cap;
   float* mean;
-  int ld_mean;
-  float* mean_lo;  // optional tf32 residual of the tape (rows up to the next 32 zero-filled)
+  int ld_mean;  // rows live..next multiple of 32 are zero-filled (weight-gradient K chunks)
 };
 struct MeanBatch {
   MeanBlock b[kMaxBlocks];
@@ -93,8 +89,6 @@ struct ProjRel {
   int din;
   const float* w;
   int ld_w;
-  const float* mean_lo;
-  const float* w_lo;
 };
 struct ProjGroup {
   ProjRel r[8];

@@ -153,7 +153,6 @@ __global__ void __launch_bounds__(256) k_wgrad_reduce(WGradBatch b, int total_ou
       P.w[at] = w;
       P.m[at] = m;
       P.v[at] = v;
-      if (P.w_lo) P.w_lo[at] = tf32_lo(w);
     }
   }
 }
@@ -234,10 +233,8 @@ __global__ void __launch_bounds__(256) k_gather_mean(MeanBatch m) {
     if (i >= n) {
       // zero tail up to the next 32-row boundary: the tensor-core weight gradient
       // streams whole 32-row K chunks of the tape
-      if (B.mean_lo && i < ((n + 31) & ~31)) {
+      if (i < ((n + 31) & ~31))
         *reinterpret_cast<float4*>(B.mean + static_cast<std::size_t>(i) * B.ld_mean + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-        *reinterpret_cast<float4*>(B.mean_lo + static_cast<std::size_t>(i) * B.ld_mean + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
       continue;
     }
     const std::uint32_t lo = B.indptr[i], hi = B.indptr[i + 1];
@@ -271,7 +268,6 @@ __global__ void __launch_bounds__(256) k_gather_mean(MeanBatch m) {
       s.w *= inv;
     }
     *reinterpret_cast<float4*>(B.mean + static_cast<std::size_t>(i) * B.ld_mean + c) = s;
-    if (B.mean_lo) *reinterpret_cast<float4*>(B.mean_lo + static_cast<std::size_t>(i) * B.ld_mean + c) = tf32_lo4(s);
   }
 }
 

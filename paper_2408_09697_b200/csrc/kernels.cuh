@@ -151,7 +151,6 @@ struct LossArgs {
   double* row_loss;   // scratch [rows_cap]
   double* loss_out;   // [1]
   std::uint32_t* err;
-  float* dlogits_lo;  // optional tf32 residual of dlogits
   unsigned* done;     // CTA completion counter (zero between launches)
   StepBumps bumps;    // applied by the last CTA (training steps)
 };
@@ -184,7 +183,6 @@ struct CscType {
   // (dpre = dH * [H > 0], hgnn.cpp:326-328), so the backward contractions read it plain
   const float* relu_h;
   int ld_h;
-  float* dh_lo;  // optional tf32 residual of dh
 };
 struct CscEdges {
   const std::uint32_t* col;
@@ -212,7 +210,6 @@ struct AdamHyper {  // hgnn.hpp:16-21
 constexpr int kMaxSlots = 64;
 // all model slots (adam_update_model, hgnn.cpp:379-390); base4 = prefix of rows*ld/4
 struct AdamModelBatch {
-  float* w_lo[kMaxSlots];  // optional tf32 residual of the updated weights
   float* w[kMaxSlots];
   float* m[kMaxSlots];
   float* v[kMaxSlots];

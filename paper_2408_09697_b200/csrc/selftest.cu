@@ -51,20 +51,6 @@ std::vector<float> rnd(std::mt19937& g, std::size_t n, int cols, int ld, float z
   return v;
 }
 
-// tf32 residual x - trunc_tf32(x) of a host array (the tensor-core "lo" operand)
-std::vector<float> lo_of(const std::vector<float>& v) {
-  std::vector<float> o(v.size());
-  for (std::size_t i = 0; i < v.size(); ++i) {
-    std::uint32_t u;
-    std::memcpy(&u, &v[i], 4);
-    u &= 0xFFFFE000u;
-    float hi;
-    std::memcpy(&hi, &u, 4);
-    o[i] = v[i] - hi;
-  }
-  return o;
-}
-
 }  // namespace
 
 // cases: (rows, nrel, din, dout); returns per case {project, dmean, wgrad} errors
@@ -77,13 +63,10 @@ std::vector<std::vector<double>> selftest_contractions(const std::vector<std::ve
     const int ldm = round_up4(din), ldo = round_up4(dout);
     Dev d;
     // ---- projection: out = sum_r mean_r . W_r, ReLU
-    std::vector<float*> means, ws, means_lo, ws_lo;
+    std::vector<float*> means, ws;
     for (int r = 0; r < nrel; ++r) {
-      const auto m = rnd(gen, rows, din, ldm), w = rnd(gen, din, dout, ldo);
-      means.push_back(d.up(m));
-      ws.push_back(d.up(w));
-      means_lo.push_back(d.up(lo_of(m)));
-      ws_lo.push_back(d.up(lo_of(w)));
+      means.push_back(d.up(rnd(gen, rows, din, ldm)));
+      ws.push_back(d.up(rnd(gen, din, dout, ldo)));
     }
     int* nrow = d.up(std::vector<int>{rows});
     std::vector<double> errs;
@@ -95,7 +78,7 @@ std::vector<std::vector<double>> selftest_contractions(const std::vector<std::ve
         pb.ng = 1;
         ProjGroup& g = pb.g[0];
         g.nrel = nrel;
-        for (int r = 0; r < nrel; ++r) g.r[r] = {means[r], ldm, din, ws[r], ldo, means_lo[r], ws_lo[r]};
+        for (int r = 0; r < nrel; ++r) g.r[r] = {means[r], ldm, din, ws[r], ldo};
         g.n_rows = nrow;
         g.rows_cap = rows;
         g.out = o;
@@ -114,7 +97,6 @@ std::vector<std::vector<double>> selftest_contractions(const std::vector<std::ve
     {
       const auto gh = rnd(gen, rows, dout, ldo, 0.3f);
       float* g = d.up(gh);
-      float* g_lo = d.up(lo_of(gh));
       float* h = nullptr;
       std::vector<std::uint32_t> ip(rows + 1, 0);
       for (int i = 0; i < rows; ++i) ip[i + 1] = ip[i] + (i % 7);
@@ -124,7 +106,7 @@ std::vector<std::vector<double>> selftest_contractions(const std::vector<std::ve
         float* o = d.up(std::vector<float>(static_cast<std::size_t>(rows) * ldm, 0.f));
         DMeanBatch db{};
         db.np = 1;
-        db.p[0] = {DpreView{g, h, ldo, dout, 1, 0, g_lo}, ws[0], ldo, din, indptr, nrow, rows, o, ldm, ws_lo[0]};
+        db.p[0] = {DpreView{g, h, ldo, dout, 1, 0}, ws[0], ldo, din, indptr, nrow, rows, o, ldm};
         umma ? dmean_umma(db, st) : dmean_tiles(db, st);
         HG_CUDA(cudaDeviceSynchronize());
         res.push_back(d.down(o, static_cast<std::size_t>(rows) * ldm));
@@ -138,7 +120,7 @@ std::vector<std::vector<double>> selftest_contractions(const std::vector<std::ve
         float* dw = d.up(std::vector<float>(static_cast<std::size_t>(din) * ldo, 0.f));
         WGradBatch wb{};
         wb.np = 1;
-        wb.p[0] = {means[0], ldm, din, DpreView{g, h, ldo, dout, 1, 0, g_lo}, nrow, rows, part, dw, ldo, means_lo[0]};
+        wb.p[0] = {means[0], ldm, din, DpreView{g, h, ldo, dout, 1, 0}, nrow, rows, part, dw, ldo};
         umma ? wgrad_umma(wb, st) : wgrad_tiles(wb, st);
         HG_CUDA(cudaDeviceSynchronize());
         resw.push_back(d.down(dw, static_cast<std::size_t>(din) * ldo));

@@ -4,16 +4,18 @@
 //   projection   out   = sum_r mean_r . W_r  (+ReLU)     matmul + agg_all, hgnn.cpp:189-203, 267-272
 //   mean grad    dmean = (dpre . W^T) / deg              matmul_nt, matrix.hpp:64-78; hgnn.cpp:337-353
 //   weight grad  dW   += mean^T . dpre  (split-K)        matmul_tn_acc, matrix.hpp:49-61; hgnn.cpp:334
-// Parity: every operand x is carried as hi = x (the tensor core reads its top
-// 19 bits) plus lo = x - trunc_tf32(x), written by the producing kernel; the
-// sum hi.hi + hi.lo + lo.hi accumulated in fp32 (3xTF32) keeps fp32-level
-// accuracy (the north star's 1e-3 tolerance is for fp32 accumulate).
+// Parity: every operand x is split as hi = x (the tensor core reads its top 19
+// bits) plus lo = x - trunc_tf32(x); the sum hi.hi + hi.lo + lo.hi accumulated in
+// fp32 (3xTF32) keeps fp32-level accuracy (the north star's 1e-3 tolerance is for
+// fp32 accumulate). Only x travels from HBM: lo is formed in shared memory.
 //
 // One CTA = 128 threads = one 128-row output tile x NT columns, warp-specialised:
-// warp 0 (one lane) streams 32-wide K chunks of A hi/lo and B hi/lo through a
-// kStages-deep shared-memory ring with 2-D TMA loads (K-major tiles with the
-// 128-byte swizzle; row-contiguous operands the tensor core reads transposed as
-// MN-major SW128_32B tiles); warp 1 (one lane) issues 4 k-steps x 3 MMAs per chunk
+// warp 0 (one lane) streams 32-wide K chunks of A and B through a kStages-deep
+// shared-memory ring with 2-D TMA loads (K-major tiles with the 128-byte swizzle;
+// row-contiguous operands the tensor core reads transposed as MN-major SW128_32B
+// tiles); warps 2-3 turn each landed tile into its tf32 residual next to it (an
+// elementwise pass, so the swizzled layout carries over) and hand the stage on
+// through a second barrier; warp 1 (one lane) issues 4 k-steps x 3 MMAs per chunk
 // and commits them to the stage's "empty" barrier; all four warps then drain TMEM
 // with tcgen05.ld (warp w owns TMEM lanes 32w..32w+31) and apply the fused ReLU /
 // 1/deg scaling / row remap. Rows and columns outside a tensor's extent are
@@ -33,7 +35,7 @@ namespace {
 
 constexpr int kUT = 128;           // threads per CTA (4 warps = 4 TMEM lane quadrants)
 constexpr int kATile = 128 * 128;  // bytes of one 128 x 32 fp32 operand tile
-constexpr int kMaxMaps = 128;
+constexpr int kMaxMaps = 64;
 
 template <int NT>
 #ifndef HG_PROJ_NT
@@ -47,7 +49,8 @@ template <int NT>
 #endif
 struct UStage {
   static constexpr int kB = NT * 128;
-  static constexpr int kBytes = 2 * kATile + 2 * kB;  // A hi, A lo, B hi, B lo
+  static constexpr int kBytes = 2 * kATile + 2 * kB;  // A, A lo, B, B lo
+  static constexpr int kTxBytes = kATile + kB;         // what TMA brings in per stage
   static constexpr int kStages = NT <= 64 ? HG_USTAGES : HG_USTAGES128;
   static constexpr int kSmem = kStages * kBytes + 1024 + 128;
   static constexpr int kTmemCols = NT <= 32 ? 32 : NT <= 64 ? 64 : NT <= 128 ? 128 : 256;
@@ -63,7 +66,7 @@ template <> struct Majors<kWGrad> { static constexpr int a = 1, b = 1; };
 
 template <typename Batch>
 struct alignas(64) UmmaArgs {
-  CUtensorMap maps[kMaxMaps];  // [A hi, A lo, B hi, B lo] per (problem[, relation])
+  CUtensorMap maps[kMaxMaps];  // [A, B] per (problem[, relation])
   Batch b;
   int tile_base[kMaxProblems + 1];
   int n_tiles[kMaxProblems];  // column tiles per problem
@@ -71,7 +74,7 @@ struct alignas(64) UmmaArgs {
   int np;
 };
 __host__ __device__ constexpr int map_index(int mode, int p, int r, int which) {
-  return mode == kProject ? (p * 8 + r) * 4 + which : p * 4 + which;
+  return mode == kProject ? (p * 8 + r) * 2 + which : p * 2 + which;
 }
 
 __device__ __forceinline__ int find_tile(const int* base, int n, int tile) {
@@ -88,7 +91,8 @@ __global__ void __launch_bounds__(kUT) k_umma(const __grid_constant__ UmmaArgs<B
   std::uint8_t* smem = reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
                                                         ~static_cast<std::uintptr_t>(1023));
   std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + S * UStage<NT>::kBytes);
-  std::uint64_t* empty = full + S;
+  std::uint64_t* conv = full + S;  // the stage's tf32 residuals are in place
+  std::uint64_t* empty = conv + S;
   std::uint64_t* done = empty + S;
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(done + 1);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -125,6 +129,7 @@ __global__ void __launch_bounds__(kUT) k_umma(const __grid_constant__ UmmaArgs<B
   if (tid == 0) {
     for (int i = 0; i < S; ++i) {
       umma::mbar_init(umma::smem_u32(&full[i]), 1);
+      umma::mbar_init(umma::smem_u32(&conv[i]), 2);  // one arrival per converter warp
       umma::mbar_init(umma::smem_u32(&empty[i]), 1);
     }
     umma::mbar_init(umma::smem_u32(done), 1);
@@ -142,9 +147,9 @@ __global__ void __launch_bounds__(kUT) k_umma(const __grid_constant__ UmmaArgs<B
       const int s = ch % S;
       if (ch >= S) umma::mbar_wait(umma::smem_u32(&empty[s]), ((ch / S) - 1) & 1);
       const std::uint32_t bar = umma::smem_u32(&full[s]);
-      umma::mbar_expect_tx(bar, UStage<NT>::kBytes);
-      const std::uint32_t a_hi = umma::smem_u32(smem + s * UStage<NT>::kBytes), a_lo = a_hi + kATile;
-      const std::uint32_t b_hi = a_hi + 2 * kATile, b_lo = b_hi + UStage<NT>::kB;
+      umma::mbar_expect_tx(bar, UStage<NT>::kTxBytes);
+      const std::uint32_t a_hi = umma::smem_u32(smem + s * UStage<NT>::kBytes);
+      const std::uint32_t b_hi = a_hi + 2 * kATile;
       if constexpr (MODE == kProject) {
         const ProjGroup& g = args.b.g[p];
         int q = 0, k0 = ch * 32;
@@ -154,29 +159,39 @@ __global__ void __launch_bounds__(kUT) k_umma(const __grid_constant__ UmmaArgs<B
         }
         const CUtensorMap* M = &args.maps[map_index(MODE, p, q, 0)];
         umma::tma_load_2d(a_hi, M + 0, k0, row0, bar);  // A = mean rows, K-major
-        umma::tma_load_2d(a_lo, M + 1, k0, row0, bar);
-        for (int j = 0; j < NT / 32; ++j) {  // B = W[k][n] boxes of 32 n x 32 k
-          umma::tma_load_2d(b_hi + j * 4096, M + 2, n0 + 32 * j, k0, bar);
-          umma::tma_load_2d(b_lo + j * 4096, M + 3, n0 + 32 * j, k0, bar);
-        }
+        for (int j = 0; j < NT / 32; ++j)                // B = W[k][n] boxes of 32 n x 32 k
+          umma::tma_load_2d(b_hi + j * 4096, M + 1, n0 + 32 * j, k0, bar);
       } else if constexpr (MODE == kDMean) {
         const CUtensorMap* M = &args.maps[map_index(MODE, p, 0, 0)];
         umma::tma_load_2d(a_hi, M + 0, ch * 32, row0, bar);  // A = dpre rows, K-major
-        umma::tma_load_2d(a_lo, M + 1, ch * 32, row0, bar);
-        umma::tma_load_2d(b_hi, M + 2, ch * 32, n0, bar);    // B = W rows c, K-major
-        umma::tma_load_2d(b_lo, M + 3, ch * 32, n0, bar);
+        umma::tma_load_2d(b_hi, M + 1, ch * 32, n0, bar);    // B = W rows c, K-major
       } else {
         const CUtensorMap* M = &args.maps[map_index(MODE, p, 0, 0)];
         const int r = row0 + ch * 32;
-        for (int j = 0; j < 4; ++j) {  // A = mean[row][c]: boxes of 32 c x 32 rows
+        for (int j = 0; j < 4; ++j)  // A = mean[row][c]: boxes of 32 c x 32 rows
           umma::tma_load_2d(a_hi + j * 4096, M + 0, m0 + 32 * j, r, bar);
-          umma::tma_load_2d(a_lo + j * 4096, M + 1, m0 + 32 * j, r, bar);
-        }
-        for (int j = 0; j < NT / 32; ++j) {  // B = dpre[row][j]: boxes of 32 j x 32 rows
-          umma::tma_load_2d(b_hi + j * 4096, M + 2, n0 + 32 * j, r, bar);
-          umma::tma_load_2d(b_lo + j * 4096, M + 3, n0 + 32 * j, r, bar);
-        }
+        for (int j = 0; j < NT / 32; ++j)  // B = dpre[row][j]: boxes of 32 j x 32 rows
+          umma::tma_load_2d(b_hi + j * 4096, M + 1, n0 + 32 * j, r, bar);
       }
+    }
+  } else if (warp >= 2) {
+    // ===== tf32 split: lo = x - trunc_tf32(x) of the tiles that just landed, written
+    // beside them (elementwise, so the swizzled layout carries over) =====
+    const int ct = tid - 64;
+    for (int ch = 0; ch < nch; ++ch) {
+      const int s = ch % S;
+      umma::mbar_wait(umma::smem_u32(&full[s]), (ch / S) & 1);
+      const float4* a = reinterpret_cast<const float4*>(smem + s * UStage<NT>::kBytes);
+      float4* a_lo = const_cast<float4*>(a) + kATile / 16;
+#pragma unroll 4
+      for (int i = ct; i < kATile / 16; i += 64) a_lo[i] = tf32_lo4(a[i]);
+      const float4* b = a + 2 * kATile / 16;
+      float4* b_lo = const_cast<float4*>(b) + UStage<NT>::kB / 16;
+#pragma unroll 4
+      for (int i = ct; i < UStage<NT>::kB / 16; i += 64) b_lo[i] = tf32_lo4(b[i]);
+      umma::fence_async_smem();  // generic-proxy writes -> visible to the tensor core
+      __syncwarp();
+      if (lane == 0) umma::mbar_arrive(umma::smem_u32(&conv[s]));
     }
   } else if (warp == 1 && lane == 0) {
     // ===== MMA issuer =====
@@ -186,7 +201,7 @@ __global__ void __launch_bounds__(kUT) k_umma(const __grid_constant__ UmmaArgs<B
     };
     for (int ch = 0; ch < nch; ++ch) {
       const int s = ch % S;
-      umma::mbar_wait(umma::smem_u32(&full[s]), (ch / S) & 1);
+      umma::mbar_wait(umma::smem_u32(&conv[s]), (ch / S) & 1);
       umma::fence_after_sync();
       const std::uint32_t a_hi = umma::smem_u32(smem + s * UStage<NT>::kBytes), a_lo = a_hi + kATile;
       const std::uint32_t b_hi = a_hi + 2 * kATile, b_lo = b_hi + UStage<NT>::kB;
@@ -286,7 +301,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // boxes of 32 columns x box_rows rows
 void encode(CUtensorMap* m, const float* base, std::uint64_t cols, std::uint64_t rows, std::uint64_t row_stride,
             std::uint32_t box_rows, bool mn_major) {
-  if (!base) throw std::invalid_argument("tensor-core operand without a tf32 residual buffer");
+  if (!base) throw std::invalid_argument("tensor-core operand without a buffer");
   const cuuint64_t dims[2] = {cols, std::max<std::uint64_t>(1, rows)};
   const cuuint64_t strides[1] = {row_stride * 4};
   const cuuint32_t box[2] = {32, box_rows};
@@ -354,9 +369,7 @@ void project_umma(ProjBatch& pb, cudaStream_t st) {
       const ProjRel& R = G.r[r];
       CUtensorMap* M = &a.maps[map_index(kProject, g, r, 0)];
       encode(M + 0, R.mean, R.ld_mean, G.rows_cap, R.ld_mean, 128, false);
-      encode(M + 1, R.mean_lo, R.ld_mean, G.rows_cap, R.ld_mean, 128, false);
-      encode(M + 2, R.w, R.ld_w, R.din, R.ld_w, 32, true);
-      encode(M + 3, R.w_lo, R.ld_w, R.din, R.ld_w, 32, true);
+      encode(M + 1, R.w, R.ld_w, R.din, R.ld_w, 32, true);
     }
   }
   a.tile_base[pb.ng] = tiles;
@@ -382,9 +395,7 @@ void dmean_umma(DMeanBatch& b, cudaStream_t st) {
     const std::size_t off = static_cast<std::size_t>(P.d.offset) * P.d.ld;
     const std::uint64_t rstride = static_cast<std::uint64_t>(P.d.stride) * P.d.ld;
     encode(M + 0, P.d.g + off, P.d.ld, P.rows_cap, rstride, 128, false);
-    encode(M + 1, P.d.g_lo ? P.d.g_lo + off : nullptr, P.d.ld, P.rows_cap, rstride, 128, false);
-    encode(M + 2, P.w, P.ld_w, P.din, P.ld_w, nt, false);
-    encode(M + 3, P.w_lo, P.ld_w, P.din, P.ld_w, nt, false);
+    encode(M + 1, P.w, P.ld_w, P.din, P.ld_w, nt, false);
   }
   a.tile_base[b.np] = tiles;
   dispatch<kDMean>(a, nt, tiles, st);
@@ -410,9 +421,7 @@ void wgrad_umma(WGradBatch& b, cudaStream_t st) {
     const std::size_t off = static_cast<std::size_t>(P.d.offset) * P.d.ld;
     const std::uint64_t rstride = static_cast<std::uint64_t>(P.d.stride) * P.d.ld;
     encode(M + 0, P.mean, P.ld_mean, P.rows_cap, P.ld_mean, 32, true);
-    encode(M + 1, P.mean_lo, P.ld_mean, P.rows_cap, P.ld_mean, 32, true);
-    encode(M + 2, P.d.g + off, P.d.ld, P.rows_cap, rstride, 32, true);
-    encode(M + 3, P.d.g_lo ? P.d.g_lo + off : nullptr, P.d.ld, P.rows_cap, rstride, 32, true);
+    encode(M + 1, P.d.g + off, P.d.ld, P.rows_cap, rstride, 32, true);
   }
   a.tile_base[b.np] = tiles;
   dispatch<kWGrad>(a, nt, tiles, st);

@@ -33,6 +33,9 @@ def assert_adam_close(w_ours, w_ref, w_before, lr=1e-2, tol=1e-3, max_flip_frac=
     bad = d > tol * scale
     frac = float(bad.mean()) if bad.size else 0.0
     assert frac <= max_flip_frac, f"{what}: {bad.sum()} of {bad.size} elements differ (max {d.max():.3e})"
+    # the tensor as a whole stays within the relative tolerance (Frobenius norm)
+    fro = float(np.linalg.norm(w_ours - w_ref) / max(np.linalg.norm(w_ref), 1e-30))
+    assert fro <= tol, f"{what}: relative Frobenius error {fro:.3e} > {tol:.1e}"
     if bad.any():
         bound = 2 * lr * steps * 1.01
         assert float(d[bad].max()) <= bound, f"{what}: a flip of {d[bad].max():.3e} > {bound:.3e} ({steps} steps)"
