@@ -33,7 +33,11 @@ namespace hetgpu {
 
 namespace {
 
-constexpr int kUT = 128;           // threads per CTA (4 warps = 4 TMEM lane quadrants)
+#ifndef HG_UMMA_WARPS
+#define HG_UMMA_WARPS 8
+#endif
+constexpr int kUT = HG_UMMA_WARPS * 32;  // threads per CTA: 4 or 8 warps (one or two per TMEM lane quadrant)
+constexpr int kConvWarps = HG_UMMA_WARPS - 2;  // warps 2.. form the tf32 residuals
 constexpr int kATile = 128 * 128;  // bytes of one 128 x 32 fp32 operand tile
 constexpr int kMaxMaps = 64;
 
@@ -85,7 +89,6 @@ __device__ __forceinline__ int find_tile(const int* base, int n, int tile) {
 
 template <int NT, int MODE, typename Batch>
 __global__ void __launch_bounds__(kUT) k_umma(const __grid_constant__ UmmaArgs<Batch> args) {
-  pdl_enter();
   constexpr int S = UStage<NT>::kStages;
   extern __shared__ std::uint8_t smem_raw[];
   std::uint8_t* smem = reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
@@ -96,11 +99,32 @@ __global__ void __launch_bounds__(kUT) k_umma(const __grid_constant__ UmmaArgs<B
   std::uint64_t* done = empty + S;
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(done + 1);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-
-  // ---- tile of this CTA -----------------------------------------------------------------
   const int p = find_tile(args.tile_base, args.np, blockIdx.x);
   const int t = blockIdx.x - args.tile_base[p];
   const int ntl = args.n_tiles[p];
+
+  // ---- setup, overlapping the predecessor's drain (PDL): barriers, TMEM, the
+  // tensor-map descriptors this CTA will use --------------------------------------------------
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      umma::mbar_init(umma::smem_u32(&full[i]), 1);
+      umma::mbar_init(umma::smem_u32(&conv[i]), kConvWarps);  // one arrival per converter warp
+      umma::mbar_init(umma::smem_u32(&empty[i]), 1);
+    }
+    umma::mbar_init(umma::smem_u32(done), 1);
+    umma::fence_mbar_init();
+    int nmaps = 2;
+    if constexpr (MODE == kProject) nmaps = 2 * args.b.g[p].nrel;
+    for (int i = 0; i < nmaps; ++i) umma::tma_prefetch_desc(&args.maps[map_index(MODE, p, 0, 0) + i]);
+  }
+  if (warp == 0) umma::tmem_alloc(umma::smem_u32(tmem_slot), UStage<NT>::kTmemCols);
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const std::uint32_t tmem = *tmem_slot;
+  pdl_enter();  // everything below reads what earlier kernels wrote
+
+  // ---- tile of this CTA -----------------------------------------------------------------
   int row0 = 0, m0 = 0, n0 = 0, nch = 0, n_live = 0;
   if constexpr (MODE == kProject) {
     const ProjGroup& g = args.b.g[p];
@@ -123,23 +147,10 @@ __global__ void __launch_bounds__(kUT) k_umma(const __grid_constant__ UmmaArgs<B
     row0 = (t / (mt * ntl)) * kWChunkRows;
     if (row0 < n_live) nch = (min(kWChunkRows, n_live - row0) + 31) / 32;
   }
-  if (row0 >= n_live) return;
-
-  // ---- setup: barriers, TMEM ---------------------------------------------------------------
-  if (tid == 0) {
-    for (int i = 0; i < S; ++i) {
-      umma::mbar_init(umma::smem_u32(&full[i]), 1);
-      umma::mbar_init(umma::smem_u32(&conv[i]), 2);  // one arrival per converter warp
-      umma::mbar_init(umma::smem_u32(&empty[i]), 1);
-    }
-    umma::mbar_init(umma::smem_u32(done), 1);
-    umma::fence_mbar_init();
+  if (row0 >= n_live) {  // an idle tile (capacity beyond the live rows)
+    if (warp == 0) umma::tmem_dealloc(tmem, UStage<NT>::kTmemCols);
+    return;
   }
-  if (warp == 0) umma::tmem_alloc(umma::smem_u32(tmem_slot), UStage<NT>::kTmemCols);
-  umma::fence_before_sync();
-  __syncthreads();
-  umma::fence_after_sync();
-  const std::uint32_t tmem = *tmem_slot;
 
   if (warp == 0 && lane == 0) {
     // ===== TMA producer =====
@@ -177,6 +188,7 @@ __global__ void __launch_bounds__(kUT) k_umma(const __grid_constant__ UmmaArgs<B
   } else if (warp >= 2) {
     // ===== tf32 split: lo = x - trunc_tf32(x) of the tiles that just landed, written
     // beside them (elementwise, so the swizzled layout carries over) =====
+    constexpr int kCT = kConvWarps * 32;
     const int ct = tid - 64;
     for (int ch = 0; ch < nch; ++ch) {
       const int s = ch % S;
@@ -184,11 +196,11 @@ __global__ void __launch_bounds__(kUT) k_umma(const __grid_constant__ UmmaArgs<B
       const float4* a = reinterpret_cast<const float4*>(smem + s * UStage<NT>::kBytes);
       float4* a_lo = const_cast<float4*>(a) + kATile / 16;
 #pragma unroll 4
-      for (int i = ct; i < kATile / 16; i += 64) a_lo[i] = tf32_lo4(a[i]);
+      for (int i = ct; i < kATile / 16; i += kCT) a_lo[i] = tf32_lo4(a[i]);
       const float4* b = a + 2 * kATile / 16;
       float4* b_lo = const_cast<float4*>(b) + UStage<NT>::kB / 16;
 #pragma unroll 4
-      for (int i = ct; i < UStage<NT>::kB / 16; i += 64) b_lo[i] = tf32_lo4(b[i]);
+      for (int i = ct; i < UStage<NT>::kB / 16; i += kCT) b_lo[i] = tf32_lo4(b[i]);
       umma::fence_async_smem();  // generic-proxy writes -> visible to the tensor core
       __syncwarp();
       if (lane == 0) umma::mbar_arrive(umma::smem_u32(&conv[s]));
@@ -201,15 +213,22 @@ __global__ void __launch_bounds__(kUT) k_umma(const __grid_constant__ UmmaArgs<B
     };
     for (int ch = 0; ch < nch; ++ch) {
       const int s = ch % S;
-      umma::mbar_wait(umma::smem_u32(&conv[s]), (ch / S) & 1);
-      umma::fence_after_sync();
       const std::uint32_t a_hi = umma::smem_u32(smem + s * UStage<NT>::kBytes), a_lo = a_hi + kATile;
       const std::uint32_t b_hi = a_hi + 2 * kATile, b_lo = b_hi + UStage<NT>::kB;
+      // hi.hi as soon as the tiles land (overlaps the residual pass) ...
+      umma::mbar_wait(umma::smem_u32(&full[s]), (ch / S) & 1);
+      umma::fence_after_sync();
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {  // 8 tf32 of K per MMA
+      for (int kk = 0; kk < 4; ++kk)  // 8 tf32 of K per MMA
+        umma::mma_tf32(tmem, dsc(Majors<MODE>::a, a_hi, kk), dsc(Majors<MODE>::b, b_hi, kk), kIdesc,
+                       (ch > 0 || kk > 0) ? 1u : 0u);
+      // ... then the two residual products
+      umma::mbar_wait(umma::smem_u32(&conv[s]), (ch / S) & 1);
+      umma::fence_after_sync();
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
         const std::uint64_t ah = dsc(Majors<MODE>::a, a_hi, kk), al = dsc(Majors<MODE>::a, a_lo, kk);
         const std::uint64_t bh = dsc(Majors<MODE>::b, b_hi, kk), bl = dsc(Majors<MODE>::b, b_lo, kk);
-        umma::mma_tf32(tmem, ah, bh, kIdesc, (ch > 0 || kk > 0) ? 1u : 0u);
         umma::mma_tf32(tmem, ah, bl, kIdesc, 1u);
         umma::mma_tf32(tmem, al, bh, kIdesc, 1u);
       }
@@ -222,10 +241,15 @@ __global__ void __launch_bounds__(kUT) k_umma(const __grid_constant__ UmmaArgs<B
   umma::fence_after_sync();
 
   // ---- epilogue: TMEM -> registers -> global ---------------------------------------------------
-  const int m = warp * 32 + lane;  // tile row owned by this thread
-  const std::uint32_t trow = tmem + (static_cast<std::uint32_t>(warp * 32) << 16);
+  // warp w reads TMEM lane quadrant w % 4 (its tile rows) and column half w / 4
+  const int quad = warp & 3;
+  const int m = quad * 32 + lane;  // tile row owned by this thread
+  const std::uint32_t trow = tmem + (static_cast<std::uint32_t>(quad * 32) << 16);
+  constexpr int kEpiWarps = HG_UMMA_WARPS < 8 ? HG_UMMA_WARPS : 8;  // warps draining TMEM
+  constexpr int kColsPerWarp = NT / (kEpiWarps / 4);
+  const int c_begin = warp < kEpiWarps ? (warp >> 2) * kColsPerWarp : NT;
 #pragma unroll 1
-  for (int c0 = 0; c0 < NT; c0 += 16) {
+  for (int c0 = c_begin; c0 < c_begin + kColsPerWarp && c0 < NT; c0 += 16) {
     float v[16];
     umma::tmem_ld16(trow + c0, v);
     if constexpr (MODE == kProject) {

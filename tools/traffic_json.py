@@ -24,12 +24,34 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9,
+         "ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
+
+
 def rows_of(path):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True,
-                         check=True).stdout
+    """Rows of an ncu report (`.ncu-rep`) or of its `--page raw --csv` export
+    (`.csv` / `.csv.gz`), with byte and time metrics normalised to bytes and us."""
+    if path.endswith(".csv.gz"):
+        import gzip
+        raw = gzip.open(path, "rt").read()
+    elif path.endswith(".csv"):
+        raw = open(path).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True,
+                             check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    h = rows[0]
-    return [dict(zip(h, r)) for r in rows[2:]]
+    h, units = rows[0], rows[1]
+    out = []
+    for r in rows[2:]:
+        d = dict(zip(h, r))
+        for k, u in zip(h, units):
+            if u in UNITS and k in d:
+                try:
+                    d[k] = str(float(d[k].replace(",", "")) * UNITS[u])
+                except ValueError:
+                    pass
+        out.append(d)
+    return out
 
 
 def num(d, k):
@@ -40,7 +62,8 @@ def num(d, k):
 
 
 def short(name):
-    n = re.sub(r"(hetgpu::)?(\(anonymous namespace\)|<unnamed>)::|^void ", "", name).strip()
+    """Kernel name without namespaces and parameter list, template arguments kept."""
+    n = name.strip()
     if n.endswith(")"):  # drop the parameter list (the trailing balanced group)
         depth = 0
         for i in range(len(n) - 1, -1, -1):
@@ -48,7 +71,13 @@ def short(name):
             if depth == 0:
                 n = n[:i]
                 break
-    return n.strip()
+    base, tmpl = (n.split("<", 1) + [""])[:2] if "<" in n and not n.startswith("<") else (n, "")
+    if n.startswith("<") or "unnamed>" in n:
+        base = n.split("::")[-1] if "<" not in n.split("::")[-1] else n
+        m = re.search(r"(k_\w+)(<.*>)?$", n)
+        return (m.group(1) + (m.group(2) or "")) if m else n
+    base = re.sub(r"^void ", "", base).split("::")[-1]
+    return base + ("<" + tmpl if tmpl else "")
 
 
 def main():
@@ -72,9 +101,8 @@ def main():
         rd = sum(num(d, "dram__bytes_read.sum") for d in ds) / len(ds)
         wr = sum(num(d, "dram__bytes_write.sum") for d in ds) / len(ds)
         us = sum(num(d, "gpu__time_duration.sum") for d in ds) / len(ds)
-        unit = ds[0].get("gpu__time_duration.sum", "")
         e = {"launches": len(ds), "dram_bytes_per_launch": int(rd + wr), "read": int(rd), "write": int(wr),
-             "duration_per_launch": us,
+             "us_per_launch": us,
              "dram_pct_of_peak": sum(num(d, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed") for d in ds) / len(ds),
              "occupancy_pct": sum(num(d, "sm__warps_active.avg.pct_of_peak_sustained_active") for d in ds) / len(ds)}
         tp = [num(d, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active") for d in ds]
@@ -89,7 +117,7 @@ def main():
                           text=True).stdout.strip()
     rec = {"source": cmd, "metrics": "dram__bytes_read.sum + dram__bytes_write.sum per launch; "
                                      "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
-           "duration_unit": unit, "lib_sha256_16": sha, "git_head_at_capture": head,
+           "lib_sha256_16": sha, "git_head_at_capture": head,
            "tensor_pipe_pct": {k: round(v["tensor_pipe_pct"], 2) for k, v in out.items() if "tensor_pipe_pct" in v},
            "kernels": out}
     print(json.dumps(rec, indent=1))
