@@ -180,7 +180,9 @@ int hg_engine_info(hg_engine* e, uint64_t* param_count, uint64_t* device_bytes, 
  * tcgen05 tensor cores, 3xTF32; 0 = SIMT fp32 tiles for A/B checks; default 1),
  * "elem_bytes" (AccountingModel::elem_bytes of the sync_bytes model: 2, 4 or 8; default 4),
  * "shard_merge" (replica groups: each replica Adam-updates only its id shard of the merged
- * learnable rows and stores them into every copy; default 0) */
+ * learnable rows and stores them into every copy; default 0), "apply_adam" (0: training
+ * steps compute every gradient but leave parameters and Adam state untouched — the caller
+ * owns the optimizer; p = 1 or partitions without replicas; default 1) */
 int hg_engine_set_option(hg_engine* e, const char* name, int value);
 /* Device self-test of the tcgen05 contractions against the fp32 SIMT tiles on random
  * problems: cases = n_cases x (rows, nrel, din, dout); err = [n_cases x 3] relative
@@ -215,6 +217,86 @@ int hg_engine_attach_nccl(hg_engine* e, const void* unique_id, int id_bytes, int
  * replicas) to hg_engine_attach_replicas after hg_engine_attach_nccl. */
 int hg_engine_replica_handle(hg_engine* e, void* out, int cap);
 int hg_engine_attach_replicas(hg_engine* e, const void* handles, int handle_bytes, int nranks);
+
+/* sample_neighbors (src/sampling.cpp:17-39) on a host CSR (indptr u64 [n_dst+1], src u32):
+ * min(fanout, deg) sources of `dst` in draw order into out (capacity >= fanout); rows with
+ * deg > fanout are drawn on the device (exact mt19937_64 + Lemire + partial Fisher-Yates) */
+int hg_sample_neighbors(const uint64_t* indptr, uint64_t n_dst, const uint32_t* src, uint32_t dst, int fanout,
+                        uint64_t rng_seed, int hop, int rel, uint32_t* out, int* n_out, int device);
+
+/* ---- model state for caller-owned models (hgnn.hpp:34-62) ------------------------------- */
+/* init_model (src/hgnn.cpp:39-62) on the BFS metatree of depth k: w.r{r}.l{l} f64
+ * [din x dout], input_dims, k. init_learnable (src/hgnn.cpp:64-81): learn.t{t} f64
+ * [count x dim]. Both bit-identical to the reference (same libstdc++ engines). */
+hg_bundle* hg_init_model(const hg_graph* g, int k, int hidden, uint64_t seed);
+hg_bundle* hg_init_learnable(const hg_graph* g, uint64_t seed);
+/* Borrowed views of the host graph: a type's dense f32 features ([rows x dim] row-major,
+ * NULL unless kind == 1) and the labels (hetgraph.hpp:58-74). */
+int hg_graph_dense(const hg_graph* g, int type, const float** data, uint64_t* rows, int* dim, int* kind);
+int hg_graph_labels(const hg_graph* g, const int32_t** labels, uint64_t* n);
+/* Caller-owned parameters for an engine (run_raf_batch with the caller's HGNNModel /
+ * LearnableStore, raf.hpp:79-82): one weight slot (f64 [din x dout]) and rows of a
+ * learnable table (f64 [n x dim]). With the option "apply_adam" = 0 a training step
+ * computes every gradient (grad.w.*, grad.f.*) and leaves the parameters untouched. */
+int hg_engine_load_weights(hg_engine* e, int rel, int layer, const double* w, int din, int dout);
+int hg_engine_load_table_rows(hg_engine* e, int type, const uint32_t* ids, int64_t n, const double* rows, int dim);
+
+/* ---- layer interface on device tensors (hgnn.hpp:76-130) ----------------------------------
+ * A context owns a device stream; every primitive is stream-ordered on it and returns at
+ * once. Device-side errors are raised by hg_ctx_sync with the reference's exception type
+ * and message ("node id not in frontier: <id>" = invalid_argument, "non-finite gradient" =
+ * runtime_error). Tensors are row-major fp32 device matrices whose row stride `ld` is a
+ * multiple of 4 with zero padding; index arrays are device u32 unless stated otherwise. */
+typedef struct hg_ctx hg_ctx;
+typedef struct {
+  float* data;
+  int64_t rows;
+  int32_t cols;
+  int32_t ld;
+} hg_tensor;
+hg_ctx* hg_ctx_create(int device);
+void hg_ctx_free(hg_ctx* c);
+int hg_ctx_sync(hg_ctx* c);
+void* hg_ctx_malloc(hg_ctx* c, size_t bytes); /* zero-filled device memory */
+int hg_ctx_mfree(hg_ctx* c, void* p);
+int hg_ctx_copy(hg_ctx* c, void* dst, const void* src, size_t bytes); /* any direction, synchronous */
+/* row_index (src/hgnn.cpp:166-171): rows[i] = position of ids[i] in the sorted list */
+int hg_rows_in(hg_ctx* c, const uint32_t* ids, int64_t n, const uint32_t* sorted, int64_t n_sorted, uint32_t* rows);
+/* mean_aggregate (src/hgnn.cpp:173-187): out[i] = mean of h_src[src_rows[e]] over the
+ * block's segment i (u32 indptr), zero rows for empty segments; out [n_dst x h_src.cols] */
+int hg_mean_aggregate(hg_ctx* c, const uint32_t* indptr, int64_t n_dst, const uint32_t* src_rows, hg_tensor h_src,
+                      hg_tensor out);
+/* agg_relation + agg_all (src/hgnn.cpp:189-203): out (+)= sum_r means[r] . ws[r], ReLU
+ * optional (src/hgnn.cpp:271-272); 1-8 relations; tcgen05 kind::tf32 3xTF32 */
+int hg_project(hg_ctx* c, const hg_tensor* means, const hg_tensor* ws, int nrel, hg_tensor out, int relu,
+               int accumulate);
+/* agg_all (src/hgnn.cpp:194-203): ordered elementwise sum of 1..32 partials */
+int hg_agg_all(hg_ctx* c, const hg_tensor* partials, int n, hg_tensor out);
+/* x = max(x, 0), or with a mask: x *= [mask > 0] (dpre = dH (x) [H > 0], src/hgnn.cpp:326-328) */
+int hg_relu(hg_ctx* c, hg_tensor x, const hg_tensor* mask);
+/* the layer-0 gather of forward_flat (src/hgnn.cpp:223-242): out[i] = table[ids[i]] */
+int hg_gather_rows(hg_ctx* c, hg_tensor table, const uint32_t* ids, int64_t n, hg_tensor out);
+/* cross_entropy (src/hgnn.cpp:281-307) on device logits; row_ids (sorted), batch and
+ * labels (indexed by node id) are HOST arrays; dlogits may be NULL; synchronous */
+int hg_cross_entropy(hg_ctx* c, hg_tensor logits, const uint32_t* row_ids, int64_t n_rows, const uint32_t* batch,
+                     int64_t n_batch, const int32_t* labels, int64_t n_labels, int num_classes,
+                     const hg_tensor* dlogits, double* loss);
+/* matmul_tn_acc (src/matrix.hpp:49-61): dw (+)= mean^T . dpre (tcgen05, ordered split-K) */
+int hg_weight_grad(hg_ctx* c, hg_tensor mean, hg_tensor dpre, hg_tensor dw, int accumulate);
+/* matmul_nt (src/matrix.hpp:64-78) with the scatter's 1/deg (src/hgnn.cpp:337-353):
+ * dmean[i] = (dpre[i] . W^T) / deg_i, deg from the block's u32 indptr */
+int hg_mean_grad(hg_ctx* c, hg_tensor dpre, hg_tensor w, const uint32_t* indptr, hg_tensor dmean);
+/* the backward scatter (src/hgnn.cpp:344-353): dh_src[src_rows[e]] += dmean[row(e)] for
+ * every edge e, as a source-major ordered gather (deterministic) */
+int hg_scatter_rows(hg_ctx* c, const uint32_t* indptr, int64_t n_dst, int64_t n_edges, const uint32_t* src_rows,
+                    hg_tensor dmean, hg_tensor dh_src);
+/* adam_step (src/hgnn.cpp:364-377) over n elements at Adam step `step` (adam_update_model
+ * calls it per slot); adam_update_rows (src/hgnn.cpp:392-410) on listed table rows at the
+ * table's advanced step */
+int hg_adam_dense(hg_ctx* c, float* w, float* m, float* v, const float* g, int64_t n, int64_t step, double lr,
+                  double beta1, double beta2, double eps);
+int hg_adam_rows(hg_ctx* c, hg_tensor w, hg_tensor m, hg_tensor v, const uint32_t* rows, int64_t n, hg_tensor grads,
+                 int64_t step, double lr, double beta1, double beta2, double eps);
 
 #ifdef __cplusplus
 }

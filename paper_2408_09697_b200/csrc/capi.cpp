@@ -12,6 +12,7 @@
 #include "engine.hpp"
 #include "gemm.cuh"
 #include "host.hpp"
+#include "layers.hpp"
 
 #ifdef HG_WITH_NCCL
 #include <nccl.h>
@@ -28,6 +29,9 @@ struct hg_engine {
   ncclComm_t comm = nullptr;
   ncclComm_t rcomm = nullptr;  // replica group (ncclCommSplit of comm)
 #endif
+};
+struct hg_ctx {
+  std::unique_ptr<LayerCtx> c;
 };
 struct hg_bundle {
   struct Item {
@@ -217,6 +221,9 @@ hg_bundle* hg_graph_schema(const hg_graph* h) {
     b->add("num_classes", "<i8", std::vector<long long>{g.num_classes});
     b->add("rel_src", "<i4", rs);
     b->add("rel_dst", "<i4", rd);
+    std::string names;  // node type names, '\n'-separated (hetgraph.hpp TypeRegistry)
+    for (const auto& t : g.types) names += t.name + "\n";
+    b->add("type_names", "|u1", std::vector<char>(names.begin(), names.end()));
     return b;
   });
 }
@@ -304,6 +311,12 @@ hg_bundle* hg_meta_partition(const hg_graph* h, int k, int p) {
       slot_rows.push_back(static_cast<int>(who.size()));
     }
     b->add("raf.slot_contributors", "<i4", slot_rows);
+    std::vector<int> leaf_rows;  // (learnable leaf type, n_possible_contributors)
+    for (const auto& [t, who] : a.leaf_owners) {
+      leaf_rows.push_back(t);
+      leaf_rows.push_back(static_cast<int>(who.size()));
+    }
+    b->add("raf.leaf_owners", "<i4", leaf_rows);
     return b;
   });
 }
@@ -564,6 +577,8 @@ int hg_engine_set_option(hg_engine* e, const char* name, int value) {
       e->e->set_trace_sampler(value != 0);
     else if (n == "shard_merge")
       e->e->set_shard_merge(value != 0);
+    else if (n == "apply_adam")
+      e->e->set_apply_adam(value != 0);
     else
       throw std::invalid_argument("unknown engine option: " + n);
     return 0;
@@ -736,6 +751,243 @@ int hg_engine_attach_nccl(hg_engine* e, const void* unique_id, int id_bytes, int
     throw std::runtime_error("built without NCCL");
     return -1;
 #endif
+  });
+}
+
+
+// ---- model state (init_model / init_learnable, hgnn.cpp:39-81) -------------------------
+hg_bundle* hg_init_model(const hg_graph* h, int k, int hidden, uint64_t seed) {
+  return guard<hg_bundle*>(nullptr, [&] {
+    const Graph& g = h->g;
+    const Tree tree = bfs_tree(schema_of(g), g.target, k);
+    const ModelInit mi = init_model(g, tree, hidden, seed);
+    auto* b = new hg_bundle;
+    b->add("input_dims", "<i4", mi.input_dims);
+    b->add("k", "<i4", std::vector<int>{mi.k});
+    for (const auto& [id, w] : mi.weights)
+      b->add("w.r" + std::to_string(id.rel) + ".l" + std::to_string(id.layer), "<f8", w.values,
+             {static_cast<long long>(w.in_dim), static_cast<long long>(w.out_dim)});
+    return b;
+  });
+}
+
+hg_bundle* hg_init_learnable(const hg_graph* h, uint64_t seed) {
+  return guard<hg_bundle*>(nullptr, [&] {
+    const Graph& g = h->g;
+    auto* b = new hg_bundle;
+    for (auto& [t, v] : init_learnable(g, seed))
+      b->add("learn.t" + std::to_string(t), "<f8", v,
+             {static_cast<long long>(g.types[t].count), static_cast<long long>(g.types[t].dim)});
+    return b;
+  });
+}
+
+int hg_graph_dense(const hg_graph* h, int type, const float** data, uint64_t* rows, int* dim, int* kind) {
+  return guard<int>(-1, [&] {
+    const Graph& g = h->g;
+    if (type < 0 || type >= g.num_types()) throw std::invalid_argument("unknown node type " + std::to_string(type));
+    const NodeTypeInfo& t = g.types[type];
+    if (data) *data = t.storage == Storage::Dense ? t.dense.data() : nullptr;
+    if (rows) *rows = t.count;
+    if (dim) *dim = t.dim;
+    if (kind) *kind = static_cast<int>(t.storage);
+    return 0;
+  });
+}
+
+int hg_graph_labels(const hg_graph* h, const int32_t** labels, uint64_t* n) {
+  return guard<int>(-1, [&] {
+    if (labels) *labels = h->g.labels.data();
+    if (n) *n = h->g.labels.size();
+    return 0;
+  });
+}
+
+int hg_engine_load_weights(hg_engine* e, int rel, int layer, const double* w, int din, int dout) {
+  return guard<int>(-1, [&] {
+    e->e->load_weights(rel, layer, w, din, dout);
+    return 0;
+  });
+}
+
+int hg_engine_load_table_rows(hg_engine* e, int type, const uint32_t* ids, int64_t n, const double* rows, int dim) {
+  return guard<int>(-1, [&] {
+    e->e->load_table_rows(type, ids, n, rows, dim);
+    return 0;
+  });
+}
+
+// ---- layer interface (hgnn.hpp:76-130) on device tensors ------------------------------------
+namespace {
+DevTensor dt(const hg_tensor& t) { return DevTensor{t.data, t.rows, t.cols, t.ld}; }
+std::vector<DevTensor> dts(const hg_tensor* t, int n) {
+  std::vector<DevTensor> v;
+  for (int i = 0; i < n; ++i) v.push_back(dt(t[i]));
+  return v;
+}
+AdamHyper hyper(double lr, double b1, double b2, double eps) {
+  AdamHyper hp;
+  hp.lr = lr;
+  hp.beta1 = b1;
+  hp.beta2 = b2;
+  hp.eps = eps;
+  return hp;
+}
+}  // namespace
+
+hg_ctx* hg_ctx_create(int device) {
+  return guard<hg_ctx*>(nullptr, [&] {
+    auto* c = new hg_ctx;
+    c->c = std::make_unique<LayerCtx>(device);
+    return c;
+  });
+}
+void hg_ctx_free(hg_ctx* c) { delete c; }
+int hg_ctx_sync(hg_ctx* c) {
+  return guard<int>(-1, [&] {
+    c->c->sync();
+    return 0;
+  });
+}
+void* hg_ctx_malloc(hg_ctx* c, size_t bytes) {
+  return guard<void*>(nullptr, [&] {
+    HG_CUDA(cudaSetDevice(c->c->device()));
+    void* p = nullptr;
+    HG_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+    HG_CUDA(cudaMemset(p, 0, std::max<size_t>(bytes, 16)));
+    return p;
+  });
+}
+int hg_ctx_mfree(hg_ctx* c, void* p) {
+  return guard<int>(-1, [&] {
+    HG_CUDA(cudaStreamSynchronize(c->c->stream()));
+    HG_CUDA(cudaFree(p));
+    return 0;
+  });
+}
+int hg_ctx_copy(hg_ctx* c, void* dst, const void* src, size_t bytes) {
+  return guard<int>(-1, [&] {
+    HG_CUDA(cudaSetDevice(c->c->device()));
+    HG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->c->stream()));
+    HG_CUDA(cudaStreamSynchronize(c->c->stream()));
+    return 0;
+  });
+}
+int hg_rows_in(hg_ctx* c, const uint32_t* ids, int64_t n, const uint32_t* sorted, int64_t n_sorted, uint32_t* rows) {
+  return guard<int>(-1, [&] {
+    c->c->rows_in(ids, n, sorted, n_sorted, rows);
+    return 0;
+  });
+}
+int hg_mean_aggregate(hg_ctx* c, const uint32_t* indptr, int64_t n_dst, const uint32_t* src_rows, hg_tensor h_src,
+                      hg_tensor out) {
+  return guard<int>(-1, [&] {
+    c->c->mean_aggregate(indptr, n_dst, src_rows, dt(h_src), dt(out));
+    return 0;
+  });
+}
+int hg_project(hg_ctx* c, const hg_tensor* means, const hg_tensor* ws, int nrel, hg_tensor out, int relu,
+               int accumulate) {
+  return guard<int>(-1, [&] {
+    const auto m = dts(means, nrel), w = dts(ws, nrel);
+    c->c->project(m.data(), w.data(), nrel, dt(out), relu != 0, accumulate != 0);
+    return 0;
+  });
+}
+int hg_agg_all(hg_ctx* c, const hg_tensor* partials, int n, hg_tensor out) {
+  return guard<int>(-1, [&] {
+    const auto p = dts(partials, n);
+    c->c->agg_all(p.data(), n, dt(out));
+    return 0;
+  });
+}
+int hg_relu(hg_ctx* c, hg_tensor x, const hg_tensor* mask) {
+  return guard<int>(-1, [&] {
+    const DevTensor mk = mask ? dt(*mask) : DevTensor{};
+    c->c->relu(dt(x), mask ? &mk : nullptr);
+    return 0;
+  });
+}
+int hg_gather_rows(hg_ctx* c, hg_tensor table, const uint32_t* ids, int64_t n, hg_tensor out) {
+  return guard<int>(-1, [&] {
+    c->c->gather_rows(dt(table), ids, n, dt(out));
+    return 0;
+  });
+}
+int hg_cross_entropy(hg_ctx* c, hg_tensor logits, const uint32_t* row_ids, int64_t n_rows, const uint32_t* batch,
+                     int64_t n_batch, const int32_t* labels, int64_t n_labels, int num_classes,
+                     const hg_tensor* dlogits, double* loss) {
+  return guard<int>(-1, [&] {
+    const DevTensor dz = dlogits ? dt(*dlogits) : DevTensor{};
+    const double l = c->c->cross_entropy(dt(logits), row_ids, n_rows, batch, n_batch, labels, n_labels, num_classes,
+                                         dlogits ? &dz : nullptr);
+    if (loss) *loss = l;
+    return 0;
+  });
+}
+int hg_weight_grad(hg_ctx* c, hg_tensor mean, hg_tensor dpre, hg_tensor dw, int accumulate) {
+  return guard<int>(-1, [&] {
+    c->c->weight_grad(dt(mean), dt(dpre), dt(dw), accumulate != 0);
+    return 0;
+  });
+}
+int hg_mean_grad(hg_ctx* c, hg_tensor dpre, hg_tensor w, const uint32_t* indptr, hg_tensor dmean) {
+  return guard<int>(-1, [&] {
+    c->c->mean_grad(dt(dpre), dt(w), indptr, dt(dmean));
+    return 0;
+  });
+}
+int hg_scatter_rows(hg_ctx* c, const uint32_t* indptr, int64_t n_dst, int64_t n_edges, const uint32_t* src_rows,
+                    hg_tensor dmean, hg_tensor dh_src) {
+  return guard<int>(-1, [&] {
+    c->c->scatter_rows(indptr, n_dst, n_edges, src_rows, dt(dmean), dt(dh_src));
+    return 0;
+  });
+}
+int hg_adam_dense(hg_ctx* c, float* w, float* m, float* v, const float* g, int64_t n, int64_t step, double lr,
+                  double beta1, double beta2, double eps) {
+  return guard<int>(-1, [&] {
+    c->c->adam_dense(w, m, v, g, n, step, hyper(lr, beta1, beta2, eps));
+    return 0;
+  });
+}
+int hg_adam_rows(hg_ctx* c, hg_tensor w, hg_tensor m, hg_tensor v, const uint32_t* rows, int64_t n, hg_tensor grads,
+                 int64_t step, double lr, double beta1, double beta2, double eps) {
+  return guard<int>(-1, [&] {
+    c->c->adam_rows(dt(w), dt(m), dt(v), rows, n, dt(grads), step, hyper(lr, beta1, beta2, eps));
+    return 0;
+  });
+}
+
+// sample_neighbors (src/sampling.cpp:17-39): copy-all rows on the host, drawn rows on the device
+int hg_sample_neighbors(const uint64_t* indptr, uint64_t n_dst, const uint32_t* src, uint32_t dst, int fanout,
+                        uint64_t rng_seed, int hop, int rel, uint32_t* out, int* n_out, int device) {
+  return guard<int>(-1, [&] {
+    if (dst >= n_dst) throw std::invalid_argument("destination id out of range: " + std::to_string(dst));
+    if (fanout < 0) throw std::invalid_argument("fanout must be non-negative");
+    const std::uint64_t lo = indptr[dst], deg = indptr[dst + 1] - lo;
+    if (deg <= static_cast<std::uint64_t>(fanout)) {
+      std::copy(src + lo, src + lo + deg, out);
+      if (n_out) *n_out = static_cast<int>(deg);
+      return 0;
+    }
+    if (deg > 0xFFFFFFFFull) throw std::invalid_argument("degree beyond the u32 position range");
+    HG_CUDA(cudaSetDevice(device));
+    const std::uint64_t seed =
+        mix_seed(rng_seed, mix_seed((static_cast<std::uint64_t>(hop) << 32) | static_cast<std::uint64_t>(rel), dst));
+    std::uint32_t *d_nbr = nullptr, *d_out = nullptr;
+    std::uint64_t* d_scr = nullptr;
+    HG_CUDA(cudaMalloc(&d_nbr, deg * 4));
+    HG_CUDA(cudaMalloc(&d_out, static_cast<std::size_t>(fanout) * 4 + 4));
+    HG_CUDA(cudaMalloc(&d_scr, (312 + static_cast<std::size_t>(fanout)) * 8));
+    HG_CUDA(cudaMemcpy(d_nbr, src + lo, deg * 4, cudaMemcpyHostToDevice));
+    sample_row(d_nbr, deg, fanout, seed, d_out, d_scr, nullptr);
+    HG_CUDA(cudaMemcpy(out, d_out, static_cast<std::size_t>(fanout) * 4, cudaMemcpyDeviceToHost));
+    cudaFree(d_nbr);
+    cudaFree(d_out);
+    cudaFree(d_scr);
+    if (n_out) *n_out = fanout;
+    return 0;
   });
 }
 

@@ -1023,7 +1023,7 @@ void Engine::run_forward() {
 void Engine::run_loss(bool train) {
   LossArgs la{};
   la.done = loss_done_;
-  if (train) {
+  if (train && apply_adam_) {
     // learnable layer-0 tables advance their Adam step before the fused row
     // update of the backward pass; the loss kernel's last CTA does it
     for (const auto& c : cscs_)
@@ -1274,7 +1274,7 @@ CscHop Engine::csc_hop(int h) {
     t.src_cap = c.src_cap;
     // replicas merge their learnable-row gradients before Adam: keep the rows
     const bool exchanged = h == o_.k && xchg_type(c.src_t);
-    const bool leaf_learnable = h == o_.k && tables_[c.src_t].learnable && !exchanged;
+    const bool leaf_learnable = h == o_.k && tables_[c.src_t].learnable && !exchanged && apply_adam_;
     t.dh = (!leaf_learnable || retain_grads_) ? c.dh : nullptr;
     t.ld_dh = c.ld;
     t.din = c.din;
@@ -1312,6 +1312,7 @@ CscHop Engine::csc_hop(int h) {
 }
 
 void Engine::run_update() {
+  if (!apply_adam_) return;        // gradient-only step (caller-owned optimizer)
   if (fused_model_adam()) return;  // applied by the weight-gradient reductions
   AdamHyper hp;
   AdamModelBatch mb{};
@@ -1901,6 +1902,69 @@ bool Engine::read_tensor(const std::string& name, std::string& dtype, std::vecto
     }
   }
   return false;
+}
+
+}  // namespace hetgpu
+
+namespace hetgpu {
+namespace {
+__global__ void k_put_rows(float* table, int ld, const std::uint32_t* ids, std::int64_t n, const float* rows,
+                           int dim) {
+  const std::int64_t total = n * dim;
+  for (std::int64_t x = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; x < total;
+       x += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    const std::int64_t i = x / dim;
+    const int c = static_cast<int>(x % dim);
+    table[static_cast<std::int64_t>(ids[i]) * ld + c] = rows[i * dim + c];
+  }
+}
+}  // namespace
+
+void Engine::load_weights(int rel, int layer, const double* w, int din, int dout) {
+  quiesce();
+  for (auto& s : slots_) {
+    if (s.rel != rel || s.layer != layer) continue;
+    if (s.din != din || s.dout != dout)
+      throw std::invalid_argument("weight/input dim mismatch for relation " + std::to_string(rel));
+    std::vector<float> host(static_cast<std::size_t>(std::max(1, s.din)) * s.ld, 0.0f);
+    for (int i = 0; i < din; ++i)
+      for (int j = 0; j < dout; ++j) host[static_cast<std::size_t>(i) * s.ld + j] = static_cast<float>(w[i * dout + j]);
+    const std::size_t bytes = host.size() * 4;
+    HG_CUDA(cudaMemcpyAsync(s.w, host.data(), bytes, cudaMemcpyHostToDevice, st_));
+    HG_CUDA(cudaMemsetAsync(s.m, 0, bytes, st_));
+    HG_CUDA(cudaMemsetAsync(s.v, 0, bytes, st_));
+    HG_CUDA(cudaStreamSynchronize(st_));
+    return;
+  }
+  // a slot this partition does not evaluate: nothing to load
+}
+
+void Engine::load_table_rows(int type, const NodeId* ids, std::int64_t n, const double* rows, int dim) {
+  if (type < 0 || type >= ntypes_ || !tables_[type].learnable)
+    throw std::invalid_argument("no learnable table for node type " + std::to_string(type));
+  const TypeTable& tb = tables_[type];
+  if (!tb.w) return;  // not a layer-0 type of this partition
+  if (dim != tb.dim) throw std::invalid_argument("learnable row width mismatch for node type " + std::to_string(type));
+  if (n <= 0) return;
+  for (std::int64_t i = 0; i < n; ++i)
+    if (ids[i] >= type_counts_[type]) throw std::invalid_argument("node id out of range: " + std::to_string(ids[i]));
+  quiesce();
+  std::vector<float> host(static_cast<std::size_t>(n) * dim);
+  for (std::size_t i = 0; i < host.size(); ++i) host[i] = static_cast<float>(rows[i]);
+  void* d_ids = nullptr;
+  void* d_rows = nullptr;
+  HG_CUDA(cudaMallocAsync(&d_ids, static_cast<std::size_t>(n) * 4, st_));
+  HG_CUDA(cudaMallocAsync(&d_rows, host.size() * 4, st_));
+  HG_CUDA(cudaMemcpyAsync(d_ids, ids, static_cast<std::size_t>(n) * 4, cudaMemcpyHostToDevice, st_));
+  HG_CUDA(cudaMemcpyAsync(d_rows, host.data(), host.size() * 4, cudaMemcpyHostToDevice, st_));
+  const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(static_cast<std::uint64_t>(n) * dim, 256),
+                                                                      8ull * num_sms()));
+  k_put_rows<<<std::max(1u, grid), 256, 0, st_>>>(tb.w, tb.ld, static_cast<const std::uint32_t*>(d_ids), n,
+                                                  static_cast<const float*>(d_rows), dim);
+  HG_CUDA(cudaGetLastError());
+  HG_CUDA(cudaFreeAsync(d_ids, st_));
+  HG_CUDA(cudaFreeAsync(d_rows, st_));
+  HG_CUDA(cudaStreamSynchronize(st_));
 }
 
 }  // namespace hetgpu

@@ -133,6 +133,21 @@ class Engine {
       drop_graphs();
     }
   }
+  // train steps compute gradients but leave the model and tables untouched (the
+  // caller owns the optimizer state: run_raf_batch with a caller's HGNNModel,
+  // raf.hpp:79-82, followed by the caller's own adam_update_* calls)
+  void set_apply_adam(bool on) {
+    if (on != apply_adam_) {
+      if (!on && replica_group_.size() > 1) throw std::invalid_argument("gradient-only steps need p = 1 or no replicas");
+      apply_adam_ = on;
+      drop_graphs();
+    }
+  }
+  // caller-owned parameters: one weight slot (f64 [din x dout] row-major; its Adam
+  // moments are reset) and rows of a learnable table (f64 [n x dim]; with
+  // apply_adam off the engine's moments are never read)
+  void load_weights(int rel, int layer, const double* w, int din, int dout);
+  void load_table_rows(int type, const NodeId* ids, std::int64_t n, const double* rows, int dim);
   StepReport finish_step();  // waits for the last trained step and reads its report
   // payload element width of the accounting model (AccountingModel::elem_bytes, raf.hpp:15-19)
   void set_trace_sampler(bool on) {
@@ -408,6 +423,7 @@ class Engine {
   bool use_umma_ = true;
   bool counting_ = false;  // count_launches capture in progress (no collectives)  // tcgen05 contractions (0: SIMT fp32 tiles, kept for A/B checks)
   bool retain_grads_ = true;
+  bool apply_adam_ = true;
   struct CscRegion {
     std::uint32_t *offs, *cursor;
     std::size_t words;
@@ -459,7 +475,7 @@ class Engine {
   }
   void run_replica_merge();
   void replica_prepare();
-  bool fused_model_adam() const { return replica_group_.size() <= 1; }
+  bool fused_model_adam() const { return replica_group_.size() <= 1 && apply_adam_; }
   std::vector<ReplicaMerge> merges_;  // built by replica_prepare for run_replica_merge
   bool training_ = false;
 };

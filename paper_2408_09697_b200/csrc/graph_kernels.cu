@@ -436,7 +436,23 @@ __global__ void __launch_bounds__(128) k_sample_slow(SampleHop h, const StepScal
   }
 }
 
+// one row of sample_neighbors (sampling.cpp:17-39) on the full-state engine
+__global__ void k_sample_row(const std::uint32_t* nbr, std::uint64_t deg, int fanout, std::uint64_t seed,
+                             std::uint32_t* out, std::uint64_t* scratch) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  MtFull eng{scratch, 0};
+  eng.seed(seed);
+  std::uint32_t* mpos = reinterpret_cast<std::uint32_t*>(scratch + 312);
+  draw_row(eng, deg, fanout, nbr, out, mpos, mpos + fanout);
+}
+
 }  // namespace
+
+void sample_row(const std::uint32_t* d_nbr, std::uint64_t deg, int fanout, std::uint64_t seed, std::uint32_t* d_out,
+                std::uint64_t* d_scratch, cudaStream_t st) {
+  k_sample_row<<<1, 32, 0, st>>>(d_nbr, deg, fanout, seed, d_out, d_scratch);
+  HG_CUDA(cudaGetLastError());
+}
 
 std::size_t sample_scratch_words(int fanout) {
   return static_cast<std::size_t>(kSlowThreads) * (312 + static_cast<std::size_t>(fanout));

@@ -90,6 +90,10 @@ struct SampleHop {
 // capacity = total rows) and are replayed with the full-state engine on
 // `scratch` (sample_scratch_words(fanout) u64).
 std::size_t sample_scratch_words(int fanout);
+// one row drawn on the device (sample_neighbors, sampling.cpp:17-39, for deg > fanout):
+// seed = mix_seed(rng_seed, mix_seed(hop << 32 | rel, dst)); scratch: 312 u64 + fanout u64
+void sample_row(const std::uint32_t* d_nbr, std::uint64_t deg, int fanout, std::uint64_t seed, std::uint32_t* d_out,
+                std::uint64_t* d_scratch, cudaStream_t st);
 void sample_hop(const SampleHop& h, const StepScalars* sc, std::uint32_t* slow, int* n_slow,
                 std::uint64_t* scratch, LbScratch& lb, cudaStream_t st);
 
