@@ -104,6 +104,11 @@ def lib():
             "hg_engine_attach_nccl": ([vp, vp, i32, i32, i32], i32),
             "hg_engine_replica_handle": ([vp, vp, i32], i32),
             "hg_engine_attach_replicas": ([vp, vp, i32, i32], i32),
+            "hg_init_model": ([vp, i32, i32, u64], vp),
+            "hg_init_learnable": ([vp, u64], vp),
+            "hg_engine_load_weights": ([vp, i32, i32, vp, i32, i32], i32),
+            "hg_engine_load_table_rows": ([vp, i32, vp, C.c_int64, vp, i32], i32),
+            "hg_sample_neighbors": ([vp, u64, vp, C.c_uint32, i32, u64, i32, i32, vp, vp, i32], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)

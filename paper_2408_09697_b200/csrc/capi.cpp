@@ -476,8 +476,11 @@ int hg_engine_bench(hg_engine* e, const uint32_t* batches, const int* lens, cons
     StepScalars* d_sc = nullptr;
     HG_CUDA(cudaMalloc(&d_all, std::max<std::size_t>(4, total * 4)));
     HG_CUDA(cudaMalloc(&d_sc, sizeof(StepScalars) * std::max(1, n_steps)));
-    HG_CUDA(cudaMemcpy(d_all, batches, total * 4, cudaMemcpyHostToDevice));
-    HG_CUDA(cudaMemcpy(d_sc, sc.data(), sizeof(StepScalars) * n_steps, cudaMemcpyHostToDevice));
+    // on the engine's (non-blocking) stream and complete before the timed region: a
+    // pageable legacy-stream copy may return before its DMA has landed
+    HG_CUDA(cudaMemcpyAsync(d_all, batches, total * 4, cudaMemcpyHostToDevice, en.stream()));
+    HG_CUDA(cudaMemcpyAsync(d_sc, sc.data(), sizeof(StepScalars) * n_steps, cudaMemcpyHostToDevice, en.stream()));
+    HG_CUDA(cudaStreamSynchronize(en.stream()));
     cudaEvent_t a, b;
     HG_CUDA(cudaEventCreate(&a));
     HG_CUDA(cudaEventCreate(&b));
@@ -854,7 +857,9 @@ void* hg_ctx_malloc(hg_ctx* c, size_t bytes) {
     HG_CUDA(cudaSetDevice(c->c->device()));
     void* p = nullptr;
     HG_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
-    HG_CUDA(cudaMemset(p, 0, std::max<size_t>(bytes, 16)));
+    // zero-fill on the context's (non-blocking) stream: ordered before every later
+    // primitive and copy on it (a legacy-stream memset would race with them)
+    HG_CUDA(cudaMemsetAsync(p, 0, std::max<size_t>(bytes, 16), c->c->stream()));
     return p;
   });
 }

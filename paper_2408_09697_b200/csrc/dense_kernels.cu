@@ -131,21 +131,119 @@ __global__ void k_csc_fill(CscHop h) {
   }
 }
 
-// make every segment ascending in (block, row): deterministic summation order
-__global__ void k_csc_sort(CscHop h) {
+// make every segment ascending in (block, row): deterministic summation order.
+// A lane owns a segment; short ones (<= kShortSeg) it insertion-sorts alone, longer
+// ones (hub sources of power-law graphs) the whole warp sorts together: a bitonic
+// network in shared memory up to kWarpSort entries, beyond that sorted runs of
+// kWarpSort merged pairwise through the type's scratch array (O(n log^2 n) instead of
+// the O(n^2) of one insertion sort).
+constexpr std::uint32_t kShortSeg = 32;
+constexpr int kWarpSort = 1024;
+constexpr int kSortThreads = 256;
+
+__device__ void warp_bitonic(std::uint32_t* a, int n, int lane) {
+  int P = 1;
+  while (P < n) P <<= 1;
+  for (int i = n + lane; i < P; i += 32) a[i] = 0xFFFFFFFFu;
+  __syncwarp();
+  for (int k = 2; k <= P; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = lane; i < P; i += 32) {
+        const int l = i ^ j;
+        if (l > i) {
+          const std::uint32_t x = a[i], y = a[l];
+          if ((x > y) == ((i & k) == 0)) {
+            a[i] = y;
+            a[l] = x;
+          }
+        }
+      }
+      __syncwarp();
+    }
+}
+
+// the warp sorts seg[0, n) in place (tmp: n words of scratch)
+__device__ void warp_sort_segment(std::uint32_t* seg, std::uint32_t* tmp, std::uint32_t n, std::uint32_t* sm, int lane) {
+  for (std::uint32_t r0 = 0; r0 < n; r0 += kWarpSort) {  // sorted runs
+    const int m = static_cast<int>(min(static_cast<std::uint32_t>(kWarpSort), n - r0));
+    for (int i = lane; i < m; i += 32) sm[i] = seg[r0 + i];
+    __syncwarp();
+    warp_bitonic(sm, m, lane);
+    for (int i = lane; i < m; i += 32) seg[r0 + i] = sm[i];
+    __syncwarp();
+  }
+  std::uint32_t* src = seg;
+  std::uint32_t* dst = tmp;
+  for (std::uint32_t w = kWarpSort; w < n; w <<= 1) {  // pairwise merges by rank
+    for (std::uint32_t i = lane; i < n; i += 32) {
+      const std::uint32_t a0 = (i / (2 * w)) * (2 * w), b0 = min(a0 + w, n), b1 = min(a0 + 2 * w, n);
+      const std::uint32_t x = src[i];
+      std::uint32_t lo, hi, pos;
+      if (i < b0) {  // rank in the right run: elements < x
+        lo = b0;
+        hi = b1;
+        while (lo < hi) {
+          const std::uint32_t mid = (lo + hi) >> 1;
+          if (src[mid] < x) lo = mid + 1; else hi = mid;
+        }
+        pos = a0 + (i - a0) + (lo - b0);
+      } else {  // rank in the left run: elements <= x
+        lo = a0;
+        hi = b0;
+        while (lo < hi) {
+          const std::uint32_t mid = (lo + hi) >> 1;
+          if (src[mid] <= x) lo = mid + 1; else hi = mid;
+        }
+        pos = a0 + (i - b0) + (lo - a0);
+      }
+      dst[pos] = x;
+    }
+    __syncwarp();
+    std::uint32_t* t = src;
+    src = dst;
+    dst = t;
+  }
+  if (src != seg) {
+    for (std::uint32_t i = lane; i < n; i += 32) seg[i] = src[i];
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_csc_sort(CscHop h) {
   pdl_enter();
+  __shared__ std::uint32_t sm[kSortThreads / 32][kWarpSort];
   const CscType& t = h.t[blockIdx.y];
   const int n = *t.n_src;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
-    const std::uint32_t lo = c ? t.offs[c - 1] : 0u, hi = t.offs[c];
-    for (std::uint32_t x = lo + 1; x < hi; ++x) {
-      const std::uint32_t v = t.entries[x];
-      std::uint32_t y = x;
-      while (y > lo && t.entries[y - 1] > v) {
-        t.entries[y] = t.entries[y - 1];
-        --y;
+  const int lane = threadIdx.x & 31;
+  std::uint32_t* wsm = sm[threadIdx.x >> 5];
+  const int stride = gridDim.x * blockDim.x;
+  // whole warps iterate together (the long segments need every lane)
+  for (int base = blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n; base += stride) {
+    const int c = base + lane;
+    std::uint32_t lo = 0, hi = 0;
+    if (c < n) {
+      lo = c ? t.offs[c - 1] : 0u;
+      hi = t.offs[c];
+    }
+    const bool is_long = hi - lo > kShortSeg;
+    if (!is_long) {
+      for (std::uint32_t x = lo + 1; x < hi; ++x) {
+        const std::uint32_t v = t.entries[x];
+        std::uint32_t y = x;
+        while (y > lo && t.entries[y - 1] > v) {
+          t.entries[y] = t.entries[y - 1];
+          --y;
+        }
+        t.entries[y] = v;
       }
-      t.entries[y] = v;
+    }
+    unsigned todo = __ballot_sync(0xffffffffu, is_long);
+    while (todo) {
+      const int src_lane = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const std::uint32_t slo = __shfl_sync(0xffffffffu, lo, src_lane);
+      const std::uint32_t shi = __shfl_sync(0xffffffffu, hi, src_lane);
+      warp_sort_segment(t.entries + slo, t.tmp + slo, shi - slo, wsm, lane);
     }
   }
 }

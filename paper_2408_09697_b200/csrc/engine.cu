@@ -658,7 +658,10 @@ void Engine::upload(const Graph& g) {
   for (auto& c : cscs_) {
     std::size_t ent = 0;
     for (int bi : c.blocks) ent = std::max<std::size_t>(ent, blocks_[bi].edge_base + blocks_[bi].edge_cap);
-    for (int sl = 0; sl < 2; ++sl) c.s_entries[sl] = static_cast<std::uint32_t*>(alloc(ent * 4));
+    for (int sl = 0; sl < 2; ++sl) {
+      c.s_entries[sl] = static_cast<std::uint32_t*>(alloc(ent * 4));
+      c.s_tmp[sl] = static_cast<std::uint32_t*>(alloc(ent * 4));
+    }
     if (!(c.hop == o_.k && xchg_type(c.src_t)))
       c.dh = static_cast<float*>(alloc(static_cast<std::size_t>(std::max(1, c.src_cap)) * c.ld * 4));
     if (c.hop < o_.k) {
@@ -750,6 +753,7 @@ void Engine::bind_slot(int s) {
     c.offs = c.s_offs[s];
     c.cursor = c.s_cursor[s];
     c.entries = c.s_entries[s];
+    c.tmp = c.s_tmp[s];
   }
   csc_region_ = csc_region_slot_[s];
   d_sc_ = d_sc_slot_[s];
@@ -1270,6 +1274,7 @@ CscHop Engine::csc_hop(int h) {
     t.offs = c.offs;
     t.cursor = c.cursor;
     t.entries = c.entries;
+    t.tmp = c.tmp;
     t.n_src = front(h, c.src_t).count;
     t.src_cap = c.src_cap;
     // replicas merge their learnable-row gradients before Adam: keep the rows
@@ -1710,8 +1715,10 @@ void Engine::set_cache(const std::vector<std::vector<NodeId>>& cached) {
   std::vector<std::uint32_t> bits(static_cast<std::size_t>(total_words_), 0u);
   for (int t = 0; t < ntypes_ && t < static_cast<int>(cached.size()); ++t)
     for (NodeId v : cached[t]) bits[word_base_[t] + (v >> 5)] |= 1u << (v & 31);
-  HG_CUDA(cudaMemcpy(cached_bits_, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice));
-  HG_CUDA(cudaMemset(cache_hm_, 0, sizeof(unsigned long long) * 2 * ntypes_));
+  quiesce();  // the engine's streams are non-blocking: order the update after all work in flight
+  HG_CUDA(cudaMemcpyAsync(cached_bits_, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice, st_));
+  HG_CUDA(cudaMemsetAsync(cache_hm_, 0, sizeof(unsigned long long) * 2 * ntypes_, st_));
+  HG_CUDA(cudaStreamSynchronize(st_));
   cache_on_ = true;
   for (int t = 0; t < ntypes_; ++t) cache_types_[t] = t < static_cast<int>(cached.size());
   drop_graphs();  // the captured steps did not look the frontier up

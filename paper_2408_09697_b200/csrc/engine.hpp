@@ -241,6 +241,7 @@ class Engine {
     std::vector<int> blocks;
     std::uint32_t *offs = nullptr, *cursor = nullptr, *entries = nullptr;  // bound sample slot
     std::uint32_t *s_offs[2] = {}, *s_cursor[2] = {}, *s_entries[2] = {};
+    std::uint32_t *tmp = nullptr, *s_tmp[2] = {};  // scratch of the long-segment sort
     float* dh = nullptr;  // gradient of H[hop][src_t] (or learnable rows)
   };
   struct TypeTable {

@@ -187,6 +187,7 @@ struct CscType {
   // (dpre = dH * [H > 0], hgnn.cpp:326-328), so the backward contractions read it plain
   const float* relu_h;
   int ld_h;
+  std::uint32_t* tmp;  // entries-sized scratch: merges of long (hub) segments
 };
 struct CscEdges {
   const std::uint32_t* col;

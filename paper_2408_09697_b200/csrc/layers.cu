@@ -183,8 +183,8 @@ LayerCtx::LayerCtx(int device) : device_(device) {
   HG_CUDA(cudaMalloc(&ints_, kIntSlots * sizeof(int)));
   HG_CUDA(cudaMallocHost(&ints_h_, kIntSlots * sizeof(int)));
   HG_CUDA(cudaMalloc(&done_, sizeof(unsigned)));
-  HG_CUDA(cudaMemset(done_, 0, sizeof(unsigned)));
-  reset_err();
+  HG_CUDA(cudaMemsetAsync(done_, 0, sizeof(unsigned), st_));
+  reset_err();  // also synchronises the stream
 }
 
 LayerCtx::~LayerCtx() {
@@ -478,6 +478,7 @@ void LayerCtx::scatter_rows(const std::uint32_t* indptr, std::int64_t n_dst, std
   t.offs = offs;
   t.cursor = cursor;
   t.entries = entries;
+  t.tmp = static_cast<std::uint32_t*>(scratch(static_cast<std::size_t>(n_edges) * 4));
   t.n_src = dev_int(n_src);
   t.src_cap = static_cast<int>(n_src);
   t.dh = sum;

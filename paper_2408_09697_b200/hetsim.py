@@ -204,6 +204,16 @@ def meta_partition(g: HetGraph, k: int, p: int) -> Dict[str, np.ndarray]:
     return N.take(N.lib().hg_meta_partition(g.handle, k, p))
 
 
+def init_model(g: HetGraph, k: int, hidden: int, seed: int) -> Dict[str, np.ndarray]:
+    """init_model (src/hgnn.cpp:39-62) on the BFS metatree of depth k: w.r{r}.l{l} f64."""
+    return N.take(N.lib().hg_init_model(g.handle, k, hidden, seed))
+
+
+def init_learnable(g: HetGraph, seed: int) -> Dict[str, np.ndarray]:
+    """init_learnable (src/hgnn.cpp:64-81): learn.t{t} f64 [count x dim]."""
+    return N.take(N.lib().hg_init_learnable(g.handle, seed))
+
+
 def make_batches(g: HetGraph, batch_size: int, max_batches: int, seed: int) -> List[np.ndarray]:
     """make_batches (src/harness.cpp:327-340)."""
     b = N.take(N.lib().hg_make_batches(g.handle, batch_size, max_batches, seed))

@@ -196,3 +196,20 @@ def test_cache_plan_matches_reference(H, ref):
             assert np.array_equal(got[key], want[key]), key
         for t in range(4):
             assert np.array_equal(got[f"cached.t{t}"], want[f"cached.t{t}"]), (budget, t)
+
+
+@pytest.mark.parametrize("name", ["mag-mini", "donor-mini"])
+def test_init_model_and_learnable_match_reference(H, ref, name):
+    # hg_init_model / hg_init_learnable (the caller-owned model state of the drop-in
+    # layer interface) are the reference's init_model / init_learnable bit for bit
+    rg = ref.RefGraph.bundled(name, 5)
+    g = H.gen_synthetic(H.bundled_spec(name), 5)
+    want = rg.flat_step(2, 16, 77, 88, [0, 1, 2], [3, 3], 1)
+    model = H.init_model(g, 2, 16, 77)
+    learn = H.init_learnable(g, 88)
+    slots = [n for n in want if n.startswith("init.r")]
+    assert slots and len(slots) == len([n for n in model if n.startswith("w.")])
+    for n in slots:
+        assert np.array_equal(model["w." + n[len("init."):]], want[n]), n
+    for n in [x for x in want if x.startswith("init.learn.t")]:
+        assert np.array_equal(learn["learn.t" + n.split(".t")[-1]], want[n]), n
