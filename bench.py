@@ -352,10 +352,12 @@ def run_b200(args):
     launches_by = {k.split(".")[1]: int(v[0]) for k, v in prof.items() if k.endswith(".launches")}
     alg = prof["alg_bytes"]
     # HBM-bound kernel classes with algorithmic bytes: the layer-1
-    # gather-mean (`aggregate`) and the backward gather + fused sparse Adam
-    # (`csc_gather`). The sampler is latency-bound (serial mt19937_64 per row) and
-    # is reported beside them, not as the roofline kernel.
-    alg_by = {"aggregate": alg[1], "csc_gather": alg[3], "aggregate_top": alg[2], "sample": alg[0]}
+    # gather-mean (`aggregate`) and the layer-1 backward gather + fused sparse Adam
+    # (`csc_gather`); the top layer's launches of the same kernels (hop-1 blocks:
+    # 1024 destination rows, latency-bound) are the `*_top` classes. The sampler is
+    # latency-bound (serial mt19937_64 per row) and is reported beside them.
+    alg_by = {"aggregate": alg[1], "csc_gather": alg[3], "aggregate_top": alg[2], "csc_gather_top": alg[4],
+              "sample": alg[0]}
 
     lib_sha = lib_digest()
     traffic_rec = load_traffic()

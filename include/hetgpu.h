@@ -172,7 +172,8 @@ int hg_engine_bench(hg_engine* e, const uint32_t* batches, const int* lens, cons
                     int n_steps, int train, double* out_ms, uint64_t* out_edges, double* out_loss);
 void hg_engine_profile(hg_engine* e, int on);
 /* per kernel class: kernel.<name>.ms / .launches; alg_bytes = cumulative algorithmic
- * bytes [sample, aggregate, aggregate_top, csc_gather] since profiling was switched on */
+ * bytes [sample, aggregate, aggregate_top, csc_gather, csc_gather_top] since profiling
+ * was switched on (the *_top classes are the top layer's launches: hop-1 blocks) */
 hg_bundle* hg_engine_profile_read(hg_engine* e);
 int hg_engine_info(hg_engine* e, uint64_t* param_count, uint64_t* device_bytes, int* model_step);
 /* options: "retain_grads" (keep learnable-row gradients readable as grad.f.*; default 1),

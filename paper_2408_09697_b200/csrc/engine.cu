@@ -104,13 +104,14 @@ struct AlgBytesArgs {
   const int* c_rows[kMaxBlocks * 4];
   int c_din[kMaxBlocks * 4];
   int c_row_bytes_mult[kMaxBlocks * 4];  // 1: dH write; 6: fused Adam (w, m, v read + write); 7: both
+  int c_top[kMaxBlocks * 4];             // the transposed view of hop 1 (the top layer's gather)
   int ncsc;
 };
 
 __global__ void k_alg_bytes(AlgBytesArgs a, double* acc) {
   pdl_enter();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double s = 0, agg[3] = {0, 0, 0}, csc = 0;
+  double s = 0, agg[3] = {0, 0, 0}, csc = 0, csc_top = 0;
   for (int i = 0; i < a.nblk; ++i) {
     const double R = *a.n_rows[i], E = a.indptr[i][*a.n_rows[i]];
     // sampling: indptr pair + dst id read, neighbour reads, src write, offset write
@@ -118,17 +119,18 @@ __global__ void k_alg_bytes(AlgBytesArgs a, double* acc) {
     // aggregation: per edge one source row + its id; offsets; tape write
     agg[a.cls[i]] += E * (4.0 * a.din[i] + 4.0) + 4.0 * (R + 1) + 4.0 * R * a.din[i];
     // backward gather: per edge one dmean row + the edge id
-    if (a.grad[i]) csc += E * (4.0 * a.din[i] + 4.0);
+    if (a.grad[i]) (a.cls[i] == 2 ? csc_top : csc) += E * (4.0 * a.din[i] + 4.0);
   }
   // per source row: segment offsets + the gradient row (or the fused Adam row update)
   for (int i = 0; i < a.ncsc; ++i) {
     const double n = *a.c_rows[i];
-    csc += 4.0 * (n + 1) + n * 4.0 * a.c_din[i] * a.c_row_bytes_mult[i];
+    (a.c_top[i] ? csc_top : csc) += 4.0 * (n + 1) + n * 4.0 * a.c_din[i] * a.c_row_bytes_mult[i];
   }
   acc[0] += s;
   acc[1] += agg[1];
   acc[2] += agg[2];
   acc[3] += csc;
+  acc[4] += csc_top;
 }
 
 template <typename T>
@@ -318,11 +320,19 @@ void Engine::build_plan(const Graph& g) {
 
   // max in-degree per relation tightens the edge capacities
   maxdeg_.assign(g.num_rels(), 0);
+  rng_frac_.assign(k, std::vector<float>(g.num_rels(), 0.f));
   for (int r = 0; r < g.num_rels(); ++r) {
     const auto& off = g.rels[r].adj.offsets;
     std::uint64_t m = 0;
-    for (std::size_t i = 0; i + 1 < off.size(); ++i) m = std::max(m, off[i + 1] - off[i]);
+    std::vector<std::uint64_t> above(k, 0);  // destinations drawn with the RNG at each hop's fanout
+    for (std::size_t i = 0; i + 1 < off.size(); ++i) {
+      const std::uint64_t d = off[i + 1] - off[i];
+      m = std::max(m, d);
+      for (int h = 0; h < k; ++h) above[h] += d > static_cast<std::uint64_t>(o_.fanouts[h]) ? 1 : 0;
+    }
     maxdeg_[r] = m;
+    for (int h = 0; h < k; ++h)
+      rng_frac_[h][r] = off.size() > 1 ? static_cast<float>(above[h]) / static_cast<float>(off.size() - 1) : 0.f;
   }
 
   // frontier capacities and blocks, hop by hop
@@ -689,7 +699,7 @@ void Engine::upload(const Graph& g) {
   row_loss_ = static_cast<double*>(alloc(static_cast<std::size_t>(o_.batch_cap) * 8));
   loss_done_ = static_cast<unsigned*>(alloc(sizeof(unsigned)));
   cache_hm_ = static_cast<unsigned long long*>(alloc(sizeof(unsigned long long) * 2 * ntypes_));
-  alg_bytes_ = static_cast<double*>(alloc(sizeof(double) * 4));
+  alg_bytes_ = static_cast<double*>(alloc(sizeof(double) * 5));
   cache_types_.assign(ntypes_, false);
 
   int max_cap = std::max(total_words_, max_rows);
@@ -847,6 +857,7 @@ void Engine::run_sampling(cudaStream_t ss) {
       s.mark_bits = nullptr;
       s.rel = b.rel;
       s.rows_cap = b.rows_cap;
+      s.rng_frac = rng_frac_[h - 1][b.rel];
     }
 
     // frontier[h][t]: bitmap of every sampled source, compacted in id order
@@ -929,6 +940,7 @@ void Engine::run_sampling(cudaStream_t ss) {
       ab.c_rows[ab.ncsc] = front(c.hop, c.src_t).count;
       ab.c_din[ab.ncsc] = c.din;
       ab.c_row_bytes_mult[ab.ncsc] = fused_adam ? (retain_grads_ ? 7 : 6) : 1;
+      ab.c_top[ab.ncsc] = c.hop == 1 ? 1 : 0;
       ++ab.ncsc;
     }
     launch_pdl(k_alg_bytes, 1, 32, 0, ss, ab, alg_bytes_);
@@ -1117,7 +1129,7 @@ void Engine::run_backward() {
     // layer-0 rows get their Adam update in the same pass)
     const CscHop ch = csc_hop(d);
     AdamHyper hp;
-    timed("csc_gather", 0, [&] { csc_gather(ch, hp, err_, st_); });
+    timed(d == 1 ? "csc_gather_top" : "csc_gather", 0, [&] { csc_gather(ch, hp, err_, st_); });
   }
   join();  // weight gradients
   if (replica_group_.size() > 1) run_replica_merge();
@@ -1591,9 +1603,9 @@ int Engine::count_launches(int n, bool train) {
 }
 
 std::vector<double> Engine::algorithmic_bytes() {
-  std::vector<double> v(4, 0.0);
+  std::vector<double> v(5, 0.0);
   HG_CUDA(cudaStreamSynchronize(st_));
-  HG_CUDA(cudaMemcpy(v.data(), alg_bytes_, sizeof(double) * 4, cudaMemcpyDeviceToHost));
+  HG_CUDA(cudaMemcpy(v.data(), alg_bytes_, sizeof(double) * 5, cudaMemcpyDeviceToHost));
   return v;
 }
 

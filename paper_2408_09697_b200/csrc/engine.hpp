@@ -188,7 +188,7 @@ class Engine {
     kernel_ms_.clear();
     kernel_bytes_.clear();
     kernel_launches_.clear();
-    if (alg_bytes_) cudaMemsetAsync(alg_bytes_, 0, sizeof(double) * 4, st_);
+    if (alg_bytes_) cudaMemsetAsync(alg_bytes_, 0, sizeof(double) * 5, st_);
   }
   // kernel launches of one step, counted from a captured (not executed) step
   int count_launches(int n, bool train);
@@ -305,6 +305,7 @@ class Engine {
   std::vector<std::uint64_t*> csr_ptr_;
   std::vector<std::uint32_t*> csr_src_;
   std::vector<std::uint64_t> maxdeg_;
+  std::vector<std::vector<float>> rng_frac_;  // [hop-1][rel]: share of destinations drawn with the RNG
   std::vector<TypeTable> tables_;
   std::int32_t* labels_ = nullptr;
   std::vector<NodeId> bad_labels_;  // target ids with labels outside [0, C), sorted

@@ -3,6 +3,8 @@
 // replaces the reference's per-hop sort+unique (sampling.cpp:82-89) and its
 // per-edge binary searches (hgnn.cpp:166-171). All HBM-bound; grids are sized
 // in multiples of the SM count or from capacities and read live counts.
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace hetgpu {
@@ -110,6 +112,7 @@ __device__ __forceinline__ int seg_of(const int* base, int nseg, int ticket) {
 struct LbLayout {
   int base[kMaxSegs + 1];  // per segment: first ticket / first state slot
   int nseg;
+  int item[kMaxSegs];      // sampler: the block each segment (in ticket order) stands for
 };
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_lb(ScanArgs a, LbLayout L, unsigned long long* state,
@@ -273,8 +276,9 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_fused(SampleHop h, Lb
   __syncthreads();
   const int tk = s_tile;
   if (tk >= L.base[L.nseg]) return;
-  const int bi = seg_of(L.base, L.nseg, tk);
-  const int t = tk - L.base[bi];
+  const int sg = seg_of(L.base, L.nseg, tk);
+  const int t = tk - L.base[sg];
+  const int bi = L.item[sg];
   const SampleBlock& b = h.b[bi];
   const int n = *b.n_rows;
   const int base = t * kSampleThreads;
@@ -295,7 +299,7 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample_fused(SampleHop h, Lb
   std::uint32_t tot;
   const std::uint32_t incl = block_incl_scan<kSampleThreads>(cnt, &tot);
   if (threadIdx.x < 32) {
-    const std::uint32_t p = lb_prefix(state + L.base[bi], t, tot);
+    const std::uint32_t p = lb_prefix(state + L.base[sg], t, tot);
     if (threadIdx.x == 0) s_prefix = p;
   }
   __syncthreads();
@@ -463,10 +467,16 @@ void sample_hop(const SampleHop& h, const StepScalars* sc, std::uint32_t* slow, 
   if (h.nblk == 0) return;
   LbLayout L{};
   L.nseg = h.nblk;
+  // tickets go out in launch order: the blocks with the most RNG rows (the 156-step
+  // seeding chains, the long pole of the hop) take the first tiles, so their chains
+  // overlap the copy-all blocks instead of forming the kernel's tail
+  for (int i = 0; i < h.nblk; ++i) L.item[i] = i;
+  std::stable_sort(L.item, L.item + h.nblk,
+                   [&](int a, int b) { return h.b[a].rng_frac * h.b[a].rows_cap > h.b[b].rng_frac * h.b[b].rows_cap; });
   int tiles = 0;
   for (int i = 0; i < h.nblk; ++i) {
     L.base[i] = tiles;
-    tiles += static_cast<int>(ceil_div(std::max(1, h.b[i].rows_cap), kSampleThreads));
+    tiles += static_cast<int>(ceil_div(std::max(1, h.b[L.item[i]].rows_cap), kSampleThreads));
   }
   L.base[h.nblk] = tiles;
   lb.reset(tiles, st);

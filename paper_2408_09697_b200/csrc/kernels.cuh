@@ -74,6 +74,7 @@ struct SampleBlock {
   std::uint32_t* mark_bits;       // frontier[h][src type] bitmap (marked as sampled), or null
   int rel;
   int rows_cap;
+  float rng_frac;  // expected share of RNG rows: blocks with more get the earliest tiles
 };
 struct SampleHop {
   SampleBlock b[kMaxBlocks];

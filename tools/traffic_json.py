@@ -4,9 +4,9 @@ on (bench.py reads it as roofline.traffic and checks the stamp).
 
     python tools/traffic_json.py gpurun_out/prof_step.ncu-rep "<ncu command>" > profiles/r02_traffic.json
 
-Classes follow bench.py's profile classes: the first k_gather_mean launch of a step
-is the layer-1 aggregation ("aggregate"), the second the top layer
-("aggregate_top"); k_csc_gather launches are averaged ("csc_gather"); the sampler
+Classes follow bench.py's profile classes: k_gather_mean / k_csc_gather launches of
+the layer-1 blocks ("aggregate" / "csc_gather") and of the top layer's hop-1 blocks
+("aggregate_top" / "csc_gather_top", the lighter launch of each pair); the sampler
 ("sample"); every k_umma instantiation is its own class (tensor pipe % reported).
 """
 from __future__ import annotations
@@ -83,19 +83,25 @@ def short(name):
 def main():
     path, cmd = sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else ""
     acc = collections.defaultdict(list)
-    gather_seen = 0
+    split = collections.defaultdict(list)
     for d in rows_of(path):
         nm = short(d.get("Kernel Name", "?"))
         if nm.startswith("k_gather_mean"):
-            cls = "aggregate" if gather_seen % 2 == 0 else "aggregate_top"
-            gather_seen += 1
+            split[("aggregate", "aggregate_top")].append(d)
         elif nm.startswith("k_csc_gather"):
-            cls = "csc_gather"
+            split[("csc_gather", "csc_gather_top")].append(d)
         elif nm.startswith("k_sample_fused"):
-            cls = "sample"
+            acc["sample"].append(d)
         else:
-            cls = nm
-        acc[cls].append(d)
+            acc[nm].append(d)
+    # each of these kernels runs once per layer: the top layer's launch (hop-1 blocks,
+    # 1024 destination rows) moves far fewer bytes than the layer-1 launch
+    for (big, small), ds in split.items():
+        vol = sorted(num(d, "dram__bytes_read.sum") + num(d, "dram__bytes_write.sum") for d in ds)
+        cut = (vol[0] + vol[-1]) / 2
+        for d in ds:
+            v = num(d, "dram__bytes_read.sum") + num(d, "dram__bytes_write.sum")
+            acc[big if v > cut else small].append(d)
     out = {}
     for cls, ds in acc.items():
         rd = sum(num(d, "dram__bytes_read.sum") for d in ds) / len(ds)
