@@ -118,6 +118,11 @@ typedef struct {
   uint64_t model_seed; /* init_model seed (src/hgnn.cpp:39) */
   uint64_t learn_seed; /* init_learnable seed (src/hgnn.cpp:64) */
   int device;
+  /* storage of the dense layer-0 feature tables: 0 f32 (parity), 1 f16, 2 bf16 */
+  int feat_dtype;
+  /* 1: dense feature tables stay in pinned host memory (read over PCIe, zero-copy);
+   * hg_engine_set_cache installs an HBM copy of the cached rows (cache.cpp:121-141) */
+  int feat_host;
 } hg_engine_opts;
 
 typedef struct {

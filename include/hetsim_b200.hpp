@@ -643,11 +643,13 @@ struct ExecutionReport {
 class RafEngine {
  public:
   // init_model / init_learnable seeds as run_experiment derives them (harness.cpp:365-366)
+  // feat_dtype: storage of the dense feature tables (0 f32, 1 f16, 2 bf16); feat_host: keep
+  // them in pinned host memory with an HBM cache of the set_cache rows
   RafEngine(const HetGraph& g, std::vector<int> fanouts, int hidden, std::uint64_t seed, int batch_cap = 1024,
-            int p = 1, int rank = 0, int device = 0)
+            int p = 1, int rank = 0, int device = 0, int feat_dtype = 0, bool feat_host = false)
       : g_(g), fanouts_(std::move(fanouts)) {
     const hg_engine_opts o{static_cast<int>(fanouts_.size()), fanouts_.data(), hidden, batch_cap, p, rank,
-                           mix_seed(seed, 0xd0de1), mix_seed(seed, 0x1ea4a), device};
+                           mix_seed(seed, 0xd0de1), mix_seed(seed, 0x1ea4a), device, feat_dtype, feat_host ? 1 : 0};
     e_.reset(detail::check(hg_engine_create(g.handle(), &o)));
   }
   // run_raf_batch (raf.cpp:344-530) + adam_update_model + adam_update_rows, as the
@@ -1313,7 +1315,7 @@ inline hg_engine* state_engine(const HetGraph& g, const std::vector<int>& fanout
   const EngineKey key{g.handle(), fanouts, hidden, c, layer_device()};
   auto it = cache.find(key);
   if (it == cache.end()) {
-    const hg_engine_opts o{static_cast<int>(fanouts.size()), fanouts.data(), hidden, c, 1, 0, 0, 0, layer_device()};
+    const hg_engine_opts o{static_cast<int>(fanouts.size()), fanouts.data(), hidden, c, 1, 0, 0, 0, layer_device(), 0, 0};
     hg_engine* e = check(hg_engine_create(g.handle(), &o));
     check(hg_engine_set_option(e, "apply_adam", 0));
     check(hg_engine_set_option(e, "retain_grads", 1));

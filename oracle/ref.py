@@ -54,6 +54,7 @@ def lib():
             "ref_graph_save": [vp, C.c_char_p],
             "ref_graph_build": [i32, vp, i32, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, vp],
             "ref_graph_export": [vp],
+            "ref_graph_round_features": [vp, i32],
             "ref_meta_partition": [vp, i32, i32],
             "ref_sample_neighbors": [vp, i32, vp, C.c_uint, i32, u64, i32, i32],
             "ref_sample_khop": [vp, vp, i32, vp, i32, u64, vp, vp],
@@ -155,6 +156,10 @@ class RefGraph:
 
     def export(self) -> Dict[str, np.ndarray]:
         return _take(lib().ref_graph_export(self.h))
+
+    def round_features(self, dtype: str) -> None:
+        """Dense features rounded in place to fp16 ("f16") or bf16 ("bf16") values."""
+        _take(lib().ref_graph_round_features(self.h, {"f16": 1, "bf16": 2}[dtype]))
 
     def meta_partition(self, k: int, p: int) -> Dict[str, np.ndarray]:
         return _take(lib().ref_meta_partition(self.h, k, p))

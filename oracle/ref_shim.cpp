@@ -16,6 +16,7 @@
 //   gen_synthetic / bundled_spec / run_experiment / stats_hash  src/harness.cpp:74,192,342,548
 //   random_hetgraph (the reference's own test fixture)          tests/test_util.hpp:17
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <cstring>
 #include <map>
@@ -249,6 +250,43 @@ void* ref_graph_build(int num_types, const unsigned long long* counts, int num_r
 }
 
 void ref_graph_free(void* sp) { delete static_cast<Session*>(sp); }
+
+// Rounds every dense feature value to the nearest fp16 (mode 1) or bf16 (mode 2)
+// value, in place: the "parity mode" inputs of SURVEY §7 (fp16-representable features
+// travel losslessly through a half-precision device table).
+void* ref_graph_round_features(void* sp, int mode) {
+  return guarded([&]() -> void* {
+    HetGraph& g = static_cast<Session*>(sp)->g;
+    auto round_f16 = [](double x) {
+      // IEEE binary16, round to nearest even, via its 11-bit significand (normals;
+      // |x| <= 1 here so no overflow; subnormals below 2^-14 use the fixed 2^-24 step)
+      const double a = std::fabs(x);
+      if (a == 0.0) return x;
+      int e;
+      std::frexp(a, &e);                       // a = m * 2^e, m in [0.5, 1)
+      const int q = std::max(e - 11, -24);     // ulp exponent
+      const double ulp = std::ldexp(1.0, q);
+      const double r = std::nearbyint(a / ulp) * ulp;  // default rounding mode: to nearest even
+      return x < 0 ? -r : r;
+    };
+    auto round_bf16 = [](double x) {
+      float f = static_cast<float>(x);  // the engine rounds the f32 table value
+      std::uint32_t u;
+      std::memcpy(&u, &f, 4);
+      u = (u + 0x7FFFu + ((u >> 16) & 1u)) & 0xFFFF0000u;
+      std::memcpy(&f, &u, 4);
+      return static_cast<double>(f);
+    };
+    for (auto& f : g.features) {
+      if (f.kind != StorageKind::Dense) continue;
+      for (double& x : f.values.data) {
+        const double xf = static_cast<double>(static_cast<float>(x));  // the engine's f32 source value
+        x = mode == 1 ? round_f16(xf) : round_bf16(xf);
+      }
+    }
+    return new Bundle;
+  });
+}
 
 void* ref_graph_export(void* sp) {
   return guarded([&]() -> void* {

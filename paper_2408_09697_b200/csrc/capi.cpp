@@ -343,6 +343,8 @@ hg_engine* hg_engine_create(const hg_graph* g, const hg_engine_opts* o) {
     eo.model_seed = o->model_seed;
     eo.learn_seed = o->learn_seed;
     eo.device = o->device;
+    eo.feat_dtype = o->feat_dtype;
+    eo.feat_host = o->feat_host;
     auto* h = new hg_engine;
     h->e = std::make_unique<Engine>(g->g, eo);
     return h;

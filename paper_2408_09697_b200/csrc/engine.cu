@@ -1,4 +1,7 @@
 // Device engine: static plan, workspace, and the per-step launch sequence.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
 #include "engine.hpp"
 #include "gemm.cuh"
 
@@ -80,12 +83,18 @@ __global__ void k_feat_sync(FeatSyncArgs a, std::uint64_t* out) {
 }
 
 __global__ void k_gather_rows(const float* table, int ld, const std::uint32_t* ids, const int* n, int cols,
-                              float* out) {
+                              float* out, int dtype) {
   pdl_enter();
   const int total = *n * cols;
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
     const int i = x / cols, c = x % cols;
-    out[x] = table[static_cast<std::size_t>(ids[i]) * ld + c];
+    const std::size_t at = static_cast<std::size_t>(ids[i]) * ld + c;
+    if (dtype == kF32)
+      out[x] = table[at];
+    else if (dtype == kF16)
+      out[x] = __half2float(reinterpret_cast<const __half*>(table)[at]);
+    else
+      out[x] = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(table)[at]);
   }
 }
 
@@ -184,6 +193,8 @@ Engine::~Engine() {
   cudaStreamSynchronize(st2_);
   for (auto e : fork_ev_) cudaEventDestroy(e);
   for (void* p : allocs_) cudaFree(p);
+  for (auto& tb : tables_)
+    if (tb.host_mem) cudaFreeHost(tb.host_mem);
   for (int sl = 0; sl < 2; ++sl) {
     if (h_sc_slot_[sl]) cudaFreeHost(h_sc_slot_[sl]);
     if (h_batch_slot_[sl]) cudaFreeHost(h_batch_slot_[sl]);
@@ -478,12 +489,12 @@ void Engine::upload(const Graph& g) {
     tb.ld = round_up4(std::max(1, nt.dim));
     const std::size_t rows = nt.count;
     if (nt.storage == Storage::Absent) throw std::runtime_error("missing features for node type " + nt.name);
-    std::vector<float> host(rows * tb.ld, 0.0f);
     if (nt.storage == Storage::Dense) {
-      tb.dense = true;
-      for (std::size_t i = 0; i < rows; ++i)
-        std::memcpy(&host[i * tb.ld], &nt.dense[i * nt.dim], sizeof(float) * nt.dim);
-    } else {
+      upload_dense(nt, tb);
+      continue;
+    }
+    std::vector<float> host(rows * tb.ld, 0.0f);
+    {
       tb.learnable = true;
       const auto& w = learn.at(t);
       for (std::size_t i = 0; i < rows; ++i)
@@ -970,8 +981,12 @@ void Engine::run_forward() {
       m.indptr = b.indptr;
       if (b.hop == k) {
         m.keys = b.src;
-        m.h = tables_[b.src_t].w;
-        m.ld_h = tables_[b.src_t].ld;
+        const TypeTable& tb = tables_[b.src_t];
+        m.h = tb.w;
+        m.ld_h = tb.ld;
+        m.h_dtype = tb.dense ? tb.dtype : kF32;
+        m.slot = tb.host ? tb.slot : nullptr;
+        m.cache = tb.cache;
       } else {
         const Group* sg = nullptr;
         for (const auto& g2 : groups_)
@@ -1733,6 +1748,29 @@ void Engine::set_cache(const std::vector<std::vector<NodeId>>& cached) {
   HG_CUDA(cudaStreamSynchronize(st_));
   cache_on_ = true;
   for (int t = 0; t < ntypes_; ++t) cache_types_[t] = t < static_cast<int>(cached.size());
+  // host-resident feature tables: copy the cached rows into HBM and map every node to
+  // its cache row (or -1: read over PCIe from the pinned table)
+  for (int t = 0; t < ntypes_ && t < static_cast<int>(cached.size()); ++t) {
+    TypeTable& tb = tables_[t];
+    if (!tb.host) continue;
+    if (!tb.slot) tb.slot = static_cast<int*>(alloc(type_counts_[t] * 4));
+    std::vector<int> slot(type_counts_[t], -1);
+    const std::size_t esz = tb.dtype == kF32 ? 4 : 2, row = static_cast<std::size_t>(tb.ld) * esz;
+    if (cached[t].size() > tb.cache_rows) {
+      tb.cache = static_cast<float*>(alloc(std::max<std::size_t>(16, cached[t].size() * row)));
+      tb.cache_rows = cached[t].size();
+    }
+    std::vector<std::uint8_t> rows(cached[t].size() * row);
+    for (std::size_t i = 0; i < cached[t].size(); ++i) {
+      const NodeId v = cached[t][i];
+      if (v >= type_counts_[t]) throw std::invalid_argument("cached node id out of range: " + std::to_string(v));
+      slot[v] = static_cast<int>(i);
+      std::memcpy(&rows[i * row], static_cast<const std::uint8_t*>(tb.host_mem) + static_cast<std::size_t>(v) * row, row);
+    }
+    if (!rows.empty()) HG_CUDA(cudaMemcpyAsync(tb.cache, rows.data(), rows.size(), cudaMemcpyHostToDevice, st_));
+    HG_CUDA(cudaMemcpyAsync(tb.slot, slot.data(), slot.size() * 4, cudaMemcpyHostToDevice, st_));
+    HG_CUDA(cudaStreamSynchronize(st_));
+  }
   drop_graphs();  // the captured steps did not look the frontier up
 }
 
@@ -1859,7 +1897,10 @@ bool Engine::read_tensor(const std::string& name, std::string& dtype, std::vecto
       const int n = dev_int(f.count);
       float* tmp = nullptr;
       HG_CUDA(cudaMalloc(&tmp, std::max<std::size_t>(16, static_cast<std::size_t>(n) * tables_[t].dim * 4)));
-      if (n) launch_pdl(k_gather_rows, 64, 256, 0, st_, tables_[t].w, tables_[t].ld, f.list, f.count, tables_[t].dim, tmp);
+      if (n)
+        launch_pdl(k_gather_rows, 64, 256, 0, st_, static_cast<const float*>(tables_[t].w), tables_[t].ld,
+                   static_cast<const std::uint32_t*>(f.list), static_cast<const int*>(f.count), tables_[t].dim, tmp,
+                   tables_[t].dense ? tables_[t].dtype : 0);
       HG_CUDA(cudaStreamSynchronize(st_));
       mat(tmp, n, tables_[t].dim, tables_[t].dim);
       cudaFree(tmp);
@@ -1984,6 +2025,68 @@ void Engine::load_table_rows(int type, const NodeId* ids, std::int64_t n, const 
   HG_CUDA(cudaFreeAsync(d_ids, st_));
   HG_CUDA(cudaFreeAsync(d_rows, st_));
   HG_CUDA(cudaStreamSynchronize(st_));
+}
+
+}  // namespace hetgpu
+
+namespace hetgpu {
+
+namespace {
+// round-to-nearest-even conversions on the host (the CUDA headers' __host__ paths)
+std::uint16_t f32_to_f16(float x) {
+  const __half_raw r = __float2half_rn(x);
+  return r.x;
+}
+std::uint16_t f32_to_bf16(float x) {
+  const __nv_bfloat16_raw r = __float2bfloat16_rn(x);
+  return r.x;
+}
+}  // namespace
+
+// One dense feature table, converted to its storage type in chunks (no full-size
+// staging copy): f32 / f16 / bf16 rows of ld elements (ld = dim rounded up to 4, zero
+// padding), in HBM or, with feat_host, in pinned host memory mapped into the device's
+// address space (the gather reads missing rows over PCIe; set_cache() adds an HBM copy
+// of the hot rows).
+void Engine::upload_dense(const NodeTypeInfo& nt, TypeTable& tb) {
+  tb.dense = true;
+  tb.dtype = o_.feat_dtype;
+  if (tb.dtype < 0 || tb.dtype > 2) throw std::invalid_argument("feature dtype must be 0 (f32), 1 (f16) or 2 (bf16)");
+  const std::size_t rows = nt.count, esz = tb.dtype == kF32 ? 4 : 2;
+  const std::size_t bytes = std::max<std::size_t>(16, rows * tb.ld * esz);
+  std::uint8_t* dst = nullptr;
+  if (o_.feat_host) {
+    tb.host = true;
+    HG_CUDA(cudaHostAlloc(&tb.host_mem, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    void* dev = nullptr;
+    HG_CUDA(cudaHostGetDevicePointer(&dev, tb.host_mem, 0));
+    tb.w = static_cast<float*>(dev);
+    dst = static_cast<std::uint8_t*>(tb.host_mem);
+  } else {
+    tb.w = static_cast<float*>(alloc(bytes));
+  }
+  const std::size_t chunk_rows = std::max<std::size_t>(1, (64u << 20) / (tb.ld * esz));
+  std::vector<std::uint8_t> stage(std::min(rows, chunk_rows) * tb.ld * esz);
+  for (std::size_t r0 = 0; r0 < rows; r0 += chunk_rows) {
+    const std::size_t n = std::min(chunk_rows, rows - r0);
+    std::fill(stage.begin(), stage.end(), 0);
+    for (std::size_t i = 0; i < n; ++i) {
+      const float* src = &nt.dense[(r0 + i) * nt.dim];
+      if (tb.dtype == kF32) {
+        std::memcpy(&stage[i * tb.ld * 4], src, sizeof(float) * nt.dim);
+      } else {
+        auto* o = reinterpret_cast<std::uint16_t*>(&stage[i * tb.ld * 2]);
+        for (int c = 0; c < nt.dim; ++c) o[c] = tb.dtype == kF16 ? f32_to_f16(src[c]) : f32_to_bf16(src[c]);
+      }
+    }
+    const std::size_t off = r0 * tb.ld * esz, len = n * tb.ld * esz;
+    if (dst) {
+      std::memcpy(dst + off, stage.data(), len);
+    } else {
+      HG_CUDA(cudaMemcpyAsync(reinterpret_cast<std::uint8_t*>(tb.w) + off, stage.data(), len, cudaMemcpyHostToDevice, st_));
+      HG_CUDA(cudaStreamSynchronize(st_));  // the staging buffer is refilled next
+    }
+  }
 }
 
 }  // namespace hetgpu

@@ -40,6 +40,11 @@ struct EngineOptions {
   std::uint64_t learn_seed = 0;  // init_learnable seed
   int device = 0;
   int elem_bytes = 4;  // byte accounting of partial messages (AccountingModel)
+  // storage of the dense layer-0 feature tables: 0 f32 (parity), 1 f16, 2 bf16 (C4's
+  // fp16 paper features); feat_host = 1 keeps them in pinned host memory (read over
+  // PCIe, zero-copy) with an HBM cache of the rows set_cache() installs
+  int feat_dtype = 0;
+  int feat_host = 0;
   // sampler-only engines (sample_khop / sample_khop_restricted, sampling.cpp:94-103):
   // explicit per-hop relation sets replace the metatree's; no model state is built
   bool sample_only = false;
@@ -247,6 +252,12 @@ class Engine {
   struct TypeTable {
     int dim = 0, ld = 0;
     bool learnable = false, dense = false;
+    int dtype = 0;               // dense tables: FeatDtype of the rows w points at
+    bool host = false;           // dense rows in pinned host memory (w = its device mapping)
+    void* host_mem = nullptr;    // the pinned allocation (host pointer)
+    int* slot = nullptr;         // host tables: per node its HBM cache row or -1
+    float* cache = nullptr;      // HBM cache rows (dtype elements)
+    std::uint64_t cache_rows = 0;
     float *w = nullptr, *m = nullptr, *v = nullptr;
     std::int64_t* step = nullptr;  // device
     std::int64_t host_step = 0;
@@ -255,6 +266,7 @@ class Engine {
   void* alloc(std::size_t bytes);
   void build_plan(const Graph& g);
   void upload(const Graph& g);
+  void upload_dense(const NodeTypeInfo& nt, TypeTable& tb);
   void run_sampling(cudaStream_t ss);  // everything of one sample slot, on stream ss
   void run_forward();
   void run_loss(bool train);

@@ -65,11 +65,18 @@ struct DMeanBatch {
 };
 
 // ---- split forward: gather-mean of every block of a hop, then projection ------------------
+// storage of a layer-0 dense feature table (fp16 features)
+enum FeatDtype : int { kF32 = 0, kF16 = 1, kBF16 = 2 };
 struct MeanBlock {
   const std::uint32_t* indptr;
   const std::uint32_t* keys;  // global ids (by_id) or frontier rows
-  const float* h;
+  const float* h;             // rows of h_dtype elements (h_dtype != kF32: reinterpret)
   int ld_h;
+  int h_dtype;                // FeatDtype of h (layer-0 dense tables; inner layers are f32)
+  // device cache of a host-resident table (cache.cpp:121-141 fill): slot[key] >= 0 reads
+  // row slot of `cache` (HBM), otherwise row key of h (pinned host memory, read over PCIe)
+  const int* slot;
+  const float* cache;
   int din;
   const int* n_rows;
   int rows_cap;

@@ -5,6 +5,9 @@
 // One 64x64 output tile per CTA, 256 threads with a 4x4 register tile each,
 // K staged through shared memory in 32-deep slabs. Several independent
 // problems share one launch (tile ids are linearised over the problems).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
 #include "adam.cuh"
 #include "gemm.cuh"
 
@@ -217,6 +220,32 @@ __global__ void __launch_bounds__(kT) k_dmean_tiles(DMeanBatch b) {
 #define HG_GATHER_BATCH 5
 #endif
 constexpr int kGatherBatch = HG_GATHER_BATCH;  // neighbour rows in flight per lane
+// 4 consecutive features (columns c..c+3) of row `key` as fp32: fp32 rows by one
+// 16-byte load, fp16 / bf16 rows by one 8-byte load; a cached host table reads the
+// HBM copy when the row is cached
+__device__ __forceinline__ float4 load_row4(const MeanBlock& B, std::uint32_t key, int c) {
+  const void* base = B.h;
+  std::size_t row = key;
+  if (B.slot) {
+    const int sl = __ldg(B.slot + key);
+    if (sl >= 0) {
+      base = B.cache;
+      row = static_cast<std::size_t>(sl);
+    }
+  }
+  const std::size_t at = row * B.ld_h + c;
+  if (B.h_dtype == kF32) return __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(base) + at));
+  const uint2 raw = __ldg(reinterpret_cast<const uint2*>(static_cast<const std::uint16_t*>(base) + at));
+  if (B.h_dtype == kF16) {
+    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
+    const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
+    return make_float4(a.x, a.y, b.x, b.y);
+  }
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
 __global__ void __launch_bounds__(256) k_gather_mean(MeanBatch m) {
   pdl_enter();
   const int hl = threadIdx.x & 15;
@@ -238,7 +267,6 @@ __global__ void __launch_bounds__(256) k_gather_mean(MeanBatch m) {
       continue;
     }
     const std::uint32_t lo = B.indptr[i], hi = B.indptr[i + 1];
-    const float* base = B.h + c;
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
     // batches of kGatherBatch neighbours (the last one predicated): one key round trip and
     // one row round trip per batch, summed in edge order
@@ -249,9 +277,7 @@ __global__ void __launch_bounds__(256) k_gather_mean(MeanBatch m) {
       for (int q = 0; q < kGatherBatch; ++q) kk[q] = q < cnt ? __ldg(B.keys + e + q) : 0u;
       float4 v[kGatherBatch];
 #pragma unroll
-      for (int q = 0; q < kGatherBatch; ++q)
-        v[q] = q < cnt ? __ldg(reinterpret_cast<const float4*>(base + static_cast<std::size_t>(kk[q]) * B.ld_h))
-                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q = 0; q < kGatherBatch; ++q) v[q] = q < cnt ? load_row4(B, kk[q], c) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int q = 0; q < kGatherBatch; ++q) {
         s.x += v[q].x;

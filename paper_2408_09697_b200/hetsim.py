@@ -233,11 +233,17 @@ def cache_plan(g: HetGraph, hot: Dict[str, np.ndarray], n_types: int, budget: in
 class Engine:
     """One meta-partition of the RAF engine on one GPU (run_raf_batch, raf.cpp:344-530)."""
 
+    FEAT_DTYPES = {"f32": 0, "f16": 1, "bf16": 2}
+
     def __init__(self, g: HetGraph, fanouts: Sequence[int], hidden: int = 64, batch_cap: int = 1024, p: int = 1,
-                 rank: int = 0, model_seed: int = 0, learn_seed: int = 0, device: int = 0):
+                 rank: int = 0, model_seed: int = 0, learn_seed: int = 0, device: int = 0, feat_dtype: str = "f32",
+                 feat_host: bool = False):
         fo = (C.c_int * len(fanouts))(*[int(f) for f in fanouts])
         self._fo = fo
-        opts = N.EngineOpts(len(fanouts), fo, hidden, batch_cap, p, rank, model_seed, learn_seed, device)
+        if feat_dtype not in self.FEAT_DTYPES:
+            raise ValueError("feature dtype must be one of f32, f16, bf16")
+        opts = N.EngineOpts(len(fanouts), fo, hidden, batch_cap, p, rank, model_seed, learn_seed, device,
+                            self.FEAT_DTYPES[feat_dtype], int(bool(feat_host)))
         self.k = len(fanouts)
         self.graph = g  # keep alive
         self._h = N.lib().hg_engine_create(g.handle, C.byref(opts))
