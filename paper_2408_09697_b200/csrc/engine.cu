@@ -2052,6 +2052,7 @@ void Engine::upload_dense(const NodeTypeInfo& nt, TypeTable& tb) {
   tb.dense = true;
   tb.dtype = o_.feat_dtype;
   if (tb.dtype < 0 || tb.dtype > 2) throw std::invalid_argument("feature dtype must be 0 (f32), 1 (f16) or 2 (bf16)");
+  if (tb.dtype != kF32) tb.ld = (std::max(1, nt.dim) + 7) & ~7;  // 16-byte rows of halves (8-wide loads)
   const std::size_t rows = nt.count, esz = tb.dtype == kF32 ? 4 : 2;
   const std::size_t bytes = std::max<std::size_t>(16, rows * tb.ld * esz);
   std::uint8_t* dst = nullptr;

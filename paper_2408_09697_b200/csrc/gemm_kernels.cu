@@ -220,10 +220,23 @@ __global__ void __launch_bounds__(kT) k_dmean_tiles(DMeanBatch b) {
 #define HG_GATHER_BATCH 5
 #endif
 constexpr int kGatherBatch = HG_GATHER_BATCH;  // neighbour rows in flight per lane
-// 4 consecutive features (columns c..c+3) of row `key` as fp32: fp32 rows by one
-// 16-byte load, fp16 / bf16 rows by one 8-byte load; a cached host table reads the
-// HBM copy when the row is cached
+// 4 consecutive fp32 features (columns c..c+3) of row `key` (one 16-byte load); a
+// cached host table reads the HBM copy when the row is cached
 __device__ __forceinline__ float4 load_row4(const MeanBlock& B, std::uint32_t key, int c) {
+  const float* base = B.h;
+  std::size_t row = key;
+  if (B.slot) {
+    const int sl = __ldg(B.slot + key);
+    if (sl >= 0) {
+      base = B.cache;
+      row = static_cast<std::size_t>(sl);
+    }
+  }
+  return __ldg(reinterpret_cast<const float4*>(base + row * B.ld_h + c));
+}
+
+// 8 consecutive features of a half-precision row (one 16-byte load)
+__device__ __forceinline__ void load_row8(const MeanBlock& B, std::uint32_t key, int c, float4& a, float4& b) {
   const void* base = B.h;
   std::size_t row = key;
   if (B.slot) {
@@ -233,18 +246,27 @@ __device__ __forceinline__ float4 load_row4(const MeanBlock& B, std::uint32_t ke
       row = static_cast<std::size_t>(sl);
     }
   }
-  const std::size_t at = row * B.ld_h + c;
-  if (B.h_dtype == kF32) return __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(base) + at));
-  const uint2 raw = __ldg(reinterpret_cast<const uint2*>(static_cast<const std::uint16_t*>(base) + at));
-  if (B.h_dtype == kF16) {
-    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
-    const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
-    return make_float4(a.x, a.y, b.x, b.y);
-  }
-  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
-  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
-  return make_float4(a.x, a.y, b.x, b.y);
+  const uint4 raw = __ldg(reinterpret_cast<const uint4*>(static_cast<const std::uint16_t*>(base) + row * B.ld_h + c));
+  float2 f[4];
+  const std::uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    f[j] = B.h_dtype == kF16 ? __half22float2(*reinterpret_cast<const __half2*>(&w[j]))
+                             : __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[j]));
+  a = make_float4(f[0].x, f[0].y, f[1].x, f[1].y);
+  b = make_float4(f[2].x, f[2].y, f[3].x, f[3].y);
 }
+
+__device__ __forceinline__ void add4(float4& s, const float4& v) {
+  s.x += v.x;
+  s.y += v.y;
+  s.z += v.z;
+  s.w += v.w;
+}
+__device__ __forceinline__ float4 scale4(float4 s, float k) { return make_float4(s.x * k, s.y * k, s.z * k, s.w * k); }
+
+// columns per half-warp item: 16 lanes x 4 fp32 features, or 16 lanes x 8 half features
+__host__ __device__ inline int gather_chunk(int h_dtype) { return h_dtype == kF32 ? 64 : 128; }
 
 __global__ void __launch_bounds__(256) k_gather_mean(MeanBatch m) {
   pdl_enter();
@@ -254,20 +276,26 @@ __global__ void __launch_bounds__(256) k_gather_mean(MeanBatch m) {
     int b = 0;
     while (b + 1 < m.nb && item >= m.item_base[b + 1]) ++b;
     const MeanBlock& B = m.b[b];
-    const int nch = (B.din + 63) / 64;
+    const bool wide = B.h_dtype != kF32;  // 8 features per lane
+    const int chunk = gather_chunk(B.h_dtype);
+    const int nch = (B.din + chunk - 1) / chunk;
     const int local = item - m.item_base[b];
-    const int i = local / nch, c = (local % nch) * 64 + 4 * hl;
+    const int i = local / nch, c = (local % nch) * chunk + (wide ? 8 : 4) * hl;
     const int n = *B.n_rows;
     if (c >= B.ld_mean) continue;
+    const bool second = wide && c + 4 < B.ld_mean;  // the lane's second float4 of output
+    float* orow = B.mean + static_cast<std::size_t>(i) * B.ld_mean + c;
     if (i >= n) {
       // zero tail up to the next 32-row boundary: the tensor-core weight gradient
       // streams whole 32-row K chunks of the tape
-      if (i < ((n + 31) & ~31))
-        *reinterpret_cast<float4*>(B.mean + static_cast<std::size_t>(i) * B.ld_mean + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i < ((n + 31) & ~31)) {
+        *reinterpret_cast<float4*>(orow) = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (second) *reinterpret_cast<float4*>(orow + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
       continue;
     }
     const std::uint32_t lo = B.indptr[i], hi = B.indptr[i + 1];
-    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f), s2 = s;
     // batches of kGatherBatch neighbours (the last one predicated): one key round trip and
     // one row round trip per batch, summed in edge order
     for (std::uint32_t e = lo; e < hi; e += kGatherBatch) {
@@ -275,25 +303,29 @@ __global__ void __launch_bounds__(256) k_gather_mean(MeanBatch m) {
       std::uint32_t kk[kGatherBatch];
 #pragma unroll
       for (int q = 0; q < kGatherBatch; ++q) kk[q] = q < cnt ? __ldg(B.keys + e + q) : 0u;
-      float4 v[kGatherBatch];
+      if (!wide) {
+        float4 v[kGatherBatch];
 #pragma unroll
-      for (int q = 0; q < kGatherBatch; ++q) v[q] = q < cnt ? load_row4(B, kk[q], c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int q = 0; q < kGatherBatch; ++q) v[q] = q < cnt ? load_row4(B, kk[q], c) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int q = 0; q < kGatherBatch; ++q) {
-        s.x += v[q].x;
-        s.y += v[q].y;
-        s.z += v[q].z;
-        s.w += v[q].w;
+        for (int q = 0; q < kGatherBatch; ++q) add4(s, v[q]);
+      } else {
+        float4 v[kGatherBatch], w[kGatherBatch];
+#pragma unroll
+        for (int q = 0; q < kGatherBatch; ++q) {
+          v[q] = w[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (q < cnt) load_row8(B, kk[q], c, v[q], w[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < kGatherBatch; ++q) {
+          add4(s, v[q]);
+          add4(s2, w[q]);
+        }
       }
     }
-    if (hi > lo) {
-      const float inv = 1.0f / static_cast<float>(hi - lo);
-      s.x *= inv;
-      s.y *= inv;
-      s.z *= inv;
-      s.w *= inv;
-    }
-    *reinterpret_cast<float4*>(B.mean + static_cast<std::size_t>(i) * B.ld_mean + c) = s;
+    const float inv = hi > lo ? 1.0f / static_cast<float>(hi - lo) : 0.f;
+    *reinterpret_cast<float4*>(orow) = scale4(s, inv);
+    if (second) *reinterpret_cast<float4*>(orow + 4) = scale4(s2, inv);
   }
 }
 
@@ -365,7 +397,7 @@ void gather_mean(MeanBatch& m, cudaStream_t st) {
   int items = 0;
   for (int b = 0; b < m.nb; ++b) {
     m.item_base[b] = items;
-    items += m.b[b].rows_cap * static_cast<int>(ceil_div(m.b[b].din, 64));
+    items += m.b[b].rows_cap * static_cast<int>(ceil_div(m.b[b].din, gather_chunk(m.b[b].h_dtype)));
   }
   m.item_base[m.nb] = items;
   const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(items, 16), HG_GATHER_WAVES * num_sms())));

@@ -96,6 +96,23 @@ def ogbn_mag_spec() -> dict:
                 self_paired=["cites"])
 
 
+def mag240m_spec(scale: float = 1.0) -> dict:
+    """BASELINE.json configs[3] / SURVEY §8(d) C4: MAG240M shape (paper 121,751,666 with
+    768-d features, author 122,383,112 and institution 25,721 learnable 64-d; writes 386.0M,
+    affiliated 44.6M, cites 1,297.7M edges; 153 classes), uniform degrees, every count
+    multiplied by `scale` (the full size exceeds one B200 and this host's memory)."""
+    def n(x):
+        return max(1, int(round(x * scale)))
+    return dict(name=f"mag240m-shape-x{scale:g}", target="paper", num_classes=153, label_noise=0.1,
+                node_types=[dict(name="paper", count=n(121751666), dim=768, storage="dense"),
+                            dict(name="author", count=n(122383112), dim=64, storage="learnable"),
+                            dict(name="institution", count=n(25721), dim=64, storage="learnable")],
+                relations=[dict(src="author", edge="writes", dst="paper", edges=n(386000000)),
+                           dict(src="author", edge="affiliated", dst="institution", edges=n(44600000)),
+                           dict(src="paper", edge="cites", dst="paper", edges=n(1297700000))],
+                self_paired=["cites"])
+
+
 def mix_seed(a: int, b: int) -> int:
     """mix_seed (src/sampling.cpp:9-15)."""
     return int(N.lib().hg_mix_seed(a, b))
