@@ -356,8 +356,8 @@ def run_b200(args):
     # (`csc_gather`); the top layer's launches of the same kernels (hop-1 blocks:
     # 1024 destination rows, latency-bound) are the `*_top` classes. The sampler is
     # latency-bound (serial mt19937_64 per row) and is reported beside them.
-    alg_by = {"aggregate": alg[1], "csc_gather": alg[3], "aggregate_top": alg[2], "csc_gather_top": alg[4],
-              "sample": alg[0]}
+    alg_by = {"aggregate": alg[1], "csc_gather": alg[3], "aggregate_top": alg[2],
+              "csc_gather_top": alg[4] if len(alg) > 4 else 0.0, "sample": alg[0]}
 
     lib_sha = lib_digest()
     traffic_rec = load_traffic()
@@ -420,6 +420,14 @@ def run_b200(args):
         "final_loss": loss,
         "setup_s": {"graph_gen": t_gen},
     }
+    if n > 1 and "agg_all" in classes:
+        # AGG_all = one ncclAllReduce of the [B+1 x C] fp32 partial logits per step (NVLink);
+        # bus bandwidth in NCCL's convention: 2 (n-1)/n x bytes / time
+        ag_bytes = (batch + 1) * (4 * ((349 + 3) // 4))
+        ag_s = classes["agg_all"] / max(1, launches_by.get("agg_all", prof_steps)) / 1000.0
+        line["agg_all"] = {"nranks": n, "bytes": ag_bytes, "us_per_call": 1e6 * ag_s,
+                           "algbw_GBps": ag_bytes / ag_s / 1e9, "busbw_GBps": 2 * (n - 1) / n * ag_bytes / ag_s / 1e9,
+                           "transport": "NCCL all-reduce over NVLink (NVSwitch)"}
     if not args.no_cpu_baseline and n == 1:
         # bounded sample: 8 batches per host thread (~10-20 s of CPU work)
         threads = os.cpu_count() or 1

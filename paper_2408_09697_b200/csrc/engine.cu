@@ -587,6 +587,8 @@ void Engine::upload(const Graph& g) {
       x.off_dh = take(static_cast<std::size_t>(std::max(1, x.cap)) * x.ld * 4);
       xchg_.push_back(x);
     }
+    // the replica barrier's flags: slot q holds the last step replica q finished reading
+    off_flags_ = take(static_cast<std::size_t>(kMaxRep) * 4);
     arena_bytes_ = std::max<std::size_t>(at, 256);
     arena_ = static_cast<std::uint8_t*>(alloc(arena_bytes_));
     for (auto& x : xchg_) {
@@ -602,7 +604,10 @@ void Engine::upload(const Graph& g) {
       x.peer_w.assign(replica_group_.size(), nullptr);
       x.peer_w[replica_pos_] = tables_[x.t].w;
     }
-    barrier_word_ = static_cast<float*>(alloc(16));
+    HG_CUDA(cudaMemsetAsync(arena_ + off_flags_, 0, static_cast<std::size_t>(kMaxRep) * 4, st_));
+    barrier_epoch_ = static_cast<unsigned*>(alloc(16));
+    HG_CUDA(cudaMemsetAsync(barrier_epoch_, 0, 16, st_));
+    HG_CUDA(cudaStreamSynchronize(st_));
     peer_arena_.assign(replica_group_.size(), nullptr);
     peer_arena_[replica_pos_] = arena_;
   }
@@ -1208,10 +1213,17 @@ void Engine::run_replica_merge() {
     }
     launch_pdl(k_feat_sync, 1, 1, 0, st_, fs, feat_sync_dev_);
   }
-  // 3. nobody rewrites its arena (next step's sampling) before every peer read it
+  // 3. nobody rewrites its arena (next step's sampling) before every peer read it:
+  //    a flag barrier over the IPC-mapped arenas (NVLink stores + acquire loads)
   timed("replica_barrier", 0, [&] {
-    if (!counting_ && ncclAllReduce(barrier_word_, barrier_word_, 1, ncclFloat, ncclSum, rcomm_, st_) != ncclSuccess)
-      throw std::runtime_error("ncclAllReduce (replica barrier) failed");
+    ReplicaBarrier rb{};
+    rb.n = static_cast<int>(peer_arena_.size());
+    rb.pos = replica_pos_;
+    for (int r = 0; r < rb.n; ++r)
+      rb.peer_flags[r] = reinterpret_cast<unsigned*>(const_cast<std::uint8_t*>(peer_arena_[r]) + off_flags_);
+    rb.my_flags = reinterpret_cast<unsigned*>(arena_ + off_flags_);
+    rb.epoch = barrier_epoch_;
+    replica_barrier(rb, st_);
   });
 #else
   throw std::runtime_error("replica groups need NCCL");

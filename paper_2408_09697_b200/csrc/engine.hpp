@@ -481,7 +481,8 @@ class Engine {
   std::size_t arena_bytes_ = 0;
   std::vector<const std::uint8_t*> peer_arena_;  // per group member (self: arena_)
   std::vector<void*> ipc_opened_;
-  float* barrier_word_ = nullptr;
+  unsigned* barrier_epoch_ = nullptr;  // steps this replica has passed the barrier (device)
+  std::size_t off_flags_ = 0;          // barrier flags in the exchange arena
   bool xchg_type(int t) const {
     for (const auto& x : xchg_)
       if (x.t == t) return true;

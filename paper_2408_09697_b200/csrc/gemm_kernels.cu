@@ -268,7 +268,12 @@ __device__ __forceinline__ float4 scale4(float4 s, float k) { return make_float4
 // columns per half-warp item: 16 lanes x 4 fp32 features, or 16 lanes x 8 half features
 __host__ __device__ inline int gather_chunk(int h_dtype) { return h_dtype == kF32 ? 64 : 128; }
 
-__global__ void __launch_bounds__(256) k_gather_mean(MeanBatch m) {
+// WIDE: the batch holds a half-precision table (8-feature lanes); the fp32-only
+// instantiation keeps the original register budget (one float4 per neighbour)
+// CACHED: a host-resident table with an HBM cache is in the batch (per-row slot lookup).
+// fp32-only batches (WIDE = false) run the 64-column items with one float4 per neighbour.
+template <bool WIDE, bool CACHED>
+__global__ void __launch_bounds__(256, WIDE ? 4 : 8) k_gather_mean(MeanBatch m) {
   pdl_enter();
   const int hl = threadIdx.x & 15;
   const int halves = gridDim.x * (blockDim.x >> 4);
@@ -276,56 +281,89 @@ __global__ void __launch_bounds__(256) k_gather_mean(MeanBatch m) {
     int b = 0;
     while (b + 1 < m.nb && item >= m.item_base[b + 1]) ++b;
     const MeanBlock& B = m.b[b];
-    const bool wide = B.h_dtype != kF32;  // 8 features per lane
-    const int chunk = gather_chunk(B.h_dtype);
-    const int nch = (B.din + chunk - 1) / chunk;
-    const int local = item - m.item_base[b];
-    const int i = local / nch, c = (local % nch) * chunk + (wide ? 8 : 4) * hl;
     const int n = *B.n_rows;
-    if (c >= B.ld_mean) continue;
-    const bool second = wide && c + 4 < B.ld_mean;  // the lane's second float4 of output
-    float* orow = B.mean + static_cast<std::size_t>(i) * B.ld_mean + c;
-    if (i >= n) {
-      // zero tail up to the next 32-row boundary: the tensor-core weight gradient
-      // streams whole 32-row K chunks of the tape
-      if (i < ((n + 31) & ~31)) {
-        *reinterpret_cast<float4*>(orow) = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (second) *reinterpret_cast<float4*>(orow + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int local = item - m.item_base[b];
+    if constexpr (!WIDE) {
+      const int nch = (B.din + 63) / 64;
+      const int i = local / nch, c = (local % nch) * 64 + 4 * hl;
+      if (c >= B.ld_mean) continue;
+      if (i >= n) {
+        // zero tail up to the next 32-row boundary: the tensor-core weight gradient
+        // streams whole 32-row K chunks of the tape
+        if (i < ((n + 31) & ~31))
+          *reinterpret_cast<float4*>(B.mean + static_cast<std::size_t>(i) * B.ld_mean + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+        continue;
       }
-      continue;
-    }
-    const std::uint32_t lo = B.indptr[i], hi = B.indptr[i + 1];
-    float4 s = make_float4(0.f, 0.f, 0.f, 0.f), s2 = s;
-    // batches of kGatherBatch neighbours (the last one predicated): one key round trip and
-    // one row round trip per batch, summed in edge order
-    for (std::uint32_t e = lo; e < hi; e += kGatherBatch) {
-      const std::uint32_t cnt = min(static_cast<std::uint32_t>(kGatherBatch), hi - e);
-      std::uint32_t kk[kGatherBatch];
+      const std::uint32_t lo = B.indptr[i], hi = B.indptr[i + 1];
+      const float* base = B.h + c;
+      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+      // batches of kGatherBatch neighbours (the last one predicated): one key round trip and
+      // one row round trip per batch, summed in edge order
+      for (std::uint32_t e = lo; e < hi; e += kGatherBatch) {
+        const std::uint32_t cnt = min(static_cast<std::uint32_t>(kGatherBatch), hi - e);
+        std::uint32_t kk[kGatherBatch];
 #pragma unroll
-      for (int q = 0; q < kGatherBatch; ++q) kk[q] = q < cnt ? __ldg(B.keys + e + q) : 0u;
-      if (!wide) {
+        for (int q = 0; q < kGatherBatch; ++q) kk[q] = q < cnt ? __ldg(B.keys + e + q) : 0u;
         float4 v[kGatherBatch];
 #pragma unroll
-        for (int q = 0; q < kGatherBatch; ++q) v[q] = q < cnt ? load_row4(B, kk[q], c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int q = 0; q < kGatherBatch; ++q) {
+          if (CACHED)
+            v[q] = q < cnt ? load_row4(B, kk[q], c) : make_float4(0.f, 0.f, 0.f, 0.f);
+          else
+            v[q] = q < cnt ? __ldg(reinterpret_cast<const float4*>(base + static_cast<std::size_t>(kk[q]) * B.ld_h))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
 #pragma unroll
         for (int q = 0; q < kGatherBatch; ++q) add4(s, v[q]);
-      } else {
-        float4 v[kGatherBatch], w[kGatherBatch];
-#pragma unroll
-        for (int q = 0; q < kGatherBatch; ++q) {
-          v[q] = w[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (q < cnt) load_row8(B, kk[q], c, v[q], w[q]);
+      }
+      if (hi > lo) s = scale4(s, 1.0f / static_cast<float>(hi - lo));
+      *reinterpret_cast<float4*>(B.mean + static_cast<std::size_t>(i) * B.ld_mean + c) = s;
+    } else {
+      const bool wide = B.h_dtype != kF32;  // 8 features per lane
+      const int chunk = gather_chunk(B.h_dtype);
+      const int nch = (B.din + chunk - 1) / chunk;
+      const int i = local / nch, c = (local % nch) * chunk + (wide ? 8 : 4) * hl;
+      if (c >= B.ld_mean) continue;
+      const bool second = wide && c + 4 < B.ld_mean;  // the lane's second float4 of output
+      float* orow = B.mean + static_cast<std::size_t>(i) * B.ld_mean + c;
+      if (i >= n) {
+        if (i < ((n + 31) & ~31)) {
+          *reinterpret_cast<float4*>(orow) = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (second) *reinterpret_cast<float4*>(orow + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
         }
+        continue;
+      }
+      const std::uint32_t lo = B.indptr[i], hi = B.indptr[i + 1];
+      float4 s = make_float4(0.f, 0.f, 0.f, 0.f), s2 = s;
+      for (std::uint32_t e = lo; e < hi; e += kGatherBatch) {
+        const std::uint32_t cnt = min(static_cast<std::uint32_t>(kGatherBatch), hi - e);
+        std::uint32_t kk[kGatherBatch];
 #pragma unroll
-        for (int q = 0; q < kGatherBatch; ++q) {
-          add4(s, v[q]);
-          add4(s2, w[q]);
+        for (int q = 0; q < kGatherBatch; ++q) kk[q] = q < cnt ? __ldg(B.keys + e + q) : 0u;
+        if (!wide) {
+          float4 v[kGatherBatch];
+#pragma unroll
+          for (int q = 0; q < kGatherBatch; ++q) v[q] = q < cnt ? load_row4(B, kk[q], c) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int q = 0; q < kGatherBatch; ++q) add4(s, v[q]);
+        } else {
+          float4 v[kGatherBatch], w[kGatherBatch];
+#pragma unroll
+          for (int q = 0; q < kGatherBatch; ++q) {
+            v[q] = w[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (q < cnt) load_row8(B, kk[q], c, v[q], w[q]);
+          }
+#pragma unroll
+          for (int q = 0; q < kGatherBatch; ++q) {
+            add4(s, v[q]);
+            add4(s2, w[q]);
+          }
         }
       }
+      const float inv = hi > lo ? 1.0f / static_cast<float>(hi - lo) : 0.f;
+      *reinterpret_cast<float4*>(orow) = scale4(s, inv);
+      if (second) *reinterpret_cast<float4*>(orow + 4) = scale4(s2, inv);
     }
-    const float inv = hi > lo ? 1.0f / static_cast<float>(hi - lo) : 0.f;
-    *reinterpret_cast<float4*>(orow) = scale4(s, inv);
-    if (second) *reinterpret_cast<float4*>(orow + 4) = scale4(s2, inv);
   }
 }
 
@@ -401,7 +439,17 @@ void gather_mean(MeanBatch& m, cudaStream_t st) {
   }
   m.item_base[m.nb] = items;
   const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(items, 16), HG_GATHER_WAVES * num_sms())));
-  launch_pdl(k_gather_mean, grid, 256, 0, st, m);
+  bool wide = false, cached = false;
+  for (int b = 0; b < m.nb; ++b) {
+    wide = wide || m.b[b].h_dtype != kF32;
+    cached = cached || m.b[b].slot != nullptr;
+  }
+  if (wide)
+    launch_pdl(k_gather_mean<true, true>, grid, 256, 0, st, m);  // half tables: host or HBM
+  else if (cached)
+    launch_pdl(k_gather_mean<false, true>, grid, 256, 0, st, m);
+  else
+    launch_pdl(k_gather_mean<false, false>, grid, 256, 0, st, m);
 }
 
 void project_tiles(ProjBatch& p, cudaStream_t st) {

@@ -20,6 +20,9 @@ int num_sms() {
 
 namespace {
 
+#ifndef HG_SAMPLE_RNG_FIRST
+#define HG_SAMPLE_RNG_FIRST 0
+#endif
 #ifndef HG_SAMPLE_UNROLL
 #define HG_SAMPLE_UNROLL 4  // sampled edges in flight per lane in the sampler's gather
 #endif
@@ -467,12 +470,14 @@ void sample_hop(const SampleHop& h, const StepScalars* sc, std::uint32_t* slow, 
   if (h.nblk == 0) return;
   LbLayout L{};
   L.nseg = h.nblk;
-  // tickets go out in launch order: the blocks with the most RNG rows (the 156-step
-  // seeding chains, the long pole of the hop) take the first tiles, so their chains
-  // overlap the copy-all blocks instead of forming the kernel's tail
+  // tickets go out in launch order, block by block. HG_SAMPLE_RNG_FIRST gives the
+  // blocks with the most RNG rows (the 156-step seeding chains) the first tiles instead:
+  // measured slower on C2 (sampling 63 -> 70 us/step), so off by default
   for (int i = 0; i < h.nblk; ++i) L.item[i] = i;
+#if HG_SAMPLE_RNG_FIRST
   std::stable_sort(L.item, L.item + h.nblk,
                    [&](int a, int b) { return h.b[a].rng_frac * h.b[a].rows_cap > h.b[b].rng_frac * h.b[b].rows_cap; });
+#endif
   int tiles = 0;
   for (int i = 0; i < h.nblk; ++i) {
     L.base[i] = tiles;
@@ -781,6 +786,33 @@ void hotness_add(const std::uint32_t* ids, const std::uint32_t* indptr, const in
 void hotness_add_list(const std::uint32_t* ids, const int* n, int cap, std::uint32_t* counts, cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, 256), 2 * num_sms()));
   launch_pdl(k_hot_add_list, std::max(grid, 1u), 256, 0, st, ids, n, counts);
+}
+
+// ---- replica barrier ----------------------------------------------------------------------------
+
+namespace {
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__global__ void k_replica_barrier(ReplicaBarrier b) {
+  pdl_enter();  // every read of the peers' arenas by the merge kernels has completed
+  if (threadIdx.x != 0) return;
+  const unsigned e = *b.epoch + 1u;
+  *b.epoch = e;
+  for (int r = 0; r < b.n; ++r) st_release_sys(b.peer_flags[r] + b.pos, e);
+  for (int r = 0; r < b.n; ++r)
+    while (static_cast<int>(ld_acquire_sys(b.my_flags + r) - e) < 0) __nanosleep(100);
+}
+}  // namespace
+
+void replica_barrier(const ReplicaBarrier& b, cudaStream_t st) {
+  if (b.n <= 1) return;
+  launch_pdl(k_replica_barrier, 1, 32, 0, st, b);
 }
 
 }  // namespace hetgpu

@@ -253,6 +253,17 @@ void bump_steps(const std::int64_t* const* steps, const int* const* counts, int 
 // union row the ordered sum over replicas (r = 0..n-1) of their gradient rows:
 // deterministic and identical on every replica, so the replicated tables stay equal.
 constexpr int kMaxRep = 8;
+// replica barrier (the end of the replica merge): every replica stores its step count
+// into flag slot `pos` of every peer's IPC-mapped arena (release, system scope), then
+// waits until all flags of its own arena reached the count (acquire)
+struct ReplicaBarrier {
+  unsigned* peer_flags[kMaxRep];  // flags of replica r's arena (ours included)
+  unsigned* my_flags;
+  unsigned* epoch;                // steps passed (device)
+  int n;
+  int pos;
+};
+void replica_barrier(const ReplicaBarrier& b, cudaStream_t st);
 struct ReplicaMerge {
   const std::uint32_t* ids[kMaxRep];
   const int* count[kMaxRep];

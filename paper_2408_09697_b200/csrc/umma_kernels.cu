@@ -33,6 +33,9 @@ namespace hetgpu {
 
 namespace {
 
+#ifndef HG_UMMA_ACC
+#define HG_UMMA_ACC 4
+#endif
 #ifndef HG_UMMA_WARPS
 #define HG_UMMA_WARPS 8
 #endif
@@ -57,7 +60,12 @@ struct UStage {
   static constexpr int kTxBytes = kATile + kB;         // what TMA brings in per stage
   static constexpr int kStages = NT <= 64 ? HG_USTAGES : HG_USTAGES128;
   static constexpr int kSmem = kStages * kBytes + 1024 + 128;
-  static constexpr int kTmemCols = NT <= 32 ? 32 : NT <= 64 ? 64 : NT <= 128 ? 128 : 256;
+  // kAcc independent TMEM accumulators take the K chunks round robin and are summed in
+  // fp32 by the epilogue: the tensor core's accumulation error grows with the length of
+  // one accumulation chain (measured: 9e-7 at K = 32, 1e-5 at K = 1024 against fp32)
+  static constexpr int kAcc = NT <= 64 ? HG_UMMA_ACC : (HG_UMMA_ACC > 2 ? 2 : HG_UMMA_ACC);
+  static constexpr int kAccCols = NT <= 32 ? 32 : NT <= 64 ? 64 : NT <= 128 ? 128 : 256;
+  static constexpr int kTmemCols = kAcc * kAccCols;
 };
 
 enum Mode { kProject = 0, kDMean = 1, kWGrad = 2 };
@@ -215,13 +223,17 @@ __global__ void __launch_bounds__(kUT) k_umma(const __grid_constant__ UmmaArgs<B
       const int s = ch % S;
       const std::uint32_t a_hi = umma::smem_u32(smem + s * UStage<NT>::kBytes), a_lo = a_hi + kATile;
       const std::uint32_t b_hi = a_hi + 2 * kATile, b_lo = b_hi + UStage<NT>::kB;
+      // chunk ch accumulates into TMEM accumulator ch % kAcc (its first chunk starts it)
+      constexpr int kA = UStage<NT>::kAcc;
+      const std::uint32_t acc = tmem + static_cast<std::uint32_t>((ch % kA) * UStage<NT>::kAccCols);
+      const bool first = ch < kA;
       // hi.hi as soon as the tiles land (overlaps the residual pass) ...
       umma::mbar_wait(umma::smem_u32(&full[s]), (ch / S) & 1);
       umma::fence_after_sync();
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)  // 8 tf32 of K per MMA
-        umma::mma_tf32(tmem, dsc(Majors<MODE>::a, a_hi, kk), dsc(Majors<MODE>::b, b_hi, kk), kIdesc,
-                       (ch > 0 || kk > 0) ? 1u : 0u);
+        umma::mma_tf32(acc, dsc(Majors<MODE>::a, a_hi, kk), dsc(Majors<MODE>::b, b_hi, kk), kIdesc,
+                       (!first || kk > 0) ? 1u : 0u);
       // ... then the two residual products
       umma::mbar_wait(umma::smem_u32(&conv[s]), (ch / S) & 1);
       umma::fence_after_sync();
@@ -229,8 +241,8 @@ __global__ void __launch_bounds__(kUT) k_umma(const __grid_constant__ UmmaArgs<B
       for (int kk = 0; kk < 4; ++kk) {
         const std::uint64_t ah = dsc(Majors<MODE>::a, a_hi, kk), al = dsc(Majors<MODE>::a, a_lo, kk);
         const std::uint64_t bh = dsc(Majors<MODE>::b, b_hi, kk), bl = dsc(Majors<MODE>::b, b_lo, kk);
-        umma::mma_tf32(tmem, ah, bl, kIdesc, 1u);
-        umma::mma_tf32(tmem, al, bh, kIdesc, 1u);
+        umma::mma_tf32(acc, ah, bl, kIdesc, 1u);
+        umma::mma_tf32(acc, al, bh, kIdesc, 1u);
       }
       umma::commit(umma::smem_u32(&empty[s]));  // frees the stage once these MMAs are done
     }
@@ -252,6 +264,13 @@ __global__ void __launch_bounds__(kUT) k_umma(const __grid_constant__ UmmaArgs<B
   for (int c0 = c_begin; c0 < c_begin + kColsPerWarp && c0 < NT; c0 += 16) {
     float v[16];
     umma::tmem_ld16(trow + c0, v);
+    // the other accumulators (only those that received a chunk), summed in fp32
+    for (int a = 1; a < UStage<NT>::kAcc && a < nch; ++a) {
+      float u[16];
+      umma::tmem_ld16(trow + static_cast<std::uint32_t>(a * UStage<NT>::kAccCols) + c0, u);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] += u[j];
+    }
     if constexpr (MODE == kProject) {
       const ProjGroup& g = args.b.g[p];
       const int row = row0 + m;
