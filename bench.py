@@ -236,7 +236,16 @@ def run_b200(args):
     g = H.gen_synthetic(H.ogbn_mag_spec(), SEED)
     t_gen = time.time() - t0
     dbg("graph generated")
-    eng = H.Engine.for_experiment(g, FANOUTS, HIDDEN, SEED, batch_cap=batch, p=n, rank=rank, device=local)
+    plan_kw, plan_desc = {}, "reference meta_partition"
+    if n > 1 and args.plan == "work":
+        # work-aware plan (not the reference's policy; same numbers): per sub-metatree the
+        # sampled edges and learnable leaf rows of 4 batches, measured on this GPU
+        sw = H.sub_work(g, FANOUTS, 4, BATCH_PER_GPU, SEED, device=local)
+        plan_kw = {"sub_work": np.concatenate([sw["work"], sw["learn_rows"]])}
+        parts = H.meta_partition_work_aware(g, len(FANOUTS), n, plan_kw["sub_work"])
+        plan_desc = "work-aware (sub-metatree groups " + " | ".join(
+            ",".join(str(int(x)) for x in parts[f"part{i}.sub_ids"]) for i in range(n)) + ")"
+    eng = H.Engine.for_experiment(g, FANOUTS, HIDDEN, SEED, batch_cap=batch, p=n, rank=rank, device=local, **plan_kw)
     if world > 1:
         import torch.distributed as dist
         uid = [H.nccl_unique_id() if rank == 0 else None]
@@ -391,6 +400,7 @@ def run_b200(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": "C2 ogbn-mag-shape (BASELINE configs[1]) 2-layer RGCN hidden 64, fanout [25,20]",
                    "global_batch": batch, "batch_per_gpu": BATCH_PER_GPU, "parallelism": f"meta-partition p={n}",
+                   "plan": plan_desc,
                    "graph_seed": SEED, "l2": "not flushed: tables 1.3 GB + CSR 0.3 GB >> 126 MB L2, new rows every step"},
         # a real epoch (len(ep_b) batches of 1024 x N) through Engine.prefetch + Engine.step
         "epoch_time_s": ep_time,
@@ -451,6 +461,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--plan", default="work", choices=["work", "reference"],
+                    help="N > 1: work-aware meta-partition (default) or the reference's meta_partition")
     ap.add_argument("--warmup-ref", type=int, default=0)
     args = ap.parse_args()
     if args.warmup < 3:

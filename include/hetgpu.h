@@ -103,6 +103,18 @@ hg_bundle* hg_graph_schema(const hg_graph* g);
  * subs.{child_pos,weight}, part{i}.{sub_ids,relations,node_types,cacheable,replica,weight},
  * hop_rels{h}. */
 hg_bundle* hg_meta_partition(const hg_graph* g, int k, int p);
+/* Work-aware meta-partitioning (NOT the reference's policy, which stays the parity mode):
+ * the same metatree and sub-metatrees, with the p workers split into groups that each
+ * replicate a set of sub-metatrees so the busiest worker's share of the sampled work is
+ * smallest. work: the sampled work of every sub-metatree, optionally followed by its learnable
+ * leaf rows per batch (both from hg_sub_work; rows weigh the replicas' gradient merge).
+ * Same bundle as hg_meta_partition. */
+hg_bundle* hg_meta_partition_work_aware(const hg_graph* g, int k, int p, const double* work, int n_work);
+/* sampled work per sub-metatree: mean sampled edges per batch of a device sampler restricted
+ * to the sub's relations, over n_batches make_batches(batch_size, seed) batches ("work" f64),
+ * and its learnable layer-0 rows per batch ("learn_rows" f64) */
+hg_bundle* hg_sub_work(const hg_graph* g, const int* fanouts, int k, int n_batches, int batch_size, uint64_t seed,
+                       int device);
 /* make_batches (src/harness.cpp:327-340): batch{i} arrays */
 hg_bundle* hg_make_batches(const hg_graph* g, int batch_size, int max_batches, uint64_t seed);
 uint64_t hg_mix_seed(uint64_t a, uint64_t b); /* src/sampling.cpp:9-15 */
@@ -143,6 +155,8 @@ typedef struct {
 } hg_step_report;
 
 hg_engine* hg_engine_create(const hg_graph* g, const hg_engine_opts* opts);
+/* An engine of the work-aware plan (hg_meta_partition_work_aware) instead of the reference's */
+hg_engine* hg_engine_create_work_aware(const hg_graph* g, const hg_engine_opts* opts, const double* work, int n_work);
 /* Sampler-only engine for sample_khop (hop_rel_flat == NULL: every relation at
  * every hop; src/sampling.cpp:94-97) and sample_khop_restricted (per-hop allowed
  * relation lists, concatenated, hop_rel_counts[h] entries each; sampling.cpp:99-103).

@@ -105,6 +105,9 @@ def lib():
             "hg_engine_replica_handle": ([vp, vp, i32], i32),
             "hg_engine_attach_replicas": ([vp, vp, i32, i32], i32),
             "hg_init_model": ([vp, i32, i32, u64], vp),
+            "hg_meta_partition_work_aware": ([vp, i32, i32, vp, i32], vp),
+            "hg_sub_work": ([vp, vp, i32, i32, i32, u64, i32], vp),
+            "hg_engine_create_work_aware": ([vp, C.POINTER(EngineOpts), vp, i32], vp),
             "hg_init_learnable": ([vp, u64], vp),
             "hg_engine_load_weights": ([vp, i32, i32, vp, i32, i32], i32),
             "hg_engine_load_table_rows": ([vp, i32, vp, C.c_int64, vp, i32], i32),

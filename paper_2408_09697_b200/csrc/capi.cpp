@@ -76,6 +76,31 @@ R guard(R fail, F&& f) {
 
 std::vector<int> ivec(const int* p, int n) { return p ? std::vector<int>(p, p + n) : std::vector<int>{}; }
 
+// work: n_subs sampled-work values, optionally followed by n_subs learnable-row counts
+Plan work_aware_plan(const Graph& g, int k, int p, const double* work, int n_work) {
+  const Schema sch = schema_of(g);
+  const int n_subs = static_cast<int>(meta_partition(sch, g.target, k, 1).subs.size());
+  std::vector<double> w(work, work + std::min(n_work, n_subs)), l;
+  if (n_work == 2 * n_subs) l.assign(work + n_subs, work + n_work);
+  return work_aware_partition(sch, g.target, k, p, w, l);
+}
+
+EngineOptions engine_options(const hg_engine_opts& o) {
+  EngineOptions eo;
+  eo.k = o.k;
+  eo.fanouts = ivec(o.fanouts, o.k);
+  eo.hidden = o.hidden;
+  eo.batch_cap = o.batch_cap;
+  eo.p = o.p;
+  eo.rank = o.rank;
+  eo.model_seed = o.model_seed;
+  eo.learn_seed = o.learn_seed;
+  eo.device = o.device;
+  eo.feat_dtype = o.feat_dtype;
+  eo.feat_host = o.feat_host;
+  return eo;
+}
+
 }  // namespace
 
 extern "C" {
@@ -264,10 +289,9 @@ hg_bundle* hg_graph_export(const hg_graph* h) {
 }
 
 // ---- planning ------------------------------------------------------------------------------
-hg_bundle* hg_meta_partition(const hg_graph* h, int k, int p) {
-  return guard<hg_bundle*>(nullptr, [&] {
-    const Graph& g = h->g;
-    const Plan plan = meta_partition(schema_of(g), g.target, k, p);
+namespace {
+hg_bundle* plan_bundle(const Graph& g, const Plan& plan, int k) {
+  {
     auto* b = new hg_bundle;
     std::vector<int> ty, de, pa, re;
     for (const auto& ps : plan.tree.pos) {
@@ -318,6 +342,71 @@ hg_bundle* hg_meta_partition(const hg_graph* h, int k, int p) {
     }
     b->add("raf.leaf_owners", "<i4", leaf_rows);
     return b;
+  }
+}
+}  // namespace
+
+hg_bundle* hg_meta_partition(const hg_graph* h, int k, int p) {
+  return guard<hg_bundle*>(nullptr, [&] {
+    const Graph& g = h->g;
+    return plan_bundle(g, meta_partition(schema_of(g), g.target, k, p), k);
+  });
+}
+
+hg_bundle* hg_meta_partition_work_aware(const hg_graph* h, int k, int p, const double* work, int n_work) {
+  return guard<hg_bundle*>(nullptr, [&] {
+    const Graph& g = h->g;
+    return plan_bundle(g, work_aware_plan(g, k, p, work, n_work), k);
+  });
+}
+
+// sampled work of every sub-metatree: mean sampled edges per batch of a sampler restricted
+// to the sub's relations at each hop, over n_batches make_batches batches
+hg_bundle* hg_sub_work(const hg_graph* h, const int* fanouts, int k, int n_batches, int batch_size, uint64_t seed,
+                       int device) {
+  return guard<hg_bundle*>(nullptr, [&] {
+    const Graph& g = h->g;
+    if (k < 1 || !fanouts) throw std::invalid_argument("fanouts must be non-empty");
+    const Plan plan = meta_partition(schema_of(g), g.target, k, 1);
+    const auto batches = make_batches(g, batch_size, n_batches, seed);
+    std::vector<double> work, learn;
+    for (const SubTree& st : plan.subs) {
+      EngineOptions eo;
+      eo.k = k;
+      eo.fanouts = ivec(fanouts, k);
+      eo.batch_cap = batch_size;
+      eo.device = device;
+      eo.sample_only = true;
+      eo.hop_relations.assign(k, {});
+      for (int pos : st.positions) {
+        const TreePos& tp = plan.tree.pos[pos];
+        if (tp.rel >= 0 && tp.depth >= 1 && tp.depth <= k) eo.hop_relations[tp.depth - 1].push_back(tp.rel);
+      }
+      Engine e(g, eo);
+      double edges = 0, rows = 0;
+      for (std::size_t i = 0; i < batches.size(); ++i) {
+        e.sample_only(batches[i].data(), static_cast<int>(batches[i].size()), mix_seed(seed, 0xb000 + i));
+        edges += static_cast<double>(e.sampled_edges());
+        rows += static_cast<double>(e.learnable_leaf_rows());
+      }
+      const double nb = std::max<double>(1.0, static_cast<double>(batches.size()));
+      work.push_back(edges / nb);
+      learn.push_back(rows / nb);
+    }
+    auto* b = new hg_bundle;
+    b->add("work", "<f8", work);
+    b->add("learn_rows", "<f8", learn);
+    return b;
+  });
+}
+
+hg_engine* hg_engine_create_work_aware(const hg_graph* g, const hg_engine_opts* o, const double* work, int n_work) {
+  return guard<hg_engine*>(nullptr, [&] {
+    EngineOptions eo = engine_options(*o);
+    eo.sub_work.assign(work, work + n_work);
+    auto* h = new hg_engine;
+    h->e = std::make_unique<Engine>(g->g, eo);
+    return h;
   });
 }
 
@@ -333,18 +422,7 @@ hg_bundle* hg_make_batches(const hg_graph* h, int batch_size, int max_batches, u
 // ---- engine --------------------------------------------------------------------------------
 hg_engine* hg_engine_create(const hg_graph* g, const hg_engine_opts* o) {
   return guard<hg_engine*>(nullptr, [&] {
-    EngineOptions eo;
-    eo.k = o->k;
-    eo.fanouts = ivec(o->fanouts, o->k);
-    eo.hidden = o->hidden;
-    eo.batch_cap = o->batch_cap;
-    eo.p = o->p;
-    eo.rank = o->rank;
-    eo.model_seed = o->model_seed;
-    eo.learn_seed = o->learn_seed;
-    eo.device = o->device;
-    eo.feat_dtype = o->feat_dtype;
-    eo.feat_host = o->feat_host;
+    const EngineOptions eo = engine_options(*o);
     auto* h = new hg_engine;
     h->e = std::make_unique<Engine>(g->g, eo);
     return h;

@@ -176,7 +176,10 @@ Engine::Engine(const Graph& g, const EngineOptions& o) : o_(o) {
   ntypes_ = g.num_types();
   target_ = g.target;
   num_classes_ = g.num_classes;
-  for (const auto& t : g.types) type_counts_.push_back(t.count);
+  for (const auto& t : g.types) {
+    type_counts_.push_back(t.count);
+    learnable_type_.push_back(t.storage == Storage::Learnable);
+  }
   for (const auto& r : g.rels) {
     rel_src_.push_back(r.src_type);
     rel_dst_.push_back(r.dst_type);
@@ -248,7 +251,15 @@ void Engine::build_plan(const Graph& g) {
     tree_ = bfs_tree(sch, target_, k);
     acct_ = raf_accounting(g, tree_, std::vector<std::vector<int>>(tree_.pos.at(0).children.size(), {0}), 1);
   } else {
-    const Plan plan = meta_partition(sch, target_, k, o_.p);
+    Plan plan;
+    if (o_.sub_work.empty()) {
+      plan = meta_partition(sch, target_, k, o_.p);
+    } else {  // [work per sub] or [work per sub, learnable rows per sub]
+      const std::size_t n_subs = meta_partition(sch, target_, k, 1).subs.size();
+      std::vector<double> w(o_.sub_work.begin(), o_.sub_work.begin() + std::min(n_subs, o_.sub_work.size())), l;
+      if (o_.sub_work.size() == 2 * n_subs) l.assign(o_.sub_work.begin() + n_subs, o_.sub_work.end());
+      plan = work_aware_partition(sch, target_, k, o_.p, w, l);
+    }
     acct_ = plan_accounting(g, plan);  // run_experiment's view: raf_view_from_plan
     const Part& part = plan.parts.at(o_.rank);
     // replica group: the partitions owning exactly this sub-metatree set

@@ -45,6 +45,9 @@ struct EngineOptions {
   // PCIe, zero-copy) with an HBM cache of the rows set_cache() installs
   int feat_dtype = 0;
   int feat_host = 0;
+  // non-empty: the work-aware plan (work_aware_partition, one value per sub-metatree)
+  // instead of the reference's meta_partition; the numbers are the flat pass's either way
+  std::vector<double> sub_work;
   // sampler-only engines (sample_khop / sample_khop_restricted, sampling.cpp:94-103):
   // explicit per-hop relation sets replace the metatree's; no model state is built
   bool sample_only = false;
@@ -213,6 +216,25 @@ class Engine {
   const std::vector<std::vector<int>>& hop_rels() const { return hop_rels_; }
   int model_step() const { return static_cast<int>(model_step_); }
   int batch_cap() const { return o_.batch_cap; }
+  // rows of the last sample's layer-0 (hop k) frontier over the learnable types
+  std::uint64_t learnable_leaf_rows() {
+    HG_CUDA(cudaStreamSynchronize(st_));
+    std::uint64_t n = 0;
+    for (int t = 0; t < ntypes_; ++t) {
+      if (!learnable_type_[t] || !front(o_.k, t).count) continue;
+      int v = 0;
+      HG_CUDA(cudaMemcpy(&v, front(o_.k, t).count, sizeof(int), cudaMemcpyDeviceToHost));
+      n += static_cast<std::uint64_t>(v);
+    }
+    return n;
+  }
+  // sampled edges of the last sample_only / step (all hops, this partition)
+  std::uint64_t sampled_edges() {
+    HG_CUDA(cudaStreamSynchronize(st_));
+    std::uint64_t v = 0;
+    HG_CUDA(cudaMemcpy(&v, edges_dev_, sizeof(v), cudaMemcpyDeviceToHost));
+    return v;
+  }
 
  private:
   struct BlockBuf {
@@ -291,6 +313,7 @@ class Engine {
   std::vector<std::vector<int>> hop_rels_;
   int ntypes_ = 0, target_ = 0, num_classes_ = 0;
   std::vector<std::uint64_t> type_counts_;
+  std::vector<bool> learnable_type_;  // Storage::Learnable per node type
   std::vector<int> rel_src_, rel_dst_;
   bool replica_ = false;
   int shard_index_ = 0, shard_count_ = 1;

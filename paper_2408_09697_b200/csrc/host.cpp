@@ -544,6 +544,97 @@ Plan meta_partition(const Schema& s, int root, int k, int p) {
   return plan;
 }
 
+// Work-aware meta-partitioning (not the reference's policy; the reference plan stays
+// the parity mode). The same metatree and sub-metatrees as meta_partition, but the p
+// workers are split into groups that each replicate a set of sub-metatrees, chosen to
+// minimise the busiest worker's cost. A group g of r_g workers splits the batch
+// (raf.cpp:390-391): each worker samples and trains sum(work[S_g]) / r_g; replicas also
+// merge their learnable-row gradients every step (the union of the replicas' rows gets
+// one summed Adam update, raf.cpp:496-510), which costs ~merge_cost x learn_rows[S_g]
+// (a row's w, m, v read-modify-write ~ that many sampled edges' gather bytes). Every set
+// partition of the subs and every split of p over its blocks is scored (the bundled
+// schemas' metatrees have <= 6 subs); ties go to fewer groups.
+Plan work_aware_partition(const Schema& s, int root, int k, int p, const std::vector<double>& work,
+                          const std::vector<double>& learn_rows, double merge_cost) {
+  Plan plan;
+  plan.p = p;
+  plan.tree = bfs_tree(s, root, k);
+  if (plan.tree.pos.empty()) throw std::invalid_argument("empty metatree");
+  plan.subs = split(plan.tree, s);
+  const int n = static_cast<int>(plan.subs.size());
+  if (static_cast<int>(work.size()) != n || (!learn_rows.empty() && static_cast<int>(learn_rows.size()) != n))
+    throw std::invalid_argument("work-aware plan: one work value per sub-metatree expected (" + std::to_string(n) + ")");
+  if (n > 8) throw std::invalid_argument("work-aware plan: more than 8 sub-metatrees");
+  if (p < 1) throw std::invalid_argument("p must be >= 1");
+  double best = -1.0;
+  std::vector<std::vector<int>> best_groups;
+  std::vector<int> best_r;
+  std::vector<int> label(n, 0);  // restricted-growth string: subs -> group
+  std::function<void(int, int)> each_partition = [&](int i, int ng) {
+    if (i == n) {
+      if (ng > p) return;
+      std::vector<std::vector<int>> groups(ng);
+      std::vector<double> w(ng, 0.0), m(ng, 0.0);
+      for (int q = 0; q < n; ++q) {
+        groups[label[q]].push_back(q);
+        w[label[q]] += work[q];
+        m[label[q]] += learn_rows.empty() ? 0.0 : merge_cost * learn_rows[q];
+      }
+      auto cost = [&](int g, int r) { return w[g] / r + (r > 1 ? m[g] : 0.0); };
+      // every extra worker goes to the group whose cost it lowers the most, while any does
+      std::vector<int> r(ng, 1);
+      for (int extra = p - ng; extra > 0; --extra) {
+        int arg = -1;
+        double gain = 0.0;
+        for (int g = 0; g < ng; ++g) {
+          const double d = cost(g, r[g]) - cost(g, r[g] + 1);
+          if (d > gain) {
+            gain = d;
+            arg = g;
+          }
+        }
+        if (arg < 0) {  // no worker lowers a cost: the one that raises it least
+          double least = 0.0;
+          for (int g = 0; g < ng; ++g) {
+            const double d = cost(g, r[g] + 1) - cost(g, r[g]);
+            if (arg < 0 || d < least) {
+              least = d;
+              arg = g;
+            }
+          }
+        }
+        ++r[arg];
+      }
+      double worst = 0.0;
+      for (int g = 0; g < ng; ++g) worst = std::max(worst, cost(g, r[g]));
+      if (best < 0 || worst < best * (1.0 - 1e-12) ||
+          (std::abs(worst - best) <= 1e-12 * best && groups.size() < best_groups.size())) {
+        best = worst;
+        best_groups = groups;
+        best_r = r;
+      }
+      return;
+    }
+    for (int g = 0; g <= ng && g < p; ++g) {
+      label[i] = g;
+      each_partition(i + 1, std::max(ng, g + 1));
+    }
+  };
+  if (n > 0) each_partition(0, 0);
+  for (std::size_t g = 0; g < best_groups.size(); ++g)
+    for (int q = 0; q < best_r[g]; ++q) {
+      Part part;
+      part.sub_ids = best_groups[g];
+      part.replica = best_r[g] > 1;
+      part.replica_index = q;
+      part.replica_count = best_r[g];
+      plan.parts.push_back(part);
+    }
+  for (auto& part : plan.parts) dedup_part(part, plan);
+  plan.deduplicated = true;
+  return plan;
+}
+
 std::vector<int> cacheable_types(const Plan& plan, int part) {
   const Tree& t = plan.tree;
   std::vector<int> leaves, kept;

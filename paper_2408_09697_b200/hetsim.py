@@ -231,6 +231,21 @@ def init_learnable(g: HetGraph, seed: int) -> Dict[str, np.ndarray]:
     return N.take(N.lib().hg_init_learnable(g.handle, seed))
 
 
+def meta_partition_work_aware(g: HetGraph, k: int, p: int, work: Sequence[float]) -> Dict[str, np.ndarray]:
+    """Work-aware plan (not the reference's policy): worker groups replicate sets of
+    sub-metatrees so the busiest worker's share of `work` is smallest."""
+    w = np.ascontiguousarray(work, dtype=np.float64)
+    return N.take(N.lib().hg_meta_partition_work_aware(g.handle, k, p, N.ptr(w), len(w)))
+
+
+def sub_work(g: HetGraph, fanouts: Sequence[int], n_batches: int = 4, batch_size: int = 1024, seed: int = 1,
+             device: int = 0) -> Dict[str, np.ndarray]:
+    """Per sub-metatree: sampled edges ("work") and learnable layer-0 rows ("learn_rows") per
+    batch, from device samplers restricted to the sub's relations."""
+    fo = np.asarray(fanouts, np.int32)
+    return N.take(N.lib().hg_sub_work(g.handle, N.ptr(fo), len(fo), n_batches, batch_size, seed, device))
+
+
 def make_batches(g: HetGraph, batch_size: int, max_batches: int, seed: int) -> List[np.ndarray]:
     """make_batches (src/harness.cpp:327-340)."""
     b = N.take(N.lib().hg_make_batches(g.handle, batch_size, max_batches, seed))
@@ -254,7 +269,7 @@ class Engine:
 
     def __init__(self, g: HetGraph, fanouts: Sequence[int], hidden: int = 64, batch_cap: int = 1024, p: int = 1,
                  rank: int = 0, model_seed: int = 0, learn_seed: int = 0, device: int = 0, feat_dtype: str = "f32",
-                 feat_host: bool = False):
+                 feat_host: bool = False, sub_work: Optional[Sequence[float]] = None):
         fo = (C.c_int * len(fanouts))(*[int(f) for f in fanouts])
         self._fo = fo
         if feat_dtype not in self.FEAT_DTYPES:
@@ -263,7 +278,11 @@ class Engine:
                             self.FEAT_DTYPES[feat_dtype], int(bool(feat_host)))
         self.k = len(fanouts)
         self.graph = g  # keep alive
-        self._h = N.lib().hg_engine_create(g.handle, C.byref(opts))
+        if sub_work is None:
+            self._h = N.lib().hg_engine_create(g.handle, C.byref(opts))
+        else:  # the work-aware plan (not the reference's meta_partition)
+            w = np.ascontiguousarray(sub_work, dtype=np.float64)
+            self._h = N.lib().hg_engine_create_work_aware(g.handle, C.byref(opts), N.ptr(w), len(w))
         if not self._h:
             N.raise_last()
 

@@ -23,7 +23,12 @@ def main():
     else:
         spec = H.bundled_spec(name)
     g = H.gen_synthetic(spec, seed)
-    eng = H.Engine.for_experiment(g, [25, 20], 32, seed, batch_cap=bsz, p=p, rank=rank, device=rank)
+    kw = {}
+    if os.environ.get("HG_PLAN_WORK", "0") != "0":  # the work-aware plan (not the reference's)
+        import numpy as _np
+        sw = H.sub_work(g, [25, 20], 4, bsz, seed, device=rank)
+        kw["sub_work"] = _np.concatenate([sw["work"], sw["learn_rows"]])
+    eng = H.Engine.for_experiment(g, [25, 20], 32, seed, batch_cap=bsz, p=p, rank=rank, device=rank, **kw)
     if rank == 0:
         uid = H.nccl_unique_id()
         with open(id_path + ".tmp", "wb") as f:

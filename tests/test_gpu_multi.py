@@ -114,3 +114,45 @@ def test_raf_multi_gpu_matches_reference(ref, name, p, shard):
         assert int(res[r]["cut_edges"][0]) == int(want["boundary_cut_edges"][0])
         assert np.array_equal(res[r]["bound_ok"], want["message_bound_ok"].astype(res[r]["bound_ok"].dtype))
         assert np.array_equal(res[r]["target_ok"], want["target_only_ok"].astype(res[r]["target_ok"].dtype))
+
+
+@pytest.mark.parametrize("name,p", [("mag-mini", 2), ("mag-mini", 4), ("igb-mini", 3)])
+def test_work_aware_plan_matches_flat_reference(ref, name, p):
+    # the work-aware plan (worker groups replicating sub-metatree sets, sized by the
+    # measured sampled work and learnable rows) computes the flat pass's numbers: the
+    # per-batch losses and the final parameters of the reference's p = 1 run
+    if n_gpus() < p:
+        pytest.skip(f"needs {p} GPUs")
+    seed, n_batches, bsz = 5, 6, 64
+    with tempfile.TemporaryDirectory() as td:
+        idp = os.path.join(td, "nccl.id")
+        procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "mp", "raf_rank.py"), name, str(seed), str(p),
+                                   str(r), idp, os.path.join(td, f"r{r}.npz"), str(n_batches), str(bsz)],
+                                  stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True,
+                                  env=dict(os.environ, HG_PLAN_WORK="1")) for r in range(p)]
+        outs = [pr.communicate(timeout=300)[0] for pr in procs]
+        for pr, o in zip(procs, outs):
+            assert pr.returncode == 0, o[-3000:]
+        res = [np.load(os.path.join(td, f"r{r}.npz")) for r in range(p)]
+    from paper_2408_09697_b200 import hetsim as H
+    from tests.util import assert_adam_close
+    g = H.gen_synthetic(H.bundled_spec(name), seed)
+    batches = H.make_batches(g, bsz, n_batches, H.mix_seed(seed, 0xBA7C))
+    want = ref.RefGraph.bundled(name, seed).raf_train(2, 32, 1, seed, [list(b) for b in batches], [25, 20])
+    for r in range(p):
+        np.testing.assert_allclose(res[r]["losses"], want["losses"], rtol=1e-3, atol=0)
+    seen = {}
+    for r in range(p):
+        for key in res[r].files:
+            if not key.startswith("T:"):
+                continue
+            n, v = key[2:], res[r][key]
+            if n in seen:
+                assert np.array_equal(seen[n], v), f"replicas disagree on {n}"
+            seen[n] = v
+            if n.startswith("post.r"):
+                assert_adam_close(v, want["final." + n[len("post."):]], None, max_flip_frac=1e-2, steps=n_batches,
+                                  what=f"rank {r}: {n}")
+            elif n.startswith("post.learn.t"):
+                assert_adam_close(v, want["final.learn.t" + n.split(".t")[-1]], None, max_flip_frac=1e-2,
+                                  steps=n_batches, what=f"rank {r}: {n}")

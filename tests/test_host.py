@@ -213,3 +213,22 @@ def test_init_model_and_learnable_match_reference(H, ref, name):
         assert np.array_equal(model["w." + n[len("init."):]], want[n]), n
     for n in [x for x in want if x.startswith("init.learn.t")]:
         assert np.array_equal(learn["learn.t" + n.split(".t")[-1]], want[n]), n
+
+
+def test_work_aware_plan_groups(H):
+    # the work-aware plan (not the reference's policy) on the ogbn-mag schema with the
+    # per-sub sampled edges of SURVEY §8(e) (S0 92k, S1 213k, S2 200k) and learnable leaf
+    # rows (S0 institution ~6k, S1 author + field ~118k, S2 none): the sub with the big
+    # learnable merge stays unreplicated, the others are replicated together
+    g = H.gen_synthetic(H.bundled_spec("mag-mini"), 5)  # the same 3-sub metatree shape
+    w = [92.0e3, 213.3e3, 200.2e3, 5.6e3, 118e3, 0.0]
+    groups = lambda plan, p: [tuple(int(x) for x in plan[f"part{i}.sub_ids"]) for i in range(p)]
+    assert groups(H.meta_partition_work_aware(g, 2, 4, w), 4) == [(0, 2), (0, 2), (0, 2), (1,)]
+    plan = H.meta_partition_work_aware(g, 2, 4, w)
+    assert [list(plan[f"part{i}.replica"]) for i in range(4)] == [[1, 0, 3], [1, 1, 3], [1, 2, 3], [0, 0, 1]]
+    # without the merge term the objective alone replicates everything (pure data parallel)
+    assert groups(H.meta_partition_work_aware(g, 2, 2, w[:3]), 2) == [(0, 1, 2), (0, 1, 2)]
+    # p = 1: one group with every sub
+    assert groups(H.meta_partition_work_aware(g, 2, 1, w), 1) == [(0, 1, 2)]
+    with pytest.raises(ValueError):
+        H.meta_partition_work_aware(g, 2, 2, [1.0, 2.0])
