@@ -212,12 +212,12 @@ hg_bundle* hg_selftest_contractions(const int* cases, int n_cases, int device);
 int hg_engine_count_launches(hg_engine* e, int n, int train);
 
 /* ---- cache (src/cache.cpp) -------------------------------------------------------------- */
-/* presample_hotness (src/cache.cpp:39-63) on the device: hot.t{t} u32 counts */
+/* presample_hotness (src/cache.cpp:39-63) on the device: hot.t{t} u64 counts */
 hg_bundle* hg_engine_presample_hotness(hg_engine* e, int epochs, uint64_t seed, int batch_size);
 /* profile_miss_penalty + allocate_cache + fill_and_serve (src/cache.cpp:11-141):
  * counts are the hot.t{t} arrays concatenated in type order. Names: profile.*,
  * alloc.bytes, alloc.capacity, cached.t{t} (sorted). */
-hg_bundle* hg_cache_plan(const hg_graph* g, const uint32_t* counts, uint64_t budget, double read_ns,
+hg_bundle* hg_cache_plan(const hg_graph* g, const uint64_t* counts, uint64_t budget, double read_ns,
                          double write_ns, double overhead_ns, int elem_bytes);
 /* Install the cached sets (concatenated sorted ids, per-type lengths) for the
  * per-batch lookup/update accounting (CacheState::lookup/update, cache.cpp:87-113;
@@ -287,7 +287,7 @@ int hg_rows_in(hg_ctx* c, const uint32_t* ids, int64_t n, const uint32_t* sorted
 int hg_mean_aggregate(hg_ctx* c, const uint32_t* indptr, int64_t n_dst, const uint32_t* src_rows, hg_tensor h_src,
                       hg_tensor out);
 /* agg_relation + agg_all (src/hgnn.cpp:189-203): out (+)= sum_r means[r] . ws[r], ReLU
- * optional (src/hgnn.cpp:271-272); 1-8 relations; tcgen05 kind::tf32 3xTF32 */
+ * optional (src/hgnn.cpp:271-272); 1-16 relations; tcgen05 kind::tf32 3xTF32 */
 int hg_project(hg_ctx* c, const hg_tensor* means, const hg_tensor* ws, int nrel, hg_tensor out, int relu,
                int accumulate);
 /* agg_all (src/hgnn.cpp:194-203): ordered elementwise sum of 1..32 partials */

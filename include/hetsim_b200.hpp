@@ -679,10 +679,10 @@ class RafEngine {
   // device tensors by name (hetgpu.h hg_engine_read), widened like the reference's Matrix
   detail::Bundle read(const std::string& names) { return detail::Bundle(hg_engine_read(e_.get(), names.c_str())); }
   // presample_hotness (cache.cpp:39-63): per type, visit counts over `epochs` id-ordered passes
-  std::vector<std::vector<std::uint32_t>> presample_hotness(int epochs, std::uint64_t seed, int batch_size = 512) {
+  std::vector<std::vector<std::uint64_t>> presample_hotness(int epochs, std::uint64_t seed, int batch_size = 512) {
     const detail::Bundle b(hg_engine_presample_hotness(e_.get(), epochs, seed, batch_size));
-    std::vector<std::vector<std::uint32_t>> out;
-    for (std::size_t t = 0; t < g_.node_counts.size(); ++t) out.push_back(b.get<std::uint32_t>("hot.t" + std::to_string(t)));
+    std::vector<std::vector<std::uint64_t>> out;
+    for (std::size_t t = 0; t < g_.node_counts.size(); ++t) out.push_back(b.get<std::uint64_t>("hot.t" + std::to_string(t)));
     return out;
   }
   // multi-GPU AGG_all: every rank attaches the same NCCL id (hg_nccl_unique_id on rank 0)
@@ -1049,18 +1049,18 @@ inline std::pair<Matrix, ForwardTape> forward_flat(const HetGraph& g, const Meta
         }
       }
       // out = sum_r mean_r . W_r (ascending relations), ReLU between layers: one tcgen05
-      // launch per 8 relations
-      for (std::size_t q0 = 0; q0 < means.size(); q0 += 8) {
+      // launch per 16 relations
+      for (std::size_t q0 = 0; q0 < means.size(); q0 += 16) {
         std::vector<hg_tensor> mt, wt;
-        for (std::size_t q = q0; q < std::min(means.size(), q0 + 8); ++q) {
+        for (std::size_t q = q0; q < std::min(means.size(), q0 + 16); ++q) {
           mt.push_back(means[q].t);
           wt.push_back(ws[q].t);
         }
-        const bool last = q0 + 8 >= means.size();
+        const bool last = q0 + 16 >= means.size();
         detail::check(hg_project(detail::ctx(), mt.data(), wt.data(), static_cast<int>(mt.size()), out.t,
                                  (l < k && last && q0 == 0) ? 1 : 0, q0 > 0 ? 1 : 0));
       }
-      if (l < k && means.size() > 8) detail::check(hg_relu(detail::ctx(), out.t, nullptr));
+      if (l < k && means.size() > 16) detail::check(hg_relu(detail::ctx(), out.t, nullptr));
       detail::check(hg_ctx_sync(detail::ctx()));
       tape.H[d - 1].emplace(t, detail::dev_download(out.t));
       Hd[d - 1].emplace(t, std::move(out));
@@ -1561,7 +1561,7 @@ struct MissPenaltyProfile {
 inline MissPenaltyProfile profile_miss_penalty(const HetGraph& g, const CostModel& cm) {
   std::uint64_t total = 0;
   for (auto c : g.node_counts) total += c;
-  const std::vector<std::uint32_t> zeros(std::max<std::uint64_t>(1, total), 0u);
+  const std::vector<std::uint64_t> zeros(std::max<std::uint64_t>(1, total), 0u);
   const detail::Bundle b(hg_cache_plan(g.handle(), zeros.data(), 0, cm.read_ns_per_byte, cm.write_ns_per_byte,
                                        cm.fixed_overhead_ns, cm.elem_bytes));
   const auto ratio = b.get<double>("profile.ratio"), tns = b.get<double>("profile.transfer_ns");
@@ -1588,7 +1588,7 @@ inline HotnessTable presample_hotness(const HetGraph& g, const Metatree& tree, c
   const detail::Bundle b(hg_engine_presample_hotness(s.handle(), epochs, seed, static_cast<int>(batch_size)));
   HotnessTable hot;
   for (std::size_t t = 0; t < g.node_counts.size(); ++t) {
-    const auto c = b.get<std::uint32_t>("hot.t" + std::to_string(t));
+    const auto c = b.get<std::uint64_t>("hot.t" + std::to_string(t));
     hot.counts.emplace_back(c.begin(), c.end());
   }
   return hot;

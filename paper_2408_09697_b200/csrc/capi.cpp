@@ -691,12 +691,12 @@ hg_bundle* hg_engine_presample_hotness(hg_engine* e, int epochs, uint64_t seed, 
   return guard<hg_bundle*>(nullptr, [&] {
     const auto counts = e->e->presample_hotness(epochs, seed, batch_size);
     auto* b = new hg_bundle;
-    for (std::size_t t = 0; t < counts.size(); ++t) b->add("hot.t" + std::to_string(t), "<u4", counts[t]);
+    for (std::size_t t = 0; t < counts.size(); ++t) b->add("hot.t" + std::to_string(t), "<u8", counts[t]);
     return b;
   });
 }
 
-hg_bundle* hg_cache_plan(const hg_graph* h, const uint32_t* counts, uint64_t budget, double read_ns, double write_ns,
+hg_bundle* hg_cache_plan(const hg_graph* h, const uint64_t* counts, uint64_t budget, double read_ns, double write_ns,
                          double overhead_ns, int elem_bytes) {
   return guard<hg_bundle*>(nullptr, [&] {
     const Graph& g = h->g;

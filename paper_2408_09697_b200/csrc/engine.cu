@@ -1018,15 +1018,19 @@ void Engine::run_forward() {
       m.ld_mean = b.ld_mean;
     }
     timed(top ? "aggregate_top" : "aggregate", bytes, [&] { gather_mean(mb, st_); });
-    // (2) per-relation projection summed over the relations into each type (agg_all)
-    ProjBatch pb{};
+    // (2) per-relation projection summed over the relations into each type (agg_all):
+    // one launch per kProjGroups destination types
+    std::vector<ProjBatch> pbs(1);
     for (const auto& gr : groups_) {
       if (gr.layer != l) continue;
       if (gr.blocks.empty()) {
         if (!top) zero_rows(gr.out, gr.ld, front(gr.depth - 1, gr.type).count, gr.rows_cap, st_);
         continue;
       }
-      if (pb.ng >= 4 || gr.blocks.size() > 8) throw std::runtime_error("projection batch too large");
+      if (gr.blocks.size() > static_cast<std::size_t>(kProjRels))
+        throw std::runtime_error("more relations into one type than a projection group holds");
+      if (pbs.back().ng == kProjGroups) pbs.emplace_back();
+      ProjBatch& pb = pbs.back();
       ProjGroup& pg = pb.g[pb.ng++];
       pg.nrel = static_cast<int>(gr.blocks.size());
       pg.n_rows = (top && replica_) ? shard_count_dev_ : front(gr.depth - 1, gr.type).count;
@@ -1043,7 +1047,9 @@ void Engine::run_forward() {
         pg.r[q] = {b.mean, b.ld_mean, b.din, s.w, s.ld};
       }
     }
-    timed(top ? "project_top" : "project", 0, [&] { use_umma_ ? project_umma(pb, st_) : project_tiles(pb, st_); });
+    timed(top ? "project_top" : "project", 0, [&] {
+      for (auto& pb : pbs) use_umma_ ? project_umma(pb, st_) : project_tiles(pb, st_);
+    });
   }
   // AGG_all: sum the partial logits of every partition (raf.cpp:427-446)
   if (o_.p > 1) {
@@ -1677,17 +1683,18 @@ void Engine::quiesce() {
 // per sampled source occurrence. All batch ids and scalars are uploaded once;
 // every batch is one replay of a captured graph (sampling without the transposed
 // views + histogram) on one stream, with no host round trip between batches.
-std::vector<std::vector<std::uint32_t>> Engine::presample_hotness(int epochs, std::uint64_t seed, int batch_size) {
+std::vector<std::vector<std::uint64_t>> Engine::presample_hotness(int epochs, std::uint64_t seed, int batch_size) {
   if (batch_size > o_.batch_cap) throw std::invalid_argument("presample batch larger than the batch capacity");
   if (batch_size <= 0) throw std::invalid_argument("presample batch size must be positive");
   quiesce();
   bind_slot(0);
   if (hot_counts_.empty()) {
     hot_counts_.assign(ntypes_, nullptr);
-    for (int t = 0; t < ntypes_; ++t) hot_counts_[t] = static_cast<std::uint32_t*>(alloc(type_counts_[t] * 4));
+    for (int t = 0; t < ntypes_; ++t)
+      hot_counts_[t] = static_cast<unsigned long long*>(alloc(std::max<std::uint64_t>(1, type_counts_[t]) * 8));
   }
   for (int t = 0; t < ntypes_; ++t)
-    HG_CUDA(cudaMemsetAsync(hot_counts_[t], 0, type_counts_[t] * 4, st_));
+    HG_CUDA(cudaMemsetAsync(hot_counts_[t], 0, type_counts_[t] * 8, st_));
   const std::uint64_t n_target = type_counts_[target_];
   std::vector<NodeId> ids(n_target);
   for (std::uint64_t v = 0; v < n_target; ++v) ids[v] = static_cast<NodeId>(v);
@@ -1752,11 +1759,11 @@ std::vector<std::vector<std::uint32_t>> Engine::presample_hotness(int epochs, st
   cudaFree(d_ids);
   cudaFree(d_sc);
   bind_slot(0);
-  std::vector<std::vector<std::uint32_t>> out(ntypes_);
+  std::vector<std::vector<std::uint64_t>> out(ntypes_);
   for (int t = 0; t < ntypes_; ++t) {
     out[t].resize(type_counts_[t]);
     if (!out[t].empty())
-      HG_CUDA(cudaMemcpy(out[t].data(), hot_counts_[t], out[t].size() * 4, cudaMemcpyDeviceToHost));
+      HG_CUDA(cudaMemcpy(out[t].data(), hot_counts_[t], out[t].size() * 8, cudaMemcpyDeviceToHost));
   }
   return out;
 }

@@ -182,7 +182,7 @@ class Engine {
   std::vector<std::string> tensor_names() const;
 
   // cache: hotness presample over `epochs` id-ordered passes (cache.cpp:39-63)
-  std::vector<std::vector<std::uint32_t>> presample_hotness(int epochs, std::uint64_t seed, int batch_size);
+  std::vector<std::vector<std::uint64_t>> presample_hotness(int epochs, std::uint64_t seed, int batch_size);
   // mark the cached ids per type (sorted lists from fill_and_serve); lookups
   // then run on every step for the layer-0 frontier (harness.cpp:425-437)
   void set_cache(const std::vector<std::vector<NodeId>>& cached);
@@ -327,7 +327,7 @@ class Engine {
   int fork_used_ = 0;
   bool side_open_ = false;  // the side stream has work forked since the last join
   bool presampling_ = false;  // run_sampling for presample_hotness: no transposed views, no cache lookups
-  std::vector<std::uint32_t*> hot_counts_;  // presample_hotness histograms (allocated once)
+  std::vector<unsigned long long*> hot_counts_;  // presample_hotness histograms, u64 (allocated once)
   LbScratch lb2_;  // look-back scratch of the side stream
   bool use_side_ = true;
   cudaStream_t side() const { return (profiling_ || !use_side_) ? st_ : st2_; }

@@ -97,8 +97,10 @@ struct ProjRel {
   const float* w;
   int ld_w;
 };
+constexpr int kProjRels = 16;   // relations into one destination type (concatenated along K)
+constexpr int kProjGroups = 4;  // destination types per projection launch
 struct ProjGroup {
-  ProjRel r[8];
+  ProjRel r[kProjRels];
   int nrel;
   const int* n_rows;
   int rows_cap;
@@ -109,8 +111,8 @@ struct ProjGroup {
   int out_stride, out_offset;
 };
 struct ProjBatch {
-  ProjGroup g[4];
-  int tile_base[5];
+  ProjGroup g[kProjGroups];
+  int tile_base[kProjGroups + 1];
   int ng;
 };
 void project_tiles(ProjBatch& p, cudaStream_t st);

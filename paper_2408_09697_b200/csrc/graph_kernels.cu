@@ -754,19 +754,20 @@ __global__ void k_cache_count(const std::uint32_t* ids, const int* n, const std:
   }
 }
 
+// u64 visit counts, as the reference's HotnessTable (cache.hpp:38-41)
 __global__ void k_hot_add(const std::uint32_t* ids, const std::uint32_t* indptr, const int* n_rows,
-                          std::uint32_t* counts) {
+                          unsigned long long* counts) {
   pdl_enter();
   const std::uint32_t total = indptr[*n_rows];
   for (std::uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x)
-    atomicAdd(counts + ids[e], 1u);
+    atomicAdd(counts + ids[e], 1ull);
 }
 
-__global__ void k_hot_add_list(const std::uint32_t* ids, const int* n, std::uint32_t* counts) {
+__global__ void k_hot_add_list(const std::uint32_t* ids, const int* n, unsigned long long* counts) {
   pdl_enter();
   const int total = *n;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x)
-    atomicAdd(counts + ids[e], 1u);
+    atomicAdd(counts + ids[e], 1ull);
 }
 
 }  // namespace
@@ -778,12 +779,12 @@ void cache_count(const std::uint32_t* ids, const int* n, int cap, const std::uin
 }
 
 void hotness_add(const std::uint32_t* ids, const std::uint32_t* indptr, const int* n_rows, int cap,
-                 std::uint32_t* counts, cudaStream_t st) {
+                 unsigned long long* counts, cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, 256), 4 * num_sms()));
   launch_pdl(k_hot_add, std::max(grid, 1u), 256, 0, st, ids, indptr, n_rows, counts);
 }
 
-void hotness_add_list(const std::uint32_t* ids, const int* n, int cap, std::uint32_t* counts, cudaStream_t st) {
+void hotness_add_list(const std::uint32_t* ids, const int* n, int cap, unsigned long long* counts, cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, 256), 2 * num_sms()));
   launch_pdl(k_hot_add_list, std::max(grid, 1u), 256, 0, st, ids, n, counts);
 }

@@ -301,8 +301,8 @@ void cache_count(const std::uint32_t* ids, const int* n, int cap, const std::uin
                  unsigned long long* hits_misses, cudaStream_t st);
 // histogram for presample_hotness
 void hotness_add(const std::uint32_t* ids, const std::uint32_t* indptr, const int* n_rows, int cap,
-                 std::uint32_t* counts, cudaStream_t st);
-void hotness_add_list(const std::uint32_t* ids, const int* n, int cap, std::uint32_t* counts,
+                 unsigned long long* counts, cudaStream_t st);
+void hotness_add_list(const std::uint32_t* ids, const int* n, int cap, unsigned long long* counts,
                       cudaStream_t st);
 
 }  // namespace hetgpu

@@ -275,7 +275,7 @@ void LayerCtx::mean_aggregate(const std::uint32_t* indptr, std::int64_t n_dst, c
 
 void LayerCtx::project(const DevTensor* means, const DevTensor* ws, int nrel, const DevTensor& out, bool relu,
                        bool accumulate) {
-  if (nrel < 1 || nrel > 8) throw std::invalid_argument("project: 1..8 relations per call");
+  if (nrel < 1 || nrel > kProjRels) throw std::invalid_argument("project: 1..16 relations per call");
   check_tensor(out, "project out");
   for (int r = 0; r < nrel; ++r) {
     check_tensor(means[r], "project mean");

@@ -42,7 +42,7 @@ namespace {
 constexpr int kUT = HG_UMMA_WARPS * 32;  // threads per CTA: 4 or 8 warps (one or two per TMEM lane quadrant)
 constexpr int kConvWarps = HG_UMMA_WARPS - 2;  // warps 2.. form the tf32 residuals
 constexpr int kATile = 128 * 128;  // bytes of one 128 x 32 fp32 operand tile
-constexpr int kMaxMaps = 64;
+constexpr int kMaxMaps = 2 * kProjGroups * kProjRels;  // [A, B] per (group, relation); 128
 
 template <int NT>
 #ifndef HG_PROJ_NT
@@ -86,7 +86,7 @@ struct alignas(64) UmmaArgs {
   int np;
 };
 __host__ __device__ constexpr int map_index(int mode, int p, int r, int which) {
-  return mode == kProject ? (p * 8 + r) * 2 + which : p * 2 + which;
+  return mode == kProject ? (p * kProjRels + r) * 2 + which : p * 2 + which;
 }
 
 __device__ __forceinline__ int find_tile(const int* base, int n, int tile) {

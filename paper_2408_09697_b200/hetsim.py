@@ -255,7 +255,7 @@ def make_batches(g: HetGraph, batch_size: int, max_batches: int, seed: int) -> L
 def cache_plan(g: HetGraph, hot: Dict[str, np.ndarray], n_types: int, budget: int, read_ns=1.0, write_ns=1.0,
                overhead_ns=1000.0, elem_bytes=4) -> Dict[str, np.ndarray]:
     """profile_miss_penalty + allocate_cache + fill_and_serve (src/cache.cpp:11-141)."""
-    counts = np.concatenate([np.asarray(hot[f"hot.t{t}"], np.uint32) for t in range(n_types)])
+    counts = np.concatenate([np.asarray(hot[f"hot.t{t}"], np.uint64) for t in range(n_types)])
     return N.take(N.lib().hg_cache_plan(g.handle, N.ptr(counts), budget, read_ns, write_ns, overhead_ns, elem_bytes))
 
 
