@@ -220,6 +220,9 @@ __global__ void __launch_bounds__(kT) k_dmean_tiles(DMeanBatch b) {
 #define HG_GATHER_BATCH 5
 #endif
 constexpr int kGatherBatch = HG_GATHER_BATCH;  // neighbour rows in flight per lane
+#ifndef HG_GATHER_BATCH_SMALL
+#define HG_GATHER_BATCH_SMALL 13  // small launches: fanout 25 in two round trips
+#endif
 // 4 consecutive fp32 features (columns c..c+3) of row `key` (one 16-byte load); a
 // cached host table reads the HBM copy when the row is cached
 __device__ __forceinline__ float4 load_row4(const MeanBlock& B, std::uint32_t key, int c) {
@@ -272,8 +275,10 @@ __host__ __device__ inline int gather_chunk(int h_dtype) { return h_dtype == kF3
 // instantiation keeps the original register budget (one float4 per neighbour)
 // CACHED: a host-resident table with an HBM cache is in the batch (per-row slot lookup).
 // fp32-only batches (WIDE = false) run the 64-column items with one float4 per neighbour.
-template <bool WIDE, bool CACHED>
-__global__ void __launch_bounds__(256, WIDE ? 4 : 8) k_gather_mean(MeanBatch m) {
+// NB: neighbour rows in flight per lane (kGatherBatch; launches too small to fill the GPU
+// — the top layer's 1024 rows — take more per trip so their few round trips finish sooner)
+template <bool WIDE, bool CACHED, int NB>
+__global__ void __launch_bounds__(256, WIDE || NB > kGatherBatch ? 4 : 8) k_gather_mean(MeanBatch m) {
   pdl_enter();
   const int hl = threadIdx.x & 15;
   const int halves = gridDim.x * (blockDim.x >> 4);
@@ -297,16 +302,16 @@ __global__ void __launch_bounds__(256, WIDE ? 4 : 8) k_gather_mean(MeanBatch m) 
       const std::uint32_t lo = B.indptr[i], hi = B.indptr[i + 1];
       const float* base = B.h + c;
       float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-      // batches of kGatherBatch neighbours (the last one predicated): one key round trip and
+      // batches of NB neighbours (the last one predicated): one key round trip and
       // one row round trip per batch, summed in edge order
-      for (std::uint32_t e = lo; e < hi; e += kGatherBatch) {
-        const std::uint32_t cnt = min(static_cast<std::uint32_t>(kGatherBatch), hi - e);
-        std::uint32_t kk[kGatherBatch];
+      for (std::uint32_t e = lo; e < hi; e += NB) {
+        const std::uint32_t cnt = min(static_cast<std::uint32_t>(NB), hi - e);
+        std::uint32_t kk[NB];
 #pragma unroll
-        for (int q = 0; q < kGatherBatch; ++q) kk[q] = q < cnt ? __ldg(B.keys + e + q) : 0u;
-        float4 v[kGatherBatch];
+        for (int q = 0; q < NB; ++q) kk[q] = q < cnt ? __ldg(B.keys + e + q) : 0u;
+        float4 v[NB];
 #pragma unroll
-        for (int q = 0; q < kGatherBatch; ++q) {
+        for (int q = 0; q < NB; ++q) {
           if (CACHED)
             v[q] = q < cnt ? load_row4(B, kk[q], c) : make_float4(0.f, 0.f, 0.f, 0.f);
           else
@@ -314,7 +319,7 @@ __global__ void __launch_bounds__(256, WIDE ? 4 : 8) k_gather_mean(MeanBatch m) 
                            : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
-        for (int q = 0; q < kGatherBatch; ++q) add4(s, v[q]);
+        for (int q = 0; q < NB; ++q) add4(s, v[q]);
       }
       if (hi > lo) s = scale4(s, 1.0f / static_cast<float>(hi - lo));
       *reinterpret_cast<float4*>(B.mean + static_cast<std::size_t>(i) * B.ld_mean + c) = s;
@@ -335,26 +340,26 @@ __global__ void __launch_bounds__(256, WIDE ? 4 : 8) k_gather_mean(MeanBatch m) 
       }
       const std::uint32_t lo = B.indptr[i], hi = B.indptr[i + 1];
       float4 s = make_float4(0.f, 0.f, 0.f, 0.f), s2 = s;
-      for (std::uint32_t e = lo; e < hi; e += kGatherBatch) {
-        const std::uint32_t cnt = min(static_cast<std::uint32_t>(kGatherBatch), hi - e);
-        std::uint32_t kk[kGatherBatch];
+      for (std::uint32_t e = lo; e < hi; e += NB) {
+        const std::uint32_t cnt = min(static_cast<std::uint32_t>(NB), hi - e);
+        std::uint32_t kk[NB];
 #pragma unroll
-        for (int q = 0; q < kGatherBatch; ++q) kk[q] = q < cnt ? __ldg(B.keys + e + q) : 0u;
+        for (int q = 0; q < NB; ++q) kk[q] = q < cnt ? __ldg(B.keys + e + q) : 0u;
         if (!wide) {
-          float4 v[kGatherBatch];
+          float4 v[NB];
 #pragma unroll
-          for (int q = 0; q < kGatherBatch; ++q) v[q] = q < cnt ? load_row4(B, kk[q], c) : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int q = 0; q < NB; ++q) v[q] = q < cnt ? load_row4(B, kk[q], c) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-          for (int q = 0; q < kGatherBatch; ++q) add4(s, v[q]);
+          for (int q = 0; q < NB; ++q) add4(s, v[q]);
         } else {
-          float4 v[kGatherBatch], w[kGatherBatch];
+          float4 v[NB], w[NB];
 #pragma unroll
-          for (int q = 0; q < kGatherBatch; ++q) {
+          for (int q = 0; q < NB; ++q) {
             v[q] = w[q] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (q < cnt) load_row8(B, kk[q], c, v[q], w[q]);
           }
 #pragma unroll
-          for (int q = 0; q < kGatherBatch; ++q) {
+          for (int q = 0; q < NB; ++q) {
             add4(s, v[q]);
             add4(s2, w[q]);
           }
@@ -444,12 +449,15 @@ void gather_mean(MeanBatch& m, cudaStream_t st) {
     wide = wide || m.b[b].h_dtype != kF32;
     cached = cached || m.b[b].slot != nullptr;
   }
+  const bool small = items <= 8 * 16 * num_sms();  // fewer half-warp items than 8 warps per SM
   if (wide)
-    launch_pdl(k_gather_mean<true, true>, grid, 256, 0, st, m);  // half tables: host or HBM
+    launch_pdl(k_gather_mean<true, true, kGatherBatch>, grid, 256, 0, st, m);  // half tables: host or HBM
   else if (cached)
-    launch_pdl(k_gather_mean<false, true>, grid, 256, 0, st, m);
+    launch_pdl(k_gather_mean<false, true, kGatherBatch>, grid, 256, 0, st, m);
+  else if (small)
+    launch_pdl(k_gather_mean<false, false, HG_GATHER_BATCH_SMALL>, grid, 256, 0, st, m);
   else
-    launch_pdl(k_gather_mean<false, false>, grid, 256, 0, st, m);
+    launch_pdl(k_gather_mean<false, false, kGatherBatch>, grid, 256, 0, st, m);
 }
 
 void project_tiles(ProjBatch& p, cudaStream_t st) {
