@@ -118,6 +118,10 @@ hg_bundle* hg_sub_work(const hg_graph* g, const int* fanouts, int k, int n_batch
 /* make_batches (src/harness.cpp:327-340): batch{i} arrays */
 hg_bundle* hg_make_batches(const hg_graph* g, int batch_size, int max_batches, uint64_t seed);
 uint64_t hg_mix_seed(uint64_t a, uint64_t b); /* src/sampling.cpp:9-15 */
+/* n raw outputs of std::mt19937_64(seed) from output index start on, reached by polynomial
+ * jump-ahead (the feature streams of src/harness.cpp:153-162 are generated in jumped chunks);
+ * returns 0, or -1 with hg_last_error set */
+int hg_mt64_outputs(uint64_t seed, uint64_t start, uint64_t n, uint64_t* out);
 
 /* ---- device engine (one meta-partition per GPU) ---------------------------------------- */
 typedef struct {

@@ -120,6 +120,14 @@ void hg_bundle_free(hg_bundle* b) { delete b; }
 
 uint64_t hg_mix_seed(uint64_t a, uint64_t b) { return mix_seed(a, b); }
 
+int hg_mt64_outputs(uint64_t seed, uint64_t start, uint64_t n, uint64_t* out) {
+  return guard<int>(-1, [&] {
+    std::mt19937_64 e = mt64_jump_engines(seed, {start})[0];
+    for (uint64_t i = 0; i < n; ++i) out[i] = e();
+    return 0;
+  });
+}
+
 // ---- graphs ----------------------------------------------------------------------------
 hg_graph* hg_graph_generate(const hg_spec* spec, uint64_t seed) {
   return guard<hg_graph*>(nullptr, [&] {

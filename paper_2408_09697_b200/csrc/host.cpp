@@ -3,11 +3,13 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <numeric>
 #include <random>
 #include <atomic>
 #include <exception>
 #include <functional>
+#include <memory>
 #include <set>
 #include <thread>
 
@@ -252,15 +254,30 @@ Graph generate(const Spec& spec, std::uint64_t seed) {
           out.emplace_back(static_cast<NodeId>(src_pick(eng)), static_cast<NodeId>(dd));
     }
   });
+  // A feature stream draws one engine output per value (generate_canonical<double, 53>
+  // over 64-bit words); a long one is cut into chunks whose engines are jumped ahead
+  // (mt64_jump_engines), so its values come out on many threads bit-identical to the
+  // serial stream. HG_FEAT_CHUNK (values per chunk) is a test knob.
+  const char* chunk_env = std::getenv("HG_FEAT_CHUNK");
+  const std::uint64_t kFeatChunk = std::max<std::uint64_t>(1, chunk_env ? std::stoull(chunk_env) : 1ULL << 26);
   std::vector<std::vector<float>> dense(spec.node_types.size());
-  for (std::size_t t = 0; t < spec.node_types.size(); ++t)
-    if (spec.node_types[t].storage == Storage::Dense)
-      tasks.emplace_back([&, t] {
-        std::mt19937_64 eng(mix_seed(seed, 0xf0ULL + t));
+  for (std::size_t t = 0; t < spec.node_types.size(); ++t) {
+    if (spec.node_types[t].storage != Storage::Dense) continue;
+    const std::uint64_t n = spec.node_types[t].count * static_cast<std::uint64_t>(spec.node_types[t].dim);
+    dense[t].resize(n);
+    std::vector<std::uint64_t> starts;
+    for (std::uint64_t c = 0; c < n; c += kFeatChunk) starts.push_back(c);
+    auto engines = std::make_shared<std::vector<std::mt19937_64>>(
+        starts.size() > 1 ? mt64_jump_engines(mix_seed(seed, 0xf0ULL + t), starts)
+                          : std::vector<std::mt19937_64>{std::mt19937_64(mix_seed(seed, 0xf0ULL + t))});
+    for (std::size_t c = 0; c < starts.size(); ++c)
+      tasks.emplace_back([&, t, c, n, engines, lo = starts[c]] {
+        std::mt19937_64& eng = (*engines)[c];
         std::uniform_real_distribution<double> u(-1.0, 1.0);
-        dense[t].resize(spec.node_types[t].count * static_cast<std::uint64_t>(spec.node_types[t].dim));
-        for (float& x : dense[t]) x = static_cast<float>(u(eng));
+        const std::uint64_t hi = std::min(n, lo + kFeatChunk);
+        for (std::uint64_t i = lo; i < hi; ++i) dense[t][i] = static_cast<float>(u(eng));
       });
+  }
   std::vector<std::int32_t> labels(counts[tgt]);
   tasks.emplace_back([&] {
     std::mt19937_64 leng(mix_seed(seed, 0x1abe1ULL));

@@ -18,6 +18,7 @@
 #include <cstdint>
 #include <map>
 #include <optional>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -34,6 +35,11 @@ inline std::uint64_t mix_seed(std::uint64_t a, std::uint64_t b) {
   z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
   return z ^ (z >> 31);
 }
+
+// std::mt19937_64(seed) engines whose next outputs are outputs starts[c] (ascending) of
+// that stream, by polynomial jump-ahead (mt_jump.cpp): a long stream generated in
+// concurrent chunks, bit-identical to the serial one.
+std::vector<std::mt19937_64> mt64_jump_engines(std::uint64_t seed, const std::vector<std::uint64_t>& starts);
 
 enum class Storage : int { Absent = 0, Dense = 1, Learnable = 2 };
 

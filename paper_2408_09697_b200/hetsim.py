@@ -118,6 +118,14 @@ def mix_seed(a: int, b: int) -> int:
     return int(N.lib().hg_mix_seed(a, b))
 
 
+def mt64_outputs(seed: int, start: int, n: int) -> np.ndarray:
+    """n raw std::mt19937_64(seed) outputs from index start on, by jump-ahead (the chunked
+    feature streams of gen_synthetic, harness.cpp:153-162)."""
+    out = np.empty(n, np.uint64)
+    N.check(N.lib().hg_mt64_outputs(seed, start, n, out.ctypes.data))
+    return out
+
+
 # ---- graphs --------------------------------------------------------------------------------
 
 

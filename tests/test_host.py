@@ -57,6 +57,24 @@ def test_gen_synthetic_bit_exact(H, ref, name, seed):
                     ref.RefGraph.bundled(name, seed).export())
 
 
+@pytest.mark.parametrize("chunk", ["311", "4096", "100003"])
+def test_gen_synthetic_jumped_feature_chunks_bit_exact(H, ref, chunk, monkeypatch):
+    # feature streams cut into HG_FEAT_CHUNK-value chunks, each engine jumped ahead
+    # (mt_jump.cpp), equal the reference's serial streams bit for bit
+    monkeypatch.setenv("HG_FEAT_CHUNK", chunk)
+    compare_exports(H.gen_synthetic(H.bundled_spec("mag-mini"), 1).export(),
+                    ref.RefGraph.bundled("mag-mini", 1).export())
+
+
+def test_mt64_jump_ahead_matches_serial_outputs(H):
+    seed = H.mix_seed(7, 0xf0)
+    serial = H.mt64_outputs(seed, 0, 400_000)  # start 0: the plain engine
+    for start in [1, 311, 312, 313, 624, 19_937, 65_536, 123_457, 399_000]:
+        got = H.mt64_outputs(seed, start, 1000)
+        want = serial[start:start + 1000]
+        assert np.array_equal(got[:len(want)], want), start
+
+
 def test_gen_synthetic_spec_variants(H, ref):
     spec = H.toy_spec()
     for t in spec["node_types"]:
