@@ -139,6 +139,10 @@ typedef struct {
   /* 1: dense feature tables stay in pinned host memory (read over PCIe, zero-copy);
    * hg_engine_set_cache installs an HBM copy of the cached rows (cache.cpp:121-141) */
   int feat_host;
+  /* layer type: 0 RGCN (src/hgnn.cpp:173-362), 1 RGAT (relational attention, no reference
+   * counterpart: DESIGN.md §3, oracle/rgat.py); heads below the top layer (0: 4) */
+  int model;
+  int heads;
 } hg_engine_opts;
 
 typedef struct {

@@ -41,7 +41,8 @@ class Spec(C.Structure):
 class EngineOpts(C.Structure):
     _fields_ = [("k", C.c_int), ("fanouts", C.POINTER(C.c_int)), ("hidden", C.c_int), ("batch_cap", C.c_int),
                 ("p", C.c_int), ("rank", C.c_int), ("model_seed", C.c_uint64), ("learn_seed", C.c_uint64),
-                ("device", C.c_int), ("feat_dtype", C.c_int), ("feat_host", C.c_int)]
+                ("device", C.c_int), ("feat_dtype", C.c_int), ("feat_host", C.c_int),
+                ("model", C.c_int), ("heads", C.c_int)]
 
 
 class StepReport(C.Structure):

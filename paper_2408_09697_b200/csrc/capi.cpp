@@ -98,6 +98,9 @@ EngineOptions engine_options(const hg_engine_opts& o) {
   eo.device = o.device;
   eo.feat_dtype = o.feat_dtype;
   eo.feat_host = o.feat_host;
+  if (o.model != 0 && o.model != 1) throw std::invalid_argument("model must be 0 (RGCN) or 1 (RGAT)");
+  eo.model = o.model;
+  eo.heads = o.heads > 0 ? o.heads : 4;
   return eo;
 }
 

@@ -127,7 +127,7 @@ __global__ void k_csc_fill(CscHop h) {
   for (std::uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
     const std::uint32_t c = b.col[e];
     const std::uint32_t pos = atomicAdd(t.cursor + c, 1u);
-    t.entries[t.offs[c] - 1 - pos] = (static_cast<std::uint32_t>(bi) << kRowBits) | b.erow[e];
+    t.entries[t.offs[c] - 1 - pos] = (static_cast<std::uint32_t>(bi) << kRowBits) | (h.edge_ids ? e : b.erow[e]);
   }
 }
 

@@ -453,6 +453,7 @@ void Engine::build_plan(const Graph& g) {
       b.need_src_grad = g.types[b.src_t].storage == Storage::Learnable;
     }
   }
+  if (rgat()) rgat_plan(g);
   for (int h = 1; h <= k; ++h)
     for (int t = 0; t < ntypes_; ++t) {
       CscBuf c;
@@ -650,10 +651,11 @@ void Engine::upload(const Graph& g) {
       b.s_erow[sl] = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(b.edge_cap) * 4));
       b.s_col[sl] = static_cast<std::uint32_t*>(alloc(static_cast<std::size_t>(b.edge_cap) * 4));
     }
-    if (!o_.sample_only) {
+    if (!o_.sample_only && !rgat()) {
       b.mean = static_cast<float*>(alloc(static_cast<std::size_t>(b.rows_cap) * b.ld_mean * 4));
     }
-    if (b.need_src_grad) b.dmean = static_cast<float*>(alloc(static_cast<std::size_t>(b.rows_cap) * b.ld_mean * 4));
+    if (b.need_src_grad && !rgat())
+      b.dmean = static_cast<float*>(alloc(static_cast<std::size_t>(b.rows_cap) * b.ld_mean * 4));
     max_rows = std::max(max_rows, b.rows_cap + 1);
     total_rows += b.rows_cap;
   }
@@ -699,7 +701,8 @@ void Engine::upload(const Graph& g) {
       c.s_entries[sl] = static_cast<std::uint32_t*>(alloc(ent * 4));
       c.s_tmp[sl] = static_cast<std::uint32_t*>(alloc(ent * 4));
     }
-    if (!(c.hop == o_.k && xchg_type(c.src_t)))
+    const bool dense_leaf = rgat() && c.hop == o_.k && !tables_[c.src_t].learnable;  // RGAT: no gradient rows
+    if (!(c.hop == o_.k && xchg_type(c.src_t)) && !dense_leaf)
       c.dh = static_cast<float*>(alloc(static_cast<std::size_t>(std::max(1, c.src_cap)) * c.ld * 4));
     if (c.hop < o_.k) {
       for (auto& gr : groups_)
@@ -769,6 +772,7 @@ void Engine::upload(const Graph& g) {
   }
   wt_scratch_ = static_cast<float*>(alloc(wt * 4));
   wgrad_partial_ = static_cast<float*>(alloc(wp * 4));
+  if (rgat()) rgat_alloc();
   HG_CUDA(cudaStreamSynchronize(st_));
   bind_slot(0);
 }
@@ -811,7 +815,7 @@ void Engine::bind_slot(int s) {
 
 std::uint64_t Engine::param_count() const {
   std::uint64_t n = 0;
-  for (const auto& s : slots_) n += static_cast<std::uint64_t>(s.din) * s.dout;
+  for (const auto& s : slots_) n += static_cast<std::uint64_t>(s.din + (rgat() ? 1 : 0)) * s.dout;
   return n;
 }
 
@@ -1076,7 +1080,7 @@ void Engine::run_forward() {
 void Engine::run_loss(bool train) {
   LossArgs la{};
   la.done = loss_done_;
-  if (train && apply_adam_) {
+  if (train && apply_adam_ && !rgat()) {
     // learnable layer-0 tables advance their Adam step before the fused row
     // update of the backward pass; the loss kernel's last CTA does it
     for (const auto& c : cscs_)
@@ -1322,6 +1326,7 @@ void Engine::attach_replicas(const std::vector<std::vector<char>>& handles_by_ra
 
 CscHop Engine::csc_hop(int h) {
   CscHop ch{};
+  ch.edge_ids = rgat() ? 1 : 0;  // RGAT's backward reads per-edge attention weights
   std::vector<int> slot(ntypes_, -1);
   for (const auto& c : cscs_) {
     if (c.hop != h) continue;
@@ -1406,11 +1411,20 @@ void Engine::train_body(bool train) {
   fork_used_ = 0;
   side_open_ = false;
   training_ = train;
-  run_forward();
-  run_loss(train);
-  if (train) {
-    run_backward();
-    run_update();
+  if (rgat()) {
+    run_forward_rgat();
+    run_loss(train);
+    if (train) {
+      run_backward_rgat();
+      run_update_rgat();
+    }
+  } else {
+    run_forward();
+    run_loss(train);
+    if (train) {
+      run_backward();
+      run_update();
+    }
   }
   join();  // nothing of this step may remain on the side stream
   HG_CUDA(cudaMemcpyAsync(h_rb_, loss_, sizeof(Readback), cudaMemcpyDeviceToHost, st_));
@@ -1831,9 +1845,10 @@ std::vector<std::string> Engine::tensor_names() const {
   }
   for (const auto& gr : groups_) {
     if (gr.layer < k) n.push_back("H" + std::to_string(gr.depth - 1) + ".t" + std::to_string(gr.type));
-    for (std::size_t q = 0; q < gr.blocks.size(); ++q)
-      n.push_back("mean.l" + std::to_string(gr.layer) + ".r" + std::to_string(blocks_[gr.blocks[q]].rel) + ".t" +
-                  std::to_string(gr.type));
+    if (!rgat())
+      for (std::size_t q = 0; q < gr.blocks.size(); ++q)
+        n.push_back("mean.l" + std::to_string(gr.layer) + ".r" + std::to_string(blocks_[gr.blocks[q]].rel) + ".t" +
+                    std::to_string(gr.type));
   }
   for (int t = 0; t < ntypes_; ++t)
     if (tables_[t].w) n.push_back("H" + std::to_string(k) + ".t" + std::to_string(t));
@@ -1842,9 +1857,13 @@ std::vector<std::string> Engine::tensor_names() const {
     const std::string key = "r" + std::to_string(s.rel) + ".l" + std::to_string(s.layer);
     n.push_back("grad.w." + key);
     n.push_back("post." + key);
+    if (rgat()) {
+      n.push_back("att." + key);
+      n.push_back("grad.att." + key);
+    }
   }
   for (const auto& c : cscs_)
-    if (c.hop == k) {
+    if (c.hop == k && (c.dh || xchg_type(c.src_t))) {
       n.push_back("grad.f.t" + std::to_string(c.src_t) + ".ids");
       n.push_back("grad.f.t" + std::to_string(c.src_t) + ".rows");
     }
@@ -1956,9 +1975,11 @@ bool Engine::read_tensor(const std::string& name, std::string& dtype, std::vecto
     const std::string key = "r" + std::to_string(s.rel) + ".l" + std::to_string(s.layer);
     if (name == "grad.w." + key) return mat(s.g, s.din, s.dout, s.ld);
     if (name == "post." + key) return mat(s.w, s.din, s.dout, s.ld);
+    if (rgat() && name == "att." + key) return mat(s.a, 1, s.dout, s.ld);
+    if (rgat() && name == "grad.att." + key) return mat(s.ag, 1, s.dout, s.ld);
   }
   for (const auto& c : cscs_) {
-    if (c.hop != k) continue;
+    if (c.hop != k || !c.dh) continue;
     const std::string p = "grad.f.t" + std::to_string(c.src_t);
     const Front& f = front(k, c.src_t);
     if (name == p + ".ids") return u32s(f.list, dev_int(f.count));

@@ -45,6 +45,10 @@ struct EngineOptions {
   // PCIe, zero-copy) with an HBM cache of the rows set_cache() installs
   int feat_dtype = 0;
   int feat_host = 0;
+  // layer type: 0 RGCN (the reference's, hgnn.cpp:173-362), 1 RGAT (rgat.cuh: relational
+  // attention with `heads` heads below the top layer, one head at the top)
+  int model = 0;
+  int heads = 4;
   // non-empty: the work-aware plan (work_aware_partition, one value per sub-metatree)
   // instead of the reference's meta_partition; the numbers are the flat pass's either way
   std::vector<double> sub_work;
@@ -246,6 +250,10 @@ class Engine {
     float* dmean = nullptr;  // rows_cap x ld_mean (only if the source needs a gradient)
     int din = 0, ld_mean = 0;
     bool need_src_grad = false;
+    // RGAT (rgat.cuh): projected source rows, scores, softmax state and gradients
+    float *z = nullptr, *sc = nullptr, *lse = nullptr, *alpha = nullptr, *dt = nullptr;
+    float *dz = nullptr, *tsum = nullptr, *da_part = nullptr;
+    int ld_z = 0, heads = 1, src_cap = 0;
   };
   struct Front {
     std::uint32_t* list = nullptr;
@@ -255,6 +263,9 @@ class Engine {
   struct Slot {
     int rel = -1, layer = 0, din = 0, dout = 0, ld = 0;
     float *w = nullptr, *m = nullptr, *v = nullptr, *g = nullptr;
+    // RGAT: attention vector [dout] (+ Adam state, gradient) and W^T [dout x ld_wt]
+    float *a = nullptr, *am = nullptr, *av = nullptr, *ag = nullptr, *wt = nullptr;
+    int ld_wt = 0;
   };
   struct Group {  // one output type of one layer
     int layer = 0, depth = 0, type = -1, dout = 0, ld = 0, rows_cap = 0;
@@ -294,6 +305,19 @@ class Engine {
   void run_loss(bool train);
   void run_backward();
   void run_update();
+  // RGAT layer type (rgat.cu)
+  bool rgat() const { return o_.model == 1; }
+  int heads_of(int layer) const { return layer == o_.k ? 1 : o_.heads; }
+  void rgat_plan(const Graph& g);
+  void rgat_alloc();
+  void run_forward_rgat();
+  void run_backward_rgat();
+  void run_update_rgat();
+  const float* rgat_src(const BlockBuf& b, int& ld);  // source-frontier rows of a block's layer input
+  std::vector<float*> leaf_x_;  // [type]: hop-k source frontier rows gathered from the table (fp32)
+  std::vector<int> leaf_ld_;
+  float* rgat_wpart_ = nullptr;  // weight-gradient split-K partials
+  std::size_t rgat_wpart_floats_ = 0;
   void timed(const char* name, double bytes, const std::function<void()>& f);
   Front& front(int h, int t) { return fronts_[h * ntypes_ + t]; }
   // destination rows of a block: frontier[hop-1][dst type]; hop-1 blocks into the

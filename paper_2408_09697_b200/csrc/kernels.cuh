@@ -173,7 +173,7 @@ void cross_entropy(const LossArgs& a, cudaStream_t st);
 struct CscType {
   std::uint32_t* offs;     // [src_cap + 1]: counts, then inclusive prefix
   std::uint32_t* cursor;   // [src_cap]
-  std::uint32_t* entries;  // packed (block << 28 | destination row) of every edge, grouped by source row
+  std::uint32_t* entries;  // packed (block << 28 | destination row, or edge) of every edge, grouped by source row
   const int* n_src;
   int src_cap;
   float* dh;               // gradient rows (nullptr: not materialised)
@@ -206,6 +206,7 @@ struct CscHop {
   int nt;
   CscEdges b[kMaxBlocks];
   int nb;
+  int edge_ids;  // entries hold (block, edge) instead of (block, destination row)
 };
 void csc_prepare(const CscHop& h, LbScratch& lb, cudaStream_t st);
 

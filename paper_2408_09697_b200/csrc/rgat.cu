@@ -1,0 +1,345 @@
+// RGAT layer type of the engine (rgat.cuh defines the layer). Per layer, on the
+// sampled blocks of one hop:
+//   forward:  z_b = H_src . W_r (tcgen05 projection over the block's source frontier),
+//             raw scores t_b = a_r . z_b per head, then per destination row the softmax
+//             over its edges and the weighted sum of z rows, summed over the relations
+//             into the type (+ReLU below the top);
+//   backward: per edge dt (softmax + LeakyReLU backward), the transposed gather over
+//             the hop's CSC view (entries = (block, edge)) into dz_b and tsum_b,
+//             dW_r = H_src^T dz_b (tcgen05 split-K, ordered reduction),
+//             da_r = sum_j tsum_b[j] z_b[j] (ordered), and the source gradient
+//             dH_src = sum_b dz_b . W_r^T (tcgen05 projection with relations along K);
+//             learnable layer-0 rows take their sparse Adam, the model its dense Adam.
+// Layer-0 inputs are gathered once per step into fp32 rows (the projection's TMA
+// operand). Inner-layer gradients are stored unmasked and masked by H > 0 when read.
+#include <cmath>
+#include <random>
+
+#include "engine.hpp"
+#include "gemm.cuh"
+#include "rgat.cuh"
+
+namespace hetgpu {
+
+void Engine::rgat_plan(const Graph& g) {
+  (void)g;
+  if (o_.heads < 1 || o_.heads > kAttMaxHeads || o_.hidden % o_.heads)
+    throw std::invalid_argument("RGAT heads must be 1..8 and divide the hidden width");
+  if (replica_group_.size() > 1) throw std::invalid_argument("RGAT with replica groups is not supported");
+  if (o_.feat_host) throw std::invalid_argument("RGAT reads its layer-0 rows from HBM tables (feat_host = 0)");
+  if (round_up4(num_classes_) > kAttMaxCols || round_up4(o_.hidden) > kAttMaxCols)
+    throw std::invalid_argument("RGAT layer wider than 512 columns");
+  for (auto& b : blocks_) {
+    b.need_src_grad = true;  // every block's transposed view: dz feeds its weight gradient
+    if (b.edge_cap >= (1 << 28)) throw std::invalid_argument("RGAT block edge capacity exceeds 2^28");
+  }
+}
+
+void Engine::rgat_alloc() {
+  const int k = o_.k;
+  auto round32 = [](int x) { return static_cast<std::size_t>(ceil_div(std::max(1, x), 32) * 32); };
+  std::size_t wpart = 0;
+  for (auto& b : blocks_) {
+    const int l = k - b.hop + 1;
+    b.ld_z = round_up4(out_dim(l));
+    b.heads = heads_of(l);
+    b.src_cap = front(b.hop, b.src_t).cap;
+    const std::size_t zr = round32(b.src_cap);
+    b.z = static_cast<float*>(alloc(zr * b.ld_z * 4));
+    b.sc = static_cast<float*>(alloc(zr * b.heads * 4));
+    b.lse = static_cast<float*>(alloc(static_cast<std::size_t>(std::max(1, b.rows_cap)) * b.heads * 4));
+    b.alpha = static_cast<float*>(alloc(static_cast<std::size_t>(b.edge_cap) * b.heads * 4));
+    b.dt = static_cast<float*>(alloc(static_cast<std::size_t>(b.edge_cap) * b.heads * 4));
+    b.dz = static_cast<float*>(alloc(zr * b.ld_z * 4));
+    b.tsum = static_cast<float*>(alloc(zr * b.heads * 4));
+    b.da_part = static_cast<float*>(alloc(ceil_div(std::max(1, b.src_cap), kAttDaChunk) * b.ld_z * 4));
+    wpart += ceil_div(zr, kWChunkRows) * static_cast<std::size_t>(std::max(1, b.din)) * out_dim(l);
+  }
+  rgat_wpart_floats_ = std::max<std::size_t>(1, wpart);
+  rgat_wpart_ = static_cast<float*>(alloc(rgat_wpart_floats_ * 4));
+  // attention vectors: U(-b, b), b = sqrt(6 / (F + 1)) (Glorot for an F x 1 vector), from
+  // their own engine per (relation, layer)
+  for (auto& s : slots_) {
+    s.ld_wt = round_up4(std::max(1, s.din));
+    s.wt = static_cast<float*>(alloc(static_cast<std::size_t>(std::max(1, s.dout)) * s.ld_wt * 4));
+    s.a = static_cast<float*>(alloc(static_cast<std::size_t>(s.ld) * 4));
+    s.am = static_cast<float*>(alloc(static_cast<std::size_t>(s.ld) * 4));
+    s.av = static_cast<float*>(alloc(static_cast<std::size_t>(s.ld) * 4));
+    s.ag = static_cast<float*>(alloc(static_cast<std::size_t>(s.ld) * 4));
+    const int F = s.dout / heads_of(s.layer);
+    const double bound = std::sqrt(6.0 / (F + 1.0));
+    std::mt19937_64 eng(mix_seed(mix_seed(o_.model_seed, 0xa77e), static_cast<std::uint64_t>(s.rel) * 64 + s.layer));
+    std::uniform_real_distribution<double> u(-bound, bound);
+    std::vector<float> host(s.ld, 0.f);
+    for (int c = 0; c < s.dout; ++c) host[c] = static_cast<float>(u(eng));
+    HG_CUDA(cudaMemcpyAsync(s.a, host.data(), host.size() * 4, cudaMemcpyHostToDevice, st_));
+    HG_CUDA(cudaStreamSynchronize(st_));
+  }
+  leaf_x_.assign(ntypes_, nullptr);
+  leaf_ld_.assign(ntypes_, 0);
+  for (int bi : hop_blocks_[k]) {
+    const int t = blocks_[bi].src_t;
+    if (leaf_x_[t] || !tables_[t].w || front(k, t).cap <= 0) continue;
+    leaf_ld_[t] = round_up4(std::max(1, tables_[t].dim));
+    leaf_x_[t] = static_cast<float*>(alloc(round32(front(k, t).cap) * leaf_ld_[t] * 4));
+  }
+}
+
+const float* Engine::rgat_src(const BlockBuf& b, int& ld) {
+  if (b.hop == o_.k) {
+    ld = leaf_ld_[b.src_t];
+    return leaf_x_[b.src_t];
+  }
+  for (const auto& gr : groups_)
+    if (gr.depth - 1 == b.hop && gr.type == b.src_t) {
+      ld = gr.ld;
+      return gr.out;
+    }
+  throw std::runtime_error("RGAT: no layer input for a block's source type");
+}
+
+void Engine::run_forward_rgat() {
+  const int k = o_.k;
+  HG_CUDA(cudaMemsetAsync(logits_, 0, static_cast<std::size_t>(o_.batch_cap + 1) * ldc_ * 4, st_));
+  LeafGatherBatch lg{};
+  for (int t = 0; t < ntypes_; ++t) {
+    if (!leaf_x_[t]) continue;
+    const TypeTable& tb = tables_[t];
+    lg.j[lg.n++] = {tb.w, tb.ld, tb.dense ? tb.dtype : static_cast<int>(kF32), tb.dim, front(k, t).list,
+                    front(k, t).count, front(k, t).cap, leaf_x_[t], leaf_ld_[t]};
+  }
+  timed("leaf_gather", 0, [&] { leaf_gather(lg, st_); });
+  for (int l = 1; l <= k; ++l) {
+    const int d = k - l + 1;
+    const bool top = l == k;
+    // (1) z_b = H_src . W_r over every block's source frontier, (2) raw scores
+    std::vector<ProjBatch> pbs(1);
+    AttScoreBatch sb{};
+    for (const auto& gr : groups_) {
+      if (gr.layer != l) continue;
+      for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
+        const BlockBuf& b = blocks_[gr.blocks[q]];
+        const Slot& s = slots_[gr.slots[q]];
+        int ld_src = 0;
+        const float* src = rgat_src(b, ld_src);
+        if (pbs.back().ng == kProjGroups) pbs.emplace_back();
+        ProjBatch& pb = pbs.back();
+        ProjGroup& pg = pb.g[pb.ng++];
+        pg.nrel = 1;
+        pg.n_rows = front(d, b.src_t).count;
+        pg.rows_cap = b.src_cap;
+        pg.out = b.z;
+        pg.ld_out = b.ld_z;
+        pg.dout = s.dout;
+        pg.relu = 0;
+        pg.out_stride = 1;
+        pg.out_offset = 0;
+        pg.r[0] = {src, ld_src, b.din, s.w, s.ld};
+        if (sb.n == static_cast<int>(sizeof(sb.j) / sizeof(sb.j[0]))) throw std::runtime_error("too many RGAT blocks");
+        sb.j[sb.n++] = {b.z, s.a, b.sc, front(d, b.src_t).count, b.src_cap, b.ld_z, s.dout, b.heads};
+      }
+    }
+    timed(top ? "rgat_project_top" : "rgat_project", 0, [&] {
+      for (auto& pb : pbs) use_umma_ ? project_umma(pb, st_) : project_tiles(pb, st_);
+    });
+    timed("rgat_scores", 0, [&] { att_scores(sb, st_); });
+    // (3) softmax-weighted sums over every destination row, relations summed per type
+    std::vector<AttBatch> abs(1);
+    for (const auto& gr : groups_) {
+      if (gr.layer != l) continue;
+      if (gr.blocks.empty()) {
+        if (!top) zero_rows(gr.out, gr.ld, front(gr.depth - 1, gr.type).count, gr.rows_cap, st_);
+        continue;
+      }
+      if (gr.blocks.size() > static_cast<std::size_t>(kProjRels))
+        throw std::runtime_error("more relations into one type than an attention group holds");
+      if (abs.back().ng == kProjGroups) abs.emplace_back();
+      AttGroup& ag = abs.back().g[abs.back().ng++];
+      ag.nrel = static_cast<int>(gr.blocks.size());
+      for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
+        const BlockBuf& b = blocks_[gr.blocks[q]];
+        ag.r[q] = {b.indptr, b.col, b.z, b.sc, b.lse, b.alpha, b.dt};
+      }
+      ag.n_rows = front(gr.depth - 1, gr.type).count;
+      ag.rows_cap = gr.rows_cap;
+      ag.out = gr.out;
+      ag.dout = nullptr;
+      ag.relu_h = nullptr;
+      ag.ld = gr.ld;
+      ag.cols = gr.dout;
+      ag.heads = heads_of(l);
+      ag.relu = top ? 0 : 1;
+    }
+    timed(top ? "rgat_attend_top" : "rgat_attend", 0, [&] {
+      for (auto& ab : abs) att_forward(ab, st_);
+    });
+  }
+  // AGG_all: sum the partial logits of every partition (raf.cpp:427-446)
+  if (o_.p > 1) {
+#ifdef HG_WITH_NCCL
+    if (comm_ && !counting_) {
+      timed("agg_all", static_cast<double>(o_.batch_cap + 1) * ldc_ * 4, [&] {
+        if (ncclAllReduce(logits_, logits_, static_cast<std::size_t>(o_.batch_cap + 1) * ldc_, ncclFloat, ncclSum,
+                          comm_, st_) != ncclSuccess)
+          throw std::runtime_error("ncclAllReduce failed");
+      });
+    }
+#endif
+  }
+}
+
+void Engine::run_backward_rgat() {
+  const int k = o_.k;
+  TransposeBatch tb{};
+  for (auto& s : slots_) tb.j[tb.n++] = {s.w, s.din, s.dout, s.ld, s.wt, s.ld_wt};
+  timed("rgat_transpose", 0, [&] { transpose_slots(tb, st_); });
+  auto group_of = [&](int depth_minus_1, int t) -> const Group* {
+    for (const auto& gr : groups_)
+      if (gr.depth - 1 == depth_minus_1 && gr.type == t) return &gr;
+    return nullptr;
+  };
+  for (int l = k; l >= 1; --l) {
+    const int d = k - l + 1;
+    const bool top = l == k;
+    // (1) per edge dt: softmax and LeakyReLU backward
+    std::vector<AttBatch> abs(1);
+    for (const auto& gr : groups_) {
+      if (gr.layer != l || gr.blocks.empty()) continue;
+      if (abs.back().ng == kProjGroups) abs.emplace_back();
+      AttGroup& ag = abs.back().g[abs.back().ng++];
+      ag.nrel = static_cast<int>(gr.blocks.size());
+      for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
+        const BlockBuf& b = blocks_[gr.blocks[q]];
+        ag.r[q] = {b.indptr, b.col, b.z, b.sc, b.lse, b.alpha, b.dt};
+      }
+      ag.n_rows = front(gr.depth - 1, gr.type).count;
+      ag.rows_cap = gr.rows_cap;
+      ag.out = nullptr;
+      ag.dout = gr.dout_buf;
+      ag.relu_h = top ? nullptr : gr.out;
+      ag.ld = gr.ld;
+      ag.cols = gr.dout;
+      ag.heads = heads_of(l);
+      ag.relu = 0;
+    }
+    timed("rgat_edge_grad", 0, [&] {
+      for (auto& ab : abs) att_edge_grad(ab, st_);
+    });
+    // (2) transposed gather over the hop's CSC view: dz_b, tsum_b
+    const CscHop ch = csc_hop(d);
+    AttScatter sc{};
+    sc.nt = ch.nt;
+    for (int t = 0; t < ch.nt; ++t) {
+      sc.offs[t] = ch.t[t].offs;
+      sc.entries[t] = ch.t[t].entries;
+      sc.n_src[t] = ch.t[t].n_src;
+      sc.src_cap[t] = ch.t[t].src_cap;
+    }
+    std::vector<int> scatter_blocks;  // BlockBuf index of every CscEdges entry (csc_hop order)
+    for (int bi : hop_blocks_[d]) {
+      const BlockBuf& b = blocks_[bi];
+      bool typed = false;
+      for (const auto& c : cscs_)
+        if (c.hop == d && c.src_t == b.src_t) typed = true;
+      if (!b.need_src_grad || !typed) continue;
+      scatter_blocks.push_back(bi);
+    }
+    if (static_cast<int>(scatter_blocks.size()) != ch.nb) throw std::runtime_error("RGAT: CSC block order mismatch");
+    WGradBatch wb{};
+    AttDaBatch db{};
+    std::size_t off = 0;
+    for (int q = 0; q < ch.nb; ++q) {
+      const BlockBuf& b = blocks_[scatter_blocks[q]];
+      const Group* gr = group_of(d - 1, b.dst_t);
+      const Slot& s = slots_[slot_of_.at(SlotId{b.rel, l})];
+      if (!gr) throw std::runtime_error("RGAT: block without a destination group");
+      sc.b[sc.nb++] = {b.erow, b.alpha, b.dt, gr->dout_buf, top ? nullptr : gr->out, gr->ld, s.a, b.dz, b.tsum,
+                       b.ld_z, s.dout, b.heads, ch.b[q].type};
+      db.j[db.n++] = {b.tsum, b.z, front(d, b.src_t).count, b.src_cap, b.ld_z, s.dout, b.heads, b.da_part, s.ag};
+      int ld_src = 0;
+      const float* src = rgat_src(b, ld_src);
+      if (wb.np == kMaxProblems) throw std::runtime_error("too many RGAT weight-gradient problems per layer");
+      // the operands' row extent; rows [n, next multiple of 32) of dz are zero
+      const int rows_cap = std::max(1, b.src_cap);
+      wb.p[wb.np++] = {src, ld_src, b.din, DpreView{b.dz, nullptr, b.ld_z, s.dout, 1, 0}, front(d, b.src_t).count,
+                       rows_cap, rgat_wpart_ + off, s.g, s.ld, nullptr, nullptr, nullptr};
+      off += ceil_div(rows_cap, kWChunkRows) * static_cast<std::size_t>(std::max(1, b.din)) * s.dout;
+    }
+    if (off > rgat_wpart_floats_) throw std::runtime_error("RGAT weight-gradient scratch too small");
+    timed(top ? "rgat_scatter_top" : "rgat_scatter", 0, [&] { att_scatter(sc, st_); });
+    timed("rgat_att_grad", 0, [&] { att_da(db, st_); });
+    timed("rgat_weight_grad", 0, [&] { use_umma_ ? wgrad_umma(wb, st_) : wgrad_tiles(wb, st_); });
+    // (3) source gradients dH_src = sum_b dz_b . W_r^T (inner types and learnable leaves)
+    std::vector<ProjBatch> pbs(1);
+    for (const auto& c : cscs_) {
+      if (c.hop != d || !c.dh) continue;
+      if (pbs.back().ng == kProjGroups) pbs.emplace_back();
+      ProjBatch& pb = pbs.back();
+      ProjGroup& pg = pb.g[pb.ng++];
+      pg.nrel = 0;
+      for (int bi : hop_blocks_[d]) {
+        const BlockBuf& b = blocks_[bi];
+        if (b.src_t != c.src_t) continue;
+        const Slot& s = slots_[slot_of_.at(SlotId{b.rel, l})];
+        if (pg.nrel == kProjRels) throw std::runtime_error("too many relations out of one source type");
+        pg.r[pg.nrel++] = {b.dz, b.ld_z, s.dout, s.wt, s.ld_wt};
+      }
+      pg.n_rows = front(d, c.src_t).count;
+      pg.rows_cap = c.src_cap;
+      pg.out = c.dh;
+      pg.ld_out = c.ld;
+      pg.dout = c.din;
+      pg.relu = 0;
+      pg.out_stride = 1;
+      pg.out_offset = 0;
+    }
+    timed("rgat_src_grad", 0, [&] {
+      for (auto& pb : pbs)
+        if (pb.ng) use_umma_ ? project_umma(pb, st_) : project_tiles(pb, st_);
+    });
+    // (4) learnable layer-0 rows: sparse Adam (step += 1 iff the type has rows)
+    if (d == k && apply_adam_) {
+      AdamRowsBatch rb{};
+      int base4 = 0;
+      for (const auto& c : cscs_) {
+        if (c.hop != k || !c.dh || !tables_[c.src_t].learnable) continue;
+        TypeTable& t = tables_[c.src_t];
+        rb.t[rb.n] = {t.w, t.m, t.v, t.ld, front(k, c.src_t).list, c.dh, c.ld, front(k, c.src_t).count, t.step};
+        rb.base4[rb.n] = base4;
+        base4 += c.src_cap * (t.ld / 4);
+        ++rb.n;
+      }
+      rb.total4 = base4;
+      AdamHyper hp;
+      timed("rgat_adam_rows", 0, [&] { adam_rows(rb, hp, err_, st_); });
+    }
+  }
+}
+
+void Engine::run_update_rgat() {
+  if (!apply_adam_) return;
+  AdamModelBatch mb{};
+  int base = 0;
+  for (auto& s : slots_) {
+    if (mb.n + 2 > kMaxSlots) throw std::runtime_error("too many model slots");
+    mb.w[mb.n] = s.w;
+    mb.m[mb.n] = s.m;
+    mb.v[mb.n] = s.v;
+    mb.g[mb.n] = s.g;
+    mb.base4[mb.n] = base;
+    base += std::max(1, s.din) * s.ld / 4;
+    ++mb.n;
+    mb.w[mb.n] = s.a;
+    mb.m[mb.n] = s.am;
+    mb.v[mb.n] = s.av;
+    mb.g[mb.n] = s.ag;
+    mb.base4[mb.n] = base;
+    base += s.ld / 4;
+    ++mb.n;
+  }
+  mb.total4 = base;
+  AdamHyper hp;
+  timed("adam", 0, [&] { adam_model(mb, &d_tsc_->model_step, hp, err_, st_); });
+}
+
+}  // namespace hetgpu

@@ -1,0 +1,144 @@
+// Relational graph attention (RGAT, BASELINE configs[2] / SURVEY §8 C3) on the RAF
+// blocks: the kernels around the tcgen05 projections (rgat_kernels.cu).
+//
+// The reference has no attention layer; this is the framework's
+// own definition, restated in oracle/rgat.py (parity against that restatement and
+// finite differences). Layer l, relation r (src type s -> dst type t), heads H,
+// head width F = d_out / H, columns of head h = [h F, (h+1) F):
+//   z_j      = h_j . W_r                              (per source row of the block)
+//   t_j^h    = a_r^h . z_j^(h)                        (raw score)
+//   alpha_e^h = softmax over the edges e of dst i of LeakyReLU_0.2(t_src(e)^h)
+//   out_i    = sum_r concat_h sum_e alpha_e^h z_src(e)^(h)   (+ ReLU below the top)
+// The blocks carry no destination features (the reference's frontiers do not
+// contain their seeds, sampling.cpp:41-103), so the score is source-side only
+// ("static" attention, the ranking GAT's own additive score gives); the top layer
+// has one head.
+#pragma once
+
+#include "gemm.cuh"
+#include "kernels.cuh"
+
+namespace hetgpu {
+
+constexpr int kAttMaxHeads = 8;
+constexpr int kAttMaxCols = 512;  // row width (ld) the attention kernels hold in registers
+constexpr float kAttSlope = 0.2f;
+
+struct AttRel {
+  const std::uint32_t* indptr;  // block rows (destination frontier order)
+  const std::uint32_t* col;     // per edge: source row in the source frontier
+  const float* z;               // [n_src x ld] projected source rows
+  const float* t;               // [n_src x heads] raw scores
+  float* lse;                   // [rows x heads] log-sum-exp of the row's LeakyReLU scores
+  float* alpha;                 // [edges x heads]
+  float* dt;                    // [edges x heads]: d loss / d t per edge (backward)
+};
+struct AttGroup {  // one destination type of one layer
+  AttRel r[kProjRels];
+  int nrel;
+  const int* n_rows;
+  int rows_cap;
+  float* out;           // forward: sum over relations (+ReLU)
+  const float* dout;    // backward: gradient of out
+  const float* relu_h;  // backward: dout masked by relu_h > 0 (inner layers), or nullptr
+  int ld;
+  int cols, heads;
+  int relu;
+};
+struct AttBatch {
+  AttGroup g[kProjGroups];
+  int ng;
+};
+// forward: per destination row, every relation's softmax and weighted sum (alpha kept)
+void att_forward(const AttBatch& b, cudaStream_t st);
+// backward, per destination row: dt of every edge (softmax and LeakyReLU backward)
+void att_edge_grad(const AttBatch& b, cudaStream_t st);
+
+// raw scores t = a . z per head for the source rows of every block
+struct AttScoreJob {
+  const float* z;
+  const float* a;
+  float* t;
+  const int* n_rows;
+  int rows_cap, ld, cols, heads;
+};
+struct AttScoreBatch {
+  AttScoreJob j[kMaxBlocks * 2];
+  int n;
+};
+void att_scores(const AttScoreBatch& b, cudaStream_t st);
+
+// backward through the CSC view of one hop (entries = packed (block, edge)):
+// per source row j and block b of its type,
+//   dz_b[j] = sum_e alpha_e^h(c) dout_dst(e)[c] + (sum_e dt_e^h(c)) a_b[c],  tsum_b[j][h] = sum_e dt_e^h
+// rows [n_src, round_up(n_src, 32)) of dz are zeroed (the weight gradient's K chunks)
+struct AttScatterBlock {
+  const std::uint32_t* erow;  // per edge: destination row
+  const float* alpha;
+  const float* dt;
+  const float* dout;
+  const float* relu_h;
+  int ld_dout;
+  const float* a;
+  float* dz;
+  float* tsum;
+  int ld, cols, heads;
+  int type;  // index into the hop's CscHop::t
+};
+struct AttScatter {
+  AttScatterBlock b[kMaxBlocks];
+  int nb;
+  const std::uint32_t* offs[kMaxSegs];
+  const std::uint32_t* entries[kMaxSegs];
+  const int* n_src[kMaxSegs];
+  int src_cap[kMaxSegs];
+  int nt;
+};
+void att_scatter(const AttScatter& s, cudaStream_t st);
+
+// da_b[c] = sum_j tsum_b[j][h(c)] z_b[j][c]: ordered chunk partials, then their ordered sum
+struct AttDaJob {
+  const float* tsum;
+  const float* z;
+  const int* n_rows;
+  int rows_cap, ld, cols, heads;
+  float* partial;  // [chunks x ld]
+  float* da;       // [ld]
+};
+struct AttDaBatch {
+  AttDaJob j[kMaxBlocks * 2];
+  int n;
+};
+constexpr int kAttDaChunk = 256;
+void att_da(const AttDaBatch& b, cudaStream_t st);
+
+// layer-0 rows of the source frontier as fp32 GEMM operands: out[i] = table[ids[i]]
+struct LeafGatherJob {
+  const void* table;
+  int ld_t, dtype, dim;
+  const std::uint32_t* ids;
+  const int* n;
+  int cap;
+  float* out;
+  int ld_out;
+};
+struct LeafGatherBatch {
+  LeafGatherJob j[kMaxSegs];
+  int n;
+};
+void leaf_gather(const LeafGatherBatch& b, cudaStream_t st);
+
+// W^T of every slot (the source-gradient contraction reads dz . W^T as a projection)
+struct TransposeJob {
+  const float* w;
+  int din, dout, ld_w;
+  float* wt;
+  int ld_wt;
+};
+struct TransposeBatch {
+  TransposeJob j[kMaxSlots];
+  int n;
+};
+void transpose_slots(const TransposeBatch& b, cudaStream_t st);
+
+}  // namespace hetgpu

@@ -274,16 +274,22 @@ class Engine:
     """One meta-partition of the RAF engine on one GPU (run_raf_batch, raf.cpp:344-530)."""
 
     FEAT_DTYPES = {"f32": 0, "f16": 1, "bf16": 2}
+    MODELS = {"rgcn": 0, "rgat": 1}  # RGAT: relational attention (DESIGN.md §3; no reference counterpart)
 
     def __init__(self, g: HetGraph, fanouts: Sequence[int], hidden: int = 64, batch_cap: int = 1024, p: int = 1,
                  rank: int = 0, model_seed: int = 0, learn_seed: int = 0, device: int = 0, feat_dtype: str = "f32",
-                 feat_host: bool = False, sub_work: Optional[Sequence[float]] = None):
+                 feat_host: bool = False, sub_work: Optional[Sequence[float]] = None, model: str = "rgcn",
+                 heads: int = 4):
         fo = (C.c_int * len(fanouts))(*[int(f) for f in fanouts])
         self._fo = fo
         if feat_dtype not in self.FEAT_DTYPES:
             raise ValueError("feature dtype must be one of f32, f16, bf16")
+        if model not in self.MODELS:
+            raise ValueError("model must be one of rgcn, rgat")
         opts = N.EngineOpts(len(fanouts), fo, hidden, batch_cap, p, rank, model_seed, learn_seed, device,
-                            self.FEAT_DTYPES[feat_dtype], int(bool(feat_host)))
+                            self.FEAT_DTYPES[feat_dtype], int(bool(feat_host)), self.MODELS[model], heads)
+        self.model = model
+        self.heads = heads
         self.k = len(fanouts)
         self.graph = g  # keep alive
         if sub_work is None:
