@@ -184,3 +184,41 @@ def test_rgat_steps_are_bit_reproducible(H):
     assert runs[0][0] == runs[1][0]
     assert np.array_equal(runs[0][1], runs[1][1])
     assert runs[0][0][-1] < runs[0][0][3]
+
+
+@pytest.mark.gpu
+def test_rgat_c2_step_matches_oracle(H, ref):
+    """The C3 configuration itself: C2's graph and batch (1024, fanout [25,20]), hidden 64,
+    4 heads; one training step against the f64 restatement on the reference's blocks."""
+    spec = H.ogbn_mag_spec()
+    rg = ref.RefGraph.from_spec(spec, 1)
+    g = port.Graph(rg.export())
+    tree = port.bfs_metatree(g, 2)
+    gd = H.gen_synthetic(spec, 1)
+    batch = [int(x) for x in H.make_batches(gd, 1024, 1, H.mix_seed(1, 0xBA7C))[0]]
+    seed = H.mix_seed(1, 0xB000)
+    blocks = blocks_from(rg.sample_khop(batch, [25, 20], seed, port.hop_relation_sets(tree, 2)), 2, g.ntypes,
+                         g.nrels)
+    eng = H.Engine.for_experiment(gd, [25, 20], 64, 1, batch_cap=1024, model="rgat", heads=4)
+    names = eng.tensor_names()
+    init = eng.read(*[n for n in names if n.startswith(("post.r", "att.", "post.learn.t"))])
+    weights = {(int(n.split(".")[1][1:]), int(n.split(".")[2][1:])): init[n] for n in init if n.startswith("post.r")}
+    att = {(int(n.split(".")[1][1:]), int(n.split(".")[2][1:])): init[n].ravel() for n in init if n.startswith("att.")}
+    learn = {int(n.split(".t")[-1]): init[n] for n in init if n.startswith("post.learn.t")}
+    loss, logits, Hw, dl, wg, ag, fg = R.step(g, tree, blocks, weights, att, learn, 64, 4, batch)
+    rep = eng.step(batch, seed, 0, train=True)
+    got = eng.read(*[n for n in names if n.startswith(("H1.", "logits", "grad."))])
+    assert abs(rep["loss"] - loss) <= TOL * abs(loss)
+    assert_close(got["logits"], logits, TOL, "C3 logits")
+    for t in range(g.ntypes):
+        if t in Hw[1]:
+            assert_close(got[f"H1.t{t}"], Hw[1][t], TOL, f"C3 H1.t{t}")
+    if _relu_flips(got, Hw, blocks, g):
+        pytest.skip("ReLU tie flipped vs the f64 oracle; forward parity checked")
+    for key, want in wg.items():
+        r, l = key
+        assert_close(got[f"grad.w.r{r}.l{l}"], want, TOL, f"C3 grad.w.r{r}.l{l}")
+        assert_close(got[f"grad.att.r{r}.l{l}"].ravel(), ag[key], TOL, f"C3 grad.att.r{r}.l{l}")
+    for t, (ids, rows) in fg.items():
+        assert [int(x) for x in got[f"grad.f.t{t}.ids"]] == ids
+        assert_close(got[f"grad.f.t{t}.rows"], rows, TOL, f"C3 grad.f.t{t}")
