@@ -254,6 +254,11 @@ class Engine {
     float *z = nullptr, *sc = nullptr, *lse = nullptr, *alpha = nullptr, *dt = nullptr;
     float *dz = nullptr, *tsum = nullptr, *da_part = nullptr;
     int ld_z = 0, heads = 1, src_cap = 0;
+    // RGAT layer 1 (aggregate first, rgat.cuh): per-head aggregates of the table rows and
+    // the block-diagonal weight; din_p = round_up4(din)
+    float *agg = nullptr, *dagg = nullptr, *te = nullptr, *qv = nullptr, *wbd = nullptr, *wbdt = nullptr;
+    float *dwfull = nullptr, *dq_part = nullptr, *dqv = nullptr;
+    int din_p = 0;
   };
   struct Front {
     std::uint32_t* list = nullptr;
@@ -313,9 +318,7 @@ class Engine {
   void run_forward_rgat();
   void run_backward_rgat();
   void run_update_rgat();
-  const float* rgat_src(const BlockBuf& b, int& ld);  // source-frontier rows of a block's layer input
-  std::vector<float*> leaf_x_;  // [type]: hop-k source frontier rows gathered from the table (fp32)
-  std::vector<int> leaf_ld_;
+  const float* rgat_src(const BlockBuf& b, int& ld);  // source-frontier rows of an inner block's layer input
   float* rgat_wpart_ = nullptr;  // weight-gradient split-K partials
   std::size_t rgat_wpart_floats_ = 0;
   void timed(const char* name, double bytes, const std::function<void()>& f);

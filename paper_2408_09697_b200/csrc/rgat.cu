@@ -1,17 +1,21 @@
-// RGAT layer type of the engine (rgat.cuh defines the layer). Per layer, on the
-// sampled blocks of one hop:
-//   forward:  z_b = H_src . W_r (tcgen05 projection over the block's source frontier),
-//             raw scores t_b = a_r . z_b per head, then per destination row the softmax
-//             over its edges and the weighted sum of z rows, summed over the relations
-//             into the type (+ReLU below the top);
-//   backward: per edge dt (softmax + LeakyReLU backward), the transposed gather over
-//             the hop's CSC view (entries = (block, edge)) into dz_b and tsum_b,
-//             dW_r = H_src^T dz_b (tcgen05 split-K, ordered reduction),
-//             da_r = sum_j tsum_b[j] z_b[j] (ordered), and the source gradient
-//             dH_src = sum_b dz_b . W_r^T (tcgen05 projection with relations along K);
-//             learnable layer-0 rows take their sparse Adam, the model its dense Adam.
-// Layer-0 inputs are gathered once per step into fp32 rows (the projection's TMA
-// operand). Inner-layer gradients are stored unmasked and masked by H > 0 when read.
+// RGAT layer type of the engine (rgat.cuh defines the layer).
+//
+// Layer 1 (hop-k blocks, sources read from the layer-0 tables), aggregate first:
+//   forward:  q_r^h = W_r^(h) a_r^h; per destination row and head the online softmax of
+//             LeakyReLU(x_j . q^h) over its edges and agg^h = sum_e alpha_e^h x_j, read from
+//             the feature / learnable table by global id (no projected source rows); then
+//             out = sum_r agg_r . W_bd,r (tcgen05 projection, relations along K, ReLU);
+//   backward: dagg = dout . W_bd^T (tcgen05), per edge dt and the ordered dq^h partials,
+//             dW_bd = agg^T dout (tcgen05 split-K), dW = its diagonal blocks + dq a^T,
+//             da = W^T dq; learnable sources also take the transposed gather into dz and
+//             dH = dz . W^T (dz carries the score term: sum_h tsum^h q^h = W (tsum a)).
+// Inner layers (sources = the previous layer's rows), project first:
+//   forward:  z_b = H_src . W_r (tcgen05), raw scores t = a . z per head, per destination
+//             row the softmax over its edges and the weighted sum of z rows;
+//   backward: per edge dt, the transposed gather over the hop's CSC view (entries =
+//             (block, edge)) into dz_b and tsum_b, dW_r = H_src^T dz_b (tcgen05 split-K),
+//             da_r = sum_j tsum_b[j] z_b[j] (ordered), dH_src = sum_b dz_b . W_r^T.
+// Inner-layer gradients are stored unmasked and masked by H > 0 where they are read.
 #include <cmath>
 #include <random>
 
@@ -23,14 +27,17 @@ namespace hetgpu {
 
 void Engine::rgat_plan(const Graph& g) {
   (void)g;
-  if (o_.heads < 1 || o_.heads > kAttMaxHeads || o_.hidden % o_.heads)
-    throw std::invalid_argument("RGAT heads must be 1..8 and divide the hidden width");
+  if (o_.heads != 1 && o_.heads != 2 && o_.heads != 4 && o_.heads != 8)
+    throw std::invalid_argument("RGAT heads must be 1, 2, 4 or 8");
+  if (o_.hidden % o_.heads) throw std::invalid_argument("RGAT heads must divide the hidden width");
   if (replica_group_.size() > 1) throw std::invalid_argument("RGAT with replica groups is not supported");
   if (o_.feat_host) throw std::invalid_argument("RGAT reads its layer-0 rows from HBM tables (feat_host = 0)");
   if (round_up4(num_classes_) > kAttMaxCols || round_up4(o_.hidden) > kAttMaxCols)
     throw std::invalid_argument("RGAT layer wider than 512 columns");
   for (auto& b : blocks_) {
-    b.need_src_grad = true;  // every block's transposed view: dz feeds its weight gradient
+    // inner blocks: every transposed view (dz feeds the weight gradient); layer-1 blocks
+    // keep theirs only for learnable sources (their rows' gradient)
+    if (b.hop < o_.k) b.need_src_grad = true;
     if (b.edge_cap >= (1 << 28)) throw std::invalid_argument("RGAT block edge capacity exceeds 2^28");
   }
 }
@@ -39,21 +46,44 @@ void Engine::rgat_alloc() {
   const int k = o_.k;
   auto round32 = [](int x) { return static_cast<std::size_t>(ceil_div(std::max(1, x), 32) * 32); };
   std::size_t wpart = 0;
+  const int halves = att_leaf_halves();
   for (auto& b : blocks_) {
     const int l = k - b.hop + 1;
-    b.ld_z = round_up4(out_dim(l));
+    const int dout = out_dim(l);
+    b.ld_z = round_up4(dout);
     b.heads = heads_of(l);
     b.src_cap = front(b.hop, b.src_t).cap;
+    b.alpha = static_cast<float*>(alloc(static_cast<std::size_t>(b.edge_cap) * b.heads * 4));
+    b.dt = static_cast<float*>(alloc(static_cast<std::size_t>(b.edge_cap) * b.heads * 4));
+    b.lse = static_cast<float*>(alloc(static_cast<std::size_t>(std::max(1, b.rows_cap)) * b.heads * 4));
+    if (b.hop == k) {
+      if (b.din > 256) throw std::invalid_argument("RGAT layer-0 rows wider than 256 columns");
+      b.din_p = round_up4(std::max(1, b.din));
+      const std::size_t ldg = static_cast<std::size_t>(b.heads) * b.din_p;
+      b.agg = static_cast<float*>(alloc(round32(b.rows_cap) * ldg * 4));
+      b.dagg = static_cast<float*>(alloc(round32(b.rows_cap) * ldg * 4));
+      b.te = static_cast<float*>(alloc(static_cast<std::size_t>(b.edge_cap) * b.heads * 4));
+      b.qv = static_cast<float*>(alloc(ldg * 4));
+      b.dqv = static_cast<float*>(alloc(static_cast<std::size_t>(att_leaf_dq_rows()) * ldg * 4));
+      b.wbd = static_cast<float*>(alloc(ldg * b.ld_z * 4));
+      b.wbdt = static_cast<float*>(alloc(static_cast<std::size_t>(dout) * ldg * 4));
+      b.dwfull = static_cast<float*>(alloc(ldg * b.ld_z * 4));
+      b.dq_part = static_cast<float*>(alloc(static_cast<std::size_t>(halves) * ldg * 4));
+      wpart += ceil_div(round32(b.rows_cap), kWChunkRows) * ldg * dout;
+      if (b.need_src_grad) {  // learnable sources: the transposed gather's dz rows
+        const std::size_t zr = round32(b.src_cap);
+        b.dz = static_cast<float*>(alloc(zr * b.ld_z * 4));
+        b.tsum = static_cast<float*>(alloc(zr * b.heads * 4));
+      }
+      continue;
+    }
     const std::size_t zr = round32(b.src_cap);
     b.z = static_cast<float*>(alloc(zr * b.ld_z * 4));
     b.sc = static_cast<float*>(alloc(zr * b.heads * 4));
-    b.lse = static_cast<float*>(alloc(static_cast<std::size_t>(std::max(1, b.rows_cap)) * b.heads * 4));
-    b.alpha = static_cast<float*>(alloc(static_cast<std::size_t>(b.edge_cap) * b.heads * 4));
-    b.dt = static_cast<float*>(alloc(static_cast<std::size_t>(b.edge_cap) * b.heads * 4));
     b.dz = static_cast<float*>(alloc(zr * b.ld_z * 4));
     b.tsum = static_cast<float*>(alloc(zr * b.heads * 4));
     b.da_part = static_cast<float*>(alloc(ceil_div(std::max(1, b.src_cap), kAttDaChunk) * b.ld_z * 4));
-    wpart += ceil_div(zr, kWChunkRows) * static_cast<std::size_t>(std::max(1, b.din)) * out_dim(l);
+    wpart += ceil_div(zr, kWChunkRows) * static_cast<std::size_t>(std::max(1, b.din)) * dout;
   }
   rgat_wpart_floats_ = std::max<std::size_t>(1, wpart);
   rgat_wpart_ = static_cast<float*>(alloc(rgat_wpart_floats_ * 4));
@@ -75,21 +105,9 @@ void Engine::rgat_alloc() {
     HG_CUDA(cudaMemcpyAsync(s.a, host.data(), host.size() * 4, cudaMemcpyHostToDevice, st_));
     HG_CUDA(cudaStreamSynchronize(st_));
   }
-  leaf_x_.assign(ntypes_, nullptr);
-  leaf_ld_.assign(ntypes_, 0);
-  for (int bi : hop_blocks_[k]) {
-    const int t = blocks_[bi].src_t;
-    if (leaf_x_[t] || !tables_[t].w || front(k, t).cap <= 0) continue;
-    leaf_ld_[t] = round_up4(std::max(1, tables_[t].dim));
-    leaf_x_[t] = static_cast<float*>(alloc(round32(front(k, t).cap) * leaf_ld_[t] * 4));
-  }
 }
 
 const float* Engine::rgat_src(const BlockBuf& b, int& ld) {
-  if (b.hop == o_.k) {
-    ld = leaf_ld_[b.src_t];
-    return leaf_x_[b.src_t];
-  }
   for (const auto& gr : groups_)
     if (gr.depth - 1 == b.hop && gr.type == b.src_t) {
       ld = gr.ld;
@@ -98,22 +116,70 @@ const float* Engine::rgat_src(const BlockBuf& b, int& ld) {
   throw std::runtime_error("RGAT: no layer input for a block's source type");
 }
 
+namespace {
+template <typename B, typename S>
+AttLeafParam leaf_param(const B& b, const S& s) {
+  return AttLeafParam{s.w, s.a, b.din, b.din_p, s.dout, s.ld, b.heads, b.qv, b.wbd, b.wbdt, b.dwfull, b.dq_part,
+                      b.dqv, s.g, s.ag};
+}
+}  // namespace
+
 void Engine::run_forward_rgat() {
   const int k = o_.k;
   HG_CUDA(cudaMemsetAsync(logits_, 0, static_cast<std::size_t>(o_.batch_cap + 1) * ldc_ * 4, st_));
-  LeafGatherBatch lg{};
-  for (int t = 0; t < ntypes_; ++t) {
-    if (!leaf_x_[t]) continue;
-    const TypeTable& tb = tables_[t];
-    lg.j[lg.n++] = {tb.w, tb.ld, tb.dense ? tb.dtype : static_cast<int>(kF32), tb.dim, front(k, t).list,
-                    front(k, t).count, front(k, t).cap, leaf_x_[t], leaf_ld_[t]};
-  }
-  timed("leaf_gather", 0, [&] { leaf_gather(lg, st_); });
   for (int l = 1; l <= k; ++l) {
     const int d = k - l + 1;
     const bool top = l == k;
-    // (1) z_b = H_src . W_r over every block's source frontier, (2) raw scores
     std::vector<ProjBatch> pbs(1);
+    if (l == 1) {
+      // (1) q and W_bd of every layer-1 relation, (2) per-head aggregates from the tables
+      AttLeafParams lp{};
+      AttLeafBatch lb{};
+      for (const auto& gr : groups_) {
+        if (gr.layer != 1) continue;
+        for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
+          const BlockBuf& b = blocks_[gr.blocks[q]];
+          const Slot& s = slots_[gr.slots[q]];
+          const TypeTable& tb = tables_[b.src_t];
+          lp.p[lp.n++] = leaf_param(b, s);
+          lb.j[lb.n++] = {b.indptr, b.src, tb.w, tb.ld, tb.dense ? tb.dtype : static_cast<int>(kF32), b.din, b.din_p,
+                          block_rows(b), b.rows_cap, b.qv, b.te, b.lse, b.alpha, b.agg, b.dagg, b.dt, b.dq_part,
+                          b.heads};
+        }
+      }
+      timed("rgat_prep", 0, [&] { att_leaf_prep(lp, st_); });
+      timed(top ? "rgat_attend_top" : "rgat_attend", 0, [&] { att_leaf_forward(lb, st_); });
+      // (3) out = sum_r agg_r . W_bd,r (+ReLU): the RGCN projection's shape
+      for (const auto& gr : groups_) {
+        if (gr.layer != 1) continue;
+        if (gr.blocks.empty()) {
+          if (!top) zero_rows(gr.out, gr.ld, front(gr.depth - 1, gr.type).count, gr.rows_cap, st_);
+          continue;
+        }
+        if (pbs.back().ng == kProjGroups) pbs.emplace_back();
+        ProjGroup& pg = pbs.back().g[pbs.back().ng++];
+        pg.nrel = static_cast<int>(gr.blocks.size());
+        pg.n_rows = front(gr.depth - 1, gr.type).count;
+        pg.rows_cap = gr.rows_cap;
+        pg.out = gr.out;
+        pg.ld_out = gr.ld;
+        pg.dout = gr.dout;
+        pg.relu = top ? 0 : 1;
+        pg.out_stride = 1;
+        pg.out_offset = 0;
+        for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
+          const BlockBuf& b = blocks_[gr.blocks[q]];
+          const Slot& s = slots_[gr.slots[q]];
+          const int ldg = b.heads * b.din_p;
+          pg.r[q] = {b.agg, ldg, ldg, b.wbd, s.ld};
+        }
+      }
+      timed(top ? "rgat_project_top" : "rgat_project", 0, [&] {
+        for (auto& pb : pbs) use_umma_ ? project_umma(pb, st_) : project_tiles(pb, st_);
+      });
+      continue;
+    }
+    // inner layers: (1) z_b = H_src . W_r over every block's source frontier, (2) raw scores
     AttScoreBatch sb{};
     for (const auto& gr : groups_) {
       if (gr.layer != l) continue;
@@ -123,8 +189,7 @@ void Engine::run_forward_rgat() {
         int ld_src = 0;
         const float* src = rgat_src(b, ld_src);
         if (pbs.back().ng == kProjGroups) pbs.emplace_back();
-        ProjBatch& pb = pbs.back();
-        ProjGroup& pg = pb.g[pb.ng++];
+        ProjGroup& pg = pbs.back().g[pbs.back().ng++];
         pg.nrel = 1;
         pg.n_rows = front(d, b.src_t).count;
         pg.rows_cap = b.src_cap;
@@ -201,31 +266,6 @@ void Engine::run_backward_rgat() {
   for (int l = k; l >= 1; --l) {
     const int d = k - l + 1;
     const bool top = l == k;
-    // (1) per edge dt: softmax and LeakyReLU backward
-    std::vector<AttBatch> abs(1);
-    for (const auto& gr : groups_) {
-      if (gr.layer != l || gr.blocks.empty()) continue;
-      if (abs.back().ng == kProjGroups) abs.emplace_back();
-      AttGroup& ag = abs.back().g[abs.back().ng++];
-      ag.nrel = static_cast<int>(gr.blocks.size());
-      for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
-        const BlockBuf& b = blocks_[gr.blocks[q]];
-        ag.r[q] = {b.indptr, b.col, b.z, b.sc, b.lse, b.alpha, b.dt};
-      }
-      ag.n_rows = front(gr.depth - 1, gr.type).count;
-      ag.rows_cap = gr.rows_cap;
-      ag.out = nullptr;
-      ag.dout = gr.dout_buf;
-      ag.relu_h = top ? nullptr : gr.out;
-      ag.ld = gr.ld;
-      ag.cols = gr.dout;
-      ag.heads = heads_of(l);
-      ag.relu = 0;
-    }
-    timed("rgat_edge_grad", 0, [&] {
-      for (auto& ab : abs) att_edge_grad(ab, st_);
-    });
-    // (2) transposed gather over the hop's CSC view: dz_b, tsum_b
     const CscHop ch = csc_hop(d);
     AttScatter sc{};
     sc.nt = ch.nt;
@@ -241,13 +281,9 @@ void Engine::run_backward_rgat() {
       bool typed = false;
       for (const auto& c : cscs_)
         if (c.hop == d && c.src_t == b.src_t) typed = true;
-      if (!b.need_src_grad || !typed) continue;
-      scatter_blocks.push_back(bi);
+      if (b.need_src_grad && typed) scatter_blocks.push_back(bi);
     }
     if (static_cast<int>(scatter_blocks.size()) != ch.nb) throw std::runtime_error("RGAT: CSC block order mismatch");
-    WGradBatch wb{};
-    AttDaBatch db{};
-    std::size_t off = 0;
     for (int q = 0; q < ch.nb; ++q) {
       const BlockBuf& b = blocks_[scatter_blocks[q]];
       const Group* gr = group_of(d - 1, b.dst_t);
@@ -255,31 +291,113 @@ void Engine::run_backward_rgat() {
       if (!gr) throw std::runtime_error("RGAT: block without a destination group");
       sc.b[sc.nb++] = {b.erow, b.alpha, b.dt, gr->dout_buf, top ? nullptr : gr->out, gr->ld, s.a, b.dz, b.tsum,
                        b.ld_z, s.dout, b.heads, ch.b[q].type};
-      db.j[db.n++] = {b.tsum, b.z, front(d, b.src_t).count, b.src_cap, b.ld_z, s.dout, b.heads, b.da_part, s.ag};
-      int ld_src = 0;
-      const float* src = rgat_src(b, ld_src);
-      if (wb.np == kMaxProblems) throw std::runtime_error("too many RGAT weight-gradient problems per layer");
-      // the operands' row extent; rows [n, next multiple of 32) of dz are zero
-      const int rows_cap = std::max(1, b.src_cap);
-      wb.p[wb.np++] = {src, ld_src, b.din, DpreView{b.dz, nullptr, b.ld_z, s.dout, 1, 0}, front(d, b.src_t).count,
-                       rows_cap, rgat_wpart_ + off, s.g, s.ld, nullptr, nullptr, nullptr};
-      off += ceil_div(rows_cap, kWChunkRows) * static_cast<std::size_t>(std::max(1, b.din)) * s.dout;
     }
-    if (off > rgat_wpart_floats_) throw std::runtime_error("RGAT weight-gradient scratch too small");
-    timed(top ? "rgat_scatter_top" : "rgat_scatter", 0, [&] { att_scatter(sc, st_); });
-    timed("rgat_att_grad", 0, [&] { att_da(db, st_); });
-    timed("rgat_weight_grad", 0, [&] { use_umma_ ? wgrad_umma(wb, st_) : wgrad_tiles(wb, st_); });
-    // (3) source gradients dH_src = sum_b dz_b . W_r^T (inner types and learnable leaves)
+    if (l == 1) {
+      // layer 1: dout masked in place, dagg = dout . W_bd^T, per edge dt + dq partials,
+      // dW_bd = agg^T dout, then dW / da
+      if (!top)
+        for (const auto& gr : groups_)
+          if (gr.layer == 1 && !gr.blocks.empty())
+            relu_mask(gr.dout_buf, gr.out, gr.ld, front(gr.depth - 1, gr.type).count, gr.rows_cap, st_);
+      std::vector<ProjBatch> dbs(1);
+      AttLeafBatch lb{};
+      AttLeafParams lp{};
+      WGradBatch wb{};
+      std::size_t off = 0;
+      for (const auto& gr : groups_) {
+        if (gr.layer != 1) continue;
+        for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
+          const BlockBuf& b = blocks_[gr.blocks[q]];
+          const Slot& s = slots_[gr.slots[q]];
+          const TypeTable& tt = tables_[b.src_t];
+          const int ldg = b.heads * b.din_p;
+          if (dbs.back().ng == kProjGroups) dbs.emplace_back();
+          ProjGroup& pg = dbs.back().g[dbs.back().ng++];
+          pg.nrel = 1;
+          pg.n_rows = block_rows(b);
+          pg.rows_cap = b.rows_cap;
+          pg.out = b.dagg;
+          pg.ld_out = ldg;
+          pg.dout = ldg;
+          pg.relu = 0;
+          pg.out_stride = 1;
+          pg.out_offset = 0;
+          pg.r[0] = {gr.dout_buf, gr.ld, gr.dout, b.wbdt, ldg};
+          lb.j[lb.n++] = {b.indptr, b.src, tt.w, tt.ld, tt.dense ? tt.dtype : static_cast<int>(kF32), b.din, b.din_p,
+                          block_rows(b), b.rows_cap, b.qv, b.te, b.lse, b.alpha, b.agg, b.dagg, b.dt, b.dq_part,
+                          b.heads};
+          lp.p[lp.n++] = leaf_param(b, s);
+          if (wb.np == kMaxProblems) throw std::runtime_error("too many RGAT weight-gradient problems per layer");
+          const int rows_cap = std::max(1, b.rows_cap);
+          wb.p[wb.np++] = {b.agg, ldg, ldg, DpreView{gr.dout_buf, nullptr, gr.ld, gr.dout, 1, 0}, block_rows(b), rows_cap,
+                           rgat_wpart_ + off, b.dwfull, s.ld, nullptr, nullptr, nullptr};
+          off += ceil_div(ceil_div(rows_cap, 32) * 32, kWChunkRows) * static_cast<std::size_t>(ldg) * gr.dout;
+        }
+      }
+      if (off > rgat_wpart_floats_) throw std::runtime_error("RGAT weight-gradient scratch too small");
+      timed("rgat_dagg", 0, [&] {
+        for (auto& pb : dbs) use_umma_ ? project_umma(pb, st_) : project_tiles(pb, st_);
+      });
+      timed("rgat_edge_grad", 0, [&] { att_leaf_grad(lb, st_); });
+      timed("rgat_weight_grad", 0, [&] { use_umma_ ? wgrad_umma(wb, st_) : wgrad_tiles(wb, st_); });
+      timed("rgat_att_grad", 0, [&] { att_leaf_finish(lp, st_); });
+      if (sc.nb) timed("rgat_scatter", 0, [&] { att_scatter(sc, st_); });
+    } else {
+      // inner layers: per edge dt, the transposed gather (dz, tsum), da, dW
+      std::vector<AttBatch> abs(1);
+      for (const auto& gr : groups_) {
+        if (gr.layer != l || gr.blocks.empty()) continue;
+        if (abs.back().ng == kProjGroups) abs.emplace_back();
+        AttGroup& ag = abs.back().g[abs.back().ng++];
+        ag.nrel = static_cast<int>(gr.blocks.size());
+        for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
+          const BlockBuf& b = blocks_[gr.blocks[q]];
+          ag.r[q] = {b.indptr, b.col, b.z, b.sc, b.lse, b.alpha, b.dt};
+        }
+        ag.n_rows = front(gr.depth - 1, gr.type).count;
+        ag.rows_cap = gr.rows_cap;
+        ag.out = nullptr;
+        ag.dout = gr.dout_buf;
+        ag.relu_h = top ? nullptr : gr.out;
+        ag.ld = gr.ld;
+        ag.cols = gr.dout;
+        ag.heads = heads_of(l);
+        ag.relu = 0;
+      }
+      timed("rgat_edge_grad", 0, [&] {
+        for (auto& ab : abs) att_edge_grad(ab, st_);
+      });
+      WGradBatch wb{};
+      AttDaBatch db{};
+      std::size_t off = 0;
+      for (int q = 0; q < ch.nb; ++q) {
+        const BlockBuf& b = blocks_[scatter_blocks[q]];
+        const Slot& s = slots_[slot_of_.at(SlotId{b.rel, l})];
+        db.j[db.n++] = {b.tsum, b.z, front(d, b.src_t).count, b.src_cap, b.ld_z, s.dout, b.heads, b.da_part, s.ag};
+        int ld_src = 0;
+        const float* src = rgat_src(b, ld_src);
+        if (wb.np == kMaxProblems) throw std::runtime_error("too many RGAT weight-gradient problems per layer");
+        // the operands' row extent; rows [n, next multiple of 32) of dz are zero
+        const int rows_cap = std::max(1, b.src_cap);
+        wb.p[wb.np++] = {src, ld_src, b.din, DpreView{b.dz, nullptr, b.ld_z, s.dout, 1, 0}, front(d, b.src_t).count,
+                         rows_cap, rgat_wpart_ + off, s.g, s.ld, nullptr, nullptr, nullptr};
+        off += ceil_div(rows_cap, kWChunkRows) * static_cast<std::size_t>(std::max(1, b.din)) * s.dout;
+      }
+      if (off > rgat_wpart_floats_) throw std::runtime_error("RGAT weight-gradient scratch too small");
+      timed(top ? "rgat_scatter_top" : "rgat_scatter", 0, [&] { att_scatter(sc, st_); });
+      timed("rgat_att_grad", 0, [&] { att_da(db, st_); });
+      timed("rgat_weight_grad", 0, [&] { use_umma_ ? wgrad_umma(wb, st_) : wgrad_tiles(wb, st_); });
+    }
+    // source gradients dH_src = sum_b dz_b . W_r^T (inner types and learnable leaves)
     std::vector<ProjBatch> pbs(1);
     for (const auto& c : cscs_) {
       if (c.hop != d || !c.dh) continue;
       if (pbs.back().ng == kProjGroups) pbs.emplace_back();
-      ProjBatch& pb = pbs.back();
-      ProjGroup& pg = pb.g[pb.ng++];
+      ProjGroup& pg = pbs.back().g[pbs.back().ng++];
       pg.nrel = 0;
       for (int bi : hop_blocks_[d]) {
         const BlockBuf& b = blocks_[bi];
-        if (b.src_t != c.src_t) continue;
+        if (b.src_t != c.src_t || !b.dz) continue;
         const Slot& s = slots_[slot_of_.at(SlotId{b.rel, l})];
         if (pg.nrel == kProjRels) throw std::runtime_error("too many relations out of one source type");
         pg.r[pg.nrel++] = {b.dz, b.ld_z, s.dout, s.wt, s.ld_wt};
@@ -297,7 +415,7 @@ void Engine::run_backward_rgat() {
       for (auto& pb : pbs)
         if (pb.ng) use_umma_ ? project_umma(pb, st_) : project_tiles(pb, st_);
     });
-    // (4) learnable layer-0 rows: sparse Adam (step += 1 iff the type has rows)
+    // learnable layer-0 rows: sparse Adam (step += 1 iff the type has rows)
     if (d == k && apply_adam_) {
       AdamRowsBatch rb{};
       int base4 = 0;

@@ -112,21 +112,62 @@ struct AttDaBatch {
 constexpr int kAttDaChunk = 256;
 void att_da(const AttDaBatch& b, cudaStream_t st);
 
-// layer-0 rows of the source frontier as fp32 GEMM operands: out[i] = table[ids[i]]
-struct LeafGatherJob {
+// ---- layer 1 (leaf sources): aggregate first. With q_r^h = W_r^(h) a_r^h the score is
+// t = x_j . q^h, so per destination row the kernel forms agg^h = sum_e alpha_e^h x_src(e)
+// straight from the feature / learnable table (by global id), and the projection reads
+// agg [rows x H din_p] against the block-diagonal W_bd [H din_p x d_out]; backward:
+// dagg = dout . W_bd^T, dt per edge, dq^h = sum_e dt_e^h x_src(e) (ordered partials),
+// dW = diag blocks of agg^T dout + dq a^T, da = W^T dq.
+struct AttLeafJob {
+  const std::uint32_t* indptr;
+  const std::uint32_t* keys;  // per edge: global source id
   const void* table;
-  int ld_t, dtype, dim;
-  const std::uint32_t* ids;
-  const int* n;
-  int cap;
-  float* out;
-  int ld_out;
+  int ld_t, dtype, din, din_p;  // din_p = round_up4(din): row stride of one head's block
+  const int* n_rows;
+  int rows_cap;
+  const float* q;    // [H x din_p]
+  float* te;         // [edges x H] raw scores
+  float* lse;        // [rows x H]
+  float* alpha;      // [edges x H]
+  float* agg;        // [rows x H din_p]; rows [n, next multiple of 32) zeroed
+  const float* dagg; // backward: [rows x H din_p]
+  float* dt;         // backward: [edges x H]
+  float* dq_part;    // backward: [halves x H din_p]
+  int heads;
 };
-struct LeafGatherBatch {
-  LeafGatherJob j[kMaxSegs];
+struct AttLeafBatch {
+  AttLeafJob j[kMaxBlocks];
   int n;
 };
-void leaf_gather(const LeafGatherBatch& b, cudaStream_t st);
+void att_leaf_forward(const AttLeafBatch& b, cudaStream_t st);
+// fixed grid (att_leaf_halves() half-warps): each half-warp's dq partial is a fixed sum
+void att_leaf_grad(const AttLeafBatch& b, cudaStream_t st);
+int att_leaf_halves();
+
+// per layer-1 block: q = W^(h) a^(h), W_bd and W_bd^T (prep); dW / da from the
+// block-diagonal weight gradient and the reduced dq (finish)
+struct AttLeafParam {
+  const float* w;  // [din x ld_w]
+  float* a;        // [ld_w]
+  int din, din_p, dout, ld_w, heads;
+  float* q;        // [H x din_p]
+  float* wbd;      // [H din_p x ld_w]
+  float* wbdt;     // [dout x H din_p]
+  const float* dwfull;  // [H din_p x ld_w]
+  const float* dq_part; // [halves x H din_p]
+  float* dq;            // [att_leaf_dq_rows() x H din_p]: group sums, then dq
+  float* dw;       // [din x ld_w]
+  float* da;       // [ld_w]
+};
+struct AttLeafParams {
+  AttLeafParam p[kMaxBlocks];
+  int n;
+};
+void att_leaf_prep(const AttLeafParams& p, cudaStream_t st);
+void att_leaf_finish(const AttLeafParams& p, cudaStream_t st);
+int att_leaf_dq_rows();
+// x[i][c] = 0 where h[i][c] <= 0 (rows < n): the ReLU mask of an inner layer's gradient
+void relu_mask(float* x, const float* h, int ld, const int* n, int rows_cap, cudaStream_t st);
 
 // W^T of every slot (the source-gradient contraction reads dz . W^T as a projection)
 struct TransposeJob {

@@ -400,8 +400,11 @@ void project_umma(ProjBatch& pb, cudaStream_t st) {
   int nt = 32;
   for (int g = 0; g < pb.ng; ++g) nt = std::max(nt, pick_nt(pb.g[g].ld_out));
   // at most 64 columns per tile: the top layer (C = 349) then runs 48 CTAs
-  // instead of 24, which shortens its latency-bound launch (measured +2%)
-  nt = std::min(nt, HG_PROJ_NT);
+  // instead of 24, which shortens its latency-bound launch (measured +2%); outputs of
+  // 512+ columns (RGAT's per-head aggregates) keep 128-wide tiles (half the CTAs)
+  int widest = 0;
+  for (int g = 0; g < pb.ng; ++g) widest = std::max(widest, pb.g[g].ld_out);
+  if (widest < 512) nt = std::min(nt, HG_PROJ_NT);
   int tiles = 0;
   for (int g = 0; g < pb.ng; ++g) {
     const ProjGroup& G = pb.g[g];
