@@ -640,16 +640,22 @@ struct ExecutionReport {
   std::vector<Message> trace;
 };
 
+// layer type of the engine: the reference's RGCN (hgnn.cpp:173-362), or relational graph
+// attention (no reference counterpart, oracle/rgat.py) with `heads` heads
+enum class LayerKind : int { RGCN = 0, RGAT = 1 };
+
 class RafEngine {
  public:
   // init_model / init_learnable seeds as run_experiment derives them (harness.cpp:365-366)
   // feat_dtype: storage of the dense feature tables (0 f32, 1 f16, 2 bf16); feat_host: keep
   // them in pinned host memory with an HBM cache of the set_cache rows
   RafEngine(const HetGraph& g, std::vector<int> fanouts, int hidden, std::uint64_t seed, int batch_cap = 1024,
-            int p = 1, int rank = 0, int device = 0, int feat_dtype = 0, bool feat_host = false)
+            int p = 1, int rank = 0, int device = 0, int feat_dtype = 0, bool feat_host = false,
+            LayerKind kind = LayerKind::RGCN, int heads = 4)
       : g_(g), fanouts_(std::move(fanouts)) {
     const hg_engine_opts o{static_cast<int>(fanouts_.size()), fanouts_.data(), hidden, batch_cap, p, rank,
-                           mix_seed(seed, 0xd0de1), mix_seed(seed, 0x1ea4a), device, feat_dtype, feat_host ? 1 : 0};
+                           mix_seed(seed, 0xd0de1), mix_seed(seed, 0x1ea4a), device, feat_dtype, feat_host ? 1 : 0,
+                           static_cast<int>(kind), heads};
     e_.reset(detail::check(hg_engine_create(g.handle(), &o)));
   }
   // run_raf_batch (raf.cpp:344-530) + adam_update_model + adam_update_rows, as the

@@ -1055,7 +1055,14 @@ void Engine::run_forward() {
       for (auto& pb : pbs) use_umma_ ? project_umma(pb, st_) : project_tiles(pb, st_);
     });
   }
-  // AGG_all: sum the partial logits of every partition (raf.cpp:427-446)
+  run_agg_all();
+  if (o_.p > 1 && training_ && replica_group_.size() > 1) replica_prepare();
+}
+
+// AGG_all: sum the partial logits of every partition (raf.cpp:427-446); the counter
+// row records which batch rows had a sampled top-level edge on this partition
+void Engine::run_agg_all() {
+  const int k = o_.k;
   if (o_.p > 1) {
     EdgeCountArgs ec{};
     for (int bi : hop_blocks_[1]) {
@@ -1073,8 +1080,8 @@ void Engine::run_forward() {
       });
     }
 #endif
-    if (training_ && replica_group_.size() > 1) replica_prepare();
   }
+  (void)k;
 }
 
 void Engine::run_loss(bool train) {
@@ -1191,10 +1198,14 @@ void Engine::run_replica_merge() {
   timed("replica_wgrad", 0, [&] {
     if (counting_) return;
     if (ncclGroupStart() != ncclSuccess) throw std::runtime_error("ncclGroupStart failed");
-    for (auto& sl : slots_)
+    for (auto& sl : slots_) {
       if (ncclAllReduce(sl.g, sl.g, static_cast<std::size_t>(std::max(1, sl.din)) * sl.ld, ncclFloat, ncclSum, rcomm_,
                         st_) != ncclSuccess)
         throw std::runtime_error("ncclAllReduce (replica weight gradients) failed");
+      if (sl.ag && ncclAllReduce(sl.ag, sl.ag, static_cast<std::size_t>(sl.ld), ncclFloat, ncclSum, rcomm_, st_) !=
+                       ncclSuccess)  // RGAT attention vectors
+        throw std::runtime_error("ncclAllReduce (replica attention gradients) failed");
+    }
     if (ncclGroupEnd() != ncclSuccess) throw std::runtime_error("ncclGroupEnd failed");
   });
   // 2. learnable rows: the union and row slots were built by replica_prepare

@@ -307,6 +307,7 @@ class Engine {
   void upload_dense(const NodeTypeInfo& nt, TypeTable& tb);
   void run_sampling(cudaStream_t ss);  // everything of one sample slot, on stream ss
   void run_forward();
+  void run_agg_all();  // AGG_all of the partial logits (p > 1)
   void run_loss(bool train);
   void run_backward();
   void run_update();

@@ -30,7 +30,8 @@ void Engine::rgat_plan(const Graph& g) {
   if (o_.heads != 1 && o_.heads != 2 && o_.heads != 4 && o_.heads != 8)
     throw std::invalid_argument("RGAT heads must be 1, 2, 4 or 8");
   if (o_.hidden % o_.heads) throw std::invalid_argument("RGAT heads must divide the hidden width");
-  if (replica_group_.size() > 1) throw std::invalid_argument("RGAT with replica groups is not supported");
+  if (replica_group_.size() > 1 && o_.k == 1)
+    throw std::invalid_argument("RGAT with replica groups needs at least two layers");
   if (o_.feat_host) throw std::invalid_argument("RGAT reads its layer-0 rows from HBM tables (feat_host = 0)");
   if (round_up4(num_classes_) > kAttMaxCols || round_up4(o_.hidden) > kAttMaxCols)
     throw std::invalid_argument("RGAT layer wider than 512 columns");
@@ -225,8 +226,9 @@ void Engine::run_forward_rgat() {
         const BlockBuf& b = blocks_[gr.blocks[q]];
         ag.r[q] = {b.indptr, b.col, b.z, b.sc, b.lse, b.alpha, b.dt};
       }
-      ag.n_rows = front(gr.depth - 1, gr.type).count;
-      ag.rows_cap = gr.rows_cap;
+      const bool shard = top && replica_;  // a replica trains its shard of the batch rows
+      ag.n_rows = shard ? shard_count_dev_ : front(gr.depth - 1, gr.type).count;
+      ag.rows_cap = shard ? static_cast<int>(ceil_div(o_.batch_cap, shard_count_)) : gr.rows_cap;
       ag.out = gr.out;
       ag.dout = nullptr;
       ag.relu_h = nullptr;
@@ -234,23 +236,15 @@ void Engine::run_forward_rgat() {
       ag.cols = gr.dout;
       ag.heads = heads_of(l);
       ag.relu = top ? 0 : 1;
+      ag.row_stride = top ? shard_count_ : 1;
+      ag.row_offset = top ? shard_index_ : 0;
     }
     timed(top ? "rgat_attend_top" : "rgat_attend", 0, [&] {
       for (auto& ab : abs) att_forward(ab, st_);
     });
   }
-  // AGG_all: sum the partial logits of every partition (raf.cpp:427-446)
-  if (o_.p > 1) {
-#ifdef HG_WITH_NCCL
-    if (comm_ && !counting_) {
-      timed("agg_all", static_cast<double>(o_.batch_cap + 1) * ldc_ * 4, [&] {
-        if (ncclAllReduce(logits_, logits_, static_cast<std::size_t>(o_.batch_cap + 1) * ldc_, ncclFloat, ncclSum,
-                          comm_, st_) != ncclSuccess)
-          throw std::runtime_error("ncclAllReduce failed");
-      });
-    }
-#endif
-  }
+  run_agg_all();
+  if (o_.p > 1 && training_ && replica_group_.size() > 1) replica_prepare();
 }
 
 void Engine::run_backward_rgat() {
@@ -290,7 +284,7 @@ void Engine::run_backward_rgat() {
       const Slot& s = slots_[slot_of_.at(SlotId{b.rel, l})];
       if (!gr) throw std::runtime_error("RGAT: block without a destination group");
       sc.b[sc.nb++] = {b.erow, b.alpha, b.dt, gr->dout_buf, top ? nullptr : gr->out, gr->ld, s.a, b.dz, b.tsum,
-                       b.ld_z, s.dout, b.heads, ch.b[q].type};
+                       b.ld_z, s.dout, b.heads, ch.b[q].type, top ? shard_count_ : 1, top ? shard_index_ : 0};
     }
     if (l == 1) {
       // layer 1: dout masked in place, dagg = dout . W_bd^T, per edge dt + dq partials,
@@ -354,8 +348,9 @@ void Engine::run_backward_rgat() {
           const BlockBuf& b = blocks_[gr.blocks[q]];
           ag.r[q] = {b.indptr, b.col, b.z, b.sc, b.lse, b.alpha, b.dt};
         }
-        ag.n_rows = front(gr.depth - 1, gr.type).count;
-        ag.rows_cap = gr.rows_cap;
+        const bool shard = top && replica_;
+        ag.n_rows = shard ? shard_count_dev_ : front(gr.depth - 1, gr.type).count;
+        ag.rows_cap = shard ? static_cast<int>(ceil_div(o_.batch_cap, shard_count_)) : gr.rows_cap;
         ag.out = nullptr;
         ag.dout = gr.dout_buf;
         ag.relu_h = top ? nullptr : gr.out;
@@ -363,6 +358,8 @@ void Engine::run_backward_rgat() {
         ag.cols = gr.dout;
         ag.heads = heads_of(l);
         ag.relu = 0;
+        ag.row_stride = top ? shard_count_ : 1;
+        ag.row_offset = top ? shard_index_ : 0;
       }
       timed("rgat_edge_grad", 0, [&] {
         for (auto& ab : abs) att_edge_grad(ab, st_);
@@ -420,7 +417,7 @@ void Engine::run_backward_rgat() {
       AdamRowsBatch rb{};
       int base4 = 0;
       for (const auto& c : cscs_) {
-        if (c.hop != k || !c.dh || !tables_[c.src_t].learnable) continue;
+        if (c.hop != k || !c.dh || !tables_[c.src_t].learnable || xchg_type(c.src_t)) continue;  // replicas: merged
         TypeTable& t = tables_[c.src_t];
         rb.t[rb.n] = {t.w, t.m, t.v, t.ld, front(k, c.src_t).list, c.dh, c.ld, front(k, c.src_t).count, t.step};
         rb.base4[rb.n] = base4;
@@ -431,6 +428,10 @@ void Engine::run_backward_rgat() {
       AdamHyper hp;
       timed("rgat_adam_rows", 0, [&] { adam_rows(rb, hp, err_, st_); });
     }
+  }
+  if (replica_group_.size() > 1) {
+    join();  // the union of the replicas' leaf ids (replica_prepare, side stream)
+    run_replica_merge();
   }
 }
 

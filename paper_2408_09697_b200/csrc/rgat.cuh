@@ -44,6 +44,9 @@ struct AttGroup {  // one destination type of one layer
   int ld;
   int cols, heads;
   int relu;
+  // row i of out / dout / relu_h is row i * row_stride + row_offset (a replica's shard of
+  // the batch writes its rows of the full logits, raf.cpp:390-391)
+  int row_stride, row_offset;
 };
 struct AttBatch {
   AttGroup g[kProjGroups];
@@ -84,6 +87,7 @@ struct AttScatterBlock {
   float* tsum;
   int ld, cols, heads;
   int type;  // index into the hop's CscHop::t
+  int row_stride, row_offset;  // destination row -> dout row (replica shards)
 };
 struct AttScatter {
   AttScatterBlock b[kMaxBlocks];

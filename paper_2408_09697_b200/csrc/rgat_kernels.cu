@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(256) k_att_forward(AttBatch b, int total) {
         }
       }
     }
-    float* o = G.out + static_cast<std::size_t>(i) * G.ld;
+    float* o = G.out + (static_cast<std::size_t>(i) * G.row_stride + G.row_offset) * G.ld;
 #pragma unroll
     for (int u = 0; u < NU4; ++u) {
       const int c = 4 * hl + 4 * GL * u;
@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(256) k_att_edge_grad(AttBatch b, int total) {
       hu[u] = c < G.cols ? c / F : -1;
       dv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (u < nu4 && c < G.ld) {
-        const std::size_t at = static_cast<std::size_t>(i) * G.ld + c;
+        const std::size_t at = (static_cast<std::size_t>(i) * G.row_stride + G.row_offset) * G.ld + c;
         dv[u] = ld4(G.dout + at);
         if (G.relu_h) {
           const float4 hv = ld4(G.relu_h + at);
@@ -444,8 +444,9 @@ __global__ void __launch_bounds__(256) k_att_scatter(AttScatter s, int total) {
           al[h] = __shfl_sync(hm, my_al[h], qq, GL);
           ts[h] += __shfl_sync(hm, my_dt[h], qq, GL);
         }
-        const float* dr = B.dout + static_cast<std::size_t>(row) * B.ld_dout;
-        const float* mr = B.relu_h ? B.relu_h + static_cast<std::size_t>(row) * B.ld_dout : nullptr;
+        const std::size_t drow = static_cast<std::size_t>(row) * B.row_stride + B.row_offset;
+        const float* dr = B.dout + drow * B.ld_dout;
+        const float* mr = B.relu_h ? B.relu_h + drow * B.ld_dout : nullptr;
         float4 d4[NU4];
 #pragma unroll
         for (int u = 0; u < NU4; ++u) {

@@ -305,6 +305,17 @@ int main() {
       EXPECT(brep.sync_bytes == rrep.sync_bytes, "ExecutionReport::sync_bytes");
       EXPECT(brep.cross_ids_target_only == rrep.cross_ids_target_only, "ExecutionReport::cross_ids_target_only");
     }
+    // the RGAT layer type behind the same engine interface (no reference counterpart:
+    // tests/test_rgat.py holds its parity): training on one batch lowers its loss
+    B::RafEngine att(bg, fanouts, hidden, seed, 256, 1, 0, 0, 0, false, B::LayerKind::RGAT, 4);
+    double first = 0.0, last = 0.0;
+    for (int it = 0; it < 8; ++it) {
+      const double l = att.run_raf_batch(batches[0], R::mix_seed(seed, 0xb000), 0).loss;
+      if (it == 0) first = l;
+      last = l;
+    }
+    std::printf("RGAT loss %.6f -> %.6f\n", first, last);
+    EXPECT(std::isfinite(last) && last < first, "RGAT engine trains");
   }
 
   // sample_neighbors (sampling.hpp:34-35) on raw CSRs: every row of several relations

@@ -28,6 +28,8 @@ def main():
         import numpy as _np
         sw = H.sub_work(g, [25, 20], 4, bsz, seed, device=rank)
         kw["sub_work"] = _np.concatenate([sw["work"], sw["learn_rows"]])
+    if os.environ.get("HG_MODEL", "rgcn") != "rgcn":  # the RGAT layer type (tests/test_rgat.py)
+        kw["model"] = os.environ["HG_MODEL"]
     eng = H.Engine.for_experiment(g, [25, 20], 32, seed, batch_cap=bsz, p=p, rank=rank, device=rank, **kw)
     if rank == 0:
         uid = H.nccl_unique_id()
@@ -73,7 +75,8 @@ def main():
         bound_ok.append(int(rep["message_bound_ok"]))
         target_ok.append(int(rep["target_only_ok"]))
         boundary = (rep["boundary_counts"], rep["boundary_cut_edges"])
-    post = eng.read(*[n for n in eng.tensor_names() if n.startswith(("post.r", "post.learn.t", "post.learn_step.t"))])
+    post = eng.read(*[n for n in eng.tensor_names()
+                      if n.startswith(("post.r", "post.learn.t", "post.learn_step.t", "att."))])
     np.savez(out_path, losses=np.asarray(losses), active=np.asarray(active, np.int64),
              sync=np.asarray(sync, np.uint64), lead=np.asarray(lead), bound_ok=np.asarray(bound_ok),
              target_ok=np.asarray(target_ok), boundary=np.asarray(boundary[0], np.uint64),

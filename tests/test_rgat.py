@@ -222,3 +222,51 @@ def test_rgat_c2_step_matches_oracle(H, ref):
     for t, (ids, rows) in fg.items():
         assert [int(x) for x in got[f"grad.f.t{t}.ids"]] == ids
         assert_close(got[f"grad.f.t{t}.rows"], rows, TOL, f"C3 grad.f.t{t}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p", [2, 4])
+def test_rgat_multi_gpu_matches_one_gpu(H, p):
+    """C3 at p GPUs (BASELINE configs[2] runs RGAT on 4): one meta-partition per GPU, AGG_all
+    of the partial logits over NCCL; at p = 4 one sub-metatree is replicated (its replicas
+    split the batch and merge weight, attention and learnable-row gradients). Every
+    batch's loss and the trained model match the single-GPU RGAT engine."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+
+    import torch
+    if torch.cuda.device_count() < p:
+        pytest.skip(f"needs {p} GPUs")
+    here = os.path.dirname(os.path.abspath(__file__))
+    seed, n_batches, bsz = 5, 6, 64
+    with tempfile.TemporaryDirectory() as td:
+        idp = os.path.join(td, "nccl.id")
+        procs = [subprocess.Popen([sys.executable, os.path.join(here, "mp", "raf_rank.py"), "mag-mini", str(seed), str(p),
+                                   str(r), idp, os.path.join(td, f"r{r}.npz"), str(n_batches), str(bsz)],
+                                  stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True,
+                                  env=dict(os.environ, HG_MODEL="rgat")) for r in range(p)]
+        outs = [pr.communicate(timeout=300)[0] for pr in procs]
+        for pr, o in zip(procs, outs):
+            assert pr.returncode == 0, o[-3000:]
+        res = [np.load(os.path.join(td, f"r{r}.npz")) for r in range(p)]
+    g = H.gen_synthetic(H.bundled_spec("mag-mini"), seed)
+    batches = H.make_batches(g, bsz, n_batches, H.mix_seed(seed, 0xBA7C))
+    one = H.Engine.for_experiment(g, [25, 20], 32, seed, batch_cap=bsz, model="rgat", heads=4)
+    losses = [one.step(b, H.mix_seed(seed, 0xB000 + i))["loss"] for i, b in enumerate(batches)]
+    want = one.read(*[n for n in one.tensor_names() if n.startswith(("post.r", "att."))])
+    for r in range(p):
+        np.testing.assert_allclose(res[r]["losses"], losses, rtol=1e-3, atol=0)
+    seen = {}
+    for r in range(p):
+        for key in res[r].files:
+            if not key.startswith("T:"):
+                continue
+            n, v = key[2:], res[r][key]
+            if n in seen:
+                assert np.array_equal(seen[n], v), f"replicas disagree on {n}"
+            seen[n] = v
+            if n in want:
+                assert_adam_close(v, want[n], None, steps=n_batches, max_flip_frac=1e-2, what=f"p={p} rank {r}: {n}")
+    assert any(n.startswith("att.") for n in seen)
