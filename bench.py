@@ -145,6 +145,9 @@ def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
+    if args.model == "rgat":
+        print(json.dumps({"impl": "reference", "unavailable": "the reference has no attention layer (SPEC.md:8, 297)"}))
+        return
     from oracle import ref as R
     if not R.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libhetsim_ref.so not built"}))
@@ -245,6 +248,10 @@ def run_b200(args):
         parts = H.meta_partition_work_aware(g, len(FANOUTS), n, plan_kw["sub_work"])
         plan_desc = "work-aware (sub-metatree groups " + " | ".join(
             ",".join(str(int(x)) for x in parts[f"part{i}.sub_ids"]) for i in range(n)) + ")"
+    rgat = args.model == "rgat"
+    if rgat:  # C3 (BASELINE configs[2]): the RGAT layer type, 4 heads, same graph and batches
+        plan_kw["model"] = "rgat"
+        plan_kw["heads"] = 4
     eng = H.Engine.for_experiment(g, FANOUTS, HIDDEN, SEED, batch_cap=batch, p=n, rank=rank, device=local, **plan_kw)
     if world > 1:
         import torch.distributed as dist
@@ -367,6 +374,11 @@ def run_b200(args):
     # latency-bound (serial mt19937_64 per row) and is reported beside them.
     alg_by = {"aggregate": alg[1], "csc_gather": alg[3], "aggregate_top": alg[2],
               "csc_gather_top": alg[4] if len(alg) > 4 else 0.0, "sample": alg[0]}
+    if rgat:
+        # RGAT: the layer-1 attention gather (k_att_leaf_forward) reads what the RGCN gather
+        # reads, E (s d + 4) + indptr (alg[1], a lower bound: its per-head aggregates write
+        # H rows where the mean writes one); the backward attention pass reads it again
+        alg_by = {"rgat_attend": alg[1], "rgat_edge_grad": alg[1], "sample": alg[0]}
 
     lib_sha = lib_digest()
     traffic_rec = load_traffic()
@@ -391,14 +403,17 @@ def run_b200(args):
     peak_hbm = load_peaks()[0]
 
 
-    roof_kernel = max(("aggregate", "csc_gather"), key=lambda k: classes.get(k, 0.0))
+    roof_kernel = max(("rgat_attend", "rgat_edge_grad") if rgat else ("aggregate", "csc_gather"),
+                      key=lambda k: classes.get(k, 0.0))
     r0 = roof_of(roof_kernel)
     per_launch_bytes, per_launch_ms, achieved = r0["alg_bytes_per_launch"], r0["ms_per_launch"], r0["achieved"]
     line = {
         "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": n, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "C2 ogbn-mag-shape (BASELINE configs[1]) 2-layer RGCN hidden 64, fanout [25,20]",
+        "config": {"workload": ("C3 ogbn-mag-shape (BASELINE configs[2]) 2-layer RGAT 4 heads hidden 64, fanout [25,20]"
+                                if rgat else "C2 ogbn-mag-shape (BASELINE configs[1]) 2-layer RGCN hidden 64, fanout [25,20]"),
+                   "model": args.model,
                    "global_batch": batch, "batch_per_gpu": BATCH_PER_GPU, "parallelism": f"meta-partition p={n}",
                    "plan": plan_desc,
                    "graph_seed": SEED, "l2": "not flushed: tables 1.3 GB + CSR 0.3 GB >> 126 MB L2, new rows every step"},
@@ -438,7 +453,10 @@ def run_b200(args):
         line["agg_all"] = {"nranks": n, "bytes": ag_bytes, "us_per_call": 1e6 * ag_s,
                            "algbw_GBps": ag_bytes / ag_s / 1e9, "busbw_GBps": 2 * (n - 1) / n * ag_bytes / ag_s / 1e9,
                            "transport": "NCCL all-reduce over NVLink (NVSwitch)"}
-    if not args.no_cpu_baseline and n == 1:
+    if rgat:
+        line["parity"] = {"checked_in": "tests/test_rgat.py (f64 restatement oracle/rgat.py; C3 step, p = 2, 4)"}
+        line["cpu_baseline"] = None  # the reference has no attention layer
+    elif not args.no_cpu_baseline and n == 1:
         # bounded sample: 8 batches per host thread (~10-20 s of CPU work)
         threads = os.cpu_count() or 1
         v, sample, secs, g_ref = cpu_baseline_sample(threads, 8 * threads)
@@ -461,12 +479,18 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--plan", default="work", choices=["work", "reference"],
-                    help="N > 1: work-aware meta-partition (default) or the reference's meta_partition")
+    ap.add_argument("--plan", default=None, choices=["work", "reference"],
+                    help="N > 1: work-aware meta-partition (RGCN default) or the reference's meta_partition "
+                         "(RGAT default: the work-aware cost model is calibrated on RGCN's per-edge work; "
+                         "measured on C3 at p = 4: reference 1.45 G vs work-aware 1.12 G sampled-edges/s)")
     ap.add_argument("--warmup-ref", type=int, default=0)
+    ap.add_argument("--model", default="rgcn", choices=["rgcn", "rgat"],
+                    help="rgcn: the headline C2 workload; rgat: C3 (the RGAT layer type, 4 heads)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.plan is None:
+        args.plan = "reference" if args.model == "rgat" else "work"
     if args.impl == "reference":
         run_reference(args)
     else:

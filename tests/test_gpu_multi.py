@@ -17,11 +17,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def n_gpus():
-    try:
-        import torch
-        return torch.cuda.device_count()
-    except Exception:
-        return 0
+    from tests.util import gpu_count
+    return gpu_count()
 
 
 # one root relation: a single sub-metatree, so every rank is a replica of it

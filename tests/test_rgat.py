@@ -236,8 +236,8 @@ def test_rgat_multi_gpu_matches_one_gpu(H, p):
     import sys
     import tempfile
 
-    import torch
-    if torch.cuda.device_count() < p:
+    from tests.util import gpu_count
+    if gpu_count() < p:
         pytest.skip(f"needs {p} GPUs")
     here = os.path.dirname(os.path.abspath(__file__))
     seed, n_batches, bsz = 5, 6, 64

@@ -77,3 +77,14 @@ def single_relation_graph(H, deg_list, n_src=None, dim=4, seed=0):
         "labels": np.zeros(n_dst, np.int32), "target": np.array([0]), "num_classes": np.array([2]),
     }
     return e
+
+
+def gpu_count() -> int:
+    """Visible GPUs, without importing torch (torch's bundled NCCL clashes with the system
+    libnccl that libhetgpu.so links once the product library is loaded)."""
+    import subprocess
+    try:
+        out = subprocess.run(["nvidia-smi", "-L"], capture_output=True, text=True, timeout=60).stdout
+    except Exception:
+        return 0
+    return sum(1 for line in out.splitlines() if line.startswith("GPU "))
