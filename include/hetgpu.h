@@ -163,6 +163,10 @@ typedef struct {
 } hg_step_report;
 
 hg_engine* hg_engine_create(const hg_graph* g, const hg_engine_opts* opts);
+/* streaming loader: an engine whose graph comes straight from an HGC1 container file
+ * (src/container.cpp:92-154 format): relations' dst-major pairs and dense feature rows
+ * stream through pinned buffers into the device CSR and tables (no host graph) */
+hg_engine* hg_engine_create_from_container(const char* path, const hg_engine_opts* o);
 /* An engine of the work-aware plan (hg_meta_partition_work_aware) instead of the reference's */
 hg_engine* hg_engine_create_work_aware(const hg_graph* g, const hg_engine_opts* opts, const double* work, int n_work);
 /* Sampler-only engine for sample_khop (hop_rel_flat == NULL: every relation at

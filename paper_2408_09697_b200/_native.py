@@ -73,6 +73,7 @@ def lib():
             "hg_bundle_free": ([vp], None),
             "hg_mix_seed": ([u64, u64], u64),
             "hg_mt64_outputs": ([u64, u64, u64, vp], i32),
+            "hg_engine_create_from_container": ([C.c_char_p, C.POINTER(EngineOpts)], vp),
             "hg_graph_generate": ([C.POINTER(Spec), u64], vp),
             "hg_graph_from_csr": ([i32, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp], vp),
             "hg_graph_from_pairs": ([i32, vp, i32, vp, vp, vp, vp, vp, i32, i32], vp),

@@ -431,6 +431,15 @@ hg_bundle* hg_make_batches(const hg_graph* h, int batch_size, int max_batches, u
 }
 
 // ---- engine --------------------------------------------------------------------------------
+hg_engine* hg_engine_create_from_container(const char* path, const hg_engine_opts* o) {
+  return guard<hg_engine*>(nullptr, [&] {
+    const EngineOptions eo = engine_options(*o);
+    auto* h = new hg_engine;
+    h->e = std::make_unique<Engine>(std::string(path), eo);
+    return h;
+  });
+}
+
 hg_engine* hg_engine_create(const hg_graph* g, const hg_engine_opts* o) {
   return guard<hg_engine*>(nullptr, [&] {
     const EngineOptions eo = engine_options(*o);

@@ -266,7 +266,7 @@ void save_container(const Graph& g, const std::string& path) {
   if (!os) throw std::runtime_error("write failed: " + path);
 }
 
-Graph load_container(const std::string& path) {
+ContainerLayout container_layout(const std::string& path) {
   std::ifstream is(path, std::ios::binary);
   if (!is) throw std::runtime_error("cannot open: " + path);
   char magic[4];
@@ -279,12 +279,8 @@ Graph load_container(const std::string& path) {
   Parser ps(header);
   const Json h = ps.value();
   if (h.at("version").i != 1) throw std::runtime_error("unsupported container version");
-  std::vector<std::string> names, edge_names;
-  std::vector<std::uint64_t> counts;
-  std::vector<int> rel_src, rel_dst, rel_et;
-  std::vector<bool> rel_rev;
-  std::vector<std::uint64_t> rel_edges;
-  std::vector<NodeTypeInfo> types;
+  ContainerLayout lay;
+  Graph& g = lay.meta;
   for (const auto& t : h.at("node_types").a) {
     NodeTypeInfo nt;
     nt.name = t.at("name").s;
@@ -292,51 +288,82 @@ Graph load_container(const std::string& path) {
     nt.dim = static_cast<int>(t.at("dim").i);
     nt.storage = storage_from(t.at("storage").s);
     nt.elem_bytes = static_cast<int>(t.at("elem_bytes").i);
-    names.push_back(nt.name);
-    counts.push_back(nt.count);
-    types.push_back(std::move(nt));
+    g.types.push_back(std::move(nt));
   }
+  std::uint64_t at = 8 + static_cast<std::uint64_t>(hlen);
   for (const auto& r : h.at("relations").a) {
-    rel_src.push_back(static_cast<int>(r.at("src").i));
-    rel_dst.push_back(static_cast<int>(r.at("dst").i));
+    RelationInfo rel;
+    rel.src_type = static_cast<int>(r.at("src").i);
+    rel.dst_type = static_cast<int>(r.at("dst").i);
     const std::string en = r.at("etype").s;
-    auto it = std::find(edge_names.begin(), edge_names.end(), en);
-    rel_et.push_back(static_cast<int>(it - edge_names.begin()));
-    if (it == edge_names.end()) edge_names.push_back(en);
-    rel_rev.push_back(r.at("reverse").b);
-    rel_edges.push_back(static_cast<std::uint64_t>(r.at("edges").i));
+    auto it = std::find(g.edge_type_names.begin(), g.edge_type_names.end(), en);
+    rel.edge_type = static_cast<int>(it - g.edge_type_names.begin());
+    if (it == g.edge_type_names.end()) g.edge_type_names.push_back(en);
+    rel.reverse = r.at("reverse").b;
+    if (rel.src_type < 0 || rel.dst_type < 0 || rel.src_type >= g.num_types() || rel.dst_type >= g.num_types())
+      throw std::runtime_error("container relation endpoint type out of range");
+    const auto edges = static_cast<std::uint64_t>(r.at("edges").i);
+    lay.rel_edges.push_back(edges);
+    lay.rel_offset.push_back(at);
+    at += 8 * edges;
+    g.rels.push_back(std::move(rel));
   }
-  std::vector<std::vector<std::pair<NodeId, NodeId>>> pairs(rel_src.size());
+  for (const auto& nt : g.types) {
+    lay.dense_offset.push_back(at);
+    if (nt.storage == Storage::Dense) at += 4ULL * nt.count * nt.dim;
+  }
+  is.seekg(0, std::ios::end);
+  if (static_cast<std::uint64_t>(is.tellg()) < at) throw std::runtime_error("container truncated");
+  g.target = static_cast<int>(h.at("target").i);
+  g.num_classes = static_cast<int>(h.at("num_classes").i);
+  for (const auto& l : h.at("labels").a) g.labels.push_back(static_cast<std::int32_t>(l.i));
+  return lay;
+}
+
+Graph load_container(const std::string& path) {
+  ContainerLayout lay = container_layout(path);
+  Graph& m = lay.meta;
+  std::ifstream is(path, std::ios::binary);
+  std::vector<std::string> names;
+  std::vector<std::uint64_t> counts;
+  for (const auto& t : m.types) {
+    names.push_back(t.name);
+    counts.push_back(t.count);
+  }
+  std::vector<int> rel_src, rel_dst;
+  std::vector<std::vector<std::pair<NodeId, NodeId>>> pairs(m.rels.size());
   std::vector<std::uint32_t> buf;
-  for (std::size_t r = 0; r < rel_src.size(); ++r) {
-    buf.resize(2 * rel_edges[r]);
+  for (std::size_t r = 0; r < m.rels.size(); ++r) {
+    rel_src.push_back(m.rels[r].src_type);
+    rel_dst.push_back(m.rels[r].dst_type);
+    buf.resize(2 * lay.rel_edges[r]);
+    is.seekg(static_cast<std::streamoff>(lay.rel_offset[r]));
     is.read(reinterpret_cast<char*>(buf.data()), static_cast<std::streamsize>(buf.size() * 4));
     if (!is) throw std::runtime_error("container truncated");
-    pairs[r].resize(rel_edges[r]);
-    for (std::size_t e = 0; e < rel_edges[r]; ++e) pairs[r][e] = {buf[2 * e], buf[2 * e + 1]};
+    pairs[r].resize(lay.rel_edges[r]);
+    for (std::size_t e = 0; e < lay.rel_edges[r]; ++e) pairs[r][e] = {buf[2 * e], buf[2 * e + 1]};
   }
   // one edge-type name per relation for assemble(); repeated names are merged below
   std::vector<std::string> rel_names;
-  for (std::size_t r = 0; r < rel_src.size(); ++r) rel_names.push_back(edge_names[rel_et[r]]);
-  Graph g = assemble(names, counts, rel_names, rel_src, rel_dst, pairs, static_cast<int>(h.at("target").i),
-                     static_cast<int>(h.at("num_classes").i));
-  g.edge_type_names = edge_names;
-  for (std::size_t r = 0; r < rel_src.size(); ++r) {
-    g.rels[r].edge_type = rel_et[r];
-    g.rels[r].reverse = rel_rev[r];
+  for (const auto& rel : m.rels) rel_names.push_back(m.edge_type_names[rel.edge_type]);
+  Graph g = assemble(names, counts, rel_names, rel_src, rel_dst, pairs, m.target, m.num_classes);
+  g.edge_type_names = m.edge_type_names;
+  for (std::size_t r = 0; r < m.rels.size(); ++r) {
+    g.rels[r].edge_type = m.rels[r].edge_type;
+    g.rels[r].reverse = m.rels[r].reverse;
   }
   for (int t = 0; t < g.num_types(); ++t) {
     NodeTypeInfo& nt = g.types[t];
-    nt.dim = types[t].dim;
-    nt.storage = types[t].storage;
-    nt.elem_bytes = types[t].elem_bytes;
+    nt.dim = m.types[t].dim;
+    nt.storage = m.types[t].storage;
+    nt.elem_bytes = m.types[t].elem_bytes;
     if (nt.storage != Storage::Dense) continue;
     nt.dense.resize(static_cast<std::size_t>(nt.count) * nt.dim);
+    is.seekg(static_cast<std::streamoff>(lay.dense_offset[t]));
     is.read(reinterpret_cast<char*>(nt.dense.data()), static_cast<std::streamsize>(nt.dense.size() * 4));
     if (!is) throw std::runtime_error("container truncated");
   }
-  g.labels.clear();
-  for (const auto& l : h.at("labels").a) g.labels.push_back(static_cast<std::int32_t>(l.i));
+  g.labels = m.labels;
   return g;
 }
 

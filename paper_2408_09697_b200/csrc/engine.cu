@@ -152,6 +152,12 @@ void put(std::vector<char>& data, const std::vector<T>& v) {
 
 // ---------------------------------------------------------------------------------------------
 Engine::Engine(const Graph& g, const EngineOptions& o) : o_(o) {
+  init_streams();
+  init_graph(g);
+}
+
+void Engine::init_streams() {
+  const EngineOptions& o = o_;
   if (static_cast<int>(o.fanouts.size()) != o.k) throw std::invalid_argument("fanout count must equal the model depth");
   if (o.k < 1) throw std::invalid_argument("fanouts must be non-empty");
   HG_CUDA(cudaSetDevice(o.device));
@@ -173,6 +179,9 @@ Engine::Engine(const Graph& g, const EngineOptions& o) : o_(o) {
   }
   fork_ev_.resize(16);
   for (auto& e : fork_ev_) HG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+}
+
+void Engine::init_graph(const Graph& g) {
   ntypes_ = g.num_types();
   target_ = g.target;
   num_classes_ = g.num_classes;
@@ -479,6 +488,11 @@ void Engine::upload(const Graph& g) {
     for (int r : hr) used[r] = true;
   for (int r = 0; r < g.num_rels(); ++r) {
     if (!used[r]) continue;
+    if (!pre_ptr_.empty()) {  // streamed from a container (loader.cu)
+      csr_ptr_[r] = pre_ptr_[r];
+      csr_src_[r] = pre_src_[r];
+      continue;
+    }
     const auto& a = g.rels[r].adj;
     csr_ptr_[r] = static_cast<std::uint64_t*>(alloc(a.offsets.size() * 8));
     csr_src_[r] = static_cast<std::uint32_t*>(alloc(a.sources.size() * 4));
@@ -502,7 +516,10 @@ void Engine::upload(const Graph& g) {
     const std::size_t rows = nt.count;
     if (nt.storage == Storage::Absent) throw std::runtime_error("missing features for node type " + nt.name);
     if (nt.storage == Storage::Dense) {
-      upload_dense(nt, tb);
+      if (lay_)
+        stream_dense(nt, t, tb);  // straight from the container file (loader.cu)
+      else
+        upload_dense(nt, tb);
       continue;
     }
     std::vector<float> host(rows * tb.ld, 0.0f);

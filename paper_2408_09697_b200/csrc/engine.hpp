@@ -82,6 +82,9 @@ struct DeviceBuffer {
 class Engine {
  public:
   Engine(const Graph& g, const EngineOptions& o);
+  // streaming loader (loader.cu): CSR and dense tables go from an HGC1 file straight into
+  // HBM (container.cpp:92-154 semantics, no host graph)
+  Engine(const std::string& container_path, const EngineOptions& o);
   ~Engine();
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
@@ -302,6 +305,14 @@ class Engine {
   };
 
   void* alloc(std::size_t bytes);
+  void init_streams();
+  void init_graph(const Graph& g);  // plan + upload
+  void stream_csr(ContainerLayout& lay, const std::string& path);
+  void stream_dense(const NodeTypeInfo& nt, int t, TypeTable& tb);
+  const ContainerLayout* lay_ = nullptr;  // set while a container-streamed engine uploads
+  std::string lay_path_;
+  std::vector<std::uint64_t*> pre_ptr_;  // streamed CSR per relation (device)
+  std::vector<std::uint32_t*> pre_src_;
   void build_plan(const Graph& g);
   void upload(const Graph& g);
   void upload_dense(const NodeTypeInfo& nt, TypeTable& tb);

@@ -60,6 +60,28 @@ void run_parallel(std::vector<std::function<void()>>& tasks) {
     if (e) std::rethrow_exception(e);
 }
 
+// n values of std::uniform_real_distribution<double>(lo, hi) over std::mt19937_64(seed)
+// (one engine output per value): the stream cut into chunks whose engines are jumped
+// ahead (mt64_jump_engines), generated as tasks; bit-identical to the serial stream.
+// HG_FEAT_CHUNK (values per chunk) is a test knob.
+template <typename T>
+void uniform_stream_tasks(std::uint64_t seed, double lo, double hi, T* out, std::uint64_t n,
+                          std::vector<std::function<void()>>& tasks) {
+  const char* chunk_env = std::getenv("HG_FEAT_CHUNK");
+  const std::uint64_t chunk = std::max<std::uint64_t>(1, chunk_env ? std::stoull(chunk_env) : 1ULL << 26);
+  std::vector<std::uint64_t> starts;
+  for (std::uint64_t c = 0; c < n; c += chunk) starts.push_back(c);
+  auto engines = std::make_shared<std::vector<std::mt19937_64>>(
+      starts.size() > 1 ? mt64_jump_engines(seed, starts) : std::vector<std::mt19937_64>{std::mt19937_64(seed)});
+  for (std::size_t c = 0; c < starts.size(); ++c)
+    tasks.emplace_back([=] {
+      std::mt19937_64& eng = (*engines)[c];
+      std::uniform_real_distribution<double> u(lo, hi);
+      const std::uint64_t end = std::min(n, starts[c] + chunk);
+      for (std::uint64_t i = starts[c]; i < end; ++i) out[i] = static_cast<T>(u(eng));
+    });
+}
+
 Adjacency dst_major(std::uint64_t n_dst, const std::vector<std::pair<NodeId, NodeId>>& pairs) {
   Adjacency a;
   a.offsets.assign(n_dst + 1, 0);
@@ -255,28 +277,14 @@ Graph generate(const Spec& spec, std::uint64_t seed) {
     }
   });
   // A feature stream draws one engine output per value (generate_canonical<double, 53>
-  // over 64-bit words); a long one is cut into chunks whose engines are jumped ahead
-  // (mt64_jump_engines), so its values come out on many threads bit-identical to the
-  // serial stream. HG_FEAT_CHUNK (values per chunk) is a test knob.
-  const char* chunk_env = std::getenv("HG_FEAT_CHUNK");
-  const std::uint64_t kFeatChunk = std::max<std::uint64_t>(1, chunk_env ? std::stoull(chunk_env) : 1ULL << 26);
+  // over 64-bit words); a long one is cut into jumped-ahead chunks generated on many
+  // threads, bit-identical to the serial stream (uniform_stream_tasks).
   std::vector<std::vector<float>> dense(spec.node_types.size());
   for (std::size_t t = 0; t < spec.node_types.size(); ++t) {
     if (spec.node_types[t].storage != Storage::Dense) continue;
     const std::uint64_t n = spec.node_types[t].count * static_cast<std::uint64_t>(spec.node_types[t].dim);
     dense[t].resize(n);
-    std::vector<std::uint64_t> starts;
-    for (std::uint64_t c = 0; c < n; c += kFeatChunk) starts.push_back(c);
-    auto engines = std::make_shared<std::vector<std::mt19937_64>>(
-        starts.size() > 1 ? mt64_jump_engines(mix_seed(seed, 0xf0ULL + t), starts)
-                          : std::vector<std::mt19937_64>{std::mt19937_64(mix_seed(seed, 0xf0ULL + t))});
-    for (std::size_t c = 0; c < starts.size(); ++c)
-      tasks.emplace_back([&, t, c, n, engines, lo = starts[c]] {
-        std::mt19937_64& eng = (*engines)[c];
-        std::uniform_real_distribution<double> u(-1.0, 1.0);
-        const std::uint64_t hi = std::min(n, lo + kFeatChunk);
-        for (std::uint64_t i = lo; i < hi; ++i) dense[t][i] = static_cast<float>(u(eng));
-      });
+    uniform_stream_tasks(mix_seed(seed, 0xf0ULL + t), -1.0, 1.0, dense[t].data(), n, tasks);
   }
   std::vector<std::int32_t> labels(counts[tgt]);
   tasks.emplace_back([&] {
@@ -727,13 +735,16 @@ std::map<int, std::vector<double>> init_learnable(const Graph& g, std::uint64_t 
   for (int t = 0; t < g.num_types(); ++t) {
     if (g.types[t].storage != Storage::Learnable) continue;
     const int d = g.types[t].dim;
-    const double scale = d > 0 ? 1.0 / std::sqrt(static_cast<double>(d)) : 0.0;
-    std::mt19937_64 eng(mix_seed(seed, 0xfeedULL + t));
-    std::uniform_real_distribution<double> u(-scale, scale);
-    std::vector<double> w(g.types[t].count * static_cast<std::uint64_t>(d));
-    for (double& x : w) x = u(eng);
-    out.emplace(t, std::move(w));
+    out.emplace(t, std::vector<double>(g.types[t].count * static_cast<std::uint64_t>(d)));
   }
+  // one uniform stream per table (hgnn.cpp:64-81), in jumped-ahead chunks on host threads
+  std::vector<std::function<void()>> tasks;
+  for (auto& [t, w] : out) {
+    const int d = g.types[t].dim;
+    const double scale = d > 0 ? 1.0 / std::sqrt(static_cast<double>(d)) : 0.0;
+    uniform_stream_tasks(mix_seed(seed, 0xfeedULL + t), -scale, scale, w.data(), w.size(), tasks);
+  }
+  run_parallel(tasks);
   return out;
 }
 

@@ -112,6 +112,14 @@ Graph generate(const Spec& spec, std::uint64_t seed);
 std::string container_header(const Graph& g);  // the reference's exact JSON header
 void save_container(const Graph& g, const std::string& path);
 Graph load_container(const std::string& path);
+// The header of a container as a Graph skeleton (types, relations, labels; no
+// adjacency or features) plus the file offset of every relation's dst-major (src, dst)
+// u32 pairs and of every dense type's f32 rows: the device loader streams those.
+struct ContainerLayout {
+  Graph meta;
+  std::vector<std::uint64_t> rel_edges, rel_offset, dense_offset;
+};
+ContainerLayout container_layout(const std::string& path);
 
 // Builds the dst-major adjacency of every relation from (src, dst) pairs in
 // insertion order (hetgraph.cpp:126-156). Features start Absent.

@@ -301,6 +301,26 @@ class Engine:
             N.raise_last()
 
     @classmethod
+    def from_container(cls, path: str, fanouts: Sequence[int], hidden: int = 64, batch_cap: int = 1024, p: int = 1,
+                       rank: int = 0, model_seed: int = 0, learn_seed: int = 0, device: int = 0,
+                       feat_dtype: str = "f32", feat_host: bool = False, model: str = "rgcn",
+                       heads: int = 4) -> "Engine":
+        """Streaming loader: the graph goes from an HGC1 container (container.cpp:92-154)
+        straight into HBM, relation pairs and feature rows through pinned buffers."""
+        self = cls.__new__(cls)
+        fo = (C.c_int * len(fanouts))(*[int(f) for f in fanouts])
+        self._fo = fo
+        if feat_dtype not in cls.FEAT_DTYPES or model not in cls.MODELS:
+            raise ValueError("feature dtype must be one of f32, f16, bf16 and model one of rgcn, rgat")
+        opts = N.EngineOpts(len(fanouts), fo, hidden, batch_cap, p, rank, model_seed, learn_seed, device,
+                            cls.FEAT_DTYPES[feat_dtype], int(bool(feat_host)), cls.MODELS[model], heads)
+        self.k, self.model, self.heads, self.graph = len(fanouts), model, heads, None
+        self._h = N.lib().hg_engine_create_from_container(str(path).encode(), C.byref(opts))
+        if not self._h:
+            N.raise_last()
+        return self
+
+    @classmethod
     def for_experiment(cls, g: HetGraph, fanouts, hidden, seed, **kw) -> "Engine":
         """Seeds as run_experiment derives them (harness.cpp:365-366)."""
         return cls(g, fanouts, hidden, model_seed=mix_seed(seed, 0xD0DE1), learn_seed=mix_seed(seed, 0x1EA4A), **kw)

@@ -216,10 +216,13 @@ def test_cache_plan_matches_reference(H, ref):
             assert np.array_equal(got[f"cached.t{t}"], want[f"cached.t{t}"]), (budget, t)
 
 
-@pytest.mark.parametrize("name", ["mag-mini", "donor-mini"])
-def test_init_model_and_learnable_match_reference(H, ref, name):
+@pytest.mark.parametrize("name,chunk", [("mag-mini", None), ("donor-mini", None), ("mag-mini", "4099")])
+def test_init_model_and_learnable_match_reference(H, ref, name, chunk, monkeypatch):
     # hg_init_model / hg_init_learnable (the caller-owned model state of the drop-in
-    # layer interface) are the reference's init_model / init_learnable bit for bit
+    # layer interface) are the reference's init_model / init_learnable bit for bit; the
+    # learnable tables are generated in jumped-ahead chunks (HG_FEAT_CHUNK values each)
+    if chunk:
+        monkeypatch.setenv("HG_FEAT_CHUNK", chunk)
     rg = ref.RefGraph.bundled(name, 5)
     g = H.gen_synthetic(H.bundled_spec(name), 5)
     want = rg.flat_step(2, 16, 77, 88, [0, 1, 2], [3, 3], 1)
