@@ -68,9 +68,14 @@ struct FeatSyncArgs {
   const int* count[kMaxSegs][kMaxRep];
   int dim[kMaxSegs];
   int nt, n_rep, elem;
+  const int* peer_slot[kMaxRep];  // each replica's bound sample slot (its arena)
+  std::uint32_t* err;
 };
 __global__ void k_feat_sync(FeatSyncArgs a, std::uint64_t* out) {
   pdl_enter();
+  // every replica must merge the same step's rows: all trained the same sample slot
+  for (int r = 0; r < a.n_rep; ++r)
+    if (*a.peer_slot[r] != *a.peer_slot[0]) atomicOr(a.err, 8u);
   std::uint64_t bytes = 0;
   for (int t = 0; t < a.nt; ++t) {
     std::uint64_t s = 0;
@@ -618,6 +623,7 @@ void Engine::upload(const Graph& g) {
     }
     // the replica barrier's flags: slot q holds the last step replica q finished reading
     off_flags_ = take(static_cast<std::size_t>(kMaxRep) * 4);
+    off_slot_ = take(sizeof(int));
     arena_bytes_ = std::max<std::size_t>(at, 256);
     arena_ = static_cast<std::uint8_t*>(alloc(arena_bytes_));
     for (auto& x : xchg_) {
@@ -1209,6 +1215,10 @@ void Engine::run_replica_merge() {
   if (!rcomm_) throw std::runtime_error("replica group without a communicator (attach_nccl first)");
   for (std::size_t r = 0; r < peer_arena_.size(); ++r)
     if (!peer_arena_[r]) throw std::runtime_error("replica peers not attached (attach_replicas)");
+  // 0. this rank's sample slot, checked against the peers' once the all-reduce below has
+  //    ordered every replica's earlier writes (a rank-local prefetch / quiesce would
+  //    otherwise pair another batch's ids with this step's rows)
+  HG_CUDA(cudaMemsetAsync(arena_ + off_slot_, bound_, sizeof(int), st_));
   // 1. weight gradients; completing it also orders every replica's gradient rows
   //    (written by its csc_gather before its all-reduce) before our reads below
   // (a launch-count capture leaves the collectives out, see count_launches)
@@ -1253,6 +1263,8 @@ void Engine::run_replica_merge() {
     FeatSyncArgs fs{};
     fs.n_rep = static_cast<int>(peer_arena_.size());
     fs.elem = elem_bytes_;
+    fs.err = err_;
+    for (int r = 0; r < fs.n_rep; ++r) fs.peer_slot[r] = reinterpret_cast<const int*>(peer_arena_[r] + off_slot_);
     for (auto& x : xchg_) {
       fs.ucount[fs.nt] = x.utotal;
       for (int r = 0; r < fs.n_rep; ++r)
@@ -1586,6 +1598,9 @@ StepReport Engine::finish_step() {
   if (r.err & 1u) throw std::invalid_argument("fanout above the sampler's supported map size");
   if (r.err & 2u) throw std::invalid_argument("label out of range in batch");
   if (r.err & 4u) throw std::runtime_error("non-finite gradient");
+  if (r.err & 8u)
+    throw std::runtime_error("replica group out of step: its ranks trained different sample slots "
+                             "(a prefetch or quiesce on one rank only)");
   if (o_.p > 1) {
     std::vector<float> row(ldc_);
     HG_CUDA(cudaMemcpy(row.data(), logits_ + static_cast<std::size_t>(o_.batch_cap) * ldc_, ldc_ * 4,

@@ -545,6 +545,7 @@ class Engine {
   std::vector<void*> ipc_opened_;
   unsigned* barrier_epoch_ = nullptr;  // steps this replica has passed the barrier (device)
   std::size_t off_flags_ = 0;          // barrier flags in the exchange arena
+  std::size_t off_slot_ = 0;           // this replica's bound sample slot (checked by the peers)
   bool xchg_type(int t) const {
     for (const auto& x : xchg_)
       if (x.t == t) return true;
