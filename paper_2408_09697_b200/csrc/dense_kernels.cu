@@ -27,6 +27,12 @@ namespace hetgpu {
 
 namespace {
 constexpr int kThreads = 256;
+#ifndef HG_CE_REG
+#define HG_CE_REG 1  // cross entropy: a row in registers (one read) instead of three passes
+#endif
+#if HG_CE_REG
+constexpr int kCeRegs = 16;  // logits per lane held in registers (C <= 512)
+#endif
 }  // namespace
 
 // ---- cross entropy ---------------------------------------------------------------------
@@ -62,6 +68,35 @@ __global__ void __launch_bounds__(kThreads) k_cross_entropy(LossArgs a) {
       continue;
     }
     // fp32 log-sum-exp (the reference's f64 agrees to ~1e-7 relative)
+    const float scale = m * invb;
+#if HG_CE_REG
+    if (a.C <= 32 * kCeRegs) {  // the row read once into registers (C <= 512)
+      float zv[kCeRegs];
+      float zmax = -FLT_MAX;
+#pragma unroll
+      for (int u = 0; u < kCeRegs; ++u) {
+        const int c = lane + 32 * u;
+        zv[u] = c < a.C ? z[c] : -FLT_MAX;
+        zmax = fmaxf(zmax, zv[u]);
+      }
+      for (int o = 16; o > 0; o >>= 1) zmax = fmaxf(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
+      float sum = 0.f;
+#pragma unroll
+      for (int u = 0; u < kCeRegs; ++u) {
+        zv[u] = expf(zv[u] - zmax);  // 0 for the padding lanes
+        sum += zv[u];
+      }
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      const float inv = 1.0f / sum;
+#pragma unroll
+      for (int u = 0; u < kCeRegs; ++u) {
+        const int c = lane + 32 * u;
+        if (c < a.C) dz[c] = (zv[u] * inv - (c == y ? 1.0f : 0.0f)) * scale;
+      }
+      if (lane == 0) a.row_loss[i] = static_cast<double>(zmax + logf(sum) - z[y]) * static_cast<double>(scale);
+      continue;
+    }
+#endif
     float zmax = -FLT_MAX;
     for (int c = lane; c < a.C; c += 32) zmax = fmaxf(zmax, z[c]);
     for (int o = 16; o > 0; o >>= 1) zmax = fmaxf(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
@@ -69,7 +104,6 @@ __global__ void __launch_bounds__(kThreads) k_cross_entropy(LossArgs a) {
     for (int c = lane; c < a.C; c += 32) sum += expf(z[c] - zmax);
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     const float lse = zmax + logf(sum);
-    const float scale = m * invb;
     for (int c = lane; c < a.C; c += 32) {
       const float g = (expf(z[c] - lse) - (c == y ? 1.0f : 0.0f)) * scale;
       dz[c] = g;
