@@ -225,6 +225,23 @@ constexpr int kGatherBatch = HG_GATHER_BATCH;  // neighbour rows in flight per l
 #endif
 // 4 consecutive fp32 features (columns c..c+3) of row `key` (one 16-byte load); a
 // cached host table reads the HBM copy when the row is cached
+#ifndef HG_GATHER_L2HINT
+#define HG_GATHER_L2HINT 1  // measured: aggregate 50.7 -> 49.4 us/step (the backward gather gets slower: not used there)
+#endif
+// a feature-row float4 that no other lane reads again: read-only path, no L1 allocation,
+// L2 fetch in 256-byte blocks (a half-warp reads 256 contiguous bytes of the row)
+__device__ __forceinline__ float4 ld_row_stream(const float* p) {
+#if HG_GATHER_L2HINT
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+#else
+  return __ldg(reinterpret_cast<const float4*>(p));
+#endif
+}
+
 __device__ __forceinline__ float4 load_row4(const MeanBlock& B, std::uint32_t key, int c) {
   const float* base = B.h;
   std::size_t row = key;
@@ -315,7 +332,7 @@ __global__ void __launch_bounds__(256, WIDE || NB > kGatherBatch ? 4 : 8) k_gath
           if (CACHED)
             v[q] = q < cnt ? load_row4(B, kk[q], c) : make_float4(0.f, 0.f, 0.f, 0.f);
           else
-            v[q] = q < cnt ? __ldg(reinterpret_cast<const float4*>(base + static_cast<std::size_t>(kk[q]) * B.ld_h))
+            v[q] = q < cnt ? ld_row_stream(base + static_cast<std::size_t>(kk[q]) * B.ld_h)
                            : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
