@@ -308,6 +308,17 @@ __global__ void __launch_bounds__(256) k_csc_gather(CscHop h, AdamHyper hp, std:
       const int f = (item % nch) * 64 + 4 * hl;
       if (f >= t.ld_dh) continue;
       const std::uint32_t lo = c ? t.offs[c - 1] : 0u, hi = t.offs[c];
+      // loads that do not depend on the sum go out first: the ReLU mask row, and the
+      // learnable row's w / m / v (their DRAM round trip overlaps the gather's)
+      float4 hm4 = make_float4(1.f, 1.f, 1.f, 1.f), w0, m0, v0;
+      std::size_t at_w = 0;
+      if (t.relu_h) hm4 = *reinterpret_cast<const float4*>(t.relu_h + static_cast<std::size_t>(c) * t.ld_h + f);
+      if (t.w) {
+        at_w = static_cast<std::size_t>(t.ids[c]) * t.ld_w + f;
+        w0 = *reinterpret_cast<const float4*>(t.w + at_w);
+        m0 = *reinterpret_cast<const float4*>(t.m + at_w);
+        v0 = *reinterpret_cast<const float4*>(t.v + at_w);
+      }
       float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
       // up to kCscBatch edges in flight: packed entries, then dmean rows
       for (std::uint32_t x0 = lo; x0 < hi; x0 += kCscBatch) {
@@ -335,22 +346,17 @@ __global__ void __launch_bounds__(256) k_csc_gather(CscHop h, AdamHyper hp, std:
         }
       }
       if (t.relu_h) {
-        const float4 h = *reinterpret_cast<const float4*>(t.relu_h + static_cast<std::size_t>(c) * t.ld_h + f);
-        if (h.x <= 0.f) s.x = 0.f;
-        if (h.y <= 0.f) s.y = 0.f;
-        if (h.z <= 0.f) s.z = 0.f;
-        if (h.w <= 0.f) s.w = 0.f;
+        if (hm4.x <= 0.f) s.x = 0.f;
+        if (hm4.y <= 0.f) s.y = 0.f;
+        if (hm4.z <= 0.f) s.z = 0.f;
+        if (hm4.w <= 0.f) s.w = 0.f;
       }
       if (t.dh) *reinterpret_cast<float4*>(t.dh + static_cast<std::size_t>(c) * t.ld_dh + f) = s;
       if (t.w) {
-        const std::size_t at = static_cast<std::size_t>(t.ids[c]) * t.ld_w + f;
-        float4 w = *reinterpret_cast<float4*>(t.w + at);
-        float4 m = *reinterpret_cast<float4*>(t.m + at);
-        float4 v = *reinterpret_cast<float4*>(t.v + at);
-        adam4(w, m, v, s, ks[ty], err);
-        *reinterpret_cast<float4*>(t.w + at) = w;
-        *reinterpret_cast<float4*>(t.m + at) = m;
-        *reinterpret_cast<float4*>(t.v + at) = v;
+        adam4(w0, m0, v0, s, ks[ty], err);
+        *reinterpret_cast<float4*>(t.w + at_w) = w0;
+        *reinterpret_cast<float4*>(t.m + at_w) = m0;
+        *reinterpret_cast<float4*>(t.v + at_w) = v0;
       }
     }
   }
