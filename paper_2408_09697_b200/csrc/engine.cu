@@ -157,8 +157,13 @@ void put(std::vector<char>& data, const std::vector<T>& v) {
 
 // ---------------------------------------------------------------------------------------------
 Engine::Engine(const Graph& g, const EngineOptions& o) : o_(o) {
-  init_streams();
-  init_graph(g);
+  try {
+    init_streams();
+    init_graph(g);
+  } catch (...) {
+    release();
+    throw;
+  }
 }
 
 void Engine::init_streams() {
@@ -202,13 +207,18 @@ void Engine::init_graph(const Graph& g) {
   upload(g);
 }
 
-Engine::~Engine() {
-  cudaStreamSynchronize(st_);
+Engine::~Engine() { release(); }
+
+// everything the engine owns; safe on a partially constructed engine (null handles are
+// skipped or rejected harmlessly), so a constructor that throws releases through it
+void Engine::release() noexcept {
+  if (st_) cudaStreamSynchronize(st_);
   drop_graphs();
   for (auto e : ev_pool_) cudaEventDestroy(e);
   for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
-  cudaStreamSynchronize(st2_);
-  for (auto e : fork_ev_) cudaEventDestroy(e);
+  if (st2_) cudaStreamSynchronize(st2_);
+  for (auto e : fork_ev_)
+    if (e) cudaEventDestroy(e);
   for (void* p : allocs_) cudaFree(p);
   for (auto& tb : tables_)
     if (tb.host_mem) cudaFreeHost(tb.host_mem);
@@ -225,8 +235,8 @@ Engine::~Engine() {
     cudaStreamSynchronize(st_s_);
     cudaStreamDestroy(st_s_);
   }
-  cudaStreamDestroy(st2_);
-  cudaStreamDestroy(st_);
+  if (st2_) cudaStreamDestroy(st2_);
+  if (st_) cudaStreamDestroy(st_);
 }
 
 void Engine::fork() {

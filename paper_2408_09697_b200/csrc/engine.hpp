@@ -305,6 +305,7 @@ class Engine {
   };
 
   void* alloc(std::size_t bytes);
+  void release() noexcept;  // the destructor's work (also for a constructor that throws)
   void init_streams();
   void init_graph(const Graph& g);  // plan + upload
   void stream_csr(ContainerLayout& lay, const std::string& path);

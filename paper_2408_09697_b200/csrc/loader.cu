@@ -135,15 +135,21 @@ Engine::Engine(const std::string& container_path, const EngineOptions& o) : o_(o
   };
   ContainerLayout lay = container_layout(container_path);
   lap("header");
-  init_streams();
-  lap("streams");
-  stream_csr(lay, container_path);
-  lap("csr");
-  lay_ = &lay;
-  lay_path_ = container_path;
-  init_graph(lay.meta);
-  lay_ = nullptr;
-  lap("plan+tables");
+  try {
+    init_streams();
+    lap("streams");
+    stream_csr(lay, container_path);
+    lap("csr");
+    lay_ = &lay;
+    lay_path_ = container_path;
+    init_graph(lay.meta);
+    lay_ = nullptr;
+    lap("plan+tables");
+  } catch (...) {  // a malformed file: release what was built
+    lay_ = nullptr;
+    release();
+    throw;
+  }
 }
 
 void Engine::stream_csr(ContainerLayout& lay, const std::string& path) {
