@@ -148,6 +148,9 @@ def run_reference(args):
     if args.model == "rgat":
         print(json.dumps({"impl": "reference", "unavailable": "the reference has no attention layer (SPEC.md:8, 297)"}))
         return
+    if args.workload != "c2":
+        print(json.dumps({"impl": "reference", "unavailable": "the reference arm times the headline workload (C2)"}))
+        return
     from oracle import ref as R
     if not R.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libhetsim_ref.so not built"}))
@@ -236,7 +239,9 @@ def run_b200(args):
     batch = BATCH_PER_GPU * n
 
     t0 = time.time()
-    g = H.gen_synthetic(H.ogbn_mag_spec(), SEED)
+    c5 = args.workload == "c5"
+    spec = H.igb_het_spec(args.scale) if c5 else H.ogbn_mag_spec()
+    g = H.gen_synthetic(spec, SEED)
     t_gen = time.time() - t0
     dbg("graph generated")
     plan_kw, plan_desc = {}, "reference meta_partition"
@@ -252,6 +257,8 @@ def run_b200(args):
     if rgat:  # C3 (BASELINE configs[2]): the RGAT layer type, 4 heads, same graph and batches
         plan_kw["model"] = "rgat"
         plan_kw["heads"] = 4
+    if c5:  # C5 (BASELINE configs[4]) shape: 1024-d dense features on every type, stored fp16
+        plan_kw["feat_dtype"] = "f16"
     eng = H.Engine.for_experiment(g, FANOUTS, HIDDEN, SEED, batch_cap=batch, p=n, rank=rank, device=local, **plan_kw)
     if world > 1:
         import torch.distributed as dist
@@ -411,7 +418,10 @@ def run_b200(args):
         "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": n, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": ("C3 ogbn-mag-shape (BASELINE configs[2]) 2-layer RGAT 4 heads hidden 64, fanout [25,20]"
+        "config": {"workload": (f"C5 IGB-HET-shape x{args.scale:g} (BASELINE configs[4]; 1024-d fp16 features on all 4 "
+                                f"types, 7 relations) 2-layer {args.model.upper()} hidden 64, fanout [25,20] (the HGT-style "
+                                "aggregator is not built: RGCN)" if c5 else
+                                "C3 ogbn-mag-shape (BASELINE configs[2]) 2-layer RGAT 4 heads hidden 64, fanout [25,20]"
                                 if rgat else "C2 ogbn-mag-shape (BASELINE configs[1]) 2-layer RGCN hidden 64, fanout [25,20]"),
                    "model": args.model,
                    "global_batch": batch, "batch_per_gpu": BATCH_PER_GPU, "parallelism": f"meta-partition p={n}",
@@ -430,7 +440,7 @@ def run_b200(args):
         # H2D: the batch ids + the 32-byte step-scalar record; D2H: the 24-byte readback
         # (loss, error flags, sampled edges) and, at p > 1, the AGG_all counter row
         "e2e": {"value": e2e_value, "unit": "edges/s", "h2d_bytes_per_step": 4 * batch + 32,
-                "d2h_bytes_per_step": 24 + (4 * ((349 + 3) // 4) if n > 1 else 0),
+                "d2h_bytes_per_step": 24 + (4 * ((spec["num_classes"] + 3) // 4) if n > 1 else 0),
                 "ms_per_step": 1000.0 * e2e_s / args.steps},
         "roofline": {"bound": "hbm", "kernel": roof_kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic_of(roof_kernel),
@@ -448,7 +458,7 @@ def run_b200(args):
     if n > 1 and "agg_all" in classes:
         # AGG_all = one ncclAllReduce of the [B+1 x C] fp32 partial logits per step (NVLink);
         # bus bandwidth in NCCL's convention: 2 (n-1)/n x bytes / time
-        ag_bytes = (batch + 1) * (4 * ((349 + 3) // 4))
+        ag_bytes = (batch + 1) * (4 * ((spec["num_classes"] + 3) // 4))
         ag_s = classes["agg_all"] / max(1, launches_by.get("agg_all", prof_steps)) / 1000.0
         line["agg_all"] = {"nranks": n, "bytes": ag_bytes, "us_per_call": 1e6 * ag_s,
                            "algbw_GBps": ag_bytes / ag_s / 1e9, "busbw_GBps": 2 * (n - 1) / n * ag_bytes / ag_s / 1e9,
@@ -456,6 +466,9 @@ def run_b200(args):
     if rgat:
         line["parity"] = {"checked_in": "tests/test_rgat.py (f64 restatement oracle/rgat.py; C3 step, p = 2, 4)"}
         line["cpu_baseline"] = None  # the reference has no attention layer
+    elif c5:
+        line["parity"] = {"checked_in": "tests/test_c4_parity.py (half-precision tables), test_gpu_numerics.py"}
+        line["cpu_baseline"] = None  # C5's reference arm would be the RGCN stand-in, not HGT
     elif not args.no_cpu_baseline and n == 1:
         # bounded sample: 8 batches per host thread (~10-20 s of CPU work)
         threads = os.cpu_count() or 1
@@ -484,6 +497,9 @@ def main():
                          "(RGAT default: the work-aware cost model is calibrated on RGCN's per-edge work; "
                          "measured on C3 at p = 4: reference 1.45 G vs work-aware 1.12 G sampled-edges/s)")
     ap.add_argument("--warmup-ref", type=int, default=0)
+    ap.add_argument("--workload", default="c2", choices=["c2", "c5"],
+                    help="c2: the headline ogbn-mag shape; c5: the IGB-HET shape (1024-d fp16 features, --scale)")
+    ap.add_argument("--scale", type=float, default=0.05, help="c5: fraction of IGB-HET's counts")
     ap.add_argument("--model", default="rgcn", choices=["rgcn", "rgat"],
                     help="rgcn: the headline C2 workload; rgat: C3 (the RGAT layer type, 4 heads)")
     args = ap.parse_args()

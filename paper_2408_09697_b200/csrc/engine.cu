@@ -112,6 +112,7 @@ struct AlgBytesArgs {
   const int* n_rows[kMaxBlocks * 4];
   int din[kMaxBlocks * 4];
   int cls[kMaxBlocks * 4];  // 1 inner aggregate, 2 top aggregate
+  int src_esz[kMaxBlocks * 4];  // bytes per gathered source feature (2: fp16 / bf16 tables)
   int nblk;
   int grad[kMaxBlocks * 4];  // block feeds a source gradient (its edges are gathered by csc_gather)
   // csc_gather per (hop, source type): live source rows, row width, bytes per row
@@ -130,8 +131,8 @@ __global__ void k_alg_bytes(AlgBytesArgs a, double* acc) {
     const double R = *a.n_rows[i], E = a.indptr[i][*a.n_rows[i]];
     // sampling: indptr pair + dst id read, neighbour reads, src write, offset write
     s += 16.0 * R + 4.0 * R + 4.0 * E + 4.0 * E + 4.0 * R;
-    // aggregation: per edge one source row + its id; offsets; tape write
-    agg[a.cls[i]] += E * (4.0 * a.din[i] + 4.0) + 4.0 * (R + 1) + 4.0 * R * a.din[i];
+    // aggregation: per edge one source row (its table's element size) + its id; offsets; tape write
+    agg[a.cls[i]] += E * (static_cast<double>(a.src_esz[i]) * a.din[i] + 4.0) + 4.0 * (R + 1) + 4.0 * R * a.din[i];
     // backward gather: per edge one dmean row + the edge id
     if (a.grad[i]) (a.cls[i] == 2 ? csc_top : csc) += E * (4.0 * a.din[i] + 4.0);
   }
@@ -991,6 +992,7 @@ void Engine::run_sampling(cudaStream_t ss) {
       ab.indptr[ab.nblk] = b.indptr;
       ab.n_rows[ab.nblk] = block_rows(b);
       ab.din[ab.nblk] = b.din;
+      ab.src_esz[ab.nblk] = (b.hop == o_.k && tables_[b.src_t].dense && tables_[b.src_t].dtype != kF32) ? 2 : 4;
       ab.cls[ab.nblk] = b.hop == 1 ? 2 : 1;
       ab.grad[ab.nblk] = b.need_src_grad ? 1 : 0;
       ++ab.nblk;

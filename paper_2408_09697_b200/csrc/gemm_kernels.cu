@@ -220,6 +220,9 @@ __global__ void __launch_bounds__(kT) k_dmean_tiles(DMeanBatch b) {
 #define HG_GATHER_BATCH 5
 #endif
 constexpr int kGatherBatch = HG_GATHER_BATCH;  // neighbour rows in flight per lane
+#ifndef HG_GATHER_BATCH_WIDE
+#define HG_GATHER_BATCH_WIDE 5  // half tables in HBM
+#endif
 #ifndef HG_GATHER_BATCH_SMALL
 #define HG_GATHER_BATCH_SMALL 13  // small launches: fanout 25 in two round trips
 #endif
@@ -256,16 +259,18 @@ __device__ __forceinline__ float4 load_row4(const MeanBlock& B, std::uint32_t ke
 }
 
 // 8 consecutive features of a half-precision row (one 16-byte load)
+template <bool CACHED>
 __device__ __forceinline__ void load_row8(const MeanBlock& B, std::uint32_t key, int c, float4& a, float4& b) {
   const void* base = B.h;
   std::size_t row = key;
-  if (B.slot) {
+  if (CACHED && B.slot) {
     const int sl = __ldg(B.slot + key);
     if (sl >= 0) {
       base = B.cache;
       row = static_cast<std::size_t>(sl);
     }
   }
+  // (the L2 256-byte hint of the fp32 rows measured slower here: 394 -> 410 us/step on C5)
   const uint4 raw = __ldg(reinterpret_cast<const uint4*>(static_cast<const std::uint16_t*>(base) + row * B.ld_h + c));
   float2 f[4];
   const std::uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
@@ -373,7 +378,7 @@ __global__ void __launch_bounds__(256, WIDE || NB > kGatherBatch ? 4 : 8) k_gath
 #pragma unroll
           for (int q = 0; q < NB; ++q) {
             v[q] = w[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (q < cnt) load_row8(B, kk[q], c, v[q], w[q]);
+            if (q < cnt) load_row8<CACHED>(B, kk[q], c, v[q], w[q]);
           }
 #pragma unroll
           for (int q = 0; q < NB; ++q) {
@@ -467,8 +472,10 @@ void gather_mean(MeanBatch& m, cudaStream_t st) {
     cached = cached || m.b[b].slot != nullptr;
   }
   const bool small = items <= 8 * 16 * num_sms();  // fewer half-warp items than 8 warps per SM
-  if (wide)
-    launch_pdl(k_gather_mean<true, true, kGatherBatch>, grid, 256, 0, st, m);  // half tables: host or HBM
+  if (wide && cached)
+    launch_pdl(k_gather_mean<true, true, kGatherBatch>, grid, 256, 0, st, m);  // half tables in host memory
+  else if (wide)
+    launch_pdl(k_gather_mean<true, false, HG_GATHER_BATCH_WIDE>, grid, 256, 0, st, m);  // half tables in HBM
   else if (cached)
     launch_pdl(k_gather_mean<false, true, kGatherBatch>, grid, 256, 0, st, m);
   else if (small)

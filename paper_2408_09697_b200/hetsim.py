@@ -113,6 +113,26 @@ def mag240m_spec(scale: float = 1.0) -> dict:
                 self_paired=["cites"])
 
 
+def igb_het_spec(scale: float = 1.0) -> dict:
+    """BASELINE.json configs[4] / SURVEY §8 C5: IGB-HET shape (4 types,
+    2.6e7 nodes, 4.9e8 edges with reverses, 7 edge types, 1024-d features on every type),
+    split as IGB-HET medium's public statistics (paper 10.0M, author 15.5M, institute 23K,
+    fos 415K; cites 120M, written 40M, affiliated 7.5M, topic 128M forward edges), uniform
+    degrees, 19 classes, every count multiplied by `scale`."""
+    def n(x):
+        return max(1, int(round(x * scale)))
+    return dict(name=f"igb-het-shape-x{scale:g}", target="paper", num_classes=19, label_noise=0.1,
+                node_types=[dict(name="paper", count=n(10000000), dim=1024, storage="dense"),
+                            dict(name="author", count=n(15544654), dim=1024, storage="dense"),
+                            dict(name="institute", count=n(23256), dim=1024, storage="dense"),
+                            dict(name="fos", count=n(415054), dim=1024, storage="dense")],
+                relations=[dict(src="paper", edge="cites", dst="paper", edges=n(120077694)),
+                           dict(src="author", edge="written", dst="paper", edges=n(39854592)),
+                           dict(src="author", edge="affiliated", dst="institute", edges=n(7501203)),
+                           dict(src="fos", edge="topic", dst="paper", edges=n(127565080))],
+                self_paired=["cites"])
+
+
 def mix_seed(a: int, b: int) -> int:
     """mix_seed (src/sampling.cpp:9-15)."""
     return int(N.lib().hg_mix_seed(a, b))
