@@ -22,6 +22,7 @@
 
 #include "host.hpp"
 #include "kernels.cuh"
+#include "rgat.cuh"
 
 #ifdef HG_WITH_NCCL
 #include <nccl.h>
@@ -332,6 +333,10 @@ class Engine {
   void run_backward_rgat();
   void run_update_rgat();
   const float* rgat_src(const BlockBuf& b, int& ld);  // source-frontier rows of an inner block's layer input
+  // aggregate-first layers (all but a replica's top layer, whose batch rows are a strided
+  // shard of the logits: that one projects its sources first)
+  bool rgat_agg_first(int layer) const { return !(layer == o_.k && replica_); }
+  AttLeafJob rgat_leaf_job(const BlockBuf& b);
   float* rgat_wpart_ = nullptr;  // weight-gradient split-K partials
   std::size_t rgat_wpart_floats_ = 0;
   void timed(const char* name, double bytes, const std::function<void()>& f);

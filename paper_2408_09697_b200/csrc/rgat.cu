@@ -36,9 +36,10 @@ void Engine::rgat_plan(const Graph& g) {
   if (round_up4(num_classes_) > kAttMaxCols || round_up4(o_.hidden) > kAttMaxCols)
     throw std::invalid_argument("RGAT layer wider than 512 columns");
   for (auto& b : blocks_) {
-    // inner blocks: every transposed view (dz feeds the weight gradient); layer-1 blocks
-    // keep theirs only for learnable sources (their rows' gradient)
-    if (b.hop < o_.k) b.need_src_grad = true;
+    // aggregate-first layers keep the transposed view only where the source needs a
+    // gradient (the RGCN rule); the project-first top layer of a replica needs every
+    // block's (dz feeds its weight gradient)
+    if (!rgat_agg_first(o_.k - b.hop + 1)) b.need_src_grad = true;
     if (b.edge_cap >= (1 << 28)) throw std::invalid_argument("RGAT block edge capacity exceeds 2^28");
   }
 }
@@ -57,8 +58,8 @@ void Engine::rgat_alloc() {
     b.alpha = static_cast<float*>(alloc(static_cast<std::size_t>(b.edge_cap) * b.heads * 4));
     b.dt = static_cast<float*>(alloc(static_cast<std::size_t>(b.edge_cap) * b.heads * 4));
     b.lse = static_cast<float*>(alloc(static_cast<std::size_t>(std::max(1, b.rows_cap)) * b.heads * 4));
-    if (b.hop == k) {
-      if (b.din > 256) throw std::invalid_argument("RGAT layer-0 rows wider than 256 columns");
+    if (rgat_agg_first(l)) {
+      if (b.din > 256) throw std::invalid_argument("RGAT input rows wider than 256 columns");
       b.din_p = round_up4(std::max(1, b.din));
       const std::size_t ldg = static_cast<std::size_t>(b.heads) * b.din_p;
       b.agg = static_cast<float*>(alloc(round32(b.rows_cap) * ldg * 4));
@@ -71,7 +72,7 @@ void Engine::rgat_alloc() {
       b.dwfull = static_cast<float*>(alloc(ldg * b.ld_z * 4));
       b.dq_part = static_cast<float*>(alloc(static_cast<std::size_t>(halves) * ldg * 4));
       wpart += ceil_div(round32(b.rows_cap), kWChunkRows) * ldg * dout;
-      if (b.need_src_grad) {  // learnable sources: the transposed gather's dz rows
+      if (b.need_src_grad) {  // sources with a gradient: the transposed gather's dz rows
         const std::size_t zr = round32(b.src_cap);
         b.dz = static_cast<float*>(alloc(zr * b.ld_z * 4));
         b.tsum = static_cast<float*>(alloc(zr * b.heads * 4));
@@ -117,6 +118,27 @@ const float* Engine::rgat_src(const BlockBuf& b, int& ld) {
   throw std::runtime_error("RGAT: no layer input for a block's source type");
 }
 
+AttLeafJob Engine::rgat_leaf_job(const BlockBuf& b) {
+  // layer 1 reads the layer-0 table by global id; inner layers the previous layer's rows
+  // by source-frontier row
+  const void* table;
+  int ld_t, dtype;
+  const std::uint32_t* keys;
+  if (b.hop == o_.k) {
+    const TypeTable& tb = tables_[b.src_t];
+    table = tb.w;
+    ld_t = tb.ld;
+    dtype = tb.dense ? tb.dtype : static_cast<int>(kF32);
+    keys = b.src;
+  } else {
+    table = rgat_src(b, ld_t);
+    dtype = kF32;
+    keys = b.col;
+  }
+  return AttLeafJob{b.indptr, keys, table, ld_t, dtype, b.din, b.din_p, block_rows(b), b.rows_cap, b.qv, b.te,
+                    b.lse, b.alpha, b.agg, b.dagg, b.dt, b.dq_part, b.heads};
+}
+
 namespace {
 template <typename B, typename S>
 AttLeafParam leaf_param(const B& b, const S& s) {
@@ -132,27 +154,24 @@ void Engine::run_forward_rgat() {
     const int d = k - l + 1;
     const bool top = l == k;
     std::vector<ProjBatch> pbs(1);
-    if (l == 1) {
-      // (1) q and W_bd of every layer-1 relation, (2) per-head aggregates from the tables
+    if (rgat_agg_first(l)) {
+      // (1) q and W_bd of every relation of the layer, (2) per-head aggregates of the input
+      //     rows (tables at layer 1, the previous layer's rows above)
       AttLeafParams lp{};
       AttLeafBatch lb{};
       for (const auto& gr : groups_) {
-        if (gr.layer != 1) continue;
+        if (gr.layer != l) continue;
         for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
           const BlockBuf& b = blocks_[gr.blocks[q]];
-          const Slot& s = slots_[gr.slots[q]];
-          const TypeTable& tb = tables_[b.src_t];
-          lp.p[lp.n++] = leaf_param(b, s);
-          lb.j[lb.n++] = {b.indptr, b.src, tb.w, tb.ld, tb.dense ? tb.dtype : static_cast<int>(kF32), b.din, b.din_p,
-                          block_rows(b), b.rows_cap, b.qv, b.te, b.lse, b.alpha, b.agg, b.dagg, b.dt, b.dq_part,
-                          b.heads};
+          lp.p[lp.n++] = leaf_param(b, slots_[gr.slots[q]]);
+          lb.j[lb.n++] = rgat_leaf_job(b);
         }
       }
       timed("rgat_prep", 0, [&] { att_leaf_prep(lp, st_); });
       timed(top ? "rgat_attend_top" : "rgat_attend", 0, [&] { att_leaf_forward(lb, st_); });
       // (3) out = sum_r agg_r . W_bd,r (+ReLU): the RGCN projection's shape
       for (const auto& gr : groups_) {
-        if (gr.layer != 1) continue;
+        if (gr.layer != l) continue;
         if (gr.blocks.empty()) {
           if (!top) zero_rows(gr.out, gr.ld, front(gr.depth - 1, gr.type).count, gr.rows_cap, st_);
           continue;
@@ -286,12 +305,12 @@ void Engine::run_backward_rgat() {
       sc.b[sc.nb++] = {b.erow, b.alpha, b.dt, gr->dout_buf, top ? nullptr : gr->out, gr->ld, s.a, b.dz, b.tsum,
                        b.ld_z, s.dout, b.heads, ch.b[q].type, top ? shard_count_ : 1, top ? shard_index_ : 0};
     }
-    if (l == 1) {
-      // layer 1: dout masked in place, dagg = dout . W_bd^T, per edge dt + dq partials,
-      // dW_bd = agg^T dout, then dW / da
+    if (rgat_agg_first(l)) {
+      // aggregate-first layer: dout masked in place, dagg = dout . W_bd^T, per edge dt + dq
+      // partials, dW_bd = agg^T dout, then dW / da
       if (!top)
         for (const auto& gr : groups_)
-          if (gr.layer == 1 && !gr.blocks.empty())
+          if (gr.layer == l && !gr.blocks.empty())
             relu_mask(gr.dout_buf, gr.out, gr.ld, front(gr.depth - 1, gr.type).count, gr.rows_cap, st_);
       std::vector<ProjBatch> dbs(1);
       AttLeafBatch lb{};
@@ -299,11 +318,10 @@ void Engine::run_backward_rgat() {
       WGradBatch wb{};
       std::size_t off = 0;
       for (const auto& gr : groups_) {
-        if (gr.layer != 1) continue;
+        if (gr.layer != l) continue;
         for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
           const BlockBuf& b = blocks_[gr.blocks[q]];
           const Slot& s = slots_[gr.slots[q]];
-          const TypeTable& tt = tables_[b.src_t];
           const int ldg = b.heads * b.din_p;
           if (dbs.back().ng == kProjGroups) dbs.emplace_back();
           ProjGroup& pg = dbs.back().g[dbs.back().ng++];
@@ -317,9 +335,7 @@ void Engine::run_backward_rgat() {
           pg.out_stride = 1;
           pg.out_offset = 0;
           pg.r[0] = {gr.dout_buf, gr.ld, gr.dout, b.wbdt, ldg};
-          lb.j[lb.n++] = {b.indptr, b.src, tt.w, tt.ld, tt.dense ? tt.dtype : static_cast<int>(kF32), b.din, b.din_p,
-                          block_rows(b), b.rows_cap, b.qv, b.te, b.lse, b.alpha, b.agg, b.dagg, b.dt, b.dq_part,
-                          b.heads};
+          lb.j[lb.n++] = rgat_leaf_job(b);
           lp.p[lp.n++] = leaf_param(b, s);
           if (wb.np == kMaxProblems) throw std::runtime_error("too many RGAT weight-gradient problems per layer");
           const int rows_cap = std::max(1, b.rows_cap);
