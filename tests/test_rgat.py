@@ -270,3 +270,37 @@ def test_rgat_multi_gpu_matches_one_gpu(H, p):
             if n in want:
                 assert_adam_close(v, want[n], None, steps=n_batches, max_flip_frac=1e-2, what=f"p={p} rank {r}: {n}")
     assert any(n.startswith("att.") for n in seen)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+def test_rgat_half_tables_match_oracle(H, ref, dtype):
+    """Layer-1 attention reads fp16 / bf16 feature rows (k_att_leaf_*'s 8-byte loads): the
+    reference's features rounded to that type make the same step as the f64 restatement."""
+    rg = ref.RefGraph.bundled("mag-mini", 5)
+    rg.round_features(dtype)
+    g = port.Graph(rg.export())
+    tree = port.bfs_metatree(g, 2)
+    blocks = blocks_from(rg.sample_khop(BATCH, FANOUTS, RNG_SEED, port.hop_relation_sets(tree, 2)), 2, g.ntypes,
+                         g.nrels)
+    gd = H.gen_synthetic(H.bundled_spec("mag-mini"), 5)
+    eng = H.Engine(gd, FANOUTS, hidden=HIDDEN, batch_cap=len(BATCH), model_seed=77, learn_seed=88, model="rgat",
+                   heads=HEADS, feat_dtype=dtype)
+    names = eng.tensor_names()
+    init = eng.read(*[n for n in names if n.startswith(("post.r", "att.", "post.learn.t"))])
+    weights = {(int(n.split(".")[1][1:]), int(n.split(".")[2][1:])): init[n] for n in init if n.startswith("post.r")}
+    att = {(int(n.split(".")[1][1:]), int(n.split(".")[2][1:])): init[n].ravel() for n in init if n.startswith("att.")}
+    learn = {int(n.split(".t")[-1]): init[n] for n in init if n.startswith("post.learn.t")}
+    loss, logits, Hw, dl, wg, ag, fg = R.step(g, tree, blocks, weights, att, learn, HIDDEN, HEADS, BATCH)
+    rep = eng.step(BATCH, RNG_SEED, 0, train=True)
+    got = eng.read(*[n for n in names if n.startswith(("H1.", "logits", "grad.w.", "grad.att."))])
+    assert abs(rep["loss"] - loss) <= TOL * abs(loss)
+    assert_close(got["logits"], logits, TOL, f"RGAT {dtype} logits")
+    for t in range(g.ntypes):
+        if t in Hw[1]:
+            assert_close(got[f"H1.t{t}"], Hw[1][t], TOL, f"RGAT {dtype} H1.t{t}")
+    if _relu_flips(got, Hw, blocks, g):
+        pytest.skip("ReLU tie flipped vs the f64 oracle; forward parity checked")
+    for (r, l), want in wg.items():
+        assert_close(got[f"grad.w.r{r}.l{l}"], want, TOL, f"RGAT {dtype} grad.w.r{r}.l{l}")
+        assert_close(got[f"grad.att.r{r}.l{l}"].ravel(), ag[(r, l)], TOL, f"RGAT {dtype} grad.att.r{r}.l{l}")
