@@ -695,8 +695,10 @@ void Engine::upload(const Graph& g) {
   }
 
   ldc_ = round_up4(num_classes_);
-  logits_ = static_cast<float*>(alloc(static_cast<std::size_t>(o_.batch_cap + 1) * ldc_ * 4));
-  dlogits_ = static_cast<float*>(alloc(static_cast<std::size_t>(o_.batch_cap + 1) * ldc_ * 4));
+  // + kMaxRep rows: a replica's strided shard view (rows i * shards + shard, i < ceil(B /
+  // shards)) may reach past the counter row by up to shards - 1 rows (never read as data)
+  logits_ = static_cast<float*>(alloc(static_cast<std::size_t>(o_.batch_cap + 1 + kMaxRep) * ldc_ * 4));
+  dlogits_ = static_cast<float*>(alloc(static_cast<std::size_t>(o_.batch_cap + 1 + kMaxRep) * ldc_ * 4));
   if (o_.p > ldc_) throw std::invalid_argument("more partitions than logit columns for the AGG_all counters");
   for (auto& gr : groups_) {
     if (gr.layer == o_.k) {

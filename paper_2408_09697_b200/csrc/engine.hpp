@@ -255,8 +255,8 @@ class Engine {
     int din = 0, ld_mean = 0;
     bool need_src_grad = false;
     // RGAT (rgat.cuh): projected source rows, scores, softmax state and gradients
-    float *z = nullptr, *sc = nullptr, *lse = nullptr, *alpha = nullptr, *dt = nullptr;
-    float *dz = nullptr, *tsum = nullptr, *da_part = nullptr;
+    float *lse = nullptr, *alpha = nullptr, *dt = nullptr;
+    float *dz = nullptr, *tsum = nullptr;
     int ld_z = 0, heads = 1, src_cap = 0;
     // RGAT layer 1 (aggregate first, rgat.cuh): per-head aggregates of the table rows and
     // the block-diagonal weight; din_p = round_up4(din)
@@ -333,10 +333,7 @@ class Engine {
   void run_backward_rgat();
   void run_update_rgat();
   const float* rgat_src(const BlockBuf& b, int& ld);  // source-frontier rows of an inner block's layer input
-  // aggregate-first layers (all but a replica's top layer, whose batch rows are a strided
-  // shard of the logits: that one projects its sources first)
-  bool rgat_agg_first(int layer) const { return !(layer == o_.k && replica_); }
-  AttLeafJob rgat_leaf_job(const BlockBuf& b);
+  AttLeafJob rgat_leaf_job(const BlockBuf& b);  // a block's aggregate-first attention job
   float* rgat_wpart_ = nullptr;  // weight-gradient split-K partials
   std::size_t rgat_wpart_floats_ = 0;
   void timed(const char* name, double bytes, const std::function<void()>& f);

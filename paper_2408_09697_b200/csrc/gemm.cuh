@@ -96,6 +96,7 @@ struct ProjRel {
   int din;
   const float* w;
   int ld_w;
+  int row_stride;  // elements between consecutive A rows (0: ld_mean); a replica's shard of the logits
 };
 constexpr int kProjRels = 16;   // relations into one destination type (concatenated along K)
 constexpr int kProjGroups = 4;  // destination types per projection launch

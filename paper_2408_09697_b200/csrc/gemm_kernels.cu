@@ -419,7 +419,8 @@ __global__ void __launch_bounds__(kT) k_project_tiles(ProjBatch pb) {
         const int m = x / (kKS / 4), kq = (x % (kKS / 4)) * 4;
         float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
         if (row0 + m < n && kq < kn)
-          a = *reinterpret_cast<const float4*>(r.mean + static_cast<std::size_t>(row0 + m) * r.ld_mean + k0 + kq);
+          a = *reinterpret_cast<const float4*>(r.mean + static_cast<std::size_t>(row0 + m) *
+                                                             (r.row_stride ? r.row_stride : r.ld_mean) + k0 + kq);
         As[(kq + 0) * kLd + m] = a.x;
         As[(kq + 1) * kLd + m] = a.y;
         As[(kq + 2) * kLd + m] = a.z;

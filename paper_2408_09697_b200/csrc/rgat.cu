@@ -1,21 +1,17 @@
-// RGAT layer type of the engine (rgat.cuh defines the layer).
-//
-// Layer 1 (hop-k blocks, sources read from the layer-0 tables), aggregate first:
+// RGAT layer type of the engine (rgat.cuh defines the layer). Every layer is aggregate
+// first (the input rows are the layer-0 tables at layer 1, the previous layer's rows above):
 //   forward:  q_r^h = W_r^(h) a_r^h; per destination row and head the online softmax of
-//             LeakyReLU(x_j . q^h) over its edges and agg^h = sum_e alpha_e^h x_j, read from
-//             the feature / learnable table by global id (no projected source rows); then
+//             LeakyReLU(x_j . q^h) over its edges and agg^h = sum_e alpha_e^h x_j, read by
+//             global id (tables) or source-frontier row (no projected source rows); then
 //             out = sum_r agg_r . W_bd,r (tcgen05 projection, relations along K, ReLU);
 //   backward: dagg = dout . W_bd^T (tcgen05), per edge dt and the ordered dq^h partials,
 //             dW_bd = agg^T dout (tcgen05 split-K), dW = its diagonal blocks + dq a^T,
-//             da = W^T dq; learnable sources also take the transposed gather into dz and
+//             da = W^T dq; sources with a gradient (inner types, learnable leaves) take the
+//             transposed gather over the hop's CSC view (entries = (block, edge)) into dz and
 //             dH = dz . W^T (dz carries the score term: sum_h tsum^h q^h = W (tsum a)).
-// Inner layers (sources = the previous layer's rows), project first:
-//   forward:  z_b = H_src . W_r (tcgen05), raw scores t = a . z per head, per destination
-//             row the softmax over its edges and the weighted sum of z rows;
-//   backward: per edge dt, the transposed gather over the hop's CSC view (entries =
-//             (block, edge)) into dz_b and tsum_b, dW_r = H_src^T dz_b (tcgen05 split-K),
-//             da_r = sum_j tsum_b[j] z_b[j] (ordered), dH_src = sum_b dz_b . W_r^T.
-// Inner-layer gradients are stored unmasked and masked by H > 0 where they are read.
+// A replica's top layer trains a strided shard of the batch rows: its projection writes and
+// its gradient GEMMs read the logits rows i * shards + shard (strided operands).
+// Inner-layer gradients are masked by H > 0 in place before they are read.
 #include <cmath>
 #include <random>
 
@@ -35,13 +31,9 @@ void Engine::rgat_plan(const Graph& g) {
   if (o_.feat_host) throw std::invalid_argument("RGAT reads its layer-0 rows from HBM tables (feat_host = 0)");
   if (round_up4(num_classes_) > kAttMaxCols || round_up4(o_.hidden) > kAttMaxCols)
     throw std::invalid_argument("RGAT layer wider than 512 columns");
-  for (auto& b : blocks_) {
-    // aggregate-first layers keep the transposed view only where the source needs a
-    // gradient (the RGCN rule); the project-first top layer of a replica needs every
-    // block's (dz feeds its weight gradient)
-    if (!rgat_agg_first(o_.k - b.hop + 1)) b.need_src_grad = true;
+  // (transposed views only where the source needs a gradient: the RGCN rule)
+  for (auto& b : blocks_)
     if (b.edge_cap >= (1 << 28)) throw std::invalid_argument("RGAT block edge capacity exceeds 2^28");
-  }
 }
 
 void Engine::rgat_alloc() {
@@ -58,34 +50,24 @@ void Engine::rgat_alloc() {
     b.alpha = static_cast<float*>(alloc(static_cast<std::size_t>(b.edge_cap) * b.heads * 4));
     b.dt = static_cast<float*>(alloc(static_cast<std::size_t>(b.edge_cap) * b.heads * 4));
     b.lse = static_cast<float*>(alloc(static_cast<std::size_t>(std::max(1, b.rows_cap)) * b.heads * 4));
-    if (rgat_agg_first(l)) {
-      if (b.din > 256) throw std::invalid_argument("RGAT input rows wider than 256 columns");
-      b.din_p = round_up4(std::max(1, b.din));
-      const std::size_t ldg = static_cast<std::size_t>(b.heads) * b.din_p;
-      b.agg = static_cast<float*>(alloc(round32(b.rows_cap) * ldg * 4));
-      b.dagg = static_cast<float*>(alloc(round32(b.rows_cap) * ldg * 4));
-      b.te = static_cast<float*>(alloc(static_cast<std::size_t>(b.edge_cap) * b.heads * 4));
-      b.qv = static_cast<float*>(alloc(ldg * 4));
-      b.dqv = static_cast<float*>(alloc(static_cast<std::size_t>(att_leaf_dq_rows()) * ldg * 4));
-      b.wbd = static_cast<float*>(alloc(ldg * b.ld_z * 4));
-      b.wbdt = static_cast<float*>(alloc(static_cast<std::size_t>(dout) * ldg * 4));
-      b.dwfull = static_cast<float*>(alloc(ldg * b.ld_z * 4));
-      b.dq_part = static_cast<float*>(alloc(static_cast<std::size_t>(halves) * ldg * 4));
-      wpart += ceil_div(round32(b.rows_cap), kWChunkRows) * ldg * dout;
-      if (b.need_src_grad) {  // sources with a gradient: the transposed gather's dz rows
-        const std::size_t zr = round32(b.src_cap);
-        b.dz = static_cast<float*>(alloc(zr * b.ld_z * 4));
-        b.tsum = static_cast<float*>(alloc(zr * b.heads * 4));
-      }
-      continue;
+    if (b.din > 256) throw std::invalid_argument("RGAT input rows wider than 256 columns");
+    b.din_p = round_up4(std::max(1, b.din));
+    const std::size_t ldg = static_cast<std::size_t>(b.heads) * b.din_p;
+    b.agg = static_cast<float*>(alloc(round32(b.rows_cap) * ldg * 4));
+    b.dagg = static_cast<float*>(alloc(round32(b.rows_cap) * ldg * 4));
+    b.te = static_cast<float*>(alloc(static_cast<std::size_t>(b.edge_cap) * b.heads * 4));
+    b.qv = static_cast<float*>(alloc(ldg * 4));
+    b.dqv = static_cast<float*>(alloc(static_cast<std::size_t>(att_leaf_dq_rows()) * ldg * 4));
+    b.wbd = static_cast<float*>(alloc(ldg * b.ld_z * 4));
+    b.wbdt = static_cast<float*>(alloc(static_cast<std::size_t>(dout) * ldg * 4));
+    b.dwfull = static_cast<float*>(alloc(ldg * b.ld_z * 4));
+    b.dq_part = static_cast<float*>(alloc(static_cast<std::size_t>(halves) * ldg * 4));
+    wpart += ceil_div(round32(b.rows_cap), kWChunkRows) * ldg * dout;
+    if (b.need_src_grad) {  // sources with a gradient: the transposed gather's dz rows
+      const std::size_t zr = round32(b.src_cap);
+      b.dz = static_cast<float*>(alloc(zr * b.ld_z * 4));
+      b.tsum = static_cast<float*>(alloc(zr * b.heads * 4));
     }
-    const std::size_t zr = round32(b.src_cap);
-    b.z = static_cast<float*>(alloc(zr * b.ld_z * 4));
-    b.sc = static_cast<float*>(alloc(zr * b.heads * 4));
-    b.dz = static_cast<float*>(alloc(zr * b.ld_z * 4));
-    b.tsum = static_cast<float*>(alloc(zr * b.heads * 4));
-    b.da_part = static_cast<float*>(alloc(ceil_div(std::max(1, b.src_cap), kAttDaChunk) * b.ld_z * 4));
-    wpart += ceil_div(zr, kWChunkRows) * static_cast<std::size_t>(std::max(1, b.din)) * dout;
   }
   rgat_wpart_floats_ = std::max<std::size_t>(1, wpart);
   rgat_wpart_ = static_cast<float*>(alloc(rgat_wpart_floats_ * 4));
@@ -151,115 +133,51 @@ void Engine::run_forward_rgat() {
   const int k = o_.k;
   HG_CUDA(cudaMemsetAsync(logits_, 0, static_cast<std::size_t>(o_.batch_cap + 1) * ldc_ * 4, st_));
   for (int l = 1; l <= k; ++l) {
-    const int d = k - l + 1;
     const bool top = l == k;
     std::vector<ProjBatch> pbs(1);
-    if (rgat_agg_first(l)) {
-      // (1) q and W_bd of every relation of the layer, (2) per-head aggregates of the input
-      //     rows (tables at layer 1, the previous layer's rows above)
-      AttLeafParams lp{};
-      AttLeafBatch lb{};
-      for (const auto& gr : groups_) {
-        if (gr.layer != l) continue;
-        for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
-          const BlockBuf& b = blocks_[gr.blocks[q]];
-          lp.p[lp.n++] = leaf_param(b, slots_[gr.slots[q]]);
-          lb.j[lb.n++] = rgat_leaf_job(b);
-        }
-      }
-      timed("rgat_prep", 0, [&] { att_leaf_prep(lp, st_); });
-      timed(top ? "rgat_attend_top" : "rgat_attend", 0, [&] { att_leaf_forward(lb, st_); });
-      // (3) out = sum_r agg_r . W_bd,r (+ReLU): the RGCN projection's shape
-      for (const auto& gr : groups_) {
-        if (gr.layer != l) continue;
-        if (gr.blocks.empty()) {
-          if (!top) zero_rows(gr.out, gr.ld, front(gr.depth - 1, gr.type).count, gr.rows_cap, st_);
-          continue;
-        }
-        if (pbs.back().ng == kProjGroups) pbs.emplace_back();
-        ProjGroup& pg = pbs.back().g[pbs.back().ng++];
-        pg.nrel = static_cast<int>(gr.blocks.size());
-        pg.n_rows = front(gr.depth - 1, gr.type).count;
-        pg.rows_cap = gr.rows_cap;
-        pg.out = gr.out;
-        pg.ld_out = gr.ld;
-        pg.dout = gr.dout;
-        pg.relu = top ? 0 : 1;
-        pg.out_stride = 1;
-        pg.out_offset = 0;
-        for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
-          const BlockBuf& b = blocks_[gr.blocks[q]];
-          const Slot& s = slots_[gr.slots[q]];
-          const int ldg = b.heads * b.din_p;
-          pg.r[q] = {b.agg, ldg, ldg, b.wbd, s.ld};
-        }
-      }
-      timed(top ? "rgat_project_top" : "rgat_project", 0, [&] {
-        for (auto& pb : pbs) use_umma_ ? project_umma(pb, st_) : project_tiles(pb, st_);
-      });
-      continue;
-    }
-    // inner layers: (1) z_b = H_src . W_r over every block's source frontier, (2) raw scores
-    AttScoreBatch sb{};
+    // (1) q and W_bd of every relation of the layer, (2) per-head aggregates of the input rows
+    //     (tables at layer 1, the previous layer's rows above)
+    AttLeafParams lp{};
+    AttLeafBatch lb{};
     for (const auto& gr : groups_) {
       if (gr.layer != l) continue;
       for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
         const BlockBuf& b = blocks_[gr.blocks[q]];
-        const Slot& s = slots_[gr.slots[q]];
-        int ld_src = 0;
-        const float* src = rgat_src(b, ld_src);
-        if (pbs.back().ng == kProjGroups) pbs.emplace_back();
-        ProjGroup& pg = pbs.back().g[pbs.back().ng++];
-        pg.nrel = 1;
-        pg.n_rows = front(d, b.src_t).count;
-        pg.rows_cap = b.src_cap;
-        pg.out = b.z;
-        pg.ld_out = b.ld_z;
-        pg.dout = s.dout;
-        pg.relu = 0;
-        pg.out_stride = 1;
-        pg.out_offset = 0;
-        pg.r[0] = {src, ld_src, b.din, s.w, s.ld};
-        if (sb.n == static_cast<int>(sizeof(sb.j) / sizeof(sb.j[0]))) throw std::runtime_error("too many RGAT blocks");
-        sb.j[sb.n++] = {b.z, s.a, b.sc, front(d, b.src_t).count, b.src_cap, b.ld_z, s.dout, b.heads};
+        lp.p[lp.n++] = leaf_param(b, slots_[gr.slots[q]]);
+        lb.j[lb.n++] = rgat_leaf_job(b);
       }
     }
-    timed(top ? "rgat_project_top" : "rgat_project", 0, [&] {
-      for (auto& pb : pbs) use_umma_ ? project_umma(pb, st_) : project_tiles(pb, st_);
-    });
-    timed("rgat_scores", 0, [&] { att_scores(sb, st_); });
-    // (3) softmax-weighted sums over every destination row, relations summed per type
-    std::vector<AttBatch> abs(1);
+    timed("rgat_prep", 0, [&] { att_leaf_prep(lp, st_); });
+    timed(top ? "rgat_attend_top" : "rgat_attend", 0, [&] { att_leaf_forward(lb, st_); });
+    // (3) out = sum_r agg_r . W_bd,r (+ReLU): the RGCN projection's shape; a replica's top
+    //     layer writes its shard rows of the logits
     for (const auto& gr : groups_) {
       if (gr.layer != l) continue;
       if (gr.blocks.empty()) {
         if (!top) zero_rows(gr.out, gr.ld, front(gr.depth - 1, gr.type).count, gr.rows_cap, st_);
         continue;
       }
-      if (gr.blocks.size() > static_cast<std::size_t>(kProjRels))
-        throw std::runtime_error("more relations into one type than an attention group holds");
-      if (abs.back().ng == kProjGroups) abs.emplace_back();
-      AttGroup& ag = abs.back().g[abs.back().ng++];
-      ag.nrel = static_cast<int>(gr.blocks.size());
+      const bool shard = top && replica_;
+      if (pbs.back().ng == kProjGroups) pbs.emplace_back();
+      ProjGroup& pg = pbs.back().g[pbs.back().ng++];
+      pg.nrel = static_cast<int>(gr.blocks.size());
+      pg.n_rows = shard ? shard_count_dev_ : front(gr.depth - 1, gr.type).count;
+      pg.rows_cap = shard ? static_cast<int>(ceil_div(o_.batch_cap, shard_count_)) : gr.rows_cap;
+      pg.out = gr.out;
+      pg.ld_out = gr.ld;
+      pg.dout = gr.dout;
+      pg.relu = top ? 0 : 1;
+      pg.out_stride = top ? shard_count_ : 1;
+      pg.out_offset = top ? shard_index_ : 0;
       for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
         const BlockBuf& b = blocks_[gr.blocks[q]];
-        ag.r[q] = {b.indptr, b.col, b.z, b.sc, b.lse, b.alpha, b.dt};
+        const Slot& s = slots_[gr.slots[q]];
+        const int ldg = b.heads * b.din_p;
+        pg.r[q] = {b.agg, ldg, ldg, b.wbd, s.ld};
       }
-      const bool shard = top && replica_;  // a replica trains its shard of the batch rows
-      ag.n_rows = shard ? shard_count_dev_ : front(gr.depth - 1, gr.type).count;
-      ag.rows_cap = shard ? static_cast<int>(ceil_div(o_.batch_cap, shard_count_)) : gr.rows_cap;
-      ag.out = gr.out;
-      ag.dout = nullptr;
-      ag.relu_h = nullptr;
-      ag.ld = gr.ld;
-      ag.cols = gr.dout;
-      ag.heads = heads_of(l);
-      ag.relu = top ? 0 : 1;
-      ag.row_stride = top ? shard_count_ : 1;
-      ag.row_offset = top ? shard_index_ : 0;
     }
-    timed(top ? "rgat_attend_top" : "rgat_attend", 0, [&] {
-      for (auto& ab : abs) att_forward(ab, st_);
+    timed(top ? "rgat_project_top" : "rgat_project", 0, [&] {
+      for (auto& pb : pbs) use_umma_ ? project_umma(pb, st_) : project_tiles(pb, st_);
     });
   }
   run_agg_all();
@@ -305,102 +223,53 @@ void Engine::run_backward_rgat() {
       sc.b[sc.nb++] = {b.erow, b.alpha, b.dt, gr->dout_buf, top ? nullptr : gr->out, gr->ld, s.a, b.dz, b.tsum,
                        b.ld_z, s.dout, b.heads, ch.b[q].type, top ? shard_count_ : 1, top ? shard_index_ : 0};
     }
-    if (rgat_agg_first(l)) {
-      // aggregate-first layer: dout masked in place, dagg = dout . W_bd^T, per edge dt + dq
-      // partials, dW_bd = agg^T dout, then dW / da
-      if (!top)
-        for (const auto& gr : groups_)
-          if (gr.layer == l && !gr.blocks.empty())
-            relu_mask(gr.dout_buf, gr.out, gr.ld, front(gr.depth - 1, gr.type).count, gr.rows_cap, st_);
-      std::vector<ProjBatch> dbs(1);
-      AttLeafBatch lb{};
-      AttLeafParams lp{};
-      WGradBatch wb{};
-      std::size_t off = 0;
-      for (const auto& gr : groups_) {
-        if (gr.layer != l) continue;
-        for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
-          const BlockBuf& b = blocks_[gr.blocks[q]];
-          const Slot& s = slots_[gr.slots[q]];
-          const int ldg = b.heads * b.din_p;
-          if (dbs.back().ng == kProjGroups) dbs.emplace_back();
-          ProjGroup& pg = dbs.back().g[dbs.back().ng++];
-          pg.nrel = 1;
-          pg.n_rows = block_rows(b);
-          pg.rows_cap = b.rows_cap;
-          pg.out = b.dagg;
-          pg.ld_out = ldg;
-          pg.dout = ldg;
-          pg.relu = 0;
-          pg.out_stride = 1;
-          pg.out_offset = 0;
-          pg.r[0] = {gr.dout_buf, gr.ld, gr.dout, b.wbdt, ldg};
-          lb.j[lb.n++] = rgat_leaf_job(b);
-          lp.p[lp.n++] = leaf_param(b, s);
-          if (wb.np == kMaxProblems) throw std::runtime_error("too many RGAT weight-gradient problems per layer");
-          const int rows_cap = std::max(1, b.rows_cap);
-          wb.p[wb.np++] = {b.agg, ldg, ldg, DpreView{gr.dout_buf, nullptr, gr.ld, gr.dout, 1, 0}, block_rows(b), rows_cap,
-                           rgat_wpart_ + off, b.dwfull, s.ld, nullptr, nullptr, nullptr};
-          off += ceil_div(ceil_div(rows_cap, 32) * 32, kWChunkRows) * static_cast<std::size_t>(ldg) * gr.dout;
-        }
-      }
-      if (off > rgat_wpart_floats_) throw std::runtime_error("RGAT weight-gradient scratch too small");
-      timed("rgat_dagg", 0, [&] {
-        for (auto& pb : dbs) use_umma_ ? project_umma(pb, st_) : project_tiles(pb, st_);
-      });
-      timed("rgat_edge_grad", 0, [&] { att_leaf_grad(lb, st_); });
-      timed("rgat_weight_grad", 0, [&] { use_umma_ ? wgrad_umma(wb, st_) : wgrad_tiles(wb, st_); });
-      timed("rgat_att_grad", 0, [&] { att_leaf_finish(lp, st_); });
-      if (sc.nb) timed("rgat_scatter", 0, [&] { att_scatter(sc, st_); });
-    } else {
-      // inner layers: per edge dt, the transposed gather (dz, tsum), da, dW
-      std::vector<AttBatch> abs(1);
-      for (const auto& gr : groups_) {
-        if (gr.layer != l || gr.blocks.empty()) continue;
-        if (abs.back().ng == kProjGroups) abs.emplace_back();
-        AttGroup& ag = abs.back().g[abs.back().ng++];
-        ag.nrel = static_cast<int>(gr.blocks.size());
-        for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
-          const BlockBuf& b = blocks_[gr.blocks[q]];
-          ag.r[q] = {b.indptr, b.col, b.z, b.sc, b.lse, b.alpha, b.dt};
-        }
-        const bool shard = top && replica_;
-        ag.n_rows = shard ? shard_count_dev_ : front(gr.depth - 1, gr.type).count;
-        ag.rows_cap = shard ? static_cast<int>(ceil_div(o_.batch_cap, shard_count_)) : gr.rows_cap;
-        ag.out = nullptr;
-        ag.dout = gr.dout_buf;
-        ag.relu_h = top ? nullptr : gr.out;
-        ag.ld = gr.ld;
-        ag.cols = gr.dout;
-        ag.heads = heads_of(l);
-        ag.relu = 0;
-        ag.row_stride = top ? shard_count_ : 1;
-        ag.row_offset = top ? shard_index_ : 0;
-      }
-      timed("rgat_edge_grad", 0, [&] {
-        for (auto& ab : abs) att_edge_grad(ab, st_);
-      });
-      WGradBatch wb{};
-      AttDaBatch db{};
-      std::size_t off = 0;
-      for (int q = 0; q < ch.nb; ++q) {
-        const BlockBuf& b = blocks_[scatter_blocks[q]];
-        const Slot& s = slots_[slot_of_.at(SlotId{b.rel, l})];
-        db.j[db.n++] = {b.tsum, b.z, front(d, b.src_t).count, b.src_cap, b.ld_z, s.dout, b.heads, b.da_part, s.ag};
-        int ld_src = 0;
-        const float* src = rgat_src(b, ld_src);
+    // dout masked in place (inner layers), dagg = dout . W_bd^T, per edge dt + dq partials,
+    // dW_bd = agg^T dout, then dW / da; a replica's top layer reads its shard rows of dlogits
+    if (!top)
+      for (const auto& gr : groups_)
+        if (gr.layer == l && !gr.blocks.empty())
+          relu_mask(gr.dout_buf, gr.out, gr.ld, front(gr.depth - 1, gr.type).count, gr.rows_cap, st_);
+    const int stride = top ? shard_count_ : 1, offset = top ? shard_index_ : 0;
+    std::vector<ProjBatch> dbs(1);
+    AttLeafBatch lb{};
+    AttLeafParams lp{};
+    WGradBatch wb{};
+    std::size_t off = 0;
+    for (const auto& gr : groups_) {
+      if (gr.layer != l) continue;
+      for (std::size_t q = 0; q < gr.blocks.size(); ++q) {
+        const BlockBuf& b = blocks_[gr.blocks[q]];
+        const Slot& s = slots_[gr.slots[q]];
+        const int ldg = b.heads * b.din_p;
+        if (dbs.back().ng == kProjGroups) dbs.emplace_back();
+        ProjGroup& pg = dbs.back().g[dbs.back().ng++];
+        pg.nrel = 1;
+        pg.n_rows = block_rows(b);
+        pg.rows_cap = b.rows_cap;
+        pg.out = b.dagg;
+        pg.ld_out = ldg;
+        pg.dout = ldg;
+        pg.relu = 0;
+        pg.out_stride = 1;
+        pg.out_offset = 0;
+        pg.r[0] = {gr.dout_buf + static_cast<std::size_t>(offset) * gr.ld, gr.ld, gr.dout, b.wbdt, ldg, stride * gr.ld};
+        lb.j[lb.n++] = rgat_leaf_job(b);
+        lp.p[lp.n++] = leaf_param(b, s);
         if (wb.np == kMaxProblems) throw std::runtime_error("too many RGAT weight-gradient problems per layer");
-        // the operands' row extent; rows [n, next multiple of 32) of dz are zero
-        const int rows_cap = std::max(1, b.src_cap);
-        wb.p[wb.np++] = {src, ld_src, b.din, DpreView{b.dz, nullptr, b.ld_z, s.dout, 1, 0}, front(d, b.src_t).count,
-                         rows_cap, rgat_wpart_ + off, s.g, s.ld, nullptr, nullptr, nullptr};
-        off += ceil_div(rows_cap, kWChunkRows) * static_cast<std::size_t>(std::max(1, b.din)) * s.dout;
+        const int rows_cap = std::max(1, b.rows_cap);
+        wb.p[wb.np++] = {b.agg, ldg, ldg, DpreView{gr.dout_buf, nullptr, gr.ld, gr.dout, stride, offset}, block_rows(b),
+                         rows_cap, rgat_wpart_ + off, b.dwfull, s.ld, nullptr, nullptr, nullptr};
+        off += ceil_div(ceil_div(rows_cap, 32) * 32, kWChunkRows) * static_cast<std::size_t>(ldg) * gr.dout;
       }
-      if (off > rgat_wpart_floats_) throw std::runtime_error("RGAT weight-gradient scratch too small");
-      timed(top ? "rgat_scatter_top" : "rgat_scatter", 0, [&] { att_scatter(sc, st_); });
-      timed("rgat_att_grad", 0, [&] { att_da(db, st_); });
-      timed("rgat_weight_grad", 0, [&] { use_umma_ ? wgrad_umma(wb, st_) : wgrad_tiles(wb, st_); });
     }
+    if (off > rgat_wpart_floats_) throw std::runtime_error("RGAT weight-gradient scratch too small");
+    timed("rgat_dagg", 0, [&] {
+      for (auto& pb : dbs) use_umma_ ? project_umma(pb, st_) : project_tiles(pb, st_);
+    });
+    timed("rgat_edge_grad", 0, [&] { att_leaf_grad(lb, st_); });
+    timed("rgat_weight_grad", 0, [&] { use_umma_ ? wgrad_umma(wb, st_) : wgrad_tiles(wb, st_); });
+    timed("rgat_att_grad", 0, [&] { att_leaf_finish(lp, st_); });
+    if (sc.nb) timed(top ? "rgat_scatter_top" : "rgat_scatter", 0, [&] { att_scatter(sc, st_); });
     // source gradients dH_src = sum_b dz_b . W_r^T (inner types and learnable leaves)
     std::vector<ProjBatch> pbs(1);
     for (const auto& c : cscs_) {

@@ -1,5 +1,5 @@
 // Relational graph attention (RGAT, BASELINE configs[2] / SURVEY §8 C3) on the RAF
-// blocks: the kernels around the tcgen05 projections (rgat_kernels.cu).
+// blocks: the kernels around the tcgen05 projections (rgat_kernels.cu, engine side rgat.cu).
 //
 // The reference has no attention layer; this is the framework's
 // own definition, restated in oracle/rgat.py (parity against that restatement and
@@ -23,53 +23,6 @@ namespace hetgpu {
 constexpr int kAttMaxHeads = 8;
 constexpr int kAttMaxCols = 512;  // row width (ld) the attention kernels hold in registers
 constexpr float kAttSlope = 0.2f;
-
-struct AttRel {
-  const std::uint32_t* indptr;  // block rows (destination frontier order)
-  const std::uint32_t* col;     // per edge: source row in the source frontier
-  const float* z;               // [n_src x ld] projected source rows
-  const float* t;               // [n_src x heads] raw scores
-  float* lse;                   // [rows x heads] log-sum-exp of the row's LeakyReLU scores
-  float* alpha;                 // [edges x heads]
-  float* dt;                    // [edges x heads]: d loss / d t per edge (backward)
-};
-struct AttGroup {  // one destination type of one layer
-  AttRel r[kProjRels];
-  int nrel;
-  const int* n_rows;
-  int rows_cap;
-  float* out;           // forward: sum over relations (+ReLU)
-  const float* dout;    // backward: gradient of out
-  const float* relu_h;  // backward: dout masked by relu_h > 0 (inner layers), or nullptr
-  int ld;
-  int cols, heads;
-  int relu;
-  // row i of out / dout / relu_h is row i * row_stride + row_offset (a replica's shard of
-  // the batch writes its rows of the full logits, raf.cpp:390-391)
-  int row_stride, row_offset;
-};
-struct AttBatch {
-  AttGroup g[kProjGroups];
-  int ng;
-};
-// forward: per destination row, every relation's softmax and weighted sum (alpha kept)
-void att_forward(const AttBatch& b, cudaStream_t st);
-// backward, per destination row: dt of every edge (softmax and LeakyReLU backward)
-void att_edge_grad(const AttBatch& b, cudaStream_t st);
-
-// raw scores t = a . z per head for the source rows of every block
-struct AttScoreJob {
-  const float* z;
-  const float* a;
-  float* t;
-  const int* n_rows;
-  int rows_cap, ld, cols, heads;
-};
-struct AttScoreBatch {
-  AttScoreJob j[kMaxBlocks * 2];
-  int n;
-};
-void att_scores(const AttScoreBatch& b, cudaStream_t st);
 
 // backward through the CSC view of one hop (entries = packed (block, edge)):
 // per source row j and block b of its type,
@@ -100,25 +53,10 @@ struct AttScatter {
 };
 void att_scatter(const AttScatter& s, cudaStream_t st);
 
-// da_b[c] = sum_j tsum_b[j][h(c)] z_b[j][c]: ordered chunk partials, then their ordered sum
-struct AttDaJob {
-  const float* tsum;
-  const float* z;
-  const int* n_rows;
-  int rows_cap, ld, cols, heads;
-  float* partial;  // [chunks x ld]
-  float* da;       // [ld]
-};
-struct AttDaBatch {
-  AttDaJob j[kMaxBlocks * 2];
-  int n;
-};
-constexpr int kAttDaChunk = 256;
-void att_da(const AttDaBatch& b, cudaStream_t st);
-
-// ---- layer 1 (leaf sources): aggregate first. With q_r^h = W_r^(h) a_r^h the score is
-// t = x_j . q^h, so per destination row the kernel forms agg^h = sum_e alpha_e^h x_src(e)
-// straight from the feature / learnable table (by global id), and the projection reads
+// ---- aggregate first (every layer). With q_r^h = W_r^(h) a_r^h the score is t = x_j . q^h,
+// so per destination row the kernel forms agg^h = sum_e alpha_e^h x_src(e) straight from
+// the input rows (the feature / learnable table by global id at layer 1, the previous
+// layer's rows by source-frontier row above), and the projection reads
 // agg [rows x H din_p] against the block-diagonal W_bd [H din_p x d_out]; backward:
 // dagg = dout . W_bd^T, dt per edge, dq^h = sum_e dt_e^h x_src(e) (ordered partials),
 // dW = diag blocks of agg^T dout + dq a^T, da = W^T dq.

@@ -1,8 +1,8 @@
-// RGAT kernels (definitions in rgat.cuh). One half-warp per destination row (forward,
-// edge gradients) or per source row (the transposed backward gather); lane l holds
-// the float4 columns 4l + 64u of the row in registers. Every sum runs in a fixed
-// order (edges ascending, relations ascending, lanes by a fixed butterfly), so the
-// results are bit-reproducible.
+// RGAT kernels (definitions in rgat.cuh). One half-warp per destination row (the
+// aggregate-first forward and edge gradients) or a 16/32-lane group per source row (the
+// transposed backward gather); lane l holds the float4 columns 4l + 4 GL u of the row in
+// registers. Every sum runs in a fixed order (edges ascending, relations ascending, lanes
+// by a fixed butterfly, partials by index), so the results are bit-reproducible.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -19,17 +19,6 @@ constexpr int kRowBitsAtt = 28;       // CSC entries: block << 28 | edge
 
 __device__ __forceinline__ float lrelu(float x) { return x > 0.f ? x : kAttSlope * x; }
 
-// item -> (group, row) over the groups' row capacities
-__device__ __forceinline__ bool group_row(const AttBatch& b, int item, int& g, int& i) {
-  g = 0;
-  i = item;
-  while (g < b.ng && i >= b.g[g].rows_cap) {
-    i -= b.g[g].rows_cap;
-    ++g;
-  }
-  return g < b.ng;
-}
-
 // Half-warp layout: 16 lanes own a row; lane hl holds the float4 columns 4 hl + 64 u.
 // Heads are F = cols / H columns wide (F % 4 == 0 or H == 1), so a float4 lies in one head.
 __device__ __forceinline__ float hsum(float v, unsigned m) {
@@ -41,12 +30,6 @@ template <int G>
 __device__ __forceinline__ float gsum(float v, unsigned m) {
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(m, v, o, G);
-  return v;
-}
-template <int G>
-__device__ __forceinline__ float gmax(float v, unsigned m) {
-#pragma unroll
-  for (int o = G / 2; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(m, v, o, G));
   return v;
 }
 template <int G>
@@ -63,291 +46,6 @@ __device__ __forceinline__ float pick(const float* v, int h) {  // v[h] without 
   for (int x = 1; x < kAttMaxHeads; ++x)
     if (x == h) r = v[x];
   return r;
-}
-
-template <int GL, int NU4>
-__global__ void __launch_bounds__(256) k_att_forward(AttBatch b, int total) {
-  pdl_enter();
-  constexpr int EIF = NU4 <= 2 ? 4 : 2;  // edges in flight
-  const int lane = threadIdx.x & 31, hl = lane & (GL - 1);
-  const unsigned hm = group_mask<GL>(lane);
-  const int halves = gridDim.x * (blockDim.x / GL);
-  for (int item = blockIdx.x * (blockDim.x / GL) + (threadIdx.x / GL); item < total; item += halves) {
-    int g, i;
-    if (!group_row(b, item, g, i)) break;
-    const AttGroup& G = b.g[g];
-    if (i >= *G.n_rows) continue;
-    const int H = G.heads, F = G.cols / H, nu4 = (G.ld + 4 * GL - 1) / (4 * GL);
-    int hu[NU4];
-    float4 acc[NU4];
-#pragma unroll
-    for (int u = 0; u < NU4; ++u) {
-      const int c = 4 * hl + 4 * GL * u;
-      hu[u] = c < G.cols ? c / F : 0;
-      acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    for (int q = 0; q < G.nrel; ++q) {
-      const AttRel& R = G.r[q];
-      const std::uint32_t lo = R.indptr[i], hi = R.indptr[i + 1];
-      if (lo == hi) continue;
-      // pass 1: per head, online max / sum over this lane's edges, merged over the half-warp
-      float m[kAttMaxHeads], s[kAttMaxHeads];
-#pragma unroll
-      for (int h = 0; h < kAttMaxHeads; ++h) {
-        m[h] = -FLT_MAX;
-        s[h] = 0.f;
-      }
-      for (std::uint32_t e = lo + hl; e < hi; e += GL) {
-        const std::uint32_t j = R.col[e];
-#pragma unroll
-        for (int h = 0; h < kAttMaxHeads; ++h) {
-          if (h >= H) break;
-          const float x = lrelu(R.t[static_cast<std::size_t>(j) * H + h]);
-          if (x > m[h]) {
-            s[h] = s[h] * __expf(m[h] - x) + 1.f;
-            m[h] = x;
-          } else {
-            s[h] += __expf(x - m[h]);
-          }
-        }
-      }
-      float lse[kAttMaxHeads];
-#pragma unroll
-      for (int h = 0; h < kAttMaxHeads; ++h) {
-        lse[h] = 0.f;
-        if (h >= H) continue;
-        const float M = gmax<GL>(m[h], hm);
-        const float S = gsum<GL>(s[h] > 0.f ? s[h] * __expf(m[h] - M) : 0.f, hm);
-        lse[h] = M + __logf(S);
-        if (hl == h) R.lse[static_cast<std::size_t>(i) * H + h] = lse[h];
-      }
-      // pass 2: GL edges at a time; lane q owns edge q's weights, the lane group sums rows
-      for (std::uint32_t base = lo; base < hi; base += GL) {
-        const int cnt = static_cast<int>(min(static_cast<std::uint32_t>(GL), hi - base));
-        std::uint32_t my_j = 0;
-        float al[kAttMaxHeads];
-#pragma unroll
-        for (int h = 0; h < kAttMaxHeads; ++h) al[h] = 0.f;
-        if (hl < cnt) {
-          my_j = R.col[base + hl];
-#pragma unroll
-          for (int h = 0; h < kAttMaxHeads; ++h) {
-            if (h >= H) break;
-            al[h] = __expf(lrelu(R.t[static_cast<std::size_t>(my_j) * H + h]) - lse[h]);
-            R.alpha[static_cast<std::size_t>(base + hl) * H + h] = al[h];
-          }
-        }
-        for (int q0 = 0; q0 < cnt; q0 += EIF) {
-          float4 zv[EIF][NU4];
-          float aw[EIF][NU4];
-#pragma unroll
-          for (int w = 0; w < EIF; ++w) {
-            const int qq = min(q0 + w, cnt - 1);
-            const std::uint32_t j = __shfl_sync(hm, my_j, qq, GL);
-            float ah[kAttMaxHeads];
-#pragma unroll
-            for (int h = 0; h < kAttMaxHeads; ++h) ah[h] = h < H ? __shfl_sync(hm, al[h], qq, GL) : 0.f;
-            const float* zr = R.z + static_cast<std::size_t>(j) * G.ld;
-#pragma unroll
-            for (int u = 0; u < NU4; ++u) {
-              const int c = 4 * hl + 4 * GL * u;
-              zv[w][u] = (u < nu4 && c < G.ld) ? ld4(zr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-              aw[w][u] = pick(ah, hu[u]);
-            }
-          }
-#pragma unroll
-          for (int w = 0; w < EIF; ++w) {
-            if (q0 + w >= cnt) break;
-#pragma unroll
-            for (int u = 0; u < NU4; ++u) {
-              acc[u].x += aw[w][u] * zv[w][u].x;
-              acc[u].y += aw[w][u] * zv[w][u].y;
-              acc[u].z += aw[w][u] * zv[w][u].z;
-              acc[u].w += aw[w][u] * zv[w][u].w;
-            }
-          }
-        }
-      }
-    }
-    float* o = G.out + (static_cast<std::size_t>(i) * G.row_stride + G.row_offset) * G.ld;
-#pragma unroll
-    for (int u = 0; u < NU4; ++u) {
-      const int c = 4 * hl + 4 * GL * u;
-      if (u < nu4 && c < G.ld) {
-        float4 v = acc[u];
-        if (G.relu) {
-          v.x = fmaxf(v.x, 0.f);
-          v.y = fmaxf(v.y, 0.f);
-          v.z = fmaxf(v.z, 0.f);
-          v.w = fmaxf(v.w, 0.f);
-        }
-        *reinterpret_cast<float4*>(o + c) = v;
-      }
-    }
-  }
-}
-
-template <int GL, int NU4>
-__global__ void __launch_bounds__(256) k_att_edge_grad(AttBatch b, int total) {
-  pdl_enter();
-  constexpr int EIF = NU4 <= 2 ? 4 : 2;
-  const int lane = threadIdx.x & 31, hl = lane & (GL - 1);
-  const unsigned hm = group_mask<GL>(lane);
-  const int halves = gridDim.x * (blockDim.x / GL);
-  for (int item = blockIdx.x * (blockDim.x / GL) + (threadIdx.x / GL); item < total; item += halves) {
-    int g, i;
-    if (!group_row(b, item, g, i)) break;
-    const AttGroup& G = b.g[g];
-    if (i >= *G.n_rows) continue;
-    const int H = G.heads, F = G.cols / H, nu4 = (G.ld + 4 * GL - 1) / (4 * GL);
-    // one float4 per lane and heads of 4..64 columns: a head is an aligned group of F/4 lanes
-    const int gsz = F / 4;
-    const bool seg = NU4 == 1 && H > 1 && F % 4 == 0 && gsz <= GL && (gsz & (gsz - 1)) == 0;
-    int hu[NU4];
-    float4 dv[NU4];
-#pragma unroll
-    for (int u = 0; u < NU4; ++u) {
-      const int c = 4 * hl + 4 * GL * u;
-      hu[u] = c < G.cols ? c / F : -1;
-      dv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (u < nu4 && c < G.ld) {
-        const std::size_t at = (static_cast<std::size_t>(i) * G.row_stride + G.row_offset) * G.ld + c;
-        dv[u] = ld4(G.dout + at);
-        if (G.relu_h) {
-          const float4 hv = ld4(G.relu_h + at);
-          if (hv.x <= 0.f) dv[u].x = 0.f;
-          if (hv.y <= 0.f) dv[u].y = 0.f;
-          if (hv.z <= 0.f) dv[u].z = 0.f;
-          if (hv.w <= 0.f) dv[u].w = 0.f;
-        }
-      }
-    }
-    for (int q = 0; q < G.nrel; ++q) {
-      const AttRel& R = G.r[q];
-      const std::uint32_t lo = R.indptr[i], hi = R.indptr[i + 1];
-      if (lo == hi) continue;
-      // pass A: d alpha of every edge (a dot per head over the half-warp), kept in dt;
-      // c_h = sum_e alpha_e^h d alpha_e^h
-      float csum[kAttMaxHeads];
-#pragma unroll
-      for (int h = 0; h < kAttMaxHeads; ++h) csum[h] = 0.f;
-      for (std::uint32_t base = lo; base < hi; base += GL) {
-        const int cnt = static_cast<int>(min(static_cast<std::uint32_t>(GL), hi - base));
-        const std::uint32_t my_j = hl < cnt ? R.col[base + hl] : 0u;
-        float my_da[kAttMaxHeads];
-#pragma unroll
-        for (int h = 0; h < kAttMaxHeads; ++h) my_da[h] = 0.f;
-        for (int q0 = 0; q0 < cnt; q0 += EIF) {
-          float4 zv[EIF][NU4];
-#pragma unroll
-          for (int w = 0; w < EIF; ++w) {
-            const int qq = min(q0 + w, cnt - 1);
-            const std::uint32_t j = __shfl_sync(hm, my_j, qq, GL);
-            const float* zr = R.z + static_cast<std::size_t>(j) * G.ld;
-#pragma unroll
-            for (int u = 0; u < NU4; ++u) {
-              const int c = 4 * hl + 4 * GL * u;
-              zv[w][u] = (u < nu4 && c < G.ld) ? ld4(zr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-          }
-#pragma unroll
-          for (int w = 0; w < EIF; ++w) {
-            if (q0 + w >= cnt) break;
-            if (seg) {
-              float p = dot4(dv[0], zv[w][0]);
-              for (int o = gsz >> 1; o > 0; o >>= 1) p += __shfl_xor_sync(hm, p, o, GL);
-#pragma unroll
-              for (int h = 0; h < kAttMaxHeads; ++h) {
-                if (h >= H) break;
-                const float d = __shfl_sync(hm, p, h * gsz, GL);
-                if (hl == q0 + w) my_da[h] = d;
-              }
-            } else {
-#pragma unroll
-              for (int h = 0; h < kAttMaxHeads; ++h) {
-                if (h >= H) break;
-                float p = 0.f;
-#pragma unroll
-                for (int u = 0; u < NU4; ++u)
-                  if (hu[u] == h) p += dot4(dv[u], zv[w][u]);
-                p = gsum<GL>(p, hm);
-                if (hl == q0 + w) my_da[h] = p;
-              }
-            }
-          }
-        }
-        if (hl < cnt) {
-#pragma unroll
-          for (int h = 0; h < kAttMaxHeads; ++h) {
-            if (h >= H) break;
-            const std::size_t at = static_cast<std::size_t>(base + hl) * H + h;
-            R.dt[at] = my_da[h];
-            csum[h] += R.alpha[at] * my_da[h];
-          }
-        }
-      }
-#pragma unroll
-      for (int h = 0; h < kAttMaxHeads; ++h)
-        if (h < H) csum[h] = gsum<GL>(csum[h], hm);
-      __syncwarp(hm);
-      // pass B: dt = alpha (d alpha - c) LeakyReLU'(t)
-      for (std::uint32_t e = lo + hl; e < hi; e += GL) {
-        const std::uint32_t j = R.col[e];
-#pragma unroll
-        for (int h = 0; h < kAttMaxHeads; ++h) {
-          if (h >= H) break;
-          const std::size_t at = static_cast<std::size_t>(e) * H + h;
-          const float x = R.t[static_cast<std::size_t>(j) * H + h];
-          R.dt[at] = R.alpha[at] * (R.dt[at] - csum[h]) * (x > 0.f ? 1.f : kAttSlope);
-        }
-      }
-      __syncwarp(hm);
-    }
-  }
-}
-
-// t = a^(h) . z^(h) per (source row, head): one thread per pair for heads up to 32
-// columns, one half-warp per pair (float4 lanes) for wider heads
-__global__ void __launch_bounds__(256) k_att_scores(AttScoreBatch b) {
-  pdl_enter();
-  const AttScoreJob& J = b.j[blockIdx.y];
-  const int H = J.heads, F = J.cols / H;
-  const std::int64_t total = static_cast<std::int64_t>(*J.n_rows) * H;
-  if (F <= 32) {
-    for (std::int64_t x = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; x < total;
-         x += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-      const std::int64_t row = x / H;
-      const int h = static_cast<int>(x % H);
-      const float* zr = J.z + row * J.ld + h * F;
-      const float* a = J.a + h * F;
-      float p = 0.f;
-      if (F % 4 == 0) {
-        for (int c = 0; c < F; c += 4) p += dot4(ld4(zr + c), ld4(a + c));
-      } else {
-        for (int c = 0; c < F; ++c) p += zr[c] * a[c];
-      }
-      J.t[x] = p;
-    }
-    return;
-  }
-  const int hl = threadIdx.x & 15;
-  const unsigned hm = 0xFFFFu << (threadIdx.x & 16);
-  const std::int64_t halves = static_cast<std::int64_t>(gridDim.x) * (blockDim.x >> 4);
-  for (std::int64_t x = blockIdx.x * static_cast<std::int64_t>(blockDim.x >> 4) + (threadIdx.x >> 4); x < total;
-       x += halves) {
-    const std::int64_t row = x / H;
-    const int h = static_cast<int>(x % H);
-    const float* zr = J.z + row * J.ld + h * F;
-    const float* a = J.a + h * F;
-    float p = 0.f;
-    if (F % 4 == 0 || H == 1) {  // the row's padding columns are zero in z and a
-      for (int c = 4 * hl; c < F; c += 64) p += dot4(ld4(zr + c), ld4(a + c));
-    } else {
-      for (int c = hl; c < F; c += 16) p += zr[c] * a[c];
-    }
-    p = hsum(p, hm);
-    if (hl == 0) J.t[x] = p;
-  }
 }
 
 template <int GL, int NU4>
@@ -477,79 +175,6 @@ __global__ void __launch_bounds__(256) k_att_scatter(AttScatter s, int total) {
     if (cur >= 0) flush_block<GL, NU4>(s.b[cur], j, acc, ts, hl);
     for (int x = cur + 1; x < s.nb; ++x)
       if (s.b[x].type == t) flush_block<GL, NU4>(s.b[x], j, zacc, zero, hl);
-  }
-}
-
-// da partials: CTA = one chunk of kAttDaChunk rows of one job; 16 row groups x 16 float4
-// columns (16 independent rows in flight per thread), combined in a fixed order
-__global__ void __launch_bounds__(256) k_att_da_partial(AttDaBatch b) {
-  pdl_enter();
-  __shared__ float4 part[16][kAttMaxCols / 4];
-  const AttDaJob& J = b.j[blockIdx.y];
-  const int n = *J.n_rows;
-  const int r0 = blockIdx.x * kAttDaChunk;
-  if (r0 >= n) return;
-  const int F = J.cols / J.heads, nf4 = J.ld / 4;
-  const int cf = threadIdx.x & 15, rg = threadIdx.x >> 4;
-  for (int f = cf; f < nf4; f += 16) {
-    const int c = 4 * f;
-    const int h = c < J.cols ? c / F : 0;
-    float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 8
-    for (int k = 0; k < kAttDaChunk / 16; ++k) {
-      const int r = r0 + rg + 16 * k;
-      if (r < n) {
-        const float ts = J.tsum[static_cast<std::size_t>(r) * J.heads + h];
-        const float4 z = ld4(J.z + static_cast<std::size_t>(r) * J.ld + c);
-        p.x += ts * z.x;
-        p.y += ts * z.y;
-        p.z += ts * z.z;
-        p.w += ts * z.w;
-      }
-    }
-    part[rg][f] = p;
-  }
-  __syncthreads();
-  for (int f = threadIdx.x; f < nf4; f += blockDim.x) {
-    float4 s = part[0][f];
-    for (int g = 1; g < 16; ++g) {
-      s.x += part[g][f].x;
-      s.y += part[g][f].y;
-      s.z += part[g][f].z;
-      s.w += part[g][f].w;
-    }
-    *reinterpret_cast<float4*>(J.partial + static_cast<std::size_t>(blockIdx.x) * J.ld + 4 * f) = s;
-  }
-}
-
-__global__ void __launch_bounds__(256) k_att_da_reduce(AttDaBatch b) {
-  pdl_enter();
-  __shared__ float4 part[16][kAttMaxCols / 4];
-  const AttDaJob& J = b.j[blockIdx.x];
-  const int chunks = static_cast<int>(ceil_div(*J.n_rows, kAttDaChunk));
-  const int nf4 = J.ld / 4;
-  const int cf = threadIdx.x & 15, rg = threadIdx.x >> 4;
-  for (int f = cf; f < nf4; f += 16) {
-    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int k = rg; k < chunks; k += 16) {
-      const float4 v = ld4(J.partial + static_cast<std::size_t>(k) * J.ld + 4 * f);
-      s.x += v.x;
-      s.y += v.y;
-      s.z += v.z;
-      s.w += v.w;
-    }
-    part[rg][f] = s;
-  }
-  __syncthreads();
-  for (int f = threadIdx.x; f < nf4; f += blockDim.x) {
-    float4 s = part[0][f];
-    for (int g = 1; g < 16; ++g) {
-      s.x += part[g][f].x;
-      s.y += part[g][f].y;
-      s.z += part[g][f].z;
-      s.w += part[g][f].w;
-    }
-    *reinterpret_cast<float4*>(J.da + 4 * f) = s;
   }
 }
 
@@ -885,52 +510,6 @@ unsigned half_grid(std::uint64_t items) {
 
 }  // namespace
 
-void att_forward(const AttBatch& b, cudaStream_t st) {
-  int total = 0;
-  for (int g = 0; g < b.ng; ++g) {
-    if (b.g[g].ld > kAttMaxCols || b.g[g].heads > kAttMaxHeads || b.g[g].heads < 1 || b.g[g].cols % b.g[g].heads)
-      throw std::invalid_argument("attention layer shape not supported (cols <= 512, heads <= 8 dividing cols)");
-    total += b.g[g].rows_cap;
-  }
-  if (total == 0) return;
-  int ld = 1;
-  for (int g = 0; g < b.ng; ++g) ld = std::max(ld, b.g[g].ld);
-  const unsigned grid16 = half_grid(total), grid32 = warp_grid(total);
-  if (ld <= 64)
-    launch_pdl(k_att_forward<16, 1>, grid16, 256, 0, st, b, total);
-  else if (ld <= 128)
-    launch_pdl(k_att_forward<16, 2>, grid16, 256, 0, st, b, total);
-  else if (ld <= 256)
-    launch_pdl(k_att_forward<32, 2>, grid32, 256, 0, st, b, total);
-  else
-    launch_pdl(k_att_forward<32, 4>, grid32, 256, 0, st, b, total);
-}
-
-void att_edge_grad(const AttBatch& b, cudaStream_t st) {
-  int total = 0;
-  for (int g = 0; g < b.ng; ++g) total += b.g[g].rows_cap;
-  if (total == 0) return;
-  int ld = 1;
-  for (int g = 0; g < b.ng; ++g) ld = std::max(ld, b.g[g].ld);
-  const unsigned grid16 = half_grid(total), grid32 = warp_grid(total);
-  if (ld <= 64)
-    launch_pdl(k_att_edge_grad<16, 1>, grid16, 256, 0, st, b, total);
-  else if (ld <= 128)
-    launch_pdl(k_att_edge_grad<16, 2>, grid16, 256, 0, st, b, total);
-  else if (ld <= 256)
-    launch_pdl(k_att_edge_grad<32, 2>, grid32, 256, 0, st, b, total);
-  else
-    launch_pdl(k_att_edge_grad<32, 4>, grid32, 256, 0, st, b, total);
-}
-
-void att_scores(const AttScoreBatch& b, cudaStream_t st) {
-  if (b.n == 0) return;
-  std::uint64_t most = 1;
-  for (int q = 0; q < b.n; ++q) most = std::max<std::uint64_t>(most, static_cast<std::uint64_t>(b.j[q].rows_cap) * b.j[q].heads);
-  const unsigned gx = static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(most, 256), 8 * num_sms()));
-  launch_pdl(k_att_scores, dim3(gx, b.n), 256, 0, st, b);
-}
-
 void att_scatter(const AttScatter& s, cudaStream_t st) {
   int total = 0;
   for (int t = 0; t < s.nt; ++t) total += (s.src_cap[t] + 31) & ~31;
@@ -946,14 +525,6 @@ void att_scatter(const AttScatter& s, cudaStream_t st) {
     launch_pdl(k_att_scatter<32, 2>, grid32, 256, 0, st, s, total);
   else
     launch_pdl(k_att_scatter<32, 4>, grid32, 256, 0, st, s, total);
-}
-
-void att_da(const AttDaBatch& b, cudaStream_t st) {
-  if (b.n == 0) return;
-  int chunks = 1;
-  for (int q = 0; q < b.n; ++q) chunks = std::max(chunks, static_cast<int>(ceil_div(std::max(1, b.j[q].rows_cap), kAttDaChunk)));
-  launch_pdl(k_att_da_partial, dim3(chunks, b.n), 256, 0, st, b);
-  launch_pdl(k_att_da_reduce, dim3(b.n), 256, 0, st, b);
 }
 
 void transpose_slots(const TransposeBatch& b, cudaStream_t st) {

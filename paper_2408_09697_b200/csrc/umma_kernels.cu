@@ -414,7 +414,7 @@ void project_umma(ProjBatch& pb, cudaStream_t st) {
     for (int r = 0; r < G.nrel; ++r) {
       const ProjRel& R = G.r[r];
       CUtensorMap* M = &a.maps[map_index(kProject, g, r, 0)];
-      encode(M + 0, R.mean, R.ld_mean, G.rows_cap, R.ld_mean, 128, false);
+      encode(M + 0, R.mean, R.ld_mean, G.rows_cap, R.row_stride ? R.row_stride : R.ld_mean, 128, false);
       encode(M + 1, R.w, R.ld_w, R.din, R.ld_w, 32, true);
     }
   }
