@@ -304,3 +304,41 @@ def test_rgat_half_tables_match_oracle(H, ref, dtype):
     for (r, l), want in wg.items():
         assert_close(got[f"grad.w.r{r}.l{l}"], want, TOL, f"RGAT {dtype} grad.w.r{r}.l{l}")
         assert_close(got[f"grad.att.r{r}.l{l}"].ravel(), ag[(r, l)], TOL, f"RGAT {dtype} grad.att.r{r}.l{l}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k,heads", [(3, 4), (2, 1), (2, 8)])
+def test_rgat_depths_and_heads_match_oracle(H, ref, k, heads):
+    """Three layers (two aggregate-first inner layers over the previous layer's rows) and
+    the 1- and 8-head kernel instantiations against the f64 restatement."""
+    fanouts = [6, 5, 4][:k]
+    rg = ref.RefGraph.bundled("mag-mini", 5)
+    g = port.Graph(rg.export())
+    tree = port.bfs_metatree(g, k)
+    batch = list(range(0, 256, 4))
+    blocks = blocks_from(rg.sample_khop(batch, fanouts, RNG_SEED, port.hop_relation_sets(tree, k)), k, g.ntypes,
+                         g.nrels)
+    gd = H.gen_synthetic(H.bundled_spec("mag-mini"), 5)
+    eng = H.Engine(gd, fanouts, hidden=HIDDEN, batch_cap=len(batch), model_seed=77, learn_seed=88, model="rgat",
+                   heads=heads)
+    names = eng.tensor_names()
+    init = eng.read(*[n for n in names if n.startswith(("post.r", "att.", "post.learn.t"))])
+    weights = {(int(n.split(".")[1][1:]), int(n.split(".")[2][1:])): init[n] for n in init if n.startswith("post.r")}
+    att = {(int(n.split(".")[1][1:]), int(n.split(".")[2][1:])): init[n].ravel() for n in init if n.startswith("att.")}
+    learn = {int(n.split(".t")[-1]): init[n] for n in init if n.startswith("post.learn.t")}
+    loss, logits, Hw, dl, wg, ag, fg = R.step(g, tree, blocks, weights, att, learn, HIDDEN, heads, batch)
+    rep = eng.step(batch, RNG_SEED, 0, train=True)
+    got = eng.read(*[n for n in names if n.startswith(("H", "logits", "grad.w.", "grad.att."))])
+    assert abs(rep["loss"] - loss) <= TOL * abs(loss)
+    assert_close(got["logits"], logits, TOL, "logits")
+    flips = 0
+    for d in range(1, k):
+        for t in range(g.ntypes):
+            if t in Hw[d] and f"H{d}.t{t}" in got:
+                assert_close(got[f"H{d}.t{t}"], Hw[d][t], TOL, f"H{d}.t{t}")
+                flips += int(((got[f"H{d}.t{t}"] > 0) != (Hw[d][t] > 0)).sum())
+    if flips:
+        pytest.skip("ReLU tie flipped vs the f64 oracle; forward parity checked")
+    for (r, l), want in wg.items():
+        assert_close(got[f"grad.w.r{r}.l{l}"], want, TOL, f"grad.w.r{r}.l{l}")
+        assert_close(got[f"grad.att.r{r}.l{l}"].ravel(), ag[(r, l)], TOL, f"grad.att.r{r}.l{l}")
