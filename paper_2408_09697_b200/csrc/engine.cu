@@ -1014,7 +1014,8 @@ void Engine::run_sampling(cudaStream_t ss) {
     launch_pdl(k_alg_bytes, 1, 32, 0, ss, ab, alg_bytes_);
   }
   // cache lookups + updates over the layer-0 frontier (harness.cpp:425-437)
-  if (cache_on_ && !presampling_)
+  // (p > 1: over the union of every partition's frontier, run_agg_all)
+  if (cache_on_ && !presampling_ && o_.p == 1)
     for (int t = 0; t < ntypes_; ++t)
       if (cache_types_[t] && front(k, t).cap > 0)
         cache_count(front(k, t).list, front(k, t).count, front(k, t).cap, cached_bits_ + word_base_[t],
@@ -1115,6 +1116,21 @@ void Engine::run_agg_all() {
                           comm_, st_) != ncclSuccess)
           throw std::runtime_error("ncclAllReduce failed");
       });
+      // cache lookups over the global layer-0 frontier (harness.cpp:425-437 samples the
+      // whole batch): the union of every partition's frontier, identical on every rank
+      if (cache_on_) {
+        timed("cache_union", 0, [&] {
+          for (int t = 0; t < ntypes_; ++t) {
+            if (!cache_types_[t]) continue;
+            HG_CUDA(cudaMemsetAsync(union_map_[t], 0, type_counts_[t], st_));
+            if (front(k, t).cap > 0) union_mark(front(k, t).list, front(k, t).count, front(k, t).cap, union_map_[t], st_);
+            if (ncclAllReduce(union_map_[t], union_map_[t], type_counts_[t], ncclUint8, ncclMax, comm_, st_) !=
+                ncclSuccess)
+              throw std::runtime_error("ncclAllReduce (cache frontier union) failed");
+            union_count(union_map_[t], type_counts_[t], cached_bits_ + word_base_[t], cache_hm_ + 2 * t, st_);
+          }
+        });
+      }
     }
 #endif
   }
@@ -1849,6 +1865,12 @@ void Engine::set_cache(const std::vector<std::vector<NodeId>>& cached) {
   HG_CUDA(cudaStreamSynchronize(st_));
   cache_on_ = true;
   for (int t = 0; t < ntypes_; ++t) cache_types_[t] = t < static_cast<int>(cached.size());
+  if (o_.p > 1) {  // the global frontier's union maps (every rank lists the same types)
+    union_map_.resize(ntypes_, nullptr);
+    for (int t = 0; t < ntypes_; ++t)
+      if (cache_types_[t] && !union_map_[t])
+        union_map_[t] = static_cast<std::uint8_t*>(alloc(std::max<std::uint64_t>(1, type_counts_[t])));
+  }
   // host-resident feature tables: copy the cached rows into HBM and map every node to
   // its cache row (or -1: read over PCIe from the pinned table)
   for (int t = 0; t < ntypes_ && t < static_cast<int>(cached.size()); ++t) {

@@ -487,6 +487,7 @@ class Engine {
 
   bool cache_on_ = false;
   std::vector<bool> cache_types_;
+  std::vector<std::uint8_t*> union_map_;  // p > 1: per cached type, the global frontier's 0/1 map
   bool profiling_ = false;
   struct PendingEvent {
     std::string name;

@@ -778,6 +778,46 @@ void cache_count(const std::uint32_t* ids, const int* n, int cap, const std::uin
   launch_pdl(k_cache_count, std::max(grid, 1u), 256, 0, st, ids, n, cached_bits, hm);
 }
 
+namespace {
+__global__ void k_union_mark(const std::uint32_t* ids, const int* n, std::uint8_t* map) {
+  pdl_enter();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < *n; i += gridDim.x * blockDim.x) map[ids[i]] = 1;
+}
+__global__ void k_union_count(const std::uint8_t* map, std::uint64_t n, const std::uint32_t* cached,
+                              unsigned long long* hm) {
+  pdl_enter();
+  unsigned long long hit = 0, miss = 0;
+  for (std::uint64_t v = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; v < n;
+       v += static_cast<std::uint64_t>(gridDim.x) * blockDim.x)
+    if (map[v]) {
+      if ((cached[v >> 5] >> (v & 31)) & 1u)
+        ++hit;
+      else
+        ++miss;
+    }
+  for (int o = 16; o > 0; o >>= 1) {
+    hit += __shfl_down_sync(0xffffffffu, hit, o);
+    miss += __shfl_down_sync(0xffffffffu, miss, o);
+  }
+  if ((threadIdx.x & 31) == 0 && (hit | miss)) {
+    atomicAdd(hm, hit);
+    atomicAdd(hm + 1, miss);
+  }
+}
+}  // namespace
+
+void union_mark(const std::uint32_t* ids, const int* n, int cap, std::uint8_t* map, cudaStream_t st) {
+  const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(std::max(1, cap), 256), 2 * num_sms()));
+  launch_pdl(k_union_mark, std::max(grid, 1u), 256, 0, st, ids, n, map);
+}
+
+void union_count(const std::uint8_t* map, std::uint64_t n, const std::uint32_t* cached_bits, unsigned long long* hm,
+                 cudaStream_t st) {
+  const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(std::max<std::uint64_t>(1, n), 256),
+                                                                      4 * num_sms()));
+  launch_pdl(k_union_count, std::max(grid, 1u), 256, 0, st, map, n, cached_bits, hm);
+}
+
 void hotness_add(const std::uint32_t* ids, const std::uint32_t* indptr, const int* n_rows, int cap,
                  unsigned long long* counts, cudaStream_t st) {
   const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(cap, 256), 4 * num_sms()));

@@ -300,6 +300,11 @@ void zero_rows(float* p, int ld, const int* n_rows, int rows_cap, cudaStream_t s
 // cache lookups: hits of frontier ids against a cached-id bitmap, accumulated
 void cache_count(const std::uint32_t* ids, const int* n, int cap, const std::uint32_t* cached_bits,
                  unsigned long long* hits_misses, cudaStream_t st);
+// p > 1: the global layer-0 frontier of a type as the union of every partition's (a 0/1
+// byte per node, OR-ed across ranks with an ncclMax all-reduce), then its cache lookups
+void union_mark(const std::uint32_t* ids, const int* n, int cap, std::uint8_t* map, cudaStream_t st);
+void union_count(const std::uint8_t* map, std::uint64_t n, const std::uint32_t* cached_bits, unsigned long long* hm,
+                 cudaStream_t st);
 // histogram for presample_hotness
 void hotness_add(const std::uint32_t* ids, const std::uint32_t* indptr, const int* n_rows, int cap,
                  unsigned long long* counts, cudaStream_t st);

@@ -61,6 +61,14 @@ def main():
             raise RuntimeError("missing replica handles")
         time.sleep(0.05)
     eng.attach_replicas([open(f"{id_path}.h{r}", "rb").read() for r in range(p)])
+    budget = int(os.environ.get("HG_CACHE_BUDGET", "0"))
+    if budget:  # run_experiment's cache (harness.cpp:373-437): plan from a whole-graph presample
+        pe = H.Engine.for_experiment(g, [25, 20], 32, seed, batch_cap=512, device=rank)
+        hot = pe.presample_hotness(2, H.mix_seed(seed, 0xCA11E), 512)
+        del pe
+        n_types = len(g.export()["node_counts"])
+        cplan = H.cache_plan(g, hot, n_types, budget)
+        eng.set_cache([cplan[f"cached.t{t}"] for t in range(n_types)])
     batches = H.make_batches(g, bsz, n_batches, H.mix_seed(seed, 0xBA7C))
     losses, active, sync, lead, bound_ok, target_ok = [], [], [], [], [], []
     for i, b in enumerate(batches):
@@ -81,7 +89,9 @@ def main():
              sync=np.asarray(sync, np.uint64), lead=np.asarray(lead), bound_ok=np.asarray(bound_ok),
              target_ok=np.asarray(target_ok), boundary=np.asarray(boundary[0], np.uint64),
              cut_edges=np.asarray([boundary[1]], np.uint64),
-             **{"T:" + k: v for k, v in post.items()}, **{"G:" + k: v for k, v in g0.items()})
+             **{"T:" + k: v for k, v in post.items()}, **{"G:" + k: v for k, v in g0.items()},
+             **({"C:" + k: v for k, v in eng.cache_counters().items()} if budget else {}),
+             **({"C:transfer_ns": cplan["profile.transfer_ns"]} if budget else {}))
 
 
 if __name__ == "__main__":

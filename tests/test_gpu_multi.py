@@ -153,3 +153,38 @@ def test_work_aware_plan_matches_flat_reference(ref, name, p):
             elif n.startswith("post.learn.t"):
                 assert_adam_close(v, want["final.learn.t" + n.split(".t")[-1]], None, max_flip_frac=1e-2,
                                   steps=n_batches, what=f"rank {r}: {n}")
+
+
+@pytest.mark.parametrize("p", [2, 4])
+def test_cache_counters_over_the_global_frontier(ref, p):
+    """run_experiment's cache accounting at p > 1 looks up the whole batch's layer-0
+    frontier (harness.cpp:425-437): every rank counts the union of the partitions'
+    frontiers (an ncclMax all-reduce of 0/1 maps), equal to the reference's hits and misses."""
+    if n_gpus() < p:
+        pytest.skip(f"needs {p} GPUs")
+    seed, n_batches, bsz, budget = 5, 4, 64, 1 << 18
+    with tempfile.TemporaryDirectory() as td:
+        idp = os.path.join(td, "nccl.id")
+        procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "mp", "raf_rank.py"), "mag-mini", str(seed), str(p),
+                                   str(r), idp, os.path.join(td, f"r{r}.npz"), str(n_batches), str(bsz)],
+                                  stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True,
+                                  env=dict(os.environ, HG_CACHE_BUDGET=str(budget))) for r in range(p)]
+        outs = [pr.communicate(timeout=300)[0] for pr in procs]
+        for pr, o in zip(procs, outs):
+            assert pr.returncode == 0, o[-3000:]
+        res = [np.load(os.path.join(td, f"r{r}.npz")) for r in range(p)]
+    from paper_2408_09697_b200 import hetsim as H
+    cfg = {"spec": "mag-mini", "partitioner": "meta", "p": p, "engine": "raf", "fanouts": [25, 20], "hidden": 32,
+           "batch_size": bsz, "epochs": 1, "max_batches_per_epoch": n_batches, "seed": seed, "cache_budget": budget}
+    stats, _, ok = ref.run_experiment(cfg)
+    assert ok
+    np.testing.assert_allclose(res[0]["losses"], [b["loss"] for b in stats["batches"]], rtol=1e-3, atol=0)
+    e = H.gen_synthetic(H.bundled_spec("mag-mini"), seed).export()
+    names = [t["name"] for t in H.bundled_spec("mag-mini")["node_types"]]
+    for r in range(p):
+        counters = {k[2:]: res[r][k] for k in res[r].files if k.startswith("C:cache.")}
+        assert counters, "no cache counters"
+        mine = {s["type"]: s for s in H.cache_stats(counters, e["kinds"], res[r]["C:transfer_ns"])}
+        for want in stats["cache"]["per_type"]:
+            got = mine[names.index(want["type"])]
+            assert (got["hits"], got["misses"]) == (want["hits"], want["misses"]), (r, want["type"], got, want)
