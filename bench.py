@@ -240,7 +240,9 @@ def run_b200(args):
 
     t0 = time.time()
     c5 = args.workload == "c5"
-    spec = H.igb_het_spec(args.scale) if c5 else H.ogbn_mag_spec()
+    c4 = args.workload == "c4"
+    spec = H.igb_het_spec(args.scale) if c5 else H.mag240m_spec(args.scale) if c4 else H.ogbn_mag_spec()
+    fanouts = [25, 15, 10] if c4 else FANOUTS  # C4: 3 layers (BASELINE configs[3])
     g = H.gen_synthetic(spec, SEED)
     t_gen = time.time() - t0
     dbg("graph generated")
@@ -248,18 +250,18 @@ def run_b200(args):
     if n > 1 and args.plan == "work":
         # work-aware plan (not the reference's policy; same numbers): per sub-metatree the
         # sampled edges and learnable leaf rows of 4 batches, measured on this GPU
-        sw = H.sub_work(g, FANOUTS, 4, BATCH_PER_GPU, SEED, device=local)
+        sw = H.sub_work(g, fanouts, 4, BATCH_PER_GPU, SEED, device=local)
         plan_kw = {"sub_work": np.concatenate([sw["work"], sw["learn_rows"]])}
-        parts = H.meta_partition_work_aware(g, len(FANOUTS), n, plan_kw["sub_work"])
+        parts = H.meta_partition_work_aware(g, len(fanouts), n, plan_kw["sub_work"])
         plan_desc = "work-aware (sub-metatree groups " + " | ".join(
             ",".join(str(int(x)) for x in parts[f"part{i}.sub_ids"]) for i in range(n)) + ")"
     rgat = args.model == "rgat"
     if rgat:  # C3 (BASELINE configs[2]): the RGAT layer type, 4 heads, same graph and batches
         plan_kw["model"] = "rgat"
         plan_kw["heads"] = 4
-    if c5:  # C5 (BASELINE configs[4]) shape: 1024-d dense features on every type, stored fp16
+    if c5 or c4:  # C5 / C4 shapes: 1024-d / 768-d dense features, stored fp16
         plan_kw["feat_dtype"] = "f16"
-    eng = H.Engine.for_experiment(g, FANOUTS, HIDDEN, SEED, batch_cap=batch, p=n, rank=rank, device=local, **plan_kw)
+    eng = H.Engine.for_experiment(g, fanouts, HIDDEN, SEED, batch_cap=batch, p=n, rank=rank, device=local, **plan_kw)
     if world > 1:
         import torch.distributed as dist
         uid = [H.nccl_unique_id() if rank == 0 else None]
@@ -418,7 +420,9 @@ def run_b200(args):
         "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": n, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": (f"C5 IGB-HET-shape x{args.scale:g} (BASELINE configs[4]; 1024-d fp16 features on all 4 "
+        "config": {"workload": (f"C4 MAG240M-shape x{args.scale:g} (BASELINE configs[3]; 768-d fp16 paper features) "
+                                f"3-layer {args.model.upper()} hidden 64, fanout [25,15,10]" if c4 else
+                                f"C5 IGB-HET-shape x{args.scale:g} (BASELINE configs[4]; 1024-d fp16 features on all 4 "
                                 f"types, 7 relations) 2-layer {args.model.upper()} hidden 64, fanout [25,20] (the HGT-style "
                                 "aggregator is not built: RGCN)" if c5 else
                                 "C3 ogbn-mag-shape (BASELINE configs[2]) 2-layer RGAT 4 heads hidden 64, fanout [25,20]"
@@ -466,9 +470,9 @@ def run_b200(args):
     if rgat:
         line["parity"] = {"checked_in": "tests/test_rgat.py (f64 restatement oracle/rgat.py; C3 step, p = 2, 4)"}
         line["cpu_baseline"] = None  # the reference has no attention layer
-    elif c5:
-        line["parity"] = {"checked_in": "tests/test_c4_parity.py (half-precision tables), test_gpu_numerics.py"}
-        line["cpu_baseline"] = None  # C5's reference arm would be the RGCN stand-in, not HGT
+    elif c5 or c4:
+        line["parity"] = {"checked_in": "tests/test_c4_parity.py (the C4 twin, half-precision tables)"}
+        line["cpu_baseline"] = None  # bounded CPU samples are taken on the headline workload (C2)
     elif not args.no_cpu_baseline and n == 1:
         # bounded sample: 8 batches per host thread (~10-20 s of CPU work)
         threads = os.cpu_count() or 1
@@ -497,9 +501,10 @@ def main():
                          "(RGAT default: the work-aware cost model is calibrated on RGCN's per-edge work; "
                          "measured on C3 at p = 4: reference 1.45 G vs work-aware 1.12 G sampled-edges/s)")
     ap.add_argument("--warmup-ref", type=int, default=0)
-    ap.add_argument("--workload", default="c2", choices=["c2", "c5"],
-                    help="c2: the headline ogbn-mag shape; c5: the IGB-HET shape (1024-d fp16 features, --scale)")
-    ap.add_argument("--scale", type=float, default=0.05, help="c5: fraction of IGB-HET's counts")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c4", "c5"],
+                    help="c2: the headline ogbn-mag shape; c4: the MAG240M shape (3 layers, 768-d fp16, --scale); "
+                         "c5: the IGB-HET shape (1024-d fp16 features, --scale)")
+    ap.add_argument("--scale", type=float, default=0.05, help="c4 / c5: fraction of the dataset's counts")
     ap.add_argument("--model", default="rgcn", choices=["rgcn", "rgat"],
                     help="rgcn: the headline C2 workload; rgat: C3 (the RGAT layer type, 4 heads)")
     args = ap.parse_args()

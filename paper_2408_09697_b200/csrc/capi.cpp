@@ -82,7 +82,9 @@ Plan work_aware_plan(const Graph& g, int k, int p, const double* work, int n_wor
   const int n_subs = static_cast<int>(meta_partition(sch, g.target, k, 1).subs.size());
   std::vector<double> w(work, work + std::min(n_work, n_subs)), l;
   if (n_work == 2 * n_subs) l.assign(work + n_subs, work + n_work);
-  return work_aware_partition(sch, g.target, k, p, w, l);
+  std::vector<bool> learnable(g.num_types());
+  for (int t = 0; t < g.num_types(); ++t) learnable[t] = g.types[t].storage == Storage::Learnable;
+  return work_aware_partition(sch, g.target, k, p, w, l, 6.0, learnable);
 }
 
 EngineOptions engine_options(const hg_engine_opts& o) {

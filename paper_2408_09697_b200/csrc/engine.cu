@@ -283,7 +283,9 @@ void Engine::build_plan(const Graph& g) {
       const std::size_t n_subs = meta_partition(sch, target_, k, 1).subs.size();
       std::vector<double> w(o_.sub_work.begin(), o_.sub_work.begin() + std::min(n_subs, o_.sub_work.size())), l;
       if (o_.sub_work.size() == 2 * n_subs) l.assign(o_.sub_work.begin() + n_subs, o_.sub_work.end());
-      plan = work_aware_partition(sch, target_, k, o_.p, w, l);
+      std::vector<bool> learnable(g.num_types());
+      for (int t = 0; t < g.num_types(); ++t) learnable[t] = g.types[t].storage == Storage::Learnable;
+      plan = work_aware_partition(sch, target_, k, o_.p, w, l, 6.0, learnable);
     }
     acct_ = plan_accounting(g, plan);  // run_experiment's view: raf_view_from_plan
     const Part& part = plan.parts.at(o_.rank);

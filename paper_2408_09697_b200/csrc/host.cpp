@@ -10,6 +10,7 @@
 #include <exception>
 #include <functional>
 #include <memory>
+#include <map>
 #include <set>
 #include <thread>
 
@@ -580,7 +581,8 @@ Plan meta_partition(const Schema& s, int root, int k, int p) {
 // partition of the subs and every split of p over its blocks is scored (the bundled
 // schemas' metatrees have <= 6 subs); ties go to fewer groups.
 Plan work_aware_partition(const Schema& s, int root, int k, int p, const std::vector<double>& work,
-                          const std::vector<double>& learn_rows, double merge_cost) {
+                          const std::vector<double>& learn_rows, double merge_cost,
+                          const std::vector<bool>& learnable_types) {
   Plan plan;
   plan.p = p;
   plan.tree = bfs_tree(s, root, k);
@@ -591,6 +593,36 @@ Plan work_aware_partition(const Schema& s, int root, int k, int p, const std::ve
     throw std::invalid_argument("work-aware plan: one work value per sub-metatree expected (" + std::to_string(n) + ")");
   if (n > 8) throw std::invalid_argument("work-aware plan: more than 8 sub-metatrees");
   if (p < 1) throw std::invalid_argument("p must be >= 1");
+  // what each sub-metatree trains: its weight slots (rel, layer) and learnable leaf types.
+  // Groups must not share either (the engine exchanges gradients only inside a replica
+  // group), which deep metatrees (a relation at several depths: MAG240M at k = 3) make
+  // binding; the single all-subs group (data parallel) is always feasible.
+  std::vector<std::set<std::pair<int, int>>> sub_slots(n);
+  std::vector<std::set<int>> sub_leaves(n);
+  for (int sid = 0; sid < n; ++sid)
+    for (std::size_t q = 1; q < plan.tree.pos.size(); ++q) {
+      if (plan.tree.root_child_ancestor(static_cast<int>(q)) != plan.subs[sid].child_pos) continue;
+      const TreePos& tp = plan.tree.pos[q];
+      sub_slots[sid].insert({tp.rel, k - tp.depth + 1});
+      if (tp.depth == k && tp.type < static_cast<int>(learnable_types.size()) && learnable_types[tp.type])
+        sub_leaves[sid].insert(tp.type);
+    }
+  auto feasible = [&](const std::vector<std::vector<int>>& groups) {
+    std::map<std::pair<int, int>, int> slot_owner;
+    std::map<int, int> leaf_owner;
+    for (int g = 0; g < static_cast<int>(groups.size()); ++g)
+      for (int sid : groups[g]) {
+        for (const auto& key : sub_slots[sid]) {
+          auto it = slot_owner.emplace(key, g).first;
+          if (it->second != g) return false;
+        }
+        for (int t : sub_leaves[sid]) {
+          auto it = leaf_owner.emplace(t, g).first;
+          if (it->second != g) return false;
+        }
+      }
+    return true;
+  };
   double best = -1.0;
   std::vector<std::vector<int>> best_groups;
   std::vector<int> best_r;
@@ -605,6 +637,7 @@ Plan work_aware_partition(const Schema& s, int root, int k, int p, const std::ve
         w[label[q]] += work[q];
         m[label[q]] += learn_rows.empty() ? 0.0 : merge_cost * learn_rows[q];
       }
+      if (!feasible(groups)) return;
       auto cost = [&](int g, int r) { return w[g] / r + (r > 1 ? m[g] : 0.0); };
       // every extra worker goes to the group whose cost it lowers the most, while any does
       std::vector<int> r(ng, 1);

@@ -197,7 +197,8 @@ Plan meta_partition(const Schema& s, int root, int k, int p);
 // work-aware alternative (not the reference policy): groups of workers replicate sets of
 // sub-metatrees, minimising the busiest worker's share of `work` (one value per sub)
 Plan work_aware_partition(const Schema& s, int root, int k, int p, const std::vector<double>& work,
-                          const std::vector<double>& learn_rows = {}, double merge_cost = 6.0);
+                          const std::vector<double>& learn_rows = {}, double merge_cost = 6.0,
+                          const std::vector<bool>& learnable_types = {});
 std::vector<int> cacheable_types(const Plan& plan, int part);
 
 // hop_relation_sets (hgnn.cpp:28-37): allowed relations per hop, ascending.

@@ -12,6 +12,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 
 
+# fanouts (HG_FANOUTS="25,15,10": a three-layer model)
+FANOUTS = [int(x) for x in os.environ.get("HG_FANOUTS", "25,20").split(",")]
+
+
 def main():
     name, seed, p, rank, id_path, out_path, n_batches, bsz = sys.argv[1:9]
     seed, p, rank, n_batches, bsz = int(seed), int(p), int(rank), int(n_batches), int(bsz)
@@ -26,11 +30,11 @@ def main():
     kw = {}
     if os.environ.get("HG_PLAN_WORK", "0") != "0":  # the work-aware plan (not the reference's)
         import numpy as _np
-        sw = H.sub_work(g, [25, 20], 4, bsz, seed, device=rank)
+        sw = H.sub_work(g, FANOUTS, 4, bsz, seed, device=rank)
         kw["sub_work"] = _np.concatenate([sw["work"], sw["learn_rows"]])
     if os.environ.get("HG_MODEL", "rgcn") != "rgcn":  # the RGAT layer type (tests/test_rgat.py)
         kw["model"] = os.environ["HG_MODEL"]
-    eng = H.Engine.for_experiment(g, [25, 20], 32, seed, batch_cap=bsz, p=p, rank=rank, device=rank, **kw)
+    eng = H.Engine.for_experiment(g, FANOUTS, 32, seed, batch_cap=bsz, p=p, rank=rank, device=rank, **kw)
     if rank == 0:
         uid = H.nccl_unique_id()
         with open(id_path + ".tmp", "wb") as f:
@@ -63,7 +67,7 @@ def main():
     eng.attach_replicas([open(f"{id_path}.h{r}", "rb").read() for r in range(p)])
     budget = int(os.environ.get("HG_CACHE_BUDGET", "0"))
     if budget:  # run_experiment's cache (harness.cpp:373-437): plan from a whole-graph presample
-        pe = H.Engine.for_experiment(g, [25, 20], 32, seed, batch_cap=512, device=rank)
+        pe = H.Engine.for_experiment(g, FANOUTS, 32, seed, batch_cap=512, device=rank)
         hot = pe.presample_hotness(2, H.mix_seed(seed, 0xCA11E), 512)
         del pe
         n_types = len(g.export()["node_counts"])

@@ -188,3 +188,41 @@ def test_cache_counters_over_the_global_frontier(ref, p):
         for want in stats["cache"]["per_type"]:
             got = mine[names.index(want["type"])]
             assert (got["hits"], got["misses"]) == (want["hits"], want["misses"]), (r, want["type"], got, want)
+
+
+@pytest.mark.parametrize("p", [2, 4])
+def test_three_layer_work_aware_plan_matches_flat_reference(ref, p):
+    """A deep metatree (the C4 MAG240M schema at k = 3: relations recur at several depths):
+    the work-aware planner only forms groups that share no weight slot or learnable leaf
+    type, here the all-subs group replicated p times (data parallel with the replica
+    merge); losses and the trained model match the reference's flat RAF run."""
+    if n_gpus() < p:
+        pytest.skip(f"needs {p} GPUs")
+    import json
+    from paper_2408_09697_b200 import hetsim as H
+    seed, n_batches, bsz = 5, 4, 64
+    spec = H.mag240m_spec(0.0005)
+    with tempfile.TemporaryDirectory() as td:
+        arg = "spec:" + os.path.join(td, "spec.json")
+        with open(arg[len("spec:"):], "w") as f:
+            json.dump(spec, f)
+        idp = os.path.join(td, "nccl.id")
+        procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "mp", "raf_rank.py"), arg, str(seed), str(p),
+                                   str(r), idp, os.path.join(td, f"r{r}.npz"), str(n_batches), str(bsz)],
+                                  stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True,
+                                  env=dict(os.environ, HG_PLAN_WORK="1", HG_FANOUTS="25,15,10")) for r in range(p)]
+        outs = [pr.communicate(timeout=300)[0] for pr in procs]
+        for pr, o in zip(procs, outs):
+            assert pr.returncode == 0, o[-3000:]
+        res = [np.load(os.path.join(td, f"r{r}.npz")) for r in range(p)]
+    g = H.gen_synthetic(spec, seed)
+    batches = H.make_batches(g, bsz, n_batches, H.mix_seed(seed, 0xBA7C))
+    want = ref.RefGraph.from_spec(spec, seed).raf_train(3, 32, 1, seed, [list(b) for b in batches], [25, 15, 10])
+    from tests.util import assert_adam_close
+    for r in range(p):
+        np.testing.assert_allclose(res[r]["losses"], want["losses"], rtol=1e-3, atol=0)
+        for key in res[r].files:
+            if key.startswith("T:post.r"):
+                n = key[len("T:post."):]
+                assert_adam_close(res[r][key], want["final." + n], None, steps=n_batches, max_flip_frac=1e-2,
+                                  what=f"p={p} rank {r}: {n}")
