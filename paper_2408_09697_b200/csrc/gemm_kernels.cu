@@ -258,9 +258,12 @@ __device__ __forceinline__ float4 load_row4(const MeanBlock& B, std::uint32_t ke
   return __ldg(reinterpret_cast<const float4*>(base + row * B.ld_h + c));
 }
 
+#ifndef HG_WIDE_NOALLOC
+#define HG_WIDE_NOALLOC 0
+#endif
 // 8 consecutive features of a half-precision row (one 16-byte load)
 template <bool CACHED>
-__device__ __forceinline__ void load_row8(const MeanBlock& B, std::uint32_t key, int c, float4& a, float4& b) {
+__device__ __forceinline__ uint4 load_row8(const MeanBlock& B, std::uint32_t key, int c) {
   const void* base = B.h;
   std::size_t row = key;
   if (CACHED && B.slot) {
@@ -271,15 +274,34 @@ __device__ __forceinline__ void load_row8(const MeanBlock& B, std::uint32_t key,
     }
   }
   // (the L2 256-byte hint of the fp32 rows measured slower here: 394 -> 410 us/step on C5)
-  const uint4 raw = __ldg(reinterpret_cast<const uint4*>(static_cast<const std::uint16_t*>(base) + row * B.ld_h + c));
+  const std::uint16_t* p = static_cast<const std::uint16_t*>(base) + row * B.ld_h + c;
+#if HG_WIDE_NOALLOC
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+#else
+  return __ldg(reinterpret_cast<const uint4*>(p));
+#endif
+}
+
+// 8 half features (one raw 16-byte row chunk) added into s (features 0-3) and s2 (4-7)
+__device__ __forceinline__ void add_row8(const uint4& raw, int h_dtype, float4& s, float4& s2) {
   float2 f[4];
   const std::uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
   for (int j = 0; j < 4; ++j)
-    f[j] = B.h_dtype == kF16 ? __half22float2(*reinterpret_cast<const __half2*>(&w[j]))
-                             : __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[j]));
-  a = make_float4(f[0].x, f[0].y, f[1].x, f[1].y);
-  b = make_float4(f[2].x, f[2].y, f[3].x, f[3].y);
+    f[j] = h_dtype == kF16 ? __half22float2(*reinterpret_cast<const __half2*>(&w[j]))
+                           : __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[j]));
+  s.x += f[0].x;
+  s.y += f[0].y;
+  s.z += f[1].x;
+  s.w += f[1].y;
+  s2.x += f[2].x;
+  s2.y += f[2].y;
+  s2.z += f[3].x;
+  s2.w += f[3].y;
 }
 
 __device__ __forceinline__ void add4(float4& s, const float4& v) {
@@ -299,8 +321,11 @@ __host__ __device__ inline int gather_chunk(int h_dtype) { return h_dtype == kF3
 // fp32-only batches (WIDE = false) run the 64-column items with one float4 per neighbour.
 // NB: neighbour rows in flight per lane (kGatherBatch; launches too small to fill the GPU
 // — the top layer's 1024 rows — take more per trip so their few round trips finish sooner)
+#ifndef HG_GATHER_WIDE_MINB
+#define HG_GATHER_WIDE_MINB 5
+#endif
 template <bool WIDE, bool CACHED, int NB>
-__global__ void __launch_bounds__(256, WIDE || NB > kGatherBatch ? 4 : 8) k_gather_mean(MeanBatch m) {
+__global__ void __launch_bounds__(256, WIDE ? HG_GATHER_WIDE_MINB : NB > kGatherBatch ? 4 : 8) k_gather_mean(MeanBatch m) {
   pdl_enter();
   const int hl = threadIdx.x & 15;
   const int halves = gridDim.x * (blockDim.x >> 4);
@@ -374,17 +399,13 @@ __global__ void __launch_bounds__(256, WIDE || NB > kGatherBatch ? 4 : 8) k_gath
 #pragma unroll
           for (int q = 0; q < NB; ++q) add4(s, v[q]);
         } else {
-          float4 v[NB], w[NB];
+          // raw 16-byte chunks in flight (4 registers per neighbour), converted after
+          // the round trip: the register budget holds HG_GATHER_WIDE_MINB CTAs per SM
+          uint4 v[NB];
 #pragma unroll
-          for (int q = 0; q < NB; ++q) {
-            v[q] = w[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (q < cnt) load_row8<CACHED>(B, kk[q], c, v[q], w[q]);
-          }
+          for (int q = 0; q < NB; ++q) v[q] = q < cnt ? load_row8<CACHED>(B, kk[q], c) : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-          for (int q = 0; q < NB; ++q) {
-            add4(s, v[q]);
-            add4(s2, w[q]);
-          }
+          for (int q = 0; q < NB; ++q) add_row8(v[q], B.h_dtype, s, s2);
         }
       }
       const float inv = hi > lo ? 1.0f / static_cast<float>(hi - lo) : 0.f;
