@@ -260,6 +260,29 @@ __global__ void __launch_bounds__(kSortThreads) k_csc_sort(CscHop h) {
       hi = t.offs[c];
     }
     const bool is_long = hi - lo > kShortSeg;
+    // the warp's sources are consecutive, so their segments are one contiguous span:
+    // when it fits the warp's shared buffer, stage it with coalesced loads, sort every
+    // lane's segment there and store it back (no dependent global round trips)
+    const std::uint32_t wlo = base ? t.offs[base - 1] : 0u;
+    const std::uint32_t whi = t.offs[min(base + 31, n - 1)];
+    if (!__any_sync(0xffffffffu, is_long) && whi - wlo <= static_cast<std::uint32_t>(kWarpSort)) {
+      for (std::uint32_t x = wlo + lane; x < whi; x += 32) wsm[x - wlo] = t.entries[x];
+      __syncwarp();
+      std::uint32_t* seg = wsm + (hi > lo ? lo - wlo : 0u);
+      for (std::uint32_t x = 1; x < hi - lo; ++x) {
+        const std::uint32_t v = seg[x];
+        std::uint32_t y = x;
+        while (y > 0 && seg[y - 1] > v) {
+          seg[y] = seg[y - 1];
+          --y;
+        }
+        seg[y] = v;
+      }
+      __syncwarp();
+      for (std::uint32_t x = wlo + lane; x < whi; x += 32) t.entries[x] = wsm[x - wlo];
+      __syncwarp();
+      continue;
+    }
     if (!is_long) {
       for (std::uint32_t x = lo + 1; x < hi; ++x) {
         const std::uint32_t v = t.entries[x];
