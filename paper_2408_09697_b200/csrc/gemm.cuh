@@ -89,9 +89,6 @@ struct MeanBatch {
   int nb;
 };
 void gather_mean(MeanBatch& m, cudaStream_t st);
-// the bulk-copy gather (gather_bulk.cu) for HBM tables with rows of <= 4 KB; false when
-// the batch does not qualify (host-resident tables) or HG_GATHER_BULK=0
-bool gather_mean_bulk(MeanBatch& m, cudaStream_t st);
 
 struct ProjRel {
   const float* mean;

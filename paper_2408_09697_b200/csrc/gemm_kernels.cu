@@ -494,7 +494,6 @@ void gather_mean(MeanBatch& m, cudaStream_t st) {
     cached = cached || m.b[b].slot != nullptr;
   }
   const bool small = items <= 8 * 16 * num_sms();  // fewer half-warp items than 8 warps per SM
-  if (!small && !cached && gather_mean_bulk(m, st)) return;
   if (wide && cached)
     launch_pdl(k_gather_mean<true, true, kGatherBatch>, grid, 256, 0, st, m);  // half tables in host memory
   else if (wide)
