@@ -261,6 +261,12 @@ __device__ __forceinline__ float4 load_row4(const MeanBlock& B, std::uint32_t ke
 #ifndef HG_WIDE_NOALLOC
 #define HG_WIDE_NOALLOC 0
 #endif
+#ifndef HG_FADD2_WIDE
+#define HG_FADD2_WIDE 1
+#endif
+#ifndef HG_FADD2_F32
+#define HG_FADD2_F32 0
+#endif
 // 8 consecutive features of a half-precision row (one 16-byte load)
 template <bool CACHED>
 __device__ __forceinline__ uint4 load_row8(const MeanBlock& B, std::uint32_t key, int c) {
@@ -294,6 +300,13 @@ __device__ __forceinline__ void add_row8(const uint4& raw, int h_dtype, float4& 
   for (int j = 0; j < 4; ++j)
     f[j] = h_dtype == kF16 ? __half22float2(*reinterpret_cast<const __half2*>(&w[j]))
                            : __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[j]));
+#if HG_FADD2_WIDE
+  // packed fp32 adds (round to nearest per lane: the same sums as the scalar adds)
+  float2 a = __fadd2_rn(make_float2(s.x, s.y), f[0]), b = __fadd2_rn(make_float2(s.z, s.w), f[1]);
+  float2 c = __fadd2_rn(make_float2(s2.x, s2.y), f[2]), d = __fadd2_rn(make_float2(s2.z, s2.w), f[3]);
+  s = make_float4(a.x, a.y, b.x, b.y);
+  s2 = make_float4(c.x, c.y, d.x, d.y);
+#else
   s.x += f[0].x;
   s.y += f[0].y;
   s.z += f[1].x;
@@ -302,13 +315,20 @@ __device__ __forceinline__ void add_row8(const uint4& raw, int h_dtype, float4& 
   s2.y += f[2].y;
   s2.z += f[3].x;
   s2.w += f[3].y;
+#endif
 }
 
 __device__ __forceinline__ void add4(float4& s, const float4& v) {
+#if HG_FADD2_F32
+  const float2 a = __fadd2_rn(make_float2(s.x, s.y), make_float2(v.x, v.y));
+  const float2 b = __fadd2_rn(make_float2(s.z, s.w), make_float2(v.z, v.w));
+  s = make_float4(a.x, a.y, b.x, b.y);
+#else
   s.x += v.x;
   s.y += v.y;
   s.z += v.z;
   s.w += v.w;
+#endif
 }
 __device__ __forceinline__ float4 scale4(float4 s, float k) { return make_float4(s.x * k, s.y * k, s.z * k, s.w * k); }
 
