@@ -61,3 +61,38 @@ def test_host_resident_table_with_hbm_cache_is_bit_identical(H, dtype):
         assert np.array_equal(x[n], y[n]), n
     assert {k: v.tolist() for k, v in dev.cache_counters().items()} == \
            {k: v.tolist() for k, v in host.cache_counters().items()}
+
+
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+def test_ragged_width_half_tables_match_reference(H, ref, dtype):
+    """Dense widths that are not multiples of the 8-feature lanes (100 and 36: the last
+    lane of a row's chunk is partly padding) and an fp32 learnable type in the same
+    half-precision gather launch, against the f64 reference on the rounded features."""
+    spec = dict(name="ragged", target="paper", num_classes=7, label_noise=0.1,
+                node_types=[dict(name="paper", count=3000, dim=100, storage="dense"),
+                            dict(name="venue", count=400, dim=36, storage="dense"),
+                            dict(name="author", count=2500, dim=20, storage="learnable")],
+                relations=[dict(src="paper", edge="cites", dst="paper", edges=24000),
+                           dict(src="venue", edge="hosts", dst="paper", edges=3000),
+                           dict(src="author", edge="writes", dst="paper", edges=9000),
+                           dict(src="paper", edge="in", dst="venue", edges=3000)],
+                self_paired=["cites"])
+    g = H.gen_synthetic(spec, 9)
+    rg = ref.RefGraph.from_spec(spec, 9)
+    rg.round_features(dtype)
+    batch = list(range(0, 2048, 8))
+    want = rg.flat_step(2, 32, 3, 4, batch, [25, 20], 13)
+    eng = H.Engine(g, [25, 20], hidden=32, batch_cap=256, model_seed=3, learn_seed=4, feat_dtype=dtype)
+    names = eng.tensor_names()
+    rep = eng.step(batch, 13, 0, train=True)
+    got = eng.read(*[n for n in names if not n.startswith("post.learn")])
+    assert abs(rep["loss"] - float(want["loss"][0])) <= TOL * abs(float(want["loss"][0]))
+    checked = 0
+    for n in want:
+        if n.startswith(("logits", "dlogits", "mean.", "grad.w.", "H1.")):
+            assert_close(got[n], want[n], TOL, f"{dtype}: {n}")
+            checked += 1
+        elif n.startswith("grad.f.") and n.endswith(".rows"):
+            assert_close(got[n], want[n], TOL, f"{dtype}: {n}")
+            checked += 1
+    assert checked > 10
