@@ -470,6 +470,72 @@ __global__ void __launch_bounds__(256, WIDE ? HG_GATHER_WIDE_MINB : NB > kGather
   }
 }
 
+// ---- half-precision tables in HBM: one warp per destination row -----------------------------
+// Lane l holds the 16-byte column slices p * 512 + 16 l (p < PM passes: 768 halves = 3, 1024 = 4)
+// of NB neighbour rows at a time, so a row is read whole by one warp (one key load per edge
+// instead of one per 128-column item) and the per-item bookkeeping is paid once per row.
+// Sums per column in edge order, as k_gather_mean: bit-identical results.
+#ifndef HG_ROWS_NB
+#define HG_ROWS_NB 2
+#endif
+#ifndef HG_ROWS_MINB
+#define HG_ROWS_MINB 3
+#endif
+template <int NB, int PM>
+__global__ void __launch_bounds__(256, HG_ROWS_MINB) k_gather_rows_half(MeanBatch m) {
+  pdl_enter();
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  int b = 0;
+  for (int item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); item < m.item_base[m.nb]; item += warps) {
+    while (b + 1 < m.nb && item >= m.item_base[b + 1]) ++b;
+    const MeanBlock& B = m.b[b];
+    const int n = *B.n_rows;
+    const int i = item - m.item_base[b];
+    const int ldm = B.ld_mean;
+    float* orow = B.mean + static_cast<std::size_t>(i) * ldm;
+    if (i >= n) {
+      if (i < ((n + 31) & ~31))
+        for (int c = 4 * lane; c < ldm; c += 128) *reinterpret_cast<float4*>(orow + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+      continue;
+    }
+    const std::uint32_t lo = B.indptr[i], hi = B.indptr[i + 1];
+    const std::uint32_t* keys = pin_ptr(B.keys);
+    const int dt = static_cast<int>(pin_u32(static_cast<std::uint32_t>(B.h_dtype)));
+    const std::uint32_t ldh = pin_u32(static_cast<std::uint32_t>(B.ld_h));
+    const std::size_t rowb = static_cast<std::size_t>(ldh) * 2;
+    const char* hb = pin_ptr(reinterpret_cast<const char*>(B.h) + 16 * lane);
+    float4 s[PM], s2[PM];
+#pragma unroll
+    for (int p = 0; p < PM; ++p) s[p] = s2[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (std::uint32_t e = lo; e < hi; e += NB) {
+      const std::uint32_t cnt = min(static_cast<std::uint32_t>(NB), hi - e);
+      std::uint32_t kk[NB];
+#pragma unroll
+      for (int q = 0; q < NB; ++q) kk[q] = q < cnt ? __ldg(keys + e + q) : 0u;
+      uint4 v[NB][PM];
+#pragma unroll
+      for (int q = 0; q < NB; ++q)
+#pragma unroll
+        for (int p = 0; p < PM; ++p)
+          v[q][p] = q < cnt && static_cast<std::uint32_t>(p * 256 + 8 * lane) < ldh
+                        ? __ldg(reinterpret_cast<const uint4*>(hb + kk[q] * rowb + p * 512))
+                        : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+      for (int q = 0; q < NB; ++q)
+#pragma unroll
+        for (int p = 0; p < PM; ++p) add_row8(v[q][p], dt, s[p], s2[p]);
+    }
+    const float inv = hi > lo ? 1.0f / static_cast<float>(hi - lo) : 0.f;
+#pragma unroll
+    for (int p = 0; p < PM; ++p) {
+      const int c = p * 256 + 8 * lane;
+      if (c < ldm) *reinterpret_cast<float4*>(orow + c) = scale4(s[p], inv);
+      if (c + 4 < ldm) *reinterpret_cast<float4*>(orow + c + 4) = scale4(s2[p], inv);
+    }
+  }
+}
+
 // ---- projection: out = sum_r mean_r . W_r (agg_all over relations), ReLU ------------------
 __global__ void __launch_bounds__(kT) k_project_tiles(ProjBatch pb) {
   pdl_enter();
@@ -534,8 +600,49 @@ __global__ void __launch_bounds__(kT) k_project_tiles(ProjBatch pb) {
 
 }  // namespace
 
+#ifndef HG_GATHER_ROWS
+#define HG_GATHER_ROWS 1
+#endif
 void gather_mean(MeanBatch& m, cudaStream_t st) {
   if (m.nb == 0) return;
+#if HG_GATHER_ROWS
+  {
+    // half-precision HBM blocks go to the warp-per-row kernel, the rest stay below
+    bool any_half = false, any_cached = false;
+    int pm = 0;
+    for (int b = 0; b < m.nb; ++b) {
+      any_cached = any_cached || m.b[b].slot != nullptr;
+      if (m.b[b].h_dtype != kF32) {
+        any_half = true;
+        pm = std::max(pm, static_cast<int>(ceil_div(static_cast<std::uint64_t>(m.b[b].ld_h), 256)));
+      }
+    }
+    if (any_half && !any_cached && pm <= 4) {
+      MeanBatch hv{}, rest{};
+      int rows = 0;
+      for (int b = 0; b < m.nb; ++b) {
+        if (m.b[b].h_dtype != kF32) {
+          hv.item_base[hv.nb] = rows;
+          rows += m.b[b].rows_cap;
+          hv.b[hv.nb++] = m.b[b];
+        } else {
+          rest.b[rest.nb++] = m.b[b];
+        }
+      }
+      hv.item_base[hv.nb] = rows;
+      const unsigned grid = static_cast<unsigned>(
+          std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(rows, 8), HG_GATHER_WAVES * num_sms())));
+      if (pm <= 2)
+        launch_pdl(k_gather_rows_half<HG_ROWS_NB, 2>, grid, 256, 0, st, hv);
+      else if (pm == 3)
+        launch_pdl(k_gather_rows_half<HG_ROWS_NB, 3>, grid, 256, 0, st, hv);
+      else
+        launch_pdl(k_gather_rows_half<HG_ROWS_NB, 4>, grid, 256, 0, st, hv);
+      if (rest.nb) gather_mean(rest, st);
+      return;
+    }
+  }
+#endif
   int items = 0;
   for (int b = 0; b < m.nb; ++b) {
     m.item_base[b] = items;
