@@ -536,6 +536,68 @@ __global__ void __launch_bounds__(256, HG_ROWS_MINB) k_gather_rows_half(MeanBatc
   }
 }
 
+// ---- fp32 tables / inner-layer rows: one half-warp per destination row --------------------
+// (HG_GATHER_ROWS_F32=0: the 64-column half-warp items instead): lane l holds the float4 slices 256 p + 16 l (bytes) of NB
+// neighbour rows; keys once per row; edge-order sums per column as k_gather_mean.
+#ifndef HG_GATHER_ROWS_F32
+#define HG_GATHER_ROWS_F32 1
+#endif
+#ifndef HG_ROWSF_NB
+#define HG_ROWSF_NB 3
+#endif
+#ifndef HG_ROWSF_MINB
+#define HG_ROWSF_MINB 5
+#endif
+template <int NB, int PM>
+__global__ void __launch_bounds__(256, HG_ROWSF_MINB) k_gather_rows_f32(MeanBatch m) {
+  pdl_enter();
+  const int hl = threadIdx.x & 15;
+  const int halves = gridDim.x * (blockDim.x >> 4);
+  int b = 0;
+  for (int item = blockIdx.x * (blockDim.x >> 4) + (threadIdx.x >> 4); item < m.item_base[m.nb]; item += halves) {
+    while (b + 1 < m.nb && item >= m.item_base[b + 1]) ++b;
+    const MeanBlock& B = m.b[b];
+    const int n = *B.n_rows;
+    const int i = item - m.item_base[b];
+    const int ldm = B.ld_mean;
+    float* orow = B.mean + static_cast<std::size_t>(i) * ldm;
+    if (i >= n) {
+      if (i < ((n + 31) & ~31))
+        for (int c = 4 * hl; c < ldm; c += 64) *reinterpret_cast<float4*>(orow + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+      continue;
+    }
+    const std::uint32_t lo = B.indptr[i], hi = B.indptr[i + 1];
+    const int ldh = B.ld_h;
+    const float* base = B.h + 4 * hl;
+    float4 s[PM];
+#pragma unroll
+    for (int p = 0; p < PM; ++p) s[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (std::uint32_t e = lo; e < hi; e += NB) {
+      const std::uint32_t cnt = min(static_cast<std::uint32_t>(NB), hi - e);
+      std::uint32_t kk[NB];
+#pragma unroll
+      for (int q = 0; q < NB; ++q) kk[q] = q < cnt ? __ldg(B.keys + e + q) : 0u;
+      float4 v[NB][PM];
+#pragma unroll
+      for (int q = 0; q < NB; ++q)
+#pragma unroll
+        for (int p = 0; p < PM; ++p)
+          v[q][p] = q < cnt && p * 64 + 4 * hl < ldm
+                        ? ld_row_stream(base + static_cast<std::size_t>(kk[q]) * ldh + p * 64)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int q = 0; q < NB; ++q)
+#pragma unroll
+        for (int p = 0; p < PM; ++p) add4(s[p], v[q][p]);
+    }
+#pragma unroll
+    for (int p = 0; p < PM; ++p) {
+      const int c = p * 64 + 4 * hl;
+      if (c < ldm) *reinterpret_cast<float4*>(orow + c) = hi > lo ? scale4(s[p], 1.0f / static_cast<float>(hi - lo)) : s[p];
+    }
+  }
+}
+
 // ---- projection: out = sum_r mean_r . W_r (agg_all over relations), ReLU ------------------
 __global__ void __launch_bounds__(kT) k_project_tiles(ProjBatch pb) {
   pdl_enter();
@@ -639,6 +701,33 @@ void gather_mean(MeanBatch& m, cudaStream_t st) {
       else
         launch_pdl(k_gather_rows_half<HG_ROWS_NB, 4>, grid, 256, 0, st, hv);
       if (rest.nb) gather_mean(rest, st);
+      return;
+    }
+  }
+#endif
+#if HG_GATHER_ROWS_F32
+  {
+    bool plain = true;
+    int pm = 0;
+    for (int b = 0; b < m.nb; ++b) {
+      plain = plain && m.b[b].slot == nullptr && m.b[b].h_dtype == kF32;
+      pm = std::max(pm, static_cast<int>(ceil_div(static_cast<std::uint64_t>(m.b[b].ld_mean), 64)));
+    }
+    int rows = 0;
+    for (int b = 0; b < m.nb; ++b) rows += m.b[b].rows_cap;
+    if (plain && pm <= 2 && rows > 8 * 16 * num_sms()) {
+      rows = 0;
+      for (int b = 0; b < m.nb; ++b) {
+        m.item_base[b] = rows;
+        rows += m.b[b].rows_cap;
+      }
+      m.item_base[m.nb] = rows;
+      const unsigned grid = static_cast<unsigned>(
+          std::max<std::uint64_t>(1, std::min<std::uint64_t>(ceil_div(rows, 16), HG_GATHER_WAVES * num_sms())));
+      if (pm <= 1)
+        launch_pdl(k_gather_rows_f32<HG_ROWSF_NB, 1>, grid, 256, 0, st, m);
+      else
+        launch_pdl(k_gather_rows_f32<HG_ROWSF_NB, 2>, grid, 256, 0, st, m);
       return;
     }
   }
